@@ -1,0 +1,220 @@
+/*
+ * mpm2p_b200.h — C ABI of the B200-native MPM-2P / MRCM velocity-update and
+ * saturation-update path.
+ *
+ * The reference (arxiv/paper_2103_11050, C++ library `mrcmflow`) has no FFI:
+ * its boundary is the C++ API in proj/include/mrcmflow/ (*.hpp), called by
+ * run() (proj/src/simulation.cpp:118-340) and by its tests. Every entry point
+ * below replaces one of those C++ functions; the citation on each names the
+ * reference declaration it stands in for. Arrays are plain host pointers in
+ * the reference layouts:
+ *   - cells row-major c = j*nx + i                        (grid.hpp:9-13)
+ *   - faces: vertical f = j*(nx+1)+i, then horizontal
+ *            (nx+1)*ny + j*nx + i, values = normal flux in +x/+y
+ *   - boundary faces in BoundarySpec order W(ny) E(ny) S(nx) N(nx)
+ *                                                          (elliptic.hpp:30-44)
+ *   - skeleton edges flattened interface-major (interfaces: vertical ones
+ *     sy-major, then horizontal; decomposition.cpp:28-56), position-minor
+ *   - interface coefficients: U_H (flux bases) then P_H (pressure bases)
+ *                                                          (mrcm.hpp:24-27)
+ * No torch/CUDA types appear in any signature. The library never retains a
+ * host pointer past the call that received it.
+ *
+ * Error convention (errors.hpp:9-24, mrcmflow_main.cpp:119-129): every call
+ * returns 0 on success, MPM2P_ECONFIG (ConfigError), MPM2P_ENUMERIC
+ * (NumericError), MPM2P_ECAPACITY (CapacityError) or MPM2P_ECUDA; the message
+ * is available from mpm2p_last_error(ctx).
+ *
+ * The CPU oracle (oracle/, test infrastructure only) exports the same
+ * functions with the prefix `oracle_` instead of `mpm2p_`.
+ */
+#ifndef MPM2P_B200_H
+#define MPM2P_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    MPM2P_OK = 0,
+    MPM2P_ECONFIG = 2,   /* ConfigError   (errors.hpp:9-12)  */
+    MPM2P_ENUMERIC = 3,  /* NumericError  (errors.hpp:14-17) */
+    MPM2P_ECAPACITY = 4, /* CapacityError (errors.hpp:19-22) */
+    MPM2P_ECUDA = 5
+};
+
+/* BcKind (elliptic.hpp:13) */
+enum { MPM2P_BC_PRESSURE = 0, MPM2P_BC_FLUX = 1, MPM2P_BC_ROBIN = 2 };
+/* InterfaceSpace::Kind (interface_space.hpp:34) */
+enum { MPM2P_SPACE_CONSTANT = 0, MPM2P_SPACE_LINEAR = 1 };
+/* HbarSpec::Mode (interface_space.hpp:12) */
+enum { MPM2P_HBAR_WHOLE = 0, MPM2P_HBAR_HALF = 1, MPM2P_HBAR_PER_EDGE = 2, MPM2P_HBAR_SEGMENT = 3 };
+/* AlphaMode (robin.hpp:11) */
+enum { MPM2P_ALPHA_UNIFORM = 0, MPM2P_ALPHA_ADAPTIVE = 1 };
+/* EpsilonMode (mpm.hpp:15) */
+enum { MPM2P_EPS_RELATIVE = 0, MPM2P_EPS_ABSOLUTE = 1, MPM2P_EPS_MOBILITY = 2 };
+/* Method (simulation.hpp:13) */
+enum {
+    MPM2P_METHOD_FINE_REFERENCE = 0,
+    MPM2P_METHOD_MRCM_EVERY_STEP = 1,
+    MPM2P_METHOD_MPM2P = 2,
+    MPM2P_METHOD_MPM2P_NO_UPDATES = 3
+};
+
+/* Everything RunInputs carries except the splitting policy and s0
+ * (simulation.hpp:99-110), plus the decomposition/space/alpha knobs that
+ * prepare() turns into shared objects (config.cpp:568-611). */
+typedef struct mpm2p_problem {
+    int32_t nx, ny;          /* build_grid (grid.cpp:9)            */
+    double lx, ly;
+    int32_t nsx, nsy;        /* build_decomposition (decomposition.cpp:21) */
+    int32_t space_kind;      /* build_interface_space (interface_space.cpp:9) */
+    int32_t hbar_mode, hbar_edges;
+    int32_t alpha_mode;      /* AlphaSpec (robin.hpp:15-22)        */
+    double alpha, alpha_min, alpha_max, percentile_lo, percentile_hi;
+    double viscosity_ratio;  /* FluidModel M = mu_o/mu_w (transport.hpp:11-13) */
+    const double* K;         /* permeability, nx*ny                */
+    const double* q;         /* sources nx*ny, or NULL for zero     */
+    const int32_t* bc_kind;  /* 2(nx+ny) BcKind                     */
+    const double* bc_value;  /* 2(nx+ny) Pressure g / Flux z (outward) */
+} mpm2p_problem;
+
+/* SplittingConfig (simulation.hpp:18-31) + RunInputs::inflow_sat. */
+typedef struct mpm2p_split {
+    int32_t method;
+    int32_t cn;
+    double eta;
+    int32_t eta_mode;
+    double cfl_safety, dt_cap;
+    int64_t te;
+    double pvi_max;
+    int32_t stop_on_breakthrough;
+    int64_t max_steps_hard;
+    double breakthrough_threshold;
+    int32_t track_errors;   /* fine-reference tracking: oracle only (out of the GPU scope) */
+    double inflow_sat;
+} mpm2p_split;
+
+/* SolveCounters (mrcm.hpp:15-21) — exact integers. */
+typedef struct mpm2p_counters {
+    int64_t homogeneous, particular, downscale, fine, interface_solves;
+} mpm2p_counters;
+
+/* StepRecord (simulation.hpp:33-45). */
+typedef struct mpm2p_step_record {
+    int64_t step;
+    double pvi, epsilon;
+    int32_t rebuilt;
+    double flux_err, sat_err;
+    int64_t bf_homog_cum, bf_part_cum;
+    double dt, wall_s, div_residual;
+} mpm2p_step_record;
+
+/* RunRecord (simulation.hpp:47-62) plus the decision-margin log (H4). */
+typedef struct mpm2p_run_record {
+    int64_t breakthrough_step;
+    double breakthrough_pvi;
+    int64_t te, tm_updates, tm_total, nhat;
+    int32_t n_sub;
+    mpm2p_counters counters;
+    double max_div_residual, max_div_ratio;
+    int32_t repair_warnings;
+    double final_pvi;
+    double min_eps_margin;  /* min over decisions of |eps - eta| / eta (bit-exactness guard) */
+    int64_t clamp_count;    /* clamp_count() (transport.hpp:24-26) */
+} mpm2p_run_record;
+
+/* DownscaleResult diagnostics (mrcm.hpp:122-130). */
+typedef struct mpm2p_downscale_info {
+    double repair_max, flux_scale;
+    int32_t repair_warning;
+    double div_residual, div_scale;
+} mpm2p_downscale_info;
+
+/* Derived sizes (grid.hpp:22-25, decomposition.hpp:40-44, interface_space.hpp:37-38). */
+typedef struct mpm2p_sizes {
+    int32_t cells, faces, bfaces;
+    int32_t n_sub, n_interfaces, skeleton_edges;
+    int32_t dim_flux, dim_pressure;
+    int64_t nhat;             /* homogeneous solves per rebuild (BasisSet::nhat) */
+    int32_t sub_nx, sub_ny;
+} mpm2p_sizes;
+
+typedef struct mpm2p_ctx mpm2p_ctx;
+
+/* ---- context ---------------------------------------------------------- */
+/* prepare() (config.cpp:568-611): grid, decomposition, interface space and
+ * boundary spec. Copies K/q/bc to the device. */
+int mpm2p_create(const mpm2p_problem* prob, mpm2p_ctx** out);
+void mpm2p_destroy(mpm2p_ctx* ctx);
+const char* mpm2p_last_error(const mpm2p_ctx* ctx);
+/* Message of the last failed mpm2p_create (no context exists then). */
+const char* mpm2p_create_error(void);
+int mpm2p_get_sizes(const mpm2p_ctx* ctx, mpm2p_sizes* out);
+
+/* ---- transport (transport.cpp) ---------------------------------------- */
+/* CellField conductivity(K, s, fluid)              transport.hpp:50  */
+int mpm2p_conductivity(mpm2p_ctx* ctx, const double* s, double* kappa);
+/* double max_fractional_flow_slope(fluid)          transport.hpp:22  */
+int mpm2p_max_fractional_flow_slope(mpm2p_ctx* ctx, double* out);
+/* double cfl_timestep(u, fluid, policy)            transport.hpp:41  */
+int mpm2p_cfl_timestep(mpm2p_ctx* ctx, const double* u, double safety, double dt_cap, double* dt);
+/* SaturationField upwind_step(s, u, dt, fluid)     transport.hpp:46-47 */
+int mpm2p_upwind_step(mpm2p_ctx* ctx, const double* s, double inflow, const double* u, double dt,
+                      double* s_out);
+/* double injection_rate(u, inflow_sat, fluid)      simulation.hpp:96 */
+int mpm2p_injection_rate(mpm2p_ctx* ctx, const double* u, double inflow, double* out);
+/* double max_outlet_saturation(s, u)               simulation.hpp:93 */
+int mpm2p_max_outlet_saturation(mpm2p_ctx* ctx, const double* s, const double* u, double* out);
+/* CellField divergence(u)                          grid.hpp:79       */
+int mpm2p_divergence(mpm2p_ctx* ctx, const double* u, double* div);
+
+/* ---- drift test (mpm.cpp:9-29) ----------------------------------------- */
+/* double epsilon(kappa_n, kappa_m, mode)           mpm.hpp:20        */
+int mpm2p_epsilon(mpm2p_ctx* ctx, const double* kappa_n, const double* kappa_m, int32_t mode,
+                  double* out);
+
+/* ---- coupling (robin.cpp) ---------------------------------------------- */
+/* RobinParameter compute_beta(kappa, dd, spec)     robin.hpp:37-38
+ * Outputs flattened per skeleton edge (interface-major), may be NULL. */
+int mpm2p_compute_beta(mpm2p_ctx* ctx, const double* kappa, double* beta_minus,
+                       double* beta_plus, double* alpha);
+
+/* ---- MRCM / MPM-2P (mrcm.cpp, mpm.cpp) --------------------------------- */
+/* GlobalSolution mrcm_solve(kappa, dd, space, beta, q, bc, counters)  mrcm.hpp:151-153
+ * beta_minus/beta_plus NULL => compute_beta(kappa) with the problem's AlphaSpec.
+ * Installs the basis and recon_m as the context's PerturbationState
+ * (mpm.hpp:26-33) for later mpm2p_mpm_update calls. Output pointers may be NULL. */
+int mpm2p_mrcm_solve(mpm2p_ctx* ctx, const double* kappa, const double* beta_minus,
+                     const double* beta_plus, double* p, double* u, double* coeffs,
+                     mpm2p_downscale_info* info, mpm2p_counters* counters);
+/* MpmResult mpm_pressure_update(state, kappa_n, q, bc, counters)      mpm.hpp:53-55 */
+int mpm2p_mpm_update(mpm2p_ctx* ctx, const double* kappa_n, double* p, double* u,
+                     double* delta_coeffs, mpm2p_downscale_info* info, mpm2p_counters* counters);
+/* BasisSet::iface_matrix (mrcm.hpp:68), dense dim x dim row-major. */
+int mpm2p_interface_matrix(mpm2p_ctx* ctx, double* M);
+
+/* ---- the driver (simulation.cpp:118-340) ------------------------------- */
+/* RunResult run(in, snapshot_steps, snap)          simulation.hpp:127-128
+ * steps may be NULL; otherwise it receives up to max_steps records. */
+int mpm2p_run(mpm2p_ctx* ctx, const mpm2p_split* split, const double* s0, double* s_final,
+              double* p_final, double* u_final, mpm2p_step_record* steps, int64_t max_steps,
+              mpm2p_run_record* rec);
+/* The same loop, one Algorithm-1 iteration per call (inputs stay resident in
+ * HBM). run_begin performs the initial solve and writes its record. */
+int mpm2p_run_begin(mpm2p_ctx* ctx, const mpm2p_split* split, const double* s0,
+                    mpm2p_step_record* first);
+int mpm2p_run_step(mpm2p_ctx* ctx, mpm2p_step_record* out, int32_t* done);
+int mpm2p_run_read(mpm2p_ctx* ctx, double* s, double* p, double* u);
+int mpm2p_run_end(mpm2p_ctx* ctx, mpm2p_run_record* rec);
+
+/* ---- cost model (simulation.cpp:11-28) --------------------------------- */
+double mpm2p_rcr(int64_t nhat, int64_t n, int64_t te, int64_t tm);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MPM2P_B200_H */
