@@ -1,0 +1,721 @@
+// capi.cu — context setup (prepare(), config.cpp:568-611), the Algorithm-1
+// driver (run(), proj/src/simulation.cpp:118-340) as a host state machine
+// over the device kernels, and the extern "C" boundary of
+// include/mpm2p_b200.h. Exceptions map to the reference's error classes
+// (errors.hpp:9-24) as status codes.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <set>
+#include <string>
+#include <vector>
+
+#include <cub/device/device_radix_sort.cuh>
+
+#include "../../include/mpm2p_b200.h"
+#include "band.cuh"
+#include "context.cuh"
+
+using namespace mpm2p;
+
+namespace {
+
+thread_local std::string g_create_err;
+
+struct Driver {
+    mpm2p_split sp{};
+    long long n = 0, ell = 0;
+    bool active = false;
+    int rebuild_next = 0;
+    mpm2p_run_record rec{};
+    std::vector<mpm2p_step_record> steps;
+    long long tm_total = 0;
+};
+
+}  // namespace
+
+struct mpm2p_ctx {
+    Ctx c;
+    Driver d;
+    std::unique_ptr<DevBuf<double>> scratch_a, scratch_b, scratch_c;
+};
+
+namespace {
+
+template <typename F>
+int guarded(mpm2p_ctx* ctx, F&& fn) {
+    std::string* err = ctx ? &ctx->c.err : &g_create_err;
+    try {
+        fn();
+        return MPM2P_OK;
+    } catch (const ConfigError& e) {
+        *err = e.what();
+        return MPM2P_ECONFIG;
+    } catch (const NumericError& e) {
+        *err = e.what();
+        return MPM2P_ENUMERIC;
+    } catch (const CapacityError& e) {
+        *err = e.what();
+        return MPM2P_ECAPACITY;
+    } catch (const CudaError& e) {
+        *err = e.what();
+        return MPM2P_ECUDA;
+    } catch (const std::exception& e) {
+        *err = e.what();
+        return MPM2P_ECONFIG;
+    }
+}
+
+void upload(Ctx& c, double* dst, const double* src, size_t n) {
+    CK(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyHostToDevice, c.st));
+}
+void download(Ctx& c, double* dst, const double* src, size_t n) {
+    if (dst) CK(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDeviceToHost, c.st));
+}
+
+// Reads the per-step scalars back and raises the reference's exceptions for
+// any guard the device tripped.
+const Scalars& sync_scalars(Ctx& c) {
+    CK(cudaMemcpyAsync(c.sc_host, c.sc.p, sizeof(Scalars), cudaMemcpyDeviceToHost, c.st));
+    CK(cudaStreamSynchronize(c.st));
+    const unsigned e = c.sc_host->err;
+    if (e) {
+        CK(cudaMemsetAsync(&c.sc.p->err, 0, sizeof(unsigned), c.st));
+        if (e & ERR_CFL) throw NumericError("upwind_step: saturation left [0,1]; CFL condition violated");
+        if (e & ERR_KAPPA) throw NumericError("CellCenteredSolver: conductivity must be positive and finite");
+        if (e & ERR_ROBIN_BETA) throw ConfigError("CellCenteredSolver: Robin face requires beta > 0");
+        if (e & ERR_PIVOT) throw NumericError("CellCenteredSolver: direct solve failed");
+        if (e & ERR_EPS_ZERO) throw NumericError("epsilon: zero reference norm in relative mode");
+        throw NumericError("device error word " + std::to_string(e));
+    }
+    return *c.sc_host;
+}
+
+void reset_scalars(Ctx& c) {
+    Scalars z{};
+    z.min_margin = INFINITY;
+    z.div_scale = 1.0;
+    const double slope = c.sc_host ? c.sc_host->slope : 0.0;
+    CK(cudaMemcpyAsync(c.sc.p, &z, sizeof(Scalars), cudaMemcpyHostToDevice, c.st));
+    CK(cudaStreamSynchronize(c.st));
+    (void)slope;
+    launch_max_slope(c);
+}
+
+// CSR pattern of the interface matrix: row r (psi rows, then phi rows) couples
+// to every basis of every interface that shares a subdomain with r's interface.
+void build_csr(Ctx& c) {
+    const Layout& L = c.L;
+    const int np = L.dim_flux;
+    std::vector<int> ptr(1, 0), col;
+    for (int R = 0; R < 2 * np; ++R) {
+        const int rb = R < np ? R : R - np;
+        const int k = L.basis_iface(rb);
+        std::set<int> nb;
+        for (int s : {L.iface_minus(k), L.iface_plus(k)}) {
+            int inc[4];
+            const int ni = L.incident(s, inc);
+            for (int a = 0; a < ni; ++a) nb.insert(inc[a]);
+        }
+        for (int kk : nb)
+            for (int t = 0; t < L.iface_nb(kk); ++t) col.push_back(L.iface_first_basis(kk) + t);
+        for (int kk : nb)
+            for (int t = 0; t < L.iface_nb(kk); ++t) col.push_back(np + L.iface_first_basis(kk) + t);
+        ptr.push_back((int)col.size());
+    }
+    c.nnz = (int)col.size();
+    c.csr_ptr.alloc(ptr.size());
+    c.csr_col.alloc(std::max<size_t>(col.size(), 1));
+    c.csr_val.alloc(std::max<size_t>(col.size(), 1));
+    CK(cudaMemcpyAsync(c.csr_ptr.p, ptr.data(), ptr.size() * sizeof(int), cudaMemcpyHostToDevice, c.st));
+    if (!col.empty()) CK(cudaMemcpyAsync(c.csr_col.p, col.data(), col.size() * sizeof(int), cudaMemcpyHostToDevice, c.st));
+    CK(cudaStreamSynchronize(c.st));
+}
+
+void create_ctx(mpm2p_ctx* ctx, const mpm2p_problem* P) {
+    Ctx& c = ctx->c;
+    // build_grid / build_decomposition validation (grid.cpp:9-15, decomposition.cpp:35-41)
+    if (P->nx < 1 || P->ny < 1)
+        throw ConfigError("build_grid: cell counts must be >= 1, got " + std::to_string(P->nx) + "x" + std::to_string(P->ny));
+    if (!(P->lx > 0.0) || !(P->ly > 0.0)) throw ConfigError("build_grid: domain lengths must be positive");
+    if (P->nsx < 1 || P->nsy < 1) throw ConfigError("build_decomposition: subdomain counts must be >= 1");
+    if (P->nx % P->nsx != 0 || P->ny % P->nsy != 0)
+        throw ConfigError("build_decomposition: subdomains do not divide the grid");
+    if (!P->K || !P->bc_kind || !P->bc_value) throw ConfigError("problem: K and the boundary spec are required");
+    Layout& L = c.L;
+    L.nx = P->nx;
+    L.ny = P->ny;
+    L.lx = P->lx;
+    L.ly = P->ly;
+    L.hx = P->lx / P->nx;
+    L.hy = P->ly / P->ny;
+    L.nsx = P->nsx;
+    L.nsy = P->nsy;
+    L.snx = P->nx / P->nsx;
+    L.sny = P->ny / P->nsy;
+    L.n_sub = P->nsx * P->nsy;
+    L.NV = P->nsy * (P->nsx - 1);
+    L.NH = (P->nsy - 1) * P->nsx;
+    L.n_iface = L.NV + L.NH;
+    L.nbe = 2 * (L.snx + L.sny);
+    L.ncs = L.snx * L.sny;
+    if (L.snx > BAND_MAX)
+        throw CapacityError("subdomain width " + std::to_string(L.snx) + " exceeds the banded kernel limit of " +
+                            std::to_string(BAND_MAX) + " cells");
+    // interface space (interface_space.cpp:9-52)
+    L.space_kind = P->space_kind;
+    if (P->space_kind == MPM2P_SPACE_LINEAR) {
+        L.nbv = L.nbh = 2;
+        L.segv = L.segh = 0;
+    } else {
+        auto seg_of = [&](int n) {
+            int seg = n;
+            switch (P->hbar_mode) {
+                case MPM2P_HBAR_WHOLE: seg = n; break;
+                case MPM2P_HBAR_HALF: seg = n / 2; break;
+                case MPM2P_HBAR_PER_EDGE: seg = 1; break;
+                case MPM2P_HBAR_SEGMENT: seg = P->hbar_edges; break;
+                default: throw ConfigError("build_interface_space: unknown hbar mode");
+            }
+            if (seg < 1 || n % seg != 0)
+                throw ConfigError("build_interface_space: segment length " + std::to_string(seg) +
+                                  " does not divide an interface of " + std::to_string(n) + " edges");
+            return seg;
+        };
+        L.segv = L.NV > 0 ? seg_of(L.sny) : 1;
+        L.segh = L.NH > 0 ? seg_of(L.snx) : 1;
+        L.nbv = L.NV > 0 ? L.sny / L.segv : 0;
+        L.nbh = L.NH > 0 ? L.snx / L.segh : 0;
+    }
+    L.dim_flux = L.NV * L.nbv + L.NH * L.nbh;
+    L.max_hom = 0;
+    c.nhat = 0;
+    for (int s = 0; s < L.n_sub; ++s) {
+        L.max_hom = std::max(L.max_hom, L.n_hom(s));
+        c.nhat += L.n_hom(s);
+    }
+    c.max_rhs = 1 + L.max_hom;
+    c.dim = 2 * L.dim_flux;
+    c.M = P->viscosity_ratio;
+    c.alpha_mode = P->alpha_mode;
+    c.alpha = P->alpha;
+    c.alpha_min = P->alpha_min;
+    c.alpha_max = P->alpha_max;
+    c.pct_lo = P->percentile_lo;
+    c.pct_hi = P->percentile_hi;
+    // boundary spec
+    const int nb = L.bfaces();
+    c.bc_kind_h.assign(P->bc_kind, P->bc_kind + nb);
+    bool pure_neumann = true;
+    for (int i = 0; i < nb; ++i) {
+        if (c.bc_kind_h[i] != BC_PRESSURE && c.bc_kind_h[i] != BC_FLUX)
+            throw ConfigError("problem: physical boundary faces must be Pressure or Flux");
+        if (c.bc_kind_h[i] == BC_PRESSURE) {
+            c.grounded = true;
+            pure_neumann = false;
+        }
+    }
+    c.anchor_m = (L.n_iface == 0) && pure_neumann;
+    c.repair_active = L.n_sub > 1 || c.grounded;
+
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&c.num_sms, cudaDevAttrMultiProcessorCount, dev));
+    CK(cudaStreamCreateWithFlags(&c.st, cudaStreamNonBlocking));
+    configure_kernels();
+    const size_t cells = L.cells(), faces = L.faces(), ns = L.n_sub, nbe = L.nbe, ncs = L.ncs;
+    const size_t skel = std::max(1, L.skeleton_edges());
+    c.K.alloc(cells);
+    c.q.alloc(cells);
+    c.bc_value.alloc(nb);
+    c.bc_kind.alloc(nb);
+    c.qsum_sub.alloc(ns);
+    c.ground.alloc(ns);
+    if (c.repair_active) c.Linv.alloc(ns * ns);
+    c.s.alloc(cells);
+    c.s2.alloc(cells);
+    c.u.alloc(faces);
+    c.p.alloc(cells);
+    c.kappa_n.alloc(cells);
+    c.kappa_m.alloc(cells);
+    c.lam_reb.alloc(cells);
+    c.T.alloc(faces);
+    c.beta_m.alloc(skel);
+    c.beta_p.alloc(skel);
+    c.alpha_e.alloc(skel);
+    c.face_kappa.alloc(skel);
+    c.sort_keys.alloc(skel);
+    if (c.alpha_mode == MPM2P_ALPHA_ADAPTIVE && L.skeleton_edges() > 0) {
+        CK(cub::DeviceRadixSort::SortKeys(nullptr, c.sort_tmp_bytes, c.face_kappa.p, c.sort_keys.p,
+                                          L.skeleton_edges(), 0, 64, c.st));
+        c.sort_tmp.alloc(std::max<size_t>(c.sort_tmp_bytes, 1));
+    }
+    const size_t B = L.snx;
+    c.BDm.alloc(ns * ncs);
+    c.BWm.alloc(ns * ncs);
+    c.BSm.alloc(ns * ncs);
+    c.Dm.alloc(ns * ncs);
+    c.Lcm.alloc(ns * ncs * B);
+    c.Lrm.alloc(ns * ncs * B);
+    const size_t hmax = std::max(1, L.max_hom);
+    c.HU.alloc(ns * hmax * nbe);
+    c.HB.alloc(ns * hmax * nbe);
+    c.HP.alloc(ns * hmax);
+    c.pm.alloc(cells);
+    c.bpm.alloc(ns * nbe);
+    c.pmsum.alloc(ns);
+    const size_t dim = std::max(1, c.dim);
+    if (c.dim > 0) {
+        c.Mdense.alloc((size_t)c.dim * c.dim);
+        c.Minv.alloc((size_t)c.dim * c.dim);
+    }
+    c.irhs.alloc(dim);
+    c.icoef.alloc(dim);
+    c.ires.alloc(dim);
+    c.idelta.alloc(dim);
+    c.X.alloc(ns * c.max_rhs * ncs);
+    c.PU.alloc(ns * nbe);
+    c.PB.alloc(ns * nbe);
+    c.PS.alloc(ns);
+    c.GZ.alloc(ns * nbe);
+    c.WU.alloc(ns * nbe);
+    c.RU.alloc(ns * nbe);
+    c.RS.alloc(ns);
+    c.skel.alloc(skel);
+    c.resid.alloc(ns);
+    c.delta.alloc(ns);
+    c.corr.alloc(std::max(1, L.n_iface));
+    c.BDd.alloc(ns * ncs);
+    c.BWd.alloc(ns * ncs);
+    c.BSd.alloc(ns * ncs);
+    c.Dd.alloc(ns * ncs);
+    c.Lrd.alloc(ns * ncs * B);
+    c.Xd.alloc(ns * ncs);
+    c.sc.alloc(1);
+    c.red.alloc(8 * 4 * (size_t)c.num_sms + 4096);
+    c.red_count.alloc(1);
+    CK(cudaMallocHost(&c.sc_host, sizeof(Scalars)));
+    std::memset(c.sc_host, 0, sizeof(Scalars));
+    c.red_count.zero(c.st);
+    c.delta.zero(c.st);
+    upload(c, c.K, P->K, cells);
+    if (P->q) upload(c, c.q, P->q, cells);
+    else c.q.zero(c.st);
+    upload(c, c.bc_value, P->bc_value, nb);
+    CK(cudaMemcpyAsync(c.bc_kind.p, P->bc_kind, nb * sizeof(int), cudaMemcpyHostToDevice, c.st));
+    if (c.dim > 0) build_csr(c);
+    reset_scalars(c);
+    launch_setup_static(c);
+    CK(cudaStreamSynchronize(c.st));
+}
+
+// ---- driver (simulation.cpp:118-340) ----------------------------------------
+void fill_counters(const Ctx& c, mpm2p_counters* o) {
+    o->homogeneous = c.c_hom;
+    o->particular = c.c_part;
+    o->downscale = c.c_down;
+    o->fine = c.c_fine;
+    o->interface_solves = c.c_iface;
+}
+
+void note(Driver& d, const Scalars& s) {  // simulation.cpp:176-181
+    d.rec.max_div_residual = std::max(d.rec.max_div_residual, s.div_residual);
+    d.rec.max_div_ratio = std::max(d.rec.max_div_ratio, s.div_residual / s.div_scale);
+    if (s.repair_warning) ++d.rec.repair_warnings;
+}
+
+mpm2p_step_record make_record(const Ctx& c, const Driver& d, const Scalars& s, int rebuilt, double dt, double wall) {
+    mpm2p_step_record r{};
+    r.step = d.n;
+    r.pvi = s.pvi;
+    r.epsilon = s.eps;
+    r.rebuilt = rebuilt;
+    r.bf_homog_cum = c.c_hom;
+    r.bf_part_cum = c.c_part;
+    r.dt = dt;
+    r.wall_s = wall;
+    r.div_residual = s.div_residual;
+    return r;
+}
+
+void breakthrough_check(Driver& d, const Scalars& s) {  // simulation.cpp:253-259
+    if (d.rec.breakthrough_step >= 0) return;
+    if (s.outlet_max > d.sp.breakthrough_threshold) {
+        d.rec.breakthrough_step = d.n - 1;
+        d.rec.breakthrough_pvi = s.pvi;
+    }
+}
+
+void run_begin(mpm2p_ctx* ctx, const mpm2p_split* sp, const double* s0, mpm2p_step_record* first) {
+    Ctx& c = ctx->c;
+    Driver& d = ctx->d;
+    if (sp->cn < 1) throw ConfigError("run: cn must be >= 1");
+    if (sp->te <= 0 && sp->pvi_max <= 0.0 && !sp->stop_on_breakthrough)
+        throw ConfigError("run: no stop condition configured");
+    if (sp->method == MPM2P_METHOD_MPM2P && sp->eta < 0.0) throw ConfigError("run: negative eta");
+    if (sp->method == MPM2P_METHOD_FINE_REFERENCE)
+        throw ConfigError("run: the fine-reference method is outside the GPU path (use the oracle)");
+    if (sp->track_errors)
+        throw ConfigError("run: fine-reference error tracking is outside the GPU path; set track_errors = 0");
+    if (!s0) throw ConfigError("run: initial saturation grid mismatch");
+    d = Driver{};
+    d.sp = *sp;
+    d.rec.breakthrough_step = -1;
+    d.rec.breakthrough_pvi = -1.0;
+    d.rec.n_sub = c.L.n_sub;
+    d.rec.min_eps_margin = INFINITY;
+    c.c_hom = c.c_part = c.c_down = c.c_fine = c.c_iface = 0;
+    reset_scalars(c);
+    const auto t0 = std::chrono::steady_clock::now();
+    upload(c, c.s, s0, c.L.cells());
+    launch_conductivity(c, c.s, c.kappa_n, -1, false);
+    launch_rebuild(c, c.kappa_n);
+    launch_lambda(c, c.s, c.lam_reb);
+    launch_outlet(c, c.s, c.u);
+    // epsilon_0 = eta: the first branch check reuses (simulation.cpp:205)
+    CK(cudaMemcpyAsync(&c.sc.p->eps_pending, &sp->eta, sizeof(double), cudaMemcpyHostToDevice, c.st));
+    launch_decide(c, 0, sp->method, sp->eta, 0);
+    const Scalars& s = sync_scalars(c);
+    note(d, s);
+    Scalars s_rec = s;
+    s_rec.eps = 0.0;
+    const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    mpm2p_step_record r = make_record(c, d, s_rec, 1, 0.0, wall);
+    d.steps.push_back(r);
+    d.tm_total = 1;
+    if (first) *first = r;
+    d.n = 1;
+    d.rebuild_next = s.rebuild_next;
+    breakthrough_check(d, s);
+    d.active = true;
+}
+
+bool run_step(mpm2p_ctx* ctx, mpm2p_step_record* out) {
+    Ctx& c = ctx->c;
+    Driver& d = ctx->d;
+    const mpm2p_split& sp = d.sp;
+    if (!d.active) throw ConfigError("run_step: run_begin not called");
+    if (sp.te > 0 && d.n >= sp.te) return false;
+    if (sp.pvi_max > 0.0 && c.sc_host->pvi >= sp.pvi_max) return false;
+    if (sp.stop_on_breakthrough && d.rec.breakthrough_step >= 0) return false;
+    if (d.n >= sp.max_steps_hard) return false;
+    const auto t0 = std::chrono::steady_clock::now();
+    launch_cfl(c, c.u, sp.cfl_safety, sp.dt_cap);
+    launch_inj_pvi(c, c.u, sp.inflow_sat, sp.cn, true);
+    for (int k = 0; k < sp.cn; ++k) {
+        launch_upwind(c, c.s, c.s2, c.u, sp.inflow_sat);
+        std::swap(c.s.p, c.s2.p);
+    }
+    const int eps_mode = sp.eta_mode;
+    launch_conductivity(c, c.s, c.kappa_n, eps_mode, true);
+    const int rebuilt = d.rebuild_next;
+    if (rebuilt) {
+        ++d.ell;
+        launch_rebuild(c, c.kappa_n);
+        launch_lambda(c, c.s, c.lam_reb);
+    } else {
+        launch_mpm(c, c.kappa_n);
+    }
+    launch_decide(c, rebuilt, sp.method, sp.eta, (int)d.n);
+    launch_outlet(c, c.s, c.u);
+    const Scalars& s = sync_scalars(c);
+    note(d, s);
+    const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    mpm2p_step_record r = make_record(c, d, s, rebuilt, s.dt, wall);
+    d.steps.push_back(r);
+    if (rebuilt) ++d.tm_total;
+    if (out) *out = r;
+    d.rebuild_next = s.rebuild_next;
+    ++d.n;
+    breakthrough_check(d, s);
+    return true;
+}
+
+void run_end(mpm2p_ctx* ctx, mpm2p_run_record* out) {
+    Ctx& c = ctx->c;
+    Driver& d = ctx->d;
+    if (!d.active) throw ConfigError("run_end: run_begin not called");
+    d.rec.te = d.n;
+    d.rec.tm_updates = d.ell;
+    d.rec.tm_total = d.tm_total;
+    d.rec.nhat = c.nhat;
+    fill_counters(c, &d.rec.counters);
+    d.rec.final_pvi = c.sc_host->pvi;
+    d.rec.min_eps_margin = c.sc_host->min_margin;
+    d.rec.clamp_count = c.sc_host->clamp;
+    if (out) *out = d.rec;
+    d.active = false;
+}
+
+DevBuf<double>& scratch(std::unique_ptr<DevBuf<double>>& b, size_t n) {
+    if (!b) b = std::make_unique<DevBuf<double>>();
+    if (b->n < n) b->alloc(n);
+    return *b;
+}
+
+void fill_info(const Scalars& s, mpm2p_downscale_info* info) {
+    if (!info) return;
+    info->repair_max = s.repair_max;
+    info->flux_scale = s.flux_scale;
+    info->repair_warning = s.repair_warning;
+    info->div_residual = s.div_residual;
+    info->div_scale = s.div_scale;
+}
+
+}  // namespace
+
+extern "C" {
+
+int mpm2p_create(const mpm2p_problem* prob, mpm2p_ctx** out) {
+    *out = nullptr;
+    auto* ctx = new mpm2p_ctx();
+    const int rc = guarded(nullptr, [&] { create_ctx(ctx, prob); });
+    if (rc != MPM2P_OK) {
+        mpm2p_destroy(ctx);
+        return rc;
+    }
+    *out = ctx;
+    return rc;
+}
+
+void mpm2p_destroy(mpm2p_ctx* ctx) {
+    if (!ctx) return;
+    if (ctx->c.st) cudaStreamSynchronize(ctx->c.st);
+    if (ctx->c.sc_host) cudaFreeHost(ctx->c.sc_host);
+    cudaStream_t st = ctx->c.st;
+    delete ctx;
+    if (st) cudaStreamDestroy(st);
+}
+
+const char* mpm2p_last_error(const mpm2p_ctx* ctx) { return ctx ? ctx->c.err.c_str() : g_create_err.c_str(); }
+const char* mpm2p_create_error(void) { return g_create_err.c_str(); }
+
+int mpm2p_get_sizes(const mpm2p_ctx* ctx, mpm2p_sizes* o) {
+    const Layout& L = ctx->c.L;
+    o->cells = L.cells();
+    o->faces = L.faces();
+    o->bfaces = L.bfaces();
+    o->n_sub = L.n_sub;
+    o->n_interfaces = L.n_iface;
+    o->skeleton_edges = L.skeleton_edges();
+    o->dim_flux = L.dim_flux;
+    o->dim_pressure = L.dim_flux;
+    o->nhat = ctx->c.nhat;
+    o->sub_nx = L.snx;
+    o->sub_ny = L.sny;
+    return MPM2P_OK;
+}
+
+int mpm2p_conductivity(mpm2p_ctx* ctx, const double* s, double* kappa) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        const size_t n = c.L.cells();
+        auto& a = scratch(ctx->scratch_a, n);
+        auto& b = scratch(ctx->scratch_b, n);
+        upload(c, a, s, n);
+        launch_conductivity(c, a, b, -1, false);
+        download(c, kappa, b, n);
+        sync_scalars(c);
+    });
+}
+
+int mpm2p_max_fractional_flow_slope(mpm2p_ctx* ctx, double* out) {
+    return guarded(ctx, [&] {
+        launch_max_slope(ctx->c);
+        *out = sync_scalars(ctx->c).slope;
+    });
+}
+
+int mpm2p_cfl_timestep(mpm2p_ctx* ctx, const double* u, double safety, double dt_cap, double* dt) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        auto& a = scratch(ctx->scratch_a, c.L.faces());
+        upload(c, a, u, c.L.faces());
+        launch_cfl(c, a, safety, dt_cap);
+        *dt = sync_scalars(c).dt;
+    });
+}
+
+int mpm2p_upwind_step(mpm2p_ctx* ctx, const double* s, double inflow, const double* u, double dt, double* s_out) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        const size_t n = c.L.cells(), f = c.L.faces();
+        auto& a = scratch(ctx->scratch_a, n);
+        auto& b = scratch(ctx->scratch_b, n);
+        auto& uu = scratch(ctx->scratch_c, f);
+        upload(c, a, s, n);
+        upload(c, uu, u, f);
+        CK(cudaMemcpyAsync(&c.sc.p->dt, &dt, sizeof(double), cudaMemcpyHostToDevice, c.st));
+        launch_upwind(c, a, b, uu, inflow);
+        sync_scalars(c);
+        download(c, s_out, b, n);
+        CK(cudaStreamSynchronize(c.st));
+    });
+}
+
+int mpm2p_injection_rate(mpm2p_ctx* ctx, const double* u, double inflow, double* out) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        auto& a = scratch(ctx->scratch_a, c.L.faces());
+        upload(c, a, u, c.L.faces());
+        launch_inj_pvi(c, a, inflow, 0, false);
+        *out = sync_scalars(c).inj;
+    });
+}
+
+int mpm2p_max_outlet_saturation(mpm2p_ctx* ctx, const double* s, const double* u, double* out) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        auto& a = scratch(ctx->scratch_a, c.L.cells());
+        auto& b = scratch(ctx->scratch_b, c.L.faces());
+        upload(c, a, s, c.L.cells());
+        upload(c, b, u, c.L.faces());
+        launch_outlet(c, a, b);
+        *out = sync_scalars(c).outlet_max;
+    });
+}
+
+int mpm2p_divergence(mpm2p_ctx* ctx, const double* u, double* div) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        auto& a = scratch(ctx->scratch_a, c.L.faces());
+        auto& b = scratch(ctx->scratch_b, c.L.cells());
+        upload(c, a, u, c.L.faces());
+        launch_divergence(c, a, b);
+        download(c, div, b, c.L.cells());
+        sync_scalars(c);
+    });
+}
+
+int mpm2p_epsilon(mpm2p_ctx* ctx, const double* kn, const double* km, int32_t mode, double* out) {
+    return guarded(ctx, [&] {
+        if (mode == MPM2P_EPS_MOBILITY)
+            throw ConfigError("epsilon: mobility mode needs saturation fields, not conductivities");
+        Ctx& c = ctx->c;
+        const size_t n = c.L.cells();
+        auto& a = scratch(ctx->scratch_a, n);
+        auto& b = scratch(ctx->scratch_b, n);
+        upload(c, a, kn, n);
+        upload(c, b, km, n);
+        launch_epsilon_fields(c, a, b, mode);
+        *out = sync_scalars(c).eps_pending;
+    });
+}
+
+int mpm2p_compute_beta(mpm2p_ctx* ctx, const double* kappa, double* bm, double* bp, double* alpha) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        const size_t n = c.L.cells(), E = c.L.skeleton_edges();
+        auto& a = scratch(ctx->scratch_a, n);
+        upload(c, a, kappa, n);
+        launch_beta(c, a);
+        sync_scalars(c);
+        if (E) {
+            download(c, bm, c.beta_m, E);
+            download(c, bp, c.beta_p, E);
+            download(c, alpha, c.alpha_e, E);
+        }
+        CK(cudaStreamSynchronize(c.st));
+    });
+}
+
+int mpm2p_mrcm_solve(mpm2p_ctx* ctx, const double* kappa, const double* bm, const double* bp, double* p, double* u,
+                     double* coeffs, mpm2p_downscale_info* info, mpm2p_counters* counters) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        const Layout& L = c.L;
+        c.c_hom = c.c_part = c.c_down = c.c_fine = c.c_iface = 0;
+        upload(c, c.kappa_n, kappa, L.cells());
+        const bool given = bm && bp;
+        if (given && L.skeleton_edges() > 0) {
+            upload(c, c.beta_m, bm, L.skeleton_edges());
+            upload(c, c.beta_p, bp, L.skeleton_edges());
+        }
+        launch_rebuild(c, c.kappa_n, !given);
+        const Scalars& s = sync_scalars(c);
+        download(c, p, c.p, L.cells());
+        download(c, u, c.u, L.faces());
+        if (coeffs && c.dim > 0) download(c, coeffs, c.icoef, c.dim);
+        CK(cudaStreamSynchronize(c.st));
+        fill_info(s, info);
+        if (counters) fill_counters(c, counters);
+    });
+}
+
+int mpm2p_mpm_update(mpm2p_ctx* ctx, const double* kappa_n, double* p, double* u, double* dcoeffs,
+                     mpm2p_downscale_info* info, mpm2p_counters* counters) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        const Layout& L = c.L;
+        if (!c.has_basis) throw ConfigError("mpm_update: no basis installed (call mrcm_solve first)");
+        c.c_hom = c.c_part = c.c_down = c.c_fine = c.c_iface = 0;
+        upload(c, c.kappa_n, kappa_n, L.cells());
+        launch_mpm(c, c.kappa_n);
+        const Scalars& s = sync_scalars(c);
+        download(c, p, c.p, L.cells());
+        download(c, u, c.u, L.faces());
+        if (dcoeffs && c.dim > 0) download(c, dcoeffs, c.icoef, c.dim);
+        CK(cudaStreamSynchronize(c.st));
+        fill_info(s, info);
+        if (counters) fill_counters(c, counters);
+    });
+}
+
+int mpm2p_interface_matrix(mpm2p_ctx* ctx, double* M) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        if (!c.has_basis) throw ConfigError("interface_matrix: no basis installed");
+        if (c.dim > 0) download(c, M, c.Mdense, (size_t)c.dim * c.dim);
+        CK(cudaStreamSynchronize(c.st));
+    });
+}
+
+int mpm2p_run(mpm2p_ctx* ctx, const mpm2p_split* sp, const double* s0, double* s_final, double* p_final,
+              double* u_final, mpm2p_step_record* steps, int64_t max_steps, mpm2p_run_record* rec) {
+    return guarded(ctx, [&] {
+        run_begin(ctx, sp, s0, nullptr);
+        while (run_step(ctx, nullptr)) {
+        }
+        Ctx& c = ctx->c;
+        download(c, s_final, c.s, c.L.cells());
+        download(c, p_final, c.p, c.L.cells());
+        download(c, u_final, c.u, c.L.faces());
+        CK(cudaStreamSynchronize(c.st));
+        if (steps)
+            for (int64_t i = 0; i < (int64_t)ctx->d.steps.size() && i < max_steps; ++i) steps[i] = ctx->d.steps[i];
+        run_end(ctx, rec);
+    });
+}
+
+int mpm2p_run_begin(mpm2p_ctx* ctx, const mpm2p_split* sp, const double* s0, mpm2p_step_record* first) {
+    return guarded(ctx, [&] { run_begin(ctx, sp, s0, first); });
+}
+
+int mpm2p_run_step(mpm2p_ctx* ctx, mpm2p_step_record* out, int32_t* done) {
+    return guarded(ctx, [&] { *done = run_step(ctx, out) ? 0 : 1; });
+}
+
+int mpm2p_run_read(mpm2p_ctx* ctx, double* s, double* p, double* u) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        download(c, s, c.s, c.L.cells());
+        download(c, p, c.p, c.L.cells());
+        download(c, u, c.u, c.L.faces());
+        CK(cudaStreamSynchronize(c.st));
+    });
+}
+
+int mpm2p_run_end(mpm2p_ctx* ctx, mpm2p_run_record* rec) {
+    return guarded(ctx, [&] { run_end(ctx, rec); });
+}
+
+double mpm2p_rcr(int64_t nhat, int64_t n, int64_t te, int64_t tm) {  // simulation.cpp:11-19
+    if (te <= 0 || nhat < 0 || n < 0 || tm < 0 || tm > te) return -1.0;
+    const double frac = (double)(te - tm) / (double)te;
+    const double bf = 1.0 - 2.0 * (double)n / (double)(nhat + 2 * n);
+    return frac * bf * 100.0;
+}
+
+}  // extern "C"

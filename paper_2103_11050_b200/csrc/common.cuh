@@ -1,0 +1,70 @@
+// common.cuh — error handling, launch helpers and deterministic reductions.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+namespace mpm2p {
+
+// errors.hpp:9-24 — mapped to C-ABI status codes at the boundary.
+struct ConfigError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct NumericError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct CapacityError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct CudaError : std::runtime_error { using std::runtime_error::runtime_error; };
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+    if (e != cudaSuccess)
+        throw CudaError(std::string(what) + ": " + cudaGetErrorString(e) + " at " + file + ":" + std::to_string(line));
+}
+#define CK(x) ::mpm2p::cuda_check((x), #x, __FILE__, __LINE__)
+#define CK_LAUNCH() ::mpm2p::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+
+// Device error word bits (checked once per step on the host).
+enum : unsigned {
+    ERR_CFL = 1u << 0,          // upwind_step: saturation left [0,1] (transport.cpp:115-116)
+    ERR_KAPPA = 1u << 1,        // conductivity not positive/finite (elliptic.cpp:73-75)
+    ERR_PIVOT = 1u << 2,        // local LDL^T breakdown (elliptic.cpp:185-188)
+    ERR_SINGULAR = 1u << 3,     // interface matrix numerically singular (mrcm.cpp:227-238)
+    ERR_EPS_ZERO = 1u << 4,     // epsilon: zero reference norm (mpm.cpp:23)
+    ERR_ROBIN_BETA = 1u << 5,   // Robin face requires beta > 0 (elliptic.cpp:134-135)
+    ERR_REPAIR_SINGULAR = 1u << 6
+};
+
+inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+// ---- double-double helpers for order-robust sums (H4) --------------------
+struct DD {
+    double hi, lo;
+};
+__device__ __forceinline__ DD dd_add(DD a, DD b) {
+    const double s = __dadd_rn(a.hi, b.hi);
+    const double bb = __dsub_rn(s, a.hi);
+    const double err = __dadd_rn(__dsub_rn(a.hi, __dsub_rn(s, bb)), __dsub_rn(b.hi, bb));
+    const double lo = __dadd_rn(err, __dadd_rn(a.lo, b.lo));
+    const double hi = __dadd_rn(s, lo);
+    return DD{hi, __dsub_rn(lo, __dsub_rn(hi, s))};
+}
+__device__ __forceinline__ DD dd_shfl_down(DD v, int off) {
+    return DD{__shfl_down_sync(0xffffffffu, v.hi, off), __shfl_down_sync(0xffffffffu, v.lo, off)};
+}
+__device__ __forceinline__ DD warp_sum_dd(DD v) {
+    for (int o = 16; o > 0; o >>= 1) v = dd_add(v, dd_shfl_down(v, o));
+    return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_down_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ double warp_min(double v) {
+    for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_down_sync(0xffffffffu, v, o));
+    return v;
+}
+
+}  // namespace mpm2p

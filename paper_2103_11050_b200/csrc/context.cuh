@@ -1,0 +1,138 @@
+// context.cuh — device-resident state of one simulation (the B200 stand-in
+// for RunInputs + BasisSet + PerturbationState + the driver's fields,
+// proj/include/mrcmflow/{simulation,mrcm,mpm}.hpp) and the kernel launchers.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "layout.cuh"
+
+namespace mpm2p {
+
+// Per-step device scalars (one 256-byte block read back once per step).
+struct Scalars {
+    double dt, pvi, inj, eps_pending, eps, slope;
+    double repair_max, flux_scale, div_residual, div_scale;
+    double outlet_max, rcond, min_margin;
+    double eps_num_hi, eps_num_lo, eps_den_hi, eps_den_lo;
+    unsigned err;
+    int any_flow;
+    int rebuild_next;
+    int repair_warning;
+    long long clamp;
+    double pad[8];
+};
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void alloc(size_t count) {
+        if (count == n && p) return;
+        release();
+        n = count;
+        if (count) CK(cudaMalloc(&p, count * sizeof(T)));
+    }
+    void zero(cudaStream_t st) {
+        if (p) CK(cudaMemsetAsync(p, 0, n * sizeof(T), st));
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    operator T*() const { return p; }
+};
+
+struct Ctx {
+    Layout L;
+    cudaStream_t st = nullptr;
+    std::string err;
+    int num_sms = 148;
+
+    // problem (host copies for validation/readback)
+    double M = 1.0;
+    int alpha_mode = 0;
+    double alpha = 1, alpha_min = 1e-2, alpha_max = 1e2, pct_lo = 10, pct_hi = 90;
+    std::vector<int> bc_kind_h;
+    bool grounded = false;
+    bool anchor_m = false;  // rebuild-time operator is pure Neumann (1x1, all-flux)
+    bool repair_active = false;
+    int max_rhs = 1;        // 1 + max homogeneous solves per subdomain
+    int dim = 0;            // interface system dimension (2 * dim_flux)
+
+    // static data
+    DevBuf<double> K, q, bc_value, qsum_sub, ground, Linv;
+    DevBuf<int> bc_kind;
+    // transport / driver state
+    DevBuf<double> s, s2, u, p, kappa_n, kappa_m, lam_reb, T;
+    // rebuild cache (BasisSet)
+    DevBuf<double> beta_m, beta_p, alpha_e, face_kappa, sort_keys;
+    DevBuf<unsigned char> sort_tmp;
+    size_t sort_tmp_bytes = 0;
+    DevBuf<double> BDm, BWm, BSm, Dm, Lcm, Lrm;
+    DevBuf<double> HU, HB, HP;
+    DevBuf<double> pm, bpm, pmsum;
+    // interface system (CSR pattern built once; values per rebuild)
+    DevBuf<int> csr_ptr, csr_col;
+    DevBuf<double> csr_val, Mdense, Minv, gj_work, gj_col, gj_row, gj_krow;
+    DevBuf<int> gj_piv;
+    DevBuf<double> irhs, icoef, ires, idelta;
+    int nnz = 0;
+    // per-solve scratch
+    DevBuf<double> X, PU, PB, PS, GZ, WU, RU, RS, skel, resid, delta, corr;
+    // downscale
+    DevBuf<double> BDd, BWd, BSd, Dd, Lrd, Xd;
+    // scalars and reduction workspace
+    DevBuf<Scalars> sc;
+    DevBuf<double> red;
+    DevBuf<unsigned> red_count;
+    Scalars* sc_host = nullptr;  // pinned
+
+    bool has_basis = false;
+    bool has_factor = false;
+    double rcond = 0.0;
+
+    // counters (exact integers, SolveCounters mrcm.hpp:15-21)
+    long long c_hom = 0, c_part = 0, c_down = 0, c_fine = 0, c_iface = 0;
+    long long nhat = 0;
+};
+
+// ---- launchers (transport.cu) ----------------------------------------------
+void launch_max_slope(Ctx& c);
+void launch_cfl(Ctx& c, const double* u, double safety, double dt_cap);
+void launch_inj_pvi(Ctx& c, const double* u, double inflow, int cn, bool add_pvi);
+void launch_upwind(Ctx& c, const double* s_in, double* s_out, const double* u, double inflow);
+void launch_conductivity(Ctx& c, const double* s, double* kappa, int eps_mode, bool want_eps);
+void launch_outlet(Ctx& c, const double* s, const double* u);
+void launch_lambda(Ctx& c, const double* s, double* lam);
+void launch_divergence(Ctx& c, const double* u, double* div);
+void launch_decide(Ctx& c, int rebuilt, int method, double eta, int step);
+void launch_epsilon_fields(Ctx& c, const double* kn, const double* km, int mode);
+
+// ---- launchers (solver.cu) -------------------------------------------------
+void launch_trans(Ctx& c, const double* kappa);
+void launch_beta(Ctx& c, const double* kappa);
+void launch_rebuild(Ctx& c, const double* kappa, bool compute_beta = true);  // basis + interface matrix + recon_m + downscale
+void launch_mpm(Ctx& c, const double* kappa_n);       // MPM-2P update + downscale
+void launch_setup_static(Ctx& c);                     // qsum, ground, repair operator inverse
+void configure_kernels();
+
+// ---- launchers (dense.cu) --------------------------------------------------
+// In-place Gauss-Jordan inverse with partial pivoting of an n x n row-major
+// matrix A into Ainv; returns the 1-norm reciprocal condition number.
+double dense_inverse(Ctx& c, const double* A, double* Ainv, int n);
+void launch_gemv(Ctx& c, const double* A, const double* x, double* y, int n);
+void launch_csr_residual(Ctx& c, const int* ptr, const int* col, const double* val, const double* x,
+                         const double* b, double* r, int n);
+void launch_axpy(Ctx& c, double* y, const double* x, int n);
+
+}  // namespace mpm2p

@@ -1,0 +1,1070 @@
+// solver.cu — the velocity-update path on the device:
+//   K2  MPM data prep (w, q', g', z')                 proj/src/mpm.cpp:48-86
+//   K3  local Robin solves, cached factor             proj/src/mrcm.cpp:242-252, elliptic.cpp:152-243
+//   K4  rebuild: factor + homogeneous/particular       proj/src/mrcm.cpp:132-194
+//   K5  interface-matrix assembly (CSR, deterministic) proj/src/mrcm.cpp:196-224
+//   K6  interface rhs                                  proj/src/mrcm.cpp:80-100
+//   K8  trace recombination (reconstruct)              proj/src/mrcm.cpp:270-288
+//   K9  averaged skeleton flux + compatibility resid   proj/src/mrcm.cpp:290-304,315-340
+//   K10 static repair solve (graph Laplacian inverse)  proj/src/mrcm.cpp:347-383
+//   K11 downscale: fresh Neumann solve with kappa_n,   proj/src/mrcm.cpp:388-437
+//       mean shift, scatter, divergence residual
+//   K12 Robin parameter beta (adaptive quantiles)      proj/src/robin.cpp:39-92
+// One warp owns one subdomain in the banded kernels (band.cuh); everything
+// else is one thread per cell / face / edge / matrix entry. No floating-point
+// atomics: every sum has a fixed order, so runs are bitwise reproducible.
+#include <cub/device/device_radix_sort.cuh>
+
+#include "band.cuh"
+#include "context.cuh"
+
+namespace mpm2p {
+
+namespace {
+
+constexpr int TPB = 256;
+constexpr int WPB = 4;  // warps (subdomains) per block in banded kernels
+
+__device__ __forceinline__ bool last_block_done(unsigned* counter) {
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    __syncthreads();
+    return last;
+}
+
+__device__ __forceinline__ double block_max(double v, double* sh) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    v = warp_max(v);
+    if (lane == 0) sh[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        v = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0.0;
+        v = warp_max(v);
+    }
+    __syncthreads();
+    return v;
+}
+
+__device__ __forceinline__ size_t xoff(const Layout& L, int max_rhs, int s, int m) {
+    return ((size_t)s * max_rhs + m) * L.ncs;
+}
+
+// beta of a skeleton edge seen from subdomain side (RobinParameter::beta, robin.hpp:24-26)
+__device__ __forceinline__ double edge_beta(const Layout& L, const EdgeInfo& e, const double* bm, const double* bp) {
+    const int i = L.skel_index(e.iface, e.pos);
+    return e.sign > 0 ? bm[i] : bp[i];
+}
+
+// ---------------------------------------------------------------- K12 ----
+__global__ void k_face_kappa(Layout L, const double* __restrict__ kappa, double* __restrict__ fk) {
+    const int E = L.skeleton_edges();
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < E; x += gridDim.x * blockDim.x) {
+        const int k = x < L.NV * L.sny ? x / L.sny : L.NV + (x - L.NV * L.sny) / L.snx;
+        const int pos = x < L.NV * L.sny ? x % L.sny : (x - L.NV * L.sny) % L.snx;
+        int cm, cp;
+        L.iface_cells(k, pos, cm, cp);
+        fk[x] = 2.0 * kappa[cm] * kappa[cp] / (kappa[cm] + kappa[cp]);
+    }
+}
+
+__device__ double quantile_sorted(const double* v, int m, double pct) {  // robin.cpp:26-35
+    if (m == 0) return 0.0;
+    double idx = pct / 100.0 * (double)(m - 1);
+    idx = fmin(fmax(idx, 0.0), (double)(m - 1));
+    const int lo = (int)idx;
+    const int hi = lo + 1 < m - 1 ? lo + 1 : m - 1;
+    const double w = idx - (double)lo;
+    return (1.0 - w) * v[lo] + w * v[hi];
+}
+
+__global__ void k_beta(Layout L, const double* __restrict__ kappa, const double* __restrict__ fk,
+                       const double* __restrict__ sorted, int adaptive, double alpha, double amin, double amax,
+                       double plo, double phi, double* bm, double* bp, double* al, Scalars* sc) {
+    const int E = L.skeleton_edges();
+    double qlo = 0.0, qhi = 0.0;
+    if (adaptive && E > 0) {
+        qlo = quantile_sorted(sorted, E, plo);
+        qhi = quantile_sorted(sorted, E, phi);
+    }
+    const double Lx = L.lx / L.nsx, Ly = L.ly / L.nsy;
+    const double H = Lx > Ly ? Lx : Ly;  // coarse_h (decomposition.cpp:15-19)
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < E; x += gridDim.x * blockDim.x) {
+        const int k = x < L.NV * L.sny ? x / L.sny : L.NV + (x - L.NV * L.sny) / L.snx;
+        const int pos = x < L.NV * L.sny ? x % L.sny : (x - L.NV * L.sny) % L.snx;
+        int cm, cp;
+        L.iface_cells(k, pos, cm, cp);
+        if (!(kappa[cm] > 0.0) || !(kappa[cp] > 0.0)) atomicOr(&sc->err, ERR_KAPPA);
+        double a = alpha;
+        if (adaptive) {
+            const double v = fk[x];
+            a = v > qhi ? amin : (v < qlo ? amax : 1.0);
+        }
+        al[x] = a;
+        bm[x] = a * H / kappa[cm];
+        bp[x] = a * H / kappa[cp];
+    }
+}
+
+// ---------------------------------------------------------- transmissibility
+__global__ void k_trans(Layout L, const double* __restrict__ kappa, double* __restrict__ T) {  // elliptic.cpp:44-61
+    const int F = L.faces();
+    for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < F; f += gridDim.x * blockDim.x) {
+        double t = 0.0;
+        if (f < L.vcount()) {
+            const int i = f % (L.nx + 1), j = f / (L.nx + 1);
+            if (i > 0 && i < L.nx) t = harm_trans_v(L, kappa[L.cell(i - 1, j)], kappa[L.cell(i, j)]);
+        } else {
+            const int fh = f - L.vcount(), i = fh % L.nx, j = fh / L.nx;
+            if (j > 0 && j < L.ny) t = harm_trans_h(L, kappa[L.cell(i, j - 1)], kappa[L.cell(i, j)]);
+        }
+        T[f] = t;
+    }
+}
+
+// boundary-edge indices of a cell in W,E,S,N order (the for_each_boundary_face order)
+__device__ __forceinline__ int cell_edges(const Layout& L, int ii, int jj, int* idx) {
+    int n = 0;
+    if (ii == 0) idx[n++] = jj;
+    if (ii == L.snx - 1) idx[n++] = L.sny + jj;
+    if (jj == 0) idx[n++] = 2 * L.sny + ii;
+    if (jj == L.sny - 1) idx[n++] = 2 * L.sny + L.snx + ii;
+    return n;
+}
+
+// Band entries of the subdomain operator (elliptic.cpp:80-141).
+// mode 0: rebuild operator (Robin beta on the skeleton, physical kinds), anchor if anchor!=0
+// mode 1: downscale operator (all Flux, anchor cell 0)
+__global__ void k_band_entries(Layout L, const double* __restrict__ kappa, const double* __restrict__ T, int mode,
+                               int anchor, const double* __restrict__ bm, const double* __restrict__ bp,
+                               const int* __restrict__ bc_kind, double* __restrict__ BD, double* __restrict__ BW,
+                               double* __restrict__ BS, Scalars* sc) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= L.cells()) return;
+    const int i = c % L.nx, j = c / L.nx;
+    const int s = (j / L.sny) * L.nsx + i / L.snx;
+    const int ii = i % L.snx, jj = j % L.sny, r = jj * L.snx + ii;
+    const double kc = kappa[c];
+    if (!(kc > 0.0) || !isfinite(kc)) atomicOr(&sc->err, ERR_KAPPA);
+    double diag = 0.0;
+    if (ii > 0) diag += T[L.vface(i, j)];
+    if (ii < L.snx - 1) diag += T[L.vface(i + 1, j)];
+    if (jj > 0) diag += T[L.hface(i, j)];
+    if (jj < L.sny - 1) diag += T[L.hface(i, j + 1)];
+    double ow = ii > 0 ? T[L.vface(i, j)] : 0.0;
+    double os = jj > 0 ? T[L.hface(i, j)] : 0.0;
+    if (mode == 0) {
+        int idx[4];
+        const int ne = cell_edges(L, ii, jj, idx);
+        for (int t = 0; t < ne; ++t) {
+            const EdgeInfo e = L.edge(s, idx[t]);
+            const double th = half_trans(L, e.side, kc);
+            if (e.iface >= 0) {
+                const double beta = edge_beta(L, e, bm, bp);
+                if (!(beta > 0.0)) atomicOr(&sc->err, ERR_ROBIN_BETA);
+                diag += eff_robin(th, beta, e.area);
+            } else if (bc_kind[e.gbc] == BC_PRESSURE) {
+                diag += th;
+            }
+        }
+    }
+    if (anchor) {
+        if (r == 0) diag = 1.0;
+        if (r == 1) ow = 0.0;
+        if (r == L.snx) os = 0.0;
+    }
+    const size_t o = (size_t)s * L.ncs + r;
+    BD[o] = diag;
+    BW[o] = ow;
+    BS[o] = os;
+}
+
+// ---------------------------------------------------------------- K4 ----
+// Particular (m = 0) and homogeneous (m = 1 + h) right-hand sides
+// (elliptic.cpp:161-180 with the data of mrcm.cpp:164-191).
+__global__ void k_rebuild_rhs(Layout L, int max_rhs, const double* __restrict__ kappa, const double* __restrict__ q,
+                              const int* __restrict__ bc_kind, const double* __restrict__ bc_value,
+                              const double* __restrict__ bm, const double* __restrict__ bp, int anchor,
+                              double* __restrict__ X) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= L.cells()) return;
+    const int i = c % L.nx, j = c / L.nx;
+    const int s = (j / L.sny) * L.nsx + i / L.snx;
+    const int ii = i % L.snx, jj = j % L.sny, r = jj * L.snx + ii;
+    const double vol = L.vol();
+    int idx[4];
+    const int ne = cell_edges(L, ii, jj, idx);
+    EdgeInfo e[4];
+    for (int t = 0; t < ne; ++t) e[t] = L.edge(s, idx[t]);
+    const int nh = L.n_hom(s);
+    for (int m = 0; m <= nh; ++m) {
+        double b = (m == 0 ? q[c] : 0.0) * vol;
+        int hk = -1, ht = 0, hcol = 0;
+        bool hflux = false;
+        if (m > 0) L.hom(s, m - 1, hk, ht, hflux, hcol);
+        for (int t = 0; t < ne; ++t) {
+            const double th = half_trans(L, e[t].side, kappa[c]);
+            if (e[t].iface >= 0) {
+                const double beta = edge_beta(L, e[t], bm, bp);
+                double rr = 0.0;
+                if (m > 0 && e[t].iface == hk) {
+                    const double v = L.basis_val(hk, ht, e[t].pos);
+                    rr = hflux ? -beta * v * e[t].sign : v;
+                }
+                b += eff_robin(th, beta, e[t].area) * rr;
+            } else {
+                const double val = m == 0 ? bc_value[e[t].gbc] : 0.0;
+                if (bc_kind[e[t].gbc] == BC_PRESSURE) b += th * val;
+                else b -= val * e[t].area;
+            }
+        }
+        if (anchor && r == 0) b = 0.0;
+        X[xoff(L, max_rhs, s, m) + r] = b;
+    }
+}
+
+// Factor the rebuild operator (stored) and solve all its right-hand sides.
+__global__ void k_factor_solve(Layout L, int max_rhs, const double* __restrict__ BD, const double* __restrict__ BW,
+                               const double* __restrict__ BS, double* __restrict__ D, double* __restrict__ Lc,
+                               double* __restrict__ Lr, double* __restrict__ X, Scalars* sc) {
+    extern __shared__ double smem[];
+    const int w = threadIdx.x >> 5;
+    const int s = blockIdx.x * WPB + w;
+    if (s >= L.n_sub) return;
+    const int n = L.ncs, B = L.snx;
+    double* sm = smem + (size_t)w * band_smem_doubles(B, RING_NR);
+    const size_t so = (size_t)s * n;
+    const BandRows A{BD + so, BW + so, BS + so};
+    const int nr = 1 + L.n_hom(s);
+    double* Xs = X + xoff(L, max_rhs, s, 0);
+    const int n0 = nr < RING_NR ? nr : RING_NR;
+    const bool ok = band_factor_fwd(n, B, A, D + so, Lc + so * B, Lr + so * B, Xs, n0, n, sm);
+    if (!ok && (threadIdx.x & 31) == 0) atomicOr(&sc->err, ERR_PIVOT);
+    for (int m0 = n0; m0 < nr; m0 += RING_NR) {
+        const int cnt = nr - m0 < RING_NR ? nr - m0 : RING_NR;
+        band_forward(n, B, Lc + so * B, Xs + (size_t)m0 * n, cnt, n, sm);
+    }
+    for (int m0 = 0; m0 < nr; m0 += RING_NR) {
+        const int cnt = nr - m0 < RING_NR ? nr - m0 : RING_NR;
+        band_backward(n, B, D + so, Lr + so * B, Xs + (size_t)m0 * n, cnt, n, sm);
+    }
+}
+
+// Traces of every rebuild solution: outward normal velocity and face
+// pressure per boundary edge (elliptic.cpp:222-240).
+__global__ void k_rebuild_traces(Layout L, int max_rhs, const double* __restrict__ kappa,
+                                 const int* __restrict__ bc_kind, const double* __restrict__ bc_value,
+                                 const double* __restrict__ bm, const double* __restrict__ bp,
+                                 const double* __restrict__ X, double* __restrict__ PU, double* __restrict__ PB,
+                                 double* __restrict__ HU, double* __restrict__ HB) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= L.n_sub * L.nbe) return;
+    const int s = x / L.nbe, idx = x % L.nbe;
+    const EdgeInfo e = L.edge(s, idx);
+    const double th = half_trans(L, e.side, kappa[e.global_cell]);
+    const int nh = L.n_hom(s);
+    double beta = 0.0, te = 0.0;
+    if (e.iface >= 0) {
+        beta = edge_beta(L, e, bm, bp);
+        te = eff_robin(th, beta, e.area);
+    }
+    for (int m = 0; m <= nh; ++m) {
+        const double pc = X[xoff(L, max_rhs, s, m) + e.local_cell];
+        double un, pf;
+        if (e.iface >= 0) {
+            double rr = 0.0;
+            if (m > 0) {
+                int hk, ht, hcol;
+                bool hflux;
+                L.hom(s, m - 1, hk, ht, hflux, hcol);
+                if (e.iface == hk) {
+                    const double v = L.basis_val(hk, ht, e.pos);
+                    rr = hflux ? -beta * v * e.sign : v;
+                }
+            }
+            un = te * (pc - rr) / e.area;
+            pf = rr + beta * un;
+        } else {
+            const double val = m == 0 ? bc_value[e.gbc] : 0.0;
+            if (bc_kind[e.gbc] == BC_PRESSURE) {
+                un = th * (pc - val) / e.area;
+                pf = val;
+            } else {
+                un = val;
+                pf = pc - val * e.area / th;
+            }
+        }
+        if (m == 0) {
+            PU[x] = un;
+            PB[x] = pf;
+        } else {
+            const size_t o = ((size_t)s * L.max_hom + (m - 1)) * L.nbe + idx;
+            HU[o] = un;
+            HB[o] = pf;
+        }
+    }
+}
+
+// Per-(subdomain, solution) pressure sums, one warp each.
+__global__ void k_psums(Layout L, int max_rhs, const double* __restrict__ X, double* __restrict__ PS,
+                        double* __restrict__ HP) {
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (gw >= L.n_sub * max_rhs) return;
+    const int s = gw / max_rhs, m = gw % max_rhs;
+    if (m > L.n_hom(s)) return;
+    const double* x = X + xoff(L, max_rhs, s, m);
+    double v = 0.0;
+    for (int r = lane; r < L.ncs; r += 32) v += x[r];
+    v = warp_sum(v);
+    if (lane == 0) {
+        if (m == 0) PS[s] = v;
+        else HP[(size_t)s * L.max_hom + m - 1] = v;
+    }
+}
+
+// ---------------------------------------------------------------- K5 ----
+// Interface matrix in CSR (rows: psi-rows then phi-rows; cols: U then P).
+// Each entry sums the contributions of the (at most two) subdomains it
+// couples through, edge by edge in the reference's order (mrcm.cpp:199-224).
+__device__ __forceinline__ int hom_index(const Layout& L, int s, int col) {
+    const bool flux = col < L.dim_flux;
+    const int b = flux ? col : col - L.dim_flux;
+    const int k = L.basis_iface(b);
+    const int t = b - L.iface_first_basis(k);
+    int inc[4];
+    const int ni = L.incident(s, inc);
+    int half = 0, before = -1, acc = 0;
+    for (int a = 0; a < ni; ++a) {
+        if (inc[a] == k) before = acc;
+        acc += L.iface_nb(inc[a]);
+        half += L.iface_nb(inc[a]);
+    }
+    if (before < 0) return -1;
+    return (flux ? 0 : half) + before + t;
+}
+
+__global__ void k_assemble(Layout L, const int* __restrict__ ptr, const int* __restrict__ colv, int nrows,
+                           const double* __restrict__ HU, const double* __restrict__ bm,
+                           const double* __restrict__ bp, double* __restrict__ val) {
+    const int row = blockIdx.x * blockDim.x + threadIdx.x;
+    if (row >= nrows) return;
+    const int np = L.dim_flux;
+    const bool phi = row >= np;
+    const int rb = phi ? row - np : row;
+    const int k = L.basis_iface(rb);
+    const int rt = rb - L.iface_first_basis(k);
+    const int ne = L.iface_edges(k);
+    const int subs[2] = {L.iface_minus(k), L.iface_plus(k)};
+    for (int z = ptr[row]; z < ptr[row + 1]; ++z) {
+        const int col = colv[z];
+        const bool ucol = col < L.dim_flux;
+        const int cb = ucol ? col : col - L.dim_flux;
+        const bool same = phi && ucol && L.basis_iface(cb) == k;
+        const int ct = same ? cb - L.iface_first_basis(k) : 0;
+        double acc = 0.0;
+        for (int a = 0; a < 2; ++a) {
+            const int s = subs[a];
+            const int h = hom_index(L, s, col);
+            const double sign = a == 0 ? 1.0 : -1.0;
+            for (int pos = 0; pos < ne; ++pos) {
+                const int idx = L.edge_index_on_iface(s, k, pos);
+                const double len = k < L.NV ? L.hy : L.hx;
+                const double bse = a == 0 ? bm[L.skel_index(k, pos)] : bp[L.skel_index(k, pos)];
+                const double vr = L.basis_val(k, rt, pos);
+                if (h >= 0) {
+                    const double un = HU[((size_t)s * L.max_hom + h) * L.nbe + idx];
+                    if (phi) acc += bse * un * vr * sign * len;
+                    else acc += un * vr * len;
+                }
+                if (same) {
+                    const double ub = L.basis_val(k, ct, pos);
+                    acc -= bse * ub * sign * vr * sign * len;
+                }
+            }
+        }
+        val[z] = acc;
+    }
+}
+
+__global__ void k_csr_to_dense(const int* __restrict__ ptr, const int* __restrict__ colv,
+                               const double* __restrict__ val, int n, double* __restrict__ A) {
+    const int row = blockIdx.x;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) A[(size_t)row * n + j] = 0.0;
+    __syncthreads();
+    for (int z = ptr[row] + threadIdx.x; z < ptr[row + 1]; z += blockDim.x) A[(size_t)row * n + colv[z]] = val[z];
+}
+
+// ---------------------------------------------------------------- K6 ----
+// Interface rhs from the particular traces (mrcm.cpp:80-100).
+__global__ void k_iface_rhs(Layout L, const double* __restrict__ PU, const double* __restrict__ bm,
+                            const double* __restrict__ bp, double* __restrict__ rhs) {
+    const int row = blockIdx.x * blockDim.x + threadIdx.x;
+    const int np = L.dim_flux;
+    if (row >= 2 * np) return;
+    const bool phi = row >= np;
+    const int rb = phi ? row - np : row;
+    const int k = L.basis_iface(rb);
+    const int rt = rb - L.iface_first_basis(k);
+    const int ne = L.iface_edges(k);
+    const double len = k < L.NV ? L.hy : L.hx;
+    double acc = 0.0;
+    for (int a = 0; a < 2; ++a) {
+        const int s = a == 0 ? L.iface_minus(k) : L.iface_plus(k);
+        const double sign = a == 0 ? 1.0 : -1.0;
+        for (int pos = 0; pos < ne; ++pos) {
+            const int idx = L.edge_index_on_iface(s, k, pos);
+            const double un = PU[(size_t)s * L.nbe + idx];
+            const double v = L.basis_val(k, rt, pos);
+            if (phi) {
+                const double beta = a == 0 ? bm[L.skel_index(k, pos)] : bp[L.skel_index(k, pos)];
+                acc -= beta * un * v * sign * len;
+            } else {
+                acc -= un * v * len;
+            }
+        }
+    }
+    rhs[row] = acc;
+}
+
+// ---------------------------------------------------------------- K8 ----
+// Recombined traces: recon = particular + sum_h c_h hom_h (+ w for MPM),
+// in hom order, skipping zero coefficients (mrcm.cpp:270-288, mpm.cpp:93-103).
+__global__ void k_recon_traces(Layout L, const double* __restrict__ coef, const double* __restrict__ PU,
+                               const double* __restrict__ PB, const double* __restrict__ HU,
+                               const double* __restrict__ HB, const double* __restrict__ WU,
+                               double* __restrict__ RU, double* __restrict__ RB) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= L.n_sub * L.nbe) return;
+    const int s = x / L.nbe, idx = x % L.nbe;
+    double u = PU[x], b = RB ? PB[x] : 0.0;
+    const int nh = L.n_hom(s);
+    for (int h = 0; h < nh; ++h) {
+        int k, t, col;
+        bool fl;
+        L.hom(s, h, k, t, fl, col);
+        const double c = coef[col];
+        if (c == 0.0) continue;
+        const size_t o = ((size_t)s * L.max_hom + h) * L.nbe + idx;
+        u += c * HU[o];
+        if (RB) b += c * HB[o];
+    }
+    if (WU) u += WU[x];
+    RU[x] = u;
+    if (RB) RB[x] = b;
+}
+
+__global__ void k_recon_psum(Layout L, const double* __restrict__ coef, const double* __restrict__ PS,
+                             const double* __restrict__ HP, const double* __restrict__ pmsum,
+                             double* __restrict__ RS) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= L.n_sub) return;
+    double v = PS[s];
+    const int nh = L.n_hom(s);
+    for (int h = 0; h < nh; ++h) {
+        int k, t, col;
+        bool fl;
+        L.hom(s, h, k, t, fl, col);
+        const double c = coef[col];
+        if (c != 0.0) v += c * HP[(size_t)s * L.max_hom + h];
+    }
+    if (pmsum) v += pmsum[s];
+    RS[s] = v;
+}
+
+// Full reconstructed pressure at a rebuild (recon_m.p, kept for MPM steps).
+__global__ void k_recon_p(Layout L, int max_rhs, const double* __restrict__ coef, const double* __restrict__ X,
+                          double* __restrict__ pm) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= L.cells()) return;
+    const int i = c % L.nx, j = c / L.nx;
+    const int s = (j / L.sny) * L.nsx + i / L.snx;
+    const int r = (j % L.sny) * L.snx + i % L.snx;
+    double v = X[xoff(L, max_rhs, s, 0) + r];
+    const int nh = L.n_hom(s);
+    for (int h = 0; h < nh; ++h) {
+        int k, t, col;
+        bool fl;
+        L.hom(s, h, k, t, fl, col);
+        const double cc = coef[col];
+        if (cc != 0.0) v += cc * X[xoff(L, max_rhs, s, 1 + h) + r];
+    }
+    pm[c] = v;
+}
+
+__global__ void k_sub_sum(Layout L, const double* __restrict__ field, double* __restrict__ out) {
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (gw >= L.n_sub) return;
+    double v = 0.0;
+    for (int r = lane; r < L.ncs; r += 32) v += field[L.gcell_of(gw, r)];
+    v = warp_sum(v);
+    if (lane == 0) out[gw] = v;
+}
+
+// ---------------------------------------------------------------- K9 ----
+__global__ void k_skel(Layout L, const double* __restrict__ RU, double* __restrict__ skel) {  // mrcm.cpp:290-304
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= L.skeleton_edges()) return;
+    const int k = x < L.NV * L.sny ? x / L.sny : L.NV + (x - L.NV * L.sny) / L.snx;
+    const int pos = x < L.NV * L.sny ? x % L.sny : (x - L.NV * L.sny) % L.snx;
+    const int sm = L.iface_minus(k), sp = L.iface_plus(k);
+    const double um = RU[(size_t)sm * L.nbe + L.edge_index_on_iface(sm, k, pos)];   // sign +1
+    const double up = -RU[(size_t)sp * L.nbe + L.edge_index_on_iface(sp, k, pos)];  // sign -1
+    skel[x] = 0.5 * (um + up);
+}
+
+// Compatibility residual per subdomain, in the reference's edge order
+// (mrcm.cpp:315-340), plus flux_scale = max |skeleton flux|.
+__global__ void k_resid(Layout L, const double* __restrict__ skel, const double* __restrict__ RU,
+                        const double* __restrict__ qsum, double* __restrict__ resid, Scalars* sc, double* part,
+                        unsigned* counter) {
+    __shared__ double sh[32];
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    double fmaxv = 0.0;
+    if (s < L.n_sub) {
+        double outflow = 0.0;
+        for (int idx = 0; idx < L.nbe; ++idx) {
+            const EdgeInfo e = L.edge(s, idx);
+            double un;
+            if (e.iface >= 0) {
+                const double v = skel[L.skel_index(e.iface, e.pos)];
+                un = e.sign * v;
+                fmaxv = fmax(fmaxv, fabs(v));
+            } else {
+                un = RU[(size_t)s * L.nbe + idx];
+            }
+            outflow += un * e.area;
+        }
+        resid[s] = qsum[s] - outflow;
+    }
+    fmaxv = block_max(fmaxv, sh);
+    if (threadIdx.x == 0) part[blockIdx.x] = fmaxv;
+    if (last_block_done(counter)) {
+        if (threadIdx.x == 0) {
+            double m = 0.0;
+            for (unsigned b = 0; b < gridDim.x; ++b) m = fmax(m, part[b]);
+            sc->flux_scale = m;
+            *counter = 0;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- K10 ----
+// delta = Linv * resid, one warp per subdomain row; then interface corrections.
+__global__ void k_repair_delta(int n, const double* __restrict__ Linv, const double* __restrict__ resid,
+                               double* __restrict__ delta) {
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (gw >= n) return;
+    const double* row = Linv + (size_t)gw * n;
+    double v = 0.0;
+    for (int t = lane; t < n; t += 32) v += row[t] * resid[t];
+    v = warp_sum(v);
+    if (lane == 0) delta[gw] = v;
+}
+
+__global__ void k_repair_corr(Layout L, int active, int grounded, const double* __restrict__ delta,
+                              const double* __restrict__ ground, double* __restrict__ corr, Scalars* sc, double* part,
+                              unsigned* counter) {
+    __shared__ double sh[32];
+    double m = 0.0;
+    const int nthreads = L.n_iface > L.n_sub ? L.n_iface : L.n_sub;
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < nthreads; x += gridDim.x * blockDim.x) {
+        if (x < L.n_iface) {
+            const double cv = active ? delta[L.iface_minus(x)] - delta[L.iface_plus(x)] : 0.0;
+            corr[x] = cv;
+            m = fmax(m, fabs(cv));
+        }
+        if (active && grounded && x < L.n_sub && ground[x] > 0.0) m = fmax(m, fabs(delta[x]));
+    }
+    m = block_max(m, sh);
+    if (threadIdx.x == 0) part[blockIdx.x] = m;
+    if (last_block_done(counter)) {
+        if (threadIdx.x == 0) {
+            double r = 0.0;
+            for (unsigned b = 0; b < gridDim.x; ++b) r = fmax(r, part[b]);
+            sc->repair_max = r;
+            const double fs = sc->flux_scale;
+            sc->repair_warning = r > 0.1 * (fs > 0 ? fs : 1.0);
+            *counter = 0;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- K11 ----
+// Downscale operator entries (kappa_n, all Flux, anchor 0) and rhs
+// (mrcm.cpp:391-411; elliptic.cpp:161-181), one thread per cell; the edge's
+// imposed outward velocity is kept in EU for the velocity scatter.
+__global__ void k_ds_prep(Layout L, const double* __restrict__ kappa, const double* __restrict__ T,
+                          const double* __restrict__ q, const int* __restrict__ bc_kind,
+                          const double* __restrict__ skel, const double* __restrict__ corr,
+                          const double* __restrict__ RU, const double* __restrict__ delta, int grounded,
+                          double* __restrict__ BD, double* __restrict__ BW, double* __restrict__ BS,
+                          double* __restrict__ Xd, double* __restrict__ EU, Scalars* sc) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= L.cells()) return;
+    const int i = c % L.nx, j = c / L.nx;
+    const int s = (j / L.sny) * L.nsx + i / L.snx;
+    const int ii = i % L.snx, jj = j % L.sny, r = jj * L.snx + ii;
+    const double kc = kappa[c];
+    if (!(kc > 0.0) || !isfinite(kc)) atomicOr(&sc->err, ERR_KAPPA);
+    double diag = 0.0;
+    if (ii > 0) diag += T[L.vface(i, j)];
+    if (ii < L.snx - 1) diag += T[L.vface(i + 1, j)];
+    if (jj > 0) diag += T[L.hface(i, j)];
+    if (jj < L.sny - 1) diag += T[L.hface(i, j + 1)];
+    double ow = ii > 0 ? T[L.vface(i, j)] : 0.0;
+    double os = jj > 0 ? T[L.hface(i, j)] : 0.0;
+    double b = q[c] * L.vol();
+    int idx[4];
+    const int ne = cell_edges(L, ii, jj, idx);
+    for (int t = 0; t < ne; ++t) {
+        const EdgeInfo e = L.edge(s, idx[t]);
+        double un;
+        if (e.iface >= 0) {
+            un = e.sign * (skel[L.skel_index(e.iface, e.pos)] + corr[e.iface]);
+        } else {
+            un = RU[(size_t)s * L.nbe + idx[t]];
+            if (grounded && bc_kind[e.gbc] == BC_PRESSURE) un += delta[s];
+        }
+        EU[(size_t)s * L.nbe + idx[t]] = un;
+        b -= un * e.area;
+    }
+    if (r == 0) {
+        diag = 1.0;
+        b = 0.0;
+    }
+    if (r == 1) ow = 0.0;
+    if (r == L.snx) os = 0.0;
+    const size_t o = (size_t)s * L.ncs + r;
+    BD[o] = diag;
+    BW[o] = ow;
+    BS[o] = os;
+    Xd[o] = b;
+}
+
+// Fresh factorization + solve per subdomain; mean shift to the recon mean
+// (mrcm.cpp:409-424). x (unshifted) stays in Xd for the velocity scatter.
+__global__ void k_ds_solve(Layout L, const double* __restrict__ BD, const double* __restrict__ BW,
+                           const double* __restrict__ BS, double* __restrict__ D, double* __restrict__ Lr,
+                           double* __restrict__ Xd, const double* __restrict__ RS, double* __restrict__ p,
+                           Scalars* sc) {
+    extern __shared__ double smem[];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int s = blockIdx.x * WPB + w;
+    if (s >= L.n_sub) return;
+    const int n = L.ncs, B = L.snx;
+    double* sm = smem + (size_t)w * band_smem_doubles(B, 1);
+    const size_t so = (size_t)s * n;
+    const BandRows A{BD + so, BW + so, BS + so};
+    double* x = Xd + so;
+    const bool ok = band_factor_fwd(n, B, A, D + so, nullptr, Lr + so * B, x, 1, n, sm);
+    if (!ok && lane == 0) atomicOr(&sc->err, ERR_PIVOT);
+    band_backward(n, B, D + so, Lr + so * B, x, 1, n, sm);
+    __syncwarp();
+    double v = 0.0;
+    for (int r = lane; r < n; r += 32) v += x[r];
+    v = warp_sum(v);
+    const double shift = (__shfl_sync(0xffffffffu, RS[s], 0) - __shfl_sync(0xffffffffu, v, 0)) / n;
+    for (int r = lane; r < n; r += 32) p[L.gcell_of(s, r)] = x[r] + shift;
+}
+
+// Velocity scatter: interior faces from the unshifted local pressure,
+// subdomain-boundary faces from the imposed outward velocity (single-valued
+// on shared edges).
+__global__ void k_ds_u(Layout L, const double* __restrict__ T, const double* __restrict__ Xd,
+                       const double* __restrict__ EU, double* __restrict__ u) {
+    const int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= L.faces()) return;
+    if (f < L.vcount()) {
+        const int i = f % (L.nx + 1), j = f / (L.nx + 1);
+        const int sy = j / L.sny, jj = j % L.sny;
+        if (i % L.snx != 0) {
+            const int sx = i / L.snx, ii = i % L.snx;
+            const size_t o = (size_t)(sy * L.nsx + sx) * L.ncs + jj * L.snx;
+            u[f] = T[f] * (Xd[o + ii - 1] - Xd[o + ii]) / L.hy;
+        } else if (i < L.nx) {  // west edge of subdomain (i / snx)
+            const int s = sy * L.nsx + i / L.snx;
+            u[f] = -EU[(size_t)s * L.nbe + jj];
+        } else {  // east domain boundary: east edge of the last column
+            const int s = sy * L.nsx + L.nsx - 1;
+            u[f] = EU[(size_t)s * L.nbe + L.sny + jj];
+        }
+    } else {
+        const int fh = f - L.vcount(), i = fh % L.nx, j = fh / L.nx;
+        const int sx = i / L.snx, ii = i % L.snx;
+        if (j % L.sny != 0) {
+            const int sy = j / L.sny, jj = j % L.sny;
+            const size_t o = (size_t)(sy * L.nsx + sx) * L.ncs + ii;
+            u[f] = T[f] * (Xd[o + (size_t)(jj - 1) * L.snx] - Xd[o + (size_t)jj * L.snx]) / L.hx;
+        } else if (j < L.ny) {  // south edge of subdomain (j / sny)
+            const int s = (j / L.sny) * L.nsx + sx;
+            u[f] = -EU[(size_t)s * L.nbe + 2 * L.sny + ii];
+        } else {
+            const int s = (L.nsy - 1) * L.nsx + sx;
+            u[f] = EU[(size_t)s * L.nbe + 2 * L.sny + L.snx + ii];
+        }
+    }
+}
+
+// max_c |div u - q| and max(|q|, |u_f| area / vol) (mrcm.cpp:429-437).
+__global__ void k_divres(Layout L, const double* __restrict__ u, const double* __restrict__ q, Scalars* sc,
+                         double* part, unsigned* counter) {
+    __shared__ double sh[32];
+    double res = 0.0, scale = 0.0;
+    const double vol = L.vol();
+    const int n = L.cells() > L.faces() ? L.cells() : L.faces();
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
+        if (x < L.cells()) {
+            const int i = x % L.nx, j = x / L.nx;
+            const double fx = (u[L.vface(i + 1, j)] - u[L.vface(i, j)]) * L.hy;
+            const double fy = (u[L.hface(i, j + 1)] - u[L.hface(i, j)]) * L.hx;
+            res = fmax(res, fabs((fx + fy) / vol - q[x]));
+            scale = fmax(scale, fabs(q[x]));
+        }
+        if (x < L.faces()) scale = fmax(scale, fabs(u[x]) * L.area(x) / vol);
+    }
+    res = block_max(res, sh);
+    scale = block_max(scale, sh);
+    if (threadIdx.x == 0) {
+        part[2 * blockIdx.x] = res;
+        part[2 * blockIdx.x + 1] = scale;
+    }
+    if (last_block_done(counter)) {
+        if (threadIdx.x == 0) {
+            double r = 0.0, sc2 = 0.0;
+            for (unsigned b = 0; b < gridDim.x; ++b) {
+                r = fmax(r, part[2 * b]);
+                sc2 = fmax(sc2, part[2 * b + 1]);
+            }
+            sc->div_residual = r;
+            sc->div_scale = sc2 > 0.0 ? sc2 : 1.0;
+            *counter = 0;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- K2 ----
+// MPM-2P data: w from p^m under kappa_n; q' = q - div w; g' = g - p^m_face;
+// z' = z - w.n_out; particular rhs under the cached (kappa_m, beta) operator
+// (mpm.cpp:48-86; elliptic.cpp:161-181).
+__global__ void k_mpm_rhs(Layout L, int max_rhs, int anchor, const double* __restrict__ kn,
+                          const double* __restrict__ km, const double* __restrict__ Tn,
+                          const double* __restrict__ q, const int* __restrict__ bc_kind,
+                          const double* __restrict__ bc_value, const double* __restrict__ bm,
+                          const double* __restrict__ bp, const double* __restrict__ pm,
+                          const double* __restrict__ bpm, double* __restrict__ X, double* __restrict__ GZ,
+                          double* __restrict__ WU) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= L.cells()) return;
+    const int i = c % L.nx, j = c / L.nx;
+    const int s = (j / L.sny) * L.nsx + i / L.snx;
+    const int ii = i % L.snx, jj = j % L.sny, r = jj * L.snx + ii;
+    const double pc = pm[c];
+    int idx[4];
+    const int ne = cell_edges(L, ii, jj, idx);
+    double wun[4];
+    for (int t = 0; t < ne; ++t) {
+        const EdgeInfo e = L.edge(s, idx[t]);
+        const double tn = half_trans(L, e.side, kn[c]);
+        wun[t] = tn * (pc - bpm[(size_t)s * L.nbe + idx[t]]) / e.area;
+    }
+    auto bw = [&](int side) -> double {  // boundary w (global orientation) for a side of this cell
+        for (int t = 0; t < ne; ++t) {
+            const int id = idx[t];
+            const int sd = id < L.sny ? SIDE_W : id < 2 * L.sny ? SIDE_E : id < 2 * L.sny + L.snx ? SIDE_S : SIDE_N;
+            if (sd == side) return (side == SIDE_E || side == SIDE_N) ? wun[t] : -wun[t];
+        }
+        return 0.0;
+    };
+    const double wW = ii > 0 ? Tn[L.vface(i, j)] * (pm[L.cell(i - 1, j)] - pc) / L.hy : bw(SIDE_W);
+    const double wE = ii < L.snx - 1 ? Tn[L.vface(i + 1, j)] * (pc - pm[L.cell(i + 1, j)]) / L.hy : bw(SIDE_E);
+    const double wS = jj > 0 ? Tn[L.hface(i, j)] * (pm[L.cell(i, j - 1)] - pc) / L.hx : bw(SIDE_S);
+    const double wN = jj < L.sny - 1 ? Tn[L.hface(i, j + 1)] * (pc - pm[L.cell(i, j + 1)]) / L.hx : bw(SIDE_N);
+    const double fx = (wE - wW) * L.hy;
+    const double fy = (wN - wS) * L.hx;
+    const double divw = (fx + fy) / L.vol();
+    double b = (q[c] - divw) * L.vol();
+    for (int t = 0; t < ne; ++t) {
+        const EdgeInfo e = L.edge(s, idx[t]);
+        const double th = half_trans(L, e.side, km[c]);
+        const size_t eo = (size_t)s * L.nbe + idx[t];
+        WU[eo] = wun[t];
+        if (e.iface >= 0) {
+            b += eff_robin(th, edge_beta(L, e, bm, bp), e.area) * 0.0;
+            GZ[eo] = 0.0;
+        } else if (bc_kind[e.gbc] == BC_PRESSURE) {
+            const double g = bc_value[e.gbc] - bpm[eo];
+            GZ[eo] = g;
+            b += th * g;
+        } else {
+            const double z = bc_value[e.gbc] - wun[t];
+            GZ[eo] = z;
+            b -= z * e.area;
+        }
+    }
+    if (anchor && r == 0) b = 0.0;
+    X[xoff(L, max_rhs, s, 0) + r] = b;
+}
+
+// Particular solve with the cached rebuild factor (mrcm.cpp:248).
+__global__ void k_part_solve(Layout L, int max_rhs, const double* __restrict__ D, const double* __restrict__ Lc,
+                             const double* __restrict__ Lr, double* __restrict__ X) {
+    extern __shared__ double smem[];
+    const int w = threadIdx.x >> 5;
+    const int s = blockIdx.x * WPB + w;
+    if (s >= L.n_sub) return;
+    const int n = L.ncs, B = L.snx;
+    double* sm = smem + (size_t)w * band_smem_doubles(B, 1);
+    const size_t so = (size_t)s * n;
+    double* x = X + xoff(L, max_rhs, s, 0);
+    band_forward(n, B, Lc + so * B, x, 1, n, sm);
+    band_backward(n, B, D + so, Lr + so * B, x, 1, n, sm);
+}
+
+// Particular traces under the cached operator with the modified data.
+__global__ void k_part_traces(Layout L, int max_rhs, const double* __restrict__ km,
+                              const int* __restrict__ bc_kind, const double* __restrict__ bm,
+                              const double* __restrict__ bp, const double* __restrict__ GZ,
+                              const double* __restrict__ X, double* __restrict__ PU) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= L.n_sub * L.nbe) return;
+    const int s = x / L.nbe, idx = x % L.nbe;
+    const EdgeInfo e = L.edge(s, idx);
+    const double th = half_trans(L, e.side, km[e.global_cell]);
+    const double pc = X[xoff(L, max_rhs, s, 0) + e.local_cell];
+    double un;
+    if (e.iface >= 0) {
+        const double te = eff_robin(th, edge_beta(L, e, bm, bp), e.area);
+        un = te * (pc - 0.0) / e.area;
+    } else if (bc_kind[e.gbc] == BC_PRESSURE) {
+        un = th * (pc - GZ[x]) / e.area;
+    } else {
+        un = GZ[x];
+    }
+    PU[x] = un;
+}
+
+__global__ void k_part_psum(Layout L, int max_rhs, const double* __restrict__ X, double* __restrict__ PS) {
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (gw >= L.n_sub) return;
+    const double* x = X + xoff(L, max_rhs, gw, 0);
+    double v = 0.0;
+    for (int r = lane; r < L.ncs; r += 32) v += x[r];
+    v = warp_sum(v);
+    if (lane == 0) PS[gw] = v;
+}
+
+// ---------------------------------------------------------------- static --
+__global__ void k_static(Layout L, const double* __restrict__ q, const int* __restrict__ bc_kind,
+                         double* __restrict__ qsum, double* __restrict__ ground) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= L.n_sub) return;
+    const double vol = L.vol();
+    double qs = 0.0;  // mrcm.cpp:323-325, row-major order
+    for (int jj = 0; jj < L.sny; ++jj)
+        for (int ii = 0; ii < L.snx; ++ii) qs += q[L.cell(L.sub_i0(s) + ii, L.sub_j0(s) + jj)] * vol;
+    qsum[s] = qs;
+    double g = 0.0;  // mrcm.cpp:333-336
+    for (int idx = 0; idx < L.nbe; ++idx) {
+        const EdgeInfo e = L.edge(s, idx);
+        if (e.iface < 0 && bc_kind[e.gbc] == BC_PRESSURE) g += e.area;
+    }
+    ground[s] = g;
+}
+
+// Dense repair operator (mrcm.cpp:351-371): one thread per row.
+__global__ void k_repair_matrix(Layout L, int grounded, const double* __restrict__ ground, double* __restrict__ A) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    const int n = L.n_sub;
+    if (s >= n) return;
+    double* row = A + (size_t)s * n;
+    for (int t = 0; t < n; ++t) row[t] = 0.0;
+    int inc[4];
+    const int ni = L.incident(s, inc);
+    for (int a = 0; a < ni; ++a) {
+        const int k = inc[a];
+        const double area = L.iface_edges(k) * (k < L.NV ? L.hy : L.hx);
+        row[s] += area;
+        const int other = L.iface_minus(k) == s ? L.iface_plus(k) : L.iface_minus(k);
+        row[other] -= area;
+    }
+    if (grounded) {
+        row[s] += ground[s];
+    } else {
+        if (s == 0)
+            for (int t = 0; t < n; ++t) row[t] = 0.0;
+        row[0] = 0.0;
+        if (s == 0) row[0] = 1.0;
+    }
+}
+
+int grid_for(long long n) { return std::max(1, cdiv(n, TPB)); }
+int band_blocks(const Layout& L) { return cdiv(L.n_sub, WPB); }
+
+}  // namespace
+
+void launch_trans(Ctx& c, const double* kappa) {
+    k_trans<<<std::min(grid_for(c.L.faces()), 8 * c.num_sms), TPB, 0, c.st>>>(c.L, kappa, c.T);
+    CK_LAUNCH();
+}
+
+void launch_beta(Ctx& c, const double* kappa) {
+    const Layout& L = c.L;
+    const int E = L.skeleton_edges();
+    if (E == 0) return;
+    k_face_kappa<<<grid_for(E), TPB, 0, c.st>>>(L, kappa, c.face_kappa);
+    CK_LAUNCH();
+    if (c.alpha_mode == 1) {
+        size_t bytes = c.sort_tmp_bytes;
+        CK(cub::DeviceRadixSort::SortKeys(c.sort_tmp.p, bytes, c.face_kappa.p, c.sort_keys.p, E, 0, 64, c.st));
+    }
+    k_beta<<<grid_for(E), TPB, 0, c.st>>>(L, kappa, c.face_kappa, c.sort_keys, c.alpha_mode, c.alpha, c.alpha_min,
+                                          c.alpha_max, c.pct_lo, c.pct_hi, c.beta_m, c.beta_p, c.alpha_e, c.sc);
+    CK_LAUNCH();
+}
+
+void launch_setup_static(Ctx& c) {
+    const Layout& L = c.L;
+    k_static<<<grid_for(L.n_sub), TPB, 0, c.st>>>(L, c.q, c.bc_kind, c.qsum_sub, c.ground);
+    CK_LAUNCH();
+    if (c.repair_active) {
+        DevBuf<double> A;
+        A.alloc((size_t)L.n_sub * L.n_sub);
+        k_repair_matrix<<<grid_for(L.n_sub), TPB, 0, c.st>>>(L, c.grounded ? 1 : 0, c.ground, A);
+        CK_LAUNCH();
+        const double rc = dense_inverse(c, A, c.Linv, L.n_sub);
+        if (!(rc > 0.0)) throw NumericError("downscale: compatibility-repair operator is singular");
+    }
+}
+
+namespace {
+
+// Downscale shared by the rebuild and the MPM step (mrcm.cpp:306-439); needs
+// c.T = transmissibility(kappa), RU/RS = recon traces and pressure sums.
+void downscale(Ctx& c, const double* kappa) {
+    const Layout& L = c.L;
+    if (L.skeleton_edges() > 0) {
+        k_skel<<<grid_for(L.skeleton_edges()), TPB, 0, c.st>>>(L, c.RU, c.skel);
+        CK_LAUNCH();
+    }
+    k_resid<<<grid_for(L.n_sub), TPB, 0, c.st>>>(L, c.skel, c.RU, c.qsum_sub, c.resid, c.sc, c.red, c.red_count);
+    CK_LAUNCH();
+    if (c.repair_active) {
+        k_repair_delta<<<cdiv((long long)L.n_sub * 32, TPB), TPB, 0, c.st>>>(L.n_sub, c.Linv, c.resid, c.delta);
+        CK_LAUNCH();
+    }
+    k_repair_corr<<<std::min(grid_for(std::max(L.n_iface, L.n_sub)), 2 * c.num_sms), TPB, 0, c.st>>>(
+        L, c.repair_active ? 1 : 0, c.grounded ? 1 : 0, c.delta, c.ground, c.corr, c.sc, c.red, c.red_count);
+    CK_LAUNCH();
+    k_ds_prep<<<grid_for(L.cells()), TPB, 0, c.st>>>(L, kappa, c.T, c.q, c.bc_kind, c.skel, c.corr, c.RU, c.delta,
+                                                     c.grounded ? 1 : 0, c.BDd, c.BWd, c.BSd, c.Xd, c.GZ, c.sc);
+    CK_LAUNCH();
+    const size_t sm1 = (size_t)WPB * band_smem_doubles(L.snx, 1) * sizeof(double);
+    k_ds_solve<<<band_blocks(L), WPB * 32, sm1, c.st>>>(L, c.BDd, c.BWd, c.BSd, c.Dd, c.Lrd, c.Xd, c.RS, c.p, c.sc);
+    CK_LAUNCH();
+    k_ds_u<<<grid_for(L.faces()), TPB, 0, c.st>>>(L, c.T, c.Xd, c.GZ, c.u);
+    CK_LAUNCH();
+    k_divres<<<std::min(grid_for(std::max(L.cells(), L.faces())), 2 * c.num_sms), TPB, 0, c.st>>>(L, c.u, c.q, c.sc,
+                                                                                               c.red, c.red_count);
+    CK_LAUNCH();
+    c.c_down += L.n_sub;
+}
+
+void interface_solve(Ctx& c) {
+    const Layout& L = c.L;
+    c.c_iface += 1;
+    if (c.dim == 0) return;
+    k_iface_rhs<<<grid_for(c.dim), TPB, 0, c.st>>>(L, c.PU, c.beta_m, c.beta_p, c.irhs);
+    CK_LAUNCH();
+    launch_gemv(c, c.Minv, c.irhs, c.icoef, c.dim);
+    // one step of iterative refinement against the sparse operator
+    launch_csr_residual(c, c.csr_ptr, c.csr_col, c.csr_val, c.icoef, c.irhs, c.ires, c.dim);
+    launch_gemv(c, c.Minv, c.ires, c.idelta, c.dim);
+    launch_axpy(c, c.icoef, c.idelta, c.dim);
+}
+
+}  // namespace
+
+void configure_kernels() {
+    CK(cudaFuncSetAttribute(k_factor_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(k_ds_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(k_part_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+}
+
+void launch_rebuild(Ctx& c, const double* kappa, bool compute_beta) {  // compute_beta + mrcm_solve (simulation.cpp:183-193)
+    const Layout& L = c.L;
+    if (compute_beta) launch_beta(c, kappa);
+    launch_trans(c, kappa);
+    k_band_entries<<<grid_for(L.cells()), TPB, 0, c.st>>>(L, kappa, c.T, 0, c.anchor_m ? 1 : 0, c.beta_m, c.beta_p,
+                                                          c.bc_kind, c.BDm, c.BWm, c.BSm, c.sc);
+    CK_LAUNCH();
+    k_rebuild_rhs<<<grid_for(L.cells()), TPB, 0, c.st>>>(L, c.max_rhs, kappa, c.q, c.bc_kind, c.bc_value, c.beta_m,
+                                                         c.beta_p, c.anchor_m ? 1 : 0, c.X);
+    CK_LAUNCH();
+    const size_t smr = (size_t)WPB * band_smem_doubles(L.snx, RING_NR) * sizeof(double);
+    k_factor_solve<<<band_blocks(L), WPB * 32, smr, c.st>>>(L, c.max_rhs, c.BDm, c.BWm, c.BSm, c.Dm, c.Lcm, c.Lrm, c.X,
+                                                            c.sc);
+    CK_LAUNCH();
+    k_rebuild_traces<<<grid_for((long long)L.n_sub * L.nbe), TPB, 0, c.st>>>(
+        L, c.max_rhs, kappa, c.bc_kind, c.bc_value, c.beta_m, c.beta_p, c.X, c.PU, c.PB, c.HU, c.HB);
+    CK_LAUNCH();
+    k_psums<<<cdiv((long long)L.n_sub * c.max_rhs * 32, TPB), TPB, 0, c.st>>>(L, c.max_rhs, c.X, c.PS, c.HP);
+    CK_LAUNCH();
+    c.c_hom += c.nhat;
+    c.c_part += L.n_sub;
+    // interface matrix: assemble, invert, guard (mrcm.cpp:196-238)
+    if (c.dim > 0) {
+        k_assemble<<<grid_for(c.dim), TPB, 0, c.st>>>(L, c.csr_ptr, c.csr_col, c.dim, c.HU, c.beta_m, c.beta_p,
+                                                      c.csr_val);
+        CK_LAUNCH();
+        k_csr_to_dense<<<c.dim, TPB, 0, c.st>>>(c.csr_ptr, c.csr_col, c.csr_val, c.dim, c.Mdense);
+        CK_LAUNCH();
+        c.rcond = dense_inverse(c, c.Mdense, c.Minv, c.dim);
+        if (!(c.rcond > 1e-14))
+            throw NumericError("compute_basis_set: interface matrix is numerically singular (rcond=" +
+                               std::to_string(c.rcond) + ")");
+    }
+    interface_solve(c);
+    // recon_m (kept for MPM steps) and its traces
+    if (c.dim == 0) CK(cudaMemsetAsync(c.icoef, 0, sizeof(double), c.st));
+    k_recon_traces<<<grid_for((long long)L.n_sub * L.nbe), TPB, 0, c.st>>>(L, c.icoef, c.PU, c.PB, c.HU, c.HB, nullptr,
+                                                                           c.RU, c.bpm);
+    CK_LAUNCH();
+    k_recon_p<<<grid_for(L.cells()), TPB, 0, c.st>>>(L, c.max_rhs, c.icoef, c.X, c.pm);
+    CK_LAUNCH();
+    k_sub_sum<<<cdiv((long long)L.n_sub * 32, TPB), TPB, 0, c.st>>>(L, c.pm, c.pmsum);
+    CK_LAUNCH();
+    CK(cudaMemcpyAsync(c.RS, c.pmsum, L.n_sub * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
+    CK(cudaMemcpyAsync(c.kappa_m, kappa, L.cells() * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
+    downscale(c, kappa);
+    c.has_basis = true;
+}
+
+void launch_mpm(Ctx& c, const double* kn) {  // mpm_pressure_update (mpm.cpp:31-114)
+    const Layout& L = c.L;
+    if (!c.has_basis) throw ConfigError("mpm_pressure_update: no basis set (rebuild first)");
+    launch_trans(c, kn);
+    k_mpm_rhs<<<grid_for(L.cells()), TPB, 0, c.st>>>(L, c.max_rhs, c.anchor_m ? 1 : 0, kn, c.kappa_m, c.T, c.q,
+                                                     c.bc_kind, c.bc_value, c.beta_m, c.beta_p, c.pm, c.bpm, c.X,
+                                                     c.GZ, c.WU);
+    CK_LAUNCH();
+    const size_t sm1 = (size_t)WPB * band_smem_doubles(L.snx, 1) * sizeof(double);
+    k_part_solve<<<band_blocks(L), WPB * 32, sm1, c.st>>>(L, c.max_rhs, c.Dm, c.Lcm, c.Lrm, c.X);
+    CK_LAUNCH();
+    k_part_traces<<<grid_for((long long)L.n_sub * L.nbe), TPB, 0, c.st>>>(L, c.max_rhs, c.kappa_m, c.bc_kind, c.beta_m,
+                                                                          c.beta_p, c.GZ, c.X, c.PU);
+    CK_LAUNCH();
+    k_part_psum<<<cdiv((long long)L.n_sub * 32, TPB), TPB, 0, c.st>>>(L, c.max_rhs, c.X, c.PS);
+    CK_LAUNCH();
+    c.c_part += L.n_sub;
+    interface_solve(c);
+    if (c.dim == 0) CK(cudaMemsetAsync(c.icoef, 0, sizeof(double), c.st));
+    k_recon_traces<<<grid_for((long long)L.n_sub * L.nbe), TPB, 0, c.st>>>(L, c.icoef, c.PU, nullptr, c.HU, nullptr,
+                                                                           c.WU, c.RU, nullptr);
+    CK_LAUNCH();
+    k_recon_psum<<<grid_for(L.n_sub), TPB, 0, c.st>>>(L, c.icoef, c.PS, c.HP, c.pmsum, c.RS);
+    CK_LAUNCH();
+    downscale(c, kn);
+}
+
+}  // namespace mpm2p

@@ -1,0 +1,421 @@
+// transport.cu — K1: explicit upwind saturation update, CFL reduction,
+// conductivity, drift (epsilon) partial sums, injection rate / PVI clock and
+// the outlet-saturation breakthrough probe (proj/src/transport.cpp:13-126,
+// proj/src/mpm.cpp:9-29, proj/src/simulation.cpp:61-101,162-174,274-289).
+//
+// Compiled with --fmad=false: every per-cell expression keeps the
+// reference's operation order and IEEE rounding, so saturation is
+// bit-identical to the CPU path given the same velocity field (Appendix B
+// items 6-7 of SURVEY.md). HBM-bound: one cell-update reads s (8 B) and two
+// faces' u (16 B amortised) and writes s (8 B).
+#include "context.cuh"
+
+namespace mpm2p {
+
+namespace {
+
+constexpr int TPB = 256;
+
+__device__ __forceinline__ double clamp_s(double s, long long* cnt) {  // transport.cpp:13-21
+    if (s < 0.0 || s > 1.0) {
+        if (cnt) atomicAdd((unsigned long long*)cnt, 1ull);
+        return s < 0.0 ? 0.0 : 1.0;
+    }
+    return s;
+}
+__device__ __forceinline__ double frac_flow(double s, double M, long long* cnt) {  // transport.cpp:39-43
+    s = clamp_s(s, cnt);
+    const double w = M * s * s;
+    return w / (w + (1.0 - s) * (1.0 - s));
+}
+__device__ __forceinline__ double total_mob(double s, double M, long long* cnt) {  // transport.cpp:34-37
+    s = clamp_s(s, cnt);
+    return M * s * s + (1.0 - s) * (1.0 - s);
+}
+__device__ __forceinline__ double fprime(double s, double M) {  // transport.cpp:23-27
+    const double d = M * s * s + (1.0 - s) * (1.0 - s);
+    const double dd = 2.0 * M * s - 2.0 * (1.0 - s);
+    return (2.0 * M * s * d - M * s * s * dd) / (d * d);
+}
+
+// Block reduction helpers; the final combination over blocks is done by the
+// last block to finish, in block order, so results are deterministic.
+__device__ __forceinline__ bool last_block_done(unsigned* counter) {
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned t = atomicAdd(counter, 1u);
+        last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    return last;
+}
+
+template <typename F>
+__device__ __forceinline__ double block_reduce(double v, F op, double* sh, double ident) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_down_sync(0xffffffffu, v, o));
+    if (lane == 0) sh[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        v = lane < (int)(blockDim.x >> 5) ? sh[lane] : ident;
+        for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_down_sync(0xffffffffu, v, o));
+    }
+    __syncthreads();
+    return v;
+}
+
+__device__ __forceinline__ DD block_reduce_dd(DD v, DD* sh) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    v = warp_sum_dd(v);
+    if (lane == 0) sh[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        v = lane < (int)(blockDim.x >> 5) ? sh[lane] : DD{0.0, 0.0};
+        v = warp_sum_dd(v);
+    }
+    __syncthreads();
+    return v;
+}
+
+__global__ void k_max_slope(Scalars* sc, double M) {  // transport.cpp:45-49
+    double m = 0.0;
+    for (int k = 0; k <= 1000; ++k) m = fmax(m, fprime(k * 1e-3, M));
+    sc->slope = m;
+}
+
+// cfl_timestep (transport.cpp:51-71): min over cells of vol/(outflux*slope).
+__global__ void k_cfl(Layout L, const double* __restrict__ u, Scalars* sc, double safety, double dt_cap,
+                      double* part, unsigned* counter) {
+    __shared__ double sh[32];
+    const double vol = L.vol(), slope = sc->slope;
+    double best = INFINITY;
+    double any = 0.0;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < L.cells(); c += gridDim.x * blockDim.x) {
+        const int i = c % L.nx, j = c / L.nx;
+        double out = 0.0;
+        const double uE = u[L.vface(i + 1, j)], uW = u[L.vface(i, j)];
+        const double uN = u[L.hface(i, j + 1)], uS = u[L.hface(i, j)];
+        out += (0.0 < uE ? uE : 0.0) * L.hy;
+        out += (0.0 < -uW ? -uW : 0.0) * L.hy;
+        out += (0.0 < uN ? uN : 0.0) * L.hx;
+        out += (0.0 < -uS ? -uS : 0.0) * L.hx;
+        if (out > 0.0) {
+            any = 1.0;
+            best = fmin(best, vol / (out * slope));
+        }
+    }
+    best = block_reduce(best, [](double a, double b) { return fmin(a, b); }, sh, INFINITY);
+    any = block_reduce(any, [](double a, double b) { return fmax(a, b); }, sh, 0.0);
+    if (threadIdx.x == 0) {
+        part[2 * blockIdx.x] = best;
+        part[2 * blockIdx.x + 1] = any;
+    }
+    if (last_block_done(counter)) {
+        if (threadIdx.x == 0) {
+            double dt = dt_cap / safety;
+            bool anyf = false;
+            for (unsigned b = 0; b < gridDim.x; ++b) {
+                dt = fmin(dt, part[2 * b]);
+                anyf = anyf || part[2 * b + 1] > 0.0;
+            }
+            sc->any_flow = anyf;
+            sc->dt = anyf ? fmin(safety * dt, dt_cap) : dt_cap;
+            *counter = 0;
+        }
+    }
+}
+
+// injection_rate (simulation.cpp:85-101), summed in the reference's face
+// order (W_j, E_j for each j, then S_i, N_i for each i) by one block, then the
+// PVI clock advanced cn times (simulation.cpp:288).
+__global__ void k_inj_pvi(Layout L, const double* __restrict__ u, Scalars* sc, double inflow, double M, int cn,
+                          int add_pvi) {
+    __shared__ double terms[2 * TPB];
+    const double fin = frac_flow(inflow, M, nullptr);
+    const int nterms = 2 * (L.nx + L.ny);
+    double rate = 0.0;
+    for (int base = 0; base < nterms; base += 2 * TPB) {
+        for (int t = threadIdx.x; t < 2 * TPB; t += blockDim.x) {
+            const int idx = base + t;
+            double v = 0.0;
+            if (idx < nterms) {
+                double un, area;
+                if (idx < 2 * L.ny) {
+                    const int j = idx >> 1;
+                    if ((idx & 1) == 0) { un = -u[L.vface(0, j)]; } else { un = u[L.vface(L.nx, j)]; }
+                    area = L.hy;
+                } else {
+                    const int k = idx - 2 * L.ny, i = k >> 1;
+                    if ((k & 1) == 0) { un = -u[L.hface(i, 0)]; } else { un = u[L.hface(i, L.ny)]; }
+                    area = L.hx;
+                }
+                v = un < 0.0 ? -un * area * fin : 0.0;
+                if (!(un < 0.0)) v = -1.0;  // marker: term skipped
+            } else {
+                v = -1.0;
+            }
+            terms[t] = v;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0)
+            for (int t = 0; t < 2 * TPB && base + t < nterms; ++t)
+                if (terms[t] >= 0.0) rate += terms[t];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        sc->inj = rate;
+        if (add_pvi) {
+            const double pore = L.lx * L.ly;
+            for (int k = 0; k < cn; ++k) sc->pvi += rate * sc->dt / pore;
+        }
+    }
+}
+
+// upwind_step (transport.cpp:73-120), one thread per cell; both cells of a
+// face compute its water flux with identical IEEE operations.
+__global__ void k_upwind(Layout L, const double* __restrict__ s, double* __restrict__ s_out,
+                         const double* __restrict__ u, Scalars* sc, double inflow, double M) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c == 0) (void)frac_flow(inflow, M, &sc->clamp);  // f_in is evaluated once per call
+    if (c >= L.cells()) return;
+    const int i = c % L.nx, j = c / L.nx;
+    const double fin = frac_flow(inflow, M, nullptr);
+    const double dt = sc->dt;
+    long long* cnt = &sc->clamp;
+    // vertical faces: owner counts clamps (face i is owned by cell i, face nx by cell nx-1)
+    auto vflux = [&](int fi, bool own) {
+        const double un = u[L.vface(fi, j)];
+        double fs;
+        if (un >= 0.0) fs = (fi == 0) ? fin : frac_flow(s[L.cell(fi - 1, j)], M, own ? cnt : nullptr);
+        else fs = (fi == L.nx) ? fin : frac_flow(s[L.cell(fi, j)], M, own ? cnt : nullptr);
+        return fs * un * L.hy;
+    };
+    auto hflux = [&](int fj, bool own) {
+        const double un = u[L.hface(i, fj)];
+        double fs;
+        if (un >= 0.0) fs = (fj == 0) ? fin : frac_flow(s[L.cell(i, fj - 1)], M, own ? cnt : nullptr);
+        else fs = (fj == L.ny) ? fin : frac_flow(s[L.cell(i, fj)], M, own ? cnt : nullptr);
+        return fs * un * L.hx;
+    };
+    const double wE = vflux(i + 1, i + 1 == L.nx), wW = vflux(i, true);
+    const double wN = hflux(j + 1, j + 1 == L.ny), wS = hflux(j, true);
+    const double net = wE - wW + wN - wS;
+    const double sn = s[c] - dt / L.vol() * net;
+    if (sn < -1e-12 || sn > 1.0 + 1e-12) atomicOr(&sc->err, ERR_CFL);
+    s_out[c] = sn < 0.0 ? 0.0 : (sn > 1.0 ? 1.0 : sn);
+}
+
+// conductivity (transport.cpp:122-126) + the drift partial sums
+// (mpm.cpp:14-20 / simulation.cpp:169-172) in double-double.
+// eps_mode: -1 none, 0 relative, 1 absolute, 2 mobility (vs lam_reb)
+__global__ void k_kappa(Layout L, const double* __restrict__ K, const double* __restrict__ s,
+                        double* __restrict__ kappa, const double* __restrict__ kappa_m,
+                        const double* __restrict__ lam_reb, Scalars* sc, double M, int eps_mode, double* part,
+                        unsigned* counter) {
+    __shared__ DD shd[32];
+    const double vol = L.vol();
+    DD num{0.0, 0.0}, den{0.0, 0.0};
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < L.cells(); c += gridDim.x * blockDim.x) {
+        const double lam = total_mob(s[c], M, &sc->clamp);
+        const double k = lam * K[c];
+        kappa[c] = k;
+        if (!(k > 0.0) || !isfinite(k)) atomicOr(&sc->err, ERR_KAPPA);
+        if (eps_mode == 0 || eps_mode == 1) {
+            const double d = k - kappa_m[c];
+            num = dd_add(num, DD{d * d * vol, 0.0});
+            den = dd_add(den, DD{kappa_m[c] * kappa_m[c] * vol, 0.0});
+        } else if (eps_mode == 2) {
+            const double d = lam - lam_reb[c];
+            num = dd_add(num, DD{d * d * vol, 0.0});
+        }
+    }
+    if (eps_mode < 0) return;
+    num = block_reduce_dd(num, shd);
+    den = block_reduce_dd(den, shd);
+    if (threadIdx.x == 0) {
+        part[4 * blockIdx.x + 0] = num.hi;
+        part[4 * blockIdx.x + 1] = num.lo;
+        part[4 * blockIdx.x + 2] = den.hi;
+        part[4 * blockIdx.x + 3] = den.lo;
+    }
+    if (last_block_done(counter)) {
+        if (threadIdx.x == 0) {
+            DD n{0.0, 0.0}, d{0.0, 0.0};
+            for (unsigned b = 0; b < gridDim.x; ++b) {
+                n = dd_add(n, DD{part[4 * b], part[4 * b + 1]});
+                d = dd_add(d, DD{part[4 * b + 2], part[4 * b + 3]});
+            }
+            const double a = sqrt(n.hi);
+            double e;
+            if (eps_mode == 1) e = a;
+            else if (eps_mode == 2) e = a / M;
+            else {
+                if (!(d.hi > 0.0)) atomicOr(&sc->err, ERR_EPS_ZERO);
+                e = a / sqrt(d.hi);
+            }
+            sc->eps_pending = e;
+            sc->eps_num_hi = n.hi;
+            sc->eps_num_lo = n.lo;
+            sc->eps_den_hi = d.hi;
+            sc->eps_den_lo = d.lo;
+            *counter = 0;
+        }
+    }
+}
+
+// The MPM-2P vs MRCM decision for the NEXT step, on the device
+// (simulation.cpp:307-323): eps is exactly 0 after a rebuild.
+__global__ void k_decide(Scalars* sc, int rebuilt, int method, double eta, int step) {
+    const double eps = rebuilt ? 0.0 : sc->eps_pending;
+    sc->eps = eps;
+    int rb = 0;
+    if (method == 1) rb = 1;                                // MrcmEveryStep
+    else if (method == 2) rb = (eta <= 0.0) || (eps > eta);  // Mpm2p, strict >
+    sc->rebuild_next = rb;
+    if (method == 2 && eta > 0.0 && step >= 1) {
+        const double m = fabs(eps - eta) / eta;
+        if (m < sc->min_margin) sc->min_margin = m;
+    }
+}
+
+// max_outlet_saturation (simulation.cpp:61-83): one block, four sides.
+__global__ void k_outlet(Layout L, const double* __restrict__ s, const double* __restrict__ u, Scalars* sc) {
+    __shared__ double sh[32];
+    double m = 0.0;
+    for (int side = 0; side < 4; ++side) {
+        const int count = side < 2 ? L.ny : L.nx;
+        const double area = side < 2 ? L.hy : L.hx;
+        auto face_of = [&](int k) {
+            switch (side) {
+                case 0: return -u[L.vface(0, k)];
+                case 1: return u[L.vface(L.nx, k)];
+                case 2: return -u[L.hface(k, 0)];
+                default: return u[L.hface(k, L.ny)];
+            }
+        };
+        auto cell_of = [&](int k) {
+            switch (side) {
+                case 0: return L.cell(0, k);
+                case 1: return L.cell(L.nx - 1, k);
+                case 2: return L.cell(k, 0);
+                default: return L.cell(k, L.ny - 1);
+            }
+        };
+        double net = 0.0;
+        for (int k = threadIdx.x; k < count; k += blockDim.x) net += face_of(k) * area;
+        net = block_reduce(net, [](double a, double b) { return a + b; }, sh, 0.0);
+        __shared__ double net_s;
+        if (threadIdx.x == 0) net_s = net;
+        __syncthreads();
+        if (net_s > 1e-14) {
+            double mm = 0.0;
+            for (int k = threadIdx.x; k < count; k += blockDim.x)
+                if (face_of(k) > 1e-14) mm = fmax(mm, s[cell_of(k)]);
+            mm = block_reduce(mm, [](double a, double b) { return fmax(a, b); }, sh, 0.0);
+            m = fmax(m, mm);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) sc->outlet_max = m;
+}
+
+__global__ void k_divergence(Layout L, const double* __restrict__ u, double* __restrict__ div) {  // grid.cpp:19-31
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= L.cells()) return;
+    const int i = c % L.nx, j = c / L.nx;
+    const double fx = (u[L.vface(i + 1, j)] - u[L.vface(i, j)]) * L.hy;
+    const double fy = (u[L.hface(i, j + 1)] - u[L.hface(i, j)]) * L.hx;
+    div[c] = (fx + fy) / L.vol();
+}
+
+// epsilon(kappa_n, kappa_m, mode) on two arbitrary fields (mpm.cpp:9-25).
+__global__ void k_eps_fields(Layout L, const double* __restrict__ kn, const double* __restrict__ km, Scalars* sc,
+                             int mode, double* part, unsigned* counter) {
+    __shared__ DD shd[32];
+    const double vol = L.vol();
+    DD num{0.0, 0.0}, den{0.0, 0.0};
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < L.cells(); c += gridDim.x * blockDim.x) {
+        const double d = kn[c] - km[c];
+        num = dd_add(num, DD{d * d * vol, 0.0});
+        den = dd_add(den, DD{km[c] * km[c] * vol, 0.0});
+    }
+    num = block_reduce_dd(num, shd);
+    den = block_reduce_dd(den, shd);
+    if (threadIdx.x == 0) {
+        part[4 * blockIdx.x + 0] = num.hi;
+        part[4 * blockIdx.x + 1] = num.lo;
+        part[4 * blockIdx.x + 2] = den.hi;
+        part[4 * blockIdx.x + 3] = den.lo;
+    }
+    if (last_block_done(counter)) {
+        if (threadIdx.x == 0) {
+            DD n{0.0, 0.0}, d{0.0, 0.0};
+            for (unsigned b = 0; b < gridDim.x; ++b) {
+                n = dd_add(n, DD{part[4 * b], part[4 * b + 1]});
+                d = dd_add(d, DD{part[4 * b + 2], part[4 * b + 3]});
+            }
+            const double a = sqrt(n.hi);
+            if (mode == 1) sc->eps_pending = a;
+            else {
+                if (!(d.hi > 0.0)) atomicOr(&sc->err, ERR_EPS_ZERO);
+                sc->eps_pending = a / sqrt(d.hi);
+            }
+            *counter = 0;
+        }
+    }
+}
+
+__global__ void k_lambda(Layout L, const double* __restrict__ s, double* __restrict__ lam, Scalars* sc, double M) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;  // mobility_field (simulation.cpp:156-160)
+    if (c < L.cells()) lam[c] = total_mob(s[c], M, &sc->clamp);
+}
+
+int red_grid(const Ctx& c) { return std::min(2 * c.num_sms, std::max(1, cdiv(c.L.cells(), TPB))); }
+
+}  // namespace
+
+void launch_max_slope(Ctx& c) {
+    k_max_slope<<<1, 1, 0, c.st>>>(c.sc, c.M);
+    CK_LAUNCH();
+}
+void launch_cfl(Ctx& c, const double* u, double safety, double dt_cap) {
+    k_cfl<<<red_grid(c), TPB, 0, c.st>>>(c.L, u, c.sc, safety, dt_cap, c.red, c.red_count);
+    CK_LAUNCH();
+}
+void launch_inj_pvi(Ctx& c, const double* u, double inflow, int cn, bool add_pvi) {
+    k_inj_pvi<<<1, TPB, 0, c.st>>>(c.L, u, c.sc, inflow, c.M, cn, add_pvi ? 1 : 0);
+    CK_LAUNCH();
+}
+void launch_upwind(Ctx& c, const double* s_in, double* s_out, const double* u, double inflow) {
+    k_upwind<<<cdiv(c.L.cells(), TPB), TPB, 0, c.st>>>(c.L, s_in, s_out, u, c.sc, inflow, c.M);
+    CK_LAUNCH();
+}
+void launch_conductivity(Ctx& c, const double* s, double* kappa, int eps_mode, bool want_eps) {
+    k_kappa<<<red_grid(c), TPB, 0, c.st>>>(c.L, c.K, s, kappa, c.kappa_m, c.lam_reb, c.sc, c.M,
+                                           want_eps ? eps_mode : -1, c.red, c.red_count);
+    CK_LAUNCH();
+}
+void launch_lambda(Ctx& c, const double* s, double* lam) {
+    k_lambda<<<cdiv(c.L.cells(), TPB), TPB, 0, c.st>>>(c.L, s, lam, c.sc, c.M);
+    CK_LAUNCH();
+}
+void launch_outlet(Ctx& c, const double* s, const double* u) {
+    k_outlet<<<1, TPB, 0, c.st>>>(c.L, s, u, c.sc);
+    CK_LAUNCH();
+}
+void launch_divergence(Ctx& c, const double* u, double* div) {
+    k_divergence<<<cdiv(c.L.cells(), TPB), TPB, 0, c.st>>>(c.L, u, div);
+    CK_LAUNCH();
+}
+void launch_decide(Ctx& c, int rebuilt, int method, double eta, int step) {
+    k_decide<<<1, 1, 0, c.st>>>(c.sc, rebuilt, method, eta, step);
+    CK_LAUNCH();
+}
+void launch_epsilon_fields(Ctx& c, const double* kn, const double* km, int mode) {
+    k_eps_fields<<<red_grid(c), TPB, 0, c.st>>>(c.L, kn, km, c.sc, mode, c.red, c.red_count);
+    CK_LAUNCH();
+}
+
+}  // namespace mpm2p
