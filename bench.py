@@ -1,0 +1,395 @@
+#!/usr/bin/env python3
+"""Benchmark of the MPM-2P velocity-update + saturation-update path on B200.
+
+A "step" is one Algorithm-1 iteration of the reference driver
+(proj/src/simulation.cpp:262-329): CFL reduction, `cn` explicit upwind
+saturation substeps, conductivity + drift test, and one velocity update
+(MPM-2P reuse, or a full MRCM rebuild when the device-side drift test says
+so). The workload is BASELINE.json configs[1] (C2: 256x256 cells, 16x16
+subdomains of 16x16, exponential-covariance lognormal field) unless
+--config says otherwise; inputs are seeded synthetic fields (no dataset).
+
+  value    velocity updates/s over the timed steps, inputs resident in HBM,
+           device time from CUDA events on the library's stream (L2 flushed
+           between steps: the C2 working set is smaller than L2)
+  e2e      the same metric for a whole simulation through the C ABI with host
+           buffers (context creation + mpm2p_run incl. all H2D/D2H copies)
+  cpu_baseline / --impl reference
+           the CPU restatement of the reference (oracle/, C++ -O3, 1 thread:
+           the reference has no threads) on a bounded sample of the same run
+
+Multi-GPU (torchrun): N independent replicas, one per GPU, no data-path
+collective (the sharded path is future work); value is the
+sum over ranks divided by the max-over-ranks device time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MPM-2P velocity updates/s + FV cell-updates/s (fp64) at 1 B200; % HBM roofline"
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+        return ws, rank, local, dist, torch
+    return ws, rank, local, None, None
+
+
+def _peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get("hbm_gbs", 6650.0), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+FP64_PEAK_TFLOPS = 34.2  # measured DFMA peak on this pool (profiles/fp64_peaks_r01.log)
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{gpu_index}.csv")
+
+    def start(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.close()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    smax = float(parts[2])
+                except ValueError:
+                    continue
+                for nm, v in zip(names, parts[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def kernel_work(name, cfg, sz, dim):
+    """Algorithmic bytes / flops per launch of each kernel."""
+    cells, faces = sz.cells, sz.faces
+    n, B, ns = sz.sub_nx * sz.sub_ny, sz.sub_nx, sz.n_sub
+    table = {
+        "k_upwind": ("hbm", 32.0 * cells),                       # s r/w + 2 faces of u
+        "k_cfl": ("hbm", 16.0 * cells),
+        "k_kappa": ("hbm", 32.0 * cells),                        # s, K, kappa_m, kappa
+        "k_part_solve": ("hbm", ns * n * (16.0 * B + 24.0)),     # Lcol, Lrow, D, x r/w
+        "k_ds_solve": ("fp64", ns * (n * B * B + 4.0 * n * B)),  # banded LDL^T factor + 2 sweeps
+        "k_factor_solve": ("fp64", ns * (n * B * B + 4.0 * n * B * (1 + sz.nhat / max(ns, 1)))),
+        "k_gemv": ("hbm", 8.0 * dim * dim),
+        "k_mpm_rhs": ("hbm", 56.0 * cells),
+        "k_ds_prep": ("hbm", 72.0 * cells),
+        "k_ds_u": ("hbm", 32.0 * faces),
+        "k_divres": ("hbm", 24.0 * cells + 8.0 * faces),
+        "k_trans": ("hbm", 16.0 * cells + 8.0 * faces),
+    }
+    return table.get(name)
+
+
+def run_ours(args, ws, rank, local, dist, torch):
+    from paper_2103_11050_b200 import api, configs
+    lib = api.product_lib()
+    if ws > 1:
+        lib.set_device(local)
+    cfg = configs.build(args.config)
+    te_needed = args.warmup + args.steps + 1
+    split = cfg.split
+    if cfg.two_pass or (split.te and split.te < te_needed):
+        import dataclasses
+        split = dataclasses.replace(split, te=max(te_needed, split.te or 0), stop_on_breakthrough=False)
+    sim = api.Simulator(cfg.problem, lib)
+    sz = sim.sizes
+    dim = sim.dim
+    cn = split.cn
+    sim.run_begin(split, cfg.s0(), cfg.inflow_sat)
+    for _ in range(args.warmup):
+        if sim.run_step() is None:
+            break
+    sampler = ClockSampler(local)
+    if ws > 1:
+        dist.barrier()
+        torch.cuda.synchronize()
+    sampler.start()
+    dev_ms = 0.0
+    done = 0
+    rebuilds = 0
+    launches0 = _launches(sim)
+    t_wall0 = time.perf_counter()
+    for _ in range(args.steps):
+        lib.flush_l2(sim.h)
+        lib.timer_record(sim.h, 0)
+        rec = sim.run_step()
+        lib.timer_record(sim.h, 1)
+        if rec is None:
+            break
+        import ctypes
+        ms = ctypes.c_double()
+        lib.timer_elapsed(sim.h, 0, 1, ctypes.byref(ms))
+        dev_ms += ms.value
+        done += 1
+        rebuilds += rec["rebuilt"]
+    wall = time.perf_counter() - t_wall0
+    launches = _launches(sim) - launches0
+    clocks = sampler.stop()
+    if ws > 1:
+        t = torch.tensor([dev_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_ms_max = float(t.item())
+        n = torch.tensor([done], device="cuda", dtype=torch.float64)
+        dist.all_reduce(n, op=dist.ReduceOp.SUM)
+        done_total = float(n.item())
+    else:
+        dev_ms_max, done_total = dev_ms, float(done)
+    # per-kernel device times over a separate profiled window (same stream, CUDA events)
+    prof = _profile(sim, lib, min(args.profile_steps, max(0, split.te - 1 - args.warmup - done)))
+    sim.run_end()
+    sim.close()
+    # end-to-end: a whole simulation through the C ABI with host buffers
+    e2e = None
+    if not args.skip_e2e:
+        e2e = _e2e(api, lib, cfg, split if cfg.two_pass else cfg.split, args)
+    return dict(cfg=cfg, split=split, sz=sz, dim=dim, cn=cn, done=done, done_total=done_total,
+                dev_ms=dev_ms, dev_ms_max=dev_ms_max, wall=wall, rebuilds=rebuilds, clocks=clocks,
+                launches=launches, prof=prof, e2e=e2e)
+
+
+def _launches(sim):
+    import ctypes
+    buf = ctypes.create_string_buffer(1 << 16)
+    sim.lib.profile_report(sim.h, buf, len(buf))
+    for line in buf.value.decode().splitlines():
+        p = line.split()
+        if p and p[0] == "__launches__":
+            return int(p[1])
+    return 0
+
+
+def _profile(sim, lib, steps):
+    import ctypes
+    if steps <= 0:
+        return {}
+    lib.profile_enable(sim.h, 1)
+    n = 0
+    for _ in range(steps):
+        if sim.run_step() is None:
+            break
+        n += 1
+    buf = ctypes.create_string_buffer(1 << 16)
+    lib.profile_report(sim.h, buf, len(buf))
+    lib.profile_enable(sim.h, 0)
+    out = {}
+    for line in buf.value.decode().splitlines():
+        p = line.split()
+        if len(p) == 3 and p[0] != "__launches__":
+            out[p[0]] = {"launches": int(p[1]), "total_ms": float(p[2])}
+    out["__steps__"] = n
+    return out
+
+
+def _e2e(api, lib, cfg, split, args):
+    t0 = time.perf_counter()
+    sim = api.Simulator(cfg.problem, lib)
+    res = sim.run(split, cfg.s0(), cfg.inflow_sat)
+    sim.close()
+    wall = time.perf_counter() - t0
+    steps = res.record.te - 1
+    cells = cfg.cells
+    faces = (cfg.problem.nx + 1) * cfg.problem.ny + cfg.problem.nx * (cfg.problem.ny + 1)
+    nb = 2 * (cfg.problem.nx + cfg.problem.ny)
+    h2d = 8 * cells * 2 + 12 * nb  # K + s0 + boundary spec
+    d2h = 8 * (2 * cells + faces) + 256 * (steps + 1)  # final s, p, u + per-step scalars
+    return {"value": steps / wall, "unit": "velocity_updates/s", "h2d_bytes_per_step": h2d / max(steps, 1),
+            "d2h_bytes_per_step": d2h / max(steps, 1), "wall_s_per_simulation": wall, "steps": steps,
+            "rebuilds": res.record.tm_total}
+
+
+def cpu_reference(cfg, split, budget_s):
+    """The reference's CPU path (oracle restatement, C++ -O3, 1 thread) on a
+    bounded sample: as many steps of the same run as fit in budget_s."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_bind import oracle_lib
+    from paper_2103_11050_b200 import api
+    lib = oracle_lib()
+    sim = api.Simulator(cfg.problem, lib)
+    t0 = time.perf_counter()
+    sim.run_begin(split, cfg.s0(), cfg.inflow_sat)
+    t_begin = time.perf_counter() - t0
+    n = 0
+    t1 = time.perf_counter()
+    while time.perf_counter() - t1 < budget_s:
+        if sim.run_step() is None:
+            break
+        n += 1
+    el = time.perf_counter() - t1
+    rec = sim.run_end()
+    sim.close()
+    return {"value": n / el if el > 0 else 0.0, "unit": "velocity_updates/s", "cores": 1, "kind": "port",
+            "sample": f"{cfg.name}: initial rebuild ({t_begin:.2f} s) then the first {n} Algorithm-1 steps "
+                      f"({el:.1f} s, {rec.tm_total - 1} rebuilds) of the same run; oracle/ C++ -O3 single thread "
+                      f"(the reference is single-threaded and cannot be built here: no Eigen)",
+            "steps": n, "seconds": el}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--profile-steps", type=int, default=50)
+    ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--skip-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    ws, rank, local, dist, torch = _dist()
+    from paper_2103_11050_b200 import configs
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        cfg = configs.build(args.config)
+        import dataclasses
+        split = dataclasses.replace(cfg.split, stop_on_breakthrough=False,
+                                    te=max(cfg.split.te or 0, args.warmup + args.steps + 1))
+        cb = cpu_reference(cfg, split, args.cpu_budget)
+        line = {"metric": METRIC, "value": cb["value"], "unit": "velocity_updates/s", "impl": "reference",
+                "n_gpus": ws, "steps": cb["steps"], "warmup": 0, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded field generator)",
+                "config": {"workload": cfg.name, "description": cfg.description},
+                "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": cb["value"], "unit": "velocity_updates/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    r = run_ours(args, ws, rank, local, dist, torch)
+    if rank != 0:
+        if dist is not None:
+            dist.barrier()
+        return
+    cfg, sz, dim = r["cfg"], r["sz"], r["dim"]
+    secs = r["dev_ms_max"] / 1e3
+    value = r["done_total"] / secs
+    cells = sz.cells
+    cell_updates = r["done_total"] * r["cn"] * cells / secs
+    hbm_peak, peak_src = _peaks()
+    # roofline of the dominant kernel (largest share of profiled device time)
+    prof = r["prof"]
+    kern = {k: v for k, v in prof.items() if not k.startswith("__")}
+    roof = None
+    shares = {}
+    tot = sum(v["total_ms"] for v in kern.values()) or 1.0
+    for k, v in sorted(kern.items(), key=lambda kv: -kv[1]["total_ms"]):
+        shares[k] = {"share": round(v["total_ms"] / tot, 4), "launches": v["launches"],
+                     "avg_us": round(1e3 * v["total_ms"] / v["launches"], 3)}
+        w = kernel_work(k, cfg, sz, dim)
+        if w:
+            avg_s = v["total_ms"] / v["launches"] / 1e3
+            if w[0] == "hbm":
+                ach = w[1] / avg_s / 1e9
+                shares[k]["achieved"] = f"{ach:.1f} GB/s ({ach / hbm_peak:.3f} of HBM)"
+            else:
+                ach = w[1] / avg_s / 1e12
+                shares[k]["achieved"] = f"{ach:.3f} TFLOP/s ({ach / FP64_PEAK_TFLOPS:.3f} of fp64 DFMA)"
+    for k in sorted(kern, key=lambda k: -kern[k]["total_ms"]):
+        w = kernel_work(k, cfg, sz, dim)
+        if not w:
+            continue
+        v = kern[k]
+        avg_s = v["total_ms"] / v["launches"] / 1e3
+        if w[0] == "hbm":
+            ach = w[1] / avg_s / 1e9
+            roof = {"kernel": k, "bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": ach / hbm_peak, "traffic": None, "peak_source": peak_src,
+                    "algorithmic_per_launch": w[1], "avg_launch_us": avg_s * 1e6}
+        else:
+            ach = w[1] / avg_s / 1e12
+            roof = {"kernel": k, "bound": "fp64", "achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                    "frac": ach / FP64_PEAK_TFLOPS, "traffic": None,
+                    "peak_source": "measured DFMA peak (profiles/fp64_peaks_r01.log)",
+                    "algorithmic_per_launch": w[1], "avg_launch_us": avg_s * 1e6}
+        break
+    cpu = None
+    if not args.skip_cpu and ws == 1:
+        import dataclasses
+        cpu_split = dataclasses.replace(r["split"], stop_on_breakthrough=False)
+        cb = cpu_reference(cfg, cpu_split, args.cpu_budget)
+        cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    line = {
+        "metric": METRIC, "value": value, "unit": "velocity_updates/s", "n_gpus": ws, "steps": r["done"],
+        "warmup": args.warmup, "ms_per_step": r["dev_ms_max"] / max(r["done"], 1), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded field generator)",
+        "config": {"workload": cfg.name, "description": cfg.description, "cells": cells,
+                   "subdomains": sz.n_sub, "interface_dim": dim, "cn": r["cn"],
+                   "l2": "flushed between timed steps (working set < L2)",
+                   "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU"},
+        "cell_updates_per_s": cell_updates,
+        "rebuilds_in_timed_steps": r["rebuilds"],
+        "host_wall_ms_per_step": 1e3 * r["wall"] / max(r["done"], 1),
+        "gpu_launches": r["launches"],
+        "roofline": roof,
+        "kernels": shares,
+        "clocks": r["clocks"],
+        "e2e": r["e2e"],
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+
+
+if __name__ == "__main__":
+    main()

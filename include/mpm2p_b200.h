@@ -213,6 +213,20 @@ int mpm2p_run_end(mpm2p_ctx* ctx, mpm2p_run_record* rec);
 /* ---- cost model (simulation.cpp:11-28) --------------------------------- */
 double mpm2p_rcr(int64_t nhat, int64_t n, int64_t te, int64_t tm);
 
+/* ---- instrumentation (no reference counterpart; used by bench.py) ------ */
+/* Selects the CUDA device for contexts created afterwards on this thread. */
+int mpm2p_set_device(int32_t device);
+/* Records CUDA event `slot` (0..15) on the context's stream. */
+int mpm2p_timer_record(mpm2p_ctx* ctx, int32_t slot);
+/* Device time between two recorded events (waits for `b`). */
+int mpm2p_timer_elapsed(mpm2p_ctx* ctx, int32_t a, int32_t b, double* ms);
+/* Writes a buffer larger than L2 (126 MB) on the context's stream. */
+int mpm2p_flush_l2(mpm2p_ctx* ctx);
+/* Per-kernel CUDA-event timing of every launch on the context's stream. */
+int mpm2p_profile_enable(mpm2p_ctx* ctx, int32_t enable);
+/* "name count total_ms" lines for every profiled kernel; resets the totals. */
+int mpm2p_profile_report(mpm2p_ctx* ctx, char* buf, int32_t buflen);
+
 #ifdef __cplusplus
 }
 #endif

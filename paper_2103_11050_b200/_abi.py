@@ -100,6 +100,16 @@ PROTOTYPES = {
     "rcr": (C.c_double, [C.c_int64, C.c_int64, C.c_int64, C.c_int64]),
 }
 
+# Instrumentation entry points (product library only).
+INSTR_PROTOTYPES = {
+    "set_device": (C.c_int, [C.c_int32]),
+    "timer_record": (C.c_int, [_vp, C.c_int32]),
+    "timer_elapsed": (C.c_int, [_vp, C.c_int32, C.c_int32, _dp]),
+    "flush_l2": (C.c_int, [_vp]),
+    "profile_enable": (C.c_int, [_vp, C.c_int32]),
+    "profile_report": (C.c_int, [_vp, C.c_char_p, C.c_int32]),
+}
+
 # Status codes (errors.hpp:9-24 mapped by the header).
 OK, ECONFIG, ENUMERIC, ECAPACITY, ECUDA = 0, 2, 3, 4, 5
 
@@ -118,6 +128,12 @@ class Lib:
             fn.restype = res
             fn.argtypes = args
             setattr(self, name, fn)
+        for name, (res, args) in INSTR_PROTOTYPES.items():
+            fn = getattr(self.dll, prefix + name, None)
+            if fn is not None:
+                fn.restype = res
+                fn.argtypes = args
+                setattr(self, name, fn)
 
     def symbols(self):
         return [self.prefix + n for n in PROTOTYPES]

@@ -80,6 +80,7 @@ void download(Ctx& c, double* dst, const double* src, size_t n) {
 const Scalars& sync_scalars(Ctx& c) {
     CK(cudaMemcpyAsync(c.sc_host, c.sc.p, sizeof(Scalars), cudaMemcpyDeviceToHost, c.st));
     CK(cudaStreamSynchronize(c.st));
+    if (c.profiling) c.resolve_profile();
     const unsigned e = c.sc_host->err;
     if (e) {
         CK(cudaMemsetAsync(&c.sc.p->err, 0, sizeof(unsigned), c.st));
@@ -484,6 +485,13 @@ void mpm2p_destroy(mpm2p_ctx* ctx) {
     if (!ctx) return;
     if (ctx->c.st) cudaStreamSynchronize(ctx->c.st);
     if (ctx->c.sc_host) cudaFreeHost(ctx->c.sc_host);
+    for (auto& p : ctx->c.pending) {
+        cudaEventDestroy(p.a);
+        cudaEventDestroy(p.b);
+    }
+    for (cudaEvent_t e : ctx->c.event_pool) cudaEventDestroy(e);
+    for (cudaEvent_t e : ctx->c.timers)
+        if (e) cudaEventDestroy(e);
     cudaStream_t st = ctx->c.st;
     delete ctx;
     if (st) cudaStreamDestroy(st);
@@ -709,6 +717,67 @@ int mpm2p_run_read(mpm2p_ctx* ctx, double* s, double* p, double* u) {
 
 int mpm2p_run_end(mpm2p_ctx* ctx, mpm2p_run_record* rec) {
     return guarded(ctx, [&] { run_end(ctx, rec); });
+}
+
+int mpm2p_timer_record(mpm2p_ctx* ctx, int32_t slot) {
+    return guarded(ctx, [&] {
+        if (slot < 0 || slot >= 16) throw ConfigError("timer slot out of range");
+        Ctx& c = ctx->c;
+        if (!c.timers[slot]) CK(cudaEventCreate(&c.timers[slot]));
+        CK(cudaEventRecord(c.timers[slot], c.st));
+    });
+}
+
+int mpm2p_timer_elapsed(mpm2p_ctx* ctx, int32_t a, int32_t b, double* ms) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        if (a < 0 || a >= 16 || b < 0 || b >= 16 || !c.timers[a] || !c.timers[b])
+            throw ConfigError("timer slot not recorded");
+        CK(cudaEventSynchronize(c.timers[b]));
+        float f = 0.f;
+        CK(cudaEventElapsedTime(&f, c.timers[a], c.timers[b]));
+        *ms = f;
+    });
+}
+
+int mpm2p_set_device(int32_t device) {
+    return guarded(nullptr, [&] { CK(cudaSetDevice(device)); });
+}
+
+int mpm2p_flush_l2(mpm2p_ctx* ctx) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        const size_t bytes = (size_t)256 << 20;
+        if (c.flush_buf.n < bytes) c.flush_buf.alloc(bytes);
+        CK(cudaMemsetAsync(c.flush_buf.p, c.flush_buf.n & 0xff, bytes, c.st));
+    });
+}
+
+int mpm2p_profile_enable(mpm2p_ctx* ctx, int32_t enable) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        CK(cudaStreamSynchronize(c.st));
+        c.resolve_profile();
+        c.profiling = enable != 0;
+    });
+}
+
+int mpm2p_profile_report(mpm2p_ctx* ctx, char* buf, int32_t buflen) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        CK(cudaStreamSynchronize(c.st));
+        c.resolve_profile();
+        std::string out = "__launches__ " + std::to_string(c.launch_count) + " 0\n";
+        for (size_t i = 0; i < c.prof_names.size(); ++i)
+            out += c.prof_names[i] + " " + std::to_string(c.prof_count[i]) + " " + std::to_string(c.prof_ms[i]) + "\n";
+        c.prof_names.clear();
+        c.prof_ms.clear();
+        c.prof_count.clear();
+        if (buf && buflen > 0) {
+            std::strncpy(buf, out.c_str(), (size_t)buflen - 1);
+            buf[buflen - 1] = '\0';
+        }
+    });
 }
 
 double mpm2p_rcr(int64_t nhat, int64_t n, int64_t te, int64_t tm) {  // simulation.cpp:11-19

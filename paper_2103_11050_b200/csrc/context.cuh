@@ -104,7 +104,71 @@ struct Ctx {
     // counters (exact integers, SolveCounters mrcm.hpp:15-21)
     long long c_hom = 0, c_part = 0, c_down = 0, c_fine = 0, c_iface = 0;
     long long nhat = 0;
+
+    // instrumentation: per-kernel CUDA-event timing on this stream, user timers
+    bool profiling = false;
+    long long launch_count = 0;  // kernels launched on this context (all launches go through PROF)
+    struct Pending { const char* name; cudaEvent_t a, b; };
+    std::vector<Pending> pending;
+    std::vector<cudaEvent_t> event_pool;
+    std::vector<std::string> prof_names;
+    std::vector<double> prof_ms;
+    std::vector<long long> prof_count;
+    cudaEvent_t timers[16] = {};
+    DevBuf<unsigned char> flush_buf;
+
+    cudaEvent_t take_event() {
+        if (event_pool.empty()) {
+            cudaEvent_t e;
+            CK(cudaEventCreate(&e));
+            return e;
+        }
+        cudaEvent_t e = event_pool.back();
+        event_pool.pop_back();
+        return e;
+    }
+    // Folds finished kernel timings into the per-name totals (stream must be idle).
+    void resolve_profile() {
+        for (auto& p : pending) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, p.a, p.b));
+            size_t i = 0;
+            while (i < prof_names.size() && prof_names[i] != p.name) ++i;
+            if (i == prof_names.size()) {
+                prof_names.emplace_back(p.name);
+                prof_ms.push_back(0.0);
+                prof_count.push_back(0);
+            }
+            prof_ms[i] += ms;
+            prof_count[i] += 1;
+            event_pool.push_back(p.a);
+            event_pool.push_back(p.b);
+        }
+        pending.clear();
+    }
 };
+
+// RAII scope recording CUDA events around one kernel launch when profiling.
+struct ProfScope {
+    Ctx& c;
+    const char* name;
+    cudaEvent_t a = nullptr;
+    ProfScope(Ctx& cc, const char* n) : c(cc), name(n) {
+        ++c.launch_count;
+        if (c.profiling) {
+            a = c.take_event();
+            CK(cudaEventRecord(a, c.st));
+        }
+    }
+    ~ProfScope() {
+        if (a) {
+            cudaEvent_t b = c.take_event();
+            cudaEventRecord(b, c.st);
+            c.pending.push_back({name, a, b});
+        }
+    }
+};
+#define PROF(c, name) ::mpm2p::ProfScope prof_scope_##__LINE__((c), (name))
 
 // ---- launchers (transport.cu) ----------------------------------------------
 void launch_max_slope(Ctx& c);

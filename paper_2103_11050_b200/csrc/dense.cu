@@ -158,8 +158,11 @@ double dense_inverse(Ctx& c, const double* A, double* Ainv, int n) {
     c.gj_row.alloc(std::max(c.gj_row.n, (size_t)2 * n));
     c.gj_krow.alloc(std::max(c.gj_krow.n, (size_t)2 * n));
     c.gj_piv.alloc(std::max(c.gj_piv.n, (size_t)2));
-    k_augment<<<std::min(cdiv(2LL * n * n, TPB), 8 * c.num_sms), TPB, 0, c.st>>>(A, c.gj_work, n);
-    CK_LAUNCH();
+    {
+        PROF(c, "k_augment");
+        k_augment<<<std::min(cdiv(2LL * n * n, TPB), 8 * c.num_sms), TPB, 0, c.st>>>(A, c.gj_work, n);
+        CK_LAUNCH();
+    }
     CK(cudaMemsetAsync(c.gj_piv.p + 1, 0, sizeof(int), c.st));
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gauss_jordan, TPB, 0));
@@ -172,14 +175,23 @@ double dense_inverse(Ctx& c, const double* A, double* Ainv, int n) {
     double* krow = c.gj_krow.p;
     int* sing = c.gj_piv.p + 1;
     void* args[] = {&W, &n, &piv, &colb, &rowb, &krow, &sing};
-    CK(cudaLaunchCooperativeKernel((void*)k_gauss_jordan, blocks, TPB, args, 0, c.st));
-    CK_LAUNCH();
-    k_extract<<<std::min(cdiv((long long)n * n, TPB), 8 * c.num_sms), TPB, 0, c.st>>>(c.gj_work, Ainv, n);
-    CK_LAUNCH();
+    {
+        PROF(c, "k_gauss_jordan");
+        CK(cudaLaunchCooperativeKernel((void*)k_gauss_jordan, blocks, TPB, args, 0, c.st));
+        CK_LAUNCH();
+    }
+    {
+        PROF(c, "k_extract");
+        k_extract<<<std::min(cdiv((long long)n * n, TPB), 8 * c.num_sms), TPB, 0, c.st>>>(c.gj_work, Ainv, n);
+        CK_LAUNCH();
+    }
     DevBuf<double> norms;
     norms.alloc(2);
-    k_norm1<<<1, 1024, 0, c.st>>>(A, Ainv, n, norms);
-    CK_LAUNCH();
+    {
+        PROF(c, "k_norm1");
+        k_norm1<<<1, 1024, 0, c.st>>>(A, Ainv, n, norms);
+        CK_LAUNCH();
+    }
     double h[2];
     int singular = 0;
     CK(cudaMemcpyAsync(h, norms.p, sizeof(h), cudaMemcpyDeviceToHost, c.st));
@@ -190,19 +202,28 @@ double dense_inverse(Ctx& c, const double* A, double* Ainv, int n) {
 }
 
 void launch_gemv(Ctx& c, const double* A, const double* x, double* y, int n) {
-    k_gemv<<<cdiv((long long)n * 32, TPB), TPB, 0, c.st>>>(A, x, y, n);
-    CK_LAUNCH();
+    {
+        PROF(c, "k_gemv");
+        k_gemv<<<cdiv((long long)n * 32, TPB), TPB, 0, c.st>>>(A, x, y, n);
+        CK_LAUNCH();
+    }
 }
 
 void launch_csr_residual(Ctx& c, const int* ptr, const int* col, const double* val, const double* x, const double* b,
                          double* r, int n) {
-    k_csr_residual<<<cdiv(n, TPB), TPB, 0, c.st>>>(ptr, col, val, x, b, r, n);
-    CK_LAUNCH();
+    {
+        PROF(c, "k_csr_residual");
+        k_csr_residual<<<cdiv(n, TPB), TPB, 0, c.st>>>(ptr, col, val, x, b, r, n);
+        CK_LAUNCH();
+    }
 }
 
 void launch_axpy(Ctx& c, double* y, const double* x, int n) {
-    k_axpy<<<cdiv(n, TPB), TPB, 0, c.st>>>(y, x, n);
-    CK_LAUNCH();
+    {
+        PROF(c, "k_axpy");
+        k_axpy<<<cdiv(n, TPB), TPB, 0, c.st>>>(y, x, n);
+        CK_LAUNCH();
+    }
 }
 
 }  // namespace mpm2p

@@ -904,34 +904,49 @@ int band_blocks(const Layout& L) { return cdiv(L.n_sub, WPB); }
 }  // namespace
 
 void launch_trans(Ctx& c, const double* kappa) {
-    k_trans<<<std::min(grid_for(c.L.faces()), 8 * c.num_sms), TPB, 0, c.st>>>(c.L, kappa, c.T);
-    CK_LAUNCH();
+    {
+        PROF(c, "k_trans");
+        k_trans<<<std::min(grid_for(c.L.faces()), 8 * c.num_sms), TPB, 0, c.st>>>(c.L, kappa, c.T);
+        CK_LAUNCH();
+    }
 }
 
 void launch_beta(Ctx& c, const double* kappa) {
     const Layout& L = c.L;
     const int E = L.skeleton_edges();
     if (E == 0) return;
-    k_face_kappa<<<grid_for(E), TPB, 0, c.st>>>(L, kappa, c.face_kappa);
-    CK_LAUNCH();
+    {
+        PROF(c, "k_face_kappa");
+        k_face_kappa<<<grid_for(E), TPB, 0, c.st>>>(L, kappa, c.face_kappa);
+        CK_LAUNCH();
+    }
     if (c.alpha_mode == 1) {
         size_t bytes = c.sort_tmp_bytes;
         CK(cub::DeviceRadixSort::SortKeys(c.sort_tmp.p, bytes, c.face_kappa.p, c.sort_keys.p, E, 0, 64, c.st));
     }
-    k_beta<<<grid_for(E), TPB, 0, c.st>>>(L, kappa, c.face_kappa, c.sort_keys, c.alpha_mode, c.alpha, c.alpha_min,
-                                          c.alpha_max, c.pct_lo, c.pct_hi, c.beta_m, c.beta_p, c.alpha_e, c.sc);
-    CK_LAUNCH();
+    {
+        PROF(c, "k_beta");
+        k_beta<<<grid_for(E), TPB, 0, c.st>>>(L, kappa, c.face_kappa, c.sort_keys, c.alpha_mode, c.alpha, c.alpha_min,
+                                              c.alpha_max, c.pct_lo, c.pct_hi, c.beta_m, c.beta_p, c.alpha_e, c.sc);
+        CK_LAUNCH();
+    }
 }
 
 void launch_setup_static(Ctx& c) {
     const Layout& L = c.L;
-    k_static<<<grid_for(L.n_sub), TPB, 0, c.st>>>(L, c.q, c.bc_kind, c.qsum_sub, c.ground);
-    CK_LAUNCH();
+    {
+        PROF(c, "k_static");
+        k_static<<<grid_for(L.n_sub), TPB, 0, c.st>>>(L, c.q, c.bc_kind, c.qsum_sub, c.ground);
+        CK_LAUNCH();
+    }
     if (c.repair_active) {
         DevBuf<double> A;
         A.alloc((size_t)L.n_sub * L.n_sub);
-        k_repair_matrix<<<grid_for(L.n_sub), TPB, 0, c.st>>>(L, c.grounded ? 1 : 0, c.ground, A);
-        CK_LAUNCH();
+        {
+            PROF(c, "k_repair_matrix");
+            k_repair_matrix<<<grid_for(L.n_sub), TPB, 0, c.st>>>(L, c.grounded ? 1 : 0, c.ground, A);
+            CK_LAUNCH();
+        }
         const double rc = dense_inverse(c, A, c.Linv, L.n_sub);
         if (!(rc > 0.0)) throw NumericError("downscale: compatibility-repair operator is singular");
     }
@@ -944,29 +959,53 @@ namespace {
 void downscale(Ctx& c, const double* kappa) {
     const Layout& L = c.L;
     if (L.skeleton_edges() > 0) {
-        k_skel<<<grid_for(L.skeleton_edges()), TPB, 0, c.st>>>(L, c.RU, c.skel);
+        {
+            PROF(c, "k_skel");
+            k_skel<<<grid_for(L.skeleton_edges()), TPB, 0, c.st>>>(L, c.RU, c.skel);
+            CK_LAUNCH();
+        }
+    }
+    {
+        PROF(c, "k_resid");
+        k_resid<<<grid_for(L.n_sub), TPB, 0, c.st>>>(L, c.skel, c.RU, c.qsum_sub, c.resid, c.sc, c.red, c.red_count);
         CK_LAUNCH();
     }
-    k_resid<<<grid_for(L.n_sub), TPB, 0, c.st>>>(L, c.skel, c.RU, c.qsum_sub, c.resid, c.sc, c.red, c.red_count);
-    CK_LAUNCH();
     if (c.repair_active) {
-        k_repair_delta<<<cdiv((long long)L.n_sub * 32, TPB), TPB, 0, c.st>>>(L.n_sub, c.Linv, c.resid, c.delta);
+        {
+            PROF(c, "k_repair_delta");
+            k_repair_delta<<<cdiv((long long)L.n_sub * 32, TPB), TPB, 0, c.st>>>(L.n_sub, c.Linv, c.resid, c.delta);
+            CK_LAUNCH();
+        }
+    }
+    {
+        PROF(c, "k_repair_corr");
+        k_repair_corr<<<std::min(grid_for(std::max(L.n_iface, L.n_sub)), 2 * c.num_sms), TPB, 0, c.st>>>(
+            L, c.repair_active ? 1 : 0, c.grounded ? 1 : 0, c.delta, c.ground, c.corr, c.sc, c.red, c.red_count);
         CK_LAUNCH();
     }
-    k_repair_corr<<<std::min(grid_for(std::max(L.n_iface, L.n_sub)), 2 * c.num_sms), TPB, 0, c.st>>>(
-        L, c.repair_active ? 1 : 0, c.grounded ? 1 : 0, c.delta, c.ground, c.corr, c.sc, c.red, c.red_count);
-    CK_LAUNCH();
-    k_ds_prep<<<grid_for(L.cells()), TPB, 0, c.st>>>(L, kappa, c.T, c.q, c.bc_kind, c.skel, c.corr, c.RU, c.delta,
-                                                     c.grounded ? 1 : 0, c.BDd, c.BWd, c.BSd, c.Xd, c.GZ, c.sc);
-    CK_LAUNCH();
+    {
+        PROF(c, "k_ds_prep");
+        k_ds_prep<<<grid_for(L.cells()), TPB, 0, c.st>>>(L, kappa, c.T, c.q, c.bc_kind, c.skel, c.corr, c.RU, c.delta,
+                                                         c.grounded ? 1 : 0, c.BDd, c.BWd, c.BSd, c.Xd, c.GZ, c.sc);
+        CK_LAUNCH();
+    }
     const size_t sm1 = (size_t)WPB * band_smem_doubles(L.snx, 1) * sizeof(double);
-    k_ds_solve<<<band_blocks(L), WPB * 32, sm1, c.st>>>(L, c.BDd, c.BWd, c.BSd, c.Dd, c.Lrd, c.Xd, c.RS, c.p, c.sc);
-    CK_LAUNCH();
-    k_ds_u<<<grid_for(L.faces()), TPB, 0, c.st>>>(L, c.T, c.Xd, c.GZ, c.u);
-    CK_LAUNCH();
-    k_divres<<<std::min(grid_for(std::max(L.cells(), L.faces())), 2 * c.num_sms), TPB, 0, c.st>>>(L, c.u, c.q, c.sc,
-                                                                                               c.red, c.red_count);
-    CK_LAUNCH();
+    {
+        PROF(c, "k_ds_solve");
+        k_ds_solve<<<band_blocks(L), WPB * 32, sm1, c.st>>>(L, c.BDd, c.BWd, c.BSd, c.Dd, c.Lrd, c.Xd, c.RS, c.p, c.sc);
+        CK_LAUNCH();
+    }
+    {
+        PROF(c, "k_ds_u");
+        k_ds_u<<<grid_for(L.faces()), TPB, 0, c.st>>>(L, c.T, c.Xd, c.GZ, c.u);
+        CK_LAUNCH();
+    }
+    {
+        PROF(c, "k_divres");
+        k_divres<<<std::min(grid_for(std::max(L.cells(), L.faces())), 2 * c.num_sms), TPB, 0, c.st>>>(L, c.u, c.q, c.sc,
+                                                                                                   c.red, c.red_count);
+        CK_LAUNCH();
+    }
     c.c_down += L.n_sub;
 }
 
@@ -974,8 +1013,11 @@ void interface_solve(Ctx& c) {
     const Layout& L = c.L;
     c.c_iface += 1;
     if (c.dim == 0) return;
-    k_iface_rhs<<<grid_for(c.dim), TPB, 0, c.st>>>(L, c.PU, c.beta_m, c.beta_p, c.irhs);
-    CK_LAUNCH();
+    {
+        PROF(c, "k_iface_rhs");
+        k_iface_rhs<<<grid_for(c.dim), TPB, 0, c.st>>>(L, c.PU, c.beta_m, c.beta_p, c.irhs);
+        CK_LAUNCH();
+    }
     launch_gemv(c, c.Minv, c.irhs, c.icoef, c.dim);
     // one step of iterative refinement against the sparse operator
     launch_csr_residual(c, c.csr_ptr, c.csr_col, c.csr_val, c.icoef, c.irhs, c.ires, c.dim);
@@ -995,30 +1037,51 @@ void launch_rebuild(Ctx& c, const double* kappa, bool compute_beta) {  // comput
     const Layout& L = c.L;
     if (compute_beta) launch_beta(c, kappa);
     launch_trans(c, kappa);
-    k_band_entries<<<grid_for(L.cells()), TPB, 0, c.st>>>(L, kappa, c.T, 0, c.anchor_m ? 1 : 0, c.beta_m, c.beta_p,
-                                                          c.bc_kind, c.BDm, c.BWm, c.BSm, c.sc);
-    CK_LAUNCH();
-    k_rebuild_rhs<<<grid_for(L.cells()), TPB, 0, c.st>>>(L, c.max_rhs, kappa, c.q, c.bc_kind, c.bc_value, c.beta_m,
-                                                         c.beta_p, c.anchor_m ? 1 : 0, c.X);
-    CK_LAUNCH();
+    {
+        PROF(c, "k_band_entries");
+        k_band_entries<<<grid_for(L.cells()), TPB, 0, c.st>>>(L, kappa, c.T, 0, c.anchor_m ? 1 : 0, c.beta_m, c.beta_p,
+                                                              c.bc_kind, c.BDm, c.BWm, c.BSm, c.sc);
+        CK_LAUNCH();
+    }
+    {
+        PROF(c, "k_rebuild_rhs");
+        k_rebuild_rhs<<<grid_for(L.cells()), TPB, 0, c.st>>>(L, c.max_rhs, kappa, c.q, c.bc_kind, c.bc_value, c.beta_m,
+                                                             c.beta_p, c.anchor_m ? 1 : 0, c.X);
+        CK_LAUNCH();
+    }
     const size_t smr = (size_t)WPB * band_smem_doubles(L.snx, RING_NR) * sizeof(double);
-    k_factor_solve<<<band_blocks(L), WPB * 32, smr, c.st>>>(L, c.max_rhs, c.BDm, c.BWm, c.BSm, c.Dm, c.Lcm, c.Lrm, c.X,
-                                                            c.sc);
-    CK_LAUNCH();
-    k_rebuild_traces<<<grid_for((long long)L.n_sub * L.nbe), TPB, 0, c.st>>>(
-        L, c.max_rhs, kappa, c.bc_kind, c.bc_value, c.beta_m, c.beta_p, c.X, c.PU, c.PB, c.HU, c.HB);
-    CK_LAUNCH();
-    k_psums<<<cdiv((long long)L.n_sub * c.max_rhs * 32, TPB), TPB, 0, c.st>>>(L, c.max_rhs, c.X, c.PS, c.HP);
-    CK_LAUNCH();
+    {
+        PROF(c, "k_factor_solve");
+        k_factor_solve<<<band_blocks(L), WPB * 32, smr, c.st>>>(L, c.max_rhs, c.BDm, c.BWm, c.BSm, c.Dm, c.Lcm, c.Lrm, c.X,
+                                                                c.sc);
+        CK_LAUNCH();
+    }
+    {
+        PROF(c, "k_rebuild_traces");
+        k_rebuild_traces<<<grid_for((long long)L.n_sub * L.nbe), TPB, 0, c.st>>>(
+            L, c.max_rhs, kappa, c.bc_kind, c.bc_value, c.beta_m, c.beta_p, c.X, c.PU, c.PB, c.HU, c.HB);
+        CK_LAUNCH();
+    }
+    {
+        PROF(c, "k_psums");
+        k_psums<<<cdiv((long long)L.n_sub * c.max_rhs * 32, TPB), TPB, 0, c.st>>>(L, c.max_rhs, c.X, c.PS, c.HP);
+        CK_LAUNCH();
+    }
     c.c_hom += c.nhat;
     c.c_part += L.n_sub;
     // interface matrix: assemble, invert, guard (mrcm.cpp:196-238)
     if (c.dim > 0) {
-        k_assemble<<<grid_for(c.dim), TPB, 0, c.st>>>(L, c.csr_ptr, c.csr_col, c.dim, c.HU, c.beta_m, c.beta_p,
-                                                      c.csr_val);
-        CK_LAUNCH();
-        k_csr_to_dense<<<c.dim, TPB, 0, c.st>>>(c.csr_ptr, c.csr_col, c.csr_val, c.dim, c.Mdense);
-        CK_LAUNCH();
+        {
+            PROF(c, "k_assemble");
+            k_assemble<<<grid_for(c.dim), TPB, 0, c.st>>>(L, c.csr_ptr, c.csr_col, c.dim, c.HU, c.beta_m, c.beta_p,
+                                                          c.csr_val);
+            CK_LAUNCH();
+        }
+        {
+            PROF(c, "k_csr_to_dense");
+            k_csr_to_dense<<<c.dim, TPB, 0, c.st>>>(c.csr_ptr, c.csr_col, c.csr_val, c.dim, c.Mdense);
+            CK_LAUNCH();
+        }
         c.rcond = dense_inverse(c, c.Mdense, c.Minv, c.dim);
         if (!(c.rcond > 1e-14))
             throw NumericError("compute_basis_set: interface matrix is numerically singular (rcond=" +
@@ -1027,13 +1090,22 @@ void launch_rebuild(Ctx& c, const double* kappa, bool compute_beta) {  // comput
     interface_solve(c);
     // recon_m (kept for MPM steps) and its traces
     if (c.dim == 0) CK(cudaMemsetAsync(c.icoef, 0, sizeof(double), c.st));
-    k_recon_traces<<<grid_for((long long)L.n_sub * L.nbe), TPB, 0, c.st>>>(L, c.icoef, c.PU, c.PB, c.HU, c.HB, nullptr,
-                                                                           c.RU, c.bpm);
-    CK_LAUNCH();
-    k_recon_p<<<grid_for(L.cells()), TPB, 0, c.st>>>(L, c.max_rhs, c.icoef, c.X, c.pm);
-    CK_LAUNCH();
-    k_sub_sum<<<cdiv((long long)L.n_sub * 32, TPB), TPB, 0, c.st>>>(L, c.pm, c.pmsum);
-    CK_LAUNCH();
+    {
+        PROF(c, "k_recon_traces");
+        k_recon_traces<<<grid_for((long long)L.n_sub * L.nbe), TPB, 0, c.st>>>(L, c.icoef, c.PU, c.PB, c.HU, c.HB, nullptr,
+                                                                               c.RU, c.bpm);
+        CK_LAUNCH();
+    }
+    {
+        PROF(c, "k_recon_p");
+        k_recon_p<<<grid_for(L.cells()), TPB, 0, c.st>>>(L, c.max_rhs, c.icoef, c.X, c.pm);
+        CK_LAUNCH();
+    }
+    {
+        PROF(c, "k_sub_sum");
+        k_sub_sum<<<cdiv((long long)L.n_sub * 32, TPB), TPB, 0, c.st>>>(L, c.pm, c.pmsum);
+        CK_LAUNCH();
+    }
     CK(cudaMemcpyAsync(c.RS, c.pmsum, L.n_sub * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
     CK(cudaMemcpyAsync(c.kappa_m, kappa, L.cells() * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
     downscale(c, kappa);
@@ -1044,26 +1116,44 @@ void launch_mpm(Ctx& c, const double* kn) {  // mpm_pressure_update (mpm.cpp:31-
     const Layout& L = c.L;
     if (!c.has_basis) throw ConfigError("mpm_pressure_update: no basis set (rebuild first)");
     launch_trans(c, kn);
-    k_mpm_rhs<<<grid_for(L.cells()), TPB, 0, c.st>>>(L, c.max_rhs, c.anchor_m ? 1 : 0, kn, c.kappa_m, c.T, c.q,
-                                                     c.bc_kind, c.bc_value, c.beta_m, c.beta_p, c.pm, c.bpm, c.X,
-                                                     c.GZ, c.WU);
-    CK_LAUNCH();
+    {
+        PROF(c, "k_mpm_rhs");
+        k_mpm_rhs<<<grid_for(L.cells()), TPB, 0, c.st>>>(L, c.max_rhs, c.anchor_m ? 1 : 0, kn, c.kappa_m, c.T, c.q,
+                                                         c.bc_kind, c.bc_value, c.beta_m, c.beta_p, c.pm, c.bpm, c.X,
+                                                         c.GZ, c.WU);
+        CK_LAUNCH();
+    }
     const size_t sm1 = (size_t)WPB * band_smem_doubles(L.snx, 1) * sizeof(double);
-    k_part_solve<<<band_blocks(L), WPB * 32, sm1, c.st>>>(L, c.max_rhs, c.Dm, c.Lcm, c.Lrm, c.X);
-    CK_LAUNCH();
-    k_part_traces<<<grid_for((long long)L.n_sub * L.nbe), TPB, 0, c.st>>>(L, c.max_rhs, c.kappa_m, c.bc_kind, c.beta_m,
-                                                                          c.beta_p, c.GZ, c.X, c.PU);
-    CK_LAUNCH();
-    k_part_psum<<<cdiv((long long)L.n_sub * 32, TPB), TPB, 0, c.st>>>(L, c.max_rhs, c.X, c.PS);
-    CK_LAUNCH();
+    {
+        PROF(c, "k_part_solve");
+        k_part_solve<<<band_blocks(L), WPB * 32, sm1, c.st>>>(L, c.max_rhs, c.Dm, c.Lcm, c.Lrm, c.X);
+        CK_LAUNCH();
+    }
+    {
+        PROF(c, "k_part_traces");
+        k_part_traces<<<grid_for((long long)L.n_sub * L.nbe), TPB, 0, c.st>>>(L, c.max_rhs, c.kappa_m, c.bc_kind, c.beta_m,
+                                                                              c.beta_p, c.GZ, c.X, c.PU);
+        CK_LAUNCH();
+    }
+    {
+        PROF(c, "k_part_psum");
+        k_part_psum<<<cdiv((long long)L.n_sub * 32, TPB), TPB, 0, c.st>>>(L, c.max_rhs, c.X, c.PS);
+        CK_LAUNCH();
+    }
     c.c_part += L.n_sub;
     interface_solve(c);
     if (c.dim == 0) CK(cudaMemsetAsync(c.icoef, 0, sizeof(double), c.st));
-    k_recon_traces<<<grid_for((long long)L.n_sub * L.nbe), TPB, 0, c.st>>>(L, c.icoef, c.PU, nullptr, c.HU, nullptr,
-                                                                           c.WU, c.RU, nullptr);
-    CK_LAUNCH();
-    k_recon_psum<<<grid_for(L.n_sub), TPB, 0, c.st>>>(L, c.icoef, c.PS, c.HP, c.pmsum, c.RS);
-    CK_LAUNCH();
+    {
+        PROF(c, "k_recon_traces");
+        k_recon_traces<<<grid_for((long long)L.n_sub * L.nbe), TPB, 0, c.st>>>(L, c.icoef, c.PU, nullptr, c.HU, nullptr,
+                                                                               c.WU, c.RU, nullptr);
+        CK_LAUNCH();
+    }
+    {
+        PROF(c, "k_recon_psum");
+        k_recon_psum<<<grid_for(L.n_sub), TPB, 0, c.st>>>(L, c.icoef, c.PS, c.HP, c.pmsum, c.RS);
+        CK_LAUNCH();
+    }
     downscale(c, kn);
 }
 

@@ -377,45 +377,75 @@ int red_grid(const Ctx& c) { return std::min(2 * c.num_sms, std::max(1, cdiv(c.L
 }  // namespace
 
 void launch_max_slope(Ctx& c) {
-    k_max_slope<<<1, 1, 0, c.st>>>(c.sc, c.M);
-    CK_LAUNCH();
+    {
+        PROF(c, "k_max_slope");
+        k_max_slope<<<1, 1, 0, c.st>>>(c.sc, c.M);
+        CK_LAUNCH();
+    }
 }
 void launch_cfl(Ctx& c, const double* u, double safety, double dt_cap) {
-    k_cfl<<<red_grid(c), TPB, 0, c.st>>>(c.L, u, c.sc, safety, dt_cap, c.red, c.red_count);
-    CK_LAUNCH();
+    {
+        PROF(c, "k_cfl");
+        k_cfl<<<red_grid(c), TPB, 0, c.st>>>(c.L, u, c.sc, safety, dt_cap, c.red, c.red_count);
+        CK_LAUNCH();
+    }
 }
 void launch_inj_pvi(Ctx& c, const double* u, double inflow, int cn, bool add_pvi) {
-    k_inj_pvi<<<1, TPB, 0, c.st>>>(c.L, u, c.sc, inflow, c.M, cn, add_pvi ? 1 : 0);
-    CK_LAUNCH();
+    {
+        PROF(c, "k_inj_pvi");
+        k_inj_pvi<<<1, TPB, 0, c.st>>>(c.L, u, c.sc, inflow, c.M, cn, add_pvi ? 1 : 0);
+        CK_LAUNCH();
+    }
 }
 void launch_upwind(Ctx& c, const double* s_in, double* s_out, const double* u, double inflow) {
-    k_upwind<<<cdiv(c.L.cells(), TPB), TPB, 0, c.st>>>(c.L, s_in, s_out, u, c.sc, inflow, c.M);
-    CK_LAUNCH();
+    {
+        PROF(c, "k_upwind");
+        k_upwind<<<cdiv(c.L.cells(), TPB), TPB, 0, c.st>>>(c.L, s_in, s_out, u, c.sc, inflow, c.M);
+        CK_LAUNCH();
+    }
 }
 void launch_conductivity(Ctx& c, const double* s, double* kappa, int eps_mode, bool want_eps) {
-    k_kappa<<<red_grid(c), TPB, 0, c.st>>>(c.L, c.K, s, kappa, c.kappa_m, c.lam_reb, c.sc, c.M,
-                                           want_eps ? eps_mode : -1, c.red, c.red_count);
-    CK_LAUNCH();
+    {
+        PROF(c, "k_kappa");
+        k_kappa<<<red_grid(c), TPB, 0, c.st>>>(c.L, c.K, s, kappa, c.kappa_m, c.lam_reb, c.sc, c.M,
+                                               want_eps ? eps_mode : -1, c.red, c.red_count);
+        CK_LAUNCH();
+    }
 }
 void launch_lambda(Ctx& c, const double* s, double* lam) {
-    k_lambda<<<cdiv(c.L.cells(), TPB), TPB, 0, c.st>>>(c.L, s, lam, c.sc, c.M);
-    CK_LAUNCH();
+    {
+        PROF(c, "k_lambda");
+        k_lambda<<<cdiv(c.L.cells(), TPB), TPB, 0, c.st>>>(c.L, s, lam, c.sc, c.M);
+        CK_LAUNCH();
+    }
 }
 void launch_outlet(Ctx& c, const double* s, const double* u) {
-    k_outlet<<<1, TPB, 0, c.st>>>(c.L, s, u, c.sc);
-    CK_LAUNCH();
+    {
+        PROF(c, "k_outlet");
+        k_outlet<<<1, TPB, 0, c.st>>>(c.L, s, u, c.sc);
+        CK_LAUNCH();
+    }
 }
 void launch_divergence(Ctx& c, const double* u, double* div) {
-    k_divergence<<<cdiv(c.L.cells(), TPB), TPB, 0, c.st>>>(c.L, u, div);
-    CK_LAUNCH();
+    {
+        PROF(c, "k_divergence");
+        k_divergence<<<cdiv(c.L.cells(), TPB), TPB, 0, c.st>>>(c.L, u, div);
+        CK_LAUNCH();
+    }
 }
 void launch_decide(Ctx& c, int rebuilt, int method, double eta, int step) {
-    k_decide<<<1, 1, 0, c.st>>>(c.sc, rebuilt, method, eta, step);
-    CK_LAUNCH();
+    {
+        PROF(c, "k_decide");
+        k_decide<<<1, 1, 0, c.st>>>(c.sc, rebuilt, method, eta, step);
+        CK_LAUNCH();
+    }
 }
 void launch_epsilon_fields(Ctx& c, const double* kn, const double* km, int mode) {
-    k_eps_fields<<<red_grid(c), TPB, 0, c.st>>>(c.L, kn, km, c.sc, mode, c.red, c.red_count);
-    CK_LAUNCH();
+    {
+        PROF(c, "k_eps_fields");
+        k_eps_fields<<<red_grid(c), TPB, 0, c.st>>>(c.L, kn, km, c.sc, mode, c.red, c.red_count);
+        CK_LAUNCH();
+    }
 }
 
 }  // namespace mpm2p
