@@ -183,12 +183,7 @@ def run_ours(args, ws, rank, local, dist, torch):
     launches = _launches(sim) - launches0
     clocks = sampler.stop()
     if ws > 1:
-        t = torch.tensor([dev_ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dev_ms_max = float(t.item())
-        n = torch.tensor([done], device="cuda", dtype=torch.float64)
-        dist.all_reduce(n, op=dist.ReduceOp.SUM)
-        done_total = float(n.item())
+        dev_ms_max, done_total = reduce_over_ranks(dev_ms, done, dist, "cuda")
     else:
         dev_ms_max, done_total = dev_ms, float(done)
     # per-kernel device times over a separate profiled window (same stream, CUDA events)
@@ -202,6 +197,16 @@ def run_ours(args, ws, rank, local, dist, torch):
     return dict(cfg=cfg, split=split, sz=sz, dim=dim, cn=cn, done=done, done_total=done_total,
                 dev_ms=dev_ms, dev_ms_max=dev_ms_max, wall=wall, rebuilds=rebuilds, clocks=clocks,
                 launches=launches, prof=prof, e2e=e2e)
+
+
+def reduce_over_ranks(dev_ms, done, dist, device):
+    """Max over ranks of the device time, sum over ranks of the work done."""
+    import torch
+    t = torch.tensor([float(dev_ms)], device=device, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    n = torch.tensor([float(done)], device=device, dtype=torch.float64)
+    dist.all_reduce(n, op=dist.ReduceOp.SUM)
+    return float(t.item()), float(n.item())
 
 
 def _launches(sim):

@@ -214,6 +214,13 @@ int mpm2p_run_end(mpm2p_ctx* ctx, mpm2p_run_record* rec);
 double mpm2p_rcr(int64_t nhat, int64_t n, int64_t te, int64_t tm);
 
 /* ---- instrumentation (no reference counterpart; used by bench.py) ------ */
+/* Host-only dump of the decomposition tables the kernels compute in closed
+ * form (decomposition.cpp:101-129, mrcm.cpp:157-189): per boundary edge of
+ * subdomain s, 8 ints {side, local_cell, local_face, global_face, interface,
+ * pos, global BC index, sign}; hom_cols gets the n_hom interface-system
+ * columns of s's homogeneous solves in order. Needs no GPU. */
+int mpm2p_layout_tables(const mpm2p_problem* prob, int32_t s, int32_t* edges, int32_t* hom_cols,
+                        int32_t* n_hom);
 /* Selects the CUDA device for contexts created afterwards on this thread. */
 int mpm2p_set_device(int32_t device);
 /* Records CUDA event `slot` (0..15) on the context's stream. */

@@ -420,4 +420,44 @@ int oracle_weak_residuals(oracle_ctx* ctx, double* flux_jump, double* pressure_j
 
 int64_t oracle_clamp_count(void) { return clamp_count(); }
 
+/* Decomposition tables built the reference's way (decomposition.cpp:35-132,
+ * mrcm.cpp:157-189), same layout as mpm2p_layout_tables. */
+int oracle_layout_tables(const mpm2p_problem* p, int32_t s, int32_t* edges, int32_t* hom_cols, int32_t* n_hom) {
+    return guarded(nullptr, [&] {
+        const Grid g = build_grid(p->nx, p->ny, p->lx, p->ly);
+        const Decomp dd = build_decomposition(g, p->nsx, p->nsy);
+        const Space sp = build_interface_space(dd, p->space_kind, HbarSpec{p->hbar_mode, p->hbar_edges});
+        if (s < 0 || s >= dd.n_sub()) throw ConfigError("layout_tables: subdomain out of range");
+        auto gbc = [&](int f) {  // mrcm.cpp:14-28
+            if (g.is_vface(f)) {
+                const int i = f % (g.nx + 1), j = f / (g.nx + 1);
+                return i == 0 ? j : (i == g.nx ? g.ny + j : -1);
+            }
+            const int fh = f - g.vcount(), i = fh % g.nx, j = fh / g.nx;
+            return j == 0 ? 2 * g.ny + i : (j == g.ny ? 2 * g.ny + g.nx + i : -1);
+        };
+        const auto& E = dd.sub_boundary[s];
+        for (size_t idx = 0; idx < E.size(); ++idx) {
+            const BoundaryEdge& e = E[idx];
+            int32_t* o = edges + 8 * idx;
+            o[0] = e.side;
+            o[1] = e.local_cell;
+            o[2] = e.local_face;
+            o[3] = e.global_face;
+            o[4] = e.iface;
+            o[5] = e.pos;
+            o[6] = e.on_skeleton ? -1 : gbc(e.global_face);
+            o[7] = e.sign > 0 ? 1 : -1;
+        }
+        std::vector<int> inc;
+        for (const auto& e : E)
+            if (e.on_skeleton && std::find(inc.begin(), inc.end(), e.iface) == inc.end()) inc.push_back(e.iface);
+        std::sort(inc.begin(), inc.end());
+        int h = 0;
+        for (int k : inc) for (int b : sp.flux_by_iface[k]) hom_cols[h++] = b;
+        for (int k : inc) for (int b : sp.pres_by_iface[k]) hom_cols[h++] = sp.dim_flux() + b;
+        *n_hom = h;
+    });
+}
+
 }  // extern "C"

@@ -135,17 +135,16 @@ void build_csr(Ctx& c) {
     CK(cudaStreamSynchronize(c.st));
 }
 
-void create_ctx(mpm2p_ctx* ctx, const mpm2p_problem* P) {
-    Ctx& c = ctx->c;
-    // build_grid / build_decomposition validation (grid.cpp:9-15, decomposition.cpp:35-41)
+// Grid, decomposition and interface-space sizes with the reference's
+// validation (grid.cpp:9-15, decomposition.cpp:35-41, interface_space.cpp:9-52).
+Layout make_layout(const mpm2p_problem* P) {
+    Layout L{};
     if (P->nx < 1 || P->ny < 1)
         throw ConfigError("build_grid: cell counts must be >= 1, got " + std::to_string(P->nx) + "x" + std::to_string(P->ny));
     if (!(P->lx > 0.0) || !(P->ly > 0.0)) throw ConfigError("build_grid: domain lengths must be positive");
     if (P->nsx < 1 || P->nsy < 1) throw ConfigError("build_decomposition: subdomain counts must be >= 1");
     if (P->nx % P->nsx != 0 || P->ny % P->nsy != 0)
         throw ConfigError("build_decomposition: subdomains do not divide the grid");
-    if (!P->K || !P->bc_kind || !P->bc_value) throw ConfigError("problem: K and the boundary spec are required");
-    Layout& L = c.L;
     L.nx = P->nx;
     L.ny = P->ny;
     L.lx = P->lx;
@@ -192,11 +191,17 @@ void create_ctx(mpm2p_ctx* ctx, const mpm2p_problem* P) {
     }
     L.dim_flux = L.NV * L.nbv + L.NH * L.nbh;
     L.max_hom = 0;
+    for (int s = 0; s < L.n_sub; ++s) L.max_hom = std::max(L.max_hom, L.n_hom(s));
+    return L;
+}
+
+void create_ctx(mpm2p_ctx* ctx, const mpm2p_problem* P) {
+    Ctx& c = ctx->c;
+    if (!P->K || !P->bc_kind || !P->bc_value) throw ConfigError("problem: K and the boundary spec are required");
+    c.L = make_layout(P);
+    const Layout& L = c.L;
     c.nhat = 0;
-    for (int s = 0; s < L.n_sub; ++s) {
-        L.max_hom = std::max(L.max_hom, L.n_hom(s));
-        c.nhat += L.n_hom(s);
-    }
+    for (int s = 0; s < L.n_sub; ++s) c.nhat += L.n_hom(s);
     c.max_rhs = 1 + L.max_hom;
     c.dim = 2 * L.dim_flux;
     c.M = P->viscosity_ratio;
@@ -737,6 +742,37 @@ int mpm2p_timer_elapsed(mpm2p_ctx* ctx, int32_t a, int32_t b, double* ms) {
         float f = 0.f;
         CK(cudaEventElapsedTime(&f, c.timers[a], c.timers[b]));
         *ms = f;
+    });
+}
+
+// Host-only introspection of the closed-form decomposition (no GPU needed):
+// per boundary edge of subdomain s, 8 ints: side, local_cell, local_face,
+// global_face, interface (-1 physical), pos, global BC index, sign (+1/-1);
+// then per homogeneous solve of s its interface-system column.
+int mpm2p_layout_tables(const mpm2p_problem* prob, int32_t s, int32_t* edges, int32_t* hom_cols, int32_t* n_hom) {
+    return guarded(nullptr, [&] {
+        const Layout L = make_layout(prob);
+        if (s < 0 || s >= L.n_sub) throw ConfigError("layout_tables: subdomain out of range");
+        for (int idx = 0; idx < L.nbe; ++idx) {
+            const EdgeInfo e = L.edge(s, idx);
+            int32_t* o = edges + 8 * idx;
+            o[0] = e.side;
+            o[1] = e.local_cell;
+            o[2] = e.local_face;
+            o[3] = e.global_face;
+            o[4] = e.iface;
+            o[5] = e.pos;
+            o[6] = e.gbc;
+            o[7] = e.sign > 0 ? 1 : -1;
+        }
+        const int nh = L.n_hom(s);
+        *n_hom = nh;
+        for (int h = 0; h < nh; ++h) {
+            int k, t, col;
+            bool fl;
+            L.hom(s, h, k, t, fl, col);
+            hom_cols[h] = col;
+        }
     });
 }
 

@@ -1,0 +1,239 @@
+"""CUDA path vs the CPU oracle through the C ABI (needs a B200).
+
+Bar (BASELINE.json north_star): decisions and indexing bit-exact; p and u
+relative L2 <= 1e-8; saturation max-abs <= 1e-8 after the full run.
+Transport and beta are checked bitwise (the kernels keep the reference's
+operation order under --fmad=false).
+"""
+import numpy as np
+import pytest
+
+from cases import problem, random_kappa, rel_l2
+from paper_2103_11050_b200 import api, configs
+
+pytestmark = pytest.mark.gpu
+
+TOL_PU = 1e-8   # relative L2 for pressure and velocity
+TOL_S = 1e-8    # max-abs for saturation
+
+
+def pair(prob, oracle):
+    return api.Simulator(prob), api.Simulator(prob, oracle)
+
+
+def test_gpu_library_is_the_cuda_path():
+    lib = api.product_lib()
+    assert lib.path.endswith("libmpm2p_b200.so")
+
+
+def test_transport_bitwise(oracle):
+    nx, ny = 48, 40
+    K = random_kappa(nx, ny, 1, 0.1, 10.0)
+    g, o = pair(problem(nx, ny, 4, 4, K, M=7.0), oracle)
+    u = o.mrcm_solve(K).u
+    rng = np.random.default_rng(3)
+    s = rng.uniform(0, 1, nx * ny)
+    assert np.array_equal(g.conductivity(s), o.conductivity(s))
+    assert g.max_fractional_flow_slope() == o.max_fractional_flow_slope()
+    for safety in (0.5, 0.9):
+        assert g.cfl_timestep(u, safety, 1.0) == o.cfl_timestep(u, safety, 1.0)
+    assert g.cfl_timestep(np.zeros_like(u), 0.9, 1.0) == 1.0
+    dt = o.cfl_timestep(u, 0.9, 1.0)
+    for inflow in (1.0, 0.3):
+        assert np.array_equal(g.upwind_step(s, inflow, u, dt), o.upwind_step(s, inflow, u, dt))
+        assert g.injection_rate(u, inflow) == o.injection_rate(u, inflow)
+    assert g.max_outlet_saturation(s, u) == o.max_outlet_saturation(s, u)
+    assert np.array_equal(g.divergence(u), o.divergence(u))
+    kn = K * np.exp(0.1 * rng.standard_normal(K.size))
+    for mode in (api.EPS_RELATIVE, api.EPS_ABSOLUTE):
+        e_g, e_o = g.epsilon(kn, K, mode), o.epsilon(kn, K, mode)
+        assert abs(e_g - e_o) <= 1e-14 * e_o
+
+
+def test_cfl_violation_raises(oracle):
+    nx = ny = 16
+    g, o = pair(problem(nx, ny, 1, 1, np.ones(nx * ny), M=1.0), oracle)
+    u = np.zeros(g.faces)
+    u[:(nx + 1) * ny] = 1.0
+    for sim in (g, o):
+        with pytest.raises(api.NumericError):
+            sim.upwind_step(np.zeros(nx * ny), 1.0, u, 1.0)
+
+
+@pytest.mark.parametrize("alpha_mode", [api.ALPHA_UNIFORM, api.ALPHA_ADAPTIVE])
+def test_beta_bitwise(oracle, alpha_mode):
+    nx, ny = 16, 12
+    K = np.where(np.arange(ny)[:, None] < 2, 1e4, np.where(np.arange(ny)[:, None] >= ny - 2, 1e-4, 1.0))
+    K = (K * np.ones((ny, nx))).ravel()
+    K *= np.exp(0.01 * np.random.default_rng(0).standard_normal(K.size))
+    g, o = pair(problem(nx, ny, 4, 3, K, alpha=api.AlphaSpec(mode=alpha_mode)), oracle)
+    for a, b in zip(g.compute_beta(K), o.compute_beta(K)):
+        assert np.array_equal(a, b)
+
+
+MRCM_CASES = [
+    # nx, ny, nsx, nsy, space, hbar, bc, lx, kappa range, q
+    (32, 32, 4, 4, api.SPACE_CONSTANT, api.HBAR_WHOLE, "pd", 1.0, (0.3, 3.0), False),
+    (32, 32, 4, 4, api.SPACE_CONSTANT, api.HBAR_HALF, "pd", 1.0, (0.1, 10.0), False),
+    (16, 16, 2, 2, api.SPACE_CONSTANT, api.HBAR_PER_EDGE, "pd", 1.0, (0.1, 10.0), False),
+    (32, 32, 4, 4, api.SPACE_LINEAR, api.HBAR_WHOLE, "pd", 1.0, (1e-2, 1e2), False),
+    (12, 6, 3, 2, api.SPACE_LINEAR, api.HBAR_WHOLE, "ui", 2.0, (1e-2, 1e2), True),
+    (40, 20, 2, 2, api.SPACE_CONSTANT, api.HBAR_WHOLE, "ui", 2.0, (0.3, 3.0), True),
+    (16, 8, 4, 1, api.SPACE_CONSTANT, api.HBAR_WHOLE, "pd", 1.0, (0.3, 3.0), False),
+    (12, 10, 1, 1, api.SPACE_CONSTANT, api.HBAR_WHOLE, "pd", 1.0, (1e-2, 1e2), True),
+    (64, 64, 2, 2, api.SPACE_CONSTANT, api.HBAR_WHOLE, "pd", 1.0, (0.1, 10.0), False),
+    (60, 40, 3, 2, api.SPACE_CONSTANT, api.HBAR_WHOLE, "pd", 1.5, (1e-3, 1e3), False),
+]
+
+
+@pytest.mark.parametrize("case", MRCM_CASES)
+def test_mrcm_and_mpm_parity(oracle, case):
+    nx, ny, nsx, nsy, space, hbar, bcn, lx, (lo, hi), with_q = case
+    K = random_kappa(nx, ny, 11, lo, hi)
+    q = np.random.default_rng(9).uniform(-1, 1, nx * ny) if with_q else None
+    if with_q and bcn == "pd":
+        q = q - q.mean()
+    bc = api.pressure_drop(nx, ny) if bcn == "pd" else api.unit_inflow(nx, ny)
+    adaptive = api.AlphaSpec(mode=api.ALPHA_ADAPTIVE if space == api.SPACE_LINEAR else api.ALPHA_UNIFORM)
+    prob = problem(nx, ny, nsx, nsy, K, bc=bc, lx=lx, q=q, space=space, hbar=hbar, alpha=adaptive)
+    g, o = pair(prob, oracle)
+    sg, so = g.mrcm_solve(K), o.mrcm_solve(K)
+    assert sg.counters == so.counters
+    if g.dim:
+        assert rel_l2(g.interface_matrix(), o.interface_matrix()) < 1e-12
+        assert rel_l2(sg.coeffs, so.coeffs) < 1e-9
+    assert rel_l2(sg.p, so.p) < TOL_PU and rel_l2(sg.u, so.u) < TOL_PU
+    assert sg.info.repair_warning == so.info.repair_warning
+    assert sg.info.div_residual <= 1e-10 * sg.info.div_scale
+    rng = np.random.default_rng(5)
+    for amp in (0.0, 0.02, 0.2):
+        kn = K * np.exp(amp * rng.standard_normal(K.size))
+        mg, mo = g.mpm_pressure_update(kn), o.mpm_pressure_update(kn)
+        assert mg.counters == mo.counters
+        assert rel_l2(mg.p, mo.p) < TOL_PU and rel_l2(mg.u, mo.u) < TOL_PU
+        assert mg.info.div_residual <= 1e-10 * mg.info.div_scale
+
+
+def test_mrcm_with_given_beta(oracle):
+    nx = ny = 32
+    K = random_kappa(nx, ny, 2)
+    g, o = pair(problem(nx, ny, 4, 4, K), oracle)
+    bm, bp, _ = o.compute_beta(K)
+    sg, so = g.mrcm_solve(K, (2 * bm, 3 * bp)), o.mrcm_solve(K, (2 * bm, 3 * bp))
+    assert rel_l2(sg.p, so.p) < TOL_PU and rel_l2(sg.u, so.u) < TOL_PU
+
+
+def test_interface_matrix_reused_byte_identically(oracle):
+    """test_mpm.cpp:177-197: an MPM step leaves the cached interface matrix untouched."""
+    nx = ny = 32
+    K = random_kappa(nx, ny, 3)
+    g = api.Simulator(problem(nx, ny, 4, 4, K))
+    g.mrcm_solve(K)
+    M0 = g.interface_matrix().copy()
+    g.mpm_pressure_update(K * 1.004)
+    assert np.array_equal(M0, g.interface_matrix())
+
+
+def _compare_runs(rg, ro):
+    seq_g = [s["rebuilt"] for s in rg.record.steps]
+    seq_o = [s["rebuilt"] for s in ro.record.steps]
+    assert seq_g == seq_o
+    assert rg.record.te == ro.record.te and rg.record.tm_total == ro.record.tm_total
+    c_g, c_o = rg.record.counters, ro.record.counters
+    assert (c_g.homogeneous, c_g.particular, c_g.downscale, c_g.interface_solves) == \
+           (c_o.homogeneous, c_o.particular, c_o.downscale, c_o.interface_solves)
+    assert rg.record.breakthrough_step == ro.record.breakthrough_step
+    assert np.max(np.abs(rg.s_final - ro.s_final)) <= TOL_S
+    assert rel_l2(rg.p_final, ro.p_final) <= TOL_PU
+    assert rel_l2(rg.u_final, ro.u_final) <= TOL_PU
+    dts_g = np.array([s["dt"] for s in rg.record.steps])
+    dts_o = np.array([s["dt"] for s in ro.record.steps])
+    np.testing.assert_allclose(dts_g, dts_o, rtol=1e-8)
+
+
+@pytest.mark.parametrize("meth,mode,eta", [(api.MPM2P, api.EPS_RELATIVE, 0.01), (api.MPM2P, api.EPS_MOBILITY, 0.01),
+                                           (api.MRCM_EVERY_STEP, api.EPS_RELATIVE, 0.01),
+                                           (api.MPM2P_NO_UPDATES, api.EPS_RELATIVE, 0.01),
+                                           (api.MPM2P, api.EPS_ABSOLUTE, 0.05), (api.MPM2P, api.EPS_RELATIVE, 0.0)])
+def test_run_parity_small(oracle, meth, mode, eta):
+    nx = ny = 64
+    K = random_kappa(nx, ny, 7, 0.1, 10.0)
+    g, o = pair(problem(nx, ny, 4, 4, K, M=5.0), oracle)
+    sp = api.SplittingConfig(method=meth, eta=eta, eta_mode=mode, te=80, cfl_safety=0.5)
+    _compare_runs(g.run(sp), o.run(sp))
+
+
+def test_config_c1_full_run(oracle):
+    """C1 (BASELINE configs[0]) end to end: 200 saturation steps."""
+    c = configs.build("C1")
+    g, o = pair(c.problem, oracle)
+    rg, ro = g.run(c.split, c.s0()), o.run(c.split, c.s0())
+    _compare_runs(rg, ro)
+    assert rg.record.max_div_ratio <= 1e-10
+
+
+def test_config_c3_two_pass(oracle):
+    """C3: run to breakthrough, then to breakthrough + 50% (bounded here by max_steps_hard)."""
+    import dataclasses
+    c = configs.build("C3")
+    sp = dataclasses.replace(c.split, max_steps_hard=400)
+    g, o = pair(c.problem, oracle)
+    r1g, r1o = g.run(sp, c.s0()), o.run(sp, c.s0())
+    _compare_runs(r1g, r1o)
+    if r1g.record.breakthrough_step >= 0:
+        te = configs.breakthrough_plus_50(r1g.record.breakthrough_step)
+        sp2 = dataclasses.replace(sp, stop_on_breakthrough=False, te=min(te, 400))
+        _compare_runs(g.run(sp2, c.s0()), o.run(sp2, c.s0()))
+
+
+@pytest.mark.parametrize("name,steps", [("C2", 120), ("C4", 40)])
+def test_config_samples(oracle, name, steps):
+    """Bounded samples of C2 / C4 (full runs are benched, not oracle-checked)."""
+    c = configs.build(name, te_override=steps + 1)
+    g, o = pair(c.problem, oracle)
+    _compare_runs(g.run(c.split, c.s0()), o.run(c.split, c.s0()))
+
+
+def test_determinism_and_eta0_equivalence():
+    """test_simulation.cpp:95-120: bitwise-identical reruns; eta = 0 == rebuild every step."""
+    c = configs.build("C1", te_override=40)
+    g = api.Simulator(c.problem)
+    a, b = g.run(c.split, c.s0()), g.run(c.split, c.s0())
+    assert np.array_equal(a.s_final, b.s_final) and np.array_equal(a.u_final, b.u_final)
+    assert [s["epsilon"] for s in a.record.steps] == [s["epsilon"] for s in b.record.steps]
+    import dataclasses
+    e0 = g.run(dataclasses.replace(c.split, eta=0.0), c.s0())
+    ev = g.run(dataclasses.replace(c.split, method=api.MRCM_EVERY_STEP), c.s0())
+    assert np.array_equal(e0.s_final, ev.s_final)
+    assert [s["rebuilt"] for s in e0.record.steps] == [1] * len(e0.record.steps)
+
+
+def test_full_size_properties_c2():
+    """At C2's full size: conservative velocities, saturation in [0,1], and a
+    zero-perturbation MPM update reproduces the MRCM solution."""
+    c = configs.build("C2", te_override=60)
+    g = api.Simulator(c.problem)
+    r = g.run(c.split, c.s0())
+    assert r.record.max_div_ratio <= 1e-10
+    assert r.s_final.min() >= 0.0 and r.s_final.max() <= 1.0
+    K = c.problem.K
+    sol = g.mrcm_solve(K)
+    m = g.mpm_pressure_update(K)
+    assert rel_l2(m.u, sol.u) < 1e-10 and rel_l2(m.p, sol.p) < 1e-10
+
+
+def test_config_errors():
+    nx = ny = 16
+    with pytest.raises(api.ConfigError):
+        api.Simulator(problem(nx, ny, 3, 3, np.ones(nx * ny)))
+    g = api.Simulator(problem(nx, ny, 2, 2, np.ones(nx * ny)))
+    with pytest.raises(api.ConfigError):
+        g.run(api.SplittingConfig(te=0))
+    with pytest.raises(api.ConfigError):
+        g.run(api.SplittingConfig(te=3, method=api.FINE_REFERENCE))
+    with pytest.raises(api.ConfigError):
+        g.mpm_pressure_update(np.ones(nx * ny))
+    bad = np.ones(nx * ny)
+    bad[3] = -1.0
+    with pytest.raises(api.NumericError):
+        g.mrcm_solve(bad)
