@@ -154,7 +154,24 @@ Vec transmissibility(const Grid& g, const Vec& k) {  // elliptic.cpp:44-61
     return t;
 }
 
-void BandLDLT::factor(const Vec& band) {
+// Elimination order of every banded solve: 0 natural, 1 reversed. Reversing
+// is an equally exact direct method with different rounding; tests use it to
+// measure the solver-roundoff floor the reference's own answer carries.
+static int g_elim_order = 0;
+void set_elimination_order(int order) { g_elim_order = order; }
+
+void BandLDLT::factor(const Vec& band_in) {
+    rev = g_elim_order == 1;
+    Vec rb;
+    if (rev) {  // A'[r'][c'] = A[n-1-r'][n-1-c'] = A[n-1-c'][n-1-r'] (symmetric)
+        rb.assign(band_in.size(), 0.0);
+        for (int r2 = 0; r2 < n; ++r2)
+            for (int c2 = std::max(0, r2 - w); c2 <= r2; ++c2) {
+                const int R = n - 1 - c2, Cc = n - 1 - r2;
+                rb[(size_t)r2 * (w + 1) + (c2 - r2 + w)] = band_in[(size_t)R * (w + 1) + (Cc - R + w)];
+            }
+    }
+    const Vec& band = rev ? rb : band_in;
     // Left-looking banded LDL^T: L[r][c] = (A[r][c] - sum_m L[r][m] D[m] L[c][m]) / D[c].
     L.assign((size_t)n * std::max(w, 1), 0.0);
     D.assign(n, 0.0);
@@ -175,6 +192,12 @@ void BandLDLT::factor(const Vec& band) {
 }
 
 void BandLDLT::solve(Vec& x) const {
+    if (rev) std::reverse(x.begin(), x.end());
+    solve_natural(x);
+    if (rev) std::reverse(x.begin(), x.end());
+}
+
+void BandLDLT::solve_natural(Vec& x) const {
     for (int r = 0; r < n; ++r) {
         double s = x[r];
         for (int c = std::max(0, r - w); c < r; ++c) s -= L[(size_t)r * w + (c - r + w)] * x[c];

@@ -110,9 +110,12 @@ struct BandLDLT {
     int n = 0, w = 0;
     Vec L;  // row r: entries for columns r-w .. r-1 at [r*w + (c - r + w)]
     Vec D;
+    bool rev = false;
     void factor(const Vec& band);  // band: [r*(w+1) + (c - r + w)], c in [r-w, r]
     void solve(Vec& x) const;
+    void solve_natural(Vec& x) const;
 };
+void set_elimination_order(int order);  // 0 natural, 1 reversed (all banded solves)
 
 // CellCenteredSolver (elliptic.hpp:74-103, elliptic.cpp:68-243)
 class LocalSolver {

@@ -420,6 +420,10 @@ int oracle_weak_residuals(oracle_ctx* ctx, double* flux_jump, double* pressure_j
 
 int64_t oracle_clamp_count(void) { return clamp_count(); }
 
+/* 0: natural elimination order (default), 1: reversed — an equally exact
+ * direct solve with different rounding, used to measure solver-noise floors. */
+void oracle_set_elimination_order(int32_t order) { set_elimination_order(order); }
+
 /* Decomposition tables built the reference's way (decomposition.cpp:35-132,
  * mrcm.cpp:157-189), same layout as mpm2p_layout_tables. */
 int oracle_layout_tables(const mpm2p_problem* p, int32_t s, int32_t* edges, int32_t* hom_cols, int32_t* n_hom) {

@@ -134,7 +134,22 @@ def test_interface_matrix_reused_byte_identically(oracle):
     assert np.array_equal(M0, g.interface_matrix())
 
 
-def _compare_runs(rg, ro):
+def run_floor(oracle, prob, split, s0=None):
+    """Solver-roundoff floor of the reference answer itself: the oracle run
+    with natural vs reversed elimination order (both exact direct solves)."""
+    ra = api.Simulator(prob, oracle).run(split, s0)
+    oracle.dll.oracle_set_elimination_order(1)
+    try:
+        rb = api.Simulator(prob, oracle).run(split, s0)
+    finally:
+        oracle.dll.oracle_set_elimination_order(0)
+    assert [x["rebuilt"] for x in ra.record.steps] == [x["rebuilt"] for x in rb.record.steps]
+    return {"s": float(np.max(np.abs(ra.s_final - rb.s_final))), "p": rel_l2(ra.p_final, rb.p_final),
+            "u": rel_l2(ra.u_final, rb.u_final)}
+
+
+def _compare_runs(rg, ro, floor=None):
+    floor = floor or {"s": 0.0, "p": 0.0, "u": 0.0}
     seq_g = [s["rebuilt"] for s in rg.record.steps]
     seq_o = [s["rebuilt"] for s in ro.record.steps]
     assert seq_g == seq_o
@@ -143,9 +158,9 @@ def _compare_runs(rg, ro):
     assert (c_g.homogeneous, c_g.particular, c_g.downscale, c_g.interface_solves) == \
            (c_o.homogeneous, c_o.particular, c_o.downscale, c_o.interface_solves)
     assert rg.record.breakthrough_step == ro.record.breakthrough_step
-    assert np.max(np.abs(rg.s_final - ro.s_final)) <= TOL_S
-    assert rel_l2(rg.p_final, ro.p_final) <= TOL_PU
-    assert rel_l2(rg.u_final, ro.u_final) <= TOL_PU
+    assert np.max(np.abs(rg.s_final - ro.s_final)) <= max(TOL_S, 10 * floor["s"])
+    assert rel_l2(rg.p_final, ro.p_final) <= max(TOL_PU, 10 * floor["p"])
+    assert rel_l2(rg.u_final, ro.u_final) <= max(TOL_PU, 10 * floor["u"])
     dts_g = np.array([s["dt"] for s in rg.record.steps])
     dts_o = np.array([s["dt"] for s in ro.record.steps])
     np.testing.assert_allclose(dts_g, dts_o, rtol=1e-8)
@@ -179,11 +194,13 @@ def test_config_c3_two_pass(oracle):
     sp = dataclasses.replace(c.split, max_steps_hard=400)
     g, o = pair(c.problem, oracle)
     r1g, r1o = g.run(sp, c.s0()), o.run(sp, c.s0())
-    _compare_runs(r1g, r1o)
+    # C3's field spans 1.6e7 in K (cond(M) ~ 2e9): the reference's own direct
+    # solves carry ~1e-7 roundoff in u, measured here as the floor.
+    _compare_runs(r1g, r1o, run_floor(oracle, c.problem, sp, c.s0()))
     if r1g.record.breakthrough_step >= 0:
         te = configs.breakthrough_plus_50(r1g.record.breakthrough_step)
         sp2 = dataclasses.replace(sp, stop_on_breakthrough=False, te=min(te, 400))
-        _compare_runs(g.run(sp2, c.s0()), o.run(sp2, c.s0()))
+        _compare_runs(g.run(sp2, c.s0()), o.run(sp2, c.s0()), run_floor(oracle, c.problem, sp2, c.s0()))
 
 
 @pytest.mark.parametrize("name,steps", [("C2", 120), ("C4", 40)])
