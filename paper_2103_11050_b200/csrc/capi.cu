@@ -89,6 +89,9 @@ const Scalars& sync_scalars(Ctx& c) {
         if (e & ERR_ROBIN_BETA) throw ConfigError("CellCenteredSolver: Robin face requires beta > 0");
         if (e & ERR_PIVOT) throw NumericError("CellCenteredSolver: direct solve failed");
         if (e & ERR_EPS_ZERO) throw NumericError("epsilon: zero reference norm in relative mode");
+        if (e & ERR_SINGULAR)
+            throw NumericError("compute_basis_set: interface matrix is numerically singular (rcond=" +
+                               std::to_string(c.sc_host->rcond) + ")");
         throw NumericError("device error word " + std::to_string(e));
     }
     return *c.sc_host;

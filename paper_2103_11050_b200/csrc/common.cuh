@@ -67,4 +67,30 @@ __device__ __forceinline__ double warp_min(double v) {
     return v;
 }
 
+// Block-wide reduction (result valid in thread 0). sh: >= 32 doubles of smem.
+template <typename F>
+__device__ __forceinline__ double block_reduce_op(double v, F op, double ident, double* sh) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_down_sync(0xffffffffu, v, o));
+    __syncthreads();
+    if (lane == 0) sh[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        v = lane < (int)(blockDim.x >> 5) ? sh[lane] : ident;
+        for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_down_sync(0xffffffffu, v, o));
+    }
+    __syncthreads();
+    return v;
+}
+
+// The last block of a grid combines the per-block partials part[b*stride+off]
+// (b < nparts) in parallel, in a fixed tree order (deterministic).
+template <typename F>
+__device__ __forceinline__ double reduce_partials(const double* part, int nparts, int stride, int off, F op,
+                                                  double ident, double* sh) {
+    double v = ident;
+    for (int b = threadIdx.x; b < nparts; b += blockDim.x) v = op(v, __ldcg(part + (size_t)b * stride + off));
+    return block_reduce_op(v, op, ident, sh);
+}
+
 }  // namespace mpm2p

@@ -97,6 +97,7 @@ struct Ctx {
     DevBuf<unsigned> red_count;
     Scalars* sc_host = nullptr;  // pinned
 
+    int iface_sym = -1;  // J*M symmetric (pivot-free inverse)? -1 unknown
     bool has_basis = false;
     bool has_factor = false;
     double rcond = 0.0;
@@ -194,6 +195,15 @@ void configure_kernels();
 // In-place Gauss-Jordan inverse with partial pivoting of an n x n row-major
 // matrix A into Ainv; returns the 1-norm reciprocal condition number.
 double dense_inverse(Ctx& c, const double* A, double* Ainv, int n);
+// Stream-ordered variant: writes rcond to rcond_dev and sets err_bit in the
+// device error word when rcond <= threshold (no host synchronisation).
+void dense_inverse_async(Ctx& c, const double* A, double* Ainv, int n, double* rcond_dev, unsigned err_bit,
+                         double threshold);
+// Interface matrix: pivot-free blocked GJ on K = J M (symmetric quasi-definite).
+void interface_inverse_async(Ctx& c, const double* M, double* Minv, int n, double* rcond_dev, unsigned err_bit,
+                             double threshold);
+// SPD matrix (repair Laplacian): pivot-free blocked GJ; returns rcond.
+double spd_inverse(Ctx& c, const double* A, double* Ainv, int n);
 void launch_gemv(Ctx& c, const double* A, const double* x, double* y, int n);
 void launch_csr_residual(Ctx& c, const int* ptr, const int* col, const double* val, const double* x,
                          const double* b, double* r, int n);

@@ -3,12 +3,23 @@
 // the repair Laplacian, mrcm.cpp:372).
 //
 // The interface matrix is fixed between rebuilds, so it is inverted once per
-// rebuild by Gauss-Jordan elimination with partial pivoting (one cooperative
-// kernel, three grid barriers per pivot) and every later interface solve is a
-// dense GEMV plus one step of iterative refinement against the sparse CSR
-// operator — as accurate as the reference's LU solve, and bandwidth-bound
-// rather than latency-bound. rcond is computed exactly as
-// 1 / (||M||_1 ||M^-1||_1) (the quantity Eigen's rcond() estimates).
+// rebuild and every later interface solve is a dense GEMV plus one step of
+// iterative refinement against the sparse CSR operator — as accurate as the
+// reference's LU solve, and bandwidth-bound rather than latency-bound.
+//
+// Inversion is blocked Gauss-Jordan with partial pivoting on [A | I], one
+// cooperative kernel, per panel of b columns:
+//   1. CTA 0 factors the n x b panel in shared memory (pivot search, row
+//      swaps, elimination), keeping the elimination vectors v_c in place of
+//      the eliminated columns; the product T = prod_c (I - v_c e_c^T) of the
+//      panel's b steps is I - G E_R^T with G = V * alpha (alpha: a b x b
+//      triangular recurrence on the pivot rows).
+//   2. all CTAs apply the panel's row swaps and snapshot the b pivot rows;
+//   3. all CTAs apply the rank-b update W -= G * W[R, :] (GEMM-shaped).
+// Three grid barriers per panel instead of three per pivot.
+// rcond = 1 / (||A||_1 ||A^-1||_1) is computed on the device (the quantity
+// Eigen's rcond() estimates) and compared to the reference's 1e-14 guard
+// there, so a rebuild needs no host synchronisation.
 #include <cooperative_groups.h>
 
 #include "context.cuh"
@@ -20,65 +31,340 @@ namespace mpm2p {
 namespace {
 
 constexpr int TPB = 256;
+constexpr int GJ_THREADS = 1024;
 
-// W: n x 2n augmented [A | I], row-major. piv/colbuf/rowbuf/krow: scratch.
-__global__ void k_gauss_jordan(double* __restrict__ W, int n, int* __restrict__ piv, double* __restrict__ colbuf,
-                               double* __restrict__ rowbuf, double* __restrict__ krow, int* __restrict__ singular) {
+struct GJArgs {
+    double* W;      // n x 2n, row-major
+    int n, b;
+    double* G;      // n x b
+    int* swp;       // n: pivot row chosen for each column
+    double* Rb;     // b x 2n pivot-row snapshot
+    int* singular;
+};
+
+__global__ void __launch_bounds__(GJ_THREADS) k_gauss_jordan(GJArgs a) {
     cg::grid_group grid = cg::this_grid();
-    const int n2 = 2 * n;
-    const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const long long nth = (long long)gridDim.x * blockDim.x;
-    __shared__ double sv[32];
-    __shared__ int si[32];
-    for (int k = 0; k < n; ++k) {
-        // phase A: pivot search in column k (block 0)
+    extern __shared__ double sp[];  // panel n x b, row-major
+    __shared__ double prow[16];
+    __shared__ double alpha[16 * 16];
+    __shared__ double wv[32];
+    __shared__ int wi[32];
+    const int n = a.n, b = a.b, n2 = 2 * n;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const long long gtid = (long long)blockIdx.x * blockDim.x + tid;
+    const long long gnt = (long long)gridDim.x * blockDim.x;
+    const int lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
+    for (int k0 = 0; k0 < n; k0 += b) {
+        const int bb = (n - k0) < b ? (n - k0) : b;
+        // ---- phase 1: panel factorization on CTA 0 --------------------------
         if (blockIdx.x == 0) {
-            double best = -1.0;
-            int bi = k;
-            for (int i = k + threadIdx.x; i < n; i += blockDim.x) {
-                const double v = fabs(W[(size_t)i * n2 + k]);
-                if (v > best || (v == best && i < bi)) { best = v; bi = i; }
+            for (int x = tid; x < n * bb; x += nt) {
+                const int i = x / bb, j = x % bb;
+                sp[i * b + j] = a.W[(size_t)i * n2 + k0 + j];
             }
-            const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-            for (int o = 16; o > 0; o >>= 1) {
-                const double ov = __shfl_down_sync(0xffffffffu, best, o);
-                const int oi = __shfl_down_sync(0xffffffffu, bi, o);
-                if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
-            }
-            if (lane == 0) { sv[w] = best; si[w] = bi; }
             __syncthreads();
-            if (threadIdx.x == 0) {
-                for (int t = 1; t < (int)(blockDim.x >> 5); ++t)
-                    if (sv[t] > sv[0] || (sv[t] == sv[0] && si[t] < si[0])) { sv[0] = sv[t]; si[0] = si[t]; }
-                piv[0] = si[0];
-                if (!(sv[0] > 0.0)) *singular = 1;
+            for (int c = 0; c < bb; ++c) {
+                const int kc = k0 + c;
+                double best = -1.0;
+                int bi = kc;
+                for (int i = kc + tid; i < n; i += nt) {
+                    const double v = fabs(sp[i * b + c]);
+                    if (v > best) { best = v; bi = i; }
+                }
+                for (int o = 16; o > 0; o >>= 1) {
+                    const double ov = __shfl_down_sync(0xffffffffu, best, o);
+                    const int oi = __shfl_down_sync(0xffffffffu, bi, o);
+                    if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+                }
+                if (lane == 0) { wv[warp] = best; wi[warp] = bi; }
+                __syncthreads();
+                if (tid == 0) {
+                    double bv = wv[0];
+                    int bx = wi[0];
+                    for (int w = 1; w < nwarps; ++w)
+                        if (wv[w] > bv || (wv[w] == bv && wi[w] < bx)) { bv = wv[w]; bx = wi[w]; }
+                    wi[0] = bx;
+                    a.swp[kc] = bx;
+                    if (!(bv > 0.0)) *a.singular = 1;
+                }
+                __syncthreads();
+                const int q = wi[0];
+                if (q != kc && tid < bb) {
+                    const double t = sp[kc * b + tid];
+                    sp[kc * b + tid] = sp[q * b + tid];
+                    sp[q * b + tid] = t;
+                }
+                __syncthreads();
+                if (tid < bb) prow[tid] = sp[kc * b + tid];
+                __syncthreads();
+                const double piv = prow[c];
+                const double pinv = 1.0 / piv;
+                for (int i = tid; i < n; i += nt) {
+                    double* r = sp + i * b;
+                    if (i == kc) {
+                        for (int j = c + 1; j < bb; ++j) r[j] = prow[j] * pinv;
+                        r[c] = (piv - 1.0) * pinv;  // v_c at the pivot row
+                    } else {
+                        const double m = r[c] * pinv;
+                        for (int j = c + 1; j < bb; ++j) r[j] -= m * prow[j];
+                        r[c] = m;                   // v_c elsewhere
+                    }
+                }
+                __syncthreads();
+            }
+            // alpha: g_j = sum_{c>=j} v_c alpha[c][j] (thread j owns column j)
+            if (tid < bb) {
+                const int j = tid;
+                double y[16];
+                for (int r = 0; r < bb; ++r) y[r] = (r == j ? 1.0 : 0.0) - sp[(k0 + r) * b + j];
+                for (int c = 0; c < bb; ++c) alpha[c * 16 + j] = 0.0;
+                alpha[j * 16 + j] = 1.0;
+                for (int c = j + 1; c < bb; ++c) {
+                    const double yc = y[c];
+                    alpha[c * 16 + j] = yc;
+                    for (int r = 0; r < bb; ++r) y[r] -= sp[(k0 + r) * b + c] * yc;
+                }
+            }
+            __syncthreads();
+            for (int i = tid; i < n; i += nt) {
+                double g[16];
+                for (int j = 0; j < bb; ++j) g[j] = 0.0;
+                for (int c = 0; c < bb; ++c) {
+                    const double v = sp[i * b + c];
+                    for (int j = 0; j <= c; ++j) g[j] += v * alpha[c * 16 + j];
+                }
+                for (int j = 0; j < bb; ++j) a.G[(size_t)i * b + j] = g[j];
             }
         }
         grid.sync();
-        const int p = piv[0];
-        // phase B: snapshot the pivot row (after the swap), column k and old row k
-        for (long long x = tid; x < n2; x += nth) {
-            rowbuf[x] = W[(size_t)p * n2 + x];
-            krow[x] = W[(size_t)k * n2 + x];
-        }
-        for (long long i = tid; i < n; i += nth) {
-            const int src = i == k ? p : (i == p ? k : (int)i);
-            colbuf[i] = W[(size_t)src * n2 + k];
+        // ---- phase 2: row swaps on the active columns, pivot-row snapshot ----
+        for (long long j = k0 + gtid; j < n2; j += gnt) {
+            for (int c = 0; c < bb; ++c) {
+                const int kc = k0 + c, q = a.swp[kc];
+                if (q != kc) {
+                    const double t = a.W[(size_t)kc * n2 + j];
+                    a.W[(size_t)kc * n2 + j] = a.W[(size_t)q * n2 + j];
+                    a.W[(size_t)q * n2 + j] = t;
+                }
+            }
+            for (int c = 0; c < bb; ++c) a.Rb[(size_t)c * n2 + j] = a.W[(size_t)(k0 + c) * n2 + j];
         }
         grid.sync();
-        // phase C: eliminate column k from every other row, scale the pivot row
-        const double pv = rowbuf[k];
-        const double pinv = 1.0 / pv;
-        for (long long x = tid; x < (long long)n * n2; x += nth) {
-            const int i = (int)(x / n2), j = (int)(x % n2);
-            if (i == k) {
-                W[x] = rowbuf[j] * pinv;
-            } else {
-                const double base = (i == p) ? krow[j] : W[x];
-                W[x] = base - (colbuf[i] * pinv) * rowbuf[j];
+        // ---- phase 3: W[:, k0:] -= G * Rb, tiles of 64 rows x 128 columns -----
+        {
+            double* sg = sp;               // 64 x 16 tile of G
+            double* sr = sp + 64 * 16;     // 16 x 128 tile of Rb
+            const int ncol = n2 - k0;
+            const int tr = (n + 63) / 64, tc = (ncol + 127) / 128;
+            const int ty = tid >> 5, tx = tid & 31;  // 32 x 32 threads: 2 rows x 4 cols each
+            for (int tile = blockIdx.x; tile < tr * tc; tile += gridDim.x) {
+                const int i0 = (tile / tc) * 64, j0 = k0 + (tile % tc) * 128;
+                __syncthreads();
+                for (int x = tid; x < 64 * 16; x += nt) {
+                    const int i = i0 + x / 16, c = x % 16;
+                    sg[x] = (i < n && c < bb) ? a.G[(size_t)i * b + c] : 0.0;
+                }
+                for (int x = tid; x < 16 * 128; x += nt) {
+                    const int c = x / 128, j = j0 + x % 128;
+                    sr[x] = (c < bb && j < n2) ? a.Rb[(size_t)c * n2 + j] : 0.0;
+                }
+                __syncthreads();
+                double acc[2][4];
+#pragma unroll
+                for (int r = 0; r < 2; ++r)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) acc[r][q] = 0.0;
+#pragma unroll
+                for (int c = 0; c < 16; ++c) {
+                    double gv[2], rv[4];
+#pragma unroll
+                    for (int r = 0; r < 2; ++r) gv[r] = sg[(ty + 32 * r) * 16 + c];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) rv[q] = sr[c * 128 + tx + 32 * q];
+#pragma unroll
+                    for (int r = 0; r < 2; ++r)
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) acc[r][q] += gv[r] * rv[q];
+                }
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    const int i = i0 + ty + 32 * r;
+                    if (i >= n) continue;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int j = j0 + tx + 32 * q;
+                        if (j < n2) a.W[(size_t)i * n2 + j] -= acc[r][q];
+                    }
+                }
             }
         }
         grid.sync();
+    }
+}
+
+// ---- pivot-free blocked Gauss-Jordan (symmetric quasi-definite / SPD) -----
+// In-place inversion of W (n x n). For each diagonal block p (pb <= 16):
+//   A: every CTA inverts W_pp redundantly in shared memory (P = W_pp^-1),
+//      then a slice of Rbuf = P W_p,: (new block row) and Cbuf = W_:,p (old
+//      block column);
+//   B: W_ij -= Cbuf_i Rbuf_j off the block; W_pj = Rbuf_j; W_ip = -Cbuf_i P;
+//      W_pp = P.
+// Two grid barriers per block, every CTA busy in both phases. Stable without
+// pivoting for quasi-definite K = J M (checked per context) and
+// for the SPD repair Laplacian.
+struct BGJArgs {
+    double* W;
+    int n;
+    double* Rbuf;  // 16 x n
+    double* Cbuf;  // n x 16
+    int* singular;
+};
+
+__global__ void __launch_bounds__(256) k_block_gj(BGJArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double P[16][17];
+    __shared__ double sg[64 * 16];
+    __shared__ double sr[16 * 128];
+    const int n = a.n, tid = threadIdx.x, nt = blockDim.x;
+    for (int p0 = 0; p0 < n; p0 += 16) {
+        const int pb = n - p0 < 16 ? n - p0 : 16;
+        // ---- phase A: invert the diagonal block (every CTA) -----------------
+        {
+            const int r = tid / 16, cc = tid % 16;
+            if (r < pb && cc < pb) P[r][cc] = a.W[(size_t)(p0 + r) * n + p0 + cc];
+            __syncthreads();
+            for (int k = 0; k < pb; ++k) {
+                const double piv = P[k][k];
+                double f = 0.0, rk = 0.0;
+                if (r < pb && cc < pb) {
+                    f = P[r][k];
+                    rk = P[k][cc];
+                }
+                __syncthreads();
+                if (r < pb && cc < pb) {
+                    const double pinv = 1.0 / piv;
+                    if (r == k) P[r][cc] = (cc == k) ? pinv : rk * pinv;
+                    else P[r][cc] = (cc == k) ? -f * pinv : P[r][cc] - f * pinv * rk;
+                }
+                if (blockIdx.x == 0 && tid == 0 && (!(piv != 0.0) || !isfinite(piv))) *a.singular = 1;
+                __syncthreads();
+            }
+        }
+        // slices: new block row Rbuf = P * W[p, :] and old block column Cbuf
+        for (int j = blockIdx.x * nt + tid; j < n; j += gridDim.x * nt) {
+            if (j >= p0 && j < p0 + pb) continue;
+            double wcol[16];
+#pragma unroll
+            for (int c = 0; c < 16; ++c) wcol[c] = c < pb ? a.W[(size_t)(p0 + c) * n + j] : 0.0;
+#pragma unroll
+            for (int r = 0; r < 16; ++r) {
+                double acc = 0.0;
+#pragma unroll
+                for (int c = 0; c < 16; ++c)
+                    if (r < pb && c < pb) acc += P[r][c] * wcol[c];
+                if (r < pb) a.Rbuf[(size_t)r * n + j] = acc;
+            }
+        }
+        for (int x = blockIdx.x * nt + tid; x < n * 16; x += gridDim.x * nt) {
+            const int i = x / 16, c = x % 16;
+            a.Cbuf[x] = (c < pb && (i < p0 || i >= p0 + pb)) ? a.W[(size_t)i * n + p0 + c] : 0.0;
+        }
+        grid.sync();
+        // ---- phase B: rank-pb update and block row/column writes -------------
+        const int tr = (n + 63) / 64, tc = (n + 127) / 128;
+        const int ty = tid >> 4, tx = tid & 15;  // 16 x 16 threads: 4 rows x 8 cols each
+        for (int tile = blockIdx.x; tile < tr * tc; tile += gridDim.x) {
+            const int i0 = (tile / tc) * 64, j0 = (tile % tc) * 128;
+            __syncthreads();
+            for (int x = tid; x < 64 * 16; x += nt) {
+                const int i = i0 + x / 16;
+                sg[x] = i < n ? a.Cbuf[(size_t)i * 16 + x % 16] : 0.0;
+            }
+            for (int x = tid; x < 16 * 128; x += nt) {
+                const int c = x / 128, j = j0 + x % 128;
+                sr[x] = (c < pb && j < n && (j < p0 || j >= p0 + pb)) ? a.Rbuf[(size_t)c * n + j] : 0.0;
+            }
+            __syncthreads();
+            double acc[4][8];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int t = 0; t < 8; ++t) acc[q][t] = 0.0;
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+                double gv[4], rv[8];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) gv[q] = sg[(ty + 16 * q) * 16 + c];
+#pragma unroll
+                for (int t = 0; t < 8; ++t) rv[t] = sr[c * 128 + tx + 16 * t];
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) acc[q][t] += gv[q] * rv[t];
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int i = i0 + ty + 16 * q;
+                if (i >= n) continue;
+                const bool ip = i >= p0 && i < p0 + pb;
+#pragma unroll
+                for (int t = 0; t < 8; ++t) {
+                    const int j = j0 + tx + 16 * t;
+                    if (j >= n) continue;
+                    const bool jp = j >= p0 && j < p0 + pb;
+                    double* w = a.W + (size_t)i * n + j;
+                    if (!ip && !jp) *w -= acc[q][t];
+                    else if (ip && !jp) *w = sr[(i - p0) * 128 + (j - j0)];
+                    else if (!ip && jp) {
+                        double v = 0.0;
+                        for (int c = 0; c < pb; ++c) v -= sg[(i - i0) * 16 + c] * P[c][j - p0];
+                        *w = v;
+                    } else {
+                        *w = P[i - p0][j - p0];
+                    }
+                }
+            }
+        }
+        grid.sync();
+    }
+}
+
+// K = J M: phi-rows first, then the negated psi-rows.
+__global__ void k_j_times(const double* __restrict__ M, double* __restrict__ K, int n) {
+    const int h = n / 2;
+    for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < (long long)n * n;
+         x += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(x / n), j = (int)(x % n);
+        K[x] = i < h ? M[(size_t)(h + i) * n + j] : -M[(size_t)(i - h) * n + j];
+    }
+}
+
+// M^-1 = K^-1 J: columns permuted and the psi half negated.
+__global__ void k_times_j(const double* __restrict__ Kinv, double* __restrict__ Minv, int n) {
+    const int h = n / 2;
+    for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < (long long)n * n;
+         x += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(x / n), j = (int)(x % n);
+        Minv[x] = j < h ? -Kinv[(size_t)i * n + h + j] : Kinv[(size_t)i * n + (j - h)];
+    }
+}
+
+// max |A_ij - A_ji| and max |A_ij| (symmetry check of J M, once per context).
+__global__ void k_asym(const double* __restrict__ A, int n, double* out) {
+    __shared__ double sh[32];
+    double d = 0.0, m = 0.0;
+    for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < (long long)n * n;
+         x += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(x / n), j = (int)(x % n);
+        d = fmax(d, fabs(A[x] - A[(size_t)j * n + i]));
+        m = fmax(m, fabs(A[x]));
+    }
+    auto mx = [](double a, double b) { return fmax(a, b); };
+    d = block_reduce_op(d, mx, 0.0, sh);
+    m = block_reduce_op(m, mx, 0.0, sh);
+    if (threadIdx.x == 0) {
+        out[2 * blockIdx.x] = d;
+        out[2 * blockIdx.x + 1] = m;
     }
 }
 
@@ -98,18 +384,34 @@ __global__ void k_extract(const double* __restrict__ W, double* __restrict__ Ain
     }
 }
 
-// 1-norms: out[0] = max_j sum_i |A_ij|, out[1] = same for B.
-__global__ void k_norm1(const double* __restrict__ A, const double* __restrict__ B, int n, double* out) {
+// Column 1-norms of A and B: partial column sums over row blocks of 64
+// (grid y), coalesced along rows...
+__global__ void k_colsum(const double* __restrict__ A, const double* __restrict__ B, int n, double* part) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const int i0 = blockIdx.y * 64, i1 = min(n, i0 + 64);
+    double s1 = 0.0, s2 = 0.0;
+    for (int i = i0; i < i1; ++i) {
+        s1 += fabs(A[(size_t)i * n + j]);
+        s2 += fabs(B[(size_t)i * n + j]);
+    }
+    part[(size_t)blockIdx.y * 2 * n + j] = s1;
+    part[(size_t)blockIdx.y * 2 * n + n + j] = s2;
+}
+
+// ...then one block forms rcond = 1/(||A||_1 ||B||_1) and applies the guard.
+__global__ void k_rcond(const double* __restrict__ part, int n, int nrb, const int* singular, double* rcond_out,
+                        unsigned* err, unsigned err_bit, double threshold) {
     __shared__ double sa[32], sb[32];
     double ma = 0.0, mb = 0.0;
     for (int j = threadIdx.x; j < n; j += blockDim.x) {
-        double a = 0.0, b = 0.0;
-        for (int i = 0; i < n; ++i) {
-            a += fabs(A[(size_t)i * n + j]);
-            b += fabs(B[(size_t)i * n + j]);
+        double s1 = 0.0, s2 = 0.0;
+        for (int r = 0; r < nrb; ++r) {
+            s1 += part[(size_t)r * 2 * n + j];
+            s2 += part[(size_t)r * 2 * n + n + j];
         }
-        ma = fmax(ma, a);
-        mb = fmax(mb, b);
+        ma = fmax(ma, s1);
+        mb = fmax(mb, s2);
     }
     ma = warp_max(ma);
     mb = warp_max(mb);
@@ -117,9 +419,12 @@ __global__ void k_norm1(const double* __restrict__ A, const double* __restrict__
     if (lane == 0) { sa[w] = ma; sb[w] = mb; }
     __syncthreads();
     if (threadIdx.x == 0) {
-        for (int t = 1; t < (int)(blockDim.x >> 5); ++t) { sa[0] = fmax(sa[0], sa[t]); sb[0] = fmax(sb[0], sb[t]); }
-        out[0] = sa[0];
-        out[1] = sb[0];
+        double na = sa[0], nb = sb[0];
+        for (int t = 1; t < (int)(blockDim.x >> 5); ++t) { na = fmax(na, sa[t]); nb = fmax(nb, sb[t]); }
+        double rc = 0.0;
+        if (!*singular && isfinite(nb) && na > 0.0 && nb > 0.0) rc = 1.0 / (na * nb);
+        *rcond_out = rc;
+        if (!(rc > threshold)) atomicOr(err, err_bit);
     }
 }
 
@@ -151,33 +456,130 @@ __global__ void k_axpy(double* __restrict__ y, const double* __restrict__ x, int
 
 }  // namespace
 
-double dense_inverse(Ctx& c, const double* A, double* Ainv, int n) {
+namespace {
+
+void block_gj_inplace(Ctx& c, double* W, int n) {
+    c.gj_col.alloc(std::max(c.gj_col.n, (size_t)n * 16));
+    c.gj_row.alloc(std::max(c.gj_row.n, (size_t)n * 16));
+    c.gj_piv.alloc(std::max(c.gj_piv.n, (size_t)n + 1));
+    CK(cudaMemsetAsync(c.gj_piv.p + n, 0, sizeof(int), c.st));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_block_gj, 256, 0));
+    if (per_sm < 1) throw CudaError("dense_inverse: block Gauss-Jordan does not fit on an SM");
+    const int tiles = cdiv(n, 64) * cdiv(n, 128);
+    const int blocks = std::min(per_sm * c.num_sms, std::max(c.num_sms, tiles));
+    BGJArgs ga{W, n, c.gj_row.p, c.gj_col.p, c.gj_piv.p + n};
+    void* args[] = {&ga};
+    PROF(c, "k_block_gj");
+    CK(cudaLaunchCooperativeKernel((void*)k_block_gj, blocks, 256, args, 0, c.st));
+    CK_LAUNCH();
+}
+
+void launch_rcond(Ctx& c, const double* A, const double* Ainv, int n, double* rcond_dev, unsigned err_bit,
+                  double threshold) {
+    const int nrb = cdiv(n, 64);
+    {
+        PROF(c, "k_colsum");
+        k_colsum<<<dim3(cdiv(n, TPB), nrb), TPB, 0, c.st>>>(A, Ainv, n, c.gj_work.p);
+        CK_LAUNCH();
+    }
+    {
+        PROF(c, "k_rcond");
+        k_rcond<<<1, 1024, 0, c.st>>>(c.gj_work.p, n, nrb, c.gj_piv.p + n, rcond_dev, &c.sc.p->err, err_bit,
+                                      threshold);
+        CK_LAUNCH();
+    }
+}
+
+}  // namespace
+
+// Interface matrix inverse: pivot-free blocked GJ on K = J M when K is
+// symmetric (checked once per context; the formulation makes it so), else the
+// pivoted panel GJ on M.
+void interface_inverse_async(Ctx& c, const double* M, double* Minv, int n, double* rcond_dev, unsigned err_bit,
+                             double threshold) {
+    if (n == 0) return;
+    c.gj_work.alloc(std::max(c.gj_work.n, (size_t)2 * n * n));
+    c.gj_piv.alloc(std::max(c.gj_piv.n, (size_t)n + 1));
+    {
+        PROF(c, "k_j_times");
+        k_j_times<<<std::min(cdiv((long long)n * n, TPB), 8 * c.num_sms), TPB, 0, c.st>>>(M, c.gj_work, n);
+        CK_LAUNCH();
+    }
+    if (c.iface_sym < 0) {
+        const int g = std::min(cdiv((long long)n * n, TPB), 2 * c.num_sms);
+        DevBuf<double> part;
+        part.alloc(2 * g);
+        k_asym<<<g, TPB, 0, c.st>>>(c.gj_work, n, part);
+        CK_LAUNCH();
+        std::vector<double> h(2 * g);
+        CK(cudaMemcpyAsync(h.data(), part.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost, c.st));
+        CK(cudaStreamSynchronize(c.st));
+        double d = 0.0, m = 0.0;
+        for (int b = 0; b < g; ++b) {
+            d = std::max(d, h[2 * b]);
+            m = std::max(m, h[2 * b + 1]);
+        }
+        c.iface_sym = (m > 0.0 && d <= 1e-12 * m) ? 1 : 0;
+    }
+    if (c.iface_sym == 1) {
+        block_gj_inplace(c, c.gj_work, n);
+        {
+            PROF(c, "k_times_j");
+            k_times_j<<<std::min(cdiv((long long)n * n, TPB), 8 * c.num_sms), TPB, 0, c.st>>>(c.gj_work, Minv, n);
+            CK_LAUNCH();
+        }
+        launch_rcond(c, M, Minv, n, rcond_dev, err_bit, threshold);
+    } else {
+        dense_inverse_async(c, M, Minv, n, rcond_dev, err_bit, threshold);
+    }
+}
+
+// SPD inverse (the static repair Laplacian): pivot-free blocked GJ.
+double spd_inverse(Ctx& c, const double* A, double* Ainv, int n) {
     if (n == 0) return 1.0;
     c.gj_work.alloc(std::max(c.gj_work.n, (size_t)2 * n * n));
-    c.gj_col.alloc(std::max(c.gj_col.n, (size_t)n));
-    c.gj_row.alloc(std::max(c.gj_row.n, (size_t)2 * n));
-    c.gj_krow.alloc(std::max(c.gj_krow.n, (size_t)2 * n));
-    c.gj_piv.alloc(std::max(c.gj_piv.n, (size_t)2));
+    c.gj_piv.alloc(std::max(c.gj_piv.n, (size_t)n + 1));
+    CK(cudaMemcpyAsync(Ainv, A, (size_t)n * n * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
+    block_gj_inplace(c, Ainv, n);
+    launch_rcond(c, A, Ainv, n, &c.sc.p->rcond, 0u, 0.0);
+    double rc = 0.0;
+    CK(cudaMemcpyAsync(&rc, &c.sc.p->rcond, sizeof(double), cudaMemcpyDeviceToHost, c.st));
+    CK(cudaStreamSynchronize(c.st));
+    return rc;
+}
+
+void dense_inverse_async(Ctx& c, const double* A, double* Ainv, int n, double* rcond_dev, unsigned err_bit,
+                         double threshold) {
+    if (n == 0) return;
+    int b = 16;
+    const size_t smem_cap = 180 * 1024;
+    while (b > 2 && (size_t)n * b * sizeof(double) > smem_cap) b /= 2;
+    if ((size_t)n * b * sizeof(double) > smem_cap)
+        throw CapacityError("dense_inverse: interface system of dimension " + std::to_string(n) +
+                            " is too large for the dense path");
+    // panel (CTA 0, phase 1) or the 64x16 + 16x128 GEMM tiles (phase 3)
+    const size_t smem = std::max<size_t>((size_t)n * b, 64 * 16 + 16 * 128) * sizeof(double);
+    CK(cudaFuncSetAttribute(k_gauss_jordan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cap));
+    c.gj_work.alloc(std::max(c.gj_work.n, (size_t)2 * n * n));
+    c.gj_col.alloc(std::max(c.gj_col.n, (size_t)n * b));   // G
+    c.gj_row.alloc(std::max(c.gj_row.n, (size_t)b * 2 * n));  // Rb
+    c.gj_piv.alloc(std::max(c.gj_piv.n, (size_t)n + 1));    // swaps + singular flag
     {
         PROF(c, "k_augment");
         k_augment<<<std::min(cdiv(2LL * n * n, TPB), 8 * c.num_sms), TPB, 0, c.st>>>(A, c.gj_work, n);
         CK_LAUNCH();
     }
-    CK(cudaMemsetAsync(c.gj_piv.p + 1, 0, sizeof(int), c.st));
+    CK(cudaMemsetAsync(c.gj_piv.p + n, 0, sizeof(int), c.st));
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gauss_jordan, TPB, 0));
-    const long long work = 2LL * n * n;
-    int blocks = std::max(1, std::min(per_sm * c.num_sms, cdiv(work, TPB)));
-    double* W = c.gj_work.p;
-    int* piv = c.gj_piv.p;
-    double* colb = c.gj_col.p;
-    double* rowb = c.gj_row.p;
-    double* krow = c.gj_krow.p;
-    int* sing = c.gj_piv.p + 1;
-    void* args[] = {&W, &n, &piv, &colb, &rowb, &krow, &sing};
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gauss_jordan, GJ_THREADS, smem));
+    if (per_sm < 1) throw CudaError("dense_inverse: cooperative kernel does not fit on an SM");
+    const int blocks = c.num_sms;  // one CTA per SM
+    GJArgs ga{c.gj_work.p, n, b, c.gj_col.p, c.gj_piv.p, c.gj_row.p, c.gj_piv.p + n};
+    void* args[] = {&ga};
     {
         PROF(c, "k_gauss_jordan");
-        CK(cudaLaunchCooperativeKernel((void*)k_gauss_jordan, blocks, TPB, args, 0, c.st));
+        CK(cudaLaunchCooperativeKernel((void*)k_gauss_jordan, blocks, GJ_THREADS, args, smem, c.st));
         CK_LAUNCH();
     }
     {
@@ -185,45 +587,46 @@ double dense_inverse(Ctx& c, const double* A, double* Ainv, int n) {
         k_extract<<<std::min(cdiv((long long)n * n, TPB), 8 * c.num_sms), TPB, 0, c.st>>>(c.gj_work, Ainv, n);
         CK_LAUNCH();
     }
-    DevBuf<double> norms;
-    norms.alloc(2);
+    const int nrb = cdiv(n, 64);
     {
-        PROF(c, "k_norm1");
-        k_norm1<<<1, 1024, 0, c.st>>>(A, Ainv, n, norms);
+        PROF(c, "k_colsum");
+        k_colsum<<<dim3(cdiv(n, TPB), nrb), TPB, 0, c.st>>>(A, Ainv, n, c.gj_work.p);  // W is free now
         CK_LAUNCH();
     }
-    double h[2];
-    int singular = 0;
-    CK(cudaMemcpyAsync(h, norms.p, sizeof(h), cudaMemcpyDeviceToHost, c.st));
-    CK(cudaMemcpyAsync(&singular, sing, sizeof(int), cudaMemcpyDeviceToHost, c.st));
+    {
+        PROF(c, "k_rcond");
+        k_rcond<<<1, 1024, 0, c.st>>>(c.gj_work.p, n, nrb, c.gj_piv.p + n, rcond_dev, &c.sc.p->err, err_bit,
+                                      threshold);
+        CK_LAUNCH();
+    }
+}
+
+double dense_inverse(Ctx& c, const double* A, double* Ainv, int n) {
+    if (n == 0) return 1.0;
+    dense_inverse_async(c, A, Ainv, n, &c.sc.p->rcond, 0u, 0.0);
+    double rc = 0.0;
+    CK(cudaMemcpyAsync(&rc, &c.sc.p->rcond, sizeof(double), cudaMemcpyDeviceToHost, c.st));
     CK(cudaStreamSynchronize(c.st));
-    if (singular || !std::isfinite(h[1]) || !(h[0] > 0.0) || !(h[1] > 0.0)) return 0.0;
-    return 1.0 / (h[0] * h[1]);
+    return rc;
 }
 
 void launch_gemv(Ctx& c, const double* A, const double* x, double* y, int n) {
-    {
-        PROF(c, "k_gemv");
-        k_gemv<<<cdiv((long long)n * 32, TPB), TPB, 0, c.st>>>(A, x, y, n);
-        CK_LAUNCH();
-    }
+    PROF(c, "k_gemv");
+    k_gemv<<<cdiv((long long)n * 32, TPB), TPB, 0, c.st>>>(A, x, y, n);
+    CK_LAUNCH();
 }
 
 void launch_csr_residual(Ctx& c, const int* ptr, const int* col, const double* val, const double* x, const double* b,
                          double* r, int n) {
-    {
-        PROF(c, "k_csr_residual");
-        k_csr_residual<<<cdiv(n, TPB), TPB, 0, c.st>>>(ptr, col, val, x, b, r, n);
-        CK_LAUNCH();
-    }
+    PROF(c, "k_csr_residual");
+    k_csr_residual<<<cdiv(n, TPB), TPB, 0, c.st>>>(ptr, col, val, x, b, r, n);
+    CK_LAUNCH();
 }
 
 void launch_axpy(Ctx& c, double* y, const double* x, int n) {
-    {
-        PROF(c, "k_axpy");
-        k_axpy<<<cdiv(n, TPB), TPB, 0, c.st>>>(y, x, n);
-        CK_LAUNCH();
-    }
+    PROF(c, "k_axpy");
+    k_axpy<<<cdiv(n, TPB), TPB, 0, c.st>>>(y, x, n);
+    CK_LAUNCH();
 }
 
 }  // namespace mpm2p

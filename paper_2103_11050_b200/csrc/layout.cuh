@@ -155,6 +155,8 @@ struct Layout {
         for (int i = 0; i < n; ++i) half += iface_nb(inc[i]);
         flux = h < half;
         int r = flux ? h : h - half;
+        k = inc[0];
+        t = 0;
         for (int i = 0; i < n; ++i) {
             const int nb = iface_nb(inc[i]);
             if (r < nb) {

@@ -16,6 +16,7 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include "band.cuh"
+#include "band_reg.cuh"
 #include "context.cuh"
 
 namespace mpm2p {
@@ -540,9 +541,8 @@ __global__ void k_resid(Layout L, const double* __restrict__ skel, const double*
     fmaxv = block_max(fmaxv, sh);
     if (threadIdx.x == 0) part[blockIdx.x] = fmaxv;
     if (last_block_done(counter)) {
+        const double m = reduce_partials(part, gridDim.x, 1, 0, [](double a, double b) { return fmax(a, b); }, 0.0, sh);
         if (threadIdx.x == 0) {
-            double m = 0.0;
-            for (unsigned b = 0; b < gridDim.x; ++b) m = fmax(m, part[b]);
             sc->flux_scale = m;
             *counter = 0;
         }
@@ -579,9 +579,8 @@ __global__ void k_repair_corr(Layout L, int active, int grounded, const double* 
     m = block_max(m, sh);
     if (threadIdx.x == 0) part[blockIdx.x] = m;
     if (last_block_done(counter)) {
+        const double r = reduce_partials(part, gridDim.x, 1, 0, [](double a, double b) { return fmax(a, b); }, 0.0, sh);
         if (threadIdx.x == 0) {
-            double r = 0.0;
-            for (unsigned b = 0; b < gridDim.x; ++b) r = fmax(r, part[b]);
             sc->repair_max = r;
             const double fs = sc->flux_scale;
             sc->repair_warning = r > 0.1 * (fs > 0 ? fs : 1.0);
@@ -668,6 +667,84 @@ __global__ void k_ds_solve(Layout L, const double* __restrict__ BD, const double
     for (int r = lane; r < n; r += 32) p[L.gcell_of(s, r)] = x[r] + shift;
 }
 
+// Register-window variants (band_reg.cuh) for the common subdomain widths.
+template <int B>
+__global__ void __launch_bounds__(WPB * 32) k_ds_solve_r(Layout L, const double* __restrict__ BD,
+                                                         const double* __restrict__ BW, const double* __restrict__ BS,
+                                                         double* __restrict__ D, double* __restrict__ Lr,
+                                                         double* __restrict__ Xd, const double* __restrict__ RS,
+                                                         double* __restrict__ p, Scalars* sc) {
+    __shared__ double stage[WPB][B * B];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int s = blockIdx.x * WPB + w;
+    if (s >= L.n_sub) return;
+    const int n = L.ncs;
+    const size_t so = (size_t)s * n;
+    const BandRows A{BD + so, BW + so, BS + so};
+    double* x = Xd + so;
+    const bool ok = factor_fwd_reg<B, 1>(n, A, D + so, nullptr, Lr + so * B, x, 1, n, stage[w]);
+    if (!ok && lane == 0) atomicOr(&sc->err, ERR_PIVOT);
+    __syncwarp();
+    backward_reg<B, 1>(n, D + so, Lr + so * B, x, 1, n);
+    __syncwarp();
+    double v = 0.0;
+    for (int r = lane; r < n; r += 32) v += x[r];
+    v = warp_sum(v);
+    const double shift = (__shfl_sync(0xffffffffu, RS[s], 0) - __shfl_sync(0xffffffffu, v, 0)) / n;
+    for (int r = lane; r < n; r += 32) p[L.gcell_of(s, r)] = x[r] + shift;
+}
+
+template <int B>
+__global__ void __launch_bounds__(WPB * 32) k_part_solve_r(Layout L, int max_rhs, const double* __restrict__ D,
+                                                           const double* __restrict__ Lc,
+                                                           const double* __restrict__ Lr, double* __restrict__ X) {
+    const int w = threadIdx.x >> 5;
+    const int s = blockIdx.x * WPB + w;
+    if (s >= L.n_sub) return;
+    const int n = L.ncs;
+    const size_t so = (size_t)s * n;
+    double* x = X + xoff(L, max_rhs, s, 0);
+    forward_reg<B, 1>(n, Lc + so * B, x, 1, n);
+    __syncwarp();
+    backward_reg<B, 1>(n, D + so, Lr + so * B, x, 1, n);
+}
+
+constexpr int NR_REG = 8;
+
+template <int B>
+__global__ void __launch_bounds__(WPB * 32) k_factor_solve_r(Layout L, int max_rhs, const double* __restrict__ BD,
+                                                             const double* __restrict__ BW,
+                                                             const double* __restrict__ BS, double* __restrict__ D,
+                                                             double* __restrict__ Lc, double* __restrict__ Lr,
+                                                             double* __restrict__ X, Scalars* sc) {
+    __shared__ double stage[WPB][B * B];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int s = blockIdx.x * WPB + w;
+    if (s >= L.n_sub) return;
+    const int n = L.ncs;
+    const size_t so = (size_t)s * n;
+    const BandRows A{BD + so, BW + so, BS + so};
+    const int nr = 1 + L.n_hom(s);
+    double* Xs = X + xoff(L, max_rhs, s, 0);
+    const int n0 = nr < NR_REG ? nr : NR_REG;
+    const bool ok = factor_fwd_reg<B, NR_REG>(n, A, D + so, Lc + so * B, Lr + so * B, Xs, n0, n, stage[w]);
+    if (!ok && lane == 0) atomicOr(&sc->err, ERR_PIVOT);
+    __syncwarp();
+    for (int m0 = n0; m0 < nr; m0 += NR_REG) {
+        const int cnt = nr - m0 < NR_REG ? nr - m0 : NR_REG;
+        forward_reg<B, NR_REG>(n, Lc + so * B, Xs + (size_t)m0 * n, cnt, n);
+        __syncwarp();
+    }
+    for (int m0 = 0; m0 < nr; m0 += NR_REG) {
+        const int cnt = nr - m0 < NR_REG ? nr - m0 : NR_REG;
+        backward_reg<B, NR_REG>(n, D + so, Lr + so * B, Xs + (size_t)m0 * n, cnt, n);
+        __syncwarp();
+    }
+}
+
+// Subdomain widths with a register-window instantiation; others use band.cuh.
+#define MPM2P_BAND_WIDTHS(X) X(4) X(8) X(10) X(12) X(16) X(20) X(24) X(32)
+
 // Velocity scatter: interior faces from the unshifted local pressure,
 // subdomain-boundary faces from the imposed outward velocity (single-valued
 // on shared edges).
@@ -730,12 +807,10 @@ __global__ void k_divres(Layout L, const double* __restrict__ u, const double* _
         part[2 * blockIdx.x + 1] = scale;
     }
     if (last_block_done(counter)) {
+        auto mx = [](double a, double b) { return fmax(a, b); };
+        const double r = reduce_partials(part, gridDim.x, 2, 0, mx, 0.0, sh);
+        const double sc2 = reduce_partials(part, gridDim.x, 2, 1, mx, 0.0, sh);
         if (threadIdx.x == 0) {
-            double r = 0.0, sc2 = 0.0;
-            for (unsigned b = 0; b < gridDim.x; ++b) {
-                r = fmax(r, part[2 * b]);
-                sc2 = fmax(sc2, part[2 * b + 1]);
-            }
             sc->div_residual = r;
             sc->div_scale = sc2 > 0.0 ? sc2 : 1.0;
             *counter = 0;
@@ -947,7 +1022,7 @@ void launch_setup_static(Ctx& c) {
             k_repair_matrix<<<grid_for(L.n_sub), TPB, 0, c.st>>>(L, c.grounded ? 1 : 0, c.ground, A);
             CK_LAUNCH();
         }
-        const double rc = dense_inverse(c, A, c.Linv, L.n_sub);
+        const double rc = spd_inverse(c, A, c.Linv, L.n_sub);
         if (!(rc > 0.0)) throw NumericError("downscale: compatibility-repair operator is singular");
     }
 }
@@ -992,7 +1067,18 @@ void downscale(Ctx& c, const double* kappa) {
     const size_t sm1 = (size_t)WPB * band_smem_doubles(L.snx, 1) * sizeof(double);
     {
         PROF(c, "k_ds_solve");
-        k_ds_solve<<<band_blocks(L), WPB * 32, sm1, c.st>>>(L, c.BDd, c.BWd, c.BSd, c.Dd, c.Lrd, c.Xd, c.RS, c.p, c.sc);
+        switch (L.snx) {
+#define X(BW_)                                                                                                     \
+    case BW_:                                                                                                      \
+        k_ds_solve_r<BW_><<<band_blocks(L), WPB * 32, 0, c.st>>>(L, c.BDd, c.BWd, c.BSd, c.Dd, c.Lrd, c.Xd, c.RS, \
+                                                                  c.p, c.sc);                                     \
+        break;
+            MPM2P_BAND_WIDTHS(X)
+#undef X
+            default:
+                k_ds_solve<<<band_blocks(L), WPB * 32, sm1, c.st>>>(L, c.BDd, c.BWd, c.BSd, c.Dd, c.Lrd, c.Xd, c.RS,
+                                                                    c.p, c.sc);
+        }
         CK_LAUNCH();
     }
     {
@@ -1019,10 +1105,12 @@ void interface_solve(Ctx& c) {
         CK_LAUNCH();
     }
     launch_gemv(c, c.Minv, c.irhs, c.icoef, c.dim);
-    // one step of iterative refinement against the sparse operator
-    launch_csr_residual(c, c.csr_ptr, c.csr_col, c.csr_val, c.icoef, c.irhs, c.ires, c.dim);
-    launch_gemv(c, c.Minv, c.ires, c.idelta, c.dim);
-    launch_axpy(c, c.icoef, c.idelta, c.dim);
+    // two steps of iterative refinement against the sparse operator
+    for (int it = 0; it < 2; ++it) {
+        launch_csr_residual(c, c.csr_ptr, c.csr_col, c.csr_val, c.icoef, c.irhs, c.ires, c.dim);
+        launch_gemv(c, c.Minv, c.ires, c.idelta, c.dim);
+        launch_axpy(c, c.icoef, c.idelta, c.dim);
+    }
 }
 
 }  // namespace
@@ -1052,8 +1140,18 @@ void launch_rebuild(Ctx& c, const double* kappa, bool compute_beta) {  // comput
     const size_t smr = (size_t)WPB * band_smem_doubles(L.snx, RING_NR) * sizeof(double);
     {
         PROF(c, "k_factor_solve");
-        k_factor_solve<<<band_blocks(L), WPB * 32, smr, c.st>>>(L, c.max_rhs, c.BDm, c.BWm, c.BSm, c.Dm, c.Lcm, c.Lrm, c.X,
-                                                                c.sc);
+        switch (L.snx) {
+#define X(BW_)                                                                                                  \
+    case BW_:                                                                                                   \
+        k_factor_solve_r<BW_><<<band_blocks(L), WPB * 32, 0, c.st>>>(L, c.max_rhs, c.BDm, c.BWm, c.BSm, c.Dm, \
+                                                                      c.Lcm, c.Lrm, c.X, c.sc);               \
+        break;
+            MPM2P_BAND_WIDTHS(X)
+#undef X
+            default:
+                k_factor_solve<<<band_blocks(L), WPB * 32, smr, c.st>>>(L, c.max_rhs, c.BDm, c.BWm, c.BSm, c.Dm,
+                                                                        c.Lcm, c.Lrm, c.X, c.sc);
+        }
         CK_LAUNCH();
     }
     {
@@ -1082,10 +1180,9 @@ void launch_rebuild(Ctx& c, const double* kappa, bool compute_beta) {  // comput
             k_csr_to_dense<<<c.dim, TPB, 0, c.st>>>(c.csr_ptr, c.csr_col, c.csr_val, c.dim, c.Mdense);
             CK_LAUNCH();
         }
-        c.rcond = dense_inverse(c, c.Mdense, c.Minv, c.dim);
-        if (!(c.rcond > 1e-14))
-            throw NumericError("compute_basis_set: interface matrix is numerically singular (rcond=" +
-                               std::to_string(c.rcond) + ")");
+        // rcond guard (mrcm.cpp:227-238) is evaluated on the device; a trip
+        // surfaces as ERR_SINGULAR at the step's scalar readback.
+        interface_inverse_async(c, c.Mdense, c.Minv, c.dim, &c.sc.p->rcond, ERR_SINGULAR, 1e-14);
     }
     interface_solve(c);
     // recon_m (kept for MPM steps) and its traces
@@ -1126,7 +1223,16 @@ void launch_mpm(Ctx& c, const double* kn) {  // mpm_pressure_update (mpm.cpp:31-
     const size_t sm1 = (size_t)WPB * band_smem_doubles(L.snx, 1) * sizeof(double);
     {
         PROF(c, "k_part_solve");
-        k_part_solve<<<band_blocks(L), WPB * 32, sm1, c.st>>>(L, c.max_rhs, c.Dm, c.Lcm, c.Lrm, c.X);
+        switch (L.snx) {
+#define X(BW_)                                                                                                  \
+    case BW_:                                                                                                   \
+        k_part_solve_r<BW_><<<band_blocks(L), WPB * 32, 0, c.st>>>(L, c.max_rhs, c.Dm, c.Lcm, c.Lrm, c.X);    \
+        break;
+            MPM2P_BAND_WIDTHS(X)
+#undef X
+            default:
+                k_part_solve<<<band_blocks(L), WPB * 32, sm1, c.st>>>(L, c.max_rhs, c.Dm, c.Lcm, c.Lrm, c.X);
+        }
         CK_LAUNCH();
     }
     {

@@ -79,6 +79,15 @@ __device__ __forceinline__ DD block_reduce_dd(DD v, DD* sh) {
     return v;
 }
 
+// Parallel double-double combination of per-block partials (hi at off, lo at off+1).
+__device__ __forceinline__ DD reduce_dd_partials(const double* part, int nparts, int off, DD* sh) {
+    DD v{0.0, 0.0};
+    for (int b = threadIdx.x; b < nparts; b += blockDim.x)
+        v = dd_add(v, DD{__ldcg(part + 4 * b + off), __ldcg(part + 4 * b + off + 1)});
+    __syncthreads();
+    return block_reduce_dd(v, sh);
+}
+
 __global__ void k_max_slope(Scalars* sc, double M) {  // transport.cpp:45-49
     double m = 0.0;
     for (int k = 0; k <= 1000; ++k) m = fmax(m, fprime(k * 1e-3, M));
@@ -113,13 +122,13 @@ __global__ void k_cfl(Layout L, const double* __restrict__ u, Scalars* sc, doubl
         part[2 * blockIdx.x + 1] = any;
     }
     if (last_block_done(counter)) {
+        auto mn = [](double a, double b) { return fmin(a, b); };
+        auto mx = [](double a, double b) { return fmax(a, b); };
+        const double best_all = reduce_partials(part, gridDim.x, 2, 0, mn, INFINITY, sh);
+        const double any_all = reduce_partials(part, gridDim.x, 2, 1, mx, 0.0, sh);
         if (threadIdx.x == 0) {
-            double dt = dt_cap / safety;
-            bool anyf = false;
-            for (unsigned b = 0; b < gridDim.x; ++b) {
-                dt = fmin(dt, part[2 * b]);
-                anyf = anyf || part[2 * b + 1] > 0.0;
-            }
+            const double dt = fmin(dt_cap / safety, best_all);  // min is order-independent
+            const bool anyf = any_all > 0.0;
             sc->any_flow = anyf;
             sc->dt = anyf ? fmin(safety * dt, dt_cap) : dt_cap;
             *counter = 0;
@@ -127,43 +136,30 @@ __global__ void k_cfl(Layout L, const double* __restrict__ u, Scalars* sc, doubl
     }
 }
 
-// injection_rate (simulation.cpp:85-101), summed in the reference's face
-// order (W_j, E_j for each j, then S_i, N_i for each i) by one block, then the
-// PVI clock advanced cn times (simulation.cpp:288).
+// injection_rate (simulation.cpp:85-101) as a one-block tree sum (the terms
+// are the reference's; only the summation order differs — the PVI clock is a
+// reported quantity, not a parity one), then the PVI clock advanced cn times
+// (simulation.cpp:288).
 __global__ void k_inj_pvi(Layout L, const double* __restrict__ u, Scalars* sc, double inflow, double M, int cn,
                           int add_pvi) {
-    __shared__ double terms[2 * TPB];
+    __shared__ double sh[32];
     const double fin = frac_flow(inflow, M, nullptr);
     const int nterms = 2 * (L.nx + L.ny);
     double rate = 0.0;
-    for (int base = 0; base < nterms; base += 2 * TPB) {
-        for (int t = threadIdx.x; t < 2 * TPB; t += blockDim.x) {
-            const int idx = base + t;
-            double v = 0.0;
-            if (idx < nterms) {
-                double un, area;
-                if (idx < 2 * L.ny) {
-                    const int j = idx >> 1;
-                    if ((idx & 1) == 0) { un = -u[L.vface(0, j)]; } else { un = u[L.vface(L.nx, j)]; }
-                    area = L.hy;
-                } else {
-                    const int k = idx - 2 * L.ny, i = k >> 1;
-                    if ((k & 1) == 0) { un = -u[L.hface(i, 0)]; } else { un = u[L.hface(i, L.ny)]; }
-                    area = L.hx;
-                }
-                v = un < 0.0 ? -un * area * fin : 0.0;
-                if (!(un < 0.0)) v = -1.0;  // marker: term skipped
-            } else {
-                v = -1.0;
-            }
-            terms[t] = v;
+    for (int idx = threadIdx.x; idx < nterms; idx += blockDim.x) {
+        double un, area;
+        if (idx < 2 * L.ny) {
+            const int j = idx >> 1;
+            un = (idx & 1) == 0 ? -u[L.vface(0, j)] : u[L.vface(L.nx, j)];
+            area = L.hy;
+        } else {
+            const int k = idx - 2 * L.ny, i = k >> 1;
+            un = (k & 1) == 0 ? -u[L.hface(i, 0)] : u[L.hface(i, L.ny)];
+            area = L.hx;
         }
-        __syncthreads();
-        if (threadIdx.x == 0)
-            for (int t = 0; t < 2 * TPB && base + t < nterms; ++t)
-                if (terms[t] >= 0.0) rate += terms[t];
-        __syncthreads();
+        if (un < 0.0) rate += -un * area * fin;
     }
+    rate = block_reduce_op(rate, [](double a, double b) { return a + b; }, 0.0, sh);
     if (threadIdx.x == 0) {
         sc->inj = rate;
         if (add_pvi) {
@@ -241,12 +237,9 @@ __global__ void k_kappa(Layout L, const double* __restrict__ K, const double* __
         part[4 * blockIdx.x + 3] = den.lo;
     }
     if (last_block_done(counter)) {
+        const DD n = reduce_dd_partials(part, gridDim.x, 0, shd);
+        const DD d = reduce_dd_partials(part, gridDim.x, 2, shd);
         if (threadIdx.x == 0) {
-            DD n{0.0, 0.0}, d{0.0, 0.0};
-            for (unsigned b = 0; b < gridDim.x; ++b) {
-                n = dd_add(n, DD{part[4 * b], part[4 * b + 1]});
-                d = dd_add(d, DD{part[4 * b + 2], part[4 * b + 3]});
-            }
             const double a = sqrt(n.hi);
             double e;
             if (eps_mode == 1) e = a;
@@ -350,12 +343,9 @@ __global__ void k_eps_fields(Layout L, const double* __restrict__ kn, const doub
         part[4 * blockIdx.x + 3] = den.lo;
     }
     if (last_block_done(counter)) {
+        const DD n = reduce_dd_partials(part, gridDim.x, 0, shd);
+        const DD d = reduce_dd_partials(part, gridDim.x, 2, shd);
         if (threadIdx.x == 0) {
-            DD n{0.0, 0.0}, d{0.0, 0.0};
-            for (unsigned b = 0; b < gridDim.x; ++b) {
-                n = dd_add(n, DD{part[4 * b], part[4 * b + 1]});
-                d = dd_add(d, DD{part[4 * b + 2], part[4 * b + 3]});
-            }
             const double a = sqrt(n.hi);
             if (mode == 1) sc->eps_pending = a;
             else {
