@@ -25,6 +25,13 @@ namespace mpm2p {
 
 constexpr unsigned FULL = 0xffffffffu;
 
+// Depth of the L prefetch ring in the sweeps: a divisor of B (ring slots stay
+// aligned with the chunk-unrolled step index).
+template <int B>
+__host__ __device__ constexpr int band_lq() {
+    return B <= 20 ? B : (B % 16 == 0 ? 16 : (B % 8 == 0 ? 8 : 4));
+}
+
 template <int B>
 __device__ __forceinline__ int band_j_of(int lane, int u) {  // window position of lane's row at pivot k0+u
     return (lane - u - 1 + 2 * B) % B;
@@ -131,15 +138,18 @@ __device__ void forward_reg(int n, const double* __restrict__ Lcol, double* __re
     double yv[NR];
 #pragma unroll
     for (int m = 0; m < NR; ++m) yv[m] = (act && lane < n && m < nr) ? Y[(size_t)m * ldy + lane] : 0.0;
-    double lc[B], ln[B], cb[NR], nbv[NR];
+    // L entries flow through an LQ-deep register ring (step k+LQ is loaded at step k)
+    constexpr int LQ = band_lq<B>();
+    auto lcol_at = [&](int k, int u) {  // lane's entry of Lcol[k], u = k mod B
+        return (act && k < n) ? Lcol[(size_t)k * B + band_j_of<B>(lane, u)] : 0.0;
+    };
+    double lq[LQ];
 #pragma unroll
-    for (int u = 0; u < B; ++u) lc[u] = act ? Lcol[(size_t)u * B + band_j_of<B>(lane, u)] : 0.0;
+    for (int t = 0; t < LQ; ++t) lq[t] = lcol_at(t, t % B);
+    double cb[NR], nbv[NR];
 #pragma unroll
     for (int m = 0; m < NR; ++m) cb[m] = (act && B + lane < n && m < nr) ? Y[(size_t)m * ldy + B + lane] : 0.0;
     for (int k0 = 0; k0 < n; k0 += B) {
-        const bool more = k0 + B < n;
-#pragma unroll
-        for (int u = 0; u < B; ++u) ln[u] = (act && more) ? Lcol[(size_t)(k0 + B + u) * B + band_j_of<B>(lane, u)] : 0.0;
         const int er = k0 + 2 * B + lane;
 #pragma unroll
         for (int m = 0; m < NR; ++m) nbv[m] = (act && er < n && m < nr) ? Y[(size_t)m * ldy + er] : 0.0;
@@ -147,6 +157,8 @@ __device__ void forward_reg(int n, const double* __restrict__ Lcol, double* __re
         for (int u = 0; u < B; ++u) {
             const int k = k0 + u;
             const bool piv = lane == u;
+            const double l = lq[u % LQ];
+            lq[u % LQ] = lcol_at(k + LQ, (u + LQ) % B);
             double yk[NR];
 #pragma unroll
             for (int m = 0; m < NR; ++m) yk[m] = __shfl_sync(FULL, yv[m], u);
@@ -158,10 +170,8 @@ __device__ void forward_reg(int n, const double* __restrict__ Lcol, double* __re
                 }
             }
 #pragma unroll
-            for (int m = 0; m < NR; ++m) yv[m] -= lc[u] * yk[m];
+            for (int m = 0; m < NR; ++m) yv[m] -= l * yk[m];
         }
-#pragma unroll
-        for (int u = 0; u < B; ++u) lc[u] = ln[u];
 #pragma unroll
         for (int m = 0; m < NR; ++m) cb[m] = nbv[m];
     }
@@ -180,13 +190,18 @@ __device__ void backward_reg(int n, const double* __restrict__ D, const double* 
 #pragma unroll
         for (int m = 0; m < NR; ++m) z[m] = (act && c >= 0 && m < nr) ? Y[(size_t)m * ldy + c] / dc : 0.0;
     }
-    double lc[B], ln[B], eb[NR], nbv[NR], ed, nd;
-    auto lrow_of = [&](int k0, int u) {  // lane's entry of Lrow[k0+u]: o = (lane - u) mod B
-        return Lrow[(size_t)(k0 + u) * B + (lane - u + B) % B];
+    constexpr int LQ = band_lq<B>();
+    auto lrow_at = [&](int k, int u) {  // lane's entry of Lrow[k]: o = (lane - u) mod B, u = k mod B
+        return (act && k >= 0) ? Lrow[(size_t)k * B + (lane - u + B) % B] : 0.0;
     };
+    double lq[LQ], eb[NR], nbv[NR], ed, nd;
     const int k0_last = n - B;
+    // ring slot of step k is (k mod LQ); prefill steps n-1 .. n-LQ
 #pragma unroll
-    for (int u = 0; u < B; ++u) lc[u] = act ? lrow_of(k0_last, u) : 0.0;
+    for (int t = 0; t < LQ; ++t) {
+        const int u = B - 1 - t;  // k = k0_last + u
+        lq[u % LQ] = lrow_at(k0_last + u, u);
+    }
     {
         const int er = k0_last - B + lane;
         const bool okr = act && er >= 0;
@@ -195,9 +210,6 @@ __device__ void backward_reg(int n, const double* __restrict__ D, const double* 
         for (int m = 0; m < NR; ++m) eb[m] = (okr && m < nr) ? Y[(size_t)m * ldy + er] : 0.0;
     }
     for (int k0 = k0_last; k0 >= 0; k0 -= B) {
-        const bool more = k0 - B >= 0;
-#pragma unroll
-        for (int u = 0; u < B; ++u) ln[u] = (act && more) ? lrow_of(k0 - B, u) : 0.0;
         {
             const int er = k0 - 2 * B + lane;
             const bool okr = act && er >= 0;
@@ -209,6 +221,8 @@ __device__ void backward_reg(int n, const double* __restrict__ D, const double* 
         for (int uu = B - 1; uu >= 0; --uu) {
             const int k = k0 + uu;
             const bool piv = lane == uu;
+            const double l = lq[uu % LQ];
+            lq[uu % LQ] = lrow_at(k - LQ, (uu + B - LQ % B) % B);
             double xk[NR];
 #pragma unroll
             for (int m = 0; m < NR; ++m) xk[m] = __shfl_sync(FULL, z[m], uu);
@@ -220,10 +234,8 @@ __device__ void backward_reg(int n, const double* __restrict__ D, const double* 
                 }
             }
 #pragma unroll
-            for (int m = 0; m < NR; ++m) z[m] -= lc[uu] * xk[m];
+            for (int m = 0; m < NR; ++m) z[m] -= l * xk[m];
         }
-#pragma unroll
-        for (int u = 0; u < B; ++u) lc[u] = ln[u];
         ed = nd;
 #pragma unroll
         for (int m = 0; m < NR; ++m) eb[m] = nbv[m];

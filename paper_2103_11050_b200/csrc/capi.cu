@@ -228,6 +228,7 @@ void create_ctx(mpm2p_ctx* ctx, const mpm2p_problem* P) {
     }
     c.anchor_m = (L.n_iface == 0) && pure_neumann;
     c.repair_active = L.n_sub > 1 || c.grounded;
+    if (const char* e = std::getenv("MPM2P_NO_GRAPHS")) c.use_graphs = e[0] != 0 && e[0] == '0';
 
     int dev = 0;
     CK(cudaGetDevice(&dev));
@@ -376,6 +377,7 @@ void run_begin(mpm2p_ctx* ctx, const mpm2p_split* sp, const double* s0, mpm2p_st
     d.rec.n_sub = c.L.n_sub;
     d.rec.min_eps_margin = INFINITY;
     c.c_hom = c.c_part = c.c_down = c.c_fine = c.c_iface = 0;
+    c.drop_graphs();
     reset_scalars(c);
     const auto t0 = std::chrono::steady_clock::now();
     upload(c, c.s, s0, c.L.cells());
@@ -411,24 +413,69 @@ bool run_step(mpm2p_ctx* ctx, mpm2p_step_record* out) {
     if (sp.stop_on_breakthrough && d.rec.breakthrough_step >= 0) return false;
     if (d.n >= sp.max_steps_hard) return false;
     const auto t0 = std::chrono::steady_clock::now();
-    launch_cfl(c, c.u, sp.cfl_safety, sp.dt_cap);
-    launch_inj_pvi(c, c.u, sp.inflow_sat, sp.cn, true);
-    for (int k = 0; k < sp.cn; ++k) {
-        launch_upwind(c, c.s, c.s2, c.u, sp.inflow_sat);
-        std::swap(c.s.p, c.s2.p);
-    }
-    const int eps_mode = sp.eta_mode;
-    launch_conductivity(c, c.s, c.kappa_n, eps_mode, true);
     const int rebuilt = d.rebuild_next;
-    if (rebuilt) {
-        ++d.ell;
-        launch_rebuild(c, c.kappa_n);
-        launch_lambda(c, c.s, c.lam_reb);
+    if (rebuilt) ++d.ell;
+    // One Algorithm-1 iteration is a fixed kernel sequence per branch; it is
+    // captured once per run as a CUDA graph (MPM-2P reuse / MRCM rebuild) and
+    // replayed, so the device runs the ~30 kernels back to back. Profiling
+    // mode launches them eagerly so each kernel can be timed.
+    auto body = [&] {
+        launch_cfl(c, c.u, sp.cfl_safety, sp.dt_cap);
+        launch_inj_pvi(c, c.u, sp.inflow_sat, sp.cn, true);
+        for (int k = 0; k < sp.cn; ++k) {
+            launch_upwind(c, k % 2 == 0 ? c.s : c.s2, k % 2 == 0 ? c.s2 : c.s, c.u, sp.inflow_sat);
+        }
+        if (sp.cn % 2 == 1)
+            CK(cudaMemcpyAsync(c.s.p, c.s2.p, c.L.cells() * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
+        launch_conductivity(c, c.s, c.kappa_n, sp.eta_mode, true);
+        if (rebuilt) {
+            launch_rebuild(c, c.kappa_n);
+            launch_lambda(c, c.s, c.lam_reb);
+        } else {
+            launch_mpm(c, c.kappa_n);
+        }
+        launch_decide(c, rebuilt, sp.method, sp.eta, 1);
+        launch_outlet(c, c.s, c.u);
+    };
+    if (c.profiling || !c.use_graphs) {
+        body();
     } else {
-        launch_mpm(c, c.kappa_n);
+        cudaGraphExec_t& g = rebuilt ? c.g_rebuild : c.g_mpm;
+        long long* delta = rebuilt ? c.gd_rebuild : c.gd_mpm;
+        if (!g) {
+            const long long before[5] = {c.c_hom, c.c_part, c.c_down, c.c_fine, c.c_iface};
+            const long long launches_before = c.launch_count;
+            CK(cudaStreamBeginCapture(c.st, cudaStreamCaptureModeThreadLocal));
+            try {
+                body();
+            } catch (...) {
+                cudaGraph_t dummy = nullptr;
+                cudaStreamEndCapture(c.st, &dummy);
+                if (dummy) cudaGraphDestroy(dummy);
+                throw;
+            }
+            cudaGraph_t graph = nullptr;
+            CK(cudaStreamEndCapture(c.st, &graph));
+            CK(cudaGraphInstantiate(&g, graph, 0));
+            CK(cudaGraphDestroy(graph));
+            const long long after[5] = {c.c_hom, c.c_part, c.c_down, c.c_fine, c.c_iface};
+            for (int i = 0; i < 5; ++i) delta[i] = after[i] - before[i];
+            delta[5] = c.launch_count - launches_before;
+            c.c_hom = before[0];
+            c.c_part = before[1];
+            c.c_down = before[2];
+            c.c_fine = before[3];
+            c.c_iface = before[4];
+            c.launch_count = launches_before;
+        }
+        CK(cudaGraphLaunch(g, c.st));
+        c.c_hom += delta[0];
+        c.c_part += delta[1];
+        c.c_down += delta[2];
+        c.c_fine += delta[3];
+        c.c_iface += delta[4];
+        c.launch_count += delta[5];
     }
-    launch_decide(c, rebuilt, sp.method, sp.eta, (int)d.n);
-    launch_outlet(c, c.s, c.u);
     const Scalars& s = sync_scalars(c);
     note(d, s);
     const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -500,6 +547,7 @@ void mpm2p_destroy(mpm2p_ctx* ctx) {
     for (cudaEvent_t e : ctx->c.event_pool) cudaEventDestroy(e);
     for (cudaEvent_t e : ctx->c.timers)
         if (e) cudaEventDestroy(e);
+    ctx->c.drop_graphs();
     cudaStream_t st = ctx->c.st;
     delete ctx;
     if (st) cudaStreamDestroy(st);

@@ -98,6 +98,15 @@ struct Ctx {
     Scalars* sc_host = nullptr;  // pinned
 
     int iface_sym = -1;  // J*M symmetric (pivot-free inverse)? -1 unknown
+    // per-run CUDA graphs of one driver step (MPM-2P reuse / MRCM rebuild)
+    bool use_graphs = true;
+    cudaGraphExec_t g_mpm = nullptr, g_rebuild = nullptr;
+    long long gd_mpm[6] = {}, gd_rebuild[6] = {};  // counter / launch deltas per replay
+    void drop_graphs() {
+        if (g_mpm) cudaGraphExecDestroy(g_mpm);
+        if (g_rebuild) cudaGraphExecDestroy(g_rebuild);
+        g_mpm = g_rebuild = nullptr;
+    }
     bool has_basis = false;
     bool has_factor = false;
     double rcond = 0.0;

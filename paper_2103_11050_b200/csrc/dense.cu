@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(GJ_THREADS) k_gauss_jordan(GJArgs a) {
 }
 
 // ---- pivot-free blocked Gauss-Jordan (symmetric quasi-definite / SPD) -----
-// In-place inversion of W (n x n). For each diagonal block p (pb <= 16):
+// In-place inversion of W (n x n). For each diagonal block p (pb <= 32):
 //   A: every CTA inverts W_pp redundantly in shared memory (P = W_pp^-1),
 //      then a slice of Rbuf = P W_p,: (new block row) and Cbuf = W_:,p (old
 //      block column);
@@ -215,58 +215,59 @@ __global__ void __launch_bounds__(GJ_THREADS) k_gauss_jordan(GJArgs a) {
 struct BGJArgs {
     double* W;
     int n;
-    double* Rbuf;  // 16 x n
-    double* Cbuf;  // n x 16
+    double* Rbuf;  // 32 x n
+    double* Cbuf;  // n x 32
     int* singular;
 };
 
+constexpr int GJB = 32;  // diagonal block width
+
 __global__ void __launch_bounds__(256) k_block_gj(BGJArgs a) {
     cg::grid_group grid = cg::this_grid();
-    __shared__ double P[16][17];
-    __shared__ double sg[64 * 16];
-    __shared__ double sr[16 * 128];
+    extern __shared__ double dsm[];
+    double (*P)[GJB + 1] = reinterpret_cast<double (*)[GJB + 1]>(dsm);  // 32 x 33
+    double* sg = dsm + GJB * (GJB + 1);                                // 64 x 32 tile of Cbuf
+    double* sr = sg + 64 * GJB;                                        // 32 x 128 tile of Rbuf
     const int n = a.n, tid = threadIdx.x, nt = blockDim.x;
-    for (int p0 = 0; p0 < n; p0 += 16) {
-        const int pb = n - p0 < 16 ? n - p0 : 16;
-        // ---- phase A: invert the diagonal block (every CTA) -----------------
-        {
-            const int r = tid / 16, cc = tid % 16;
-            if (r < pb && cc < pb) P[r][cc] = a.W[(size_t)(p0 + r) * n + p0 + cc];
+    const long long gtid = (long long)blockIdx.x * nt + tid, gnt = (long long)gridDim.x * nt;
+    for (int p0 = 0; p0 < n; p0 += GJB) {
+        const int pb = n - p0 < GJB ? n - p0 : GJB;
+        // ---- phase A: every CTA inverts the diagonal block ------------------
+        for (int x = tid; x < GJB * GJB; x += nt) {
+            const int r = x / GJB, cc = x % GJB;
+            P[r][cc] = (r < pb && cc < pb) ? a.W[(size_t)(p0 + r) * n + p0 + cc] : (r == cc ? 1.0 : 0.0);
+        }
+        __syncthreads();
+        for (int k = 0; k < pb; ++k) {
+            const double piv = P[k][k];
+            const double pinv = 1.0 / piv;
+            double f[4], rk[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int x = tid + q * 256, r = x / GJB, cc = x % GJB;
+                f[q] = P[r][k];
+                rk[q] = P[k][cc];
+            }
             __syncthreads();
-            for (int k = 0; k < pb; ++k) {
-                const double piv = P[k][k];
-                double f = 0.0, rk = 0.0;
-                if (r < pb && cc < pb) {
-                    f = P[r][k];
-                    rk = P[k][cc];
-                }
-                __syncthreads();
-                if (r < pb && cc < pb) {
-                    const double pinv = 1.0 / piv;
-                    if (r == k) P[r][cc] = (cc == k) ? pinv : rk * pinv;
-                    else P[r][cc] = (cc == k) ? -f * pinv : P[r][cc] - f * pinv * rk;
-                }
-                if (blockIdx.x == 0 && tid == 0 && (!(piv != 0.0) || !isfinite(piv))) *a.singular = 1;
-                __syncthreads();
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int x = tid + q * 256, r = x / GJB, cc = x % GJB;
+                if (r == k) P[r][cc] = (cc == k) ? pinv : rk[q] * pinv;
+                else P[r][cc] = (cc == k) ? -f[q] * pinv : P[r][cc] - f[q] * pinv * rk[q];
             }
+            if (blockIdx.x == 0 && tid == 0 && (!(piv != 0.0) || !isfinite(piv))) *a.singular = 1;
+            __syncthreads();
         }
-        // slices: new block row Rbuf = P * W[p, :] and old block column Cbuf
-        for (int j = blockIdx.x * nt + tid; j < n; j += gridDim.x * nt) {
-            if (j >= p0 && j < p0 + pb) continue;
-            double wcol[16];
-#pragma unroll
-            for (int c = 0; c < 16; ++c) wcol[c] = c < pb ? a.W[(size_t)(p0 + c) * n + j] : 0.0;
-#pragma unroll
-            for (int r = 0; r < 16; ++r) {
-                double acc = 0.0;
-#pragma unroll
-                for (int c = 0; c < 16; ++c)
-                    if (r < pb && c < pb) acc += P[r][c] * wcol[c];
-                if (r < pb) a.Rbuf[(size_t)r * n + j] = acc;
-            }
+        // new block row Rbuf = P W[p, :] (one thread per (r, j)), old block column Cbuf
+        for (long long x = gtid; x < (long long)GJB * n; x += gnt) {
+            const int r = (int)(x / n), j = (int)(x % n);
+            if (r >= pb || (j >= p0 && j < p0 + pb)) continue;
+            double acc = 0.0;
+            for (int c = 0; c < pb; ++c) acc += P[r][c] * a.W[(size_t)(p0 + c) * n + j];
+            a.Rbuf[(size_t)r * n + j] = acc;
         }
-        for (int x = blockIdx.x * nt + tid; x < n * 16; x += gridDim.x * nt) {
-            const int i = x / 16, c = x % 16;
+        for (long long x = gtid; x < (long long)n * GJB; x += gnt) {
+            const int i = (int)(x / GJB), c = (int)(x % GJB);
             a.Cbuf[x] = (c < pb && (i < p0 || i >= p0 + pb)) ? a.W[(size_t)i * n + p0 + c] : 0.0;
         }
         grid.sync();
@@ -276,11 +277,11 @@ __global__ void __launch_bounds__(256) k_block_gj(BGJArgs a) {
         for (int tile = blockIdx.x; tile < tr * tc; tile += gridDim.x) {
             const int i0 = (tile / tc) * 64, j0 = (tile % tc) * 128;
             __syncthreads();
-            for (int x = tid; x < 64 * 16; x += nt) {
-                const int i = i0 + x / 16;
-                sg[x] = i < n ? a.Cbuf[(size_t)i * 16 + x % 16] : 0.0;
+            for (int x = tid; x < 64 * GJB; x += nt) {
+                const int i = i0 + x / GJB;
+                sg[x] = i < n ? a.Cbuf[(size_t)i * GJB + x % GJB] : 0.0;
             }
-            for (int x = tid; x < 16 * 128; x += nt) {
+            for (int x = tid; x < GJB * 128; x += nt) {
                 const int c = x / 128, j = j0 + x % 128;
                 sr[x] = (c < pb && j < n && (j < p0 || j >= p0 + pb)) ? a.Rbuf[(size_t)c * n + j] : 0.0;
             }
@@ -290,11 +291,11 @@ __global__ void __launch_bounds__(256) k_block_gj(BGJArgs a) {
             for (int q = 0; q < 4; ++q)
 #pragma unroll
                 for (int t = 0; t < 8; ++t) acc[q][t] = 0.0;
-#pragma unroll
-            for (int c = 0; c < 16; ++c) {
+#pragma unroll 8
+            for (int c = 0; c < GJB; ++c) {
                 double gv[4], rv[8];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) gv[q] = sg[(ty + 16 * q) * 16 + c];
+                for (int q = 0; q < 4; ++q) gv[q] = sg[(ty + 16 * q) * GJB + c];
 #pragma unroll
                 for (int t = 0; t < 8; ++t) rv[t] = sr[c * 128 + tx + 16 * t];
 #pragma unroll
@@ -317,7 +318,7 @@ __global__ void __launch_bounds__(256) k_block_gj(BGJArgs a) {
                     else if (ip && !jp) *w = sr[(i - p0) * 128 + (j - j0)];
                     else if (!ip && jp) {
                         double v = 0.0;
-                        for (int c = 0; c < pb; ++c) v -= sg[(i - i0) * 16 + c] * P[c][j - p0];
+                        for (int c = 0; c < pb; ++c) v -= sg[(i - i0) * GJB + c] * P[c][j - p0];
                         *w = v;
                     } else {
                         *w = P[i - p0][j - p0];
@@ -328,6 +329,9 @@ __global__ void __launch_bounds__(256) k_block_gj(BGJArgs a) {
         grid.sync();
     }
 }
+
+constexpr size_t GJB_SMEM = (GJB * (GJB + 1) + 64 * GJB + GJB * 128) * sizeof(double);
+
 
 // K = J M: phi-rows first, then the negated psi-rows.
 __global__ void k_j_times(const double* __restrict__ M, double* __restrict__ K, int n) {
@@ -433,9 +437,16 @@ __global__ void k_gemv(const double* __restrict__ A, const double* __restrict__ 
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (gw >= n) return;
     const double* row = A + (size_t)gw * n;
-    double v = 0.0;
-    for (int j = lane; j < n; j += 32) v += row[j] * x[j];
-    v = warp_sum(v);
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;  // 4 loads in flight per lane
+    int j = lane;
+    for (; j + 96 < n; j += 128) {
+        v0 += __ldg(row + j) * __ldg(x + j);
+        v1 += __ldg(row + j + 32) * __ldg(x + j + 32);
+        v2 += __ldg(row + j + 64) * __ldg(x + j + 64);
+        v3 += __ldg(row + j + 96) * __ldg(x + j + 96);
+    }
+    for (; j < n; j += 32) v0 += __ldg(row + j) * __ldg(x + j);
+    const double v = warp_sum((v0 + v1) + (v2 + v3));
     if (lane == 0) y[gw] = v;
 }
 
@@ -459,19 +470,24 @@ __global__ void k_axpy(double* __restrict__ y, const double* __restrict__ x, int
 namespace {
 
 void block_gj_inplace(Ctx& c, double* W, int n) {
-    c.gj_col.alloc(std::max(c.gj_col.n, (size_t)n * 16));
-    c.gj_row.alloc(std::max(c.gj_row.n, (size_t)n * 16));
+    c.gj_col.alloc(std::max(c.gj_col.n, (size_t)n * GJB));
+    c.gj_row.alloc(std::max(c.gj_row.n, (size_t)n * GJB));
+    static bool attr_set = false;  // set once, outside any graph capture
+    if (!attr_set) {
+        CK(cudaFuncSetAttribute(k_block_gj, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GJB_SMEM));
+        attr_set = true;
+    }
     c.gj_piv.alloc(std::max(c.gj_piv.n, (size_t)n + 1));
     CK(cudaMemsetAsync(c.gj_piv.p + n, 0, sizeof(int), c.st));
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_block_gj, 256, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_block_gj, 256, GJB_SMEM));
     if (per_sm < 1) throw CudaError("dense_inverse: block Gauss-Jordan does not fit on an SM");
     const int tiles = cdiv(n, 64) * cdiv(n, 128);
     const int blocks = std::min(per_sm * c.num_sms, std::max(c.num_sms, tiles));
     BGJArgs ga{W, n, c.gj_row.p, c.gj_col.p, c.gj_piv.p + n};
     void* args[] = {&ga};
     PROF(c, "k_block_gj");
-    CK(cudaLaunchCooperativeKernel((void*)k_block_gj, blocks, 256, args, 0, c.st));
+    CK(cudaLaunchCooperativeKernel((void*)k_block_gj, blocks, 256, args, GJB_SMEM, c.st));
     CK_LAUNCH();
 }
 

@@ -400,7 +400,8 @@ __global__ void k_csr_to_dense(const int* __restrict__ ptr, const int* __restric
 // Interface rhs from the particular traces (mrcm.cpp:80-100).
 __global__ void k_iface_rhs(Layout L, const double* __restrict__ PU, const double* __restrict__ bm,
                             const double* __restrict__ bp, double* __restrict__ rhs) {
-    const int row = blockIdx.x * blockDim.x + threadIdx.x;
+    // one warp per row; lanes stride the (side, position) terms
+    const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     const int np = L.dim_flux;
     if (row >= 2 * np) return;
     const bool phi = row >= np;
@@ -410,10 +411,11 @@ __global__ void k_iface_rhs(Layout L, const double* __restrict__ PU, const doubl
     const int ne = L.iface_edges(k);
     const double len = k < L.NV ? L.hy : L.hx;
     double acc = 0.0;
-    for (int a = 0; a < 2; ++a) {
-        const int s = a == 0 ? L.iface_minus(k) : L.iface_plus(k);
-        const double sign = a == 0 ? 1.0 : -1.0;
-        for (int pos = 0; pos < ne; ++pos) {
+    for (int t = lane; t < 2 * ne; t += 32) {
+        const int a = t / ne, pos = t % ne;
+        {
+            const int s = a == 0 ? L.iface_minus(k) : L.iface_plus(k);
+            const double sign = a == 0 ? 1.0 : -1.0;
             const int idx = L.edge_index_on_iface(s, k, pos);
             const double un = PU[(size_t)s * L.nbe + idx];
             const double v = L.basis_val(k, rt, pos);
@@ -425,7 +427,8 @@ __global__ void k_iface_rhs(Layout L, const double* __restrict__ PU, const doubl
             }
         }
     }
-    rhs[row] = acc;
+    acc = warp_sum(acc);
+    if (lane == 0) rhs[row] = acc;
 }
 
 // ---------------------------------------------------------------- K8 ----
@@ -519,12 +522,13 @@ __global__ void k_skel(Layout L, const double* __restrict__ RU, double* __restri
 __global__ void k_resid(Layout L, const double* __restrict__ skel, const double* __restrict__ RU,
                         const double* __restrict__ qsum, double* __restrict__ resid, Scalars* sc, double* part,
                         unsigned* counter) {
+    // one warp per subdomain; lanes stride the boundary edges (W,E,S,N order)
     __shared__ double sh[32];
-    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     double fmaxv = 0.0;
     if (s < L.n_sub) {
         double outflow = 0.0;
-        for (int idx = 0; idx < L.nbe; ++idx) {
+        for (int idx = lane; idx < L.nbe; idx += 32) {
             const EdgeInfo e = L.edge(s, idx);
             double un;
             if (e.iface >= 0) {
@@ -536,7 +540,8 @@ __global__ void k_resid(Layout L, const double* __restrict__ skel, const double*
             }
             outflow += un * e.area;
         }
-        resid[s] = qsum[s] - outflow;
+        outflow = warp_sum(outflow);
+        if (lane == 0) resid[s] = qsum[s] - outflow;
     }
     fmaxv = block_max(fmaxv, sh);
     if (threadIdx.x == 0) part[blockIdx.x] = fmaxv;
@@ -709,9 +714,14 @@ __global__ void __launch_bounds__(WPB * 32) k_part_solve_r(Layout L, int max_rhs
     backward_reg<B, 1>(n, D + so, Lr + so * B, x, 1, n);
 }
 
-constexpr int NR_REG = 8;
-
+// RHS carried through one register sweep of the rebuild (1 particular + up to
+// 8 homogeneous for constant H-bar = H; 16 for linear / H/2 spaces).
 template <int B>
+constexpr int rebuild_nr(int max_rhs) {
+    return (B <= 16 && max_rhs > 9) ? 17 : 9;
+}
+
+template <int B, int NR_REG>
 __global__ void __launch_bounds__(WPB * 32) k_factor_solve_r(Layout L, int max_rhs, const double* __restrict__ BD,
                                                              const double* __restrict__ BW,
                                                              const double* __restrict__ BS, double* __restrict__ D,
@@ -1042,7 +1052,7 @@ void downscale(Ctx& c, const double* kappa) {
     }
     {
         PROF(c, "k_resid");
-        k_resid<<<grid_for(L.n_sub), TPB, 0, c.st>>>(L, c.skel, c.RU, c.qsum_sub, c.resid, c.sc, c.red, c.red_count);
+        k_resid<<<grid_for(32LL * L.n_sub), TPB, 0, c.st>>>(L, c.skel, c.RU, c.qsum_sub, c.resid, c.sc, c.red, c.red_count);
         CK_LAUNCH();
     }
     if (c.repair_active) {
@@ -1101,7 +1111,7 @@ void interface_solve(Ctx& c) {
     if (c.dim == 0) return;
     {
         PROF(c, "k_iface_rhs");
-        k_iface_rhs<<<grid_for(c.dim), TPB, 0, c.st>>>(L, c.PU, c.beta_m, c.beta_p, c.irhs);
+        k_iface_rhs<<<grid_for(32LL * c.dim), TPB, 0, c.st>>>(L, c.PU, c.beta_m, c.beta_p, c.irhs);
         CK_LAUNCH();
     }
     launch_gemv(c, c.Minv, c.irhs, c.icoef, c.dim);
@@ -1141,10 +1151,14 @@ void launch_rebuild(Ctx& c, const double* kappa, bool compute_beta) {  // comput
     {
         PROF(c, "k_factor_solve");
         switch (L.snx) {
-#define X(BW_)                                                                                                  \
-    case BW_:                                                                                                   \
-        k_factor_solve_r<BW_><<<band_blocks(L), WPB * 32, 0, c.st>>>(L, c.max_rhs, c.BDm, c.BWm, c.BSm, c.Dm, \
-                                                                      c.Lcm, c.Lrm, c.X, c.sc);               \
+#define X(BW_)                                                                                                      \
+    case BW_:                                                                                                       \
+        if (rebuild_nr<BW_>(c.max_rhs) == 17)                                                                       \
+            k_factor_solve_r<BW_, (BW_ <= 16 ? 17 : 9)><<<band_blocks(L), WPB * 32, 0, c.st>>>(                    \
+                L, c.max_rhs, c.BDm, c.BWm, c.BSm, c.Dm, c.Lcm, c.Lrm, c.X, c.sc);                                   \
+        else                                                                                                        \
+            k_factor_solve_r<BW_, 9><<<band_blocks(L), WPB * 32, 0, c.st>>>(L, c.max_rhs, c.BDm, c.BWm, c.BSm,     \
+                                                                           c.Dm, c.Lcm, c.Lrm, c.X, c.sc);          \
         break;
             MPM2P_BAND_WIDTHS(X)
 #undef X
