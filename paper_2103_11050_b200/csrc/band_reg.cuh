@@ -60,22 +60,30 @@ __device__ bool factor_fwd_reg(int n, const BandRows A, double* __restrict__ D, 
 #pragma unroll
     for (int m = 0; m < NR; ++m) yv[m] = (act && lane < n && m < nr) ? Y[(size_t)m * ldy + lane] : 0.0;
     for (int x = lane; x < B * B; x += 32) stage[x] = 0.0;
-    // entering-row data for the first chunk: row B + lane
+    // entering-row data for the first chunk: row B + lane. Loads use clamped
+    // (always valid) indices and a select, so the step body has no branches.
     auto fetch = [&](int row, double& fd, double& fw, double& fs, double* fb) {
         const bool ok = act && row < n;
-        fd = ok ? A.diag[row] : 0.0;
-        fw = ok ? A.offw[row] : 0.0;
-        fs = ok ? A.offs[row] : 0.0;
+        const int rr = row < n ? row : n - 1;
+        const double vd = A.diag[rr], vw = A.offw[rr], vs = A.offs[rr];
+        fd = ok ? vd : 0.0;
+        fw = ok ? vw : 0.0;
+        fs = ok ? vs : 0.0;
 #pragma unroll
-        for (int m = 0; m < NR; ++m) fb[m] = (ok && m < nr) ? Y[(size_t)m * ldy + row] : 0.0;
+        for (int m = 0; m < NR; ++m) {
+            const double v = Y[(size_t)(m < nr ? m : nr - 1) * ldy + rr];
+            fb[m] = (ok && m < nr) ? v : 0.0;
+        }
     };
     double cd, cw, cs, cb[NR];
     fetch(B + lane, cd, cw, cs, cb);
     bool ok = true;
+    const bool has_lcol = Lcol != nullptr;
     __syncwarp();
     for (int k0 = 0; k0 < n; k0 += B) {
         double nd, nw, ns, nbv[NR];
         fetch(k0 + 2 * B + lane, nd, nw, ns, nbv);
+        const bool ent_chunk = k0 + 2 * B <= n;  // every row k+B of this chunk exists
 #pragma unroll
         for (int u = 0; u < B; ++u) {
             const int k = k0 + u;
@@ -84,41 +92,31 @@ __device__ bool factor_fwd_reg(int n, const BandRows A, double* __restrict__ D, 
             double yk[NR];
 #pragma unroll
             for (int m = 0; m < NR; ++m) yk[m] = __shfl_sync(FULL, yv[m], u);
-            if (piv) {
-                D[k] = d;
+            if (piv) D[k] = d;
 #pragma unroll
-                for (int m = 0; m < NR; ++m)
-                    if (m < nr) Y[(size_t)m * ldy + k] = yk[m];
-            }
+            for (int m = 0; m < NR; ++m)
+                if (piv && m < nr) Y[(size_t)m * ldy + k] = yk[m];
             if (act) Lrow[(size_t)k * B + lane] = stage[u * B + lane];
             __syncwarp();
-            if (!(d > 0.0)) ok = false;
-            const bool ent = k + B < n;
+            ok = ok && (d > 0.0);
+            // pivot lane: row k leaves, row k+B enters (its coupling to column k is c)
+            const bool ent = ent_chunk;
             const double c = piv ? (ent ? -cs : 0.0) : reg[u];
-            if (piv) {
-#pragma unroll
-                for (int t = 0; t < B; ++t) reg[t] = 0.0;
-                if (ent) {
-                    reg[(u + B - 1) % B] = -cw;
-                    reg[u] = cd;
-                }
-#pragma unroll
-                for (int m = 0; m < NR; ++m) yv[m] = ent ? cb[m] : 0.0;
-            }
-            const double l = c * (1.0 / d);
+            const double keep = piv ? 0.0 : 1.0;
+            const double fd_ = (piv && ent) ? cd : 0.0, fw_ = (piv && ent) ? -cw : 0.0;
+            const double l = c * fast_rcp(d);
             const int j = band_j_of<B>(lane, u);
-            if (act) {
-                if (Lcol) Lcol[(size_t)k * B + j] = l;
-                stage[lane * B + (B - 1 - j)] = l;
-            }
+            if (act && has_lcol) Lcol[(size_t)k * B + j] = l;
+            if (act) stage[lane * B + (B - 1 - j)] = l;
 #pragma unroll
             for (int i = 0; i < B; ++i) {
                 const int ci = (u + 1 + i) % B;
                 const double a = __shfl_sync(FULL, c, ci);
-                reg[ci] -= l * a;
+                const double fresh = (ci == u) ? fd_ : ((ci == (u + B - 1) % B) ? fw_ : 0.0);
+                reg[ci] = fma(-l, a, fma(reg[ci], keep, fresh));
             }
 #pragma unroll
-            for (int m = 0; m < NR; ++m) yv[m] -= l * yk[m];
+            for (int m = 0; m < NR; ++m) yv[m] = fma(-l, yk[m], fma(yv[m], keep, (piv && ent) ? cb[m] : 0.0));
             __syncwarp();
         }
         cd = nd;
@@ -135,42 +133,43 @@ template <int B, int NR>
 __device__ void forward_reg(int n, const double* __restrict__ Lcol, double* __restrict__ Y, int nr, int ldy) {
     const int lane = threadIdx.x & 31;
     const bool act = lane < B;
+    auto yat = [&](int m, int row) {  // clamped (always valid) load + select
+        const double v = Y[(size_t)(m < nr ? m : nr - 1) * ldy + (row < n ? row : n - 1)];
+        return (act && row < n && m < nr) ? v : 0.0;
+    };
     double yv[NR];
 #pragma unroll
-    for (int m = 0; m < NR; ++m) yv[m] = (act && lane < n && m < nr) ? Y[(size_t)m * ldy + lane] : 0.0;
+    for (int m = 0; m < NR; ++m) yv[m] = yat(m, lane);
     // L entries flow through an LQ-deep register ring (step k+LQ is loaded at step k)
     constexpr int LQ = band_lq<B>();
     auto lcol_at = [&](int k, int u) {  // lane's entry of Lcol[k], u = k mod B
-        return (act && k < n) ? Lcol[(size_t)k * B + band_j_of<B>(lane, u)] : 0.0;
+        const double v = Lcol[(size_t)(k < n ? k : n - 1) * B + band_j_of<B>(lane, u)];
+        return (act && k < n) ? v : 0.0;
     };
     double lq[LQ];
 #pragma unroll
     for (int t = 0; t < LQ; ++t) lq[t] = lcol_at(t, t % B);
     double cb[NR], nbv[NR];
 #pragma unroll
-    for (int m = 0; m < NR; ++m) cb[m] = (act && B + lane < n && m < nr) ? Y[(size_t)m * ldy + B + lane] : 0.0;
+    for (int m = 0; m < NR; ++m) cb[m] = yat(m, B + lane);
     for (int k0 = 0; k0 < n; k0 += B) {
-        const int er = k0 + 2 * B + lane;
 #pragma unroll
-        for (int m = 0; m < NR; ++m) nbv[m] = (act && er < n && m < nr) ? Y[(size_t)m * ldy + er] : 0.0;
+        for (int m = 0; m < NR; ++m) nbv[m] = yat(m, k0 + 2 * B + lane);
 #pragma unroll
         for (int u = 0; u < B; ++u) {
             const int k = k0 + u;
             const bool piv = lane == u;
+            const double keep = piv ? 0.0 : 1.0;
             const double l = lq[u % LQ];
             lq[u % LQ] = lcol_at(k + LQ, (u + LQ) % B);
             double yk[NR];
 #pragma unroll
             for (int m = 0; m < NR; ++m) yk[m] = __shfl_sync(FULL, yv[m], u);
-            if (piv) {
 #pragma unroll
-                for (int m = 0; m < NR; ++m) {
-                    if (m < nr) Y[(size_t)m * ldy + k] = yk[m];
-                    yv[m] = cb[m];
-                }
+            for (int m = 0; m < NR; ++m) {
+                if (piv && m < nr) Y[(size_t)m * ldy + k] = yk[m];
+                yv[m] = fma(-l, yk[m], fma(yv[m], keep, piv ? cb[m] : 0.0));
             }
-#pragma unroll
-            for (int m = 0; m < NR; ++m) yv[m] -= l * yk[m];
         }
 #pragma unroll
         for (int m = 0; m < NR; ++m) cb[m] = nbv[m];
@@ -183,18 +182,25 @@ __device__ void backward_reg(int n, const double* __restrict__ D, const double* 
                              double* __restrict__ Y, int nr, int ldy) {
     const int lane = threadIdx.x & 31;
     const bool act = lane < B;
-    double z[NR];
-    {
-        const int c = n - B + lane;  // c == lane (mod B)
-        const double dc = (act && c >= 0) ? D[c] : 1.0;
+    // entering value z = y / d of row `row` (0 outside the matrix); clamped loads
+    auto zat = [&](int row, double* out) {
+        const bool ok = act && row >= 0;
+        const int rr = ok ? row : 0;  // lanes >= B would address past the subdomain
+        const double dinv = 1.0 / D[rr];
 #pragma unroll
-        for (int m = 0; m < NR; ++m) z[m] = (act && c >= 0 && m < nr) ? Y[(size_t)m * ldy + c] / dc : 0.0;
-    }
+        for (int m = 0; m < NR; ++m) {
+            const double v = Y[(size_t)(m < nr ? m : nr - 1) * ldy + rr];
+            out[m] = (ok && m < nr) ? v * dinv : 0.0;
+        }
+    };
+    double z[NR];
+    zat(n - B + lane, z);  // row n-B+lane == lane (mod B)
     constexpr int LQ = band_lq<B>();
     auto lrow_at = [&](int k, int u) {  // lane's entry of Lrow[k]: o = (lane - u) mod B, u = k mod B
-        return (act && k >= 0) ? Lrow[(size_t)k * B + (lane - u + B) % B] : 0.0;
+        const double v = Lrow[(size_t)(k >= 0 ? k : 0) * B + (lane - u + B) % B];
+        return (act && k >= 0) ? v : 0.0;
     };
-    double lq[LQ], eb[NR], nbv[NR], ed, nd;
+    double lq[LQ], ez[NR], nz[NR];
     const int k0_last = n - B;
     // ring slot of step k is (k mod LQ); prefill steps n-1 .. n-LQ
 #pragma unroll
@@ -202,43 +208,27 @@ __device__ void backward_reg(int n, const double* __restrict__ D, const double* 
         const int u = B - 1 - t;  // k = k0_last + u
         lq[u % LQ] = lrow_at(k0_last + u, u);
     }
-    {
-        const int er = k0_last - B + lane;
-        const bool okr = act && er >= 0;
-        ed = okr ? D[er] : 1.0;
-#pragma unroll
-        for (int m = 0; m < NR; ++m) eb[m] = (okr && m < nr) ? Y[(size_t)m * ldy + er] : 0.0;
-    }
+    zat(k0_last - B + lane, ez);
     for (int k0 = k0_last; k0 >= 0; k0 -= B) {
-        {
-            const int er = k0 - 2 * B + lane;
-            const bool okr = act && er >= 0;
-            nd = okr ? D[er] : 1.0;
-#pragma unroll
-            for (int m = 0; m < NR; ++m) nbv[m] = (okr && m < nr) ? Y[(size_t)m * ldy + er] : 0.0;
-        }
+        zat(k0 - 2 * B + lane, nz);
 #pragma unroll
         for (int uu = B - 1; uu >= 0; --uu) {
             const int k = k0 + uu;
             const bool piv = lane == uu;
+            const double keep = piv ? 0.0 : 1.0;
             const double l = lq[uu % LQ];
             lq[uu % LQ] = lrow_at(k - LQ, (uu + B - LQ % B) % B);
             double xk[NR];
 #pragma unroll
             for (int m = 0; m < NR; ++m) xk[m] = __shfl_sync(FULL, z[m], uu);
-            if (piv) {
 #pragma unroll
-                for (int m = 0; m < NR; ++m) {
-                    if (m < nr) Y[(size_t)m * ldy + k] = xk[m];
-                    z[m] = (k - B >= 0) ? eb[m] / ed : 0.0;
-                }
+            for (int m = 0; m < NR; ++m) {
+                if (piv && m < nr) Y[(size_t)m * ldy + k] = xk[m];
+                z[m] = fma(-l, xk[m], fma(z[m], keep, piv ? ez[m] : 0.0));
             }
-#pragma unroll
-            for (int m = 0; m < NR; ++m) z[m] -= l * xk[m];
         }
-        ed = nd;
 #pragma unroll
-        for (int m = 0; m < NR; ++m) eb[m] = nbv[m];
+        for (int m = 0; m < NR; ++m) ez[m] = nz[m];
     }
 }
 

@@ -229,6 +229,7 @@ void create_ctx(mpm2p_ctx* ctx, const mpm2p_problem* P) {
     c.anchor_m = (L.n_iface == 0) && pure_neumann;
     c.repair_active = L.n_sub > 1 || c.grounded;
     if (const char* e = std::getenv("MPM2P_NO_GRAPHS")) c.use_graphs = e[0] != 0 && e[0] == '0';
+    if (const char* e = std::getenv("MPM2P_NO_REGBAND")) c.no_regband = e[0] == '1';
 
     int dev = 0;
     CK(cudaGetDevice(&dev));

@@ -67,6 +67,17 @@ __device__ __forceinline__ double warp_min(double v) {
     return v;
 }
 
+// 1/d without the IEEE-division slow path: MUFU reciprocal approximation and
+// two Newton steps (relative error ~1 ulp; d is a positive pivot).
+__device__ __forceinline__ double fast_rcp(double d) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+    double e = fma(-d, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-d, r, 1.0);
+    return fma(r, e, r);
+}
+
 // Block-wide reduction (result valid in thread 0). sh: >= 32 doubles of smem.
 template <typename F>
 __device__ __forceinline__ double block_reduce_op(double v, F op, double ident, double* sh) {

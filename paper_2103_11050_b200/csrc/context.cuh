@@ -100,6 +100,7 @@ struct Ctx {
     int iface_sym = -1;  // J*M symmetric (pivot-free inverse)? -1 unknown
     // per-run CUDA graphs of one driver step (MPM-2P reuse / MRCM rebuild)
     bool use_graphs = true;
+    bool no_regband = false;  // MPM2P_NO_REGBAND=1: generic shared-memory band kernels only
     cudaGraphExec_t g_mpm = nullptr, g_rebuild = nullptr;
     long long gd_mpm[6] = {}, gd_rebuild[6] = {};  // counter / launch deltas per replay
     void drop_graphs() {

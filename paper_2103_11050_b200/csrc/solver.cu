@@ -1077,7 +1077,7 @@ void downscale(Ctx& c, const double* kappa) {
     const size_t sm1 = (size_t)WPB * band_smem_doubles(L.snx, 1) * sizeof(double);
     {
         PROF(c, "k_ds_solve");
-        switch (L.snx) {
+        switch (c.no_regband ? -1 : L.snx) {
 #define X(BW_)                                                                                                     \
     case BW_:                                                                                                      \
         k_ds_solve_r<BW_><<<band_blocks(L), WPB * 32, 0, c.st>>>(L, c.BDd, c.BWd, c.BSd, c.Dd, c.Lrd, c.Xd, c.RS, \
@@ -1150,7 +1150,7 @@ void launch_rebuild(Ctx& c, const double* kappa, bool compute_beta) {  // comput
     const size_t smr = (size_t)WPB * band_smem_doubles(L.snx, RING_NR) * sizeof(double);
     {
         PROF(c, "k_factor_solve");
-        switch (L.snx) {
+        switch (c.no_regband ? -1 : L.snx) {
 #define X(BW_)                                                                                                      \
     case BW_:                                                                                                       \
         if (rebuild_nr<BW_>(c.max_rhs) == 17)                                                                       \
@@ -1237,7 +1237,7 @@ void launch_mpm(Ctx& c, const double* kn) {  // mpm_pressure_update (mpm.cpp:31-
     const size_t sm1 = (size_t)WPB * band_smem_doubles(L.snx, 1) * sizeof(double);
     {
         PROF(c, "k_part_solve");
-        switch (L.snx) {
+        switch (c.no_regband ? -1 : L.snx) {
 #define X(BW_)                                                                                                  \
     case BW_:                                                                                                   \
         k_part_solve_r<BW_><<<band_blocks(L), WPB * 32, 0, c.st>>>(L, c.max_rhs, c.Dm, c.Lcm, c.Lrm, c.X);    \
