@@ -367,6 +367,14 @@ def main():
                     "peak_source": "measured DFMA peak (profiles/fp64_peaks_r01.log)",
                     "algorithmic_per_launch": w[1], "avg_launch_us": avg_s * 1e6}
         break
+    if roof is not None:  # dram bytes per launch from the committed ncu --set full capture
+        try:
+            with open(os.path.join(ROOT, "profiles", f"ncu_traffic_r01_{cfg.name}.json")) as f:
+                tr = {k.split("::")[-1]: v for k, v in json.load(f).items()}
+            roof["traffic"] = tr.get(roof["kernel"] + "_r", tr.get(roof["kernel"]))
+            roof["traffic_source"] = f"profiles/ncu_traffic_r01_{cfg.name}.json (dram__bytes_read+write per launch)"
+        except (OSError, ValueError):
+            pass
     cpu = None
     if not args.skip_cpu and ws == 1:
         import dataclasses
