@@ -131,6 +131,11 @@ void build_csr(Ctx& c) {
     }
     c.nnz = (int)col.size();
     c.csr_ptr.alloc(ptr.size());
+    std::vector<int> rowv(col.size());
+    for (size_t r = 0; r + 1 < ptr.size(); ++r)
+        for (int z = ptr[r]; z < ptr[r + 1]; ++z) rowv[z] = (int)r;
+    c.csr_row.alloc(std::max<size_t>(rowv.size(), 1));
+    if (!rowv.empty()) CK(cudaMemcpyAsync(c.csr_row.p, rowv.data(), rowv.size() * sizeof(int), cudaMemcpyHostToDevice, c.st));
     c.csr_col.alloc(std::max<size_t>(col.size(), 1));
     c.csr_val.alloc(std::max<size_t>(col.size(), 1));
     CK(cudaMemcpyAsync(c.csr_ptr.p, ptr.data(), ptr.size() * sizeof(int), cudaMemcpyHostToDevice, c.st));

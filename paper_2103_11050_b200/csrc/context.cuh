@@ -82,7 +82,7 @@ struct Ctx {
     DevBuf<double> HU, HB, HP;
     DevBuf<double> pm, bpm, pmsum;
     // interface system (CSR pattern built once; values per rebuild)
-    DevBuf<int> csr_ptr, csr_col;
+    DevBuf<int> csr_ptr, csr_col, csr_row;
     DevBuf<double> csr_val, Mdense, Minv, gj_work, gj_col, gj_row, gj_krow;
     DevBuf<int> gj_piv;
     DevBuf<double> irhs, icoef, ires, idelta;

@@ -432,22 +432,35 @@ __global__ void k_rcond(const double* __restrict__ part, int n, int nrb, const i
     }
 }
 
-// y = A x, one warp per row (coalesced row reads).
-__global__ void k_gemv(const double* __restrict__ A, const double* __restrict__ x, double* __restrict__ y, int n) {
-    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-    if (gw >= n) return;
-    const double* row = A + (size_t)gw * n;
-    double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;  // 4 loads in flight per lane
-    int j = lane;
-    for (; j + 96 < n; j += 128) {
-        v0 += __ldg(row + j) * __ldg(x + j);
-        v1 += __ldg(row + j + 32) * __ldg(x + j + 32);
-        v2 += __ldg(row + j + 64) * __ldg(x + j + 64);
-        v3 += __ldg(row + j + 96) * __ldg(x + j + 96);
+// y = A x: a 256-thread block covers 2 rows, 4 warps per row, each warp a
+// quarter of the row with 4 independent loads in flight per lane (the GEMV is
+// load-latency bound at these sizes, so more bytes in flight is the lever).
+__global__ void __launch_bounds__(256) k_gemv(const double* __restrict__ A, const double* __restrict__ x,
+                                              double* __restrict__ y, int n) {
+    __shared__ double part[8];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int r = blockIdx.x * 2 + (w >> 2), q = w & 3;
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+    if (r < n) {
+        const int cw = (n + 3) / 4, j0 = q * cw, j1 = min(n, j0 + cw);
+        const double* row = A + (size_t)r * n;
+        int j = j0 + lane;
+        for (; j + 96 < j1; j += 128) {
+            v0 += __ldg(row + j) * __ldg(x + j);
+            v1 += __ldg(row + j + 32) * __ldg(x + j + 32);
+            v2 += __ldg(row + j + 64) * __ldg(x + j + 64);
+            v3 += __ldg(row + j + 96) * __ldg(x + j + 96);
+        }
+        for (; j < j1; j += 32) v0 += __ldg(row + j) * __ldg(x + j);
     }
-    for (; j < n; j += 32) v0 += __ldg(row + j) * __ldg(x + j);
     const double v = warp_sum((v0 + v1) + (v2 + v3));
-    if (lane == 0) y[gw] = v;
+    if (lane == 0) part[w] = v;
+    __syncthreads();
+    if (threadIdx.x < 2) {
+        const int rr = blockIdx.x * 2 + threadIdx.x;
+        if (rr < n) y[rr] = (part[4 * threadIdx.x] + part[4 * threadIdx.x + 1]) +
+                            (part[4 * threadIdx.x + 2] + part[4 * threadIdx.x + 3]);
+    }
 }
 
 // r = b - M x with M in CSR, one thread per row.
@@ -628,7 +641,7 @@ double dense_inverse(Ctx& c, const double* A, double* Ainv, int n) {
 
 void launch_gemv(Ctx& c, const double* A, const double* x, double* y, int n) {
     PROF(c, "k_gemv");
-    k_gemv<<<cdiv((long long)n * 32, TPB), TPB, 0, c.st>>>(A, x, y, n);
+    k_gemv<<<cdiv(n, 2), 256, 0, c.st>>>(A, x, y, n);
     CK_LAUNCH();
 }
 

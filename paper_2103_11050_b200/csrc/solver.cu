@@ -345,11 +345,12 @@ __device__ __forceinline__ int hom_index(const Layout& L, int s, int col) {
     return (flux ? 0 : half) + before + t;
 }
 
-__global__ void k_assemble(Layout L, const int* __restrict__ ptr, const int* __restrict__ colv, int nrows,
+__global__ void k_assemble(Layout L, const int* __restrict__ rowv, const int* __restrict__ colv, int nnz,
                            const double* __restrict__ HU, const double* __restrict__ bm,
                            const double* __restrict__ bp, double* __restrict__ val) {
-    const int row = blockIdx.x * blockDim.x + threadIdx.x;
-    if (row >= nrows) return;
+    const int z = blockIdx.x * blockDim.x + threadIdx.x;  // one thread per nonzero
+    if (z >= nnz) return;
+    const int row = rowv[z];
     const int np = L.dim_flux;
     const bool phi = row >= np;
     const int rb = phi ? row - np : row;
@@ -357,7 +358,7 @@ __global__ void k_assemble(Layout L, const int* __restrict__ ptr, const int* __r
     const int rt = rb - L.iface_first_basis(k);
     const int ne = L.iface_edges(k);
     const int subs[2] = {L.iface_minus(k), L.iface_plus(k)};
-    for (int z = ptr[row]; z < ptr[row + 1]; ++z) {
+    {
         const int col = colv[z];
         const bool ucol = col < L.dim_flux;
         const int cb = ucol ? col : col - L.dim_flux;
@@ -1115,8 +1116,8 @@ void interface_solve(Ctx& c) {
         CK_LAUNCH();
     }
     launch_gemv(c, c.Minv, c.irhs, c.icoef, c.dim);
-    // two steps of iterative refinement against the sparse operator
-    for (int it = 0; it < 2; ++it) {
+    // one step of iterative refinement against the sparse operator
+    for (int it = 0; it < 1; ++it) {
         launch_csr_residual(c, c.csr_ptr, c.csr_col, c.csr_val, c.icoef, c.irhs, c.ires, c.dim);
         launch_gemv(c, c.Minv, c.ires, c.idelta, c.dim);
         launch_axpy(c, c.icoef, c.idelta, c.dim);
@@ -1185,7 +1186,7 @@ void launch_rebuild(Ctx& c, const double* kappa, bool compute_beta) {  // comput
     if (c.dim > 0) {
         {
             PROF(c, "k_assemble");
-            k_assemble<<<grid_for(c.dim), TPB, 0, c.st>>>(L, c.csr_ptr, c.csr_col, c.dim, c.HU, c.beta_m, c.beta_p,
+            k_assemble<<<grid_for(c.nnz), TPB, 0, c.st>>>(L, c.csr_row, c.csr_col, c.nnz, c.HU, c.beta_m, c.beta_p,
                                                           c.csr_val);
             CK_LAUNCH();
         }
