@@ -202,6 +202,9 @@ class RunRecord:  # simulation.hpp:47-62
     final_pvi: float
     min_eps_margin: float
     clamp_count: int
+    interface_krylov: int = 0
+    interface_max_iterations: int = 0
+    interface_iterations: int = 0
 
     @property
     def update_steps(self):
@@ -227,7 +230,8 @@ def _counters(c: _abi.Counters) -> SolveCounters:
 def _record(steps, r: _abi.RunRecord) -> RunRecord:
     return RunRecord(steps, r.breakthrough_step, r.breakthrough_pvi, r.te, r.tm_updates, r.tm_total, r.nhat,
                      r.n_sub, _counters(r.counters), r.max_div_residual, r.max_div_ratio, r.repair_warnings,
-                     r.final_pvi, r.min_eps_margin, r.clamp_count)
+                     r.final_pvi, r.min_eps_margin, r.clamp_count, r.interface_krylov,
+                     r.interface_max_iterations, r.interface_iterations)
 
 
 class Simulator:

@@ -141,6 +141,7 @@ void build_csr(Ctx& c) {
     CK(cudaMemcpyAsync(c.csr_ptr.p, ptr.data(), ptr.size() * sizeof(int), cudaMemcpyHostToDevice, c.st));
     if (!col.empty()) CK(cudaMemcpyAsync(c.csr_col.p, col.data(), col.size() * sizeof(int), cudaMemcpyHostToDevice, c.st));
     CK(cudaStreamSynchronize(c.st));
+    if (c.use_krylov) krylov_setup(c, ptr, col);
 }
 
 // Grid, decomposition and interface-space sizes with the reference's
@@ -235,6 +236,11 @@ void create_ctx(mpm2p_ctx* ctx, const mpm2p_problem* P) {
     c.repair_active = L.n_sub > 1 || c.grounded;
     if (const char* e = std::getenv("MPM2P_NO_GRAPHS")) c.use_graphs = e[0] != 0 && e[0] == '0';
     if (const char* e = std::getenv("MPM2P_NO_REGBAND")) c.no_regband = e[0] == '1';
+    c.use_krylov = c.dim > DENSE_IFACE_MAX;
+    if (const char* e = std::getenv("MPM2P_IFACE")) {
+        if (std::strcmp(e, "krylov") == 0) c.use_krylov = c.dim > 0;
+        else if (std::strcmp(e, "dense") == 0) c.use_krylov = false;
+    }
 
     int dev = 0;
     CK(cudaGetDevice(&dev));
@@ -283,7 +289,7 @@ void create_ctx(mpm2p_ctx* ctx, const mpm2p_problem* P) {
     c.bpm.alloc(ns * nbe);
     c.pmsum.alloc(ns);
     const size_t dim = std::max(1, c.dim);
-    if (c.dim > 0) {
+    if (c.dim > 0 && !c.use_krylov) {
         c.Mdense.alloc((size_t)c.dim * c.dim);
         c.Minv.alloc((size_t)c.dim * c.dim);
     }
@@ -507,6 +513,9 @@ void run_end(mpm2p_ctx* ctx, mpm2p_run_record* out) {
     d.rec.final_pvi = c.sc_host->pvi;
     d.rec.min_eps_margin = c.sc_host->min_margin;
     d.rec.clamp_count = c.sc_host->clamp;
+    d.rec.interface_krylov = c.use_krylov ? 1 : 0;
+    d.rec.interface_max_iterations = c.sc_host->kr_iters_max;
+    d.rec.interface_iterations = c.sc_host->kr_iters_total;
     if (out) *out = d.rec;
     d.active = false;
 }
@@ -737,7 +746,18 @@ int mpm2p_interface_matrix(mpm2p_ctx* ctx, double* M) {
     return guarded(ctx, [&] {
         Ctx& c = ctx->c;
         if (!c.has_basis) throw ConfigError("interface_matrix: no basis installed");
-        if (c.dim > 0) download(c, M, c.Mdense, (size_t)c.dim * c.dim);
+        if (c.dim > 0 && !c.use_krylov) download(c, M, c.Mdense, (size_t)c.dim * c.dim);
+        if (c.dim > 0 && c.use_krylov && M) {  // no dense copy on the Krylov path: scatter the CSR values
+            std::vector<int> ptr(c.dim + 1), col(c.nnz);
+            std::vector<double> val(c.nnz);
+            CK(cudaMemcpyAsync(ptr.data(), c.csr_ptr.p, ptr.size() * sizeof(int), cudaMemcpyDeviceToHost, c.st));
+            CK(cudaMemcpyAsync(col.data(), c.csr_col.p, col.size() * sizeof(int), cudaMemcpyDeviceToHost, c.st));
+            CK(cudaMemcpyAsync(val.data(), c.csr_val.p, val.size() * sizeof(double), cudaMemcpyDeviceToHost, c.st));
+            CK(cudaStreamSynchronize(c.st));
+            std::fill(M, M + (size_t)c.dim * c.dim, 0.0);
+            for (int r = 0; r < c.dim; ++r)
+                for (int z = ptr[r]; z < ptr[r + 1]; ++z) M[(size_t)r * c.dim + col[z]] = val[z];
+        }
         CK(cudaStreamSynchronize(c.st));
     });
 }

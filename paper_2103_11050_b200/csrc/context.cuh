@@ -24,7 +24,9 @@ struct Scalars {
     int rebuild_next;
     int repair_warning;
     long long clamp;
-    double pad[8];
+    long long kr_iters_total;  // MINRES iterations (K7), summed over solves
+    int kr_iters_max, kr_solves;
+    double pad[6];
 };
 
 template <typename T>
@@ -87,6 +89,13 @@ struct Ctx {
     DevBuf<int> gj_piv;
     DevBuf<double> irhs, icoef, ires, idelta;
     int nnz = 0;
+    // K7 Krylov interface solve (dimension above the dense limit, or forced by
+    // MPM2P_IFACE=krylov): K = J M in CSR, Jacobi preconditioner, MINRES work.
+    bool use_krylov = false;
+    double krylov_tol = 1e-13;
+    int krylov_maxit = 20000;
+    DevBuf<int> k_ptr, k_col;
+    DevBuf<double> k_val, kr_pinv, kr_work;
     // per-solve scratch
     DevBuf<double> X, PU, PB, PS, GZ, WU, RU, RS, skel, resid, delta, corr;
     // downscale
@@ -218,5 +227,11 @@ void launch_gemv(Ctx& c, const double* A, const double* x, double* y, int n);
 void launch_csr_residual(Ctx& c, const int* ptr, const int* col, const double* val, const double* x,
                          const double* b, double* r, int n);
 void launch_axpy(Ctx& c, double* y, const double* x, int n);
+
+// ---- launchers (krylov.cu) -------------------------------------------------
+constexpr int DENSE_IFACE_MAX = 16384;  // above this the interface solve is MINRES
+void krylov_setup(Ctx& c, const std::vector<int>& mptr, const std::vector<int>& mcol);
+void krylov_prepare(Ctx& c);                                  // after assembly
+void krylov_solve(Ctx& c, const double* rhs, double* x);      // x = M^-1 rhs
 
 }  // namespace mpm2p

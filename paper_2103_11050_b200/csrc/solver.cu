@@ -1115,6 +1115,10 @@ void interface_solve(Ctx& c) {
         k_iface_rhs<<<grid_for(32LL * c.dim), TPB, 0, c.st>>>(L, c.PU, c.beta_m, c.beta_p, c.irhs);
         CK_LAUNCH();
     }
+    if (c.use_krylov) {
+        krylov_solve(c, c.irhs, c.icoef);
+        return;
+    }
     launch_gemv(c, c.Minv, c.irhs, c.icoef, c.dim);
     // one step of iterative refinement against the sparse operator
     for (int it = 0; it < 1; ++it) {
@@ -1190,14 +1194,20 @@ void launch_rebuild(Ctx& c, const double* kappa, bool compute_beta) {  // comput
                                                           c.csr_val);
             CK_LAUNCH();
         }
-        {
-            PROF(c, "k_csr_to_dense");
-            k_csr_to_dense<<<c.dim, TPB, 0, c.st>>>(c.csr_ptr, c.csr_col, c.csr_val, c.dim, c.Mdense);
-            CK_LAUNCH();
+        if (c.use_krylov) {
+            // no dense factorisation: the rcond guard becomes MINRES
+            // non-convergence (ERR_SINGULAR raised by k_minres)
+            krylov_prepare(c);
+        } else {
+            {
+                PROF(c, "k_csr_to_dense");
+                k_csr_to_dense<<<c.dim, TPB, 0, c.st>>>(c.csr_ptr, c.csr_col, c.csr_val, c.dim, c.Mdense);
+                CK_LAUNCH();
+            }
+            // rcond guard (mrcm.cpp:227-238) is evaluated on the device; a trip
+            // surfaces as ERR_SINGULAR at the step's scalar readback.
+            interface_inverse_async(c, c.Mdense, c.Minv, c.dim, &c.sc.p->rcond, ERR_SINGULAR, 1e-14);
         }
-        // rcond guard (mrcm.cpp:227-238) is evaluated on the device; a trip
-        // surfaces as ERR_SINGULAR at the step's scalar readback.
-        interface_inverse_async(c, c.Mdense, c.Minv, c.dim, &c.sc.p->rcond, ERR_SINGULAR, 1e-14);
     }
     interface_solve(c);
     // recon_m (kept for MPM steps) and its traces
