@@ -14,7 +14,15 @@
 //    chunk (B pivots) ahead, so the pivot chain never waits on memory;
 //  * entries right of the diagonal receive harmless garbage (the entering
 //    row resets its registers), so the rank-1 update needs no predicates.
-// Per pivot the critical path is one shuffle, one reciprocal and two FMAs.
+//  * no pointer here is __restrict__: every buffer is written by one lane and
+//    read by others (a restrict pointer licenses the compiler to hoist a
+//    lane's load above another lane's store across __syncwarp);
+//  * the pivot column is broadcast through a per-warp shared-memory exchange
+//    buffer (one STS per lane, then LDS.128 broadcasts), not warp shuffles:
+//    a 64-bit shuffle issues once per ~10 cycles per warp on B200
+//    (tools/lat_probe.cu), so B of them per pivot made the step MIO-bound.
+// Per pivot the critical path is one smem round trip (~43 cycles), one
+// reciprocal and two FMAs.
 // Outputs match band.cuh: D[n], Lcol[n][B] (L[k+1+j][k]), Lrow[n][B]
 // (L[k][k-B+o]); right-hand sides are transformed in place b -> y -> x.
 #pragma once
@@ -32,6 +40,17 @@ __host__ __device__ constexpr int band_lq() {
     return B <= 20 ? B : (B % 16 == 0 ? 16 : (B % 8 == 0 ? 8 : 4));
 }
 
+// Per-warp exchange buffer (doubles, 16-byte aligned): two parity slots of
+// the pivot column (B), of the pivot (2, padded) and of the pivot's RHS values.
+template <int NR>
+__host__ __device__ constexpr int xchg_ys() {
+    return (NR + 1) & ~1;
+}
+template <int B, int NR>
+__host__ __device__ constexpr int xchg_doubles() {
+    return 2 * B + 4 + 2 * xchg_ys<NR>();
+}
+
 template <int B>
 __device__ __forceinline__ int band_j_of(int lane, int u) {  // window position of lane's row at pivot k0+u
     return (lane - u - 1 + 2 * B) % B;
@@ -40,9 +59,11 @@ __device__ __forceinline__ int band_j_of(int lane, int u) {  // window position 
 // Factorization with the forward sweep of NR right-hand sides fused in.
 // stage: B*B doubles of shared memory (per warp) used to transpose L rows.
 template <int B, int NR>
-__device__ bool factor_fwd_reg(int n, const BandRows A, double* __restrict__ D, double* __restrict__ Lcol,
-                               double* __restrict__ Lrow, double* __restrict__ Y, int nr, int ldy,
-                               double* __restrict__ stage) {
+__device__ bool factor_fwd_reg(int n, const BandRows A, double* D, double* Lcol,
+                               double* Lrow, double* Y, int nr, int ldy,
+                               double* stage, double* xb) {
+    static_assert(B % 2 == 0 || B == 1, "pairs of the pivot column are read as double2");
+    constexpr int YS = xchg_ys<NR>();
     const int lane = threadIdx.x & 31;
     const bool act = lane < B;
     double reg[B];
@@ -79,6 +100,8 @@ __device__ bool factor_fwd_reg(int n, const BandRows A, double* __restrict__ D, 
     fetch(B + lane, cd, cw, cs, cb);
     bool ok = true;
     const bool has_lcol = Lcol != nullptr;
+    double st_l = 0.0;  // deferred stage write (position st_pos of this lane's row)
+    int st_pos = 0;
     __syncwarp();
     for (int k0 = 0; k0 < n; k0 += B) {
         double nd, nw, ns, nbv[NR];
@@ -88,33 +111,54 @@ __device__ bool factor_fwd_reg(int n, const BandRows A, double* __restrict__ D, 
         for (int u = 0; u < B; ++u) {
             const int k = k0 + u;
             const bool piv = lane == u;
-            const double d = __shfl_sync(FULL, reg[u], u);
+            // pivot lane: row k leaves, row k+B enters (its coupling to column k is c)
+            const bool ent = ent_chunk;
+            const double c = piv ? (ent ? -cs : 0.0) : reg[u];
+            double* cbuf = xb + (u & 1) * B;            // column k of the window
+            double* dbuf = xb + 2 * B + (u & 1) * 2;    // pivot d_k
+            double* ybuf = xb + 2 * B + 4 + (u & 1) * YS;  // y_k of the NR right-hand sides
+            // previous step's L entry into the transposition tile (ordered after
+            // every read of step k-1 by the end-of-step barrier)
+            if (act) stage[lane * B + st_pos] = st_l;
+            if (act) cbuf[lane] = c;
+            if (piv) {
+                dbuf[0] = reg[u];
+#pragma unroll
+                for (int m = 0; m < NR; ++m) ybuf[m] = yv[m];
+            }
+            __syncwarp();
+            const double d = dbuf[0];
             double yk[NR];
 #pragma unroll
-            for (int m = 0; m < NR; ++m) yk[m] = __shfl_sync(FULL, yv[m], u);
+            for (int m = 0; m < NR; ++m) yk[m] = ybuf[m];
             if (piv) D[k] = d;
 #pragma unroll
             for (int m = 0; m < NR; ++m)
                 if (piv && m < nr) Y[(size_t)m * ldy + k] = yk[m];
             if (act) Lrow[(size_t)k * B + lane] = stage[u * B + lane];
-            __syncwarp();
             ok = ok && (d > 0.0);
-            // pivot lane: row k leaves, row k+B enters (its coupling to column k is c)
-            const bool ent = ent_chunk;
-            const double c = piv ? (ent ? -cs : 0.0) : reg[u];
             const double keep = piv ? 0.0 : 1.0;
             const double fd_ = (piv && ent) ? cd : 0.0, fw_ = (piv && ent) ? -cw : 0.0;
             const double l = c * fast_rcp(d);
             const int j = band_j_of<B>(lane, u);
             if (act && has_lcol) Lcol[(size_t)k * B + j] = l;
-            if (act) stage[lane * B + (B - 1 - j)] = l;
+            st_l = l;
+            st_pos = B - 1 - j;
+            const double2* cb2 = reinterpret_cast<const double2*>(cbuf);
 #pragma unroll
-            for (int i = 0; i < B; ++i) {
-                const int ci = (u + 1 + i) % B;
-                const double a = __shfl_sync(FULL, c, ci);
-                const double fresh = (ci == u) ? fd_ : ((ci == (u + B - 1) % B) ? fw_ : 0.0);
-                reg[ci] = fma(-l, a, fma(reg[ci], keep, fresh));
+            for (int q = 0; q < B / 2; ++q) {
+                const double2 a2 = cb2[q];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int ci = 2 * q + h;
+                    if (ci == u) continue;  // column k itself: reset below
+                    const double a = h ? a2.y : a2.x;
+                    const double fresh = (ci == (u + B - 1) % B) ? fw_ : 0.0;
+                    reg[ci] = fma(-l, a, fma(reg[ci], keep, fresh));
+                }
             }
+            // register u (column k leaves, column k+B enters): a = c of the pivot lane
+            reg[u] = fma(-l, u % 2 ? cb2[u / 2].y : cb2[u / 2].x, fma(reg[u], keep, fd_));
 #pragma unroll
             for (int m = 0; m < NR; ++m) yv[m] = fma(-l, yk[m], fma(yv[m], keep, (piv && ent) ? cb[m] : 0.0));
             __syncwarp();
@@ -130,7 +174,9 @@ __device__ bool factor_fwd_reg(int n, const BandRows A, double* __restrict__ D, 
 
 // Forward sweep L y = b with a stored factor (Lcol), NR RHS in place.
 template <int B, int NR>
-__device__ void forward_reg(int n, const double* __restrict__ Lcol, double* __restrict__ Y, int nr, int ldy) {
+__device__ void forward_reg(int n, const double* Lcol, double* Y, int nr, int ldy,
+                            double* xb) {
+    constexpr int YS = xchg_ys<NR>();
     const int lane = threadIdx.x & 31;
     const bool act = lane < B;
     auto yat = [&](int m, int row) {  // clamped (always valid) load + select
@@ -163,8 +209,18 @@ __device__ void forward_reg(int n, const double* __restrict__ Lcol, double* __re
             const double l = lq[u % LQ];
             lq[u % LQ] = lcol_at(k + LQ, (u + LQ) % B);
             double yk[NR];
+            if constexpr (NR == 1) {
+                yk[0] = __shfl_sync(FULL, yv[0], u);
+            } else {  // smem broadcast (NR 64-bit shuffles would be issue-bound)
+                double* ybuf = xb + (u & 1) * YS;
+                if (piv) {
 #pragma unroll
-            for (int m = 0; m < NR; ++m) yk[m] = __shfl_sync(FULL, yv[m], u);
+                    for (int m = 0; m < NR; ++m) ybuf[m] = yv[m];
+                }
+                __syncwarp();
+#pragma unroll
+                for (int m = 0; m < NR; ++m) yk[m] = ybuf[m];
+            }
 #pragma unroll
             for (int m = 0; m < NR; ++m) {
                 if (piv && m < nr) Y[(size_t)m * ldy + k] = yk[m];
@@ -178,8 +234,9 @@ __device__ void forward_reg(int n, const double* __restrict__ Lcol, double* __re
 
 // Backward sweep L^T x = D^-1 y with a stored factor (Lrow, D), NR RHS in place.
 template <int B, int NR>
-__device__ void backward_reg(int n, const double* __restrict__ D, const double* __restrict__ Lrow,
-                             double* __restrict__ Y, int nr, int ldy) {
+__device__ void backward_reg(int n, const double* D, const double* Lrow,
+                             double* Y, int nr, int ldy, double* xb) {
+    constexpr int YS = xchg_ys<NR>();
     const int lane = threadIdx.x & 31;
     const bool act = lane < B;
     // entering value z = y / d of row `row` (0 outside the matrix); clamped loads
@@ -219,8 +276,18 @@ __device__ void backward_reg(int n, const double* __restrict__ D, const double* 
             const double l = lq[uu % LQ];
             lq[uu % LQ] = lrow_at(k - LQ, (uu + B - LQ % B) % B);
             double xk[NR];
+            if constexpr (NR == 1) {
+                xk[0] = __shfl_sync(FULL, z[0], uu);
+            } else {
+                double* zbuf = xb + (uu & 1) * YS;
+                if (piv) {
 #pragma unroll
-            for (int m = 0; m < NR; ++m) xk[m] = __shfl_sync(FULL, z[m], uu);
+                    for (int m = 0; m < NR; ++m) zbuf[m] = z[m];
+                }
+                __syncwarp();
+#pragma unroll
+                for (int m = 0; m < NR; ++m) xk[m] = zbuf[m];
+            }
 #pragma unroll
             for (int m = 0; m < NR; ++m) {
                 if (piv && m < nr) Y[(size_t)m * ldy + k] = xk[m];

@@ -677,10 +677,11 @@ __global__ void k_ds_solve(Layout L, const double* __restrict__ BD, const double
 template <int B>
 __global__ void __launch_bounds__(WPB * 32) k_ds_solve_r(Layout L, const double* __restrict__ BD,
                                                          const double* __restrict__ BW, const double* __restrict__ BS,
-                                                         double* __restrict__ D, double* __restrict__ Lr,
-                                                         double* __restrict__ Xd, const double* __restrict__ RS,
-                                                         double* __restrict__ p, Scalars* sc) {
+                                                         double* D, double* Lr,
+                                                         double* Xd, const double* __restrict__ RS,
+                                                         double* p, Scalars* sc) {
     __shared__ double stage[WPB][B * B];
+    __shared__ __align__(16) double xbuf[WPB][xchg_doubles<B, 1>()];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int s = blockIdx.x * WPB + w;
     if (s >= L.n_sub) return;
@@ -688,10 +689,10 @@ __global__ void __launch_bounds__(WPB * 32) k_ds_solve_r(Layout L, const double*
     const size_t so = (size_t)s * n;
     const BandRows A{BD + so, BW + so, BS + so};
     double* x = Xd + so;
-    const bool ok = factor_fwd_reg<B, 1>(n, A, D + so, nullptr, Lr + so * B, x, 1, n, stage[w]);
+    const bool ok = factor_fwd_reg<B, 1>(n, A, D + so, nullptr, Lr + so * B, x, 1, n, stage[w], xbuf[w]);
     if (!ok && lane == 0) atomicOr(&sc->err, ERR_PIVOT);
     __syncwarp();
-    backward_reg<B, 1>(n, D + so, Lr + so * B, x, 1, n);
+    backward_reg<B, 1>(n, D + so, Lr + so * B, x, 1, n, xbuf[w]);
     __syncwarp();
     double v = 0.0;
     for (int r = lane; r < n; r += 32) v += x[r];
@@ -703,16 +704,16 @@ __global__ void __launch_bounds__(WPB * 32) k_ds_solve_r(Layout L, const double*
 template <int B>
 __global__ void __launch_bounds__(WPB * 32) k_part_solve_r(Layout L, int max_rhs, const double* __restrict__ D,
                                                            const double* __restrict__ Lc,
-                                                           const double* __restrict__ Lr, double* __restrict__ X) {
+                                                           const double* __restrict__ Lr, double* X) {
     const int w = threadIdx.x >> 5;
     const int s = blockIdx.x * WPB + w;
     if (s >= L.n_sub) return;
     const int n = L.ncs;
     const size_t so = (size_t)s * n;
     double* x = X + xoff(L, max_rhs, s, 0);
-    forward_reg<B, 1>(n, Lc + so * B, x, 1, n);
+    forward_reg<B, 1>(n, Lc + so * B, x, 1, n, nullptr);
     __syncwarp();
-    backward_reg<B, 1>(n, D + so, Lr + so * B, x, 1, n);
+    backward_reg<B, 1>(n, D + so, Lr + so * B, x, 1, n, nullptr);
 }
 
 // RHS carried through one register sweep of the rebuild (1 particular + up to
@@ -725,10 +726,11 @@ constexpr int rebuild_nr(int max_rhs) {
 template <int B, int NR_REG>
 __global__ void __launch_bounds__(WPB * 32) k_factor_solve_r(Layout L, int max_rhs, const double* __restrict__ BD,
                                                              const double* __restrict__ BW,
-                                                             const double* __restrict__ BS, double* __restrict__ D,
-                                                             double* __restrict__ Lc, double* __restrict__ Lr,
-                                                             double* __restrict__ X, Scalars* sc) {
+                                                             const double* __restrict__ BS, double* D,
+                                                             double* Lc, double* Lr,
+                                                             double* X, Scalars* sc) {
     __shared__ double stage[WPB][B * B];
+    __shared__ __align__(16) double xbuf[WPB][xchg_doubles<B, NR_REG>()];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int s = blockIdx.x * WPB + w;
     if (s >= L.n_sub) return;
@@ -738,17 +740,18 @@ __global__ void __launch_bounds__(WPB * 32) k_factor_solve_r(Layout L, int max_r
     const int nr = 1 + L.n_hom(s);
     double* Xs = X + xoff(L, max_rhs, s, 0);
     const int n0 = nr < NR_REG ? nr : NR_REG;
-    const bool ok = factor_fwd_reg<B, NR_REG>(n, A, D + so, Lc + so * B, Lr + so * B, Xs, n0, n, stage[w]);
+    const bool ok =
+        factor_fwd_reg<B, NR_REG>(n, A, D + so, Lc + so * B, Lr + so * B, Xs, n0, n, stage[w], xbuf[w]);
     if (!ok && lane == 0) atomicOr(&sc->err, ERR_PIVOT);
     __syncwarp();
     for (int m0 = n0; m0 < nr; m0 += NR_REG) {
         const int cnt = nr - m0 < NR_REG ? nr - m0 : NR_REG;
-        forward_reg<B, NR_REG>(n, Lc + so * B, Xs + (size_t)m0 * n, cnt, n);
+        forward_reg<B, NR_REG>(n, Lc + so * B, Xs + (size_t)m0 * n, cnt, n, xbuf[w]);
         __syncwarp();
     }
     for (int m0 = 0; m0 < nr; m0 += NR_REG) {
         const int cnt = nr - m0 < NR_REG ? nr - m0 : NR_REG;
-        backward_reg<B, NR_REG>(n, D + so, Lr + so * B, Xs + (size_t)m0 * n, cnt, n);
+        backward_reg<B, NR_REG>(n, D + so, Lr + so * B, Xs + (size_t)m0 * n, cnt, n, xbuf[w]);
         __syncwarp();
     }
 }
