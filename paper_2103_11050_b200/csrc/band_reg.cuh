@@ -66,6 +66,7 @@ __device__ bool factor_fwd_reg(int n, const BandRows A, double* D, double* Lcol,
     constexpr int YS = xchg_ys<NR>();
     const int lane = threadIdx.x & 31;
     const bool act = lane < B;
+    const int lane_c = act ? lane : 0;  // in-bounds smem index for idle lanes
     double reg[B];
     double yv[NR];
     // rows 0..B-1: lane l holds row l (diag in reg[l], west coupling in reg[l-1])
@@ -82,19 +83,16 @@ __device__ bool factor_fwd_reg(int n, const BandRows A, double* D, double* Lcol,
     for (int m = 0; m < NR; ++m) yv[m] = (act && lane < n && m < nr) ? Y[(size_t)m * ldy + lane] : 0.0;
     for (int x = lane; x < B * B; x += 32) stage[x] = 0.0;
     // entering-row data for the first chunk: row B + lane. Loads use clamped
-    // (always valid) indices and a select, so the step body has no branches.
+    // (always valid) indices and no select: a value is only consumed under
+    // `ent` (the row exists), so the prefetch never stalls the issuing step.
+    // Slots m >= nr carry a copy of RHS nr-1 (finite, never stored).
     auto fetch = [&](int row, double& fd, double& fw, double& fs, double* fb) {
-        const bool ok = act && row < n;
         const int rr = row < n ? row : n - 1;
-        const double vd = A.diag[rr], vw = A.offw[rr], vs = A.offs[rr];
-        fd = ok ? vd : 0.0;
-        fw = ok ? vw : 0.0;
-        fs = ok ? vs : 0.0;
+        fd = A.diag[rr];
+        fw = A.offw[rr];
+        fs = A.offs[rr];
 #pragma unroll
-        for (int m = 0; m < NR; ++m) {
-            const double v = Y[(size_t)(m < nr ? m : nr - 1) * ldy + rr];
-            fb[m] = (ok && m < nr) ? v : 0.0;
-        }
+        for (int m = 0; m < NR; ++m) fb[m] = Y[(size_t)(m < nr ? m : nr - 1) * ldy + rr];
     };
     double cd, cw, cs, cb[NR];
     fetch(B + lane, cd, cw, cs, cb);
@@ -131,17 +129,16 @@ __device__ bool factor_fwd_reg(int n, const BandRows A, double* D, double* Lcol,
             double yk[NR];
 #pragma unroll
             for (int m = 0; m < NR; ++m) yk[m] = ybuf[m];
-            if (piv) D[k] = d;
+            st_global_if(D + k, d, piv);
 #pragma unroll
-            for (int m = 0; m < NR; ++m)
-                if (piv && m < nr) Y[(size_t)m * ldy + k] = yk[m];
-            if (act) Lrow[(size_t)k * B + lane] = stage[u * B + lane];
+            for (int m = 0; m < NR; ++m) st_global_if(Y + (size_t)m * ldy + k, yk[m], piv && m < nr);
+            st_global_if(Lrow + (size_t)k * B + lane, stage[u * B + lane_c], act);
             ok = ok && (d > 0.0);
             const double keep = piv ? 0.0 : 1.0;
             const double fd_ = (piv && ent) ? cd : 0.0, fw_ = (piv && ent) ? -cw : 0.0;
             const double l = c * fast_rcp(d);
             const int j = band_j_of<B>(lane, u);
-            if (act && has_lcol) Lcol[(size_t)k * B + j] = l;
+            if (has_lcol) st_global_if(Lcol + (size_t)k * B + j, l, act);
             st_l = l;
             st_pos = B - 1 - j;
             const double2* cb2 = reinterpret_cast<const double2*>(cbuf);

@@ -67,6 +67,16 @@ __device__ __forceinline__ double warp_min(double v) {
     return v;
 }
 
+// Predicated global store without a divergent branch (the compiler otherwise
+// wraps lane-conditional stores in BSSY/WARPSYNC regions, which stall the
+// latency-bound pivot loop). No memory clobber: callers order it with later
+// reads through __syncwarp.
+__device__ __forceinline__ void st_global_if(double* p, double v, bool pred) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.f64 [%0], %1;\n\t}" ::"l"(p), "d"(v),
+        "r"((int)pred));
+}
+
 // 1/d without the IEEE-division slow path: MUFU reciprocal approximation and
 // two Newton steps (relative error ~1 ulp; d is a positive pivot).
 __device__ __forceinline__ double fast_rcp(double d) {
