@@ -236,6 +236,7 @@ void create_ctx(mpm2p_ctx* ctx, const mpm2p_problem* P) {
     c.repair_active = L.n_sub > 1 || c.grounded;
     if (const char* e = std::getenv("MPM2P_NO_GRAPHS")) c.use_graphs = e[0] != 0 && e[0] == '0';
     if (const char* e = std::getenv("MPM2P_NO_REGBAND")) c.no_regband = e[0] == '1';
+    if (const char* e = std::getenv("MPM2P_GJ")) c.gj_legacy = std::strcmp(e, "legacy") == 0;
     c.use_krylov = c.dim > DENSE_IFACE_MAX;
     if (const char* e = std::getenv("MPM2P_IFACE")) {
         if (std::strcmp(e, "krylov") == 0) c.use_krylov = c.dim > 0;

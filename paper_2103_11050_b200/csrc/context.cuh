@@ -87,6 +87,8 @@ struct Ctx {
     DevBuf<int> csr_ptr, csr_col, csr_row;
     DevBuf<double> csr_val, Mdense, Minv, gj_work, gj_col, gj_row, gj_krow;
     DevBuf<int> gj_piv;
+    DevBuf<double> gj_pp;     // ping-pong GJ: two padded copies + two 32 x 32 pivot inverses
+    bool gj_legacy = false;   // MPM2P_GJ=legacy: the two-barrier k_block_gj
     DevBuf<double> irhs, icoef, ires, idelta;
     int nnz = 0;
     // K7 Krylov interface solve (dimension above the dense limit, or forced by

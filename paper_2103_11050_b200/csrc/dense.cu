@@ -22,6 +22,9 @@
 // there, so a rebuild needs no host synchronisation.
 #include <cooperative_groups.h>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "context.cuh"
 
 namespace cg = cooperative_groups;
@@ -332,6 +335,258 @@ __global__ void __launch_bounds__(256) k_block_gj(BGJArgs a) {
 
 constexpr size_t GJB_SMEM = (GJB * (GJB + 1) + 64 * GJB + GJB * 128) * sizeof(double);
 
+// ---- ping-pong blocked Gauss-Jordan with lookahead -------------------------
+// Same mathematics as k_block_gj (pivot-free GJ over 32 x 32 blocks of a
+// padded npad x npad matrix), restructured so each block step costs ONE grid
+// barrier: step k reads W_src and writes W_dst (no read/write conflicts inside
+// a step), and a dedicated lookahead CTA updates the next diagonal block and
+// inverts it during step k, so P_{k+1} = W_{k+1,k+1}^-1 is ready when step k+1
+// starts. Work items are (block row i, chunk of cpb block columns). Per step:
+//   i != k : T = W_ik P_k ;  W'_ij = W_ij - T W_kj (j != k) ;  W'_ik = -T
+//   i == k : W'_kj = P_k W_kj (j != k) ;  W'_kk = P_k
+constexpr int PPB = 32;
+struct PPArgs {
+    double* W0;
+    double* W1;
+    double* P;  // two 32 x 32 slots (P_k in slot k % 2)
+    int ld;     // = npad = nb * 32
+    int nb, nch, cpb;
+    int* singular;
+    unsigned long long* trace;  // optional (MPM2P_GJ_TRACE=1): per-step %globaltimer marks
+};
+typedef double PPTile[PPB][PPB + 1];
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// All loads issued before any store (one L2 round trip, not four); 256 threads.
+__device__ __forceinline__ void pp_load(PPTile S, const double* g, int ld) {
+    double v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int x = threadIdx.x + 256 * q;
+        v[q] = __ldcg(g + (size_t)(x >> 5) * ld + (x & 31));
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int x = threadIdx.x + 256 * q;
+        S[x >> 5][x & 31] = v[q];
+    }
+}
+// thread t owns row t >> 3 and columns (t & 7) + 8 m of a 32 x 32 result
+__device__ __forceinline__ void pp_mul(const PPTile X, const PPTile Y, double out[4]) {
+    const int r = threadIdx.x >> 3, c0 = threadIdx.x & 7;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) out[m] = 0.0;
+#pragma unroll 8
+    for (int t = 0; t < PPB; ++t) {
+        const double x = X[r][t];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) out[m] = fma(x, Y[t][c0 + 8 * m], out[m]);
+    }
+}
+// In-place inverse of S (pivot-free GJ) on 4 warps (one per SM sub-
+// partition): warp w keeps columns 8w..8w+7 of row `lane` in registers. Per
+// pivot k the 8-column slice of row k is exchanged inside each warp and
+// column k (with the pivot) across the 4 warps, double-buffered by pivot
+// parity: one 128-thread named barrier per pivot. Row update
+// v = fma(-f, r_k, v) * s with (f, s) = (A_rk p, 1) off the pivot row and
+// (0, p) on it, so the new pivot row is r_k * p exactly. Flags a zero /
+// non-finite pivot. Uses xb[2 * 32 + 4 * 2 * 8] doubles (16-byte aligned).
+__device__ void pp_invert(PPTile S, double* xb, int* singular) {
+    if (threadIdx.x < 128) {
+        const int w = threadIdx.x >> 5, r = threadIdx.x & 31;
+        double v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = S[r][8 * w + j];
+#pragma unroll
+        for (int k = 0; k < PPB; ++k) {
+            const int kw = k >> 3, kj = k & 7;
+            double* cb = xb + (k & 1) * PPB;
+            double2* rb = reinterpret_cast<double2*>(xb + 2 * PPB + (w * 2 + (k & 1)) * 8);
+            if (r == k) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) rb[q] = make_double2(v[2 * q], v[2 * q + 1]);
+            }
+            if (w == kw) cb[r] = v[kj];
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            double rk[8];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const double2 t = rb[q];
+                rk[2 * q] = t.x;
+                rk[2 * q + 1] = t.y;
+            }
+            const double piv = cb[k];
+            const double colk = cb[r];
+            const double p = 1.0 / piv;
+            if (threadIdx.x == 0 && (!(piv != 0.0) || !isfinite(piv))) *singular = 1;
+            const bool on = r == k;
+            const double f = on ? 0.0 : colk * p;
+            const double sc = on ? p : 1.0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] = fma(-f, rk[j], v[j]) * sc;
+            if (w == kw) v[kj] = on ? p : -f;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) S[r][8 * w + j] = v[j];
+    }
+    __syncthreads();
+}
+
+// Dynamic shared memory of k_gj_pp: four 32 x 33 tiles, a 32 x 128 slice of
+// the pivot block row, and the pivot row/column exchange buffers.
+constexpr int PPW = 128;  // columns per work item (4 blocks)
+constexpr size_t PP_SMEM = (4 * PPB * (PPB + 1) + PPB * PPW + 2 * PPB + 4 * 2 * 8) * sizeof(double);
+
+__global__ void __launch_bounds__(256, 2) k_gj_pp(PPArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ double pp_sm[];
+    PPTile& Ps = *reinterpret_cast<PPTile*>(pp_sm);
+    PPTile& Cs = *reinterpret_cast<PPTile*>(pp_sm + PPB * (PPB + 1));
+    PPTile& Ts = *reinterpret_cast<PPTile*>(pp_sm + 2 * PPB * (PPB + 1));
+    PPTile& Bs = *reinterpret_cast<PPTile*>(pp_sm + 3 * PPB * (PPB + 1));
+    double* Ws = pp_sm + 4 * PPB * (PPB + 1);  // 32 x 128, row-major
+    double* xrow = Ws + PPB * PPW;  // pivot-row exchange (2 x 32, 16-byte aligned)
+    const int ld = a.ld, nb = a.nb, np = nb * PPB;
+    const int r = threadIdx.x >> 3, c0 = threadIdx.x & 7;
+    const int wy = threadIdx.x >> 5, wx = threadIdx.x & 31;  // 4 x 4 register tile: rows 4 wy.., cols wx + 32 m
+    const bool look = blockIdx.x == gridDim.x - 1;
+    const int nwork = gridDim.x - 1;
+    const int nch = (np + PPW - 1) / PPW;
+    auto blk = [&](double* W, int I, int J) { return W + (size_t)I * PPB * ld + (size_t)J * PPB; };
+    auto pslot = [&](int k) { return a.P + (size_t)(k & 1) * PPB * PPB; };
+    if (look) {  // P_0
+        pp_load(Cs, a.W0, ld);
+        __syncthreads();
+        pp_invert(Cs, xrow, a.singular);
+        for (int x = threadIdx.x; x < PPB * PPB; x += blockDim.x) pslot(0)[x] = Cs[x >> 5][x & 31];
+    }
+    grid.sync();
+    for (int k = 0; k < nb; ++k) {
+        double* src = (k & 1) ? a.W1 : a.W0;
+        double* dst = (k & 1) ? a.W0 : a.W1;
+        auto mark = [&](int slot) {
+            if (a.trace && threadIdx.x == 0) a.trace[(size_t)k * 8 + slot] = gtimer();
+        };
+        pp_load(Ps, pslot(k), PPB);
+        if (look) mark(0);
+        if (!look && blockIdx.x == 0) mark(5);
+        if (look) {
+            if (k + 1 < nb) {  // next pivot block: W_{k+1,k+1} - (W_{k+1,k} P_k) W_{k,k+1}, inverted
+                // all inputs in one round of loads (P_k was loaded above)
+                const double* g = blk(src, k + 1, k + 1);
+                double gv[4];
+#pragma unroll
+                for (int m = 0; m < 4; ++m) gv[m] = __ldcg(g + (size_t)r * ld + c0 + 8 * m);
+                pp_load(Cs, blk(src, k + 1, k), ld);
+                pp_load(Bs, blk(src, k, k + 1), ld);
+                __syncthreads();
+                double t[4];
+                pp_mul(Cs, Ps, t);
+#pragma unroll
+                for (int m = 0; m < 4; ++m) Ts[r][c0 + 8 * m] = t[m];
+                __syncthreads();
+                pp_mul(Ts, Bs, t);
+                __syncthreads();
+#pragma unroll
+                for (int m = 0; m < 4; ++m) Cs[r][c0 + 8 * m] = gv[m] - t[m];
+                __syncthreads();
+                mark(1);
+                const long long cy0 = clock64();
+                pp_invert(Cs, xrow, a.singular);
+                if (a.trace && threadIdx.x == 0) a.trace[(size_t)k * 8 + 4] = (unsigned long long)(clock64() - cy0);
+                mark(2);
+                for (int x = threadIdx.x; x < PPB * PPB; x += blockDim.x) pslot(k + 1)[x] = Cs[x >> 5][x & 31];
+                mark(3);
+            }
+        } else {
+            for (int item = blockIdx.x; item < nb * nch; item += nwork) {
+                const int i = item / nch, q = item % nch;
+                const int col0 = q * PPW;
+                __syncthreads();  // previous item's readers of Cs / Ts / Ws are done
+                if (i != k) pp_load(Cs, blk(src, i, k), ld);
+                {  // pivot block-row slice W_k,[col0, col0+128) (columns past np read as 0), loads batched
+                    double v[PPB * PPW / 256];
+#pragma unroll
+                    for (int q = 0; q < PPB * PPW / 256; ++q) {
+                        const int x = threadIdx.x + 256 * q, rr = x / PPW, cc = col0 + x % PPW;
+                        v[q] = cc < np ? __ldcg(src + (size_t)(k * PPB + rr) * ld + cc) : 0.0;
+                    }
+#pragma unroll
+                    for (int q = 0; q < PPB * PPW / 256; ++q) Ws[threadIdx.x + 256 * q] = v[q];
+                }
+                __syncthreads();
+                if (i != k) {  // T = W_ik P_k
+                    double t[4];
+                    pp_mul(Cs, Ps, t);
+#pragma unroll
+                    for (int m = 0; m < 4; ++m) Ts[r][c0 + 8 * m] = t[m];
+                    __syncthreads();
+                }
+                const PPTile& Lf = (i == k) ? Ps : Ts;
+                double acc[4][4];
+#pragma unroll
+                for (int a2 = 0; a2 < 4; ++a2)
+#pragma unroll
+                    for (int m = 0; m < 4; ++m) acc[a2][m] = 0.0;
+#pragma unroll 4
+                for (int t = 0; t < PPB; ++t) {
+                    double xl[4], yl[4];
+#pragma unroll
+                    for (int a2 = 0; a2 < 4; ++a2) xl[a2] = Lf[4 * wy + a2][t];
+#pragma unroll
+                    for (int m = 0; m < 4; ++m) yl[m] = Ws[t * PPW + wx + 32 * m];
+#pragma unroll
+                    for (int a2 = 0; a2 < 4; ++a2)
+#pragma unroll
+                        for (int m = 0; m < 4; ++m) acc[a2][m] = fma(xl[a2], yl[m], acc[a2][m]);
+                }
+#pragma unroll
+                for (int a2 = 0; a2 < 4; ++a2) {
+                    const int row = 4 * wy + a2;
+                    double* orow = dst + (size_t)(i * PPB + row) * ld;
+                    const double* srow = src + (size_t)(i * PPB + row) * ld;
+#pragma unroll
+                    for (int m = 0; m < 4; ++m) {
+                        const int col = col0 + wx + 32 * m;
+                        if (col >= np) continue;
+                        const int jb = col / PPB, cl = col % PPB;
+                        double o;
+                        if (jb == k) o = (i == k) ? Ps[row][cl] : -Ts[row][cl];
+                        else if (i == k) o = acc[a2][m];
+                        else if (i == k + 1 && jb == k + 1) continue;  // the lookahead's block
+                        else o = __ldcg(srow + col) - acc[a2][m];
+                        orow[col] = o;
+                    }
+                }
+            }
+            if (blockIdx.x == 0) mark(6);
+        }
+        grid.sync();
+        if (blockIdx.x == 0) mark(7);
+    }
+}
+
+// npad x npad copy with identity padding (and back).
+__global__ void k_pad_in(const double* __restrict__ A, int n, double* __restrict__ W, int ld) {
+    for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < (long long)ld * ld;
+         x += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(x / ld), j = (int)(x % ld);
+        W[x] = (i < n && j < n) ? A[(size_t)i * n + j] : (i == j ? 1.0 : 0.0);
+    }
+}
+__global__ void k_pad_out(const double* __restrict__ W, int ld, double* __restrict__ A, int n) {
+    for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < (long long)n * n;
+         x += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(x / n), j = (int)(x % n);
+        A[x] = W[(size_t)i * ld + j];
+    }
+}
+
 
 // K = J M: phi-rows first, then the negated psi-rows.
 __global__ void k_j_times(const double* __restrict__ M, double* __restrict__ K, int n) {
@@ -482,7 +737,72 @@ __global__ void k_axpy(double* __restrict__ y, const double* __restrict__ x, int
 
 namespace {
 
+void block_gj_legacy(Ctx& c, double* W, int n);
+
+// In-place inverse of W (n x n) by the ping-pong blocked GJ (k_gj_pp).
 void block_gj_inplace(Ctx& c, double* W, int n) {
+    if (c.gj_legacy) {
+        block_gj_legacy(c, W, n);
+        return;
+    }
+    const int nb = cdiv(n, PPB), ld = nb * PPB;
+    c.gj_pp.alloc(std::max(c.gj_pp.n, 2 * (size_t)ld * ld + 2 * PPB * PPB));
+    c.gj_piv.alloc(std::max(c.gj_piv.n, (size_t)n + 1));
+    CK(cudaMemsetAsync(c.gj_piv.p + n, 0, sizeof(int), c.st));
+    double* W0 = c.gj_pp.p;
+    double* W1 = W0 + (size_t)ld * ld;
+    const int g = std::min(cdiv((long long)ld * ld, TPB), 8 * c.num_sms);
+    {
+        PROF(c, "k_pad_in");
+        k_pad_in<<<g, TPB, 0, c.st>>>(W, n, W0, ld);
+        CK_LAUNCH();
+    }
+    static int per_sm = -1;
+    if (per_sm < 0) {  // set once, outside any graph capture
+        CK(cudaFuncSetAttribute(k_gj_pp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PP_SMEM));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gj_pp, 256, PP_SMEM));
+    }
+    const int cap = per_sm * c.num_sms;
+    if (cap < 2) throw CudaError("dense_inverse: ping-pong Gauss-Jordan does not fit");
+    const int nch = cdiv(ld, PPW), cpb = PPW / PPB;  // work item: one block row x 128 columns
+    const int blocks = std::min(nb * nch, cap - 1) + 1;
+    static const bool trace = [] {
+        const char* e = std::getenv("MPM2P_GJ_TRACE");
+        return e && e[0] == '1';
+    }();
+    DevBuf<unsigned long long> tr;
+    if (trace) {
+        tr.alloc((size_t)nb * 8);
+        tr.zero(c.st);
+    }
+    PPArgs pa{W0, W1, W1 + (size_t)ld * ld, ld, nb, nch, cpb, c.gj_piv.p + n, trace ? tr.p : nullptr};
+    void* args[] = {&pa};
+    {
+        PROF(c, "k_gj_pp");
+        CK(cudaLaunchCooperativeKernel((void*)k_gj_pp, blocks, 256, args, PP_SMEM, c.st));
+        CK_LAUNCH();
+    }
+    {
+        PROF(c, "k_pad_out");
+        k_pad_out<<<g, TPB, 0, c.st>>>((nb & 1) ? W1 : W0, ld, W, n);
+        CK_LAUNCH();
+    }
+    if (trace) {  // developer trace: lookahead load+mul / invert / publish, worker, barrier (us)
+        std::vector<unsigned long long> h((size_t)nb * 8);
+        CK(cudaMemcpyAsync(h.data(), tr.p, h.size() * 8, cudaMemcpyDeviceToHost, c.st));
+        CK(cudaStreamSynchronize(c.st));
+        std::fprintf(stderr, "k_gj_pp n=%d nb=%d nch=%d cpb=%d blocks=%d\n", n, nb, nch, cpb, blocks);
+        for (int k = 0; k < nb && k < 6; ++k) {
+            const unsigned long long* t = h.data() + (size_t)k * 8;
+            std::fprintf(stderr,
+                         "  step %d: look prep %.2f inv %.2f (%llu cycles) pub %.2f | worker %.2f | step %.2f\n", k,
+                         (t[1] - t[0]) * 1e-3, (t[2] - t[1]) * 1e-3, t[4], (t[3] - t[2]) * 1e-3, (t[6] - t[5]) * 1e-3,
+                         (t[7] - t[5]) * 1e-3);
+        }
+    }
+}
+
+void block_gj_legacy(Ctx& c, double* W, int n) {
     c.gj_col.alloc(std::max(c.gj_col.n, (size_t)n * GJB));
     c.gj_row.alloc(std::max(c.gj_row.n, (size_t)n * GJB));
     static bool attr_set = false;  // set once, outside any graph capture
