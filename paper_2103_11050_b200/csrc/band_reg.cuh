@@ -169,16 +169,53 @@ __device__ bool factor_fwd_reg(int n, const BandRows A, double* D, double* Lcol,
     return __all_sync(FULL, ok);
 }
 
+// Prefetches in both sweeps load raw values from clamped (always valid)
+// addresses and select nothing: a value is consumed only for an existing row
+// on an active lane, so the loads never stall the step that issues them
+// (a select right after a load would). Idle lanes and missing rows carry
+// finite junk that is never stored.
+
+// Deep prefetch of the stored factor for the sweeps: whole B x B chunks of
+// Lcol / Lrow (rows k0..k0+B-1, contiguous) are copied by cp.async into a
+// per-warp shared-memory ring SWEEP_RING<B> chunks ahead (the register ring
+// alone looks only B steps ahead, shorter than an HBM round trip once L2 is
+// cold). Widths above 16 keep the register ring (0: no smem ring).
+template <int B>
+__host__ __device__ constexpr int sweep_ring() {
+    return B <= 16 ? 4 : 0;
+}
+
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Copy chunk `c` (clamped to the last chunk; rows past n are never consumed)
+// of a B-wide band factor into ring slot `slot`.
+template <int B>
+__device__ __forceinline__ void sweep_fetch(const double* Lb, int nchunks, int c, double* ring, int slot) {
+    const int cc = c < 0 ? 0 : (c < nchunks ? c : nchunks - 1);
+    const double* g = Lb + (size_t)cc * B * B;
+    double* d = ring + (size_t)slot * B * B;
+    for (int p = threadIdx.x & 31; p < B * B / 2; p += 32) cp_async16(d + 2 * p, g + 2 * p);
+    cp_async_commit();
+}
+
 // Forward sweep L y = b with a stored factor (Lcol), NR RHS in place.
 template <int B, int NR>
-__device__ void forward_reg(int n, const double* Lcol, double* Y, int nr, int ldy,
-                            double* xb) {
+__device__ void forward_reg(int n, const double* Lcol, double* Y, int nr, int ldy, double* xb,
+                            double* ring = nullptr) {
     constexpr int YS = xchg_ys<NR>();
+    constexpr int RG = sweep_ring<B>();
     const int lane = threadIdx.x & 31;
-    const bool act = lane < B;
-    auto yat = [&](int m, int row) {  // clamped (always valid) load + select
-        const double v = Y[(size_t)(m < nr ? m : nr - 1) * ldy + (row < n ? row : n - 1)];
-        return (act && row < n && m < nr) ? v : 0.0;
+    const int nchunks = n / B;
+    auto yat = [&](int m, int row) {
+        return Y[(size_t)(m < nr ? m : nr - 1) * ldy + (row < n ? row : n - 1)];
     };
     double yv[NR];
 #pragma unroll
@@ -186,25 +223,39 @@ __device__ void forward_reg(int n, const double* Lcol, double* Y, int nr, int ld
     // L entries flow through an LQ-deep register ring (step k+LQ is loaded at step k)
     constexpr int LQ = band_lq<B>();
     auto lcol_at = [&](int k, int u) {  // lane's entry of Lcol[k], u = k mod B
-        const double v = Lcol[(size_t)(k < n ? k : n - 1) * B + band_j_of<B>(lane, u)];
-        return (act && k < n) ? v : 0.0;
+        return Lcol[(size_t)(k < n ? k : n - 1) * B + band_j_of<B>(lane, u)];
     };
     double lq[LQ];
+    if constexpr (RG > 0) {
 #pragma unroll
-    for (int t = 0; t < LQ; ++t) lq[t] = lcol_at(t, t % B);
+        for (int c = 0; c < RG; ++c) sweep_fetch<B>(Lcol, nchunks, c, ring, c);
+    } else {
+#pragma unroll
+        for (int t = 0; t < LQ; ++t) lq[t] = lcol_at(t, t % B);
+    }
     double cb[NR], nbv[NR];
 #pragma unroll
     for (int m = 0; m < NR; ++m) cb[m] = yat(m, B + lane);
     for (int k0 = 0; k0 < n; k0 += B) {
 #pragma unroll
         for (int m = 0; m < NR; ++m) nbv[m] = yat(m, k0 + 2 * B + lane);
+        if constexpr (RG > 0) {  // chunk k0/B has landed: its B entries of this lane into registers
+            const int c = k0 / B, slot = c % RG;
+            cp_async_wait<RG - 1>();
+            __syncwarp();
+            const double* rs = ring + (size_t)slot * B * B;
+#pragma unroll
+            for (int u = 0; u < B; ++u) lq[u] = rs[u * B + band_j_of<B>(lane, u)];
+            __syncwarp();
+            sweep_fetch<B>(Lcol, nchunks, c + RG, ring, slot);
+        }
 #pragma unroll
         for (int u = 0; u < B; ++u) {
             const int k = k0 + u;
             const bool piv = lane == u;
             const double keep = piv ? 0.0 : 1.0;
             const double l = lq[u % LQ];
-            lq[u % LQ] = lcol_at(k + LQ, (u + LQ) % B);
+            if constexpr (RG == 0) lq[u % LQ] = lcol_at(k + LQ, (u + LQ) % B);
             double yk[NR];
             if constexpr (NR == 1) {
                 yk[0] = __shfl_sync(FULL, yv[0], u);
@@ -220,7 +271,7 @@ __device__ void forward_reg(int n, const double* Lcol, double* Y, int nr, int ld
             }
 #pragma unroll
             for (int m = 0; m < NR; ++m) {
-                if (piv && m < nr) Y[(size_t)m * ldy + k] = yk[m];
+                st_global_if(Y + (size_t)m * ldy + k, yk[m], piv && m < nr);
                 yv[m] = fma(-l, yk[m], fma(yv[m], keep, piv ? cb[m] : 0.0));
             }
         }
@@ -231,47 +282,65 @@ __device__ void forward_reg(int n, const double* Lcol, double* Y, int nr, int ld
 
 // Backward sweep L^T x = D^-1 y with a stored factor (Lrow, D), NR RHS in place.
 template <int B, int NR>
-__device__ void backward_reg(int n, const double* D, const double* Lrow,
-                             double* Y, int nr, int ldy, double* xb) {
+__device__ void backward_reg(int n, const double* D, const double* Lrow, double* Y, int nr, int ldy, double* xb,
+                             double* ring = nullptr) {
     constexpr int YS = xchg_ys<NR>();
+    constexpr int RG = sweep_ring<B>();
     const int lane = threadIdx.x & 31;
-    const bool act = lane < B;
-    // entering value z = y / d of row `row` (0 outside the matrix); clamped loads
-    auto zat = [&](int row, double* out) {
-        const bool ok = act && row >= 0;
-        const int rr = ok ? row : 0;  // lanes >= B would address past the subdomain
-        const double dinv = 1.0 / D[rr];
+    const int nchunks = n / B;
+    // raw (d, y) of row `row`; z = y * (1/d) is formed one chunk later, at use
+    auto raw = [&](int row, double& d, double* y) {
+        const int rr = row < 0 ? 0 : (row < n ? row : n - 1);
+        d = D[rr];
 #pragma unroll
-        for (int m = 0; m < NR; ++m) {
-            const double v = Y[(size_t)(m < nr ? m : nr - 1) * ldy + rr];
-            out[m] = (ok && m < nr) ? v * dinv : 0.0;
-        }
+        for (int m = 0; m < NR; ++m) y[m] = Y[(size_t)(m < nr ? m : nr - 1) * ldy + rr];
     };
-    double z[NR];
-    zat(n - B + lane, z);  // row n-B+lane == lane (mod B)
+    auto scale = [&](double d, const double* y, double* z) {
+        const double dinv = 1.0 / d;
+#pragma unroll
+        for (int m = 0; m < NR; ++m) z[m] = y[m] * dinv;
+    };
+    double z[NR], ez[NR], rd, ry[NR];
+    raw(n - B + lane, rd, ry);  // row n-B+lane == lane (mod B)
+    scale(rd, ry, z);
     constexpr int LQ = band_lq<B>();
     auto lrow_at = [&](int k, int u) {  // lane's entry of Lrow[k]: o = (lane - u) mod B, u = k mod B
-        const double v = Lrow[(size_t)(k >= 0 ? k : 0) * B + (lane - u + B) % B];
-        return (act && k >= 0) ? v : 0.0;
+        return Lrow[(size_t)(k >= 0 ? k : 0) * B + (lane - u + B) % B];
     };
-    double lq[LQ], ez[NR], nz[NR];
+    double lq[LQ];
     const int k0_last = n - B;
-    // ring slot of step k is (k mod LQ); prefill steps n-1 .. n-LQ
+    if constexpr (RG > 0) {  // chunks are consumed last to first: ring position i holds chunk nchunks-1-i
 #pragma unroll
-    for (int t = 0; t < LQ; ++t) {
-        const int u = B - 1 - t;  // k = k0_last + u
-        lq[u % LQ] = lrow_at(k0_last + u, u);
+        for (int i = 0; i < RG; ++i) sweep_fetch<B>(Lrow, nchunks, nchunks - 1 - i, ring, i);
+    } else {
+        // ring slot of step k is (k mod LQ); prefill steps n-1 .. n-LQ
+#pragma unroll
+        for (int t = 0; t < LQ; ++t) {
+            const int u = B - 1 - t;  // k = k0_last + u
+            lq[u % LQ] = lrow_at(k0_last + u, u);
+        }
     }
-    zat(k0_last - B + lane, ez);
+    raw(k0_last - B + lane, rd, ry);
     for (int k0 = k0_last; k0 >= 0; k0 -= B) {
-        zat(k0 - 2 * B + lane, nz);
+        scale(rd, ry, ez);                 // entering rows of this chunk (loaded one chunk ago)
+        raw(k0 - 2 * B + lane, rd, ry);    // ... and of the next
+        if constexpr (RG > 0) {
+            const int i = nchunks - 1 - k0 / B, slot = i % RG;
+            cp_async_wait<RG - 1>();
+            __syncwarp();
+            const double* rs = ring + (size_t)slot * B * B;
+#pragma unroll
+            for (int u = 0; u < B; ++u) lq[u] = rs[u * B + (lane - u + B) % B];
+            __syncwarp();
+            sweep_fetch<B>(Lrow, nchunks, nchunks - 1 - (i + RG), ring, slot);
+        }
 #pragma unroll
         for (int uu = B - 1; uu >= 0; --uu) {
             const int k = k0 + uu;
             const bool piv = lane == uu;
             const double keep = piv ? 0.0 : 1.0;
             const double l = lq[uu % LQ];
-            lq[uu % LQ] = lrow_at(k - LQ, (uu + B - LQ % B) % B);
+            if constexpr (RG == 0) lq[uu % LQ] = lrow_at(k - LQ, (uu + B - LQ % B) % B);
             double xk[NR];
             if constexpr (NR == 1) {
                 xk[0] = __shfl_sync(FULL, z[0], uu);
@@ -287,12 +356,10 @@ __device__ void backward_reg(int n, const double* D, const double* Lrow,
             }
 #pragma unroll
             for (int m = 0; m < NR; ++m) {
-                if (piv && m < nr) Y[(size_t)m * ldy + k] = xk[m];
+                st_global_if(Y + (size_t)m * ldy + k, xk[m], piv && m < nr);
                 z[m] = fma(-l, xk[m], fma(z[m], keep, piv ? ez[m] : 0.0));
             }
         }
-#pragma unroll
-        for (int m = 0; m < NR; ++m) ez[m] = nz[m];
     }
 }
 

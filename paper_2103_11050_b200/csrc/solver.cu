@@ -682,6 +682,7 @@ __global__ void __launch_bounds__(WPB * 32) k_ds_solve_r(Layout L, const double*
                                                          double* p, Scalars* sc) {
     __shared__ double stage[WPB][B * B];
     __shared__ __align__(16) double xbuf[WPB][xchg_doubles<B, 1>()];
+    __shared__ __align__(16) double ring[WPB][sweep_ring<B>() * B * B + 2];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int s = blockIdx.x * WPB + w;
     if (s >= L.n_sub) return;
@@ -692,7 +693,7 @@ __global__ void __launch_bounds__(WPB * 32) k_ds_solve_r(Layout L, const double*
     const bool ok = factor_fwd_reg<B, 1>(n, A, D + so, nullptr, Lr + so * B, x, 1, n, stage[w], xbuf[w]);
     if (!ok && lane == 0) atomicOr(&sc->err, ERR_PIVOT);
     __syncwarp();
-    backward_reg<B, 1>(n, D + so, Lr + so * B, x, 1, n, xbuf[w]);
+    backward_reg<B, 1>(n, D + so, Lr + so * B, x, 1, n, xbuf[w], ring[w]);
     __syncwarp();
     double v = 0.0;
     for (int r = lane; r < n; r += 32) v += x[r];
@@ -705,15 +706,16 @@ template <int B>
 __global__ void __launch_bounds__(WPB * 32) k_part_solve_r(Layout L, int max_rhs, const double* __restrict__ D,
                                                            const double* __restrict__ Lc,
                                                            const double* __restrict__ Lr, double* X) {
+    __shared__ __align__(16) double ring[WPB][sweep_ring<B>() * B * B + 2];
     const int w = threadIdx.x >> 5;
     const int s = blockIdx.x * WPB + w;
     if (s >= L.n_sub) return;
     const int n = L.ncs;
     const size_t so = (size_t)s * n;
     double* x = X + xoff(L, max_rhs, s, 0);
-    forward_reg<B, 1>(n, Lc + so * B, x, 1, n, nullptr);
+    forward_reg<B, 1>(n, Lc + so * B, x, 1, n, nullptr, ring[w]);
     __syncwarp();
-    backward_reg<B, 1>(n, D + so, Lr + so * B, x, 1, n, nullptr);
+    backward_reg<B, 1>(n, D + so, Lr + so * B, x, 1, n, nullptr, ring[w]);
 }
 
 // RHS carried through one register sweep of the rebuild (1 particular + up to
@@ -731,6 +733,7 @@ __global__ void __launch_bounds__(WPB * 32) k_factor_solve_r(Layout L, int max_r
                                                              double* X, Scalars* sc) {
     __shared__ double stage[WPB][B * B];
     __shared__ __align__(16) double xbuf[WPB][xchg_doubles<B, NR_REG>()];
+    __shared__ __align__(16) double ring[WPB][sweep_ring<B>() * B * B + 2];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int s = blockIdx.x * WPB + w;
     if (s >= L.n_sub) return;
@@ -746,12 +749,12 @@ __global__ void __launch_bounds__(WPB * 32) k_factor_solve_r(Layout L, int max_r
     __syncwarp();
     for (int m0 = n0; m0 < nr; m0 += NR_REG) {
         const int cnt = nr - m0 < NR_REG ? nr - m0 : NR_REG;
-        forward_reg<B, NR_REG>(n, Lc + so * B, Xs + (size_t)m0 * n, cnt, n, xbuf[w]);
+        forward_reg<B, NR_REG>(n, Lc + so * B, Xs + (size_t)m0 * n, cnt, n, xbuf[w], ring[w]);
         __syncwarp();
     }
     for (int m0 = 0; m0 < nr; m0 += NR_REG) {
         const int cnt = nr - m0 < NR_REG ? nr - m0 : NR_REG;
-        backward_reg<B, NR_REG>(n, D + so, Lr + so * B, Xs + (size_t)m0 * n, cnt, n, xbuf[w]);
+        backward_reg<B, NR_REG>(n, D + so, Lr + so * B, Xs + (size_t)m0 * n, cnt, n, xbuf[w], ring[w]);
         __syncwarp();
     }
 }

@@ -17,13 +17,14 @@ __global__ void k_check(int n, const double* BD, const double* BW, const double*
                         double* Lr, double* Y, int nr, int two_pass) {
     __shared__ double stage[B * B];
     __shared__ __align__(16) double xb[xchg_doubles<B, NR>()];
+    __shared__ __align__(16) double ring[sweep_ring<B>() * B * B + 2];
     const BandRows A{BD, BW, BS};
     const int n0 = two_pass ? (nr < NR ? nr : NR) : nr;
     factor_fwd_reg<B, NR>(n, A, D, Lc, Lr, Y, n0, n, stage, xb);
     __syncwarp();
-    if (two_pass && nr > n0) forward_reg<B, NR>(n, Lc, Y + (size_t)n0 * n, nr - n0, n, xb);
+    if (two_pass && nr > n0) forward_reg<B, NR>(n, Lc, Y + (size_t)n0 * n, nr - n0, n, xb, ring);
     __syncwarp();
-    backward_reg<B, NR>(n, D, Lr, Y, nr, n, xb);
+    backward_reg<B, NR>(n, D, Lr, Y, nr, n, xb, ring);
 }
 
 // Same as k_check with 4 warps per block, one independent system per warp
@@ -33,12 +34,13 @@ __global__ void k_check4(int n, const double* BD, const double* BW, const double
                          double* Lr, double* Y, int nr) {
     __shared__ double stage[4][B * B];
     __shared__ __align__(16) double xb[4][xchg_doubles<B, NR>()];
+    __shared__ __align__(16) double ring[4][sweep_ring<B>() * B * B + 2];
     const int w = threadIdx.x >> 5;
     const BandRows A{BD, BW, BS};
     double* Yw = Y + (size_t)w * nr * n;
     factor_fwd_reg<B, NR>(n, A, D + w * n, Lc + (size_t)w * n * B, Lr + (size_t)w * n * B, Yw, nr, n, stage[w], xb[w]);
     __syncwarp();
-    backward_reg<B, NR>(n, D + w * n, Lr + (size_t)w * n * B, Yw, nr, n, xb[w]);
+    backward_reg<B, NR>(n, D + w * n, Lr + (size_t)w * n * B, Yw, nr, n, xb[w], ring[w]);
 }
 
 template <int B, int NR>
