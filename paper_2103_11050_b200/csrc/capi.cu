@@ -432,28 +432,33 @@ bool run_step(mpm2p_ctx* ctx, mpm2p_step_record* out) {
     // captured once per run as a CUDA graph (MPM-2P reuse / MRCM rebuild) and
     // replayed, so the device runs the ~30 kernels back to back. Profiling
     // mode launches them eagerly so each kernel can be timed.
+    // cn upwind sub-steps ping-pong between s and s2; the step's saturation
+    // ends in `cur` and the buffers are swapped afterwards (no copy)
+    double* cur = (sp.cn % 2 == 1) ? c.s2.p : c.s.p;
     auto body = [&] {
-        launch_cfl(c, c.u, sp.cfl_safety, sp.dt_cap);
-        launch_inj_pvi(c, c.u, sp.inflow_sat, sp.cn, true);
+        launch_cfl_inj(c, c.u, sp.cfl_safety, sp.dt_cap, sp.inflow_sat, sp.cn);
         for (int k = 0; k < sp.cn; ++k) {
             launch_upwind(c, k % 2 == 0 ? c.s : c.s2, k % 2 == 0 ? c.s2 : c.s, c.u, sp.inflow_sat);
         }
-        if (sp.cn % 2 == 1)
-            CK(cudaMemcpyAsync(c.s.p, c.s2.p, c.L.cells() * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
-        launch_conductivity(c, c.s, c.kappa_n, sp.eta_mode, true);
+        launch_conductivity_decide(c, cur, c.kappa_n, sp.eta_mode, rebuilt, sp.method, sp.eta);
+        c.outlet_s = cur;  // the step's last k_divres also takes max_outlet_saturation
         if (rebuilt) {
             launch_rebuild(c, c.kappa_n);
-            launch_lambda(c, c.s, c.lam_reb);
+            launch_lambda(c, cur, c.lam_reb);
         } else {
             launch_mpm(c, c.kappa_n);
         }
-        launch_decide(c, rebuilt, sp.method, sp.eta, 1);
-        launch_outlet(c, c.s, c.u);
+        c.outlet_s = nullptr;
     };
     if (c.profiling || !c.use_graphs) {
-        body();
+        try {
+            body();
+        } catch (...) {
+            c.outlet_s = nullptr;
+            throw;
+        }
     } else {
-        cudaGraphExec_t& g = rebuilt ? c.g_rebuild : c.g_mpm;
+        cudaGraphExec_t& g = rebuilt ? c.g_rebuild[c.s_par] : c.g_mpm[c.s_par];
         long long* delta = rebuilt ? c.gd_rebuild : c.gd_mpm;
         if (!g) {
             const long long before[5] = {c.c_hom, c.c_part, c.c_down, c.c_fine, c.c_iface};
@@ -462,6 +467,7 @@ bool run_step(mpm2p_ctx* ctx, mpm2p_step_record* out) {
             try {
                 body();
             } catch (...) {
+                c.outlet_s = nullptr;
                 cudaGraph_t dummy = nullptr;
                 cudaStreamEndCapture(c.st, &dummy);
                 if (dummy) cudaGraphDestroy(dummy);
@@ -488,6 +494,10 @@ bool run_step(mpm2p_ctx* ctx, mpm2p_step_record* out) {
         c.c_fine += delta[3];
         c.c_iface += delta[4];
         c.launch_count += delta[5];
+    }
+    if (sp.cn % 2 == 1) {
+        std::swap(c.s.p, c.s2.p);
+        c.s_par ^= 1;
     }
     const Scalars& s = sync_scalars(c);
     note(d, s);

@@ -114,4 +114,35 @@ __device__ __forceinline__ double reduce_partials(const double* part, int nparts
     return block_reduce_op(v, op, ident, sh);
 }
 
+// N values reduced at once (bit `i` of sum_mask: slot i is a sum, else a
+// max), one barrier: warp shuffles per slot, then thread i < N combines the
+// warps of slot i. Results land in out[0..N-1] (shared), valid after the
+// trailing barrier. sh must hold 32 * N doubles.
+template <int N>
+__device__ __forceinline__ void block_reduce_multi(double (&v)[N], unsigned sum_mask, double* sh, double* out) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        const bool sm = (sum_mask >> i) & 1u;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double t = __shfl_down_sync(0xffffffffu, v[i], o);
+            v[i] = sm ? v[i] + t : fmax(v[i], t);
+        }
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) sh[w * N + i] = v[i];
+    }
+    __syncthreads();
+    if (threadIdx.x < N) {
+        const int i = threadIdx.x;
+        const bool sm = (sum_mask >> i) & 1u;
+        double a = sh[i];
+        for (int ww = 1; ww < nw; ++ww) a = sm ? a + sh[ww * N + i] : fmax(a, sh[ww * N + i]);
+        out[i] = a;
+    }
+    __syncthreads();
+}
+
 }  // namespace mpm2p

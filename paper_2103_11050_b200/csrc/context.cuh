@@ -112,12 +112,18 @@ struct Ctx {
     // per-run CUDA graphs of one driver step (MPM-2P reuse / MRCM rebuild)
     bool use_graphs = true;
     bool no_regband = false;  // MPM2P_NO_REGBAND=1: generic shared-memory band kernels only
-    cudaGraphExec_t g_mpm = nullptr, g_rebuild = nullptr;
+    // one graph per (branch, saturation-buffer parity): the upwind ping-pong
+    // swaps s/s2 instead of copying, so the captured pointers alternate
+    cudaGraphExec_t g_mpm[2] = {}, g_rebuild[2] = {};
     long long gd_mpm[6] = {}, gd_rebuild[6] = {};  // counter / launch deltas per replay
+    int s_par = 0;                                 // parity of the s/s2 pointer swap
+    const double* outlet_s = nullptr;              // set during driver steps: k_divres also probes the outlet
     void drop_graphs() {
-        if (g_mpm) cudaGraphExecDestroy(g_mpm);
-        if (g_rebuild) cudaGraphExecDestroy(g_rebuild);
-        g_mpm = g_rebuild = nullptr;
+        for (int i = 0; i < 2; ++i) {
+            if (g_mpm[i]) cudaGraphExecDestroy(g_mpm[i]);
+            if (g_rebuild[i]) cudaGraphExecDestroy(g_rebuild[i]);
+            g_mpm[i] = g_rebuild[i] = nullptr;
+        }
     }
     bool has_basis = false;
     bool has_factor = false;
@@ -198,6 +204,9 @@ void launch_cfl(Ctx& c, const double* u, double safety, double dt_cap);
 void launch_inj_pvi(Ctx& c, const double* u, double inflow, int cn, bool add_pvi);
 void launch_upwind(Ctx& c, const double* s_in, double* s_out, const double* u, double inflow);
 void launch_conductivity(Ctx& c, const double* s, double* kappa, int eps_mode, bool want_eps);
+void launch_cfl_inj(Ctx& c, const double* u, double safety, double dt_cap, double inflow, int cn);
+void launch_conductivity_decide(Ctx& c, const double* s, double* kappa, int eps_mode, int rebuilt, int method,
+                                double eta);
 void launch_outlet(Ctx& c, const double* s, const double* u);
 void launch_lambda(Ctx& c, const double* s, double* lam);
 void launch_divergence(Ctx& c, const double* u, double* div);

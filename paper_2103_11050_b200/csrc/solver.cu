@@ -801,12 +801,19 @@ __global__ void k_ds_u(Layout L, const double* __restrict__ T, const double* __r
 }
 
 // max_c |div u - q| and max(|q|, |u_f| area / vol) (mrcm.cpp:429-437).
+// Divergence residual of the downscaled velocity (simulation.cpp:176-181).
+// With s_out != nullptr (driver steps) it also evaluates
+// max_outlet_saturation (simulation.cpp:61-83) grid-parallel: per side the
+// net outflow sum and the max saturation over outflow faces, combined by the
+// last block (a side counts when its net outflow exceeds 1e-14).
 __global__ void k_divres(Layout L, const double* __restrict__ u, const double* __restrict__ q, Scalars* sc,
-                         double* part, unsigned* counter) {
-    __shared__ double sh[32];
-    double res = 0.0, scale = 0.0;
+                         double* part, unsigned* counter, const double* __restrict__ s_out = nullptr) {
+    constexpr int NP = 10;  // res, scale, 4 x side net, 4 x side max
+    double res = 0.0, scale = 0.0, net[4] = {0.0, 0.0, 0.0, 0.0}, smax[4] = {0.0, 0.0, 0.0, 0.0};
     const double vol = L.vol();
-    const int n = L.cells() > L.faces() ? L.cells() : L.faces();
+    const int nbt = s_out ? 2 * (L.nx + L.ny) : 0;
+    int n = L.cells() > L.faces() ? L.cells() : L.faces();
+    n = n > nbt ? n : nbt;
     for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
         if (x < L.cells()) {
             const int i = x % L.nx, j = x / L.nx;
@@ -816,20 +823,50 @@ __global__ void k_divres(Layout L, const double* __restrict__ u, const double* _
             scale = fmax(scale, fabs(q[x]));
         }
         if (x < L.faces()) scale = fmax(scale, fabs(u[x]) * L.area(x) / vol);
+        if (x < nbt) {  // boundary face x: sides W (ny), E (ny), S (nx), N (nx)
+            int side, k;
+            if (x < 2 * L.ny) side = x / L.ny, k = x % L.ny;
+            else side = 2 + (x - 2 * L.ny) / L.nx, k = (x - 2 * L.ny) % L.nx;
+            double fo;
+            int cell;
+            if (side == 0) fo = -u[L.vface(0, k)], cell = L.cell(0, k);
+            else if (side == 1) fo = u[L.vface(L.nx, k)], cell = L.cell(L.nx - 1, k);
+            else if (side == 2) fo = -u[L.hface(k, 0)], cell = L.cell(k, 0);
+            else fo = u[L.hface(k, L.ny)], cell = L.cell(k, L.ny - 1);
+            const double area = side < 2 ? L.hy : L.hx;
+#pragma unroll
+            for (int sd = 0; sd < 4; ++sd) {
+                if (sd != side) continue;
+                net[sd] += fo * area;
+                if (fo > 1e-14) smax[sd] = fmax(smax[sd], s_out[cell]);
+            }
+        }
     }
-    res = block_max(res, sh);
-    scale = block_max(scale, sh);
-    if (threadIdx.x == 0) {
-        part[2 * blockIdx.x] = res;
-        part[2 * blockIdx.x + 1] = scale;
-    }
+    __shared__ double shm[32 * NP];
+    __shared__ double red[NP];
+    constexpr unsigned SUMS = 0x3Cu;  // slots 2..5 (side nets) are sums, the rest maxima
+    double v[NP] = {res, scale, net[0], net[1], net[2], net[3], smax[0], smax[1], smax[2], smax[3]};
+    block_reduce_multi<NP>(v, SUMS, shm, red);
+    if (threadIdx.x < NP) part[NP * blockIdx.x + threadIdx.x] = red[threadIdx.x];
     if (last_block_done(counter)) {
-        auto mx = [](double a, double b) { return fmax(a, b); };
-        const double r = reduce_partials(part, gridDim.x, 2, 0, mx, 0.0, sh);
-        const double sc2 = reduce_partials(part, gridDim.x, 2, 1, mx, 0.0, sh);
+        double a[NP];
+#pragma unroll
+        for (int i = 0; i < NP; ++i) a[i] = 0.0;  // identity of both (all maxima are of |x| or s >= 0)
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+#pragma unroll
+            for (int i = 0; i < NP; ++i) {
+                const double t = __ldcg(part + (size_t)NP * b + i);
+                a[i] = ((SUMS >> i) & 1u) ? a[i] + t : fmax(a[i], t);
+            }
+        }
+        block_reduce_multi<NP>(a, SUMS, shm, red);
         if (threadIdx.x == 0) {
-            sc->div_residual = r;
-            sc->div_scale = sc2 > 0.0 ? sc2 : 1.0;
+            double om = 0.0;
+            for (int sd = 0; sd < 4; ++sd)
+                if (red[2 + sd] > 1e-14) om = fmax(om, red[6 + sd]);
+            sc->div_residual = red[0];
+            sc->div_scale = red[1] > 0.0 ? red[1] : 1.0;
+            if (s_out) sc->outlet_max = om;
             *counter = 0;
         }
     }
@@ -1105,8 +1142,8 @@ void downscale(Ctx& c, const double* kappa) {
     }
     {
         PROF(c, "k_divres");
-        k_divres<<<std::min(grid_for(std::max(L.cells(), L.faces())), 2 * c.num_sms), TPB, 0, c.st>>>(L, c.u, c.q, c.sc,
-                                                                                                   c.red, c.red_count);
+        k_divres<<<std::min(grid_for(std::max(L.cells(), L.faces())), 2 * c.num_sms), TPB, 0, c.st>>>(
+            L, c.u, c.q, c.sc, c.red, c.red_count, c.outlet_s);
         CK_LAUNCH();
     }
     c.c_down += L.n_sub;

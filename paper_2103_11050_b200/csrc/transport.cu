@@ -95,8 +95,12 @@ __global__ void k_max_slope(Scalars* sc, double M) {  // transport.cpp:45-49
 }
 
 // cfl_timestep (transport.cpp:51-71): min over cells of vol/(outflux*slope).
+__device__ double inj_rate_block(const Layout& L, const double* __restrict__ u, double fin, double* sh);
+
+// With inj_cn > 0 the last block also evaluates injection_rate and advances
+// the PVI clock inj_cn times (the driver's k_cfl + k_inj_pvi in one launch).
 __global__ void k_cfl(Layout L, const double* __restrict__ u, Scalars* sc, double safety, double dt_cap,
-                      double* part, unsigned* counter) {
+                      double* part, unsigned* counter, int inj_cn = 0, double inflow = 0.0, double M = 1.0) {
     __shared__ double sh[32];
     const double vol = L.vol(), slope = sc->slope;
     double best = INFINITY;
@@ -133,6 +137,14 @@ __global__ void k_cfl(Layout L, const double* __restrict__ u, Scalars* sc, doubl
             sc->dt = anyf ? fmin(safety * dt, dt_cap) : dt_cap;
             *counter = 0;
         }
+        if (inj_cn > 0) {
+            const double rate = inj_rate_block(L, u, frac_flow(inflow, M, nullptr), sh);
+            if (threadIdx.x == 0) {
+                sc->inj = rate;
+                const double pore = L.lx * L.ly;
+                for (int k = 0; k < inj_cn; ++k) sc->pvi += rate * sc->dt / pore;
+            }
+        }
     }
 }
 
@@ -140,10 +152,7 @@ __global__ void k_cfl(Layout L, const double* __restrict__ u, Scalars* sc, doubl
 // are the reference's; only the summation order differs — the PVI clock is a
 // reported quantity, not a parity one), then the PVI clock advanced cn times
 // (simulation.cpp:288).
-__global__ void k_inj_pvi(Layout L, const double* __restrict__ u, Scalars* sc, double inflow, double M, int cn,
-                          int add_pvi) {
-    __shared__ double sh[32];
-    const double fin = frac_flow(inflow, M, nullptr);
+__device__ double inj_rate_block(const Layout& L, const double* __restrict__ u, double fin, double* sh) {
     const int nterms = 2 * (L.nx + L.ny);
     double rate = 0.0;
     for (int idx = threadIdx.x; idx < nterms; idx += blockDim.x) {
@@ -159,7 +168,13 @@ __global__ void k_inj_pvi(Layout L, const double* __restrict__ u, Scalars* sc, d
         }
         if (un < 0.0) rate += -un * area * fin;
     }
-    rate = block_reduce_op(rate, [](double a, double b) { return a + b; }, 0.0, sh);
+    return block_reduce_op(rate, [](double a, double b) { return a + b; }, 0.0, sh);
+}
+
+__global__ void k_inj_pvi(Layout L, const double* __restrict__ u, Scalars* sc, double inflow, double M, int cn,
+                          int add_pvi) {
+    __shared__ double sh[32];
+    const double rate = inj_rate_block(L, u, frac_flow(inflow, M, nullptr), sh);
     if (threadIdx.x == 0) {
         sc->inj = rate;
         if (add_pvi) {
@@ -206,10 +221,14 @@ __global__ void k_upwind(Layout L, const double* __restrict__ s, double* __restr
 // conductivity (transport.cpp:122-126) + the drift partial sums
 // (mpm.cpp:14-20 / simulation.cpp:169-172) in double-double.
 // eps_mode: -1 none, 0 relative, 1 absolute, 2 mobility (vs lam_reb)
+__device__ __forceinline__ void decide(Scalars* sc, int rebuilt, int method, double eta, int step);
+
+// With decide_method >= 0 the last block also takes the next-step decision
+// (k_decide) from the drift it just formed.
 __global__ void k_kappa(Layout L, const double* __restrict__ K, const double* __restrict__ s,
                         double* __restrict__ kappa, const double* __restrict__ kappa_m,
                         const double* __restrict__ lam_reb, Scalars* sc, double M, int eps_mode, double* part,
-                        unsigned* counter) {
+                        unsigned* counter, int decide_method = -1, int rebuilt = 0, double eta = 0.0) {
     __shared__ DD shd[32];
     const double vol = L.vol();
     DD num{0.0, 0.0}, den{0.0, 0.0};
@@ -254,13 +273,14 @@ __global__ void k_kappa(Layout L, const double* __restrict__ K, const double* __
             sc->eps_den_hi = d.hi;
             sc->eps_den_lo = d.lo;
             *counter = 0;
+            if (decide_method >= 0) decide(sc, rebuilt, decide_method, eta, 1);
         }
     }
 }
 
 // The MPM-2P vs MRCM decision for the NEXT step, on the device
 // (simulation.cpp:307-323): eps is exactly 0 after a rebuild.
-__global__ void k_decide(Scalars* sc, int rebuilt, int method, double eta, int step) {
+__device__ __forceinline__ void decide(Scalars* sc, int rebuilt, int method, double eta, int step) {
     const double eps = rebuilt ? 0.0 : sc->eps_pending;
     sc->eps = eps;
     int rb = 0;
@@ -271,6 +291,9 @@ __global__ void k_decide(Scalars* sc, int rebuilt, int method, double eta, int s
         const double m = fabs(eps - eta) / eta;
         if (m < sc->min_margin) sc->min_margin = m;
     }
+}
+__global__ void k_decide(Scalars* sc, int rebuilt, int method, double eta, int step) {
+    decide(sc, rebuilt, method, eta, step);
 }
 
 // max_outlet_saturation (simulation.cpp:61-83): one block, four sides.
@@ -393,6 +416,18 @@ void launch_upwind(Ctx& c, const double* s_in, double* s_out, const double* u, d
         k_upwind<<<cdiv(c.L.cells(), TPB), TPB, 0, c.st>>>(c.L, s_in, s_out, u, c.sc, inflow, c.M);
         CK_LAUNCH();
     }
+}
+void launch_cfl_inj(Ctx& c, const double* u, double safety, double dt_cap, double inflow, int cn) {
+    PROF(c, "k_cfl");
+    k_cfl<<<red_grid(c), TPB, 0, c.st>>>(c.L, u, c.sc, safety, dt_cap, c.red, c.red_count, cn, inflow, c.M);
+    CK_LAUNCH();
+}
+void launch_conductivity_decide(Ctx& c, const double* s, double* kappa, int eps_mode, int rebuilt, int method,
+                                double eta) {
+    PROF(c, "k_kappa");
+    k_kappa<<<red_grid(c), TPB, 0, c.st>>>(c.L, c.K, s, kappa, c.kappa_m, c.lam_reb, c.sc, c.M, eps_mode, c.red,
+                                           c.red_count, method, rebuilt, eta);
+    CK_LAUNCH();
 }
 void launch_conductivity(Ctx& c, const double* s, double* kappa, int eps_mode, bool want_eps) {
     {
