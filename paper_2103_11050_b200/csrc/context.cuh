@@ -235,6 +235,7 @@ void interface_inverse_async(Ctx& c, const double* M, double* Minv, int n, doubl
 // SPD matrix (repair Laplacian): pivot-free blocked GJ; returns rcond.
 double spd_inverse(Ctx& c, const double* A, double* Ainv, int n);
 void launch_gemv(Ctx& c, const double* A, const double* x, double* y, int n);
+void launch_gemv_acc(Ctx& c, const double* A, const double* x, double* y, int n);  // y += A x
 void launch_csr_residual(Ctx& c, const int* ptr, const int* col, const double* val, const double* x,
                          const double* b, double* r, int n);
 void launch_axpy(Ctx& c, double* y, const double* x, int n);

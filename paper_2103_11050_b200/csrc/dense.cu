@@ -690,32 +690,40 @@ __global__ void k_rcond(const double* __restrict__ part, int n, int nrb, const i
 // y = A x: a 256-thread block covers 2 rows, 4 warps per row, each warp a
 // quarter of the row with 4 independent loads in flight per lane (the GEMV is
 // load-latency bound at these sizes, so more bytes in flight is the lever).
-__global__ void __launch_bounds__(256) k_gemv(const double* __restrict__ A, const double* __restrict__ x,
-                                              double* __restrict__ y, int n) {
-    __shared__ double part[8];
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int r = blockIdx.x * 2 + (w >> 2), q = w & 3;
-    double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
-    if (r < n) {
-        const int cw = (n + 3) / 4, j0 = q * cw, j1 = min(n, j0 + cw);
-        const double* row = A + (size_t)r * n;
-        int j = j0 + lane;
-        for (; j + 96 < j1; j += 128) {
-            v0 += __ldg(row + j) * __ldg(x + j);
-            v1 += __ldg(row + j + 32) * __ldg(x + j + 32);
-            v2 += __ldg(row + j + 64) * __ldg(x + j + 64);
-            v3 += __ldg(row + j + 96) * __ldg(x + j + 96);
+// y = A x (ACC: y += A x), one warp per row. HBM-bound: every lane issues
+// its 16-byte loads of the row (and of x, L1/L2-resident) for 256 columns
+// before any FMA, so ~8 KB per warp is in flight. Rows must be 16-byte
+// aligned (n even); odd n takes the scalar loop.
+template <bool ACC>
+__global__ void __launch_bounds__(256) k_gemv_w(const double* __restrict__ A, const double* __restrict__ x,
+                                                double* __restrict__ y, int n) {
+    const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (row >= n) return;
+    const double* a = A + (size_t)row * n;
+    double acc0 = 0.0, acc1 = 0.0;
+    if ((n & 1) == 0) {
+        const double2* a2 = reinterpret_cast<const double2*>(a);
+        const double2* x2 = reinterpret_cast<const double2*>(x);
+        const int n2 = n >> 1;
+        for (int base = 0; base < n2; base += 256) {
+            double2 av[8], xv[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                const int q = base + lane + 32 * t;
+                av[t] = q < n2 ? __ldg(a2 + q) : make_double2(0.0, 0.0);
+                xv[t] = q < n2 ? __ldg(x2 + q) : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                acc0 = fma(av[t].x, xv[t].x, acc0);
+                acc1 = fma(av[t].y, xv[t].y, acc1);
+            }
         }
-        for (; j < j1; j += 32) v0 += __ldg(row + j) * __ldg(x + j);
+    } else {
+        for (int j = lane; j < n; j += 32) acc0 = fma(__ldg(a + j), __ldg(x + j), acc0);
     }
-    const double v = warp_sum((v0 + v1) + (v2 + v3));
-    if (lane == 0) part[w] = v;
-    __syncthreads();
-    if (threadIdx.x < 2) {
-        const int rr = blockIdx.x * 2 + threadIdx.x;
-        if (rr < n) y[rr] = (part[4 * threadIdx.x] + part[4 * threadIdx.x + 1]) +
-                            (part[4 * threadIdx.x + 2] + part[4 * threadIdx.x + 3]);
-    }
+    const double v = warp_sum(acc0 + acc1);
+    if (lane == 0) y[row] = ACC ? y[row] + v : v;
 }
 
 // r = b - M x with M in CSR, one thread per row.
@@ -961,7 +969,13 @@ double dense_inverse(Ctx& c, const double* A, double* Ainv, int n) {
 
 void launch_gemv(Ctx& c, const double* A, const double* x, double* y, int n) {
     PROF(c, "k_gemv");
-    k_gemv<<<cdiv(n, 2), 256, 0, c.st>>>(A, x, y, n);
+    k_gemv_w<false><<<cdiv(n, 8), 256, 0, c.st>>>(A, x, y, n);
+    CK_LAUNCH();
+}
+
+void launch_gemv_acc(Ctx& c, const double* A, const double* x, double* y, int n) {
+    PROF(c, "k_gemv");
+    k_gemv_w<true><<<cdiv(n, 8), 256, 0, c.st>>>(A, x, y, n);
     CK_LAUNCH();
 }
 

@@ -459,6 +459,49 @@ __global__ void k_recon_traces(Layout L, const double* __restrict__ coef, const 
     if (RB) RB[x] = b;
 }
 
+// MPM-2P recombination, one warp per subdomain: boundary traces
+// RU = PU + sum_h c_h HU_h + WU (k_recon_traces) and the pressure sum
+// RS = PS + sum_h c_h HP_h + pmsum (k_recon_psum), same operation order. The
+// coefficients c_h of the subdomain's homogeneous functions are warp-uniform.
+__global__ void k_recon_mpm(Layout L, const double* __restrict__ coef, const double* __restrict__ PU,
+                            const double* __restrict__ HU, const double* __restrict__ WU, double* __restrict__ RU,
+                            const double* __restrict__ PS, const double* __restrict__ HP,
+                            const double* __restrict__ pmsum, double* __restrict__ RS) {
+    constexpr int MAXH = 16;
+    const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (s >= L.n_sub) return;
+    const int nh = L.n_hom(s);
+    double ch[MAXH];
+#pragma unroll
+    for (int h = 0; h < MAXH; ++h) {
+        double cv = 0.0;
+        if (h < nh) {
+            int k, t, col;
+            bool fl;
+            L.hom(s, h, k, t, fl, col);
+            cv = coef[col];
+        }
+        ch[h] = cv;
+    }
+    for (int idx = lane; idx < L.nbe; idx += 32) {
+        const size_t x = (size_t)s * L.nbe + idx;
+        double u = PU[x];
+#pragma unroll
+        for (int h = 0; h < MAXH; ++h)
+            if (h < nh && ch[h] != 0.0) u += ch[h] * HU[((size_t)s * L.max_hom + h) * L.nbe + idx];
+        if (WU) u += WU[x];
+        RU[x] = u;
+    }
+    if (lane == 0) {
+        double v = PS[s];
+#pragma unroll
+        for (int h = 0; h < MAXH; ++h)
+            if (h < nh && ch[h] != 0.0) v += ch[h] * HP[(size_t)s * L.max_hom + h];
+        if (pmsum) v += pmsum[s];
+        RS[s] = v;
+    }
+}
+
 __global__ void k_recon_psum(Layout L, const double* __restrict__ coef, const double* __restrict__ PS,
                              const double* __restrict__ HP, const double* __restrict__ pmsum,
                              double* __restrict__ RS) {
@@ -702,12 +745,37 @@ __global__ void __launch_bounds__(WPB * 32) k_ds_solve_r(Layout L, const double*
     for (int r = lane; r < n; r += 32) p[L.gcell_of(s, r)] = x[r] + shift;
 }
 
+// Outward normal velocity of the particular solution on boundary edge idx of
+// subdomain s (the k_part_traces formula, mpm.cpp:86-96).
+__device__ __forceinline__ double part_trace(const Layout& L, int s, int idx, double pc, const double* km,
+                                             const int* bc_kind, const double* bm, const double* bp,
+                                             const double* GZ) {
+    const EdgeInfo e = L.edge(s, idx);
+    const double th = half_trans(L, e.side, km[e.global_cell]);
+    const size_t x = (size_t)s * L.nbe + idx;
+    if (e.iface >= 0) {
+        const double te = eff_robin(th, edge_beta(L, e, bm, bp), e.area);
+        return te * (pc - 0.0) / e.area;
+    }
+    if (bc_kind[e.gbc] == BC_PRESSURE) return th * (pc - GZ[x]) / e.area;
+    return GZ[x];
+}
+
+// MPM-2P particular solve with the cached factor, then (same warp, same
+// subdomain) its boundary traces PU and pressure sum PS — the work of
+// k_part_traces / k_part_psum without two more launches.
 template <int B>
 __global__ void __launch_bounds__(WPB * 32) k_part_solve_r(Layout L, int max_rhs, const double* __restrict__ D,
                                                            const double* __restrict__ Lc,
-                                                           const double* __restrict__ Lr, double* X) {
+                                                           const double* __restrict__ Lr, double* X,
+                                                           const double* __restrict__ km,
+                                                           const int* __restrict__ bc_kind,
+                                                           const double* __restrict__ bm,
+                                                           const double* __restrict__ bp,
+                                                           const double* __restrict__ GZ, double* __restrict__ PU,
+                                                           double* __restrict__ PS) {
     __shared__ __align__(16) double ring[WPB][sweep_ring<B>() * B * B + 2];
-    const int w = threadIdx.x >> 5;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int s = blockIdx.x * WPB + w;
     if (s >= L.n_sub) return;
     const int n = L.ncs;
@@ -716,6 +784,15 @@ __global__ void __launch_bounds__(WPB * 32) k_part_solve_r(Layout L, int max_rhs
     forward_reg<B, 1>(n, Lc + so * B, x, 1, n, nullptr, ring[w]);
     __syncwarp();
     backward_reg<B, 1>(n, D + so, Lr + so * B, x, 1, n, nullptr, ring[w]);
+    __syncwarp();  // x written by the pivot lanes is read by all lanes below
+    for (int idx = lane; idx < L.nbe; idx += 32) {
+        const EdgeInfo e = L.edge(s, idx);
+        PU[(size_t)s * L.nbe + idx] = part_trace(L, s, idx, x[e.local_cell], km, bc_kind, bm, bp, GZ);
+    }
+    double v = 0.0;
+    for (int r = lane; r < n; r += 32) v += x[r];
+    v = warp_sum(v);
+    if (lane == 0) PS[s] = v;
 }
 
 // RHS carried through one register sweep of the rebuild (1 particular + up to
@@ -1166,8 +1243,7 @@ void interface_solve(Ctx& c) {
     // one step of iterative refinement against the sparse operator
     for (int it = 0; it < 1; ++it) {
         launch_csr_residual(c, c.csr_ptr, c.csr_col, c.csr_val, c.icoef, c.irhs, c.ires, c.dim);
-        launch_gemv(c, c.Minv, c.ires, c.idelta, c.dim);
-        launch_axpy(c, c.icoef, c.idelta, c.dim);
+        launch_gemv_acc(c, c.Minv, c.ires, c.icoef, c.dim);  // x += M^-1 (b - M x)
     }
 }
 
@@ -1289,12 +1365,16 @@ void launch_mpm(Ctx& c, const double* kn) {  // mpm_pressure_update (mpm.cpp:31-
         CK_LAUNCH();
     }
     const size_t sm1 = (size_t)WPB * band_smem_doubles(L.snx, 1) * sizeof(double);
+    bool fused_traces = false;  // the register-window kernel also writes PU / PS
     {
         PROF(c, "k_part_solve");
         switch (c.no_regband ? -1 : L.snx) {
 #define X(BW_)                                                                                                  \
     case BW_:                                                                                                   \
-        k_part_solve_r<BW_><<<band_blocks(L), WPB * 32, 0, c.st>>>(L, c.max_rhs, c.Dm, c.Lcm, c.Lrm, c.X);    \
+        k_part_solve_r<BW_><<<band_blocks(L), WPB * 32, 0, c.st>>>(L, c.max_rhs, c.Dm, c.Lcm, c.Lrm, c.X,     \
+                                                                   c.kappa_m, c.bc_kind, c.beta_m, c.beta_p,   \
+                                                                   c.GZ, c.PU, c.PS);                          \
+        fused_traces = true;                                                                                    \
         break;
             MPM2P_BAND_WIDTHS(X)
 #undef X
@@ -1303,30 +1383,39 @@ void launch_mpm(Ctx& c, const double* kn) {  // mpm_pressure_update (mpm.cpp:31-
         }
         CK_LAUNCH();
     }
-    {
-        PROF(c, "k_part_traces");
-        k_part_traces<<<grid_for((long long)L.n_sub * L.nbe), TPB, 0, c.st>>>(L, c.max_rhs, c.kappa_m, c.bc_kind, c.beta_m,
-                                                                              c.beta_p, c.GZ, c.X, c.PU);
-        CK_LAUNCH();
-    }
-    {
-        PROF(c, "k_part_psum");
-        k_part_psum<<<cdiv((long long)L.n_sub * 32, TPB), TPB, 0, c.st>>>(L, c.max_rhs, c.X, c.PS);
-        CK_LAUNCH();
+    if (!fused_traces) {
+        {
+            PROF(c, "k_part_traces");
+            k_part_traces<<<grid_for((long long)L.n_sub * L.nbe), TPB, 0, c.st>>>(
+                L, c.max_rhs, c.kappa_m, c.bc_kind, c.beta_m, c.beta_p, c.GZ, c.X, c.PU);
+            CK_LAUNCH();
+        }
+        {
+            PROF(c, "k_part_psum");
+            k_part_psum<<<cdiv((long long)L.n_sub * 32, TPB), TPB, 0, c.st>>>(L, c.max_rhs, c.X, c.PS);
+            CK_LAUNCH();
+        }
     }
     c.c_part += L.n_sub;
     interface_solve(c);
     if (c.dim == 0) CK(cudaMemsetAsync(c.icoef, 0, sizeof(double), c.st));
-    {
-        PROF(c, "k_recon_traces");
-        k_recon_traces<<<grid_for((long long)L.n_sub * L.nbe), TPB, 0, c.st>>>(L, c.icoef, c.PU, nullptr, c.HU, nullptr,
-                                                                               c.WU, c.RU, nullptr);
+    if (L.max_hom <= 16) {
+        PROF(c, "k_recon_mpm");
+        k_recon_mpm<<<cdiv((long long)L.n_sub * 32, TPB), TPB, 0, c.st>>>(L, c.icoef, c.PU, c.HU, c.WU, c.RU, c.PS,
+                                                                          c.HP, c.pmsum, c.RS);
         CK_LAUNCH();
-    }
-    {
-        PROF(c, "k_recon_psum");
-        k_recon_psum<<<grid_for(L.n_sub), TPB, 0, c.st>>>(L, c.icoef, c.PS, c.HP, c.pmsum, c.RS);
-        CK_LAUNCH();
+    } else {  // per-edge interface spaces: more homogeneous functions than k_recon_mpm keeps in registers
+        {
+            PROF(c, "k_recon_traces");
+            k_recon_traces<<<grid_for((long long)L.n_sub * L.nbe), TPB, 0, c.st>>>(L, c.icoef, c.PU, nullptr, c.HU,
+                                                                                   nullptr, c.WU, c.RU, nullptr);
+            CK_LAUNCH();
+        }
+        {
+            PROF(c, "k_recon_psum");
+            k_recon_psum<<<grid_for(L.n_sub), TPB, 0, c.st>>>(L, c.icoef, c.PS, c.HP, c.pmsum, c.RS);
+            CK_LAUNCH();
+        }
     }
     downscale(c, kn);
 }
