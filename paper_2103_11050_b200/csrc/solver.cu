@@ -795,21 +795,17 @@ __global__ void __launch_bounds__(WPB * 32) k_part_solve_r(Layout L, int max_rhs
     if (lane == 0) PS[s] = v;
 }
 
-// RHS carried through one register sweep of the rebuild (1 particular + up to
-// 8 homogeneous for constant H-bar = H; 16 for linear / H/2 spaces).
+// Rebuild, split for parallelism: k_factor1_r factors each subdomain operator
+// with only the particular right-hand side carried through the (sequential)
+// elimination, then k_hom_solve_r solves the homogeneous right-hand sides with
+// the stored factor, one warp per (subdomain, function) — 8x more warps than
+// carrying all of them through the factorisation, same arithmetic per RHS.
 template <int B>
-constexpr int rebuild_nr(int max_rhs) {
-    return (B <= 16 && max_rhs > 9) ? 17 : 9;
-}
-
-template <int B, int NR_REG>
-__global__ void __launch_bounds__(WPB * 32) k_factor_solve_r(Layout L, int max_rhs, const double* __restrict__ BD,
-                                                             const double* __restrict__ BW,
-                                                             const double* __restrict__ BS, double* D,
-                                                             double* Lc, double* Lr,
-                                                             double* X, Scalars* sc) {
+__global__ void __launch_bounds__(WPB * 32) k_factor1_r(Layout L, int max_rhs, const double* __restrict__ BD,
+                                                        const double* __restrict__ BW, const double* __restrict__ BS,
+                                                        double* D, double* Lc, double* Lr, double* X, Scalars* sc) {
     __shared__ double stage[WPB][B * B];
-    __shared__ __align__(16) double xbuf[WPB][xchg_doubles<B, NR_REG>()];
+    __shared__ __align__(16) double xbuf[WPB][xchg_doubles<B, 1>()];
     __shared__ __align__(16) double ring[WPB][sweep_ring<B>() * B * B + 2];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int s = blockIdx.x * WPB + w;
@@ -817,23 +813,28 @@ __global__ void __launch_bounds__(WPB * 32) k_factor_solve_r(Layout L, int max_r
     const int n = L.ncs;
     const size_t so = (size_t)s * n;
     const BandRows A{BD + so, BW + so, BS + so};
-    const int nr = 1 + L.n_hom(s);
-    double* Xs = X + xoff(L, max_rhs, s, 0);
-    const int n0 = nr < NR_REG ? nr : NR_REG;
-    const bool ok =
-        factor_fwd_reg<B, NR_REG>(n, A, D + so, Lc + so * B, Lr + so * B, Xs, n0, n, stage[w], xbuf[w]);
+    double* x = X + xoff(L, max_rhs, s, 0);
+    const bool ok = factor_fwd_reg<B, 1>(n, A, D + so, Lc + so * B, Lr + so * B, x, 1, n, stage[w], xbuf[w]);
     if (!ok && lane == 0) atomicOr(&sc->err, ERR_PIVOT);
     __syncwarp();
-    for (int m0 = n0; m0 < nr; m0 += NR_REG) {
-        const int cnt = nr - m0 < NR_REG ? nr - m0 : NR_REG;
-        forward_reg<B, NR_REG>(n, Lc + so * B, Xs + (size_t)m0 * n, cnt, n, xbuf[w], ring[w]);
-        __syncwarp();
-    }
-    for (int m0 = 0; m0 < nr; m0 += NR_REG) {
-        const int cnt = nr - m0 < NR_REG ? nr - m0 : NR_REG;
-        backward_reg<B, NR_REG>(n, D + so, Lr + so * B, Xs + (size_t)m0 * n, cnt, n, xbuf[w], ring[w]);
-        __syncwarp();
-    }
+    backward_reg<B, 1>(n, D + so, Lr + so * B, x, 1, n, nullptr, ring[w]);
+}
+
+template <int B>
+__global__ void __launch_bounds__(WPB * 32) k_hom_solve_r(Layout L, int max_rhs, const double* __restrict__ D,
+                                                          const double* __restrict__ Lc,
+                                                          const double* __restrict__ Lr, double* X) {
+    __shared__ __align__(16) double ring[WPB][sweep_ring<B>() * B * B + 2];
+    const int w = threadIdx.x >> 5;
+    const int gw = blockIdx.x * WPB + w;
+    const int s = gw / L.max_hom, h = gw % L.max_hom;
+    if (s >= L.n_sub || h >= L.n_hom(s)) return;
+    const int n = L.ncs;
+    const size_t so = (size_t)s * n;
+    double* x = X + xoff(L, max_rhs, s, 1 + h);
+    forward_reg<B, 1>(n, Lc + so * B, x, 1, n, nullptr, ring[w]);
+    __syncwarp();
+    backward_reg<B, 1>(n, D + so, Lr + so * B, x, 1, n, nullptr, ring[w]);
 }
 
 // Subdomain widths with a register-window instantiation; others use band.cuh.
@@ -1277,12 +1278,14 @@ void launch_rebuild(Ctx& c, const double* kappa, bool compute_beta) {  // comput
         switch (c.no_regband ? -1 : L.snx) {
 #define X(BW_)                                                                                                      \
     case BW_:                                                                                                       \
-        if (rebuild_nr<BW_>(c.max_rhs) == 17)                                                                       \
-            k_factor_solve_r<BW_, (BW_ <= 16 ? 17 : 9)><<<band_blocks(L), WPB * 32, 0, c.st>>>(                    \
-                L, c.max_rhs, c.BDm, c.BWm, c.BSm, c.Dm, c.Lcm, c.Lrm, c.X, c.sc);                                   \
-        else                                                                                                        \
-            k_factor_solve_r<BW_, 9><<<band_blocks(L), WPB * 32, 0, c.st>>>(L, c.max_rhs, c.BDm, c.BWm, c.BSm,     \
-                                                                           c.Dm, c.Lcm, c.Lrm, c.X, c.sc);          \
+        k_factor1_r<BW_><<<band_blocks(L), WPB * 32, 0, c.st>>>(L, c.max_rhs, c.BDm, c.BWm, c.BSm, c.Dm, c.Lcm,   \
+                                                                c.Lrm, c.X, c.sc);                                  \
+        if (L.max_hom > 0) {                                                                                        \
+            CK_LAUNCH();                                                                                            \
+            PROF(c, "k_hom_solve");                                                                                 \
+            k_hom_solve_r<BW_><<<cdiv((long long)L.n_sub * L.max_hom, WPB), WPB * 32, 0, c.st>>>(                  \
+                L, c.max_rhs, c.Dm, c.Lcm, c.Lrm, c.X);                                                             \
+        }                                                                                                           \
         break;
             MPM2P_BAND_WIDTHS(X)
 #undef X
