@@ -550,22 +550,11 @@ __global__ void k_sub_sum(Layout L, const double* __restrict__ field, double* __
 }
 
 // ---------------------------------------------------------------- K9 ----
-__global__ void k_skel(Layout L, const double* __restrict__ RU, double* __restrict__ skel) {  // mrcm.cpp:290-304
-    const int x = blockIdx.x * blockDim.x + threadIdx.x;
-    if (x >= L.skeleton_edges()) return;
-    const int k = x < L.NV * L.sny ? x / L.sny : L.NV + (x - L.NV * L.sny) / L.snx;
-    const int pos = x < L.NV * L.sny ? x % L.sny : (x - L.NV * L.sny) % L.snx;
-    const int sm = L.iface_minus(k), sp = L.iface_plus(k);
-    const double um = RU[(size_t)sm * L.nbe + L.edge_index_on_iface(sm, k, pos)];   // sign +1
-    const double up = -RU[(size_t)sp * L.nbe + L.edge_index_on_iface(sp, k, pos)];  // sign -1
-    skel[x] = 0.5 * (um + up);
-}
-
 // Compatibility residual per subdomain, in the reference's edge order
 // (mrcm.cpp:315-340), plus flux_scale = max |skeleton flux|.
-__global__ void k_resid(Layout L, const double* __restrict__ skel, const double* __restrict__ RU,
+__global__ void k_resid(Layout L, const double* skel, const double* __restrict__ RU,
                         const double* __restrict__ qsum, double* __restrict__ resid, Scalars* sc, double* part,
-                        unsigned* counter) {
+                        unsigned* counter, int fuse_skel = 0) {
     // one warp per subdomain; lanes stride the boundary edges (W,E,S,N order)
     __shared__ double sh[32];
     const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
@@ -576,7 +565,16 @@ __global__ void k_resid(Layout L, const double* __restrict__ skel, const double*
             const EdgeInfo e = L.edge(s, idx);
             double un;
             if (e.iface >= 0) {
-                const double v = skel[L.skel_index(e.iface, e.pos)];
+                double v;
+                if (fuse_skel) {  // k_skel's arithmetic, written once (by the minus side) for k_ds_prep
+                    const int k = e.iface, sm = L.iface_minus(k), sp = L.iface_plus(k);
+                    const double um = RU[(size_t)sm * L.nbe + L.edge_index_on_iface(sm, k, e.pos)];
+                    const double up = -RU[(size_t)sp * L.nbe + L.edge_index_on_iface(sp, k, e.pos)];
+                    v = 0.5 * (um + up);
+                    if (s == sm) const_cast<double*>(skel)[L.skel_index(k, e.pos)] = v;
+                } else {
+                    v = skel[L.skel_index(e.iface, e.pos)];
+                }
                 un = e.sign * v;
                 fmaxv = fmax(fmaxv, fabs(v));
             } else {
@@ -600,15 +598,48 @@ __global__ void k_resid(Layout L, const double* __restrict__ skel, const double*
 
 // ---------------------------------------------------------------- K10 ----
 // delta = Linv * resid, one warp per subdomain row; then interface corrections.
+__device__ void repair_corr_last(const Layout& L, int grounded, const double* delta, const double* ground,
+                                 double* corr, Scalars* sc, double* sh);
+
+// With the last block also forming the interface corrections and the repair
+// diagnostics (k_repair_corr's work, active repair only).
 __global__ void k_repair_delta(int n, const double* __restrict__ Linv, const double* __restrict__ resid,
-                               double* __restrict__ delta) {
+                               double* delta, Layout L, int grounded, const double* __restrict__ ground,
+                               double* __restrict__ corr, Scalars* sc, unsigned* counter) {
+    __shared__ double sh[32];
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-    if (gw >= n) return;
-    const double* row = Linv + (size_t)gw * n;
-    double v = 0.0;
-    for (int t = lane; t < n; t += 32) v += row[t] * resid[t];
-    v = warp_sum(v);
-    if (lane == 0) delta[gw] = v;
+    if (gw < n) {
+        const double* row = Linv + (size_t)gw * n;
+        double v = 0.0;
+        for (int t = lane; t < n; t += 32) v += row[t] * resid[t];
+        v = warp_sum(v);
+        if (lane == 0) delta[gw] = v;
+    }
+    if (last_block_done(counter)) {
+        repair_corr_last(L, grounded, delta, ground, corr, sc, sh);
+        if (threadIdx.x == 0) *counter = 0;
+    }
+}
+
+// corr = delta_minus - delta_plus per interface; repair_max and the warning
+// flag, by one block (the last of k_repair_delta), deterministic order.
+__device__ void repair_corr_last(const Layout& L, int grounded, const double* delta, const double* ground,
+                                 double* corr, Scalars* sc, double* sh) {
+    double m = 0.0;
+    for (int x = threadIdx.x; x < L.n_iface; x += blockDim.x) {
+        const double cv = __ldcg(delta + L.iface_minus(x)) - __ldcg(delta + L.iface_plus(x));
+        corr[x] = cv;
+        m = fmax(m, fabs(cv));
+    }
+    if (grounded)
+        for (int x = threadIdx.x; x < L.n_sub; x += blockDim.x)
+            if (ground[x] > 0.0) m = fmax(m, fabs(__ldcg(delta + x)));
+    m = block_max(m, sh);
+    if (threadIdx.x == 0) {
+        sc->repair_max = m;
+        const double fs = sc->flux_scale;
+        sc->repair_warning = m > 0.1 * (fs > 0 ? fs : 1.0);
+    }
 }
 
 __global__ void k_repair_corr(Layout L, int active, int grounded, const double* __restrict__ delta,
@@ -1165,29 +1196,21 @@ namespace {
 // c.T = transmissibility(kappa), RU/RS = recon traces and pressure sums.
 void downscale(Ctx& c, const double* kappa) {
     const Layout& L = c.L;
-    if (L.skeleton_edges() > 0) {
-        {
-            PROF(c, "k_skel");
-            k_skel<<<grid_for(L.skeleton_edges()), TPB, 0, c.st>>>(L, c.RU, c.skel);
-            CK_LAUNCH();
-        }
-    }
-    {
+    {  // skeleton fluxes (k_skel) are formed inside k_resid
         PROF(c, "k_resid");
-        k_resid<<<grid_for(32LL * L.n_sub), TPB, 0, c.st>>>(L, c.skel, c.RU, c.qsum_sub, c.resid, c.sc, c.red, c.red_count);
+        k_resid<<<grid_for(32LL * L.n_sub), TPB, 0, c.st>>>(L, c.skel, c.RU, c.qsum_sub, c.resid, c.sc, c.red,
+                                                             c.red_count, 1);
         CK_LAUNCH();
     }
     if (c.repair_active) {
-        {
-            PROF(c, "k_repair_delta");
-            k_repair_delta<<<cdiv((long long)L.n_sub * 32, TPB), TPB, 0, c.st>>>(L.n_sub, c.Linv, c.resid, c.delta);
-            CK_LAUNCH();
-        }
-    }
-    {
+        PROF(c, "k_repair_delta");
+        k_repair_delta<<<cdiv((long long)L.n_sub * 32, TPB), TPB, 0, c.st>>>(
+            L.n_sub, c.Linv, c.resid, c.delta, L, c.grounded ? 1 : 0, c.ground, c.corr, c.sc, c.red_count);
+        CK_LAUNCH();
+    } else {
         PROF(c, "k_repair_corr");
         k_repair_corr<<<std::min(grid_for(std::max(L.n_iface, L.n_sub)), 2 * c.num_sms), TPB, 0, c.st>>>(
-            L, c.repair_active ? 1 : 0, c.grounded ? 1 : 0, c.delta, c.ground, c.corr, c.sc, c.red, c.red_count);
+            L, 0, c.grounded ? 1 : 0, c.delta, c.ground, c.corr, c.sc, c.red, c.red_count);
         CK_LAUNCH();
     }
     {
@@ -1213,7 +1236,7 @@ void downscale(Ctx& c, const double* kappa) {
         }
         CK_LAUNCH();
     }
-    {
+    {  // (fusing this into k_ds_solve_r serialises ~17 dependent loads per lane: slower)
         PROF(c, "k_ds_u");
         k_ds_u<<<grid_for(L.faces()), TPB, 0, c.st>>>(L, c.T, c.Xd, c.GZ, c.u);
         CK_LAUNCH();
