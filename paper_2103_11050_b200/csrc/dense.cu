@@ -691,7 +691,7 @@ __global__ void k_rcond(const double* __restrict__ part, int n, int nrb, const i
 // quarter of the row with 4 independent loads in flight per lane (the GEMV is
 // load-latency bound at these sizes, so more bytes in flight is the lever).
 // y = A x (ACC: y += A x), one warp per row. HBM-bound: every lane issues
-// its 16-byte loads of the row (and of x, L1/L2-resident) for 256 columns
+// its 16-byte loads of the row (and of x, L1/L2-resident) for 1024 columns
 // before any FMA, so ~8 KB per warp is in flight. Rows must be 16-byte
 // aligned (n even); odd n takes the scalar loop.
 template <bool ACC>
@@ -705,16 +705,16 @@ __global__ void __launch_bounds__(256) k_gemv_w(const double* __restrict__ A, co
         const double2* a2 = reinterpret_cast<const double2*>(a);
         const double2* x2 = reinterpret_cast<const double2*>(x);
         const int n2 = n >> 1;
-        for (int base = 0; base < n2; base += 256) {
-            double2 av[8], xv[8];
+        for (int base = 0; base < n2; base += 512) {  // n <= 1024: the whole row in one round trip
+            double2 av[16], xv[16];
 #pragma unroll
-            for (int t = 0; t < 8; ++t) {
+            for (int t = 0; t < 16; ++t) {
                 const int q = base + lane + 32 * t;
                 av[t] = q < n2 ? __ldg(a2 + q) : make_double2(0.0, 0.0);
                 xv[t] = q < n2 ? __ldg(x2 + q) : make_double2(0.0, 0.0);
             }
 #pragma unroll
-            for (int t = 0; t < 8; ++t) {
+            for (int t = 0; t < 16; ++t) {
                 acc0 = fma(av[t].x, xv[t].x, acc0);
                 acc1 = fma(av[t].y, xv[t].y, acc1);
             }
@@ -724,6 +724,42 @@ __global__ void __launch_bounds__(256) k_gemv_w(const double* __restrict__ A, co
     }
     const double v = warp_sum(acc0 + acc1);
     if (lane == 0) y[row] = ACC ? y[row] + v : v;
+}
+
+// Same product for n <= GEMV_TMA_MAX (even): one elected thread moves x and
+// the block's 8 rows into shared memory with TMA bulk copies on one mbarrier
+// (all bytes in flight at once, no per-load issue slots), then each warp
+// reduces its row from shared memory.
+constexpr int GEMV_TMA_MAX = 2816;  // 9 n doubles of dynamic shared memory <= 198 KB
+template <bool ACC>
+__global__ void __launch_bounds__(256) k_gemv_tma(const double* __restrict__ A, const double* __restrict__ x,
+                                                  double* __restrict__ y, int n) {
+    extern __shared__ __align__(128) double gsm[];
+    __shared__ __align__(8) unsigned long long bar;
+    const int r0 = blockIdx.x * 8, nr = min(8, n - r0);
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* xs = gsm;
+    double* rows = gsm + n;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        const unsigned rb = (unsigned)n * 8u;
+        mbar_expect_tx(&bar, rb * (unsigned)(1 + nr));
+        bulk_g2s(xs, x, rb, &bar);
+        for (int k = 0; k < nr; ++k) bulk_g2s(rows + (size_t)k * n, A + (size_t)(r0 + k) * n, rb, &bar);
+    }
+    __syncthreads();  // barrier initialised before anyone waits on it
+    mbar_wait(&bar, 0);
+    if (w >= nr) return;
+    const double2* a2 = reinterpret_cast<const double2*>(rows + (size_t)w * n);
+    const double2* x2 = reinterpret_cast<const double2*>(xs);
+    double acc0 = 0.0, acc1 = 0.0;
+    for (int q = lane; q < (n >> 1); q += 32) {
+        const double2 a = a2[q], b = x2[q];
+        acc0 = fma(a.x, b.x, acc0);
+        acc1 = fma(a.y, b.y, acc1);
+    }
+    const double v = warp_sum(acc0 + acc1);
+    if (lane == 0) y[r0 + w] = ACC ? y[r0 + w] + v : v;
 }
 
 // r = b - M x with M in CSR, one thread per row.
@@ -967,16 +1003,28 @@ double dense_inverse(Ctx& c, const double* A, double* Ainv, int n) {
     return rc;
 }
 
-void launch_gemv(Ctx& c, const double* A, const double* x, double* y, int n) {
+template <bool ACC>
+void gemv_dispatch(Ctx& c, const double* A, const double* x, double* y, int n) {
     PROF(c, "k_gemv");
-    k_gemv_w<false><<<cdiv(n, 8), 256, 0, c.st>>>(A, x, y, n);
+    if ((n & 1) == 0 && n <= GEMV_TMA_MAX) {
+        static bool attr = false;  // once, outside any graph capture (first use is eager)
+        if (!attr) {
+            CK(cudaFuncSetAttribute(k_gemv_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    9 * GEMV_TMA_MAX * (int)sizeof(double)));
+            CK(cudaFuncSetAttribute(k_gemv_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    9 * GEMV_TMA_MAX * (int)sizeof(double)));
+            attr = true;
+        }
+        k_gemv_tma<ACC><<<cdiv(n, 8), 256, (size_t)9 * n * sizeof(double), c.st>>>(A, x, y, n);
+    } else {
+        k_gemv_w<ACC><<<cdiv(n, 8), 256, 0, c.st>>>(A, x, y, n);
+    }
     CK_LAUNCH();
 }
 
+void launch_gemv(Ctx& c, const double* A, const double* x, double* y, int n) { gemv_dispatch<false>(c, A, x, y, n); }
 void launch_gemv_acc(Ctx& c, const double* A, const double* x, double* y, int n) {
-    PROF(c, "k_gemv");
-    k_gemv_w<true><<<cdiv(n, 8), 256, 0, c.st>>>(A, x, y, n);
-    CK_LAUNCH();
+    gemv_dispatch<true>(c, A, x, y, n);
 }
 
 void launch_csr_residual(Ctx& c, const int* ptr, const int* col, const double* val, const double* x, const double* b,
