@@ -255,3 +255,68 @@ def test_config_errors():
     bad[3] = -1.0
     with pytest.raises(api.NumericError):
         g.mrcm_solve(bad)
+
+
+# ---- K7: MINRES interface solve (the path C5 takes; forced here at small sizes)
+
+def _krylov_sim(prob):
+    import os
+    os.environ["MPM2P_IFACE"] = "krylov"
+    try:
+        return api.Simulator(prob)
+    finally:
+        os.environ.pop("MPM2P_IFACE", None)
+
+
+@pytest.mark.parametrize("nsx,nsy,space,hbar,contrast", [(4, 4, api.SPACE_CONSTANT, api.HBAR_WHOLE, 10.0),
+                                                         (4, 4, api.SPACE_LINEAR, api.HBAR_WHOLE, 10.0),
+                                                         (2, 4, api.SPACE_CONSTANT, api.HBAR_HALF, 100.0),
+                                                         (8, 8, api.SPACE_CONSTANT, api.HBAR_WHOLE, 1e3)])
+def test_krylov_interface_parity(oracle, nsx, nsy, space, hbar, contrast):
+    """MINRES on K = J M (quasi-definite) vs the reference's LU, through mrcm_solve and mpm_update."""
+    nx = ny = 32
+    K = random_kappa(nx, ny, 1, 1.0 / contrast, 1.0)
+    prob = problem(nx, ny, nsx, nsy, K, M=5.0, space=space, hbar=hbar)
+    g, o = _krylov_sim(prob), api.Simulator(prob, oracle)
+    sg, so = g.mrcm_solve(K), o.mrcm_solve(K)
+    assert sg.counters == so.counters
+    assert rel_l2(g.interface_matrix(), o.interface_matrix()) < 1e-12  # scattered from the CSR operator
+    for a, b in ((sg.coeffs, so.coeffs), (sg.p, so.p), (sg.u, so.u)):
+        assert rel_l2(a, b) <= 1e-10
+    kn = K * np.exp(0.05 * np.random.default_rng(3).standard_normal(K.size))
+    mg, mo = g.mpm_pressure_update(kn), o.mpm_pressure_update(kn)
+    assert rel_l2(mg.p, mo.p) <= 1e-10 and rel_l2(mg.u, mo.u) <= 1e-10
+
+
+def test_krylov_matches_dense_c1_run():
+    """A whole C1 run with the MINRES interface solve vs the dense-inverse path:
+    same decisions, fields within roundoff."""
+    c = configs.build("C1")
+    rd = api.Simulator(c.problem).run(c.split, c.s0())
+    rk = _krylov_sim(c.problem).run(c.split, c.s0())
+    assert rk.record.interface_krylov == 1 and rd.record.interface_krylov == 0
+    assert rk.record.interface_iterations > 0
+    assert [s["rebuilt"] for s in rk.record.steps] == [s["rebuilt"] for s in rd.record.steps]
+    assert np.max(np.abs(rk.s_final - rd.s_final)) <= TOL_S
+    assert rel_l2(rk.p_final, rd.p_final) <= TOL_PU and rel_l2(rk.u_final, rd.u_final) <= TOL_PU
+
+
+def test_c5_scale_properties():
+    """C5 (128 x 128 subdomains, interface dim 65,024: beyond the dense path,
+    solved by MINRES) through size-independent properties: conservative
+    velocities, saturation in [0, 1], the PVI clock advancing, counters of an
+    Algorithm-1 run, and a zero-perturbation MPM update reproducing MRCM."""
+    c = configs.build("C5", te_override=3)
+    g = api.Simulator(c.problem)
+    assert g.dim == 65024
+    r = g.run(c.split, c.s0())
+    rec = r.record
+    assert rec.interface_krylov == 1 and rec.interface_max_iterations > 0
+    assert rec.max_div_ratio <= 1e-9
+    assert r.s_final.min() >= 0.0 and r.s_final.max() <= 1.0 and r.s_final.max() > 0.0
+    assert rec.final_pvi > 0.0 and rec.te == 3
+    assert rec.counters.downscale % (128 * 128) == 0 and rec.counters.downscale >= (rec.te - 1) * 128 * 128
+    K = c.problem.K
+    sol = g.mrcm_solve(K)
+    m = g.mpm_pressure_update(K)
+    assert rel_l2(m.u, sol.u) < 1e-9 and rel_l2(m.p, sol.p) < 1e-9
