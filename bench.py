@@ -371,7 +371,10 @@ def main():
         try:
             with open(os.path.join(ROOT, "profiles", f"ncu_traffic_r01_{cfg.name}.json")) as f:
                 tr = {k.split("::")[-1]: v for k, v in json.load(f).items()}
-            roof["traffic"] = tr.get(roof["kernel"] + "_r", tr.get(roof["kernel"]))
+            # keys carry template arguments (k_ds_solve_r<16>): match the launcher name as a prefix
+            hit = [v for k, v in tr.items() if k == roof["kernel"] or k.startswith(roof["kernel"] + "_r<")
+                   or k.startswith(roof["kernel"] + "<")]
+            roof["traffic"] = hit[0] if hit else None
             roof["traffic_source"] = f"profiles/ncu_traffic_r01_{cfg.name}.json (dram__bytes_read+write per launch)"
         except (OSError, ValueError):
             pass
