@@ -237,6 +237,7 @@ void create_ctx(mpm2p_ctx* ctx, const mpm2p_problem* P) {
     if (const char* e = std::getenv("MPM2P_NO_GRAPHS")) c.use_graphs = e[0] != 0 && e[0] == '0';
     if (const char* e = std::getenv("MPM2P_NO_REGBAND")) c.no_regband = e[0] == '1';
     if (const char* e = std::getenv("MPM2P_GJ")) c.gj_legacy = std::strcmp(e, "legacy") == 0;
+    if (const char* e = std::getenv("MPM2P_NO_TWIST")) c.no_twist = e[0] == '1';
     c.use_krylov = c.dim > DENSE_IFACE_MAX;
     if (const char* e = std::getenv("MPM2P_IFACE")) {
         if (std::strcmp(e, "krylov") == 0) c.use_krylov = c.dim > 0;
@@ -316,6 +317,7 @@ void create_ctx(mpm2p_ctx* ctx, const mpm2p_problem* P) {
     c.Dd.alloc(ns * ncs);
     c.Lrd.alloc(ns * ncs * B);
     c.Xd.alloc(ns * ncs);
+    c.Yv.alloc(ns * ncs);
     c.sc.alloc(1);
     c.red.alloc(8 * 4 * (size_t)c.num_sms + 4096);
     c.red_count.alloc(1);

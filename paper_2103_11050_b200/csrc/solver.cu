@@ -17,6 +17,7 @@
 
 #include "band.cuh"
 #include "band_reg.cuh"
+#include "band_twist.cuh"
 #include "context.cuh"
 
 namespace mpm2p {
@@ -868,6 +869,33 @@ __global__ void __launch_bounds__(WPB * 32) k_hom_solve_r(Layout L, int max_rhs,
     backward_reg<B, 1>(n, D + so, Lr + so * B, x, 1, n, nullptr, ring[w]);
 }
 
+// Downscale solve with the two-sided elimination (band_twist.cuh): the two
+// half-warps factor from both ends, so the dependent chain is ~half as long.
+constexpr int WPBT = 2;  // warps per block (shared memory: ~18 KB per warp at B = 16)
+template <int B>
+__global__ void __launch_bounds__(WPBT * 32) k_ds_solve_t(Layout L, const double* __restrict__ BD,
+                                                          const double* __restrict__ BW, const double* __restrict__ BS,
+                                                          double* D, double* Lr, double* Xd, double* Yv,
+                                                          const double* __restrict__ RS, double* p, Scalars* sc) {
+    __shared__ __align__(16) double sm[WPBT][twist_smem_doubles<B>()];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int s = blockIdx.x * WPBT + w;
+    if (s >= L.n_sub) return;
+    const int n = L.ncs;
+    const size_t so = (size_t)s * n;
+    const BandRows A{BD + so, BW + so, BS + so};
+    double* x = Xd + so;
+    const bool ok = twisted_solve<B>(n, A, D + so, Lr + so * B, x, Yv + so, sm[w]);
+    if (!ok && lane == 0) atomicOr(&sc->err, ERR_PIVOT);
+    __syncwarp();
+    double v = 0.0;
+    for (int r = lane; r < n; r += 32) v += x[r];
+    v = warp_sum(v);
+    const double shift = (__shfl_sync(0xffffffffu, RS[s], 0) - __shfl_sync(0xffffffffu, v, 0)) / n;
+    for (int r = lane; r < n; r += 32) p[L.gcell_of(s, r)] = x[r] + shift;
+}
+#define MPM2P_TWIST_WIDTHS(X) X(4) X(8) X(10) X(12) X(16)
+
 // Subdomain widths with a register-window instantiation; others use band.cuh.
 #define MPM2P_BAND_WIDTHS(X) X(4) X(8) X(10) X(12) X(16) X(20) X(24) X(32)
 
@@ -1220,7 +1248,25 @@ void downscale(Ctx& c, const double* kappa) {
         CK_LAUNCH();
     }
     const size_t sm1 = (size_t)WPB * band_smem_doubles(L.snx, 1) * sizeof(double);
-    {
+    const bool twist = !c.no_regband && !c.no_twist && L.sny >= 3;
+    bool done = false;
+    if (twist) {
+        PROF(c, "k_ds_solve");
+        switch (L.snx) {
+#define X(BW_)                                                                                                  \
+    case BW_:                                                                                                   \
+        k_ds_solve_t<BW_><<<cdiv(L.n_sub, WPBT), WPBT * 32, 0, c.st>>>(L, c.BDd, c.BWd, c.BSd, c.Dd, c.Lrd, c.Xd, \
+                                                                       c.Yv, c.RS, c.p, c.sc);                  \
+        done = true;                                                                                            \
+        break;
+            MPM2P_TWIST_WIDTHS(X)
+#undef X
+            default:
+                break;
+        }
+        if (done) CK_LAUNCH();
+    }
+    if (!done) {
         PROF(c, "k_ds_solve");
         switch (c.no_regband ? -1 : L.snx) {
 #define X(BW_)                                                                                                     \

@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "../paper_2103_11050_b200/csrc/band_reg.cuh"
+#include "../paper_2103_11050_b200/csrc/band_twist.cuh"
 
 using namespace mpm2p;
 
@@ -41,6 +42,91 @@ __global__ void k_check4(int n, const double* BD, const double* BW, const double
     factor_fwd_reg<B, NR>(n, A, D + w * n, Lc + (size_t)w * n * B, Lr + (size_t)w * n * B, Yw, nr, n, stage[w], xb[w]);
     __syncwarp();
     backward_reg<B, NR>(n, D + w * n, Lr + (size_t)w * n * B, Yw, nr, n, xb[w], ring[w]);
+}
+
+// Twisted (two-sided) solve, WARPS independent copies per block.
+template <int B, int WARPS>
+__global__ void k_twist(int n, const double* BD, const double* BW, const double* BS, double* D, double* Lr,
+                        double* Y, double* Yv, int* okf) {
+    __shared__ __align__(16) double sm[WARPS][twist_smem_doubles<B>()];
+    const int w = threadIdx.x >> 5;
+    const BandRows A{BD, BW, BS};
+    const bool ok = twisted_solve<B>(n, A, D + w * n, Lr + (size_t)w * n * B, Y + (size_t)w * n, Yv + (size_t)w * n,
+                                     sm[w]);
+    if ((threadIdx.x & 31) == 0) okf[w] = ok;
+}
+
+template <int B, int WARPS>
+void run_twist(int m) {
+    const int n = B * m;
+    std::mt19937_64 g(B * 7000 + m);
+    std::uniform_real_distribution<double> U(0.1, 2.0);
+    std::vector<double> bd(n), bw(n), bs(n), y(n);
+    for (int r = 0; r < n; ++r) {
+        bw[r] = (r % B) ? U(g) : 0.0;
+        bs[r] = (r >= B) ? U(g) : 0.0;
+    }
+    for (int r = 0; r < n; ++r) {
+        double s = bw[r] + bs[r] + 0.05;
+        if (r % B != B - 1 && r + 1 < n) s += bw[r + 1];
+        if (r + B < n) s += bs[r + B];
+        bd[r] = s;
+    }
+    for (auto& v : y) v = U(g) - 1.0;
+    // dense CPU LDL^T solve
+    std::vector<double> A((size_t)n * n, 0.0);
+    for (int r = 0; r < n; ++r) {
+        A[(size_t)r * n + r] = bd[r];
+        if (r % B) A[(size_t)r * n + r - 1] = A[(size_t)(r - 1) * n + r] = -bw[r];
+        if (r >= B) A[(size_t)r * n + r - B] = A[(size_t)(r - B) * n + r] = -bs[r];
+    }
+    std::vector<double> x = y;
+    for (int k = 0; k < n; ++k) {
+        const double d = A[(size_t)k * n + k];
+        const int hi = std::min(n, k + B + 1);
+        for (int i = k + 1; i < hi; ++i) {
+            const double l = A[(size_t)i * n + k] / d;
+            for (int j = k + 1; j <= i; ++j) A[(size_t)i * n + j] -= l * A[(size_t)j * n + k];
+            x[i] -= l * x[k];
+        }
+        for (int i = k + 1; i < hi; ++i) A[(size_t)i * n + k] /= d;
+    }
+    for (int i = 0; i < n; ++i) x[i] /= A[(size_t)i * n + i];
+    for (int i = n - 1; i >= 0; --i)
+        for (int k = i + 1; k < std::min(n, i + B + 1); ++k) x[i] -= A[(size_t)k * n + i] * x[k];
+    double *dBD, *dBW, *dBS, *dD, *dLr, *dY, *dYv;
+    int* dok;
+    cudaMalloc(&dBD, n * 8);
+    cudaMalloc(&dBW, n * 8);
+    cudaMalloc(&dBS, n * 8);
+    cudaMalloc(&dD, WARPS * n * 8);
+    cudaMalloc(&dLr, (size_t)WARPS * n * B * 8);
+    cudaMalloc(&dY, (size_t)WARPS * n * 8);
+    cudaMalloc(&dYv, (size_t)WARPS * n * 8);
+    cudaMalloc(&dok, WARPS * 4);
+    cudaMemcpy(dBD, bd.data(), n * 8, cudaMemcpyHostToDevice);
+    cudaMemcpy(dBW, bw.data(), n * 8, cudaMemcpyHostToDevice);
+    cudaMemcpy(dBS, bs.data(), n * 8, cudaMemcpyHostToDevice);
+    for (int w = 0; w < WARPS; ++w) cudaMemcpy(dY + (size_t)w * n, y.data(), n * 8, cudaMemcpyHostToDevice);
+    k_twist<B, WARPS><<<1, 32 * WARPS>>>(n, dBD, dBW, dBS, dD, dLr, dY, dYv, dok);
+    cudaError_t e = cudaDeviceSynchronize();
+    std::vector<double> xg((size_t)WARPS * n);
+    int okh[WARPS];
+    cudaMemcpy(xg.data(), dY, xg.size() * 8, cudaMemcpyDeviceToHost);
+    cudaMemcpy(okh, dok, WARPS * 4, cudaMemcpyDeviceToHost);
+    double ex = 0.0, nx = 0.0;
+    bool nan = false;
+    for (int w = 0; w < WARPS; ++w)
+        for (int i = 0; i < n; ++i) {
+            const double v = xg[(size_t)w * n + i];
+            if (!(v == v)) nan = true;
+            ex = std::max(ex, std::fabs(v - x[i]));
+            nx = std::max(nx, std::fabs(x[i]));
+        }
+    printf("twisted B=%2d rows=%3d warps=%d: x rel err %.2e ok=%d nan=%d %s\n", B, m, WARPS, ex / nx, okh[0], nan,
+           cudaGetErrorString(e));
+    cudaFree(dBD); cudaFree(dBW); cudaFree(dBS); cudaFree(dD); cudaFree(dLr); cudaFree(dY); cudaFree(dYv);
+    cudaFree(dok);
 }
 
 template <int B, int NR>
@@ -172,5 +258,14 @@ int main() {
     run<16, 1>(16, 1, 2);
     run<32, 1>(32, 1, 2);
     run<32, 9>(32, 9, 2);
+    run_twist<16, 1>(16);
+    run_twist<16, 1>(15);
+    run_twist<16, 2>(16);
+    run_twist<16, 1>(3);
+    run_twist<16, 1>(4);
+    run_twist<8, 1>(8);
+    run_twist<8, 2>(9);
+    run_twist<4, 1>(8);
+    run_twist<12, 1>(12);
     return 0;
 }
