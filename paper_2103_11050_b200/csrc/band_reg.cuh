@@ -278,6 +278,10 @@ __device__ void forward_reg(int n, const double* Lcol, double* Y, int nr, int ld
 #pragma unroll
         for (int m = 0; m < NR; ++m) cb[m] = nbv[m];
     }
+    if constexpr (RG > 0) {  // drain the trailing prefetches: the next sweep refills the same ring slots
+        cp_async_wait<0>();
+        __syncwarp();
+    }
 }
 
 // Backward sweep L^T x = D^-1 y with a stored factor (Lrow, D), NR RHS in place.
@@ -360,6 +364,10 @@ __device__ void backward_reg(int n, const double* D, const double* Lrow, double*
                 z[m] = fma(-l, xk[m], fma(z[m], keep, piv ? ez[m] : 0.0));
             }
         }
+    }
+    if constexpr (RG > 0) {  // no copy may still be landing in the ring when the caller reuses it
+        cp_async_wait<0>();
+        __syncwarp();
     }
 }
 

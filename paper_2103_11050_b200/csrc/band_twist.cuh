@@ -83,8 +83,11 @@ __device__ bool twisted_solve(int n, const BandRows A, double* D, double* Lrow, 
         fs = vofs(rr < B ? B : rr);
         fb = vrhs(rr);
     };
-    double cd, cw, cs, cb;
+    // entering-row data two chunks ahead (one chunk of steps is shorter than a
+    // cold HBM round trip)
+    double cd, cw, cs, cb, md, mw, ms, mb;
     fetch(B + llc, cd, cw, cs, cb);
+    fetch(2 * B + llc, md, mw, ms, mb);
     bool ok = true;
     double st_l = 0.0;
     int st_pos = 0;
@@ -95,7 +98,7 @@ __device__ bool twisted_solve(int n, const BandRows A, double* D, double* Lrow, 
         const int k0 = c * B;
         const bool active = c < Ch;
         double nd, nw, ns, nb;
-        fetch(k0 + 2 * B + llc, nd, nw, ns, nb);
+        fetch(k0 + 3 * B + llc, nd, nw, ns, nb);
 #pragma unroll
         for (int u = 0; u < B; ++u) {
             const int k = k0 + u;
@@ -142,10 +145,14 @@ __device__ bool twisted_solve(int n, const BandRows A, double* D, double* Lrow, 
             yv = fma(-l, yk, fma(yv, keep, reset ? cb : 0.0));
             __syncwarp();
         }
-        cd = nd;
-        cw = nw;
-        cs = ns;
-        cb = nb;
+        cd = md;
+        cw = mw;
+        cs = ms;
+        cb = mb;
+        md = nd;
+        mw = nw;
+        ms = ns;
+        mb = nb;
     }
     if (act && st_act) stage[ll * B + st_pos] = st_l;
     // ---- middle block ------------------------------------------------------
@@ -233,14 +240,17 @@ __device__ bool twisted_solve(int n, const BandRows A, double* D, double* Lrow, 
         d = D[obase + rr];
         y = Yel[rr];
     };
-    double rd, ry;
+    double rd, ry, rd2, ry2;  // (d, y) of the entering rows one and two chunks ahead
     raw((nch - 2) * B + llc, rd, ry);
+    raw((nch - 3) * B + llc, rd2, ry2);
     double lq[B];
     for (int t = 0; t < nch; ++t) {
         const int c = nch - 1 - t, k0 = c * B;
         const bool active = c < Ch;
-        const double ez = ry * (1.0 / rd);  // entering rows of this chunk (chunk c-1), loaded one chunk ago
-        raw(k0 - 2 * B + llc, rd, ry);
+        const double ez = ry * (1.0 / rd);  // entering rows of this chunk (chunk c-1), loaded two chunks ago
+        rd = rd2;
+        ry = ry2;
+        raw(k0 - 3 * B + llc, rd2, ry2);
         {
             const int slot = t % RG;
             cp_async_wait<RG - 1>();
@@ -263,6 +273,8 @@ __device__ bool twisted_solve(int n, const BandRows A, double* D, double* Lrow, 
             z = fma(-l, xk, fma(z, keep, reset ? ez : 0.0));
         }
     }
+    cp_async_wait<0>();  // drain the trailing ring prefetches before the caller reuses shared memory
+    __syncwarp();
     return __all_sync(FULL, ok);
 }
 

@@ -888,11 +888,35 @@ __global__ void __launch_bounds__(WPBT * 32) k_ds_solve_t(Layout L, const double
     const bool ok = twisted_solve<B>(n, A, D + so, Lr + so * B, x, Yv + so, sm[w]);
     if (!ok && lane == 0) atomicOr(&sc->err, ERR_PIVOT);
     __syncwarp();
+    // mean shift (mrcm.cpp:430-437): all loads of x first, then the scatter
+    constexpr int PER = 8;
     double v = 0.0;
-    for (int r = lane; r < n; r += 32) v += x[r];
+    const double rs = RS[s];
+    for (int r0 = 0; r0 < n; r0 += 32 * PER) {
+        double xv[PER];
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int r = r0 + lane + 32 * q;
+            xv[q] = r < n ? __ldcg(x + r) : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < PER; ++q) v += xv[q];
+    }
     v = warp_sum(v);
-    const double shift = (__shfl_sync(0xffffffffu, RS[s], 0) - __shfl_sync(0xffffffffu, v, 0)) / n;
-    for (int r = lane; r < n; r += 32) p[L.gcell_of(s, r)] = x[r] + shift;
+    const double shift = (rs - __shfl_sync(0xffffffffu, v, 0)) / n;
+    for (int r0 = 0; r0 < n; r0 += 32 * PER) {
+        double xv[PER];
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int r = r0 + lane + 32 * q;
+            xv[q] = r < n ? __ldcg(x + r) : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int r = r0 + lane + 32 * q;
+            if (r < n) p[L.gcell_of(s, r)] = xv[q] + shift;
+        }
+    }
 }
 #define MPM2P_TWIST_WIDTHS(X) X(4) X(8) X(10) X(12) X(16)
 
