@@ -507,6 +507,15 @@ __global__ void __launch_bounds__(256, 2) k_gj_pp(PPArgs a) {
             for (int item = blockIdx.x; item < nb * nch; item += nwork) {
                 const int i = item / nch, q = item % nch;
                 const int col0 = q * PPW;
+                // this thread's 4 x 4 source values, issued first (used last)
+                double gsrc[4][4];
+#pragma unroll
+                for (int a2 = 0; a2 < 4; ++a2)
+#pragma unroll
+                    for (int m = 0; m < 4; ++m) {
+                        const int col = col0 + wx + 32 * m;
+                        gsrc[a2][m] = col < np ? __ldcg(src + (size_t)(i * PPB + 4 * wy + a2) * ld + col) : 0.0;
+                    }
                 __syncthreads();  // previous item's readers of Cs / Ts / Ws are done
                 if (i != k) pp_load(Cs, blk(src, i, k), ld);
                 {  // pivot block-row slice W_k,[col0, col0+128) (columns past np read as 0), loads batched
@@ -549,7 +558,6 @@ __global__ void __launch_bounds__(256, 2) k_gj_pp(PPArgs a) {
                 for (int a2 = 0; a2 < 4; ++a2) {
                     const int row = 4 * wy + a2;
                     double* orow = dst + (size_t)(i * PPB + row) * ld;
-                    const double* srow = src + (size_t)(i * PPB + row) * ld;
 #pragma unroll
                     for (int m = 0; m < 4; ++m) {
                         const int col = col0 + wx + 32 * m;
@@ -559,7 +567,7 @@ __global__ void __launch_bounds__(256, 2) k_gj_pp(PPArgs a) {
                         if (jb == k) o = (i == k) ? Ps[row][cl] : -Ts[row][cl];
                         else if (i == k) o = acc[a2][m];
                         else if (i == k + 1 && jb == k + 1) continue;  // the lookahead's block
-                        else o = __ldcg(srow + col) - acc[a2][m];
+                        else o = gsrc[a2][m] - acc[a2][m];
                         orow[col] = o;
                     }
                 }

@@ -88,10 +88,14 @@ __device__ __forceinline__ DD reduce_dd_partials(const double* part, int nparts,
     return block_reduce_dd(v, sh);
 }
 
-__global__ void k_max_slope(Scalars* sc, double M) {  // transport.cpp:45-49
+// max over the reference's 1001 sample points (transport.cpp:45-49); max is
+// order-independent, so one thread per point gives the same value.
+__global__ void k_max_slope(Scalars* sc, double M) {
+    __shared__ double sh[32];
     double m = 0.0;
-    for (int k = 0; k <= 1000; ++k) m = fmax(m, fprime(k * 1e-3, M));
-    sc->slope = m;
+    for (int k = threadIdx.x; k <= 1000; k += blockDim.x) m = fmax(m, fprime(k * 1e-3, M));
+    m = block_reduce_op(m, [](double a, double b) { return fmax(a, b); }, 0.0, sh);
+    if (threadIdx.x == 0) sc->slope = m;
 }
 
 // cfl_timestep (transport.cpp:51-71): min over cells of vol/(outflux*slope).
@@ -392,7 +396,7 @@ int red_grid(const Ctx& c) { return std::min(2 * c.num_sms, std::max(1, cdiv(c.L
 void launch_max_slope(Ctx& c) {
     {
         PROF(c, "k_max_slope");
-        k_max_slope<<<1, 1, 0, c.st>>>(c.sc, c.M);
+        k_max_slope<<<1, 1024, 0, c.st>>>(c.sc, c.M);
         CK_LAUNCH();
     }
 }
