@@ -130,6 +130,22 @@ void build_csr(Ctx& c) {
         ptr.push_back((int)col.size());
     }
     c.nnz = (int)col.size();
+    // transposed positions (the pattern is structurally symmetric): tpos[z] for
+    // z = (i, j) is the index of (j, i) in row j
+    std::vector<int> tpos(col.size(), -1);
+    for (int r = 0; r + 1 < (int)ptr.size(); ++r)
+        for (int z = ptr[r]; z < ptr[r + 1]; ++z) {
+            const int j = col[z];
+            for (int z2 = ptr[j]; z2 < ptr[j + 1]; ++z2)
+                if (col[z2] == r) {
+                    tpos[z] = z2;
+                    break;
+                }
+            if (tpos[z] < 0) throw ConfigError("interface system: CSR pattern is not symmetric");
+        }
+    c.csr_tpos.alloc(std::max<size_t>(tpos.size(), 1));
+    if (!tpos.empty())
+        CK(cudaMemcpyAsync(c.csr_tpos.p, tpos.data(), tpos.size() * sizeof(int), cudaMemcpyHostToDevice, c.st));
     c.csr_ptr.alloc(ptr.size());
     std::vector<int> rowv(col.size());
     for (size_t r = 0; r + 1 < ptr.size(); ++r)
@@ -291,10 +307,7 @@ void create_ctx(mpm2p_ctx* ctx, const mpm2p_problem* P) {
     c.bpm.alloc(ns * nbe);
     c.pmsum.alloc(ns);
     const size_t dim = std::max(1, c.dim);
-    if (c.dim > 0 && !c.use_krylov) {
-        c.Mdense.alloc((size_t)c.dim * c.dim);
-        c.Minv.alloc((size_t)c.dim * c.dim);
-    }
+    if (c.dim > 0 && !c.use_krylov) c.Minv.alloc((size_t)c.dim * c.dim);  // dense M only on the pivoted fallback
     c.irhs.alloc(dim);
     c.icoef.alloc(dim);
     c.ires.alloc(dim);
@@ -759,8 +772,7 @@ int mpm2p_interface_matrix(mpm2p_ctx* ctx, double* M) {
     return guarded(ctx, [&] {
         Ctx& c = ctx->c;
         if (!c.has_basis) throw ConfigError("interface_matrix: no basis installed");
-        if (c.dim > 0 && !c.use_krylov) download(c, M, c.Mdense, (size_t)c.dim * c.dim);
-        if (c.dim > 0 && c.use_krylov && M) {  // no dense copy on the Krylov path: scatter the CSR values
+        if (c.dim > 0 && M) {  // the operator lives in CSR: scatter its values
             std::vector<int> ptr(c.dim + 1), col(c.nnz);
             std::vector<double> val(c.nnz);
             CK(cudaMemcpyAsync(ptr.data(), c.csr_ptr.p, ptr.size() * sizeof(int), cudaMemcpyDeviceToHost, c.st));

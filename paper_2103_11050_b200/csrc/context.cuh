@@ -84,7 +84,7 @@ struct Ctx {
     DevBuf<double> HU, HB, HP;
     DevBuf<double> pm, bpm, pmsum;
     // interface system (CSR pattern built once; values per rebuild)
-    DevBuf<int> csr_ptr, csr_col, csr_row;
+    DevBuf<int> csr_ptr, csr_col, csr_row, csr_tpos;  // tpos[z]: position of the transposed entry
     DevBuf<double> csr_val, Mdense, Minv, gj_work, gj_col, gj_row, gj_krow;
     DevBuf<int> gj_piv;
     DevBuf<double> gj_pp;     // ping-pong GJ: two padded copies + two 32 x 32 pivot inverses
@@ -230,6 +230,10 @@ double dense_inverse(Ctx& c, const double* A, double* Ainv, int n);
 // device error word when rcond <= threshold (no host synchronisation).
 void dense_inverse_async(Ctx& c, const double* A, double* Ainv, int n, double* rcond_dev, unsigned err_bit,
                          double threshold);
+// Interface inverse straight from the CSR operator (K = J M built padded,
+// ping-pong GJ, M^-1 and the device rcond guard). Returns false when K is
+// not symmetric (the caller then takes the pivoted dense path).
+bool interface_inverse_csr(Ctx& c, double* rcond_dev, unsigned err_bit, double threshold);
 // Interface matrix: pivot-free blocked GJ on K = J M (symmetric quasi-definite).
 void interface_inverse_async(Ctx& c, const double* M, double* Minv, int n, double* rcond_dev, unsigned err_bit,
                              double threshold);

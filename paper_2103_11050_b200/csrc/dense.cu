@@ -579,6 +579,68 @@ __global__ void __launch_bounds__(256, 2) k_gj_pp(PPArgs a) {
     }
 }
 
+// Rebuild path straight from the sparse operator (no dense M, no extra
+// n^2 passes): padded K = J M is written row by row from the CSR rows of M
+// (one warp per row: zero the row, then scatter), and the Gauss-Jordan
+// result is turned into M^-1 = K^-1 J together with its column 1-norm
+// partials in one pass (k_kinv_out); ||M||_1 comes from the CSR through the
+// transposed-position table (the pattern is structurally symmetric).
+__global__ void k_build_k(const int* __restrict__ ptr, const int* __restrict__ col, const double* __restrict__ val,
+                          int n, double* __restrict__ W, int ld) {
+    const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (r >= ld) return;
+    double* row = W + (size_t)r * ld;
+    for (int j = lane; j < ld; j += 32) row[j] = (r >= n && j == r) ? 1.0 : 0.0;
+    __syncwarp();
+    if (r < n) {
+        const int h = n / 2;
+        const int srow = r < h ? h + r : r - h;
+        const double sg = r < h ? 1.0 : -1.0;
+        for (int z = ptr[srow] + lane; z < ptr[srow + 1]; z += 32) row[col[z]] = sg * val[z];
+    }
+}
+
+// Minv[i][j] = (j < h ? -Kinv[i][h+j] : Kinv[i][j-h]); part[slab][n + j] =
+// sum over the slab's 64 rows of |Minv[i][j]| (fixed order), part[slab][j] = 0
+// (the A half is filled by k_mnorm). Block: 32 columns x 8 row groups.
+__global__ void k_kinv_out(const double* __restrict__ Kinv, int ld, int n, double* __restrict__ Minv, double* part) {
+    __shared__ double red[8][33];
+    const int c = threadIdx.x & 31, rg = threadIdx.x >> 5;
+    const int j = blockIdx.x * 32 + c, slab = blockIdx.y;
+    const int h = n / 2;
+    double acc = 0.0;
+    if (j < n) {
+        const int pj = j < h ? h + j : j - h;
+        const double sg = j < h ? -1.0 : 1.0;
+        for (int t = 0; t < 8; ++t) {
+            const int i = slab * 64 + rg + 8 * t;
+            if (i >= n) break;
+            const double v = sg * Kinv[(size_t)i * ld + pj];
+            Minv[(size_t)i * n + j] = v;
+            acc += fabs(v);
+        }
+    }
+    red[rg][c] = acc;
+    __syncthreads();
+    if (rg == 0 && j < n) {
+        double sacc = red[0][c];
+        for (int g = 1; g < 8; ++g) sacc += red[g][c];
+        part[(size_t)slab * 2 * n + n + j] = sacc;
+        part[(size_t)slab * 2 * n + j] = 0.0;
+    }
+}
+
+// ||M||_1 column sums from the CSR: column j's entries are M[i][j] for the
+// pattern of row j (symmetric pattern), found at tpos[z] (z in row j).
+__global__ void k_mnorm(const int* __restrict__ ptr, const int* __restrict__ tpos, const double* __restrict__ val,
+                        int n, double* part) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    double s = 0.0;
+    for (int z = ptr[j]; z < ptr[j + 1]; ++z) s += fabs(val[tpos[z]]);
+    part[j] = s;  // slab 0, A half
+}
+
 // npad x npad copy with identity padding (and back).
 __global__ void k_pad_in(const double* __restrict__ A, int n, double* __restrict__ W, int ld) {
     for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < (long long)ld * ld;
@@ -790,6 +852,7 @@ __global__ void k_axpy(double* __restrict__ y, const double* __restrict__ x, int
 namespace {
 
 void block_gj_legacy(Ctx& c, double* W, int n);
+void gj_pp_run(Ctx& c, double* W0, double* W1, int nb, int ld, int n);
 
 // In-place inverse of W (n x n) by the ping-pong blocked GJ (k_gj_pp).
 void block_gj_inplace(Ctx& c, double* W, int n) {
@@ -809,6 +872,17 @@ void block_gj_inplace(Ctx& c, double* W, int n) {
         k_pad_in<<<g, TPB, 0, c.st>>>(W, n, W0, ld);
         CK_LAUNCH();
     }
+    gj_pp_run(c, W0, W1, nb, ld, n);
+    {
+        PROF(c, "k_pad_out");
+        k_pad_out<<<g, TPB, 0, c.st>>>((nb & 1) ? W1 : W0, ld, W, n);
+        CK_LAUNCH();
+    }
+}
+
+// k_gj_pp on the padded pair (W0 holds the matrix; the inverse ends in
+// W[nb % 2]).
+void gj_pp_run(Ctx& c, double* W0, double* W1, int nb, int ld, int n) {
     static int per_sm = -1;
     if (per_sm < 0) {  // set once, outside any graph capture
         CK(cudaFuncSetAttribute(k_gj_pp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PP_SMEM));
@@ -832,11 +906,6 @@ void block_gj_inplace(Ctx& c, double* W, int n) {
     {
         PROF(c, "k_gj_pp");
         CK(cudaLaunchCooperativeKernel((void*)k_gj_pp, blocks, 256, args, PP_SMEM, c.st));
-        CK_LAUNCH();
-    }
-    {
-        PROF(c, "k_pad_out");
-        k_pad_out<<<g, TPB, 0, c.st>>>((nb & 1) ? W1 : W0, ld, W, n);
         CK_LAUNCH();
     }
     if (trace) {  // developer trace: lookahead load+mul / invert / publish, worker, barrier (us)
@@ -893,6 +962,75 @@ void launch_rcond(Ctx& c, const double* A, const double* Ainv, int n, double* rc
 }
 
 }  // namespace
+
+// Interface inverse from the CSR operator (dense path): K = J M built padded
+// into the ping-pong buffer, k_gj_pp, then M^-1 and the rcond guard. The
+// symmetry of K is checked once per context on the CSR values (host).
+bool interface_inverse_csr(Ctx& c, double* rcond_dev, unsigned err_bit, double threshold) {
+    const int n = c.dim;
+    if (n == 0) return true;
+    if (c.iface_sym < 0) {
+        std::vector<int> ptr(n + 1), col(c.nnz), tpos(c.nnz);
+        std::vector<double> val(c.nnz);
+        CK(cudaMemcpyAsync(ptr.data(), c.csr_ptr.p, ptr.size() * sizeof(int), cudaMemcpyDeviceToHost, c.st));
+        CK(cudaMemcpyAsync(col.data(), c.csr_col.p, col.size() * sizeof(int), cudaMemcpyDeviceToHost, c.st));
+        CK(cudaMemcpyAsync(tpos.data(), c.csr_tpos.p, tpos.size() * sizeof(int), cudaMemcpyDeviceToHost, c.st));
+        CK(cudaMemcpyAsync(val.data(), c.csr_val.p, val.size() * sizeof(double), cudaMemcpyDeviceToHost, c.st));
+        CK(cudaStreamSynchronize(c.st));
+        const int h = n / 2;
+        auto kval = [&](int r, int z) { return (r < h ? 1.0 : -1.0) * val[z]; };  // K row r = J-permuted M row
+        auto src = [&](int r) { return r < h ? h + r : r - h; };
+        // K[i][j] with i = K row: its CSR row is M row src(i); K[j][i] likewise.
+        double d = 0.0, m = 0.0;
+        std::vector<int> inv(n);
+        for (int r = 0; r < n; ++r) inv[src(r)] = r;  // M row -> K row
+        for (int mr = 0; mr < n; ++mr) {
+            const int kr = inv[mr];
+            for (int z = ptr[mr]; z < ptr[mr + 1]; ++z) {
+                const int kc = col[z];  // K[kr][kc] = kval(kr, z); K[kc][kr] lives in M row src(kc)
+                const int mr2 = src(kc);
+                double other = 0.0;
+                for (int z2 = ptr[mr2]; z2 < ptr[mr2 + 1]; ++z2)
+                    if (col[z2] == kr) other = kval(kc, z2);
+                d = std::max(d, std::fabs(kval(kr, z) - other));
+                m = std::max(m, std::fabs(kval(kr, z)));
+            }
+        }
+        c.iface_sym = (m > 0.0 && d <= 1e-12 * m) ? 1 : 0;
+    }
+    if (c.iface_sym != 1) return false;  // caller takes the pivoted dense path
+    const int nb = cdiv(n, PPB), ld = nb * PPB;
+    c.gj_pp.alloc(std::max(c.gj_pp.n, 2 * (size_t)ld * ld + 2 * PPB * PPB));
+    c.gj_piv.alloc(std::max(c.gj_piv.n, (size_t)n + 1));
+    CK(cudaMemsetAsync(c.gj_piv.p + n, 0, sizeof(int), c.st));
+    double* W0 = c.gj_pp.p;
+    double* W1 = W0 + (size_t)ld * ld;
+    {
+        PROF(c, "k_build_k");
+        k_build_k<<<cdiv((long long)ld * 32, TPB), TPB, 0, c.st>>>(c.csr_ptr, c.csr_col, c.csr_val, n, W0, ld);
+        CK_LAUNCH();
+    }
+    gj_pp_run(c, W0, W1, nb, ld, n);
+    const int nrb = cdiv(n, 64);
+    c.gj_work.alloc(std::max(c.gj_work.n, (size_t)2 * n * nrb));
+    {
+        PROF(c, "k_kinv_out");
+        k_kinv_out<<<dim3(cdiv(n, 32), nrb), 256, 0, c.st>>>((nb & 1) ? W1 : W0, ld, n, c.Minv, c.gj_work.p);
+        CK_LAUNCH();
+    }
+    {
+        PROF(c, "k_mnorm");
+        k_mnorm<<<cdiv(n, TPB), TPB, 0, c.st>>>(c.csr_ptr, c.csr_tpos, c.csr_val, n, c.gj_work.p);
+        CK_LAUNCH();
+    }
+    {
+        PROF(c, "k_rcond");
+        k_rcond<<<1, 1024, 0, c.st>>>(c.gj_work.p, n, nrb, c.gj_piv.p + n, rcond_dev, &c.sc.p->err, err_bit,
+                                      threshold);
+        CK_LAUNCH();
+    }
+    return true;
+}
 
 // Interface matrix inverse: pivot-free blocked GJ on K = J M when K is
 // symmetric (checked once per context; the formulation makes it so), else the

@@ -1413,7 +1413,9 @@ void launch_rebuild(Ctx& c, const double* kappa, bool compute_beta) {  // comput
             // no dense factorisation: the rcond guard becomes MINRES
             // non-convergence (ERR_SINGULAR raised by k_minres)
             krylov_prepare(c);
-        } else {
+        } else if (c.gj_legacy || !interface_inverse_csr(c, &c.sc.p->rcond, ERR_SINGULAR, 1e-14)) {
+            // legacy / non-symmetric fallback through a dense copy of M
+            c.Mdense.alloc((size_t)c.dim * c.dim);
             {
                 PROF(c, "k_csr_to_dense");
                 k_csr_to_dense<<<c.dim, TPB, 0, c.st>>>(c.csr_ptr, c.csr_col, c.csr_val, c.dim, c.Mdense);
