@@ -1,5 +1,5 @@
-// band_twist.cuh — two-sided ("twisted") banded LDL^T solve of one subdomain
-// system on one warp, for half-bandwidth B <= 16.
+// band_twist.cuh — two-sided ("twisted") banded LDL^T on one warp, for
+// half-bandwidth B <= 16 (even).
 //
 // The register-window factorisation (band_reg.cuh) is a sequential chain of
 // n pivots and, for B <= 16, leaves lanes 16..31 idle. Here the two half-warps
@@ -7,20 +7,22 @@
 //   * the top half (lanes 0..15) eliminates rows 0 .. m-1 in natural order;
 //   * the bottom half (lanes 16..31) eliminates rows n-1 .. m+B in reverse
 //     order, i.e. the natural elimination of the reversed matrix
-//     A'[i][j] = A[n-1-i][n-1-j] (band structure preserved);
-// where the middle rows m .. m+B-1 (m = B * floor((rows-1)/2)) stay. Each
-// elimination only updates the middle block besides its own rows, so its
-// Schur complement is S = W_top + W_bot^T - A_mid (both windows end holding
-// the middle rows, each reduced by its own side). S (B x B, SPD) is solved
-// densely in registers, then both halves back-substitute outwards from the
-// middle, first folding the middle solution into their window with the
-// multipliers L[mid][*] left in their stage tiles.
-// The sequential chain drops from 2n steps to about n + B + small.
+//     A'[i][j] = A[n-1-i][n-1-j] (band structure preserved; "virtual" rows);
+// and the middle rows m .. m+B-1 (m = B * floor((rows-1)/2)) stay. Each
+// elimination only updates the middle block besides its own rows, so the
+// middle Schur complement is S = W_top + W_bot^T - A_mid (both register
+// windows end holding the middle rows, each reduced by its own side). S
+// (B x B, SPD) is solved or inverted densely in registers; both halves then
+// back-substitute outwards from the middle after folding the middle solution
+// into their window with the multipliers L[mid][*] of their side.
+// The sequential chain drops from 2n steps to about n + B.
 //
-// Outputs: x in Y (natural order). Factor storage (used inside the kernel
-// only): top rows in D/Lrow[0, m), bottom rows (reversed order) in
-// D/Lrow[m+B, n); the bottom's forward-eliminated RHS goes to Yv[0, n-m-B)
-// (a separate buffer: Y's entries there are still unread inputs).
+// Storage of a factor (twisted layout): top rows at [0, m) of D / Lcol /
+// Lrow, the top's middle multipliers as Lrow rows [m, m+B); bottom rows in
+// virtual order at [m+B, n); the bottom's middle multipliers and S^-1 in two
+// per-subdomain B x B arrays. A right-hand side is kept in natural order
+// throughout: a half stores the eliminated value of a pivot row at that row's
+// original position (its input was consumed when the row entered the window).
 #pragma once
 
 #include "band_reg.cuh"
@@ -28,43 +30,52 @@
 namespace mpm2p {
 
 template <int B>
-__host__ __device__ constexpr int twist_ring() {
-    return 2;
+__host__ __device__ constexpr int twist_ring() {  // chunks of stored factor in flight per half
+    return 4;
 }
+// shared memory per warp of the twisted kernels
 template <int B>
-__host__ __device__ constexpr int twist_smem_doubles() {  // per warp
-    return 2 * B * B                 // stage tiles (one per half)
-           + 2 * xchg_doubles<B, 1>()  // exchange buffers (one per half)
-           + 2 * twist_ring<B>() * B * B  // cp.async rings for the back substitution (one per half)
-           + 2 * B * B + 4 * B + 2 * B;   // middle block: both windows, RHS, solution
+__host__ __device__ constexpr int twist_smem_doubles() {
+    return 2 * B * B                       // stage tiles (one per half)
+           + 2 * xchg_doubles<B, 1>()      // exchange buffers (one per half)
+           + 2 * twist_ring<B>() * B * B   // cp.async rings for the sweeps (one per half)
+           + 2 * B * B + 4 * B + 2 * B;    // middle block: both windows, RHS, solution
 }
 
+// Per-lane geometry of the two-sided scheme.
 template <int B>
-__device__ bool twisted_solve(int n, const BandRows A, double* D, double* Lrow, double* Y, double* Yv, double* sm) {
-    static_assert(B <= 16 && B % 2 == 0, "two half-warps of B lanes");
-    constexpr int XB = xchg_doubles<B, 1>();
-    constexpr int RG = twist_ring<B>();
-    const int lane = threadIdx.x & 31;
-    const int h = lane >> 4, ll = lane & 15;
-    const bool act = ll < B;
-    const int llc = act ? ll : 0;
-    const int rows = n / B;
-    const int Ct = (rows - 1) / 2, Cb = rows - 1 - Ct;  // chunks eliminated by each half (Cb >= Ct)
-    const int m = Ct * B;                              // first middle row
-    const int Ch = h ? Cb : Ct;
-    const int obase = h ? m + B : 0;                   // storage offset of this half's factor rows
-    double* stage = sm + h * B * B;
-    double* xb = sm + 2 * B * B + h * XB;
-    double* ring = sm + 2 * B * B + 2 * XB + h * RG * B * B;
-    double* mid = sm + 2 * B * B + 2 * XB + 2 * RG * B * B;  // [2][B][B] windows, then RHS and x
-    double* Yel = h ? Yv : Y;                           // forward-eliminated RHS, virtual order
-    // virtual row -> matrix entries of this half
+struct Twist {
+    int n, rows, Ct, Cb, m, Ch, obase, h, ll, llc;
+    bool act;
+    __device__ Twist(int n_) : n(n_) {
+        const int lane = threadIdx.x & 31;
+        h = lane >> 4;
+        ll = lane & 15;
+        act = ll < B;
+        llc = act ? ll : 0;
+        rows = n / B;
+        Ct = (rows - 1) / 2;
+        Cb = rows - 1 - Ct;
+        m = Ct * B;
+        Ch = h ? Cb : Ct;
+        obase = h ? m + B : 0;
+    }
+    __device__ int orig(int v) const { return h ? n - 1 - v : v; }  // virtual row -> natural row
+};
+
+// ---- phase 1: elimination ---------------------------------------------------
+// Both halves eliminate their rows (top idles for chunk >= Ct), carrying one
+// right-hand side Y (natural order, eliminated values written in place).
+// Stores D, Lrow and (LCOL) Lcol in the twisted layout. On return the window
+// registers hold the middle rows and `stage` (per half) their multipliers.
+template <int B, bool LCOL>
+__device__ bool twist_eliminate(const Twist<B>& T, const BandRows A, double* D, double* Lcol, double* Lrow, double* Y,
+                                double* stage, double* xb, double (&reg)[B], double& yv) {
+    const int n = T.n, h = T.h, ll = T.ll, llc = T.llc;
+    const bool act = T.act;
     auto vdiag = [&](int i) { return A.diag[h ? n - 1 - i : i]; };
     auto vofw = [&](int i) { return A.offw[h ? n - i : i]; };          // i >= 1
     auto vofs = [&](int i) { return A.offs[h ? n - 1 - i + B : i]; };  // i >= B
-    auto vrhs = [&](int i) { return Y[h ? n - 1 - i : i]; };
-    double reg[B];
-    double yv;
 #pragma unroll
     for (int t = 0; t < B; ++t) {
         double v = 0.0;
@@ -74,17 +85,16 @@ __device__ bool twisted_solve(int n, const BandRows A, double* D, double* Lrow, 
         }
         reg[t] = v;
     }
-    yv = vrhs(llc);
+    yv = Y[T.orig(llc)];
     for (int x = ll; x < B * B; x += 16) stage[x] = 0.0;
     auto fetch = [&](int row, double& fd, double& fw, double& fs, double& fb) {
         const int rr = row < n ? row : n - 1;
         fd = vdiag(rr);
         fw = vofw(rr < 1 ? 1 : rr);
         fs = vofs(rr < B ? B : rr);
-        fb = vrhs(rr);
+        fb = Y[T.orig(rr)];
     };
-    // entering-row data two chunks ahead (one chunk of steps is shorter than a
-    // cold HBM round trip)
+    // entering-row data two chunks ahead
     double cd, cw, cs, cb, md, mw, ms, mb;
     fetch(B + llc, cd, cw, cs, cb);
     fetch(2 * B + llc, md, mw, ms, mb);
@@ -93,10 +103,9 @@ __device__ bool twisted_solve(int n, const BandRows A, double* D, double* Lrow, 
     int st_pos = 0;
     bool st_act = false;
     __syncwarp();
-    // ---- elimination: chunk c, both halves; the top idles for c >= Ct ------
-    for (int c = 0; c < Cb; ++c) {
+    for (int c = 0; c < T.Cb; ++c) {
         const int k0 = c * B;
-        const bool active = c < Ch;
+        const bool active = c < T.Ch;
         double nd, nw, ns, nb;
         fetch(k0 + 3 * B + llc, nd, nw, ns, nb);
 #pragma unroll
@@ -116,15 +125,16 @@ __device__ bool twisted_solve(int n, const BandRows A, double* D, double* Lrow, 
             __syncwarp();
             const double d = dbuf[0];
             const double yk = ybuf[0];
-            st_global_if(D + obase + k, d, piv && active);
-            st_global_if(Yel + k, yk, piv && active);
-            st_global_if(Lrow + (size_t)(obase + k) * B + llc, stage[u * B + llc], act && active);
+            st_global_if(D + T.obase + k, d, piv && active);
+            st_global_if(Y + T.orig(k), yk, piv && active);
+            st_global_if(Lrow + (size_t)(T.obase + k) * B + llc, stage[u * B + llc], act && active);
             ok = ok && (!active || d > 0.0);
             const bool reset = piv && active;
             const double keep = reset ? 0.0 : 1.0;
             const double fd_ = reset ? cd : 0.0, fw_ = reset ? -cw : 0.0;
             const double l = active ? cval * fast_rcp(d) : 0.0;
             const int j = band_j_of<B>(ll, u);
+            if (LCOL) st_global_if(Lcol + (size_t)(T.obase + k) * B + j, l, act && active);
             st_l = l;
             st_pos = B - 1 - j;
             st_act = active;
@@ -155,21 +165,26 @@ __device__ bool twisted_solve(int n, const BandRows A, double* D, double* Lrow, 
         mb = nb;
     }
     if (act && st_act) stage[ll * B + st_pos] = st_l;
-    // ---- middle block ------------------------------------------------------
-    // window lane i of each half holds middle row (top) m+i / (bottom) m+B-1-i;
-    // register j holds its entry in middle column (top) m+j / (bottom) m+B-1-j
-    double* W = mid + h * B * B;
+    __syncwarp();
+    return ok;
+}
+
+// ---- phase 2: the middle block ----------------------------------------------
+// Writes both windows and RHS to `mid`, assembles S in lanes 0..B-1 (row i of
+// S in srow) and the middle RHS r_i = y_top[i] + y_bot[B-1-i] - b[m+i].
+template <int B>
+__device__ void twist_middle_assemble(const Twist<B>& T, const BandRows A, const double* Y, const double (&reg)[B],
+                                      double yv, double* mid, double (&srow)[B], double& sr) {
+    const int lane = threadIdx.x & 31, m = T.m;
+    double* W = mid + T.h * B * B;
     double* rhs = mid + 2 * B * B;  // [2][B]
-    double* xm = rhs + 2 * B;       // [B] middle solution (+ B spare)
-    if (act) {
+    if (T.act) {
 #pragma unroll
-        for (int t = 0; t < B; ++t) W[ll * B + t] = reg[t];
-        rhs[h * B + ll] = yv;
+        for (int t = 0; t < B; ++t) W[T.ll * B + t] = reg[t];
+        rhs[T.h * B + T.ll] = yv;
     }
     __syncwarp();
-    // lanes 0..B-1: row i of S = W_top[i][j] + W_bot[B-1-j][B-1-i] - A_mid[i][j] (j <= i, mirrored)
-    double srow[B];
-    double sr = 0.0;
+    sr = 0.0;
     if (lane < B) {
         const int i = lane;
 #pragma unroll
@@ -186,15 +201,30 @@ __device__ bool twisted_solve(int n, const BandRows A, double* D, double* Lrow, 
         for (int jj = 0; jj < B; ++jj) srow[jj] = (jj == 0 ? 1.0 : 0.0);
     }
     __syncwarp();
-    // dense Gauss-Jordan on [S | r] (SPD: no pivoting), row i in lane i
-    double* pr = mid;  // reuse the window area: pivot row broadcast (B + 1 doubles, two parities)
+}
+
+// Dense Gauss-Jordan (SPD, no pivoting) on rows [S | I | r] held by lanes
+// 0..B-1; on return srow is row i of S^-1 (if INV) and sr is x_i. pr: 2(2B+2)
+// doubles of shared scratch (may alias the window area of `mid`).
+template <int B, bool INV>
+__device__ bool twist_middle_gj(double (&srow)[B], double& sr, double* pr) {
+    const int lane = threadIdx.x & 31;
+    double iv[B];
+#pragma unroll
+    for (int jj = 0; jj < B; ++jj) iv[jj] = (INV && lane == jj) ? 1.0 : 0.0;
+    bool ok = true;
+    constexpr int W = 2 * B + 2;
 #pragma unroll
     for (int k = 0; k < B; ++k) {
-        double* prk = pr + (k & 1) * (B + 2);
+        double* prk = pr + (k & 1) * W;
         if (lane == k) {
 #pragma unroll
             for (int jj = 0; jj < B; ++jj) prk[jj] = srow[jj];
-            prk[B] = sr;
+            if (INV) {
+#pragma unroll
+                for (int jj = 0; jj < B; ++jj) prk[B + jj] = iv[jj];
+            }
+            prk[2 * B] = sr;
         }
         __syncwarp();
         const double p = 1.0 / prk[k];
@@ -204,31 +234,40 @@ __device__ bool twisted_solve(int n, const BandRows A, double* D, double* Lrow, 
         const double sc = on ? p : 1.0;
 #pragma unroll
         for (int jj = 0; jj < B; ++jj) srow[jj] = fma(-f, prk[jj], srow[jj]) * sc;
-        sr = fma(-f, prk[B], sr) * sc;
+        if (INV) {
+#pragma unroll
+            for (int jj = 0; jj < B; ++jj) iv[jj] = fma(-f, prk[B + jj], iv[jj]) * sc;
+        }
+        sr = fma(-f, prk[2 * B], sr) * sc;
         __syncwarp();
     }
-    if (lane < B) {
-        xm[lane] = sr;
-        Y[m + lane] = sr;
+    if (INV) {
+#pragma unroll
+        for (int jj = 0; jj < B; ++jj) srow[jj] = iv[jj];
     }
-    __syncwarp();
-    // ---- back substitution, both halves outwards from the middle ------------
-    // this half's middle solution in its own (virtual) order
+    return ok;
+}
+
+// ---- phase 3: back substitution, both halves outwards from the middle -------
+// midL(i, o): multiplier of this half's middle row i (its virtual order) at
+// Lrow position o; xm: the middle solution (natural order, shared memory).
+template <int B, typename MidL>
+__device__ void twist_backward(const Twist<B>& T, const double* D, const double* Lrow, double* Y, const double* xm,
+                               double* ring, MidL midL) {
+    constexpr int RG = twist_ring<B>();
+    const int h = T.h, ll = T.ll, llc = T.llc, nch = T.Cb;
     auto xmid = [&](int i) { return xm[h ? B - 1 - i : i]; };
-    const int nch = Cb;
-    // window: rows of this half's last chunk Ch-1 (virtual), z = y/d - sum_mid L[mid][row] x_mid
     double z;
     {
-        const int row = (Ch - 1) * B + llc;
-        z = Yel[row] * (1.0 / D[obase + row]);
+        const int row = (T.Ch - 1) * B + llc;
+        z = Y[T.orig(row)] * (1.0 / D[T.obase + row]);
         double corr = 0.0;
-        for (int i = 0; i <= llc; ++i) corr = fma(stage[i * B + (llc - i)], xmid(i), corr);
+        for (int i = 0; i <= llc; ++i) corr = fma(midL(i, llc - i), xmid(i), corr);
         z -= corr;
     }
-    // stored factor rows of this half: chunk c of Lrow starts at row obase + c*B
     auto rfetch = [&](int c, int slot) {
         const int cc = c < 0 ? 0 : c;
-        const double* g = Lrow + (size_t)(obase + cc * B) * B;
+        const double* g = Lrow + (size_t)(T.obase + cc * B) * B;
         double* dst = ring + (size_t)slot * B * B;
         for (int p = ll; p < B * B / 2; p += 16) cp_async16(dst + 2 * p, g + 2 * p);
         cp_async_commit();
@@ -237,8 +276,8 @@ __device__ bool twisted_solve(int n, const BandRows A, double* D, double* Lrow, 
     for (int i = 0; i < RG; ++i) rfetch(nch - 1 - i, i);
     auto raw = [&](int row, double& d, double& y) {
         const int rr = row < 0 ? 0 : row;
-        d = D[obase + rr];
-        y = Yel[rr];
+        d = D[T.obase + rr];
+        y = Y[T.orig(rr)];
     };
     double rd, ry, rd2, ry2;  // (d, y) of the entering rows one and two chunks ahead
     raw((nch - 2) * B + llc, rd, ry);
@@ -246,8 +285,8 @@ __device__ bool twisted_solve(int n, const BandRows A, double* D, double* Lrow, 
     double lq[B];
     for (int t = 0; t < nch; ++t) {
         const int c = nch - 1 - t, k0 = c * B;
-        const bool active = c < Ch;
-        const double ez = ry * (1.0 / rd);  // entering rows of this chunk (chunk c-1), loaded two chunks ago
+        const bool active = c < T.Ch;
+        const double ez = ry * (1.0 / rd);
         rd = rd2;
         ry = ry2;
         raw(k0 - 3 * B + llc, rd2, ry2);
@@ -266,7 +305,7 @@ __device__ bool twisted_solve(int n, const BandRows A, double* D, double* Lrow, 
             const int k = k0 + uu;
             const bool piv = ll == uu;
             const double xk = __shfl_sync(FULL, z, (h << 4) + uu);
-            st_global_if(Y + (h ? n - 1 - k : k), xk, piv && active);
+            st_global_if(Y + T.orig(k), xk, piv && active);
             const bool reset = piv && active;
             const double keep = reset ? 0.0 : 1.0;
             const double l = active ? lq[uu] : 0.0;
@@ -275,7 +314,151 @@ __device__ bool twisted_solve(int n, const BandRows A, double* D, double* Lrow, 
     }
     cp_async_wait<0>();  // drain the trailing ring prefetches before the caller reuses shared memory
     __syncwarp();
+}
+
+// ---- phase 1': forward sweep with a stored factor ---------------------------
+// On return yv (window lanes) holds this half's reduced middle RHS.
+template <int B>
+__device__ void twist_forward(const Twist<B>& T, const double* Lcol, double* Y, double* ring, double& yv) {
+    constexpr int RG = twist_ring<B>();
+    const int n = T.n, h = T.h, ll = T.ll, llc = T.llc, nch = T.Cb;
+    yv = Y[T.orig(llc)];
+    auto yat = [&](int row) { return Y[T.orig(row < n ? row : n - 1)]; };
+    auto rfetch = [&](int c, int slot) {
+        const int cc = c < nch ? c : nch - 1;
+        const double* g = Lcol + (size_t)(T.obase + cc * B) * B;
+        double* dst = ring + (size_t)slot * B * B;
+        for (int p = ll; p < B * B / 2; p += 16) cp_async16(dst + 2 * p, g + 2 * p);
+        cp_async_commit();
+    };
+#pragma unroll
+    for (int i = 0; i < RG; ++i) rfetch(i, i);
+    double cb = yat(B + llc), mb = yat(2 * B + llc);
+    double lq[B];
+    for (int c = 0; c < nch; ++c) {
+        const int k0 = c * B;
+        const bool active = c < T.Ch;
+        const double nb = yat(k0 + 3 * B + llc);
+        {
+            const int slot = c % RG;
+            cp_async_wait<RG - 1>();
+            __syncwarp();
+            const double* rs = ring + (size_t)slot * B * B;
+#pragma unroll
+            for (int u = 0; u < B; ++u) lq[u] = rs[u * B + band_j_of<B>(llc, u)];
+            __syncwarp();
+            rfetch(c + RG, slot);
+        }
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            const int k = k0 + u;
+            const bool piv = ll == u;
+            const double yk = __shfl_sync(FULL, yv, (h << 4) + u);
+            st_global_if(Y + T.orig(k), yk, piv && active);
+            const bool reset = piv && active;
+            const double keep = reset ? 0.0 : 1.0;
+            const double l = active ? lq[u] : 0.0;
+            yv = fma(-l, yk, fma(yv, keep, reset ? cb : 0.0));
+        }
+        cb = mb;
+        mb = nb;
+    }
+    cp_async_wait<0>();
+    __syncwarp();
+}
+
+// ---- solvers built from the phases -------------------------------------------
+// Fresh operator, one RHS (the downscale): x in Y; D / Lrow used as scratch.
+template <int B>
+__device__ bool twisted_solve(int n, const BandRows A, double* D, double* Lrow, double* Y, double* sm) {
+    static_assert(B <= 16 && B % 2 == 0, "two half-warps of B lanes");
+    constexpr int XB = xchg_doubles<B, 1>();
+    constexpr int RG = twist_ring<B>();
+    const Twist<B> T(n);
+    double* stage = sm + T.h * B * B;
+    double* xb = sm + 2 * B * B + T.h * XB;
+    double* ring = sm + 2 * B * B + 2 * XB + T.h * RG * B * B;
+    double* mid = sm + 2 * B * B + 2 * XB + 2 * RG * B * B;
+    double reg[B], yv;
+    bool ok = twist_eliminate<B, false>(T, A, D, nullptr, Lrow, Y, stage, xb, reg, yv);
+    double srow[B], sr;
+    twist_middle_assemble<B>(T, A, Y, reg, yv, mid, srow, sr);
+    ok = twist_middle_gj<B, false>(srow, sr, mid) && ok;
+    double* xm = mid + 2 * B * B + 2 * B;
+    const int lane = threadIdx.x & 31;
+    if (lane < B) {
+        xm[lane] = sr;
+        Y[T.m + lane] = sr;
+    }
+    __syncwarp();
+    const double* st = stage;  // this half's middle multipliers, Lrow layout
+    twist_backward<B>(T, D, Lrow, Y, xm, ring, [&](int i, int o) { return st[i * B + o]; });
     return __all_sync(FULL, ok);
+}
+
+// Rebuild factor: stores the twisted factor (D, Lcol, Lrow, the bottom's
+// middle multipliers MidB and S^-1 Sinv, B x B each) and solves one RHS.
+template <int B>
+__device__ bool twisted_factor(int n, const BandRows A, double* D, double* Lcol, double* Lrow, double* MidB,
+                               double* Sinv, double* Y, double* sm) {
+    static_assert(B <= 16 && B % 2 == 0, "two half-warps of B lanes");
+    constexpr int XB = xchg_doubles<B, 1>();
+    constexpr int RG = twist_ring<B>();
+    const Twist<B> T(n);
+    double* stage = sm + T.h * B * B;
+    double* xb = sm + 2 * B * B + T.h * XB;
+    double* ring = sm + 2 * B * B + 2 * XB + T.h * RG * B * B;
+    double* mid = sm + 2 * B * B + 2 * XB + 2 * RG * B * B;
+    double reg[B], yv;
+    bool ok = twist_eliminate<B, true>(T, A, D, Lcol, Lrow, Y, stage, xb, reg, yv);
+    {  // middle multipliers of each side: top as Lrow rows [m, m+B), bottom in MidB
+        double* dst = T.h ? MidB : Lrow + (size_t)T.m * B;
+        for (int x = T.ll; x < B * B; x += 16) dst[x] = stage[x];
+    }
+    double srow[B], sr;
+    twist_middle_assemble<B>(T, A, Y, reg, yv, mid, srow, sr);
+    ok = twist_middle_gj<B, true>(srow, sr, mid) && ok;
+    double* xm = mid + 2 * B * B + 2 * B;
+    const int lane = threadIdx.x & 31;
+    if (lane < B) {
+#pragma unroll
+        for (int jj = 0; jj < B; ++jj) Sinv[lane * B + jj] = srow[jj];
+        xm[lane] = sr;
+        Y[T.m + lane] = sr;
+    }
+    __syncwarp();
+    const double* st = stage;
+    twist_backward<B>(T, D, Lrow, Y, xm, ring, [&](int i, int o) { return st[i * B + o]; });
+    return __all_sync(FULL, ok);
+}
+
+// Solve with a stored twisted factor (rebuild's homogeneous RHS, MPM-2P's
+// particular RHS): forward sweeps, x_mid = S^-1 r_mid, back substitution.
+template <int B>
+__device__ void twisted_sweep(int n, const double* D, const double* Lcol, const double* Lrow, const double* MidB,
+                              const double* Sinv, double* Y, double* sm) {
+    constexpr int XB = xchg_doubles<B, 1>();
+    constexpr int RG = twist_ring<B>();
+    const Twist<B> T(n);
+    double* ring = sm + 2 * B * B + 2 * XB + T.h * RG * B * B;
+    double* mid = sm + 2 * B * B + 2 * XB + 2 * RG * B * B;
+    double yv;
+    twist_forward<B>(T, Lcol, Y, ring, yv);
+    double* rhs = mid + 2 * B * B;  // [2][B]
+    double* xm = rhs + 2 * B;
+    if (T.act) rhs[T.h * B + T.ll] = yv;
+    __syncwarp();
+    const int lane = threadIdx.x & 31;
+    if (lane < B) {
+        double x = 0.0;
+#pragma unroll
+        for (int jj = 0; jj < B; ++jj) x = fma(Sinv[lane * B + jj], rhs[jj] + rhs[B + B - 1 - jj] - Y[T.m + jj], x);
+        xm[lane] = x;
+    }
+    __syncwarp();
+    if (lane < B) Y[T.m + lane] = xm[lane];
+    const double* mids = T.h ? MidB : Lrow + (size_t)T.m * B;
+    twist_backward<B>(T, D, Lrow, Y, xm, ring, [&](int i, int o) { return mids[i * B + o]; });
 }
 
 }  // namespace mpm2p

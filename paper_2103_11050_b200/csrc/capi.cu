@@ -330,7 +330,13 @@ void create_ctx(mpm2p_ctx* ctx, const mpm2p_problem* P) {
     c.Dd.alloc(ns * ncs);
     c.Lrd.alloc(ns * ncs * B);
     c.Xd.alloc(ns * ncs);
-    c.Yv.alloc(ns * ncs);
+    // two-sided band solves: even widths <= 16 with at least 3 rows of cells
+    c.twist_store = !c.no_regband && !c.no_twist && L.sny >= 3 && L.snx <= 16 && L.snx % 2 == 0 && L.snx != 2 &&
+                    L.snx != 6 && L.snx != 14;
+    if (c.twist_store) {
+        c.tw_midb.alloc(ns * B * B);
+        c.tw_sinv.alloc(ns * B * B);
+    }
     c.sc.alloc(1);
     c.red.alloc(8 * 4 * (size_t)c.num_sms + 4096);
     c.red_count.alloc(1);

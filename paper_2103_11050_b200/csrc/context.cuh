@@ -101,7 +101,7 @@ struct Ctx {
     // per-solve scratch
     DevBuf<double> X, PU, PB, PS, GZ, WU, RU, RS, skel, resid, delta, corr;
     // downscale
-    DevBuf<double> BDd, BWd, BSd, Dd, Lrd, Xd, Yv;  // Yv: two-sided solve's bottom-half RHS
+    DevBuf<double> BDd, BWd, BSd, Dd, Lrd, Xd;
     // scalars and reduction workspace
     DevBuf<Scalars> sc;
     DevBuf<double> red;
@@ -112,7 +112,9 @@ struct Ctx {
     // per-run CUDA graphs of one driver step (MPM-2P reuse / MRCM rebuild)
     bool use_graphs = true;
     bool no_regband = false;  // MPM2P_NO_REGBAND=1: generic shared-memory band kernels only
-    bool no_twist = false;    // MPM2P_NO_TWIST=1: one-sided register-window downscale solve
+    bool no_twist = false;    // MPM2P_NO_TWIST=1: one-sided register-window band solves
+    bool twist_store = false; // rebuild factor stored in the two-sided layout (band_twist.cuh)
+    DevBuf<double> tw_midb, tw_sinv;  // per subdomain: bottom middle multipliers, middle S^-1 (B x B)
     // one graph per (branch, saturation-buffer parity): the upwind ping-pong
     // swaps s/s2 instead of copying, so the captured pointers alternate
     cudaGraphExec_t g_mpm[2] = {}, g_rebuild[2] = {};

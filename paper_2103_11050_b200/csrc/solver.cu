@@ -871,11 +871,11 @@ __global__ void __launch_bounds__(WPB * 32) k_hom_solve_r(Layout L, int max_rhs,
 
 // Downscale solve with the two-sided elimination (band_twist.cuh): the two
 // half-warps factor from both ends, so the dependent chain is ~half as long.
-constexpr int WPBT = 2;  // warps per block (shared memory: ~18 KB per warp at B = 16)
+constexpr int WPBT = 1;  // warps per block (shared memory: ~25 KB per warp at B = 16)
 template <int B>
 __global__ void __launch_bounds__(WPBT * 32) k_ds_solve_t(Layout L, const double* __restrict__ BD,
                                                           const double* __restrict__ BW, const double* __restrict__ BS,
-                                                          double* D, double* Lr, double* Xd, double* Yv,
+                                                          double* D, double* Lr, double* Xd,
                                                           const double* __restrict__ RS, double* p, Scalars* sc) {
     __shared__ __align__(16) double sm[WPBT][twist_smem_doubles<B>()];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -885,7 +885,7 @@ __global__ void __launch_bounds__(WPBT * 32) k_ds_solve_t(Layout L, const double
     const size_t so = (size_t)s * n;
     const BandRows A{BD + so, BW + so, BS + so};
     double* x = Xd + so;
-    const bool ok = twisted_solve<B>(n, A, D + so, Lr + so * B, x, Yv + so, sm[w]);
+    const bool ok = twisted_solve<B>(n, A, D + so, Lr + so * B, x, sm[w]);
     if (!ok && lane == 0) atomicOr(&sc->err, ERR_PIVOT);
     __syncwarp();
     // mean shift (mrcm.cpp:430-437): all loads of x first, then the scatter
@@ -919,6 +919,76 @@ __global__ void __launch_bounds__(WPBT * 32) k_ds_solve_t(Layout L, const double
     }
 }
 #define MPM2P_TWIST_WIDTHS(X) X(4) X(8) X(10) X(12) X(16)
+
+// Rebuild with the two-sided scheme: the factor (twisted layout + the middle
+// block's S^-1 and bottom multipliers) and the particular solve...
+template <int B>
+__global__ void __launch_bounds__(WPBT * 32) k_factor1_t(Layout L, int max_rhs, const double* __restrict__ BD,
+                                                         const double* __restrict__ BW, const double* __restrict__ BS,
+                                                         double* D, double* Lc, double* Lr, double* MidB, double* Sinv,
+                                                         double* X, Scalars* sc) {
+    __shared__ __align__(16) double sm[WPBT][twist_smem_doubles<B>()];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int s = blockIdx.x * WPBT + w;
+    if (s >= L.n_sub) return;
+    const int n = L.ncs;
+    const size_t so = (size_t)s * n;
+    const BandRows A{BD + so, BW + so, BS + so};
+    const bool ok = twisted_factor<B>(n, A, D + so, Lc + so * B, Lr + so * B, MidB + (size_t)s * B * B,
+                                      Sinv + (size_t)s * B * B, X + xoff(L, max_rhs, s, 0), sm[w]);
+    if (!ok && lane == 0) atomicOr(&sc->err, ERR_PIVOT);
+}
+
+// ... then one warp per (subdomain, homogeneous function) with the stored factor.
+template <int B>
+__global__ void __launch_bounds__(WPBT * 32) k_hom_solve_t(Layout L, int max_rhs, const double* __restrict__ D,
+                                                           const double* __restrict__ Lc,
+                                                           const double* __restrict__ Lr,
+                                                           const double* __restrict__ MidB,
+                                                           const double* __restrict__ Sinv, double* X) {
+    __shared__ __align__(16) double sm[WPBT][twist_smem_doubles<B>()];
+    const int w = threadIdx.x >> 5;
+    const int gw = blockIdx.x * WPBT + w;
+    const int s = gw / L.max_hom, h = gw % L.max_hom;
+    if (s >= L.n_sub || h >= L.n_hom(s)) return;
+    const int n = L.ncs;
+    const size_t so = (size_t)s * n;
+    twisted_sweep<B>(n, D + so, Lc + so * B, Lr + so * B, MidB + (size_t)s * B * B, Sinv + (size_t)s * B * B,
+                     X + xoff(L, max_rhs, s, 1 + h), sm[w]);
+}
+
+// MPM-2P particular solve with the stored two-sided factor + traces + psum.
+template <int B>
+__global__ void __launch_bounds__(WPBT * 32) k_part_solve_t(Layout L, int max_rhs, const double* __restrict__ D,
+                                                            const double* __restrict__ Lc,
+                                                            const double* __restrict__ Lr,
+                                                            const double* __restrict__ MidB,
+                                                            const double* __restrict__ Sinv, double* X,
+                                                            const double* __restrict__ km,
+                                                            const int* __restrict__ bc_kind,
+                                                            const double* __restrict__ bm,
+                                                            const double* __restrict__ bp,
+                                                            const double* __restrict__ GZ, double* __restrict__ PU,
+                                                            double* __restrict__ PS) {
+    __shared__ __align__(16) double sm[WPBT][twist_smem_doubles<B>()];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int s = blockIdx.x * WPBT + w;
+    if (s >= L.n_sub) return;
+    const int n = L.ncs;
+    const size_t so = (size_t)s * n;
+    double* x = X + xoff(L, max_rhs, s, 0);
+    twisted_sweep<B>(n, D + so, Lc + so * B, Lr + so * B, MidB + (size_t)s * B * B, Sinv + (size_t)s * B * B, x,
+                     sm[w]);
+    __syncwarp();
+    for (int idx = lane; idx < L.nbe; idx += 32) {
+        const EdgeInfo e = L.edge(s, idx);
+        PU[(size_t)s * L.nbe + idx] = part_trace(L, s, idx, x[e.local_cell], km, bc_kind, bm, bp, GZ);
+    }
+    double v = 0.0;
+    for (int r = lane; r < n; r += 32) v += x[r];
+    v = warp_sum(v);
+    if (lane == 0) PS[s] = v;
+}
 
 // Subdomain widths with a register-window instantiation; others use band.cuh.
 #define MPM2P_BAND_WIDTHS(X) X(4) X(8) X(10) X(12) X(16) X(20) X(24) X(32)
@@ -1280,7 +1350,7 @@ void downscale(Ctx& c, const double* kappa) {
 #define X(BW_)                                                                                                  \
     case BW_:                                                                                                   \
         k_ds_solve_t<BW_><<<cdiv(L.n_sub, WPBT), WPBT * 32, 0, c.st>>>(L, c.BDd, c.BWd, c.BSd, c.Dd, c.Lrd, c.Xd, \
-                                                                       c.Yv, c.RS, c.p, c.sc);                  \
+                                                                       c.RS, c.p, c.sc);                        \
         done = true;                                                                                            \
         break;
             MPM2P_TWIST_WIDTHS(X)
@@ -1366,7 +1436,39 @@ void launch_rebuild(Ctx& c, const double* kappa, bool compute_beta) {  // comput
         CK_LAUNCH();
     }
     const size_t smr = (size_t)WPB * band_smem_doubles(L.snx, RING_NR) * sizeof(double);
-    {
+    if (c.twist_store) {  // two-sided factor (band_twist.cuh)
+        {
+            PROF(c, "k_factor_solve");
+            switch (L.snx) {
+#define X(BW_)                                                                                                  \
+    case BW_:                                                                                                   \
+        k_factor1_t<BW_><<<cdiv(L.n_sub, WPBT), WPBT * 32, 0, c.st>>>(L, c.max_rhs, c.BDm, c.BWm, c.BSm, c.Dm,   \
+                                                                      c.Lcm, c.Lrm, c.tw_midb, c.tw_sinv, c.X, \
+                                                                      c.sc);                                   \
+        break;
+                MPM2P_TWIST_WIDTHS(X)
+#undef X
+                default:
+                    throw ConfigError("two-sided factor: unsupported subdomain width");
+            }
+            CK_LAUNCH();
+        }
+        if (L.max_hom > 0) {
+            PROF(c, "k_hom_solve");
+            switch (L.snx) {
+#define X(BW_)                                                                                                  \
+    case BW_:                                                                                                   \
+        k_hom_solve_t<BW_><<<cdiv((long long)L.n_sub * L.max_hom, WPBT), WPBT * 32, 0, c.st>>>(                 \
+            L, c.max_rhs, c.Dm, c.Lcm, c.Lrm, c.tw_midb, c.tw_sinv, c.X);                                       \
+        break;
+                MPM2P_TWIST_WIDTHS(X)
+#undef X
+                default:
+                    break;
+            }
+            CK_LAUNCH();
+        }
+    } else {
         PROF(c, "k_factor_solve");
         switch (c.no_regband ? -1 : L.snx) {
 #define X(BW_)                                                                                                      \
@@ -1464,7 +1566,23 @@ void launch_mpm(Ctx& c, const double* kn) {  // mpm_pressure_update (mpm.cpp:31-
     }
     const size_t sm1 = (size_t)WPB * band_smem_doubles(L.snx, 1) * sizeof(double);
     bool fused_traces = false;  // the register-window kernel also writes PU / PS
-    {
+    if (c.twist_store) {
+        PROF(c, "k_part_solve");
+        switch (L.snx) {
+#define X(BW_)                                                                                                  \
+    case BW_:                                                                                                   \
+        k_part_solve_t<BW_><<<cdiv(L.n_sub, WPBT), WPBT * 32, 0, c.st>>>(                                       \
+            L, c.max_rhs, c.Dm, c.Lcm, c.Lrm, c.tw_midb, c.tw_sinv, c.X, c.kappa_m, c.bc_kind, c.beta_m,        \
+            c.beta_p, c.GZ, c.PU, c.PS);                                                                        \
+        break;
+            MPM2P_TWIST_WIDTHS(X)
+#undef X
+            default:
+                throw ConfigError("two-sided factor: unsupported subdomain width");
+        }
+        fused_traces = true;
+        CK_LAUNCH();
+    } else {
         PROF(c, "k_part_solve");
         switch (c.no_regband ? -1 : L.snx) {
 #define X(BW_)                                                                                                  \
