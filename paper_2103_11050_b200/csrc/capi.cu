@@ -254,6 +254,7 @@ void create_ctx(mpm2p_ctx* ctx, const mpm2p_problem* P) {
     if (const char* e = std::getenv("MPM2P_NO_REGBAND")) c.no_regband = e[0] == '1';
     if (const char* e = std::getenv("MPM2P_GJ")) c.gj_legacy = std::strcmp(e, "legacy") == 0;
     if (const char* e = std::getenv("MPM2P_NO_TWIST")) c.no_twist = e[0] == '1';
+    if (const char* e = std::getenv("MPM2P_PDL")) c.pdl = e[0] == '1';
     c.use_krylov = c.dim > DENSE_IFACE_MAX;
     if (const char* e = std::getenv("MPM2P_IFACE")) {
         if (std::strcmp(e, "krylov") == 0) c.use_krylov = c.dim > 0;

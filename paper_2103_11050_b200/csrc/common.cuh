@@ -67,6 +67,22 @@ __device__ __forceinline__ double warp_min(double v) {
     return v;
 }
 
+// ---- Programmatic dependent launch (griddepcontrol, sm_90+) ----------------
+// Every kernel starts with pdl_begin(): it waits until the previous kernel in
+// the stream has completed and its writes are visible (a no-op when the
+// launch carried no programmatic dependency), then lets the next kernel be
+// scheduled. Kernels are launched with programmatic stream serialisation
+// (launch_k), so the next kernel's launch and block scheduling overlap this
+// kernel's execution instead of following its completion.
+__device__ __forceinline__ void pdl_begin() {
+#ifdef MPM2P_PDL_EARLY_TRIGGER
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#else
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // dependents are released as this grid's blocks exit
+#endif
+}
+
 // ---- TMA bulk copies (cp.async.bulk, SASS UBLKCP) completing on an mbarrier
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {

@@ -111,6 +111,7 @@ struct Ctx {
     int iface_sym = -1;  // J*M symmetric (pivot-free inverse)? -1 unknown
     // per-run CUDA graphs of one driver step (MPM-2P reuse / MRCM rebuild)
     bool use_graphs = true;
+    bool pdl = false;  // programmatic dependent launch between kernels (MPM2P_PDL=1; measured neutral on C2)
     bool no_regband = false;  // MPM2P_NO_REGBAND=1: generic shared-memory band kernels only
     bool no_twist = false;    // MPM2P_NO_TWIST=1: one-sided register-window band solves
     bool twist_store = false; // rebuild factor stored in the two-sided layout (band_twist.cuh)
@@ -178,6 +179,25 @@ struct Ctx {
         pending.clear();
     }
 };
+
+// Kernel launch on the context's stream with programmatic stream
+// serialisation when enabled (every kernel begins with pdl_begin()).
+// MPM2P_PDL=1 turns it on; on C2 it measured neutral (launch gaps are not
+// the bottleneck), so it is off by default.
+template <typename... KArgs, typename... Args>
+inline void launch_k(const Ctx& c, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c.st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = c.pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
+}
 
 // RAII scope recording CUDA events around one kernel launch when profiling.
 struct ProfScope {

@@ -46,6 +46,7 @@ struct GJArgs {
 };
 
 __global__ void __launch_bounds__(GJ_THREADS) k_gauss_jordan(GJArgs a) {
+    pdl_begin();
     cg::grid_group grid = cg::this_grid();
     extern __shared__ double sp[];  // panel n x b, row-major
     __shared__ double prow[16];
@@ -226,6 +227,7 @@ struct BGJArgs {
 constexpr int GJB = 32;  // diagonal block width
 
 __global__ void __launch_bounds__(256) k_block_gj(BGJArgs a) {
+    pdl_begin();
     cg::grid_group grid = cg::this_grid();
     extern __shared__ double dsm[];
     double (*P)[GJB + 1] = reinterpret_cast<double (*)[GJB + 1]>(dsm);  // 32 x 33
@@ -443,6 +445,7 @@ constexpr int PPW = 128;  // columns per work item (4 blocks)
 constexpr size_t PP_SMEM = (4 * PPB * (PPB + 1) + PPB * PPW + 2 * PPB + 4 * 2 * 8) * sizeof(double);
 
 __global__ void __launch_bounds__(256, 2) k_gj_pp(PPArgs a) {
+    pdl_begin();
     cg::grid_group grid = cg::this_grid();
     extern __shared__ double pp_sm[];
     PPTile& Ps = *reinterpret_cast<PPTile*>(pp_sm);
@@ -587,6 +590,7 @@ __global__ void __launch_bounds__(256, 2) k_gj_pp(PPArgs a) {
 // transposed-position table (the pattern is structurally symmetric).
 __global__ void k_build_k(const int* __restrict__ ptr, const int* __restrict__ col, const double* __restrict__ val,
                           int n, double* __restrict__ W, int ld) {
+    pdl_begin();
     const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (r >= ld) return;
     double* row = W + (size_t)r * ld;
@@ -604,6 +608,7 @@ __global__ void k_build_k(const int* __restrict__ ptr, const int* __restrict__ c
 // sum over the slab's 64 rows of |Minv[i][j]| (fixed order), part[slab][j] = 0
 // (the A half is filled by k_mnorm). Block: 32 columns x 8 row groups.
 __global__ void k_kinv_out(const double* __restrict__ Kinv, int ld, int n, double* __restrict__ Minv, double* part) {
+    pdl_begin();
     __shared__ double red[8][33];
     const int c = threadIdx.x & 31, rg = threadIdx.x >> 5;
     const int j = blockIdx.x * 32 + c, slab = blockIdx.y;
@@ -634,6 +639,7 @@ __global__ void k_kinv_out(const double* __restrict__ Kinv, int ld, int n, doubl
 // pattern of row j (symmetric pattern), found at tpos[z] (z in row j).
 __global__ void k_mnorm(const int* __restrict__ ptr, const int* __restrict__ tpos, const double* __restrict__ val,
                         int n, double* part) {
+    pdl_begin();
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n) return;
     double s = 0.0;
@@ -643,6 +649,7 @@ __global__ void k_mnorm(const int* __restrict__ ptr, const int* __restrict__ tpo
 
 // npad x npad copy with identity padding (and back).
 __global__ void k_pad_in(const double* __restrict__ A, int n, double* __restrict__ W, int ld) {
+    pdl_begin();
     for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < (long long)ld * ld;
          x += (long long)gridDim.x * blockDim.x) {
         const int i = (int)(x / ld), j = (int)(x % ld);
@@ -650,6 +657,7 @@ __global__ void k_pad_in(const double* __restrict__ A, int n, double* __restrict
     }
 }
 __global__ void k_pad_out(const double* __restrict__ W, int ld, double* __restrict__ A, int n) {
+    pdl_begin();
     for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < (long long)n * n;
          x += (long long)gridDim.x * blockDim.x) {
         const int i = (int)(x / n), j = (int)(x % n);
@@ -660,6 +668,7 @@ __global__ void k_pad_out(const double* __restrict__ W, int ld, double* __restri
 
 // K = J M: phi-rows first, then the negated psi-rows.
 __global__ void k_j_times(const double* __restrict__ M, double* __restrict__ K, int n) {
+    pdl_begin();
     const int h = n / 2;
     for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < (long long)n * n;
          x += (long long)gridDim.x * blockDim.x) {
@@ -670,6 +679,7 @@ __global__ void k_j_times(const double* __restrict__ M, double* __restrict__ K, 
 
 // M^-1 = K^-1 J: columns permuted and the psi half negated.
 __global__ void k_times_j(const double* __restrict__ Kinv, double* __restrict__ Minv, int n) {
+    pdl_begin();
     const int h = n / 2;
     for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < (long long)n * n;
          x += (long long)gridDim.x * blockDim.x) {
@@ -680,6 +690,7 @@ __global__ void k_times_j(const double* __restrict__ Kinv, double* __restrict__ 
 
 // max |A_ij - A_ji| and max |A_ij| (symmetry check of J M, once per context).
 __global__ void k_asym(const double* __restrict__ A, int n, double* out) {
+    pdl_begin();
     __shared__ double sh[32];
     double d = 0.0, m = 0.0;
     for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < (long long)n * n;
@@ -698,6 +709,7 @@ __global__ void k_asym(const double* __restrict__ A, int n, double* out) {
 }
 
 __global__ void k_augment(const double* __restrict__ A, double* __restrict__ W, int n) {
+    pdl_begin();
     const long long tot = 2LL * n * n;
     for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < tot; x += (long long)gridDim.x * blockDim.x) {
         const int i = (int)(x / (2 * n)), j = (int)(x % (2 * n));
@@ -706,6 +718,7 @@ __global__ void k_augment(const double* __restrict__ A, double* __restrict__ W, 
 }
 
 __global__ void k_extract(const double* __restrict__ W, double* __restrict__ Ainv, int n) {
+    pdl_begin();
     const long long tot = (long long)n * n;
     for (long long x = (long long)blockIdx.x * blockDim.x + threadIdx.x; x < tot; x += (long long)gridDim.x * blockDim.x) {
         const int i = (int)(x / n), j = (int)(x % n);
@@ -716,6 +729,7 @@ __global__ void k_extract(const double* __restrict__ W, double* __restrict__ Ain
 // Column 1-norms of A and B: partial column sums over row blocks of 64
 // (grid y), coalesced along rows...
 __global__ void k_colsum(const double* __restrict__ A, const double* __restrict__ B, int n, double* part) {
+    pdl_begin();
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n) return;
     const int i0 = blockIdx.y * 64, i1 = min(n, i0 + 64);
@@ -731,6 +745,7 @@ __global__ void k_colsum(const double* __restrict__ A, const double* __restrict_
 // ...then one block forms rcond = 1/(||A||_1 ||B||_1) and applies the guard.
 __global__ void k_rcond(const double* __restrict__ part, int n, int nrb, const int* singular, double* rcond_out,
                         unsigned* err, unsigned err_bit, double threshold) {
+    pdl_begin();
     __shared__ double sa[32], sb[32];
     double ma = 0.0, mb = 0.0;
     for (int j = threadIdx.x; j < n; j += blockDim.x) {
@@ -767,6 +782,7 @@ __global__ void k_rcond(const double* __restrict__ part, int n, int nrb, const i
 template <bool ACC>
 __global__ void __launch_bounds__(256) k_gemv_w(const double* __restrict__ A, const double* __restrict__ x,
                                                 double* __restrict__ y, int n) {
+    pdl_begin();
     const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (row >= n) return;
     const double* a = A + (size_t)row * n;
@@ -804,6 +820,7 @@ constexpr int GEMV_TMA_MAX = 2816;  // 9 n doubles of dynamic shared memory <= 1
 template <bool ACC>
 __global__ void __launch_bounds__(256) k_gemv_tma(const double* __restrict__ A, const double* __restrict__ x,
                                                   double* __restrict__ y, int n) {
+    pdl_begin();
     extern __shared__ __align__(128) double gsm[];
     __shared__ __align__(8) unsigned long long bar;
     const int r0 = blockIdx.x * 8, nr = min(8, n - r0);
@@ -835,6 +852,7 @@ __global__ void __launch_bounds__(256) k_gemv_tma(const double* __restrict__ A, 
 // r = b - M x with M in CSR, one thread per row.
 __global__ void k_csr_residual(const int* __restrict__ ptr, const int* __restrict__ col, const double* __restrict__ val,
                                const double* __restrict__ x, const double* __restrict__ b, double* __restrict__ r, int n) {
+    pdl_begin();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     double acc = 0.0;
@@ -843,6 +861,7 @@ __global__ void k_csr_residual(const int* __restrict__ ptr, const int* __restric
 }
 
 __global__ void k_axpy(double* __restrict__ y, const double* __restrict__ x, int n) {
+    pdl_begin();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) y[i] += x[i];
 }
@@ -869,13 +888,13 @@ void block_gj_inplace(Ctx& c, double* W, int n) {
     const int g = std::min(cdiv((long long)ld * ld, TPB), 8 * c.num_sms);
     {
         PROF(c, "k_pad_in");
-        k_pad_in<<<g, TPB, 0, c.st>>>(W, n, W0, ld);
+        launch_k(c, k_pad_in, g, TPB, 0, W, n, W0, ld);
         CK_LAUNCH();
     }
     gj_pp_run(c, W0, W1, nb, ld, n);
     {
         PROF(c, "k_pad_out");
-        k_pad_out<<<g, TPB, 0, c.st>>>((nb & 1) ? W1 : W0, ld, W, n);
+        launch_k(c, k_pad_out, g, TPB, 0, (nb & 1) ? W1 : W0, ld, W, n);
         CK_LAUNCH();
     }
 }
@@ -950,12 +969,12 @@ void launch_rcond(Ctx& c, const double* A, const double* Ainv, int n, double* rc
     const int nrb = cdiv(n, 64);
     {
         PROF(c, "k_colsum");
-        k_colsum<<<dim3(cdiv(n, TPB), nrb), TPB, 0, c.st>>>(A, Ainv, n, c.gj_work.p);
+        launch_k(c, k_colsum, dim3(cdiv(n, TPB), nrb), TPB, 0, A, Ainv, n, c.gj_work.p);
         CK_LAUNCH();
     }
     {
         PROF(c, "k_rcond");
-        k_rcond<<<1, 1024, 0, c.st>>>(c.gj_work.p, n, nrb, c.gj_piv.p + n, rcond_dev, &c.sc.p->err, err_bit,
+        launch_k(c, k_rcond, 1, 1024, 0, c.gj_work.p, n, nrb, c.gj_piv.p + n, rcond_dev, &c.sc.p->err, err_bit,
                                       threshold);
         CK_LAUNCH();
     }
@@ -1007,7 +1026,7 @@ bool interface_inverse_csr(Ctx& c, double* rcond_dev, unsigned err_bit, double t
     double* W1 = W0 + (size_t)ld * ld;
     {
         PROF(c, "k_build_k");
-        k_build_k<<<cdiv((long long)ld * 32, TPB), TPB, 0, c.st>>>(c.csr_ptr, c.csr_col, c.csr_val, n, W0, ld);
+        launch_k(c, k_build_k, cdiv((long long)ld * 32, TPB), TPB, 0, c.csr_ptr, c.csr_col, c.csr_val, n, W0, ld);
         CK_LAUNCH();
     }
     gj_pp_run(c, W0, W1, nb, ld, n);
@@ -1015,17 +1034,17 @@ bool interface_inverse_csr(Ctx& c, double* rcond_dev, unsigned err_bit, double t
     c.gj_work.alloc(std::max(c.gj_work.n, (size_t)2 * n * nrb));
     {
         PROF(c, "k_kinv_out");
-        k_kinv_out<<<dim3(cdiv(n, 32), nrb), 256, 0, c.st>>>((nb & 1) ? W1 : W0, ld, n, c.Minv, c.gj_work.p);
+        launch_k(c, k_kinv_out, dim3(cdiv(n, 32), nrb), 256, 0, (nb & 1) ? W1 : W0, ld, n, c.Minv, c.gj_work.p);
         CK_LAUNCH();
     }
     {
         PROF(c, "k_mnorm");
-        k_mnorm<<<cdiv(n, TPB), TPB, 0, c.st>>>(c.csr_ptr, c.csr_tpos, c.csr_val, n, c.gj_work.p);
+        launch_k(c, k_mnorm, cdiv(n, TPB), TPB, 0, c.csr_ptr, c.csr_tpos, c.csr_val, n, c.gj_work.p);
         CK_LAUNCH();
     }
     {
         PROF(c, "k_rcond");
-        k_rcond<<<1, 1024, 0, c.st>>>(c.gj_work.p, n, nrb, c.gj_piv.p + n, rcond_dev, &c.sc.p->err, err_bit,
+        launch_k(c, k_rcond, 1, 1024, 0, c.gj_work.p, n, nrb, c.gj_piv.p + n, rcond_dev, &c.sc.p->err, err_bit,
                                       threshold);
         CK_LAUNCH();
     }
@@ -1042,14 +1061,14 @@ void interface_inverse_async(Ctx& c, const double* M, double* Minv, int n, doubl
     c.gj_piv.alloc(std::max(c.gj_piv.n, (size_t)n + 1));
     {
         PROF(c, "k_j_times");
-        k_j_times<<<std::min(cdiv((long long)n * n, TPB), 8 * c.num_sms), TPB, 0, c.st>>>(M, c.gj_work, n);
+        launch_k(c, k_j_times, std::min(cdiv((long long)n * n, TPB), 8 * c.num_sms), TPB, 0, M, c.gj_work, n);
         CK_LAUNCH();
     }
     if (c.iface_sym < 0) {
         const int g = std::min(cdiv((long long)n * n, TPB), 2 * c.num_sms);
         DevBuf<double> part;
         part.alloc(2 * g);
-        k_asym<<<g, TPB, 0, c.st>>>(c.gj_work, n, part);
+        launch_k(c, k_asym, g, TPB, 0, c.gj_work, n, part);
         CK_LAUNCH();
         std::vector<double> h(2 * g);
         CK(cudaMemcpyAsync(h.data(), part.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost, c.st));
@@ -1065,7 +1084,7 @@ void interface_inverse_async(Ctx& c, const double* M, double* Minv, int n, doubl
         block_gj_inplace(c, c.gj_work, n);
         {
             PROF(c, "k_times_j");
-            k_times_j<<<std::min(cdiv((long long)n * n, TPB), 8 * c.num_sms), TPB, 0, c.st>>>(c.gj_work, Minv, n);
+            launch_k(c, k_times_j, std::min(cdiv((long long)n * n, TPB), 8 * c.num_sms), TPB, 0, c.gj_work, Minv, n);
             CK_LAUNCH();
         }
         launch_rcond(c, M, Minv, n, rcond_dev, err_bit, threshold);
@@ -1106,7 +1125,7 @@ void dense_inverse_async(Ctx& c, const double* A, double* Ainv, int n, double* r
     c.gj_piv.alloc(std::max(c.gj_piv.n, (size_t)n + 1));    // swaps + singular flag
     {
         PROF(c, "k_augment");
-        k_augment<<<std::min(cdiv(2LL * n * n, TPB), 8 * c.num_sms), TPB, 0, c.st>>>(A, c.gj_work, n);
+        launch_k(c, k_augment, std::min(cdiv(2LL * n * n, TPB), 8 * c.num_sms), TPB, 0, A, c.gj_work, n);
         CK_LAUNCH();
     }
     CK(cudaMemsetAsync(c.gj_piv.p + n, 0, sizeof(int), c.st));
@@ -1123,18 +1142,18 @@ void dense_inverse_async(Ctx& c, const double* A, double* Ainv, int n, double* r
     }
     {
         PROF(c, "k_extract");
-        k_extract<<<std::min(cdiv((long long)n * n, TPB), 8 * c.num_sms), TPB, 0, c.st>>>(c.gj_work, Ainv, n);
+        launch_k(c, k_extract, std::min(cdiv((long long)n * n, TPB), 8 * c.num_sms), TPB, 0, c.gj_work, Ainv, n);
         CK_LAUNCH();
     }
     const int nrb = cdiv(n, 64);
     {
         PROF(c, "k_colsum");
-        k_colsum<<<dim3(cdiv(n, TPB), nrb), TPB, 0, c.st>>>(A, Ainv, n, c.gj_work.p);  // W is free now
+        launch_k(c, k_colsum, dim3(cdiv(n, TPB), nrb), TPB, 0, A, Ainv, n, c.gj_work.p);  // W is free now
         CK_LAUNCH();
     }
     {
         PROF(c, "k_rcond");
-        k_rcond<<<1, 1024, 0, c.st>>>(c.gj_work.p, n, nrb, c.gj_piv.p + n, rcond_dev, &c.sc.p->err, err_bit,
+        launch_k(c, k_rcond, 1, 1024, 0, c.gj_work.p, n, nrb, c.gj_piv.p + n, rcond_dev, &c.sc.p->err, err_bit,
                                       threshold);
         CK_LAUNCH();
     }
@@ -1161,9 +1180,9 @@ void gemv_dispatch(Ctx& c, const double* A, const double* x, double* y, int n) {
                                     9 * GEMV_TMA_MAX * (int)sizeof(double)));
             attr = true;
         }
-        k_gemv_tma<ACC><<<cdiv(n, 8), 256, (size_t)9 * n * sizeof(double), c.st>>>(A, x, y, n);
+        launch_k(c, k_gemv_tma<ACC>, cdiv(n, 8), 256, (size_t)9 * n * sizeof(double), A, x, y, n);
     } else {
-        k_gemv_w<ACC><<<cdiv(n, 8), 256, 0, c.st>>>(A, x, y, n);
+        launch_k(c, k_gemv_w<ACC>, cdiv(n, 8), 256, 0, A, x, y, n);
     }
     CK_LAUNCH();
 }
@@ -1176,13 +1195,13 @@ void launch_gemv_acc(Ctx& c, const double* A, const double* x, double* y, int n)
 void launch_csr_residual(Ctx& c, const int* ptr, const int* col, const double* val, const double* x, const double* b,
                          double* r, int n) {
     PROF(c, "k_csr_residual");
-    k_csr_residual<<<cdiv(n, TPB), TPB, 0, c.st>>>(ptr, col, val, x, b, r, n);
+    launch_k(c, k_csr_residual, cdiv(n, TPB), TPB, 0, ptr, col, val, x, b, r, n);
     CK_LAUNCH();
 }
 
 void launch_axpy(Ctx& c, double* y, const double* x, int n) {
     PROF(c, "k_axpy");
-    k_axpy<<<cdiv(n, TPB), TPB, 0, c.st>>>(y, x, n);
+    launch_k(c, k_axpy, cdiv(n, TPB), TPB, 0, y, x, n);
     CK_LAUNCH();
 }
 

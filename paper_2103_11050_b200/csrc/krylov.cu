@@ -64,6 +64,7 @@ __device__ __forceinline__ double all_sum(const double* part, int nb, double* sh
 }
 
 __global__ void __launch_bounds__(KTPB) k_minres(MinresArgs a) {
+    pdl_begin();
     cg::grid_group grid = cg::this_grid();
     __shared__ double sh[32];
     const int n = a.n;
@@ -159,6 +160,7 @@ __global__ void __launch_bounds__(KTPB) k_minres(MinresArgs a) {
 // K = J M in CSR: K row r is M row (r < h ? h + r : r - h), negated for r >= h.
 __global__ void k_fill_k(const int* __restrict__ mptr, const double* __restrict__ mval,
                          const int* __restrict__ kptr, double* __restrict__ kval, int n) {
+    pdl_begin();
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n) return;
     const int h = n / 2;
@@ -171,6 +173,7 @@ __global__ void k_fill_k(const int* __restrict__ mptr, const double* __restrict_
 // Jacobi preconditioner 1/|K_rr| (K_rr = M_(src) diagonal entry of column r).
 __global__ void k_kdiag(const int* __restrict__ kptr, const int* __restrict__ kcol, const double* __restrict__ kval,
                         double* __restrict__ pinv, int n) {
+    pdl_begin();
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n) return;
     double d = 0.0;
@@ -181,6 +184,7 @@ __global__ void k_kdiag(const int* __restrict__ kptr, const int* __restrict__ kc
 
 // b_K = J b: phi-rows first, then the negated psi-rows.
 __global__ void k_jvec(const double* __restrict__ b, double* __restrict__ bk, int n) {
+    pdl_begin();
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n) return;
     const int h = n / 2;
@@ -215,12 +219,12 @@ void krylov_prepare(Ctx& c) {
     const int n = c.dim;
     {
         PROF(c, "k_fill_k");
-        k_fill_k<<<cdiv(n, KTPB), KTPB, 0, c.st>>>(c.csr_ptr, c.csr_val, c.k_ptr, c.k_val, n);
+        launch_k(c, k_fill_k, cdiv(n, KTPB), KTPB, 0, c.csr_ptr, c.csr_val, c.k_ptr, c.k_val, n);
         CK_LAUNCH();
     }
     {
         PROF(c, "k_kdiag");
-        k_kdiag<<<cdiv(n, KTPB), KTPB, 0, c.st>>>(c.k_ptr, c.k_col, c.k_val, c.kr_pinv, n);
+        launch_k(c, k_kdiag, cdiv(n, KTPB), KTPB, 0, c.k_ptr, c.k_col, c.k_val, c.kr_pinv, n);
         CK_LAUNCH();
     }
 }
@@ -237,7 +241,7 @@ void krylov_solve(Ctx& c, const double* rhs, double* x) {
     double* bk = wk + 9 * v;
     {
         PROF(c, "k_jvec");
-        k_jvec<<<cdiv(n, KTPB), KTPB, 0, c.st>>>(rhs, bk, n);
+        launch_k(c, k_jvec, cdiv(n, KTPB), KTPB, 0, rhs, bk, n);
         CK_LAUNCH();
     }
     MinresArgs a{c.k_ptr, c.k_col, c.k_val, c.kr_pinv, bk, x, wk, wk + v, wk + 2 * v, wk + 3 * v, wk + 4 * v,

@@ -61,6 +61,7 @@ __device__ __forceinline__ double edge_beta(const Layout& L, const EdgeInfo& e, 
 
 // ---------------------------------------------------------------- K12 ----
 __global__ void k_face_kappa(Layout L, const double* __restrict__ kappa, double* __restrict__ fk) {
+    pdl_begin();
     const int E = L.skeleton_edges();
     for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < E; x += gridDim.x * blockDim.x) {
         const int k = x < L.NV * L.sny ? x / L.sny : L.NV + (x - L.NV * L.sny) / L.snx;
@@ -84,6 +85,7 @@ __device__ double quantile_sorted(const double* v, int m, double pct) {  // robi
 __global__ void k_beta(Layout L, const double* __restrict__ kappa, const double* __restrict__ fk,
                        const double* __restrict__ sorted, int adaptive, double alpha, double amin, double amax,
                        double plo, double phi, double* bm, double* bp, double* al, Scalars* sc) {
+    pdl_begin();
     const int E = L.skeleton_edges();
     double qlo = 0.0, qhi = 0.0;
     if (adaptive && E > 0) {
@@ -110,7 +112,8 @@ __global__ void k_beta(Layout L, const double* __restrict__ kappa, const double*
 }
 
 // ---------------------------------------------------------- transmissibility
-__global__ void k_trans(Layout L, const double* __restrict__ kappa, double* __restrict__ T) {  // elliptic.cpp:44-61
+__global__ void k_trans(Layout L, const double* __restrict__ kappa, double* __restrict__ T) {
+    pdl_begin();  // elliptic.cpp:44-61
     const int F = L.faces();
     for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < F; f += gridDim.x * blockDim.x) {
         double t = 0.0;
@@ -142,6 +145,7 @@ __global__ void k_band_entries(Layout L, const double* __restrict__ kappa, const
                                int anchor, const double* __restrict__ bm, const double* __restrict__ bp,
                                const int* __restrict__ bc_kind, double* __restrict__ BD, double* __restrict__ BW,
                                double* __restrict__ BS, Scalars* sc) {
+    pdl_begin();
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= L.cells()) return;
     const int i = c % L.nx, j = c / L.nx;
@@ -189,6 +193,7 @@ __global__ void k_rebuild_rhs(Layout L, int max_rhs, const double* __restrict__ 
                               const int* __restrict__ bc_kind, const double* __restrict__ bc_value,
                               const double* __restrict__ bm, const double* __restrict__ bp, int anchor,
                               double* __restrict__ X) {
+    pdl_begin();
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= L.cells()) return;
     const int i = c % L.nx, j = c / L.nx;
@@ -230,6 +235,7 @@ __global__ void k_rebuild_rhs(Layout L, int max_rhs, const double* __restrict__ 
 __global__ void k_factor_solve(Layout L, int max_rhs, const double* __restrict__ BD, const double* __restrict__ BW,
                                const double* __restrict__ BS, double* __restrict__ D, double* __restrict__ Lc,
                                double* __restrict__ Lr, double* __restrict__ X, Scalars* sc) {
+    pdl_begin();
     extern __shared__ double smem[];
     const int w = threadIdx.x >> 5;
     const int s = blockIdx.x * WPB + w;
@@ -260,6 +266,7 @@ __global__ void k_rebuild_traces(Layout L, int max_rhs, const double* __restrict
                                  const double* __restrict__ bm, const double* __restrict__ bp,
                                  const double* __restrict__ X, double* __restrict__ PU, double* __restrict__ PB,
                                  double* __restrict__ HU, double* __restrict__ HB) {
+    pdl_begin();
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     if (x >= L.n_sub * L.nbe) return;
     const int s = x / L.nbe, idx = x % L.nbe;
@@ -311,6 +318,7 @@ __global__ void k_rebuild_traces(Layout L, int max_rhs, const double* __restrict
 // Per-(subdomain, solution) pressure sums, one warp each.
 __global__ void k_psums(Layout L, int max_rhs, const double* __restrict__ X, double* __restrict__ PS,
                         double* __restrict__ HP) {
+    pdl_begin();
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (gw >= L.n_sub * max_rhs) return;
     const int s = gw / max_rhs, m = gw % max_rhs;
@@ -349,6 +357,7 @@ __device__ __forceinline__ int hom_index(const Layout& L, int s, int col) {
 __global__ void k_assemble(Layout L, const int* __restrict__ rowv, const int* __restrict__ colv, int nnz,
                            const double* __restrict__ HU, const double* __restrict__ bm,
                            const double* __restrict__ bp, double* __restrict__ val) {
+    pdl_begin();
     const int z = blockIdx.x * blockDim.x + threadIdx.x;  // one thread per nonzero
     if (z >= nnz) return;
     const int row = rowv[z];
@@ -392,6 +401,7 @@ __global__ void k_assemble(Layout L, const int* __restrict__ rowv, const int* __
 
 __global__ void k_csr_to_dense(const int* __restrict__ ptr, const int* __restrict__ colv,
                                const double* __restrict__ val, int n, double* __restrict__ A) {
+    pdl_begin();
     const int row = blockIdx.x;
     for (int j = threadIdx.x; j < n; j += blockDim.x) A[(size_t)row * n + j] = 0.0;
     __syncthreads();
@@ -402,6 +412,7 @@ __global__ void k_csr_to_dense(const int* __restrict__ ptr, const int* __restric
 // Interface rhs from the particular traces (mrcm.cpp:80-100).
 __global__ void k_iface_rhs(Layout L, const double* __restrict__ PU, const double* __restrict__ bm,
                             const double* __restrict__ bp, double* __restrict__ rhs) {
+    pdl_begin();
     // one warp per row; lanes stride the (side, position) terms
     const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     const int np = L.dim_flux;
@@ -440,6 +451,7 @@ __global__ void k_recon_traces(Layout L, const double* __restrict__ coef, const 
                                const double* __restrict__ PB, const double* __restrict__ HU,
                                const double* __restrict__ HB, const double* __restrict__ WU,
                                double* __restrict__ RU, double* __restrict__ RB) {
+    pdl_begin();
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     if (x >= L.n_sub * L.nbe) return;
     const int s = x / L.nbe, idx = x % L.nbe;
@@ -468,6 +480,7 @@ __global__ void k_recon_mpm(Layout L, const double* __restrict__ coef, const dou
                             const double* __restrict__ HU, const double* __restrict__ WU, double* __restrict__ RU,
                             const double* __restrict__ PS, const double* __restrict__ HP,
                             const double* __restrict__ pmsum, double* __restrict__ RS) {
+    pdl_begin();
     constexpr int MAXH = 16;
     const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (s >= L.n_sub) return;
@@ -506,6 +519,7 @@ __global__ void k_recon_mpm(Layout L, const double* __restrict__ coef, const dou
 __global__ void k_recon_psum(Layout L, const double* __restrict__ coef, const double* __restrict__ PS,
                              const double* __restrict__ HP, const double* __restrict__ pmsum,
                              double* __restrict__ RS) {
+    pdl_begin();
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= L.n_sub) return;
     double v = PS[s];
@@ -524,6 +538,7 @@ __global__ void k_recon_psum(Layout L, const double* __restrict__ coef, const do
 // Full reconstructed pressure at a rebuild (recon_m.p, kept for MPM steps).
 __global__ void k_recon_p(Layout L, int max_rhs, const double* __restrict__ coef, const double* __restrict__ X,
                           double* __restrict__ pm) {
+    pdl_begin();
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= L.cells()) return;
     const int i = c % L.nx, j = c / L.nx;
@@ -542,6 +557,7 @@ __global__ void k_recon_p(Layout L, int max_rhs, const double* __restrict__ coef
 }
 
 __global__ void k_sub_sum(Layout L, const double* __restrict__ field, double* __restrict__ out) {
+    pdl_begin();
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (gw >= L.n_sub) return;
     double v = 0.0;
@@ -556,6 +572,7 @@ __global__ void k_sub_sum(Layout L, const double* __restrict__ field, double* __
 __global__ void k_resid(Layout L, const double* skel, const double* __restrict__ RU,
                         const double* __restrict__ qsum, double* __restrict__ resid, Scalars* sc, double* part,
                         unsigned* counter, int fuse_skel = 0) {
+    pdl_begin();
     // one warp per subdomain; lanes stride the boundary edges (W,E,S,N order)
     __shared__ double sh[32];
     const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
@@ -607,6 +624,7 @@ __device__ void repair_corr_last(const Layout& L, int grounded, const double* de
 __global__ void k_repair_delta(int n, const double* __restrict__ Linv, const double* __restrict__ resid,
                                double* delta, Layout L, int grounded, const double* __restrict__ ground,
                                double* __restrict__ corr, Scalars* sc, unsigned* counter) {
+    pdl_begin();
     __shared__ double sh[32];
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (gw < n) {
@@ -646,6 +664,7 @@ __device__ void repair_corr_last(const Layout& L, int grounded, const double* de
 __global__ void k_repair_corr(Layout L, int active, int grounded, const double* __restrict__ delta,
                               const double* __restrict__ ground, double* __restrict__ corr, Scalars* sc, double* part,
                               unsigned* counter) {
+    pdl_begin();
     __shared__ double sh[32];
     double m = 0.0;
     const int nthreads = L.n_iface > L.n_sub ? L.n_iface : L.n_sub;
@@ -680,6 +699,7 @@ __global__ void k_ds_prep(Layout L, const double* __restrict__ kappa, const doub
                           const double* __restrict__ RU, const double* __restrict__ delta, int grounded,
                           double* __restrict__ BD, double* __restrict__ BW, double* __restrict__ BS,
                           double* __restrict__ Xd, double* __restrict__ EU, Scalars* sc) {
+    pdl_begin();
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= L.cells()) return;
     const int i = c % L.nx, j = c / L.nx;
@@ -728,6 +748,7 @@ __global__ void k_ds_solve(Layout L, const double* __restrict__ BD, const double
                            const double* __restrict__ BS, double* __restrict__ D, double* __restrict__ Lr,
                            double* __restrict__ Xd, const double* __restrict__ RS, double* __restrict__ p,
                            Scalars* sc) {
+    pdl_begin();
     extern __shared__ double smem[];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int s = blockIdx.x * WPB + w;
@@ -755,6 +776,7 @@ __global__ void __launch_bounds__(WPB * 32) k_ds_solve_r(Layout L, const double*
                                                          double* D, double* Lr,
                                                          double* Xd, const double* __restrict__ RS,
                                                          double* p, Scalars* sc) {
+    pdl_begin();
     __shared__ double stage[WPB][B * B];
     __shared__ __align__(16) double xbuf[WPB][xchg_doubles<B, 1>()];
     __shared__ __align__(16) double ring[WPB][sweep_ring<B>() * B * B + 2];
@@ -806,6 +828,7 @@ __global__ void __launch_bounds__(WPB * 32) k_part_solve_r(Layout L, int max_rhs
                                                            const double* __restrict__ bp,
                                                            const double* __restrict__ GZ, double* __restrict__ PU,
                                                            double* __restrict__ PS) {
+    pdl_begin();
     __shared__ __align__(16) double ring[WPB][sweep_ring<B>() * B * B + 2];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int s = blockIdx.x * WPB + w;
@@ -836,6 +859,7 @@ template <int B>
 __global__ void __launch_bounds__(WPB * 32) k_factor1_r(Layout L, int max_rhs, const double* __restrict__ BD,
                                                         const double* __restrict__ BW, const double* __restrict__ BS,
                                                         double* D, double* Lc, double* Lr, double* X, Scalars* sc) {
+    pdl_begin();
     __shared__ double stage[WPB][B * B];
     __shared__ __align__(16) double xbuf[WPB][xchg_doubles<B, 1>()];
     __shared__ __align__(16) double ring[WPB][sweep_ring<B>() * B * B + 2];
@@ -856,6 +880,7 @@ template <int B>
 __global__ void __launch_bounds__(WPB * 32) k_hom_solve_r(Layout L, int max_rhs, const double* __restrict__ D,
                                                           const double* __restrict__ Lc,
                                                           const double* __restrict__ Lr, double* X) {
+    pdl_begin();
     __shared__ __align__(16) double ring[WPB][sweep_ring<B>() * B * B + 2];
     const int w = threadIdx.x >> 5;
     const int gw = blockIdx.x * WPB + w;
@@ -877,6 +902,7 @@ __global__ void __launch_bounds__(WPBT * 32) k_ds_solve_t(Layout L, const double
                                                           const double* __restrict__ BW, const double* __restrict__ BS,
                                                           double* D, double* Lr, double* Xd,
                                                           const double* __restrict__ RS, double* p, Scalars* sc) {
+    pdl_begin();
     __shared__ __align__(16) double sm[WPBT][twist_smem_doubles<B>()];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int s = blockIdx.x * WPBT + w;
@@ -927,6 +953,7 @@ __global__ void __launch_bounds__(WPBT * 32) k_factor1_t(Layout L, int max_rhs, 
                                                          const double* __restrict__ BW, const double* __restrict__ BS,
                                                          double* D, double* Lc, double* Lr, double* MidB, double* Sinv,
                                                          double* X, Scalars* sc) {
+    pdl_begin();
     __shared__ __align__(16) double sm[WPBT][twist_smem_doubles<B>()];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int s = blockIdx.x * WPBT + w;
@@ -946,6 +973,7 @@ __global__ void __launch_bounds__(WPBT * 32) k_hom_solve_t(Layout L, int max_rhs
                                                            const double* __restrict__ Lr,
                                                            const double* __restrict__ MidB,
                                                            const double* __restrict__ Sinv, double* X) {
+    pdl_begin();
     __shared__ __align__(16) double sm[WPBT][twist_smem_doubles<B>()];
     const int w = threadIdx.x >> 5;
     const int gw = blockIdx.x * WPBT + w;
@@ -970,6 +998,7 @@ __global__ void __launch_bounds__(WPBT * 32) k_part_solve_t(Layout L, int max_rh
                                                             const double* __restrict__ bp,
                                                             const double* __restrict__ GZ, double* __restrict__ PU,
                                                             double* __restrict__ PS) {
+    pdl_begin();
     __shared__ __align__(16) double sm[WPBT][twist_smem_doubles<B>()];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int s = blockIdx.x * WPBT + w;
@@ -998,6 +1027,7 @@ __global__ void __launch_bounds__(WPBT * 32) k_part_solve_t(Layout L, int max_rh
 // on shared edges).
 __global__ void k_ds_u(Layout L, const double* __restrict__ T, const double* __restrict__ Xd,
                        const double* __restrict__ EU, double* __restrict__ u) {
+    pdl_begin();
     const int f = blockIdx.x * blockDim.x + threadIdx.x;
     if (f >= L.faces()) return;
     if (f < L.vcount()) {
@@ -1039,6 +1069,7 @@ __global__ void k_ds_u(Layout L, const double* __restrict__ T, const double* __r
 // last block (a side counts when its net outflow exceeds 1e-14).
 __global__ void k_divres(Layout L, const double* __restrict__ u, const double* __restrict__ q, Scalars* sc,
                          double* part, unsigned* counter, const double* __restrict__ s_out = nullptr) {
+    pdl_begin();
     constexpr int NP = 10;  // res, scale, 4 x side net, 4 x side max
     double res = 0.0, scale = 0.0, net[4] = {0.0, 0.0, 0.0, 0.0}, smax[4] = {0.0, 0.0, 0.0, 0.0};
     const double vol = L.vol();
@@ -1114,6 +1145,7 @@ __global__ void k_mpm_rhs(Layout L, int max_rhs, int anchor, const double* __res
                           const double* __restrict__ bp, const double* __restrict__ pm,
                           const double* __restrict__ bpm, double* __restrict__ X, double* __restrict__ GZ,
                           double* __restrict__ WU) {
+    pdl_begin();
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= L.cells()) return;
     const int i = c % L.nx, j = c / L.nx;
@@ -1169,6 +1201,7 @@ __global__ void k_mpm_rhs(Layout L, int max_rhs, int anchor, const double* __res
 // Particular solve with the cached rebuild factor (mrcm.cpp:248).
 __global__ void k_part_solve(Layout L, int max_rhs, const double* __restrict__ D, const double* __restrict__ Lc,
                              const double* __restrict__ Lr, double* __restrict__ X) {
+    pdl_begin();
     extern __shared__ double smem[];
     const int w = threadIdx.x >> 5;
     const int s = blockIdx.x * WPB + w;
@@ -1186,6 +1219,7 @@ __global__ void k_part_traces(Layout L, int max_rhs, const double* __restrict__ 
                               const int* __restrict__ bc_kind, const double* __restrict__ bm,
                               const double* __restrict__ bp, const double* __restrict__ GZ,
                               const double* __restrict__ X, double* __restrict__ PU) {
+    pdl_begin();
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     if (x >= L.n_sub * L.nbe) return;
     const int s = x / L.nbe, idx = x % L.nbe;
@@ -1205,6 +1239,7 @@ __global__ void k_part_traces(Layout L, int max_rhs, const double* __restrict__ 
 }
 
 __global__ void k_part_psum(Layout L, int max_rhs, const double* __restrict__ X, double* __restrict__ PS) {
+    pdl_begin();
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (gw >= L.n_sub) return;
     const double* x = X + xoff(L, max_rhs, gw, 0);
@@ -1217,6 +1252,7 @@ __global__ void k_part_psum(Layout L, int max_rhs, const double* __restrict__ X,
 // ---------------------------------------------------------------- static --
 __global__ void k_static(Layout L, const double* __restrict__ q, const int* __restrict__ bc_kind,
                          double* __restrict__ qsum, double* __restrict__ ground) {
+    pdl_begin();
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= L.n_sub) return;
     const double vol = L.vol();
@@ -1234,6 +1270,7 @@ __global__ void k_static(Layout L, const double* __restrict__ q, const int* __re
 
 // Dense repair operator (mrcm.cpp:351-371): one thread per row.
 __global__ void k_repair_matrix(Layout L, int grounded, const double* __restrict__ ground, double* __restrict__ A) {
+    pdl_begin();
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     const int n = L.n_sub;
     if (s >= n) return;
@@ -1266,7 +1303,7 @@ int band_blocks(const Layout& L) { return cdiv(L.n_sub, WPB); }
 void launch_trans(Ctx& c, const double* kappa) {
     {
         PROF(c, "k_trans");
-        k_trans<<<std::min(grid_for(c.L.faces()), 8 * c.num_sms), TPB, 0, c.st>>>(c.L, kappa, c.T);
+        launch_k(c, k_trans, std::min(grid_for(c.L.faces()), 8 * c.num_sms), TPB, 0, c.L, kappa, c.T);
         CK_LAUNCH();
     }
 }
@@ -1277,7 +1314,7 @@ void launch_beta(Ctx& c, const double* kappa) {
     if (E == 0) return;
     {
         PROF(c, "k_face_kappa");
-        k_face_kappa<<<grid_for(E), TPB, 0, c.st>>>(L, kappa, c.face_kappa);
+        launch_k(c, k_face_kappa, grid_for(E), TPB, 0, L, kappa, c.face_kappa);
         CK_LAUNCH();
     }
     if (c.alpha_mode == 1) {
@@ -1286,7 +1323,7 @@ void launch_beta(Ctx& c, const double* kappa) {
     }
     {
         PROF(c, "k_beta");
-        k_beta<<<grid_for(E), TPB, 0, c.st>>>(L, kappa, c.face_kappa, c.sort_keys, c.alpha_mode, c.alpha, c.alpha_min,
+        launch_k(c, k_beta, grid_for(E), TPB, 0, L, kappa, c.face_kappa, c.sort_keys, c.alpha_mode, c.alpha, c.alpha_min,
                                               c.alpha_max, c.pct_lo, c.pct_hi, c.beta_m, c.beta_p, c.alpha_e, c.sc);
         CK_LAUNCH();
     }
@@ -1296,7 +1333,7 @@ void launch_setup_static(Ctx& c) {
     const Layout& L = c.L;
     {
         PROF(c, "k_static");
-        k_static<<<grid_for(L.n_sub), TPB, 0, c.st>>>(L, c.q, c.bc_kind, c.qsum_sub, c.ground);
+        launch_k(c, k_static, grid_for(L.n_sub), TPB, 0, L, c.q, c.bc_kind, c.qsum_sub, c.ground);
         CK_LAUNCH();
     }
     if (c.repair_active) {
@@ -1304,7 +1341,7 @@ void launch_setup_static(Ctx& c) {
         A.alloc((size_t)L.n_sub * L.n_sub);
         {
             PROF(c, "k_repair_matrix");
-            k_repair_matrix<<<grid_for(L.n_sub), TPB, 0, c.st>>>(L, c.grounded ? 1 : 0, c.ground, A);
+            launch_k(c, k_repair_matrix, grid_for(L.n_sub), TPB, 0, L, c.grounded ? 1 : 0, c.ground, A);
             CK_LAUNCH();
         }
         const double rc = spd_inverse(c, A, c.Linv, L.n_sub);
@@ -1320,24 +1357,24 @@ void downscale(Ctx& c, const double* kappa) {
     const Layout& L = c.L;
     {  // skeleton fluxes (k_skel) are formed inside k_resid
         PROF(c, "k_resid");
-        k_resid<<<grid_for(32LL * L.n_sub), TPB, 0, c.st>>>(L, c.skel, c.RU, c.qsum_sub, c.resid, c.sc, c.red,
+        launch_k(c, k_resid, grid_for(32LL * L.n_sub), TPB, 0, L, c.skel, c.RU, c.qsum_sub, c.resid, c.sc, c.red,
                                                              c.red_count, 1);
         CK_LAUNCH();
     }
     if (c.repair_active) {
         PROF(c, "k_repair_delta");
-        k_repair_delta<<<cdiv((long long)L.n_sub * 32, TPB), TPB, 0, c.st>>>(
+        launch_k(c, k_repair_delta, cdiv((long long)L.n_sub * 32, TPB), TPB, 0, 
             L.n_sub, c.Linv, c.resid, c.delta, L, c.grounded ? 1 : 0, c.ground, c.corr, c.sc, c.red_count);
         CK_LAUNCH();
     } else {
         PROF(c, "k_repair_corr");
-        k_repair_corr<<<std::min(grid_for(std::max(L.n_iface, L.n_sub)), 2 * c.num_sms), TPB, 0, c.st>>>(
+        launch_k(c, k_repair_corr, std::min(grid_for(std::max(L.n_iface, L.n_sub)), 2 * c.num_sms), TPB, 0, 
             L, 0, c.grounded ? 1 : 0, c.delta, c.ground, c.corr, c.sc, c.red, c.red_count);
         CK_LAUNCH();
     }
     {
         PROF(c, "k_ds_prep");
-        k_ds_prep<<<grid_for(L.cells()), TPB, 0, c.st>>>(L, kappa, c.T, c.q, c.bc_kind, c.skel, c.corr, c.RU, c.delta,
+        launch_k(c, k_ds_prep, grid_for(L.cells()), TPB, 0, L, kappa, c.T, c.q, c.bc_kind, c.skel, c.corr, c.RU, c.delta,
                                                          c.grounded ? 1 : 0, c.BDd, c.BWd, c.BSd, c.Xd, c.GZ, c.sc);
         CK_LAUNCH();
     }
@@ -1349,7 +1386,7 @@ void downscale(Ctx& c, const double* kappa) {
         switch (L.snx) {
 #define X(BW_)                                                                                                  \
     case BW_:                                                                                                   \
-        k_ds_solve_t<BW_><<<cdiv(L.n_sub, WPBT), WPBT * 32, 0, c.st>>>(L, c.BDd, c.BWd, c.BSd, c.Dd, c.Lrd, c.Xd, \
+        launch_k(c, k_ds_solve_t<BW_>, cdiv(L.n_sub, WPBT), WPBT * 32, 0, L, c.BDd, c.BWd, c.BSd, c.Dd, c.Lrd, c.Xd, \
                                                                        c.RS, c.p, c.sc);                        \
         done = true;                                                                                            \
         break;
@@ -1365,25 +1402,25 @@ void downscale(Ctx& c, const double* kappa) {
         switch (c.no_regband ? -1 : L.snx) {
 #define X(BW_)                                                                                                     \
     case BW_:                                                                                                      \
-        k_ds_solve_r<BW_><<<band_blocks(L), WPB * 32, 0, c.st>>>(L, c.BDd, c.BWd, c.BSd, c.Dd, c.Lrd, c.Xd, c.RS, \
+        launch_k(c, k_ds_solve_r<BW_>, band_blocks(L), WPB * 32, 0, L, c.BDd, c.BWd, c.BSd, c.Dd, c.Lrd, c.Xd, c.RS, \
                                                                   c.p, c.sc);                                     \
         break;
             MPM2P_BAND_WIDTHS(X)
 #undef X
             default:
-                k_ds_solve<<<band_blocks(L), WPB * 32, sm1, c.st>>>(L, c.BDd, c.BWd, c.BSd, c.Dd, c.Lrd, c.Xd, c.RS,
+                launch_k(c, k_ds_solve, band_blocks(L), WPB * 32, sm1, L, c.BDd, c.BWd, c.BSd, c.Dd, c.Lrd, c.Xd, c.RS,
                                                                     c.p, c.sc);
         }
         CK_LAUNCH();
     }
     {  // (fusing this into k_ds_solve_r serialises ~17 dependent loads per lane: slower)
         PROF(c, "k_ds_u");
-        k_ds_u<<<grid_for(L.faces()), TPB, 0, c.st>>>(L, c.T, c.Xd, c.GZ, c.u);
+        launch_k(c, k_ds_u, grid_for(L.faces()), TPB, 0, L, c.T, c.Xd, c.GZ, c.u);
         CK_LAUNCH();
     }
     {
         PROF(c, "k_divres");
-        k_divres<<<std::min(grid_for(std::max(L.cells(), L.faces())), 2 * c.num_sms), TPB, 0, c.st>>>(
+        launch_k(c, k_divres, std::min(grid_for(std::max(L.cells(), L.faces())), 2 * c.num_sms), TPB, 0, 
             L, c.u, c.q, c.sc, c.red, c.red_count, c.outlet_s);
         CK_LAUNCH();
     }
@@ -1396,7 +1433,7 @@ void interface_solve(Ctx& c) {
     if (c.dim == 0) return;
     {
         PROF(c, "k_iface_rhs");
-        k_iface_rhs<<<grid_for(32LL * c.dim), TPB, 0, c.st>>>(L, c.PU, c.beta_m, c.beta_p, c.irhs);
+        launch_k(c, k_iface_rhs, grid_for(32LL * c.dim), TPB, 0, L, c.PU, c.beta_m, c.beta_p, c.irhs);
         CK_LAUNCH();
     }
     if (c.use_krylov) {
@@ -1425,13 +1462,13 @@ void launch_rebuild(Ctx& c, const double* kappa, bool compute_beta) {  // comput
     launch_trans(c, kappa);
     {
         PROF(c, "k_band_entries");
-        k_band_entries<<<grid_for(L.cells()), TPB, 0, c.st>>>(L, kappa, c.T, 0, c.anchor_m ? 1 : 0, c.beta_m, c.beta_p,
+        launch_k(c, k_band_entries, grid_for(L.cells()), TPB, 0, L, kappa, c.T, 0, c.anchor_m ? 1 : 0, c.beta_m, c.beta_p,
                                                               c.bc_kind, c.BDm, c.BWm, c.BSm, c.sc);
         CK_LAUNCH();
     }
     {
         PROF(c, "k_rebuild_rhs");
-        k_rebuild_rhs<<<grid_for(L.cells()), TPB, 0, c.st>>>(L, c.max_rhs, kappa, c.q, c.bc_kind, c.bc_value, c.beta_m,
+        launch_k(c, k_rebuild_rhs, grid_for(L.cells()), TPB, 0, L, c.max_rhs, kappa, c.q, c.bc_kind, c.bc_value, c.beta_m,
                                                              c.beta_p, c.anchor_m ? 1 : 0, c.X);
         CK_LAUNCH();
     }
@@ -1442,7 +1479,7 @@ void launch_rebuild(Ctx& c, const double* kappa, bool compute_beta) {  // comput
             switch (L.snx) {
 #define X(BW_)                                                                                                  \
     case BW_:                                                                                                   \
-        k_factor1_t<BW_><<<cdiv(L.n_sub, WPBT), WPBT * 32, 0, c.st>>>(L, c.max_rhs, c.BDm, c.BWm, c.BSm, c.Dm,   \
+        launch_k(c, k_factor1_t<BW_>, cdiv(L.n_sub, WPBT), WPBT * 32, 0, L, c.max_rhs, c.BDm, c.BWm, c.BSm, c.Dm,   \
                                                                       c.Lcm, c.Lrm, c.tw_midb, c.tw_sinv, c.X, \
                                                                       c.sc);                                   \
         break;
@@ -1458,7 +1495,7 @@ void launch_rebuild(Ctx& c, const double* kappa, bool compute_beta) {  // comput
             switch (L.snx) {
 #define X(BW_)                                                                                                  \
     case BW_:                                                                                                   \
-        k_hom_solve_t<BW_><<<cdiv((long long)L.n_sub * L.max_hom, WPBT), WPBT * 32, 0, c.st>>>(                 \
+        launch_k(c, k_hom_solve_t<BW_>, cdiv((long long)L.n_sub * L.max_hom, WPBT), WPBT * 32, 0,                  \
             L, c.max_rhs, c.Dm, c.Lcm, c.Lrm, c.tw_midb, c.tw_sinv, c.X);                                       \
         break;
                 MPM2P_TWIST_WIDTHS(X)
@@ -1473,32 +1510,32 @@ void launch_rebuild(Ctx& c, const double* kappa, bool compute_beta) {  // comput
         switch (c.no_regband ? -1 : L.snx) {
 #define X(BW_)                                                                                                      \
     case BW_:                                                                                                       \
-        k_factor1_r<BW_><<<band_blocks(L), WPB * 32, 0, c.st>>>(L, c.max_rhs, c.BDm, c.BWm, c.BSm, c.Dm, c.Lcm,   \
+        launch_k(c, k_factor1_r<BW_>, band_blocks(L), WPB * 32, 0, L, c.max_rhs, c.BDm, c.BWm, c.BSm, c.Dm, c.Lcm,   \
                                                                 c.Lrm, c.X, c.sc);                                  \
         if (L.max_hom > 0) {                                                                                        \
             CK_LAUNCH();                                                                                            \
             PROF(c, "k_hom_solve");                                                                                 \
-            k_hom_solve_r<BW_><<<cdiv((long long)L.n_sub * L.max_hom, WPB), WPB * 32, 0, c.st>>>(                  \
+            launch_k(c, k_hom_solve_r<BW_>, cdiv((long long)L.n_sub * L.max_hom, WPB), WPB * 32, 0,                   \
                 L, c.max_rhs, c.Dm, c.Lcm, c.Lrm, c.X);                                                             \
         }                                                                                                           \
         break;
             MPM2P_BAND_WIDTHS(X)
 #undef X
             default:
-                k_factor_solve<<<band_blocks(L), WPB * 32, smr, c.st>>>(L, c.max_rhs, c.BDm, c.BWm, c.BSm, c.Dm,
+                launch_k(c, k_factor_solve, band_blocks(L), WPB * 32, smr, L, c.max_rhs, c.BDm, c.BWm, c.BSm, c.Dm,
                                                                         c.Lcm, c.Lrm, c.X, c.sc);
         }
         CK_LAUNCH();
     }
     {
         PROF(c, "k_rebuild_traces");
-        k_rebuild_traces<<<grid_for((long long)L.n_sub * L.nbe), TPB, 0, c.st>>>(
+        launch_k(c, k_rebuild_traces, grid_for((long long)L.n_sub * L.nbe), TPB, 0, 
             L, c.max_rhs, kappa, c.bc_kind, c.bc_value, c.beta_m, c.beta_p, c.X, c.PU, c.PB, c.HU, c.HB);
         CK_LAUNCH();
     }
     {
         PROF(c, "k_psums");
-        k_psums<<<cdiv((long long)L.n_sub * c.max_rhs * 32, TPB), TPB, 0, c.st>>>(L, c.max_rhs, c.X, c.PS, c.HP);
+        launch_k(c, k_psums, cdiv((long long)L.n_sub * c.max_rhs * 32, TPB), TPB, 0, L, c.max_rhs, c.X, c.PS, c.HP);
         CK_LAUNCH();
     }
     c.c_hom += c.nhat;
@@ -1507,7 +1544,7 @@ void launch_rebuild(Ctx& c, const double* kappa, bool compute_beta) {  // comput
     if (c.dim > 0) {
         {
             PROF(c, "k_assemble");
-            k_assemble<<<grid_for(c.nnz), TPB, 0, c.st>>>(L, c.csr_row, c.csr_col, c.nnz, c.HU, c.beta_m, c.beta_p,
+            launch_k(c, k_assemble, grid_for(c.nnz), TPB, 0, L, c.csr_row, c.csr_col, c.nnz, c.HU, c.beta_m, c.beta_p,
                                                           c.csr_val);
             CK_LAUNCH();
         }
@@ -1520,7 +1557,7 @@ void launch_rebuild(Ctx& c, const double* kappa, bool compute_beta) {  // comput
             c.Mdense.alloc((size_t)c.dim * c.dim);
             {
                 PROF(c, "k_csr_to_dense");
-                k_csr_to_dense<<<c.dim, TPB, 0, c.st>>>(c.csr_ptr, c.csr_col, c.csr_val, c.dim, c.Mdense);
+                launch_k(c, k_csr_to_dense, c.dim, TPB, 0, c.csr_ptr, c.csr_col, c.csr_val, c.dim, c.Mdense);
                 CK_LAUNCH();
             }
             // rcond guard (mrcm.cpp:227-238) is evaluated on the device; a trip
@@ -1533,18 +1570,18 @@ void launch_rebuild(Ctx& c, const double* kappa, bool compute_beta) {  // comput
     if (c.dim == 0) CK(cudaMemsetAsync(c.icoef, 0, sizeof(double), c.st));
     {
         PROF(c, "k_recon_traces");
-        k_recon_traces<<<grid_for((long long)L.n_sub * L.nbe), TPB, 0, c.st>>>(L, c.icoef, c.PU, c.PB, c.HU, c.HB, nullptr,
+        launch_k(c, k_recon_traces, grid_for((long long)L.n_sub * L.nbe), TPB, 0, L, c.icoef, c.PU, c.PB, c.HU, c.HB, nullptr,
                                                                                c.RU, c.bpm);
         CK_LAUNCH();
     }
     {
         PROF(c, "k_recon_p");
-        k_recon_p<<<grid_for(L.cells()), TPB, 0, c.st>>>(L, c.max_rhs, c.icoef, c.X, c.pm);
+        launch_k(c, k_recon_p, grid_for(L.cells()), TPB, 0, L, c.max_rhs, c.icoef, c.X, c.pm);
         CK_LAUNCH();
     }
     {
         PROF(c, "k_sub_sum");
-        k_sub_sum<<<cdiv((long long)L.n_sub * 32, TPB), TPB, 0, c.st>>>(L, c.pm, c.pmsum);
+        launch_k(c, k_sub_sum, cdiv((long long)L.n_sub * 32, TPB), TPB, 0, L, c.pm, c.pmsum);
         CK_LAUNCH();
     }
     CK(cudaMemcpyAsync(c.RS, c.pmsum, L.n_sub * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
@@ -1559,7 +1596,7 @@ void launch_mpm(Ctx& c, const double* kn) {  // mpm_pressure_update (mpm.cpp:31-
     launch_trans(c, kn);
     {
         PROF(c, "k_mpm_rhs");
-        k_mpm_rhs<<<grid_for(L.cells()), TPB, 0, c.st>>>(L, c.max_rhs, c.anchor_m ? 1 : 0, kn, c.kappa_m, c.T, c.q,
+        launch_k(c, k_mpm_rhs, grid_for(L.cells()), TPB, 0, L, c.max_rhs, c.anchor_m ? 1 : 0, kn, c.kappa_m, c.T, c.q,
                                                          c.bc_kind, c.bc_value, c.beta_m, c.beta_p, c.pm, c.bpm, c.X,
                                                          c.GZ, c.WU);
         CK_LAUNCH();
@@ -1571,7 +1608,7 @@ void launch_mpm(Ctx& c, const double* kn) {  // mpm_pressure_update (mpm.cpp:31-
         switch (L.snx) {
 #define X(BW_)                                                                                                  \
     case BW_:                                                                                                   \
-        k_part_solve_t<BW_><<<cdiv(L.n_sub, WPBT), WPBT * 32, 0, c.st>>>(                                       \
+        launch_k(c, k_part_solve_t<BW_>, cdiv(L.n_sub, WPBT), WPBT * 32, 0,                                        \
             L, c.max_rhs, c.Dm, c.Lcm, c.Lrm, c.tw_midb, c.tw_sinv, c.X, c.kappa_m, c.bc_kind, c.beta_m,        \
             c.beta_p, c.GZ, c.PU, c.PS);                                                                        \
         break;
@@ -1587,7 +1624,7 @@ void launch_mpm(Ctx& c, const double* kn) {  // mpm_pressure_update (mpm.cpp:31-
         switch (c.no_regband ? -1 : L.snx) {
 #define X(BW_)                                                                                                  \
     case BW_:                                                                                                   \
-        k_part_solve_r<BW_><<<band_blocks(L), WPB * 32, 0, c.st>>>(L, c.max_rhs, c.Dm, c.Lcm, c.Lrm, c.X,     \
+        launch_k(c, k_part_solve_r<BW_>, band_blocks(L), WPB * 32, 0, L, c.max_rhs, c.Dm, c.Lcm, c.Lrm, c.X,     \
                                                                    c.kappa_m, c.bc_kind, c.beta_m, c.beta_p,   \
                                                                    c.GZ, c.PU, c.PS);                          \
         fused_traces = true;                                                                                    \
@@ -1595,20 +1632,20 @@ void launch_mpm(Ctx& c, const double* kn) {  // mpm_pressure_update (mpm.cpp:31-
             MPM2P_BAND_WIDTHS(X)
 #undef X
             default:
-                k_part_solve<<<band_blocks(L), WPB * 32, sm1, c.st>>>(L, c.max_rhs, c.Dm, c.Lcm, c.Lrm, c.X);
+                launch_k(c, k_part_solve, band_blocks(L), WPB * 32, sm1, L, c.max_rhs, c.Dm, c.Lcm, c.Lrm, c.X);
         }
         CK_LAUNCH();
     }
     if (!fused_traces) {
         {
             PROF(c, "k_part_traces");
-            k_part_traces<<<grid_for((long long)L.n_sub * L.nbe), TPB, 0, c.st>>>(
+            launch_k(c, k_part_traces, grid_for((long long)L.n_sub * L.nbe), TPB, 0, 
                 L, c.max_rhs, c.kappa_m, c.bc_kind, c.beta_m, c.beta_p, c.GZ, c.X, c.PU);
             CK_LAUNCH();
         }
         {
             PROF(c, "k_part_psum");
-            k_part_psum<<<cdiv((long long)L.n_sub * 32, TPB), TPB, 0, c.st>>>(L, c.max_rhs, c.X, c.PS);
+            launch_k(c, k_part_psum, cdiv((long long)L.n_sub * 32, TPB), TPB, 0, L, c.max_rhs, c.X, c.PS);
             CK_LAUNCH();
         }
     }
@@ -1617,19 +1654,19 @@ void launch_mpm(Ctx& c, const double* kn) {  // mpm_pressure_update (mpm.cpp:31-
     if (c.dim == 0) CK(cudaMemsetAsync(c.icoef, 0, sizeof(double), c.st));
     if (L.max_hom <= 16) {
         PROF(c, "k_recon_mpm");
-        k_recon_mpm<<<cdiv((long long)L.n_sub * 32, TPB), TPB, 0, c.st>>>(L, c.icoef, c.PU, c.HU, c.WU, c.RU, c.PS,
+        launch_k(c, k_recon_mpm, cdiv((long long)L.n_sub * 32, TPB), TPB, 0, L, c.icoef, c.PU, c.HU, c.WU, c.RU, c.PS,
                                                                           c.HP, c.pmsum, c.RS);
         CK_LAUNCH();
     } else {  // per-edge interface spaces: more homogeneous functions than k_recon_mpm keeps in registers
         {
             PROF(c, "k_recon_traces");
-            k_recon_traces<<<grid_for((long long)L.n_sub * L.nbe), TPB, 0, c.st>>>(L, c.icoef, c.PU, nullptr, c.HU,
+            launch_k(c, k_recon_traces, grid_for((long long)L.n_sub * L.nbe), TPB, 0, L, c.icoef, c.PU, nullptr, c.HU,
                                                                                    nullptr, c.WU, c.RU, nullptr);
             CK_LAUNCH();
         }
         {
             PROF(c, "k_recon_psum");
-            k_recon_psum<<<grid_for(L.n_sub), TPB, 0, c.st>>>(L, c.icoef, c.PS, c.HP, c.pmsum, c.RS);
+            launch_k(c, k_recon_psum, grid_for(L.n_sub), TPB, 0, L, c.icoef, c.PS, c.HP, c.pmsum, c.RS);
             CK_LAUNCH();
         }
     }

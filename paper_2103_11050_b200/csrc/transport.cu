@@ -91,6 +91,7 @@ __device__ __forceinline__ DD reduce_dd_partials(const double* part, int nparts,
 // max over the reference's 1001 sample points (transport.cpp:45-49); max is
 // order-independent, so one thread per point gives the same value.
 __global__ void k_max_slope(Scalars* sc, double M) {
+    pdl_begin();
     __shared__ double sh[32];
     double m = 0.0;
     for (int k = threadIdx.x; k <= 1000; k += blockDim.x) m = fmax(m, fprime(k * 1e-3, M));
@@ -105,6 +106,7 @@ __device__ double inj_rate_block(const Layout& L, const double* __restrict__ u, 
 // the PVI clock inj_cn times (the driver's k_cfl + k_inj_pvi in one launch).
 __global__ void k_cfl(Layout L, const double* __restrict__ u, Scalars* sc, double safety, double dt_cap,
                       double* part, unsigned* counter, int inj_cn = 0, double inflow = 0.0, double M = 1.0) {
+    pdl_begin();
     __shared__ double sh[32];
     const double vol = L.vol(), slope = sc->slope;
     double best = INFINITY;
@@ -177,6 +179,7 @@ __device__ double inj_rate_block(const Layout& L, const double* __restrict__ u, 
 
 __global__ void k_inj_pvi(Layout L, const double* __restrict__ u, Scalars* sc, double inflow, double M, int cn,
                           int add_pvi) {
+    pdl_begin();
     __shared__ double sh[32];
     const double rate = inj_rate_block(L, u, frac_flow(inflow, M, nullptr), sh);
     if (threadIdx.x == 0) {
@@ -192,6 +195,7 @@ __global__ void k_inj_pvi(Layout L, const double* __restrict__ u, Scalars* sc, d
 // face compute its water flux with identical IEEE operations.
 __global__ void k_upwind(Layout L, const double* __restrict__ s, double* __restrict__ s_out,
                          const double* __restrict__ u, Scalars* sc, double inflow, double M) {
+    pdl_begin();
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c == 0) (void)frac_flow(inflow, M, &sc->clamp);  // f_in is evaluated once per call
     if (c >= L.cells()) return;
@@ -233,6 +237,7 @@ __global__ void k_kappa(Layout L, const double* __restrict__ K, const double* __
                         double* __restrict__ kappa, const double* __restrict__ kappa_m,
                         const double* __restrict__ lam_reb, Scalars* sc, double M, int eps_mode, double* part,
                         unsigned* counter, int decide_method = -1, int rebuilt = 0, double eta = 0.0) {
+    pdl_begin();
     __shared__ DD shd[32];
     const double vol = L.vol();
     DD num{0.0, 0.0}, den{0.0, 0.0};
@@ -297,11 +302,13 @@ __device__ __forceinline__ void decide(Scalars* sc, int rebuilt, int method, dou
     }
 }
 __global__ void k_decide(Scalars* sc, int rebuilt, int method, double eta, int step) {
+    pdl_begin();
     decide(sc, rebuilt, method, eta, step);
 }
 
 // max_outlet_saturation (simulation.cpp:61-83): one block, four sides.
 __global__ void k_outlet(Layout L, const double* __restrict__ s, const double* __restrict__ u, Scalars* sc) {
+    pdl_begin();
     __shared__ double sh[32];
     double m = 0.0;
     for (int side = 0; side < 4; ++side) {
@@ -341,7 +348,8 @@ __global__ void k_outlet(Layout L, const double* __restrict__ s, const double* _
     if (threadIdx.x == 0) sc->outlet_max = m;
 }
 
-__global__ void k_divergence(Layout L, const double* __restrict__ u, double* __restrict__ div) {  // grid.cpp:19-31
+__global__ void k_divergence(Layout L, const double* __restrict__ u, double* __restrict__ div) {
+    pdl_begin();  // grid.cpp:19-31
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= L.cells()) return;
     const int i = c % L.nx, j = c / L.nx;
@@ -353,6 +361,7 @@ __global__ void k_divergence(Layout L, const double* __restrict__ u, double* __r
 // epsilon(kappa_n, kappa_m, mode) on two arbitrary fields (mpm.cpp:9-25).
 __global__ void k_eps_fields(Layout L, const double* __restrict__ kn, const double* __restrict__ km, Scalars* sc,
                              int mode, double* part, unsigned* counter) {
+    pdl_begin();
     __shared__ DD shd[32];
     const double vol = L.vol();
     DD num{0.0, 0.0}, den{0.0, 0.0};
@@ -385,6 +394,7 @@ __global__ void k_eps_fields(Layout L, const double* __restrict__ kn, const doub
 }
 
 __global__ void k_lambda(Layout L, const double* __restrict__ s, double* __restrict__ lam, Scalars* sc, double M) {
+    pdl_begin();
     const int c = blockIdx.x * blockDim.x + threadIdx.x;  // mobility_field (simulation.cpp:156-160)
     if (c < L.cells()) lam[c] = total_mob(s[c], M, &sc->clamp);
 }
@@ -396,83 +406,83 @@ int red_grid(const Ctx& c) { return std::min(2 * c.num_sms, std::max(1, cdiv(c.L
 void launch_max_slope(Ctx& c) {
     {
         PROF(c, "k_max_slope");
-        k_max_slope<<<1, 1024, 0, c.st>>>(c.sc, c.M);
+        launch_k(c, k_max_slope, 1, 1024, 0, c.sc, c.M);
         CK_LAUNCH();
     }
 }
 void launch_cfl(Ctx& c, const double* u, double safety, double dt_cap) {
     {
         PROF(c, "k_cfl");
-        k_cfl<<<red_grid(c), TPB, 0, c.st>>>(c.L, u, c.sc, safety, dt_cap, c.red, c.red_count);
+        launch_k(c, k_cfl, red_grid(c), TPB, 0, c.L, u, c.sc, safety, dt_cap, c.red, c.red_count, 0, 0.0, 1.0);
         CK_LAUNCH();
     }
 }
 void launch_inj_pvi(Ctx& c, const double* u, double inflow, int cn, bool add_pvi) {
     {
         PROF(c, "k_inj_pvi");
-        k_inj_pvi<<<1, TPB, 0, c.st>>>(c.L, u, c.sc, inflow, c.M, cn, add_pvi ? 1 : 0);
+        launch_k(c, k_inj_pvi, 1, TPB, 0, c.L, u, c.sc, inflow, c.M, cn, add_pvi ? 1 : 0);
         CK_LAUNCH();
     }
 }
 void launch_upwind(Ctx& c, const double* s_in, double* s_out, const double* u, double inflow) {
     {
         PROF(c, "k_upwind");
-        k_upwind<<<cdiv(c.L.cells(), TPB), TPB, 0, c.st>>>(c.L, s_in, s_out, u, c.sc, inflow, c.M);
+        launch_k(c, k_upwind, cdiv(c.L.cells(), TPB), TPB, 0, c.L, s_in, s_out, u, c.sc, inflow, c.M);
         CK_LAUNCH();
     }
 }
 void launch_cfl_inj(Ctx& c, const double* u, double safety, double dt_cap, double inflow, int cn) {
     PROF(c, "k_cfl");
-    k_cfl<<<red_grid(c), TPB, 0, c.st>>>(c.L, u, c.sc, safety, dt_cap, c.red, c.red_count, cn, inflow, c.M);
+    launch_k(c, k_cfl, red_grid(c), TPB, 0, c.L, u, c.sc, safety, dt_cap, c.red, c.red_count, cn, inflow, c.M);
     CK_LAUNCH();
 }
 void launch_conductivity_decide(Ctx& c, const double* s, double* kappa, int eps_mode, int rebuilt, int method,
                                 double eta) {
     PROF(c, "k_kappa");
-    k_kappa<<<red_grid(c), TPB, 0, c.st>>>(c.L, c.K, s, kappa, c.kappa_m, c.lam_reb, c.sc, c.M, eps_mode, c.red,
+    launch_k(c, k_kappa, red_grid(c), TPB, 0, c.L, c.K, s, kappa, c.kappa_m, c.lam_reb, c.sc, c.M, eps_mode, c.red,
                                            c.red_count, method, rebuilt, eta);
     CK_LAUNCH();
 }
 void launch_conductivity(Ctx& c, const double* s, double* kappa, int eps_mode, bool want_eps) {
     {
         PROF(c, "k_kappa");
-        k_kappa<<<red_grid(c), TPB, 0, c.st>>>(c.L, c.K, s, kappa, c.kappa_m, c.lam_reb, c.sc, c.M,
-                                               want_eps ? eps_mode : -1, c.red, c.red_count);
+        launch_k(c, k_kappa, red_grid(c), TPB, 0, c.L, c.K, s, kappa, c.kappa_m, c.lam_reb, c.sc, c.M,
+                                               want_eps ? eps_mode : -1, c.red, c.red_count, -1, 0, 0.0);
         CK_LAUNCH();
     }
 }
 void launch_lambda(Ctx& c, const double* s, double* lam) {
     {
         PROF(c, "k_lambda");
-        k_lambda<<<cdiv(c.L.cells(), TPB), TPB, 0, c.st>>>(c.L, s, lam, c.sc, c.M);
+        launch_k(c, k_lambda, cdiv(c.L.cells(), TPB), TPB, 0, c.L, s, lam, c.sc, c.M);
         CK_LAUNCH();
     }
 }
 void launch_outlet(Ctx& c, const double* s, const double* u) {
     {
         PROF(c, "k_outlet");
-        k_outlet<<<1, TPB, 0, c.st>>>(c.L, s, u, c.sc);
+        launch_k(c, k_outlet, 1, TPB, 0, c.L, s, u, c.sc);
         CK_LAUNCH();
     }
 }
 void launch_divergence(Ctx& c, const double* u, double* div) {
     {
         PROF(c, "k_divergence");
-        k_divergence<<<cdiv(c.L.cells(), TPB), TPB, 0, c.st>>>(c.L, u, div);
+        launch_k(c, k_divergence, cdiv(c.L.cells(), TPB), TPB, 0, c.L, u, div);
         CK_LAUNCH();
     }
 }
 void launch_decide(Ctx& c, int rebuilt, int method, double eta, int step) {
     {
         PROF(c, "k_decide");
-        k_decide<<<1, 1, 0, c.st>>>(c.sc, rebuilt, method, eta, step);
+        launch_k(c, k_decide, 1, 1, 0, c.sc, rebuilt, method, eta, step);
         CK_LAUNCH();
     }
 }
 void launch_epsilon_fields(Ctx& c, const double* kn, const double* km, int mode) {
     {
         PROF(c, "k_eps_fields");
-        k_eps_fields<<<red_grid(c), TPB, 0, c.st>>>(c.L, kn, km, c.sc, mode, c.red, c.red_count);
+        launch_k(c, k_eps_fields, red_grid(c), TPB, 0, c.L, kn, km, c.sc, mode, c.red, c.red_count);
         CK_LAUNCH();
     }
 }
