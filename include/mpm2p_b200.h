@@ -125,8 +125,8 @@ typedef struct mpm2p_run_record {
     double min_eps_margin;  /* min over decisions of |eps - eta| / eta (bit-exactness guard) */
     int64_t clamp_count;    /* clamp_count() (transport.hpp:24-26) */
     /* Interface-solve diagnostics of this implementation (no reference
-     * counterpart; the oracle writes zeros): 1 when the interface system was
-     * solved by MINRES instead of the dense inverse, total and max iterations. */
+     * counterpart; the oracle writes zeros): interface_krylov = 0 dense
+     * inverse, 1 MINRES, 2 direct block-tridiagonal; MINRES iteration counts. */
     int32_t interface_krylov, interface_max_iterations;
     int64_t interface_iterations;
 } mpm2p_run_record;

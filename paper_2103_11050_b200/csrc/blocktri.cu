@@ -1,0 +1,295 @@
+// blocktri.cu — K7b: direct block-tridiagonal interface solve for systems
+// above the dense limit (C5: dim 65,024; the reference's dense PartialPivLU
+// there would be 34 GB, proj/src/mrcm.cpp:198,226,264).
+//
+// Ordered by subdomain row (the vertical interfaces of row j and the
+// horizontal interfaces between rows j and j+1 form block j), K = J M is
+// block tridiagonal: an interface only couples to interfaces that share a
+// subdomain with it. K is symmetric quasi-definite, so block
+// LDL^T needs no pivoting:
+//   S_0 = D_0,  T_{j-1} = S_{j-1}^-1 E_{j-1},  S_j = D_j - E_{j-1}^T T_{j-1};
+//   solve: y_j = b_j - T_{j-1}^T y_{j-1} (forward),
+//          x_j = S_j^-1 y_j - T_j x_{j+1} (backward).
+// Per rebuild: nblk dense inversions (ping-pong Gauss-Jordan, dense.cu) and
+// two GEMMs per block; per solve: 2 nblk - 1 dependent block products, each
+// HBM-bound. At C5: 128 blocks of 510 unknowns, S^-1 / T / T^T / D / E about
+// 0.27 GB each.
+#include "context.cuh"
+
+namespace mpm2p {
+
+namespace {
+
+constexpr int TPB = 256;
+
+// C[m x n] = op(A)[m x k] * B[k x n] (+ beta C0), row-major. TA: A is stored
+// k x m (use A^T). 64 x 64 tiles, k-slabs of 16, 4 x 4 outputs per thread.
+template <bool TA>
+__global__ void __launch_bounds__(256) k_dgemm(int m, int n, int kk, const double* __restrict__ A, int lda,
+                                               const double* __restrict__ Bm, int ldb, double* __restrict__ C,
+                                               int ldc, double alpha, const double* __restrict__ C0, int ldc0) {
+    pdl_begin();
+    __shared__ double As[16][64 + 1], Bs[16][64 + 1];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int i0 = blockIdx.y * 64, j0 = blockIdx.x * 64;
+    double acc[4][4] = {};
+    for (int k0 = 0; k0 < kk; k0 += 16) {
+        for (int x = threadIdx.x; x < 16 * 64; x += 256) {
+            const int kq = x / 64, ii = x % 64;  // As[kq][ii] = op(A)[i0+ii][k0+kq]
+            const int gi = i0 + ii, gk = k0 + kq;
+            double v = 0.0;
+            if (gi < m && gk < kk) v = TA ? A[(size_t)gk * lda + gi] : A[(size_t)gi * lda + gk];
+            As[kq][ii] = v;
+            const int gj = j0 + ii;  // Bs[kq][jj] = B[k0+kq][j0+jj]
+            Bs[kq][ii] = (gj < n && gk < kk) ? Bm[(size_t)gk * ldb + gj] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kq = 0; kq < 16; ++kq) {
+            double a[4], b[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                a[q] = As[kq][ty + 16 * q];
+                b[q] = Bs[kq][tx + 16 * q];
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int r = 0; r < 4; ++r) acc[q][r] = fma(a[q], b[r], acc[q][r]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int gi = i0 + ty + 16 * q, gj = j0 + tx + 16 * r;
+            if (gi < m && gj < n) {
+                double v = alpha * acc[q][r];
+                if (C0) v += C0[(size_t)gi * ldc0 + gj];
+                C[(size_t)gi * ldc + gj] = v;
+            }
+        }
+}
+
+// D_j and E_j (= K[block j, block j+1]) from the CSR of K.
+__global__ void k_bt_scatter(const int* __restrict__ kptr, const int* __restrict__ kcol, const double* __restrict__ kval,
+                             int n, const int* __restrict__ blk, const int* __restrict__ loc,
+                             const long long* __restrict__ doff, const long long* __restrict__ eoff,
+                             const int* __restrict__ bsz, double* __restrict__ D, double* __restrict__ E) {
+    pdl_begin();
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const int j = blk[r], lr = loc[r];
+    for (int z = kptr[r]; z < kptr[r + 1]; ++z) {
+        const int c = kcol[z], jc = blk[c], lc = loc[c];
+        if (jc == j) D[doff[j] + (long long)lr * bsz[j] + lc] = kval[z];
+        else if (jc == j + 1) E[eoff[j] + (long long)lr * bsz[j + 1] + lc] = kval[z];
+    }
+}
+
+// out[cols x rows] = in[rows x cols]^T
+__global__ void k_transpose(const double* __restrict__ in, int rows, int cols, double* __restrict__ out) {
+    pdl_begin();
+    __shared__ double t[32][33];
+    const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+    for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+        const int r = by + y, cc = bx + threadIdx.x;
+        t[y][threadIdx.x] = (r < rows && cc < cols) ? in[(size_t)r * cols + cc] : 0.0;
+    }
+    __syncthreads();
+    for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+        const int cc = bx + y, r = by + threadIdx.x;
+        if (cc < cols && r < rows) out[(size_t)cc * rows + r] = t[threadIdx.x][y];
+    }
+}
+
+__global__ void k_flag_err(const int* flag, Scalars* sc, unsigned bit) {
+    pdl_begin();
+    if (*flag) atomicOr(&sc->err, bit);
+}
+
+// y (block order) <- J rhs gathered: y[off[blk[r]] + loc[r]] = (J rhs)_r
+__global__ void k_bt_gather(const double* __restrict__ rhs, int n, const int* __restrict__ blk,
+                            const int* __restrict__ loc, const int* __restrict__ voff, double* __restrict__ y) {
+    pdl_begin();
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const int h = n / 2;
+    const double v = r < h ? rhs[h + r] : -rhs[r - h];
+    y[voff[blk[r]] + loc[r]] = v;
+}
+
+__global__ void k_bt_unpermute(const double* __restrict__ xb, int n, const int* __restrict__ blk,
+                               const int* __restrict__ loc, const int* __restrict__ voff, double* __restrict__ x) {
+    pdl_begin();
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    x[r] = xb[voff[blk[r]] + loc[r]];
+}
+
+// y_j -= G y_{j-1} (G = T_{j-1}^T, rows x cols), one warp per row
+__global__ void k_bt_fwd(const double* __restrict__ G, int rows, int cols, const double* __restrict__ yprev,
+                         double* __restrict__ y) {
+    pdl_begin();
+    const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    const double* g = G + (size_t)row * cols;
+    double acc = 0.0;
+    for (int c = lane; c < cols; c += 32) acc = fma(g[c], yprev[c], acc);
+    acc = warp_sum(acc);
+    if (lane == 0) y[row] -= acc;
+}
+
+// x_j = Sinv_j y_j - T_j x_{j+1} (T_j: rows x cols_next), one warp per row
+__global__ void k_bt_bwd(const double* __restrict__ Sinv, const double* __restrict__ T, int rows, int cols_next,
+                         const double* __restrict__ y, const double* __restrict__ xnext, double* __restrict__ x) {
+    pdl_begin();
+    const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    const double* s = Sinv + (size_t)row * rows;
+    double acc = 0.0;
+    for (int c = lane; c < rows; c += 32) acc = fma(s[c], y[c], acc);
+    if (T) {
+        const double* t = T + (size_t)row * cols_next;
+        for (int c = lane; c < cols_next; c += 32) acc = fma(-t[c], xnext[c], acc);
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) x[row] = acc;
+}
+
+}  // namespace
+
+// In-place inverse of an n x n row-major matrix (dense.cu).
+void block_gj_inplace_pub(Ctx& c, double* W, int n);
+
+void bt_setup(Ctx& c) {
+    const Layout& L = c.L;
+    const int n = c.dim, np = L.dim_flux;
+    auto block_of_iface = [&](int k) { return k < L.NV ? k / (L.nsx - 1) : (k - L.NV) / L.nsx; };
+    std::vector<int> blk(n), loc(n);
+    int nblk = 0;
+    for (int r = 0; r < n; ++r) {
+        blk[r] = block_of_iface(L.basis_iface(r % np));
+        nblk = std::max(nblk, blk[r] + 1);
+    }
+    std::vector<int> sz(nblk, 0);
+    for (int r = 0; r < n; ++r) loc[r] = sz[blk[r]]++;
+    std::vector<long long> doff(nblk + 1, 0), eoff(nblk + 1, 0);
+    std::vector<int> voff(nblk + 1, 0);
+    for (int j = 0; j < nblk; ++j) {
+        if (sz[j] == 0) throw ConfigError("block-tridiagonal interface solve: empty block");
+        doff[j + 1] = doff[j] + (long long)sz[j] * sz[j];
+        eoff[j + 1] = eoff[j] + (j + 1 < nblk ? (long long)sz[j] * sz[j + 1] : 0);
+        voff[j + 1] = voff[j] + sz[j];
+    }
+    c.bt_nblk = nblk;
+    c.bt_sz = sz;
+    c.bt_doff = doff;
+    c.bt_eoff = eoff;
+    c.bt_voff = voff;
+    auto up_i = [&](DevBuf<int>& d, const std::vector<int>& h) {
+        d.alloc(std::max<size_t>(h.size(), 1));
+        CK(cudaMemcpyAsync(d.p, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice, c.st));
+    };
+    up_i(c.bt_blk, blk);
+    up_i(c.bt_loc, loc);
+    up_i(c.bt_bsz, sz);
+    up_i(c.bt_voffd, voff);
+    c.bt_doffd.alloc(doff.size());
+    c.bt_eoffd.alloc(eoff.size());
+    CK(cudaMemcpyAsync(c.bt_doffd.p, doff.data(), doff.size() * sizeof(long long), cudaMemcpyHostToDevice, c.st));
+    CK(cudaMemcpyAsync(c.bt_eoffd.p, eoff.data(), eoff.size() * sizeof(long long), cudaMemcpyHostToDevice, c.st));
+    c.bt_D.alloc(doff[nblk]);
+    c.bt_Sinv.alloc(doff[nblk]);
+    c.bt_E.alloc(std::max<long long>(eoff[nblk], 1));
+    c.bt_T.alloc(std::max<long long>(eoff[nblk], 1));
+    c.bt_G.alloc(std::max<long long>(eoff[nblk], 1));
+    c.bt_y.alloc(n);
+    c.bt_x.alloc(n);
+    CK(cudaStreamSynchronize(c.st));
+}
+
+// Factorisation at every rebuild (after the CSR of K holds the new values).
+void bt_factor(Ctx& c) {
+    const int n = c.dim, nb = c.bt_nblk;
+    c.bt_D.zero(c.st);
+    c.bt_E.zero(c.st);
+    {
+        PROF(c, "k_bt_scatter");
+        launch_k(c, k_bt_scatter, cdiv(n, TPB), TPB, 0, c.k_ptr, c.k_col, c.k_val, n, c.bt_blk, c.bt_loc, c.bt_doffd,
+                 c.bt_eoffd, c.bt_bsz, c.bt_D, c.bt_E);
+        CK_LAUNCH();
+    }
+    auto gemm = [&](bool ta, int m, int nn, int kk, const double* A, int lda, const double* Bm, int ldb, double* C,
+                    int ldc, double alpha, const double* C0, int ldc0) {
+        PROF(c, "k_dgemm");
+        const dim3 g(cdiv(nn, 64), cdiv(m, 64));
+        if (ta) launch_k(c, k_dgemm<true>, g, 256, 0, m, nn, kk, A, lda, Bm, ldb, C, ldc, alpha, C0, ldc0);
+        else launch_k(c, k_dgemm<false>, g, 256, 0, m, nn, kk, A, lda, Bm, ldb, C, ldc, alpha, C0, ldc0);
+        CK_LAUNCH();
+    };
+    for (int j = 0; j < nb; ++j) {
+        const int s = c.bt_sz[j];
+        double* Sj = c.bt_Sinv.p + c.bt_doff[j];
+        const double* Dj = c.bt_D.p + c.bt_doff[j];
+        if (j == 0) {
+            CK(cudaMemcpyAsync(Sj, Dj, (size_t)s * s * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
+        } else {
+            const int sp = c.bt_sz[j - 1];
+            const double* Sp = c.bt_Sinv.p + c.bt_doff[j - 1];
+            const double* Ep = c.bt_E.p + c.bt_eoff[j - 1];  // sp x s
+            double* Tp = c.bt_T.p + c.bt_eoff[j - 1];         // sp x s
+            gemm(false, sp, s, sp, Sp, sp, Ep, s, Tp, s, 1.0, nullptr, 0);  // T = Sinv_{j-1} E_{j-1}
+            gemm(true, s, s, sp, Ep, s, Tp, s, Sj, s, -1.0, Dj, s);         // S_j = D_j - E^T T
+            {
+                PROF(c, "k_transpose");
+                launch_k(c, k_transpose, dim3(cdiv(s, 32), cdiv(sp, 32)), dim3(32, 8), 0, Tp, sp, s,
+                         c.bt_G.p + c.bt_eoff[j - 1]);  // G = T^T (s x sp)
+                CK_LAUNCH();
+            }
+        }
+        block_gj_inplace_pub(c, Sj, s);
+        {
+            PROF(c, "k_flag_err");
+            launch_k(c, k_flag_err, 1, 1, 0, c.gj_piv.p + s, c.sc.p, ERR_SINGULAR);
+            CK_LAUNCH();
+        }
+    }
+}
+
+// x = M^-1 rhs through K x = J rhs.
+void bt_solve(Ctx& c, const double* rhs, double* x) {
+    const int n = c.dim, nb = c.bt_nblk;
+    double* y = c.bt_y.p;
+    double* xb = c.bt_x.p;
+    {
+        PROF(c, "k_bt_gather");
+        launch_k(c, k_bt_gather, cdiv(n, TPB), TPB, 0, rhs, n, c.bt_blk, c.bt_loc, c.bt_voffd, y);
+        CK_LAUNCH();
+    }
+    for (int j = 1; j < nb; ++j) {
+        const int s = c.bt_sz[j], sp = c.bt_sz[j - 1];
+        PROF(c, "k_bt_fwd");
+        launch_k(c, k_bt_fwd, cdiv((long long)s * 32, TPB), TPB, 0, c.bt_G.p + c.bt_eoff[j - 1], s, sp,
+                 y + c.bt_voff[j - 1], y + c.bt_voff[j]);
+        CK_LAUNCH();
+    }
+    for (int j = nb - 1; j >= 0; --j) {
+        const int s = c.bt_sz[j];
+        const bool last = j == nb - 1;
+        const int sn = last ? 0 : c.bt_sz[j + 1];
+        PROF(c, "k_bt_bwd");
+        launch_k(c, k_bt_bwd, cdiv((long long)s * 32, TPB), TPB, 0, c.bt_Sinv.p + c.bt_doff[j],
+                 last ? nullptr : c.bt_T.p + c.bt_eoff[j], s, sn, y + c.bt_voff[j], last ? nullptr : xb + c.bt_voff[j + 1],
+                 xb + c.bt_voff[j]);
+        CK_LAUNCH();
+    }
+    {
+        PROF(c, "k_bt_unpermute");
+        launch_k(c, k_bt_unpermute, cdiv(n, TPB), TPB, 0, xb, n, c.bt_blk, c.bt_loc, c.bt_voffd, x);
+        CK_LAUNCH();
+    }
+}
+
+}  // namespace mpm2p

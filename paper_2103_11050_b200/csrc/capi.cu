@@ -157,7 +157,8 @@ void build_csr(Ctx& c) {
     CK(cudaMemcpyAsync(c.csr_ptr.p, ptr.data(), ptr.size() * sizeof(int), cudaMemcpyHostToDevice, c.st));
     if (!col.empty()) CK(cudaMemcpyAsync(c.csr_col.p, col.data(), col.size() * sizeof(int), cudaMemcpyHostToDevice, c.st));
     CK(cudaStreamSynchronize(c.st));
-    if (c.use_krylov) krylov_setup(c, ptr, col);
+    if (c.use_krylov || c.use_blocktri) krylov_setup(c, ptr, col);  // K = J M in CSR
+    if (c.use_blocktri) bt_setup(c);
 }
 
 // Grid, decomposition and interface-space sizes with the reference's
@@ -255,10 +256,19 @@ void create_ctx(mpm2p_ctx* ctx, const mpm2p_problem* P) {
     if (const char* e = std::getenv("MPM2P_GJ")) c.gj_legacy = std::strcmp(e, "legacy") == 0;
     if (const char* e = std::getenv("MPM2P_NO_TWIST")) c.no_twist = e[0] == '1';
     if (const char* e = std::getenv("MPM2P_PDL")) c.pdl = e[0] == '1';
-    c.use_krylov = c.dim > DENSE_IFACE_MAX;
+    // interface solver: dense inverse up to DENSE_IFACE_MAX, direct block-
+    // tridiagonal above; MPM2P_IFACE = dense | blocktri | krylov overrides
+    c.use_blocktri = c.dim > DENSE_IFACE_MAX;
+    c.use_krylov = false;
     if (const char* e = std::getenv("MPM2P_IFACE")) {
-        if (std::strcmp(e, "krylov") == 0) c.use_krylov = c.dim > 0;
-        else if (std::strcmp(e, "dense") == 0) c.use_krylov = false;
+        if (std::strcmp(e, "krylov") == 0) {
+            c.use_krylov = c.dim > 0;
+            c.use_blocktri = false;
+        } else if (std::strcmp(e, "blocktri") == 0) {
+            c.use_blocktri = c.dim > 0;
+        } else if (std::strcmp(e, "dense") == 0) {
+            c.use_blocktri = false;
+        }
     }
 
     int dev = 0;
@@ -308,7 +318,8 @@ void create_ctx(mpm2p_ctx* ctx, const mpm2p_problem* P) {
     c.bpm.alloc(ns * nbe);
     c.pmsum.alloc(ns);
     const size_t dim = std::max(1, c.dim);
-    if (c.dim > 0 && !c.use_krylov) c.Minv.alloc((size_t)c.dim * c.dim);  // dense M only on the pivoted fallback
+    if (c.dim > 0 && !c.use_krylov && !c.use_blocktri)
+        c.Minv.alloc((size_t)c.dim * c.dim);  // dense M only on the pivoted fallback
     c.irhs.alloc(dim);
     c.icoef.alloc(dim);
     c.ires.alloc(dim);
@@ -546,7 +557,7 @@ void run_end(mpm2p_ctx* ctx, mpm2p_run_record* out) {
     d.rec.final_pvi = c.sc_host->pvi;
     d.rec.min_eps_margin = c.sc_host->min_margin;
     d.rec.clamp_count = c.sc_host->clamp;
-    d.rec.interface_krylov = c.use_krylov ? 1 : 0;
+    d.rec.interface_krylov = c.use_krylov ? 1 : (c.use_blocktri ? 2 : 0);
     d.rec.interface_max_iterations = c.sc_host->kr_iters_max;
     d.rec.interface_iterations = c.sc_host->kr_iters_total;
     if (out) *out = d.rec;

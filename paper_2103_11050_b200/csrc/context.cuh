@@ -98,6 +98,15 @@ struct Ctx {
     int krylov_maxit = 20000;
     DevBuf<int> k_ptr, k_col;
     DevBuf<double> k_val, kr_pinv, kr_work;
+    // K7b direct block-tridiagonal interface solve (blocktri.cu): the default
+    // above the dense limit; MPM2P_IFACE=blocktri forces it, =krylov selects MINRES
+    bool use_blocktri = false;
+    int bt_nblk = 0;
+    std::vector<int> bt_sz, bt_voff;
+    std::vector<long long> bt_doff, bt_eoff;
+    DevBuf<int> bt_blk, bt_loc, bt_bsz, bt_voffd;
+    DevBuf<long long> bt_doffd, bt_eoffd;
+    DevBuf<double> bt_D, bt_E, bt_Sinv, bt_T, bt_G, bt_y, bt_x;
     // per-solve scratch
     DevBuf<double> X, PU, PB, PS, GZ, WU, RU, RS, skel, resid, delta, corr;
     // downscale
@@ -272,5 +281,10 @@ constexpr int DENSE_IFACE_MAX = 16384;  // above this the interface solve is MIN
 void krylov_setup(Ctx& c, const std::vector<int>& mptr, const std::vector<int>& mcol);
 void krylov_prepare(Ctx& c);                                  // after assembly
 void krylov_solve(Ctx& c, const double* rhs, double* x);      // x = M^-1 rhs
+
+// ---- launchers (blocktri.cu) ----------------------------------------------
+void bt_setup(Ctx& c);                                    // block layout and buffers (once)
+void bt_factor(Ctx& c);                                   // block LDL^T with explicit S_j^-1 (each rebuild)
+void bt_solve(Ctx& c, const double* rhs, double* x);      // x = M^-1 rhs
 
 }  // namespace mpm2p

@@ -982,6 +982,9 @@ void launch_rcond(Ctx& c, const double* A, const double* Ainv, int n, double* rc
 
 }  // namespace
 
+// Public entry for the block-tridiagonal solver (blocktri.cu).
+void block_gj_inplace_pub(Ctx& c, double* W, int n) { block_gj_inplace(c, W, n); }
+
 // Interface inverse from the CSR operator (dense path): K = J M built padded
 // into the ping-pong buffer, k_gj_pp, then M^-1 and the rcond guard. The
 // symmetry of K is checked once per context on the CSR values (host).

@@ -1440,6 +1440,10 @@ void interface_solve(Ctx& c) {
         krylov_solve(c, c.irhs, c.icoef);
         return;
     }
+    if (c.use_blocktri) {
+        bt_solve(c, c.irhs, c.icoef);
+        return;
+    }
     launch_gemv(c, c.Minv, c.irhs, c.icoef, c.dim);
     // one step of iterative refinement against the sparse operator
     for (int it = 0; it < 1; ++it) {
@@ -1552,6 +1556,10 @@ void launch_rebuild(Ctx& c, const double* kappa, bool compute_beta) {  // comput
             // no dense factorisation: the rcond guard becomes MINRES
             // non-convergence (ERR_SINGULAR raised by k_minres)
             krylov_prepare(c);
+        } else if (c.use_blocktri) {
+            // block LDL^T; a zero / non-finite pivot in any block raises ERR_SINGULAR
+            krylov_prepare(c);
+            bt_factor(c);
         } else if (c.gj_legacy || !interface_inverse_csr(c, &c.sc.p->rcond, ERR_SINGULAR, 1e-14)) {
             // legacy / non-symmetric fallback through a dense copy of M
             c.Mdense.alloc((size_t)c.dim * c.dim);

@@ -303,7 +303,8 @@ def test_krylov_matches_dense_c1_run():
 
 def test_c5_scale_properties():
     """C5 (128 x 128 subdomains, interface dim 65,024: beyond the dense path,
-    solved by MINRES) through size-independent properties: conservative
+    solved by the block-tridiagonal direct solver) through size-independent
+    properties: conservative
     velocities, saturation in [0, 1], the PVI clock advancing, counters of an
     Algorithm-1 run, and a zero-perturbation MPM update reproducing MRCM."""
     c = configs.build("C5", te_override=3)
@@ -311,7 +312,7 @@ def test_c5_scale_properties():
     assert g.dim == 65024
     r = g.run(c.split, c.s0())
     rec = r.record
-    assert rec.interface_krylov == 1 and rec.interface_max_iterations > 0
+    assert rec.interface_krylov == 2  # direct block-tridiagonal (the dense inverse would be 34 GB)
     assert rec.max_div_ratio <= 1e-9
     assert r.s_final.min() >= 0.0 and r.s_final.max() <= 1.0 and r.s_final.max() > 0.0
     assert rec.final_pvi > 0.0 and rec.te == 3
@@ -341,3 +342,45 @@ def test_repeated_rebuilds_bitwise_stable(oracle):
         assert np.isfinite(m.p).all()
     so = api.Simulator(prob, oracle).mrcm_solve(K)
     assert rel_l2(ref.p, so.p) <= TOL_PU and rel_l2(ref.u, so.u) <= TOL_PU
+
+
+# ---- K7b: direct block-tridiagonal interface solve (C5's default; forced here)
+
+def _sim_iface(prob, mode):
+    import os
+    os.environ["MPM2P_IFACE"] = mode
+    try:
+        return api.Simulator(prob)
+    finally:
+        os.environ.pop("MPM2P_IFACE", None)
+
+
+@pytest.mark.parametrize("nsx,nsy,space,hbar,contrast", [(4, 4, api.SPACE_CONSTANT, api.HBAR_WHOLE, 10.0),
+                                                         (4, 4, api.SPACE_LINEAR, api.HBAR_WHOLE, 10.0),
+                                                         (2, 4, api.SPACE_CONSTANT, api.HBAR_HALF, 100.0),
+                                                         (8, 8, api.SPACE_CONSTANT, api.HBAR_WHOLE, 1e3),
+                                                         (4, 1, api.SPACE_CONSTANT, api.HBAR_WHOLE, 10.0)])
+def test_blocktri_interface_parity(oracle, nsx, nsy, space, hbar, contrast):
+    """Block LDL^T of K = J M by subdomain rows vs the reference's LU."""
+    nx = ny = 32
+    K = random_kappa(nx, ny, 1, 1.0 / contrast, 1.0)
+    prob = problem(nx, ny, nsx, nsy, K, M=5.0, space=space, hbar=hbar)
+    g, o = _sim_iface(prob, "blocktri"), api.Simulator(prob, oracle)
+    sg, so = g.mrcm_solve(K), o.mrcm_solve(K)
+    assert sg.counters == so.counters
+    for a, b in ((sg.coeffs, so.coeffs), (sg.p, so.p), (sg.u, so.u)):
+        assert rel_l2(a, b) <= 1e-10
+    kn = K * np.exp(0.05 * np.random.default_rng(3).standard_normal(K.size))
+    mg, mo = g.mpm_pressure_update(kn), o.mpm_pressure_update(kn)
+    assert rel_l2(mg.p, mo.p) <= 1e-10 and rel_l2(mg.u, mo.u) <= 1e-10
+
+
+def test_blocktri_matches_dense_c2_sample():
+    """A C2 sample run with the block-tridiagonal solve vs the dense inverse."""
+    c = configs.build("C2", te_override=61)
+    rd = api.Simulator(c.problem).run(c.split, c.s0())
+    rb = _sim_iface(c.problem, "blocktri").run(c.split, c.s0())
+    assert rb.record.interface_krylov == 2
+    assert [s["rebuilt"] for s in rb.record.steps] == [s["rebuilt"] for s in rd.record.steps]
+    assert np.max(np.abs(rb.s_final - rd.s_final)) <= TOL_S
+    assert rel_l2(rb.p_final, rd.p_final) <= TOL_PU and rel_l2(rb.u_final, rd.u_final) <= TOL_PU
