@@ -1,9 +1,10 @@
-// band_twist.cuh — two-sided ("twisted") banded LDL^T on one warp, for
-// half-bandwidth B <= 16 (even).
+// band_twist.cuh — two-sided ("twisted") banded LDL^T of one subdomain
+// system, for even half-bandwidth B <= 32: on one warp (two half-warps of 16
+// lanes) for B <= 16, on a team of two warps (one per block) for B > 16.
 //
 // The register-window factorisation (band_reg.cuh) is a sequential chain of
-// n pivots and, for B <= 16, leaves lanes 16..31 idle. Here the two half-warps
-// run the same register-window step at once on two halves of the matrix:
+// n pivots. Here two halves (half-warps, or warps of a two-warp team) run the
+// same register-window step at once on two halves of the matrix:
 //   * the top half (lanes 0..15) eliminates rows 0 .. m-1 in natural order;
 //   * the bottom half (lanes 16..31) eliminates rows n-1 .. m+B in reverse
 //     order, i.e. the natural elimination of the reversed matrix
@@ -30,8 +31,16 @@
 namespace mpm2p {
 
 template <int B>
+__host__ __device__ constexpr bool twist_warps() {  // halves are whole warps (team of two per block)
+    return B > 16;
+}
+template <int B>
 __host__ __device__ constexpr int twist_ring() {  // chunks of stored factor in flight per half
-    return 4;
+    return B > 16 ? 2 : 4;
+}
+template <int B>
+__host__ __device__ constexpr int twist_threads() {
+    return twist_warps<B>() ? 64 : 32;
 }
 // shared memory per warp of the twisted kernels
 template <int B>
@@ -45,12 +54,14 @@ __host__ __device__ constexpr int twist_smem_doubles() {
 // Per-lane geometry of the two-sided scheme.
 template <int B>
 struct Twist {
+    static constexpr bool W = twist_warps<B>();
+    static constexpr int NL = W ? 32 : 16;  // lanes per half
     int n, rows, Ct, Cb, m, Ch, obase, h, ll, llc;
     bool act;
     __device__ Twist(int n_) : n(n_) {
         const int lane = threadIdx.x & 31;
-        h = lane >> 4;
-        ll = lane & 15;
+        h = W ? ((threadIdx.x >> 5) & 1) : (lane >> 4);
+        ll = W ? lane : (lane & 15);
         act = ll < B;
         llc = act ? ll : 0;
         rows = n / B;
@@ -61,6 +72,13 @@ struct Twist {
         obase = h ? m + B : 0;
     }
     __device__ int orig(int v) const { return h ? n - 1 - v : v; }  // virtual row -> natural row
+    __device__ int src(int u) const { return W ? u : (h << 4) + u; }  // shuffle source lane of row slot u
+    __device__ bool leader() const { return !W || h == 0; }           // the half that solves the middle block
+    __device__ void team_sync() const {
+        if (W) __syncthreads();  // one team per block
+        else __syncwarp();
+    }
+    __device__ bool team_all(bool v) const { return W ? (__syncthreads_and(v) != 0) : (__all_sync(FULL, v) != 0); }
 };
 
 // ---- phase 1: elimination ---------------------------------------------------
@@ -86,7 +104,7 @@ __device__ bool twist_eliminate(const Twist<B>& T, const BandRows A, double* D, 
         reg[t] = v;
     }
     yv = Y[T.orig(llc)];
-    for (int x = ll; x < B * B; x += 16) stage[x] = 0.0;
+    for (int x = ll; x < B * B; x += T.NL) stage[x] = 0.0;
     auto fetch = [&](int row, double& fd, double& fw, double& fs, double& fb) {
         const int rr = row < n ? row : n - 1;
         fd = vdiag(rr);
@@ -183,9 +201,9 @@ __device__ void twist_middle_assemble(const Twist<B>& T, const BandRows A, const
         for (int t = 0; t < B; ++t) W[T.ll * B + t] = reg[t];
         rhs[T.h * B + T.ll] = yv;
     }
-    __syncwarp();
+    T.team_sync();
     sr = 0.0;
-    if (lane < B) {
+    if (T.leader() && lane < B) {
         const int i = lane;
 #pragma unroll
         for (int jj = 0; jj < B; ++jj) {
@@ -269,7 +287,7 @@ __device__ void twist_backward(const Twist<B>& T, const double* D, const double*
         const int cc = c < 0 ? 0 : c;
         const double* g = Lrow + (size_t)(T.obase + cc * B) * B;
         double* dst = ring + (size_t)slot * B * B;
-        for (int p = ll; p < B * B / 2; p += 16) cp_async16(dst + 2 * p, g + 2 * p);
+        for (int p = ll; p < B * B / 2; p += T.NL) cp_async16(dst + 2 * p, g + 2 * p);
         cp_async_commit();
     };
 #pragma unroll
@@ -304,7 +322,7 @@ __device__ void twist_backward(const Twist<B>& T, const double* D, const double*
         for (int uu = B - 1; uu >= 0; --uu) {
             const int k = k0 + uu;
             const bool piv = ll == uu;
-            const double xk = __shfl_sync(FULL, z, (h << 4) + uu);
+            const double xk = __shfl_sync(FULL, z, T.src(uu));
             st_global_if(Y + T.orig(k), xk, piv && active);
             const bool reset = piv && active;
             const double keep = reset ? 0.0 : 1.0;
@@ -328,7 +346,7 @@ __device__ void twist_forward(const Twist<B>& T, const double* Lcol, double* Y, 
         const int cc = c < nch ? c : nch - 1;
         const double* g = Lcol + (size_t)(T.obase + cc * B) * B;
         double* dst = ring + (size_t)slot * B * B;
-        for (int p = ll; p < B * B / 2; p += 16) cp_async16(dst + 2 * p, g + 2 * p);
+        for (int p = ll; p < B * B / 2; p += T.NL) cp_async16(dst + 2 * p, g + 2 * p);
         cp_async_commit();
     };
 #pragma unroll
@@ -353,7 +371,7 @@ __device__ void twist_forward(const Twist<B>& T, const double* Lcol, double* Y, 
         for (int u = 0; u < B; ++u) {
             const int k = k0 + u;
             const bool piv = ll == u;
-            const double yk = __shfl_sync(FULL, yv, (h << 4) + u);
+            const double yk = __shfl_sync(FULL, yv, T.src(u));
             st_global_if(Y + T.orig(k), yk, piv && active);
             const bool reset = piv && active;
             const double keep = reset ? 0.0 : 1.0;
@@ -368,32 +386,43 @@ __device__ void twist_forward(const Twist<B>& T, const double* Lcol, double* Y, 
 }
 
 // ---- solvers built from the phases -------------------------------------------
+// Shared-memory carve-up of one team (twist_smem_doubles<B>() doubles).
+template <int B>
+struct TwistSmem {
+    double *stage, *xb, *ring, *mid;
+    __device__ TwistSmem(const Twist<B>& T, double* sm) {
+        constexpr int XB = xchg_doubles<B, 1>();
+        constexpr int RG = twist_ring<B>();
+        stage = sm + T.h * B * B;
+        xb = sm + 2 * B * B + T.h * XB;
+        ring = sm + 2 * B * B + 2 * XB + T.h * RG * B * B;
+        mid = sm + 2 * B * B + 2 * XB + 2 * RG * B * B;
+    }
+};
+
 // Fresh operator, one RHS (the downscale): x in Y; D / Lrow used as scratch.
 template <int B>
 __device__ bool twisted_solve(int n, const BandRows A, double* D, double* Lrow, double* Y, double* sm) {
-    static_assert(B <= 16 && B % 2 == 0, "two half-warps of B lanes");
-    constexpr int XB = xchg_doubles<B, 1>();
-    constexpr int RG = twist_ring<B>();
+    static_assert(B <= 32 && B % 2 == 0, "two halves of B lanes");
     const Twist<B> T(n);
-    double* stage = sm + T.h * B * B;
-    double* xb = sm + 2 * B * B + T.h * XB;
-    double* ring = sm + 2 * B * B + 2 * XB + T.h * RG * B * B;
-    double* mid = sm + 2 * B * B + 2 * XB + 2 * RG * B * B;
+    const TwistSmem<B> S(T, sm);
     double reg[B], yv;
-    bool ok = twist_eliminate<B, false>(T, A, D, nullptr, Lrow, Y, stage, xb, reg, yv);
+    bool ok = twist_eliminate<B, false>(T, A, D, nullptr, Lrow, Y, S.stage, S.xb, reg, yv);
     double srow[B], sr;
-    twist_middle_assemble<B>(T, A, Y, reg, yv, mid, srow, sr);
-    ok = twist_middle_gj<B, false>(srow, sr, mid) && ok;
-    double* xm = mid + 2 * B * B + 2 * B;
+    twist_middle_assemble<B>(T, A, Y, reg, yv, S.mid, srow, sr);
+    double* xm = S.mid + 2 * B * B + 2 * B;
     const int lane = threadIdx.x & 31;
-    if (lane < B) {
-        xm[lane] = sr;
-        Y[T.m + lane] = sr;
+    if (T.leader()) {
+        ok = twist_middle_gj<B, false>(srow, sr, S.mid) && ok;
+        if (lane < B) {
+            xm[lane] = sr;
+            Y[T.m + lane] = sr;
+        }
     }
-    __syncwarp();
-    const double* st = stage;  // this half's middle multipliers, Lrow layout
-    twist_backward<B>(T, D, Lrow, Y, xm, ring, [&](int i, int o) { return st[i * B + o]; });
-    return __all_sync(FULL, ok);
+    T.team_sync();
+    const double* st = S.stage;  // this half's middle multipliers, Lrow layout
+    twist_backward<B>(T, D, Lrow, Y, xm, S.ring, [&](int i, int o) { return st[i * B + o]; });
+    return T.team_all(ok);
 }
 
 // Rebuild factor: stores the twisted factor (D, Lcol, Lrow, the bottom's
@@ -401,35 +430,32 @@ __device__ bool twisted_solve(int n, const BandRows A, double* D, double* Lrow, 
 template <int B>
 __device__ bool twisted_factor(int n, const BandRows A, double* D, double* Lcol, double* Lrow, double* MidB,
                                double* Sinv, double* Y, double* sm) {
-    static_assert(B <= 16 && B % 2 == 0, "two half-warps of B lanes");
-    constexpr int XB = xchg_doubles<B, 1>();
-    constexpr int RG = twist_ring<B>();
+    static_assert(B <= 32 && B % 2 == 0, "two halves of B lanes");
     const Twist<B> T(n);
-    double* stage = sm + T.h * B * B;
-    double* xb = sm + 2 * B * B + T.h * XB;
-    double* ring = sm + 2 * B * B + 2 * XB + T.h * RG * B * B;
-    double* mid = sm + 2 * B * B + 2 * XB + 2 * RG * B * B;
+    const TwistSmem<B> S(T, sm);
     double reg[B], yv;
-    bool ok = twist_eliminate<B, true>(T, A, D, Lcol, Lrow, Y, stage, xb, reg, yv);
+    bool ok = twist_eliminate<B, true>(T, A, D, Lcol, Lrow, Y, S.stage, S.xb, reg, yv);
     {  // middle multipliers of each side: top as Lrow rows [m, m+B), bottom in MidB
         double* dst = T.h ? MidB : Lrow + (size_t)T.m * B;
-        for (int x = T.ll; x < B * B; x += 16) dst[x] = stage[x];
+        for (int x = T.ll; x < B * B; x += T.NL) dst[x] = S.stage[x];
     }
     double srow[B], sr;
-    twist_middle_assemble<B>(T, A, Y, reg, yv, mid, srow, sr);
-    ok = twist_middle_gj<B, true>(srow, sr, mid) && ok;
-    double* xm = mid + 2 * B * B + 2 * B;
+    twist_middle_assemble<B>(T, A, Y, reg, yv, S.mid, srow, sr);
+    double* xm = S.mid + 2 * B * B + 2 * B;
     const int lane = threadIdx.x & 31;
-    if (lane < B) {
+    if (T.leader()) {
+        ok = twist_middle_gj<B, true>(srow, sr, S.mid) && ok;
+        if (lane < B) {
 #pragma unroll
-        for (int jj = 0; jj < B; ++jj) Sinv[lane * B + jj] = srow[jj];
-        xm[lane] = sr;
-        Y[T.m + lane] = sr;
+            for (int jj = 0; jj < B; ++jj) Sinv[lane * B + jj] = srow[jj];
+            xm[lane] = sr;
+            Y[T.m + lane] = sr;
+        }
     }
-    __syncwarp();
-    const double* st = stage;
-    twist_backward<B>(T, D, Lrow, Y, xm, ring, [&](int i, int o) { return st[i * B + o]; });
-    return __all_sync(FULL, ok);
+    T.team_sync();
+    const double* st = S.stage;
+    twist_backward<B>(T, D, Lrow, Y, xm, S.ring, [&](int i, int o) { return st[i * B + o]; });
+    return T.team_all(ok);
 }
 
 // Solve with a stored twisted factor (rebuild's homogeneous RHS, MPM-2P's
@@ -437,28 +463,26 @@ __device__ bool twisted_factor(int n, const BandRows A, double* D, double* Lcol,
 template <int B>
 __device__ void twisted_sweep(int n, const double* D, const double* Lcol, const double* Lrow, const double* MidB,
                               const double* Sinv, double* Y, double* sm) {
-    constexpr int XB = xchg_doubles<B, 1>();
-    constexpr int RG = twist_ring<B>();
     const Twist<B> T(n);
-    double* ring = sm + 2 * B * B + 2 * XB + T.h * RG * B * B;
-    double* mid = sm + 2 * B * B + 2 * XB + 2 * RG * B * B;
+    const TwistSmem<B> S(T, sm);
     double yv;
-    twist_forward<B>(T, Lcol, Y, ring, yv);
-    double* rhs = mid + 2 * B * B;  // [2][B]
+    twist_forward<B>(T, Lcol, Y, S.ring, yv);
+    double* rhs = S.mid + 2 * B * B;  // [2][B]
     double* xm = rhs + 2 * B;
     if (T.act) rhs[T.h * B + T.ll] = yv;
-    __syncwarp();
+    T.team_sync();
     const int lane = threadIdx.x & 31;
-    if (lane < B) {
+    if (T.leader() && lane < B) {
         double x = 0.0;
 #pragma unroll
         for (int jj = 0; jj < B; ++jj) x = fma(Sinv[lane * B + jj], rhs[jj] + rhs[B + B - 1 - jj] - Y[T.m + jj], x);
         xm[lane] = x;
     }
-    __syncwarp();
-    if (lane < B) Y[T.m + lane] = xm[lane];
+    T.team_sync();
+    if (T.leader() && lane < B) Y[T.m + lane] = xm[lane];
     const double* mids = T.h ? MidB : Lrow + (size_t)T.m * B;
-    twist_backward<B>(T, D, Lrow, Y, xm, ring, [&](int i, int o) { return mids[i * B + o]; });
+    twist_backward<B>(T, D, Lrow, Y, xm, S.ring, [&](int i, int o) { return mids[i * B + o]; });
+    T.team_sync();
 }
 
 }  // namespace mpm2p

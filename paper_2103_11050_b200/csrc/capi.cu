@@ -343,8 +343,13 @@ void create_ctx(mpm2p_ctx* ctx, const mpm2p_problem* P) {
     c.Lrd.alloc(ns * ncs * B);
     c.Xd.alloc(ns * ncs);
     // two-sided band solves: even widths <= 16 with at least 3 rows of cells
-    c.twist_store = !c.no_regband && !c.no_twist && L.sny >= 3 && L.snx <= 16 && L.snx % 2 == 0 && L.snx != 2 &&
-                    L.snx != 6 && L.snx != 14;
+    // two-sided solves pay off where the local solves are latency-bound (few
+    // subdomains per SM); with many subdomains the one-warp kernels keep
+    // higher occupancy (C5: 16,384 subdomains)
+    c.twist_ok = !c.no_regband && !c.no_twist && L.sny >= 3 && L.n_sub <= 8 * c.num_sms;
+    c.twist_store = c.twist_ok &&
+                    (L.snx == 4 || L.snx == 8 || L.snx == 10 || L.snx == 12 || L.snx == 16 || L.snx == 20 ||
+                     L.snx == 24 || L.snx == 32);
     if (c.twist_store) {
         c.tw_midb.alloc(ns * B * B);
         c.tw_sinv.alloc(ns * B * B);

@@ -894,26 +894,41 @@ __global__ void __launch_bounds__(WPB * 32) k_hom_solve_r(Layout L, int max_rhs,
     backward_reg<B, 1>(n, D + so, Lr + so * B, x, 1, n, nullptr, ring[w]);
 }
 
-// Downscale solve with the two-sided elimination (band_twist.cuh): the two
-// half-warps factor from both ends, so the dependent chain is ~half as long.
-constexpr int WPBT = 1;  // warps per block (shared memory: ~25 KB per warp at B = 16)
+// Two-sided band kernels (band_twist.cuh): one team per block — one warp
+// (two half-warps) for B <= 16, two warps for B > 16 — dynamic shared memory
+// twist_smem_doubles<B>() doubles.
 template <int B>
-__global__ void __launch_bounds__(WPBT * 32) k_ds_solve_t(Layout L, const double* __restrict__ BD,
-                                                          const double* __restrict__ BW, const double* __restrict__ BS,
-                                                          double* D, double* Lr, double* Xd,
-                                                          const double* __restrict__ RS, double* p, Scalars* sc) {
+constexpr size_t twist_smem_bytes() {  // dynamic part (two-warp teams only)
+    return twist_warps<B>() ? (size_t)twist_smem_doubles<B>() * sizeof(double) : 0;
+}
+
+// Downscale solve with the two-sided elimination: the two halves factor from
+// both ends, so the dependent chain is ~half as long.
+template <int B>
+__global__ void __launch_bounds__(twist_threads<B>()) k_ds_solve_t(Layout L, const double* __restrict__ BD,
+                                                                   const double* __restrict__ BW,
+                                                                   const double* __restrict__ BS, double* D, double* Lr,
+                                                                   double* Xd, const double* __restrict__ RS,
+                                                                   double* p, Scalars* sc) {
     pdl_begin();
-    __shared__ __align__(16) double sm[WPBT][twist_smem_doubles<B>()];
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int s = blockIdx.x * WPBT + w;
+    double* tsm;  // static shared memory for one-warp teams (faster code), dynamic for two-warp teams
+    if constexpr (twist_warps<B>()) {
+        extern __shared__ __align__(16) double tsm_dyn[];
+        tsm = tsm_dyn;
+    } else {
+        __shared__ __align__(16) double tsm_st[twist_smem_doubles<B>()];
+        tsm = tsm_st;
+    }
+    const int lane = threadIdx.x & 31;
+    const int s = blockIdx.x;
     if (s >= L.n_sub) return;
     const int n = L.ncs;
     const size_t so = (size_t)s * n;
     const BandRows A{BD + so, BW + so, BS + so};
     double* x = Xd + so;
-    const bool ok = twisted_solve<B>(n, A, D + so, Lr + so * B, x, sm[w]);
+    const bool ok = twisted_solve<B>(n, A, D + so, Lr + so * B, x, tsm);
+    if (threadIdx.x >= 32) return;  // epilogue on warp 0
     if (!ok && lane == 0) atomicOr(&sc->err, ERR_PIVOT);
-    __syncwarp();
     // mean shift (mrcm.cpp:430-437): all loads of x first, then the scatter
     constexpr int PER = 8;
     double v = 0.0;
@@ -944,71 +959,90 @@ __global__ void __launch_bounds__(WPBT * 32) k_ds_solve_t(Layout L, const double
         }
     }
 }
-#define MPM2P_TWIST_WIDTHS(X) X(4) X(8) X(10) X(12) X(16)
+#define MPM2P_TWIST_WIDTHS(X) X(4) X(8) X(10) X(12) X(16) X(20) X(24) X(32)
 
 // Rebuild with the two-sided scheme: the factor (twisted layout + the middle
 // block's S^-1 and bottom multipliers) and the particular solve...
 template <int B>
-__global__ void __launch_bounds__(WPBT * 32) k_factor1_t(Layout L, int max_rhs, const double* __restrict__ BD,
-                                                         const double* __restrict__ BW, const double* __restrict__ BS,
-                                                         double* D, double* Lc, double* Lr, double* MidB, double* Sinv,
-                                                         double* X, Scalars* sc) {
+__global__ void __launch_bounds__(twist_threads<B>()) k_factor1_t(Layout L, int max_rhs, const double* __restrict__ BD,
+                                                                  const double* __restrict__ BW,
+                                                                  const double* __restrict__ BS, double* D, double* Lc,
+                                                                  double* Lr, double* MidB, double* Sinv, double* X,
+                                                                  Scalars* sc) {
     pdl_begin();
-    __shared__ __align__(16) double sm[WPBT][twist_smem_doubles<B>()];
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int s = blockIdx.x * WPBT + w;
+    double* tsm;  // static shared memory for one-warp teams (faster code), dynamic for two-warp teams
+    if constexpr (twist_warps<B>()) {
+        extern __shared__ __align__(16) double tsm_dyn[];
+        tsm = tsm_dyn;
+    } else {
+        __shared__ __align__(16) double tsm_st[twist_smem_doubles<B>()];
+        tsm = tsm_st;
+    }
+    const int s = blockIdx.x;
     if (s >= L.n_sub) return;
     const int n = L.ncs;
     const size_t so = (size_t)s * n;
     const BandRows A{BD + so, BW + so, BS + so};
     const bool ok = twisted_factor<B>(n, A, D + so, Lc + so * B, Lr + so * B, MidB + (size_t)s * B * B,
-                                      Sinv + (size_t)s * B * B, X + xoff(L, max_rhs, s, 0), sm[w]);
-    if (!ok && lane == 0) atomicOr(&sc->err, ERR_PIVOT);
+                                      Sinv + (size_t)s * B * B, X + xoff(L, max_rhs, s, 0), tsm);
+    if (!ok && threadIdx.x == 0) atomicOr(&sc->err, ERR_PIVOT);
 }
 
-// ... then one warp per (subdomain, homogeneous function) with the stored factor.
+// ... then one team per (subdomain, homogeneous function) with the stored factor.
 template <int B>
-__global__ void __launch_bounds__(WPBT * 32) k_hom_solve_t(Layout L, int max_rhs, const double* __restrict__ D,
-                                                           const double* __restrict__ Lc,
-                                                           const double* __restrict__ Lr,
-                                                           const double* __restrict__ MidB,
-                                                           const double* __restrict__ Sinv, double* X) {
+__global__ void __launch_bounds__(twist_threads<B>()) k_hom_solve_t(Layout L, int max_rhs, const double* __restrict__ D,
+                                                                    const double* __restrict__ Lc,
+                                                                    const double* __restrict__ Lr,
+                                                                    const double* __restrict__ MidB,
+                                                                    const double* __restrict__ Sinv, double* X) {
     pdl_begin();
-    __shared__ __align__(16) double sm[WPBT][twist_smem_doubles<B>()];
-    const int w = threadIdx.x >> 5;
-    const int gw = blockIdx.x * WPBT + w;
+    double* tsm;  // static shared memory for one-warp teams (faster code), dynamic for two-warp teams
+    if constexpr (twist_warps<B>()) {
+        extern __shared__ __align__(16) double tsm_dyn[];
+        tsm = tsm_dyn;
+    } else {
+        __shared__ __align__(16) double tsm_st[twist_smem_doubles<B>()];
+        tsm = tsm_st;
+    }
+    const int gw = blockIdx.x;
     const int s = gw / L.max_hom, h = gw % L.max_hom;
     if (s >= L.n_sub || h >= L.n_hom(s)) return;
     const int n = L.ncs;
     const size_t so = (size_t)s * n;
     twisted_sweep<B>(n, D + so, Lc + so * B, Lr + so * B, MidB + (size_t)s * B * B, Sinv + (size_t)s * B * B,
-                     X + xoff(L, max_rhs, s, 1 + h), sm[w]);
+                     X + xoff(L, max_rhs, s, 1 + h), tsm);
 }
 
 // MPM-2P particular solve with the stored two-sided factor + traces + psum.
 template <int B>
-__global__ void __launch_bounds__(WPBT * 32) k_part_solve_t(Layout L, int max_rhs, const double* __restrict__ D,
-                                                            const double* __restrict__ Lc,
-                                                            const double* __restrict__ Lr,
-                                                            const double* __restrict__ MidB,
-                                                            const double* __restrict__ Sinv, double* X,
-                                                            const double* __restrict__ km,
-                                                            const int* __restrict__ bc_kind,
-                                                            const double* __restrict__ bm,
-                                                            const double* __restrict__ bp,
-                                                            const double* __restrict__ GZ, double* __restrict__ PU,
-                                                            double* __restrict__ PS) {
+__global__ void __launch_bounds__(twist_threads<B>()) k_part_solve_t(Layout L, int max_rhs, const double* __restrict__ D,
+                                                                     const double* __restrict__ Lc,
+                                                                     const double* __restrict__ Lr,
+                                                                     const double* __restrict__ MidB,
+                                                                     const double* __restrict__ Sinv, double* X,
+                                                                     const double* __restrict__ km,
+                                                                     const int* __restrict__ bc_kind,
+                                                                     const double* __restrict__ bm,
+                                                                     const double* __restrict__ bp,
+                                                                     const double* __restrict__ GZ,
+                                                                     double* __restrict__ PU, double* __restrict__ PS) {
     pdl_begin();
-    __shared__ __align__(16) double sm[WPBT][twist_smem_doubles<B>()];
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int s = blockIdx.x * WPBT + w;
+    double* tsm;  // static shared memory for one-warp teams (faster code), dynamic for two-warp teams
+    if constexpr (twist_warps<B>()) {
+        extern __shared__ __align__(16) double tsm_dyn[];
+        tsm = tsm_dyn;
+    } else {
+        __shared__ __align__(16) double tsm_st[twist_smem_doubles<B>()];
+        tsm = tsm_st;
+    }
+    const int lane = threadIdx.x & 31;
+    const int s = blockIdx.x;
     if (s >= L.n_sub) return;
     const int n = L.ncs;
     const size_t so = (size_t)s * n;
     double* x = X + xoff(L, max_rhs, s, 0);
-    twisted_sweep<B>(n, D + so, Lc + so * B, Lr + so * B, MidB + (size_t)s * B * B, Sinv + (size_t)s * B * B, x,
-                     sm[w]);
-    __syncwarp();
+    twisted_sweep<B>(n, D + so, Lc + so * B, Lr + so * B, MidB + (size_t)s * B * B, Sinv + (size_t)s * B * B, x, tsm);
+    if (threadIdx.x >= 32) return;  // epilogue on warp 0
     for (int idx = lane; idx < L.nbe; idx += 32) {
         const EdgeInfo e = L.edge(s, idx);
         PU[(size_t)s * L.nbe + idx] = part_trace(L, s, idx, x[e.local_cell], km, bc_kind, bm, bp, GZ);
@@ -1017,6 +1051,19 @@ __global__ void __launch_bounds__(WPBT * 32) k_part_solve_t(Layout L, int max_rh
     for (int r = lane; r < n; r += 32) v += x[r];
     v = warp_sum(v);
     if (lane == 0) PS[s] = v;
+}
+
+// Dynamic shared memory opt-in for each instantiation (once, outside capture).
+template <int B>
+void twist_configure() {
+    static bool done = false;
+    if (done || !twist_warps<B>()) return;
+    const int bytes = (int)twist_smem_bytes<B>();
+    CK(cudaFuncSetAttribute(k_ds_solve_t<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    CK(cudaFuncSetAttribute(k_factor1_t<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    CK(cudaFuncSetAttribute(k_hom_solve_t<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    CK(cudaFuncSetAttribute(k_part_solve_t<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    done = true;
 }
 
 // Subdomain widths with a register-window instantiation; others use band.cuh.
@@ -1379,14 +1426,15 @@ void downscale(Ctx& c, const double* kappa) {
         CK_LAUNCH();
     }
     const size_t sm1 = (size_t)WPB * band_smem_doubles(L.snx, 1) * sizeof(double);
-    const bool twist = !c.no_regband && !c.no_twist && L.sny >= 3;
+    const bool twist = c.twist_ok;
     bool done = false;
     if (twist) {
         PROF(c, "k_ds_solve");
         switch (L.snx) {
 #define X(BW_)                                                                                                  \
     case BW_:                                                                                                   \
-        launch_k(c, k_ds_solve_t<BW_>, cdiv(L.n_sub, WPBT), WPBT * 32, 0, L, c.BDd, c.BWd, c.BSd, c.Dd, c.Lrd, c.Xd, \
+        twist_configure<BW_>();                                                                                 \
+        launch_k(c, k_ds_solve_t<BW_>, L.n_sub, twist_threads<BW_>(), twist_smem_bytes<BW_>(), L, c.BDd, c.BWd, c.BSd, c.Dd, c.Lrd, c.Xd, \
                                                                        c.RS, c.p, c.sc);                        \
         done = true;                                                                                            \
         break;
@@ -1483,7 +1531,8 @@ void launch_rebuild(Ctx& c, const double* kappa, bool compute_beta) {  // comput
             switch (L.snx) {
 #define X(BW_)                                                                                                  \
     case BW_:                                                                                                   \
-        launch_k(c, k_factor1_t<BW_>, cdiv(L.n_sub, WPBT), WPBT * 32, 0, L, c.max_rhs, c.BDm, c.BWm, c.BSm, c.Dm,   \
+        twist_configure<BW_>();                                                                                 \
+        launch_k(c, k_factor1_t<BW_>, L.n_sub, twist_threads<BW_>(), twist_smem_bytes<BW_>(), L, c.max_rhs, c.BDm, c.BWm, c.BSm, c.Dm,   \
                                                                       c.Lcm, c.Lrm, c.tw_midb, c.tw_sinv, c.X, \
                                                                       c.sc);                                   \
         break;
@@ -1499,7 +1548,7 @@ void launch_rebuild(Ctx& c, const double* kappa, bool compute_beta) {  // comput
             switch (L.snx) {
 #define X(BW_)                                                                                                  \
     case BW_:                                                                                                   \
-        launch_k(c, k_hom_solve_t<BW_>, cdiv((long long)L.n_sub * L.max_hom, WPBT), WPBT * 32, 0,                  \
+        launch_k(c, k_hom_solve_t<BW_>, L.n_sub * L.max_hom, twist_threads<BW_>(), twist_smem_bytes<BW_>(),    \
             L, c.max_rhs, c.Dm, c.Lcm, c.Lrm, c.tw_midb, c.tw_sinv, c.X);                                       \
         break;
                 MPM2P_TWIST_WIDTHS(X)
@@ -1616,7 +1665,7 @@ void launch_mpm(Ctx& c, const double* kn) {  // mpm_pressure_update (mpm.cpp:31-
         switch (L.snx) {
 #define X(BW_)                                                                                                  \
     case BW_:                                                                                                   \
-        launch_k(c, k_part_solve_t<BW_>, cdiv(L.n_sub, WPBT), WPBT * 32, 0,                                        \
+        launch_k(c, k_part_solve_t<BW_>, L.n_sub, twist_threads<BW_>(), twist_smem_bytes<BW_>(),                  \
             L, c.max_rhs, c.Dm, c.Lcm, c.Lrm, c.tw_midb, c.tw_sinv, c.X, c.kappa_m, c.bc_kind, c.beta_m,        \
             c.beta_p, c.GZ, c.PU, c.PS);                                                                        \
         break;

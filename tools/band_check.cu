@@ -45,26 +45,27 @@ __global__ void k_check4(int n, const double* BD, const double* BW, const double
 }
 
 // Twisted (two-sided) solve, WARPS independent copies per block.
+// one team per block (blockIdx = copy index), dynamic shared memory
 template <int B, int WARPS>
 __global__ void k_twist(int n, const double* BD, const double* BW, const double* BS, double* D, double* Lr,
                         double* Y, double* Yv, int* okf) {
-    __shared__ __align__(16) double sm[WARPS][twist_smem_doubles<B>()];
-    const int w = threadIdx.x >> 5;
+    extern __shared__ __align__(16) double sm[];
+    const int w = blockIdx.x;
     const BandRows A{BD, BW, BS};
-    const bool ok = twisted_solve<B>(n, A, D + w * n, Lr + (size_t)w * n * B, Y + (size_t)w * n, sm[w]);
-    if ((threadIdx.x & 31) == 0) okf[w] = ok;
+    const bool ok = twisted_solve<B>(n, A, D + w * n, Lr + (size_t)w * n * B, Y + (size_t)w * n, sm);
+    if (threadIdx.x == 0) okf[w] = ok;
 }
 
 // Stored two-sided factor: factor with RHS Y (solved in place), then solve Y2 with the stored factor.
 template <int B>
 __global__ void k_twist_fs(int n, const double* BD, const double* BW, const double* BS, double* D, double* Lc,
                            double* Lr, double* MidB, double* Sinv, double* Y, double* Y2, int* okf) {
-    __shared__ __align__(16) double sm[twist_smem_doubles<B>()];
+    extern __shared__ __align__(16) double sm[];
     const BandRows A{BD, BW, BS};
     const bool ok = twisted_factor<B>(n, A, D, Lc, Lr, MidB, Sinv, Y, sm);
-    __syncwarp();
+    __syncthreads();
     twisted_sweep<B>(n, D, Lc, Lr, MidB, Sinv, Y2, sm);
-    if ((threadIdx.x & 31) == 0) okf[0] = ok;
+    if (threadIdx.x == 0) okf[0] = ok;
 }
 
 template <int B, int WARPS>
@@ -119,7 +120,10 @@ void run_twist(int m) {
     cudaMemcpy(dBW, bw.data(), n * 8, cudaMemcpyHostToDevice);
     cudaMemcpy(dBS, bs.data(), n * 8, cudaMemcpyHostToDevice);
     for (int w = 0; w < WARPS; ++w) cudaMemcpy(dY + (size_t)w * n, y.data(), n * 8, cudaMemcpyHostToDevice);
-    k_twist<B, WARPS><<<1, 32 * WARPS>>>(n, dBD, dBW, dBS, dD, dLr, dY, dYv, dok);
+    const int smb = twist_smem_doubles<B>() * 8;
+    cudaFuncSetAttribute(k_twist<B, WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smb);
+    cudaFuncSetAttribute(k_twist_fs<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, smb);
+    k_twist<B, WARPS><<<WARPS, twist_threads<B>(), smb>>>(n, dBD, dBW, dBS, dD, dLr, dY, dYv, dok);
     cudaError_t e = cudaDeviceSynchronize();
     {  // factor + stored sweep (RHS 2 = reversed RHS 1), single warp
         double *dLc, *dMid, *dS, *dY2;
@@ -130,7 +134,7 @@ void run_twist(int m) {
         std::vector<double> y2(y.rbegin(), y.rend());
         cudaMemcpy(dY, y.data(), n * 8, cudaMemcpyHostToDevice);
         cudaMemcpy(dY2, y2.data(), n * 8, cudaMemcpyHostToDevice);
-        k_twist_fs<B><<<1, 32>>>(n, dBD, dBW, dBS, dD, dLc, dLr, dMid, dS, dY, dY2, dok);
+        k_twist_fs<B><<<1, twist_threads<B>(), smb>>>(n, dBD, dBW, dBS, dD, dLc, dLr, dMid, dS, dY, dY2, dok);
         cudaError_t e2 = cudaDeviceSynchronize();
         std::vector<double> x1(n), x2g(n);
         cudaMemcpy(x1.data(), dY, n * 8, cudaMemcpyDeviceToHost);
@@ -304,6 +308,10 @@ int main() {
     run_twist<16, 1>(16);
     run_twist<16, 1>(15);
     run_twist<12, 2>(12);
+    run_twist<32, 1>(32);
+    run_twist<32, 1>(9);
+    run_twist<20, 1>(20);
+    run_twist<24, 1>(7);
     run_twist<16, 1>(3);
     run_twist<16, 1>(4);
     run_twist<8, 1>(8);
