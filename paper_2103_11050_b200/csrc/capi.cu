@@ -366,6 +366,20 @@ void create_ctx(mpm2p_ctx* ctx, const mpm2p_problem* P) {
     else c.q.zero(c.st);
     upload(c, c.bc_value, P->bc_value, nb);
     CK(cudaMemcpyAsync(c.bc_kind.p, P->bc_kind, nb * sizeof(int), cudaMemcpyHostToDevice, c.st));
+    if (L.max_hom > 0) {  // static (interface, basis, flux?, column) table of the homogeneous functions
+        std::vector<int4> tab((size_t)L.n_sub * L.max_hom, make_int4(0, 0, 0, 0));
+        for (int sd = 0; sd < L.n_sub; ++sd)
+            for (int h = 0; h < L.n_hom(sd); ++h) {
+                int k, t, col;
+                bool fl;
+                L.hom(sd, h, k, t, fl, col);
+                tab[(size_t)sd * L.max_hom + h] = make_int4(k, t, fl ? 1 : 0, col);
+            }
+        c.homtab.alloc(tab.size());
+        CK(cudaMemcpyAsync(c.homtab.p, tab.data(), tab.size() * sizeof(int4), cudaMemcpyHostToDevice, c.st));
+        CK(cudaStreamSynchronize(c.st));
+        c.L.homtab = c.homtab.p;
+    }
     if (c.dim > 0) build_csr(c);
     reset_scalars(c);
     launch_setup_static(c);

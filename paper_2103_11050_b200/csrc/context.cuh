@@ -73,6 +73,7 @@ struct Ctx {
 
     // static data
     DevBuf<double> K, q, bc_value, qsum_sub, ground, Linv;
+    DevBuf<int4> homtab;  // Layout::hom(s, h) for every (subdomain, homogeneous function)
     DevBuf<int> bc_kind;
     // transport / driver state
     DevBuf<double> s, s2, u, p, kappa_n, kappa_m, lam_reb, T;

@@ -53,6 +53,7 @@ struct Layout {
     int nbv, nbh;
     int dim_flux;    // == dim_pressure
     int max_hom;     // max homogeneous solves per subdomain
+    const int4* homtab = nullptr;  // device table of hom(s, h) (set once the context exists)
 
     HD int cells() const { return nx * ny; }
     HD int vcount() const { return (nx + 1) * ny; }
@@ -149,6 +150,16 @@ struct Layout {
     }
     // homogeneous solve h of subdomain s: interface, basis t on it, flux?, column
     HD void hom(int s, int h, int& k, int& t, bool& flux, int& col) const {
+#ifdef __CUDA_ARCH__
+        if (homtab) {  // precomputed (interface, basis, flux?, column) per (subdomain, function)
+            const int4 v = homtab[(size_t)s * max_hom + h];
+            k = v.x;
+            t = v.y;
+            flux = v.z != 0;
+            col = v.w;
+            return;
+        }
+#endif
         int inc[4];
         const int n = incident(s, inc);
         int half = 0;

@@ -203,27 +203,41 @@ __global__ void k_rebuild_rhs(Layout L, int max_rhs, const double* __restrict__ 
     int idx[4];
     const int ne = cell_edges(L, ii, jj, idx);
     EdgeInfo e[4];
-    for (int t = 0; t < ne; ++t) e[t] = L.edge(s, idx[t]);
-    const int nh = L.n_hom(s);
-    for (int m = 0; m <= nh; ++m) {
-        double b = (m == 0 ? q[c] : 0.0) * vol;
-        int hk = -1, ht = 0, hcol = 0;
-        bool hflux = false;
-        if (m > 0) L.hom(s, m - 1, hk, ht, hflux, hcol);
+    double th[4], beta[4], er[4];
+    for (int t = 0; t < ne; ++t) {
+        e[t] = L.edge(s, idx[t]);
+        th[t] = half_trans(L, e[t].side, kappa[c]);
+        beta[t] = e[t].iface >= 0 ? edge_beta(L, e[t], bm, bp) : 0.0;
+        er[t] = e[t].iface >= 0 ? eff_robin(th[t], beta[t], e[t].area) : 0.0;
+    }
+    // m = 0 (particular): interface edges contribute er * 0
+    {
+        double b = q[c] * vol;
         for (int t = 0; t < ne; ++t) {
-            const double th = half_trans(L, e[t].side, kappa[c]);
             if (e[t].iface >= 0) {
-                const double beta = edge_beta(L, e[t], bm, bp);
-                double rr = 0.0;
-                if (m > 0 && e[t].iface == hk) {
-                    const double v = L.basis_val(hk, ht, e[t].pos);
-                    rr = hflux ? -beta * v * e[t].sign : v;
-                }
-                b += eff_robin(th, beta, e[t].area) * rr;
+                b += er[t] * 0.0;
             } else {
-                const double val = m == 0 ? bc_value[e[t].gbc] : 0.0;
-                if (bc_kind[e[t].gbc] == BC_PRESSURE) b += th * val;
+                const double val = bc_value[e[t].gbc];
+                if (bc_kind[e[t].gbc] == BC_PRESSURE) b += th[t] * val;
                 else b -= val * e[t].area;
+            }
+        }
+        if (anchor && r == 0) b = 0.0;
+        X[xoff(L, max_rhs, s, 0) + r] = b;
+    }
+    // m > 0 (homogeneous): only edges on the function's interface are nonzero
+    // (the skipped terms are +-0 additions; the sums are bit-identical)
+    const int nh = L.n_hom(s);
+    for (int m = 1; m <= nh; ++m) {
+        int hk, ht, hcol;
+        bool hflux;
+        L.hom(s, m - 1, hk, ht, hflux, hcol);
+        double b = 0.0;
+        for (int t = 0; t < ne; ++t) {
+            if (e[t].iface == hk) {
+                const double v = L.basis_val(hk, ht, e[t].pos);
+                const double rr = hflux ? -beta[t] * v * e[t].sign : v;
+                b += er[t] * rr;
             }
         }
         if (anchor && r == 0) b = 0.0;
