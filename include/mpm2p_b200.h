@@ -129,6 +129,7 @@ typedef struct mpm2p_run_record {
      * inverse, 1 MINRES, 2 direct block-tridiagonal; MINRES iteration counts. */
     int32_t interface_krylov, interface_max_iterations;
     int64_t interface_iterations;
+    double min_rcond;  /* smallest interface-matrix rcond over the run's rebuilds (dense path; -1 otherwise) */
 } mpm2p_run_record;
 
 /* DownscaleResult diagnostics (mrcm.hpp:122-130). */

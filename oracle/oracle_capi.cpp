@@ -110,6 +110,7 @@ void fill_run(mpm2p_run_record* o, const RunRecord& r, int64_t clamps) {
     o->interface_krylov = 0;
     o->interface_max_iterations = 0;
     o->interface_iterations = 0;
+    o->min_rcond = -1.0;
 }
 
 RunInputs make_inputs(const oracle_ctx* ctx, const mpm2p_split* sp, const double* s0) {

@@ -57,7 +57,7 @@ class RunRecord(C.Structure):
         ("max_div_ratio", C.c_double), ("repair_warnings", C.c_int32), ("final_pvi", C.c_double),
         ("min_eps_margin", C.c_double), ("clamp_count", C.c_int64),
         ("interface_krylov", C.c_int32), ("interface_max_iterations", C.c_int32),
-        ("interface_iterations", C.c_int64),
+        ("interface_iterations", C.c_int64), ("min_rcond", C.c_double),
     ]
 
 

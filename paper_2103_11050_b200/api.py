@@ -205,6 +205,7 @@ class RunRecord:  # simulation.hpp:47-62
     interface_krylov: int = 0
     interface_max_iterations: int = 0
     interface_iterations: int = 0
+    min_rcond: float = -1.0
 
     @property
     def update_steps(self):
@@ -231,7 +232,7 @@ def _record(steps, r: _abi.RunRecord) -> RunRecord:
     return RunRecord(steps, r.breakthrough_step, r.breakthrough_pvi, r.te, r.tm_updates, r.tm_total, r.nhat,
                      r.n_sub, _counters(r.counters), r.max_div_residual, r.max_div_ratio, r.repair_warnings,
                      r.final_pvi, r.min_eps_margin, r.clamp_count, r.interface_krylov,
-                     r.interface_max_iterations, r.interface_iterations)
+                     r.interface_max_iterations, r.interface_iterations, r.min_rcond)
 
 
 class Simulator:

@@ -121,6 +121,10 @@ struct Ctx {
     int iface_sym = -1;  // J*M symmetric (pivot-free inverse)? -1 unknown
     // per-run CUDA graphs of one driver step (MPM-2P reuse / MRCM rebuild)
     bool use_graphs = true;
+    bool refine = true;        // one refinement step in MPM-2P interface solves (decided per rebuild from rcond)
+    bool force_refine = false; // MPM2P_REFINE=1: always refine
+    bool never_refine = false; // MPM2P_REFINE=0: never (accuracy experiments)
+    double refine_rcond = 1e-8;  // refine when rcond <= this (cond >= 1e8; C3 yes, C1/C2/C4 no)
     bool pdl = false;  // programmatic dependent launch between kernels (MPM2P_PDL=1; measured neutral on C2)
     bool no_regband = false;  // MPM2P_NO_REGBAND=1: generic shared-memory band kernels only
     bool no_twist = false;    // MPM2P_NO_TWIST=1: one-sided register-window band solves
@@ -129,15 +133,18 @@ struct Ctx {
     DevBuf<double> tw_midb, tw_sinv;  // per subdomain: bottom middle multipliers, middle S^-1 (B x B)
     // one graph per (branch, saturation-buffer parity): the upwind ping-pong
     // swaps s/s2 instead of copying, so the captured pointers alternate
-    cudaGraphExec_t g_mpm[2] = {}, g_rebuild[2] = {};
+    cudaGraphExec_t g_mpm[2][2] = {}, g_rebuild[2] = {};  // mpm: [parity][refine]
     long long gd_mpm[6] = {}, gd_rebuild[6] = {};  // counter / launch deltas per replay
     int s_par = 0;                                 // parity of the s/s2 pointer swap
     const double* outlet_s = nullptr;              // set during driver steps: k_divres also probes the outlet
     void drop_graphs() {
         for (int i = 0; i < 2; ++i) {
-            if (g_mpm[i]) cudaGraphExecDestroy(g_mpm[i]);
+            for (int r = 0; r < 2; ++r) {
+                if (g_mpm[i][r]) cudaGraphExecDestroy(g_mpm[i][r]);
+                g_mpm[i][r] = nullptr;
+            }
             if (g_rebuild[i]) cudaGraphExecDestroy(g_rebuild[i]);
-            g_mpm[i] = g_rebuild[i] = nullptr;
+            g_rebuild[i] = nullptr;
         }
     }
     bool has_basis = false;

@@ -1489,7 +1489,7 @@ void downscale(Ctx& c, const double* kappa) {
     c.c_down += L.n_sub;
 }
 
-void interface_solve(Ctx& c) {
+void interface_solve(Ctx& c, bool refine) {
     const Layout& L = c.L;
     c.c_iface += 1;
     if (c.dim == 0) return;
@@ -1507,6 +1507,7 @@ void interface_solve(Ctx& c) {
         return;
     }
     launch_gemv(c, c.Minv, c.irhs, c.icoef, c.dim);
+    if (!refine) return;
     // one step of iterative refinement against the sparse operator
     for (int it = 0; it < 1; ++it) {
         launch_csr_residual(c, c.csr_ptr, c.csr_col, c.csr_val, c.icoef, c.irhs, c.ires, c.dim);
@@ -1636,7 +1637,7 @@ void launch_rebuild(Ctx& c, const double* kappa, bool compute_beta) {  // comput
             interface_inverse_async(c, c.Mdense, c.Minv, c.dim, &c.sc.p->rcond, ERR_SINGULAR, 1e-14);
         }
     }
-    interface_solve(c);
+    interface_solve(c, true);  // the new inverse's rcond is not known yet
     // recon_m (kept for MPM steps) and its traces
     if (c.dim == 0) CK(cudaMemsetAsync(c.icoef, 0, sizeof(double), c.st));
     {
@@ -1721,7 +1722,7 @@ void launch_mpm(Ctx& c, const double* kn) {  // mpm_pressure_update (mpm.cpp:31-
         }
     }
     c.c_part += L.n_sub;
-    interface_solve(c);
+    interface_solve(c, c.refine);
     if (c.dim == 0) CK(cudaMemsetAsync(c.icoef, 0, sizeof(double), c.st));
     if (L.max_hom <= 16) {
         PROF(c, "k_recon_mpm");
