@@ -520,12 +520,14 @@ bool run_step(mpm2p_ctx* ctx, mpm2p_step_record* out) {
             launch_mpm(c, c.kappa_n);
         }
         c.outlet_s = nullptr;
+        c.trans_fresh = false;
     };
     if (c.profiling || !c.use_graphs) {
         try {
             body();
         } catch (...) {
             c.outlet_s = nullptr;
+            c.trans_fresh = false;
             throw;
         }
     } else {
@@ -539,6 +541,7 @@ bool run_step(mpm2p_ctx* ctx, mpm2p_step_record* out) {
                 body();
             } catch (...) {
                 c.outlet_s = nullptr;
+                c.trans_fresh = false;
                 cudaGraph_t dummy = nullptr;
                 cudaStreamEndCapture(c.st, &dummy);
                 if (dummy) cudaGraphDestroy(dummy);

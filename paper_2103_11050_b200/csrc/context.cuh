@@ -121,6 +121,7 @@ struct Ctx {
     int iface_sym = -1;  // J*M symmetric (pivot-free inverse)? -1 unknown
     // per-run CUDA graphs of one driver step (MPM-2P reuse / MRCM rebuild)
     bool use_graphs = true;
+    bool trans_fresh = false;  // T already matches kappa_n (set by the driver's fused k_kappa)
     bool refine = true;        // one refinement step in MPM-2P interface solves (decided per rebuild from rcond)
     bool force_refine = false; // MPM2P_REFINE=1: always refine
     bool never_refine = false; // MPM2P_REFINE=0: never (accuracy experiments)

@@ -1123,6 +1123,107 @@ __global__ void k_ds_u(Layout L, const double* __restrict__ T, const double* __r
 }
 
 // max_c |div u - q| and max(|q|, |u_f| area / vol) (mrcm.cpp:429-437).
+// Velocity scatter + divergence residual (+ outlet probe) in one pass: each
+// cell evaluates its four face velocities with k_ds_u's formulas (interior
+// faces from the unshifted local pressure Xd, subdomain-edge faces from the
+// imposed outward velocity EU), writes the faces it owns (west, south, and
+// the east / north domain boundary), and feeds k_divres's reductions with the
+// same face values.
+__global__ void k_ds_u_div(Layout L, const double* __restrict__ T, const double* __restrict__ Xd,
+                           const double* __restrict__ EU, double* __restrict__ u, const double* __restrict__ q,
+                           Scalars* sc, double* part, unsigned* counter, const double* __restrict__ s_out) {
+    pdl_begin();
+    constexpr int NP = 10;  // res, scale, 4 x side net, 4 x side max
+    double res = 0.0, scale = 0.0, net[4] = {0.0, 0.0, 0.0, 0.0}, smax[4] = {0.0, 0.0, 0.0, 0.0};
+    const double vol = L.vol();
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < L.cells(); c += gridDim.x * blockDim.x) {
+        const int i = c % L.nx, j = c / L.nx;
+        const int sx = i / L.snx, ii = i % L.snx, sy = j / L.sny, jj = j % L.sny;
+        const int s = sy * L.nsx + sx;
+        const size_t xo = (size_t)s * L.ncs;
+        const int r = jj * L.snx + ii;
+        const size_t eo = (size_t)s * L.nbe;
+        const int fW = L.vface(i, j), fE = L.vface(i + 1, j), fS = L.hface(i, j), fN = L.hface(i, j + 1);
+        const double uW = ii > 0 ? T[fW] * (Xd[xo + r - 1] - Xd[xo + r]) / L.hy : -EU[eo + jj];
+        double uE;
+        if (ii + 1 < L.snx) uE = T[fE] * (Xd[xo + r] - Xd[xo + r + 1]) / L.hy;
+        else if (i + 1 < L.nx) uE = -EU[eo + L.nbe + jj];  // west edge of the subdomain to the east
+        else uE = EU[eo + L.sny + jj];                    // east domain boundary
+        const double uS = jj > 0 ? T[fS] * (Xd[xo + r - L.snx] - Xd[xo + r]) / L.hx : -EU[eo + 2 * L.sny + ii];
+        double uN;
+        if (jj + 1 < L.sny) uN = T[fN] * (Xd[xo + r] - Xd[xo + r + L.snx]) / L.hx;
+        else if (j + 1 < L.ny) uN = -EU[(size_t)(s + L.nsx) * L.nbe + 2 * L.sny + ii];  // south edge of the one above
+        else uN = EU[eo + 2 * L.sny + L.snx + ii];                                         // north domain boundary
+        u[fW] = uW;
+        u[fS] = uS;
+        scale = fmax(scale, fabs(uW) * L.hy / vol);
+        scale = fmax(scale, fabs(uS) * L.hx / vol);
+        if (i == L.nx - 1) {
+            u[fE] = uE;
+            scale = fmax(scale, fabs(uE) * L.hy / vol);
+        }
+        if (j == L.ny - 1) {
+            u[fN] = uN;
+            scale = fmax(scale, fabs(uN) * L.hx / vol);
+        }
+        const double fx = (uE - uW) * L.hy;
+        const double fy = (uN - uS) * L.hx;
+        res = fmax(res, fabs((fx + fy) / vol - q[c]));
+        scale = fmax(scale, fabs(q[c]));
+        if (s_out) {  // outlet probe: outward flux of boundary faces, sides W, E, S, N
+            const double so = s_out[c];
+            if (i == 0) {
+                const double fo = -uW;
+                net[0] += fo * L.hy;
+                if (fo > 1e-14) smax[0] = fmax(smax[0], so);
+            }
+            if (i == L.nx - 1) {
+                const double fo = uE;
+                net[1] += fo * L.hy;
+                if (fo > 1e-14) smax[1] = fmax(smax[1], so);
+            }
+            if (j == 0) {
+                const double fo = -uS;
+                net[2] += fo * L.hx;
+                if (fo > 1e-14) smax[2] = fmax(smax[2], so);
+            }
+            if (j == L.ny - 1) {
+                const double fo = uN;
+                net[3] += fo * L.hx;
+                if (fo > 1e-14) smax[3] = fmax(smax[3], so);
+            }
+        }
+    }
+    __shared__ double shm[32 * NP];
+    __shared__ double red[NP];
+    constexpr unsigned SUMS = 0x3Cu;  // slots 2..5 (side nets) are sums, the rest maxima
+    double v[NP] = {res, scale, net[0], net[1], net[2], net[3], smax[0], smax[1], smax[2], smax[3]};
+    block_reduce_multi<NP>(v, SUMS, shm, red);
+    if (threadIdx.x < NP) part[NP * blockIdx.x + threadIdx.x] = red[threadIdx.x];
+    if (last_block_done(counter)) {
+        double a[NP];
+#pragma unroll
+        for (int k = 0; k < NP; ++k) a[k] = 0.0;
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+#pragma unroll
+            for (int k = 0; k < NP; ++k) {
+                const double t = __ldcg(part + (size_t)NP * b + k);
+                a[k] = ((SUMS >> k) & 1u) ? a[k] + t : fmax(a[k], t);
+            }
+        }
+        block_reduce_multi<NP>(a, SUMS, shm, red);
+        if (threadIdx.x == 0) {
+            double om = 0.0;
+            for (int sd = 0; sd < 4; ++sd)
+                if (red[2 + sd] > 1e-14) om = fmax(om, red[6 + sd]);
+            sc->div_residual = red[0];
+            sc->div_scale = red[1] > 0.0 ? red[1] : 1.0;
+            if (s_out) sc->outlet_max = om;
+            *counter = 0;
+        }
+    }
+}
+
 // Divergence residual of the downscaled velocity (simulation.cpp:176-181).
 // With s_out != nullptr (driver steps) it also evaluates
 // max_outlet_saturation (simulation.cpp:61-83) grid-parallel: per side the
@@ -1362,6 +1463,10 @@ int band_blocks(const Layout& L) { return cdiv(L.n_sub, WPB); }
 }  // namespace
 
 void launch_trans(Ctx& c, const double* kappa) {
+    if (c.trans_fresh) {  // the driver's k_kappa already wrote T for this kappa
+        c.trans_fresh = false;
+        return;
+    }
     {
         PROF(c, "k_trans");
         launch_k(c, k_trans, std::min(grid_for(c.L.faces()), 8 * c.num_sms), TPB, 0, c.L, kappa, c.T);
@@ -1475,15 +1580,10 @@ void downscale(Ctx& c, const double* kappa) {
         }
         CK_LAUNCH();
     }
-    {  // (fusing this into k_ds_solve_r serialises ~17 dependent loads per lane: slower)
-        PROF(c, "k_ds_u");
-        launch_k(c, k_ds_u, grid_for(L.faces()), TPB, 0, L, c.T, c.Xd, c.GZ, c.u);
-        CK_LAUNCH();
-    }
-    {
-        PROF(c, "k_divres");
-        launch_k(c, k_divres, std::min(grid_for(std::max(L.cells(), L.faces())), 2 * c.num_sms), TPB, 0, 
-            L, c.u, c.q, c.sc, c.red, c.red_count, c.outlet_s);
+    {  // velocity scatter + divergence residual (+ outlet probe) in one pass
+        PROF(c, "k_ds_u_div");
+        launch_k(c, k_ds_u_div, std::min(grid_for(L.cells()), 2 * c.num_sms), TPB, 0, L, c.T, c.Xd, c.GZ, c.u, c.q,
+                 c.sc.p, c.red.p, c.red_count.p, c.outlet_s);
         CK_LAUNCH();
     }
     c.c_down += L.n_sub;

@@ -233,10 +233,14 @@ __device__ __forceinline__ void decide(Scalars* sc, int rebuilt, int method, dou
 
 // With decide_method >= 0 the last block also takes the next-step decision
 // (k_decide) from the drift it just formed.
+// With T != nullptr it also writes the face transmissibilities of k_trans for
+// the faces each cell owns (west/south, plus the east/north domain boundary),
+// recomputing the neighbour's conductivity with the same operations.
 __global__ void k_kappa(Layout L, const double* __restrict__ K, const double* __restrict__ s,
                         double* __restrict__ kappa, const double* __restrict__ kappa_m,
                         const double* __restrict__ lam_reb, Scalars* sc, double M, int eps_mode, double* part,
-                        unsigned* counter, int decide_method = -1, int rebuilt = 0, double eta = 0.0) {
+                        unsigned* counter, int decide_method = -1, int rebuilt = 0, double eta = 0.0,
+                        double* __restrict__ T = nullptr) {
     pdl_begin();
     __shared__ DD shd[32];
     const double vol = L.vol();
@@ -245,6 +249,14 @@ __global__ void k_kappa(Layout L, const double* __restrict__ K, const double* __
         const double lam = total_mob(s[c], M, &sc->clamp);
         const double k = lam * K[c];
         kappa[c] = k;
+        if (T) {  // elliptic.cpp:44-61 for this cell's faces (boundary faces carry 0)
+            const int i = c % L.nx, j = c / L.nx;
+            const int cw = L.cell(i - 1, j), cs = L.cell(i, j - 1);
+            T[L.vface(i, j)] = i > 0 ? harm_trans_v(L, total_mob(s[cw], M, nullptr) * K[cw], k) : 0.0;
+            T[L.hface(i, j)] = j > 0 ? harm_trans_h(L, total_mob(s[cs], M, nullptr) * K[cs], k) : 0.0;
+            if (i == L.nx - 1) T[L.vface(L.nx, j)] = 0.0;
+            if (j == L.ny - 1) T[L.hface(i, L.ny)] = 0.0;
+        }
         if (!(k > 0.0) || !isfinite(k)) atomicOr(&sc->err, ERR_KAPPA);
         if (eps_mode == 0 || eps_mode == 1) {
             const double d = k - kappa_m[c];
@@ -440,14 +452,15 @@ void launch_conductivity_decide(Ctx& c, const double* s, double* kappa, int eps_
                                 double eta) {
     PROF(c, "k_kappa");
     launch_k(c, k_kappa, red_grid(c), TPB, 0, c.L, c.K, s, kappa, c.kappa_m, c.lam_reb, c.sc, c.M, eps_mode, c.red,
-                                           c.red_count, method, rebuilt, eta);
+                                           c.red_count, method, rebuilt, eta, c.T.p);
+    c.trans_fresh = true;  // T = transmissibility(kappa) is current: the next rebuild / MPM step skips k_trans
     CK_LAUNCH();
 }
 void launch_conductivity(Ctx& c, const double* s, double* kappa, int eps_mode, bool want_eps) {
     {
         PROF(c, "k_kappa");
         launch_k(c, k_kappa, red_grid(c), TPB, 0, c.L, c.K, s, kappa, c.kappa_m, c.lam_reb, c.sc, c.M,
-                                               want_eps ? eps_mode : -1, c.red, c.red_count, -1, 0, 0.0);
+                                               want_eps ? eps_mode : -1, c.red, c.red_count, -1, 0, 0.0, nullptr);
         CK_LAUNCH();
     }
 }
