@@ -1083,44 +1083,6 @@ void twist_configure() {
 // Subdomain widths with a register-window instantiation; others use band.cuh.
 #define MPM2P_BAND_WIDTHS(X) X(4) X(8) X(10) X(12) X(16) X(20) X(24) X(32)
 
-// Velocity scatter: interior faces from the unshifted local pressure,
-// subdomain-boundary faces from the imposed outward velocity (single-valued
-// on shared edges).
-__global__ void k_ds_u(Layout L, const double* __restrict__ T, const double* __restrict__ Xd,
-                       const double* __restrict__ EU, double* __restrict__ u) {
-    pdl_begin();
-    const int f = blockIdx.x * blockDim.x + threadIdx.x;
-    if (f >= L.faces()) return;
-    if (f < L.vcount()) {
-        const int i = f % (L.nx + 1), j = f / (L.nx + 1);
-        const int sy = j / L.sny, jj = j % L.sny;
-        if (i % L.snx != 0) {
-            const int sx = i / L.snx, ii = i % L.snx;
-            const size_t o = (size_t)(sy * L.nsx + sx) * L.ncs + jj * L.snx;
-            u[f] = T[f] * (Xd[o + ii - 1] - Xd[o + ii]) / L.hy;
-        } else if (i < L.nx) {  // west edge of subdomain (i / snx)
-            const int s = sy * L.nsx + i / L.snx;
-            u[f] = -EU[(size_t)s * L.nbe + jj];
-        } else {  // east domain boundary: east edge of the last column
-            const int s = sy * L.nsx + L.nsx - 1;
-            u[f] = EU[(size_t)s * L.nbe + L.sny + jj];
-        }
-    } else {
-        const int fh = f - L.vcount(), i = fh % L.nx, j = fh / L.nx;
-        const int sx = i / L.snx, ii = i % L.snx;
-        if (j % L.sny != 0) {
-            const int sy = j / L.sny, jj = j % L.sny;
-            const size_t o = (size_t)(sy * L.nsx + sx) * L.ncs + ii;
-            u[f] = T[f] * (Xd[o + (size_t)(jj - 1) * L.snx] - Xd[o + (size_t)jj * L.snx]) / L.hx;
-        } else if (j < L.ny) {  // south edge of subdomain (j / sny)
-            const int s = (j / L.sny) * L.nsx + sx;
-            u[f] = -EU[(size_t)s * L.nbe + 2 * L.sny + ii];
-        } else {
-            const int s = (L.nsy - 1) * L.nsx + sx;
-            u[f] = EU[(size_t)s * L.nbe + 2 * L.sny + L.snx + ii];
-        }
-    }
-}
 
 // max_c |div u - q| and max(|q|, |u_f| area / vol) (mrcm.cpp:429-437).
 // Velocity scatter + divergence residual (+ outlet probe) in one pass: each
@@ -1224,77 +1186,6 @@ __global__ void k_ds_u_div(Layout L, const double* __restrict__ T, const double*
     }
 }
 
-// Divergence residual of the downscaled velocity (simulation.cpp:176-181).
-// With s_out != nullptr (driver steps) it also evaluates
-// max_outlet_saturation (simulation.cpp:61-83) grid-parallel: per side the
-// net outflow sum and the max saturation over outflow faces, combined by the
-// last block (a side counts when its net outflow exceeds 1e-14).
-__global__ void k_divres(Layout L, const double* __restrict__ u, const double* __restrict__ q, Scalars* sc,
-                         double* part, unsigned* counter, const double* __restrict__ s_out = nullptr) {
-    pdl_begin();
-    constexpr int NP = 10;  // res, scale, 4 x side net, 4 x side max
-    double res = 0.0, scale = 0.0, net[4] = {0.0, 0.0, 0.0, 0.0}, smax[4] = {0.0, 0.0, 0.0, 0.0};
-    const double vol = L.vol();
-    const int nbt = s_out ? 2 * (L.nx + L.ny) : 0;
-    int n = L.cells() > L.faces() ? L.cells() : L.faces();
-    n = n > nbt ? n : nbt;
-    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
-        if (x < L.cells()) {
-            const int i = x % L.nx, j = x / L.nx;
-            const double fx = (u[L.vface(i + 1, j)] - u[L.vface(i, j)]) * L.hy;
-            const double fy = (u[L.hface(i, j + 1)] - u[L.hface(i, j)]) * L.hx;
-            res = fmax(res, fabs((fx + fy) / vol - q[x]));
-            scale = fmax(scale, fabs(q[x]));
-        }
-        if (x < L.faces()) scale = fmax(scale, fabs(u[x]) * L.area(x) / vol);
-        if (x < nbt) {  // boundary face x: sides W (ny), E (ny), S (nx), N (nx)
-            int side, k;
-            if (x < 2 * L.ny) side = x / L.ny, k = x % L.ny;
-            else side = 2 + (x - 2 * L.ny) / L.nx, k = (x - 2 * L.ny) % L.nx;
-            double fo;
-            int cell;
-            if (side == 0) fo = -u[L.vface(0, k)], cell = L.cell(0, k);
-            else if (side == 1) fo = u[L.vface(L.nx, k)], cell = L.cell(L.nx - 1, k);
-            else if (side == 2) fo = -u[L.hface(k, 0)], cell = L.cell(k, 0);
-            else fo = u[L.hface(k, L.ny)], cell = L.cell(k, L.ny - 1);
-            const double area = side < 2 ? L.hy : L.hx;
-#pragma unroll
-            for (int sd = 0; sd < 4; ++sd) {
-                if (sd != side) continue;
-                net[sd] += fo * area;
-                if (fo > 1e-14) smax[sd] = fmax(smax[sd], s_out[cell]);
-            }
-        }
-    }
-    __shared__ double shm[32 * NP];
-    __shared__ double red[NP];
-    constexpr unsigned SUMS = 0x3Cu;  // slots 2..5 (side nets) are sums, the rest maxima
-    double v[NP] = {res, scale, net[0], net[1], net[2], net[3], smax[0], smax[1], smax[2], smax[3]};
-    block_reduce_multi<NP>(v, SUMS, shm, red);
-    if (threadIdx.x < NP) part[NP * blockIdx.x + threadIdx.x] = red[threadIdx.x];
-    if (last_block_done(counter)) {
-        double a[NP];
-#pragma unroll
-        for (int i = 0; i < NP; ++i) a[i] = 0.0;  // identity of both (all maxima are of |x| or s >= 0)
-        for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
-#pragma unroll
-            for (int i = 0; i < NP; ++i) {
-                const double t = __ldcg(part + (size_t)NP * b + i);
-                a[i] = ((SUMS >> i) & 1u) ? a[i] + t : fmax(a[i], t);
-            }
-        }
-        block_reduce_multi<NP>(a, SUMS, shm, red);
-        if (threadIdx.x == 0) {
-            double om = 0.0;
-            for (int sd = 0; sd < 4; ++sd)
-                if (red[2 + sd] > 1e-14) om = fmax(om, red[6 + sd]);
-            sc->div_residual = red[0];
-            sc->div_scale = red[1] > 0.0 ? red[1] : 1.0;
-            if (s_out) sc->outlet_max = om;
-            *counter = 0;
-        }
-    }
-}
 
 // ---------------------------------------------------------------- K2 ----
 // MPM-2P data: w from p^m under kappa_n; q' = q - div w; g' = g - p^m_face;
