@@ -111,6 +111,22 @@ __global__ void k_cfl(Layout L, const double* __restrict__ u, Scalars* sc, doubl
     const double vol = L.vol(), slope = sc->slope;
     double best = INFINITY;
     double any = 0.0;
+    double rate = 0.0;  // injection_rate terms (simulation.cpp:85-101) when inj_cn > 0
+    const int nterms = inj_cn > 0 ? 2 * (L.nx + L.ny) : 0;
+    const double fin = inj_cn > 0 ? frac_flow(inflow, M, nullptr) : 0.0;
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < nterms; x += gridDim.x * blockDim.x) {
+        double un, area;
+        if (x < 2 * L.ny) {
+            const int j = x >> 1;
+            un = (x & 1) == 0 ? -u[L.vface(0, j)] : u[L.vface(L.nx, j)];
+            area = L.hy;
+        } else {
+            const int k = x - 2 * L.ny, i = k >> 1;
+            un = (k & 1) == 0 ? -u[L.hface(i, 0)] : u[L.hface(i, L.ny)];
+            area = L.hx;
+        }
+        if (un < 0.0) rate += -un * area * fin;
+    }
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < L.cells(); c += gridDim.x * blockDim.x) {
         const int i = c % L.nx, j = c / L.nx;
         double out = 0.0;
@@ -125,33 +141,36 @@ __global__ void k_cfl(Layout L, const double* __restrict__ u, Scalars* sc, doubl
             best = fmin(best, vol / (out * slope));
         }
     }
-    best = block_reduce(best, [](double a, double b) { return fmin(a, b); }, sh, INFINITY);
-    any = block_reduce(any, [](double a, double b) { return fmax(a, b); }, sh, 0.0);
-    if (threadIdx.x == 0) {
-        part[2 * blockIdx.x] = best;
-        part[2 * blockIdx.x + 1] = any;
-    }
+    // one multi-value reduction: -best (max), any (max), rate (sum)
+    __shared__ double shm[32 * 3];
+    __shared__ double red[3];
+    double v[3] = {-best, any, rate};
+    block_reduce_multi<3>(v, 0x4u, shm, red);
+    if (threadIdx.x < 3) part[3 * blockIdx.x + threadIdx.x] = red[threadIdx.x];
     if (last_block_done(counter)) {
-        auto mn = [](double a, double b) { return fmin(a, b); };
-        auto mx = [](double a, double b) { return fmax(a, b); };
-        const double best_all = reduce_partials(part, gridDim.x, 2, 0, mn, INFINITY, sh);
-        const double any_all = reduce_partials(part, gridDim.x, 2, 1, mx, 0.0, sh);
+        double a[3] = {-INFINITY, 0.0, 0.0};
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+            a[0] = fmax(a[0], __ldcg(part + 3 * b));
+            a[1] = fmax(a[1], __ldcg(part + 3 * b + 1));
+            a[2] += __ldcg(part + 3 * b + 2);
+        }
+        block_reduce_multi<3>(a, 0x4u, shm, red);
         if (threadIdx.x == 0) {
+            const double best_all = -red[0];
             const double dt = fmin(dt_cap / safety, best_all);  // min is order-independent
-            const bool anyf = any_all > 0.0;
+            const bool anyf = red[1] > 0.0;
             sc->any_flow = anyf;
             sc->dt = anyf ? fmin(safety * dt, dt_cap) : dt_cap;
             *counter = 0;
-        }
-        if (inj_cn > 0) {
-            const double rate = inj_rate_block(L, u, frac_flow(inflow, M, nullptr), sh);
-            if (threadIdx.x == 0) {
-                sc->inj = rate;
+            if (inj_cn > 0) {
+                const double rt = red[2];
+                sc->inj = rt;
                 const double pore = L.lx * L.ly;
-                for (int k = 0; k < inj_cn; ++k) sc->pvi += rate * sc->dt / pore;
+                for (int k = 0; k < inj_cn; ++k) sc->pvi += rt * sc->dt / pore;
             }
         }
     }
+    (void)sh;
 }
 
 // injection_rate (simulation.cpp:85-101) as a one-block tree sum (the terms
