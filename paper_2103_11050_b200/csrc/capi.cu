@@ -361,7 +361,7 @@ void create_ctx(mpm2p_ctx* ctx, const mpm2p_problem* P) {
         c.tw_sinv.alloc(ns * B * B);
     }
     c.sc.alloc(1);
-    c.red.alloc(8 * 4 * (size_t)c.num_sms + 4096);
+    c.red.alloc(16 * 8 * (size_t)c.num_sms + 4096);  // <= 16 values x 8 resident blocks / SM (red_blocks)
     c.red_count.alloc(1);
     CK(cudaMallocHost(&c.sc_host, sizeof(Scalars)));
     std::memset(c.sc_host, 0, sizeof(Scalars));
@@ -461,9 +461,15 @@ void run_begin(mpm2p_ctx* ctx, const mpm2p_split* sp, const double* s0, mpm2p_st
     d.rec.min_eps_margin = INFINITY;
     c.c_hom = c.c_part = c.c_down = c.c_fine = c.c_iface = 0;
     c.drop_graphs();
+    c.cfl_fused = false;
     reset_scalars(c);
     const auto t0 = std::chrono::steady_clock::now();
     upload(c, c.s, s0, c.L.cells());
+    // every pressure update of the run also forms the next step's CFL dt
+    c.cfl_fused = true;
+    c.cfl_safety = sp->cfl_safety;
+    c.cfl_dt_cap = sp->dt_cap;
+    c.cfl_inflow = sp->inflow_sat;
     launch_conductivity(c, c.s, c.kappa_n, -1, false);
     launch_rebuild(c, c.kappa_n);
     launch_lambda(c, c.s, c.lam_reb);
@@ -507,9 +513,10 @@ bool run_step(mpm2p_ctx* ctx, mpm2p_step_record* out) {
     // ends in `cur` and the buffers are swapped afterwards (no copy)
     double* cur = (sp.cn % 2 == 1) ? c.s2.p : c.s.p;
     auto body = [&] {
-        launch_cfl_inj(c, c.u, sp.cfl_safety, sp.dt_cap, sp.inflow_sat, sp.cn);
+        // cfl_timestep + injection_rate of this step were formed by the previous
+        // pressure update's k_ds_u_div (c.cfl_fused); the first sub-step promotes them
         for (int k = 0; k < sp.cn; ++k) {
-            launch_upwind(c, k % 2 == 0 ? c.s : c.s2, k % 2 == 0 ? c.s2 : c.s, c.u, sp.inflow_sat);
+            launch_upwind(c, k % 2 == 0 ? c.s : c.s2, k % 2 == 0 ? c.s2 : c.s, c.u, sp.inflow_sat, k == 0, sp.cn);
         }
         launch_conductivity_decide(c, cur, c.kappa_n, sp.eta_mode, rebuilt, sp.method, sp.eta);
         c.outlet_s = cur;  // the step's last k_divres also takes max_outlet_saturation
@@ -607,6 +614,7 @@ void run_end(mpm2p_ctx* ctx, mpm2p_run_record* out) {
     d.rec.min_rcond = d.min_rcond;
     if (out) *out = d.rec;
     d.active = false;
+    c.cfl_fused = false;
 }
 
 DevBuf<double>& scratch(std::unique_ptr<DevBuf<double>>& b, size_t n) {

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "common.cuh"
@@ -26,7 +27,10 @@ struct Scalars {
     long long clamp;
     long long kr_iters_total;  // MINRES iterations (K7), summed over solves
     int kr_iters_max, kr_solves;
-    double pad[6];
+    double dt_next, inj_next;  // next step's cfl_timestep / injection_rate (k_ds_u_div with CflNext)
+    int any_next;
+    int pad_i;
+    double pad[3];
 };
 
 template <typename T>
@@ -121,6 +125,11 @@ struct Ctx {
     int iface_sym = -1;  // J*M symmetric (pivot-free inverse)? -1 unknown
     // per-run CUDA graphs of one driver step (MPM-2P reuse / MRCM rebuild)
     bool use_graphs = true;
+    // The driver's steps take dt from the previous pressure update's k_ds_u_div
+    // (CflNext) instead of a separate k_cfl pass.
+    bool cfl_fused = false;
+    double cfl_safety = 0.0, cfl_dt_cap = 0.0, cfl_inflow = 0.0;
+    std::unordered_map<const void*, int> occ;  // resident blocks / SM per grid-stride kernel (TPB threads)
     bool trans_fresh = false;  // T already matches kappa_n (set by the driver's fused k_kappa)
     bool refine = true;        // one refinement step in MPM-2P interface solves (decided per rebuild from rcond)
     bool force_refine = false; // MPM2P_REFINE=1: always refine
@@ -218,6 +227,21 @@ inline void launch_k(const Ctx& c, void (*kern)(KArgs...), dim3 grid, dim3 block
     CK(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
 }
 
+// Grid for a grid-stride reduction kernel of 256-thread blocks over `work`
+// items: one wave of resident blocks (at most 8 per SM, which the reduction
+// partial buffer c.red is sized for), never more blocks than items need.
+template <typename... KArgs>
+inline int red_blocks(Ctx& c, void (*kern)(KArgs...), long long work) {
+    int& n = c.occ[(const void*)kern];
+    if (n == 0) {
+        int b = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, 256, 0));
+        n = b < 1 ? 1 : (b > 8 ? 8 : b);
+    }
+    const int need = cdiv(work, 256);
+    return need < n * c.num_sms ? (need < 1 ? 1 : need) : n * c.num_sms;
+}
+
 // RAII scope recording CUDA events around one kernel launch when profiling.
 struct ProfScope {
     Ctx& c;
@@ -244,7 +268,8 @@ struct ProfScope {
 void launch_max_slope(Ctx& c);
 void launch_cfl(Ctx& c, const double* u, double safety, double dt_cap);
 void launch_inj_pvi(Ctx& c, const double* u, double inflow, int cn, bool add_pvi);
-void launch_upwind(Ctx& c, const double* s_in, double* s_out, const double* u, double inflow);
+void launch_upwind(Ctx& c, const double* s_in, double* s_out, const double* u, double inflow, bool take_next = false,
+                   int inj_cn = 0);
 void launch_conductivity(Ctx& c, const double* s, double* kappa, int eps_mode, bool want_eps);
 void launch_cfl_inj(Ctx& c, const double* u, double safety, double dt_cap, double inflow, int cn);
 void launch_conductivity_decide(Ctx& c, const double* s, double* kappa, int eps_mode, int rebuilt, int method,

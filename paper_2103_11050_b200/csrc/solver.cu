@@ -1091,13 +1091,34 @@ void twist_configure() {
 // imposed outward velocity EU), writes the faces it owns (west, south, and
 // the east / north domain boundary), and feeds k_divres's reductions with the
 // same face values.
+//
+// With cfl.on it also takes the NEXT step's cfl_timestep + injection_rate
+// (transport.cpp:51-71, simulation.cpp:85-101) from the same face values, so
+// the step needs no separate k_cfl pass: dt_next / any_next / inj_next are
+// promoted by the first upwind sub-step (k_upwind take_next). The CFL terms
+// use explicitly rounded operations (no FMA contraction) in k_cfl's order,
+// so dt is bit-identical to the separate reduction.
+struct CflNext {
+    int on = 0;
+    double safety = 0.0, dt_cap = 0.0, inflow = 0.0, M = 1.0;
+};
 __global__ void k_ds_u_div(Layout L, const double* __restrict__ T, const double* __restrict__ Xd,
                            const double* __restrict__ EU, double* __restrict__ u, const double* __restrict__ q,
-                           Scalars* sc, double* part, unsigned* counter, const double* __restrict__ s_out) {
+                           Scalars* sc, double* part, unsigned* counter, const double* __restrict__ s_out,
+                           CflNext cfl) {
     pdl_begin();
-    constexpr int NP = 10;  // res, scale, 4 x side net, 4 x side max
+    // res, scale, 4 x side net, 4 x side max, -min cfl dt, any outflow, injection rate
+    constexpr int NP = 13;
     double res = 0.0, scale = 0.0, net[4] = {0.0, 0.0, 0.0, 0.0}, smax[4] = {0.0, 0.0, 0.0, 0.0};
+    double best = INFINITY, anyf = 0.0, rate = 0.0;
     const double vol = L.vol();
+    const double slope = cfl.on ? sc->slope : 1.0;
+    double fin = 0.0;  // frac_flow(inflow) (transport.cpp:39-43), clamped, unrounded-FMA-free
+    if (cfl.on) {
+        const double si = cfl.inflow < 0.0 ? 0.0 : (cfl.inflow > 1.0 ? 1.0 : cfl.inflow);
+        const double w = __dmul_rn(__dmul_rn(cfl.M, si), si), t = 1.0 - si;
+        fin = __ddiv_rn(w, __dadd_rn(w, __dmul_rn(t, t)));
+    }
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < L.cells(); c += gridDim.x * blockDim.x) {
         const int i = c % L.nx, j = c / L.nx;
         const int sx = i / L.snx, ii = i % L.snx, sy = j / L.sny, jj = j % L.sny;
@@ -1132,6 +1153,21 @@ __global__ void k_ds_u_div(Layout L, const double* __restrict__ T, const double*
         const double fy = (uN - uS) * L.hx;
         res = fmax(res, fabs((fx + fy) / vol - q[c]));
         scale = fmax(scale, fabs(q[c]));
+        if (cfl.on) {  // k_cfl's per-cell outflux, same term order and rounding
+            double o = __dmul_rn(0.0 < uE ? uE : 0.0, L.hy);
+            o = __dadd_rn(o, __dmul_rn(0.0 < -uW ? -uW : 0.0, L.hy));
+            o = __dadd_rn(o, __dmul_rn(0.0 < uN ? uN : 0.0, L.hx));
+            o = __dadd_rn(o, __dmul_rn(0.0 < -uS ? -uS : 0.0, L.hx));
+            if (o > 0.0) {
+                anyf = 1.0;
+                best = fmin(best, __ddiv_rn(vol, __dmul_rn(o, slope)));
+            }
+            // injection_rate terms of the boundary faces (inflow: outward normal velocity < 0)
+            if (i == 0 && -uW < 0.0) rate = __dadd_rn(rate, __dmul_rn(__dmul_rn(uW, L.hy), fin));
+            if (i == L.nx - 1 && uE < 0.0) rate = __dadd_rn(rate, __dmul_rn(__dmul_rn(-uE, L.hy), fin));
+            if (j == 0 && -uS < 0.0) rate = __dadd_rn(rate, __dmul_rn(__dmul_rn(uS, L.hx), fin));
+            if (j == L.ny - 1 && uN < 0.0) rate = __dadd_rn(rate, __dmul_rn(__dmul_rn(-uN, L.hx), fin));
+        }
         if (s_out) {  // outlet probe: outward flux of boundary faces, sides W, E, S, N
             const double so = s_out[c];
             if (i == 0) {
@@ -1158,14 +1194,14 @@ __global__ void k_ds_u_div(Layout L, const double* __restrict__ T, const double*
     }
     __shared__ double shm[32 * NP];
     __shared__ double red[NP];
-    constexpr unsigned SUMS = 0x3Cu;  // slots 2..5 (side nets) are sums, the rest maxima
-    double v[NP] = {res, scale, net[0], net[1], net[2], net[3], smax[0], smax[1], smax[2], smax[3]};
+    constexpr unsigned SUMS = 0x103Cu;  // slots 2..5 (side nets) and 12 (rate) are sums, the rest maxima
+    double v[NP] = {res, scale, net[0], net[1], net[2], net[3], smax[0], smax[1], smax[2], smax[3], -best, anyf, rate};
     block_reduce_multi<NP>(v, SUMS, shm, red);
     if (threadIdx.x < NP) part[NP * blockIdx.x + threadIdx.x] = red[threadIdx.x];
     if (last_block_done(counter)) {
         double a[NP];
 #pragma unroll
-        for (int k = 0; k < NP; ++k) a[k] = 0.0;
+        for (int k = 0; k < NP; ++k) a[k] = k == 10 ? -INFINITY : 0.0;
         for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
 #pragma unroll
             for (int k = 0; k < NP; ++k) {
@@ -1181,6 +1217,13 @@ __global__ void k_ds_u_div(Layout L, const double* __restrict__ T, const double*
             sc->div_residual = red[0];
             sc->div_scale = red[1] > 0.0 ? red[1] : 1.0;
             if (s_out) sc->outlet_max = om;
+            if (cfl.on) {  // k_cfl's epilogue, for the next step
+                const double dt = fmin(cfl.dt_cap / cfl.safety, -red[10]);
+                const bool af = red[11] > 0.0;
+                sc->any_next = af;
+                sc->dt_next = af ? fmin(cfl.safety * dt, cfl.dt_cap) : cfl.dt_cap;
+                sc->inj_next = red[12];
+            }
             *counter = 0;
         }
     }
@@ -1473,8 +1516,10 @@ void downscale(Ctx& c, const double* kappa) {
     }
     {  // velocity scatter + divergence residual (+ outlet probe) in one pass
         PROF(c, "k_ds_u_div");
-        launch_k(c, k_ds_u_div, std::min(grid_for(L.cells()), 2 * c.num_sms), TPB, 0, L, c.T, c.Xd, c.GZ, c.u, c.q,
-                 c.sc.p, c.red.p, c.red_count.p, c.outlet_s);
+        CflNext cfl;
+        if (c.cfl_fused) cfl = CflNext{1, c.cfl_safety, c.cfl_dt_cap, c.cfl_inflow, c.M};
+        launch_k(c, k_ds_u_div, red_blocks(c, k_ds_u_div, L.cells()), TPB, 0, L, c.T, c.Xd, c.GZ, c.u, c.q,
+                 c.sc.p, c.red.p, c.red_count.p, c.outlet_s, cfl);
         CK_LAUNCH();
     }
     c.c_down += L.n_sub;

@@ -79,6 +79,24 @@ __device__ __forceinline__ DD block_reduce_dd(DD v, DD* sh) {
     return v;
 }
 
+// Two double-double sums reduced together (one barrier pair instead of two).
+__device__ __forceinline__ void block_reduce_dd2(DD& a, DD& b, DD* sh /* 64 */) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    a = warp_sum_dd(a);
+    b = warp_sum_dd(b);
+    if (lane == 0) {
+        sh[w] = a;
+        sh[32 + w] = b;
+    }
+    __syncthreads();
+    if (w == 0) {
+        const bool in = lane < (int)(blockDim.x >> 5);
+        a = warp_sum_dd(in ? sh[lane] : DD{0.0, 0.0});
+        b = warp_sum_dd(in ? sh[32 + lane] : DD{0.0, 0.0});
+    }
+    __syncthreads();
+}
+
 // Parallel double-double combination of per-block partials (hi at off, lo at off+1).
 __device__ __forceinline__ DD reduce_dd_partials(const double* part, int nparts, int off, DD* sh) {
     DD v{0.0, 0.0};
@@ -107,7 +125,6 @@ __device__ double inj_rate_block(const Layout& L, const double* __restrict__ u, 
 __global__ void k_cfl(Layout L, const double* __restrict__ u, Scalars* sc, double safety, double dt_cap,
                       double* part, unsigned* counter, int inj_cn = 0, double inflow = 0.0, double M = 1.0) {
     pdl_begin();
-    __shared__ double sh[32];
     const double vol = L.vol(), slope = sc->slope;
     double best = INFINITY;
     double any = 0.0;
@@ -170,7 +187,6 @@ __global__ void k_cfl(Layout L, const double* __restrict__ u, Scalars* sc, doubl
             }
         }
     }
-    (void)sh;
 }
 
 // injection_rate (simulation.cpp:85-101) as a one-block tree sum (the terms
@@ -212,15 +228,30 @@ __global__ void k_inj_pvi(Layout L, const double* __restrict__ u, Scalars* sc, d
 
 // upwind_step (transport.cpp:73-120), one thread per cell; both cells of a
 // face compute its water flux with identical IEEE operations.
+// take_next: the step's cfl_timestep / injection_rate were formed by the
+// previous pressure update's k_ds_u_div (CflNext); this first sub-step reads
+// dt_next and thread 0 promotes it (dt, any_flow, inj) and advances the PVI
+// clock inj_cn times exactly as k_cfl's epilogue does.
 __global__ void k_upwind(Layout L, const double* __restrict__ s, double* __restrict__ s_out,
-                         const double* __restrict__ u, Scalars* sc, double inflow, double M) {
+                         const double* __restrict__ u, Scalars* sc, double inflow, double M, int take_next = 0,
+                         int inj_cn = 0) {
     pdl_begin();
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c == 0) (void)frac_flow(inflow, M, &sc->clamp);  // f_in is evaluated once per call
+    const double dt = take_next ? sc->dt_next : sc->dt;
+    if (c == 0) {
+        (void)frac_flow(inflow, M, &sc->clamp);  // f_in is evaluated once per call
+        if (take_next) {
+            sc->dt = dt;
+            sc->any_flow = sc->any_next;
+            const double rt = sc->inj_next;
+            sc->inj = rt;
+            const double pore = L.lx * L.ly;
+            for (int k = 0; k < inj_cn; ++k) sc->pvi += rt * dt / pore;
+        }
+    }
     if (c >= L.cells()) return;
     const int i = c % L.nx, j = c / L.nx;
     const double fin = frac_flow(inflow, M, nullptr);
-    const double dt = sc->dt;
     long long* cnt = &sc->clamp;
     // vertical faces: owner counts clamps (face i is owned by cell i, face nx by cell nx-1)
     auto vflux = [&](int fi, bool own) {
@@ -261,7 +292,6 @@ __global__ void k_kappa(Layout L, const double* __restrict__ K, const double* __
                         unsigned* counter, int decide_method = -1, int rebuilt = 0, double eta = 0.0,
                         double* __restrict__ T = nullptr) {
     pdl_begin();
-    __shared__ DD shd[32];
     const double vol = L.vol();
     DD num{0.0, 0.0}, den{0.0, 0.0};
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < L.cells(); c += gridDim.x * blockDim.x) {
@@ -287,8 +317,8 @@ __global__ void k_kappa(Layout L, const double* __restrict__ K, const double* __
         }
     }
     if (eps_mode < 0) return;
-    num = block_reduce_dd(num, shd);
-    den = block_reduce_dd(den, shd);
+    __shared__ DD shd2[64];
+    block_reduce_dd2(num, den, shd2);
     if (threadIdx.x == 0) {
         part[4 * blockIdx.x + 0] = num.hi;
         part[4 * blockIdx.x + 1] = num.lo;
@@ -296,8 +326,12 @@ __global__ void k_kappa(Layout L, const double* __restrict__ K, const double* __
         part[4 * blockIdx.x + 3] = den.lo;
     }
     if (last_block_done(counter)) {
-        const DD n = reduce_dd_partials(part, gridDim.x, 0, shd);
-        const DD d = reduce_dd_partials(part, gridDim.x, 2, shd);
+        DD n{0.0, 0.0}, d{0.0, 0.0};
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+            n = dd_add(n, DD{__ldcg(part + 4 * b), __ldcg(part + 4 * b + 1)});
+            d = dd_add(d, DD{__ldcg(part + 4 * b + 2), __ldcg(part + 4 * b + 3)});
+        }
+        block_reduce_dd2(n, d, shd2);
         if (threadIdx.x == 0) {
             const double a = sqrt(n.hi);
             double e;
@@ -430,7 +464,6 @@ __global__ void k_lambda(Layout L, const double* __restrict__ s, double* __restr
     if (c < L.cells()) lam[c] = total_mob(s[c], M, &sc->clamp);
 }
 
-int red_grid(const Ctx& c) { return std::min(2 * c.num_sms, std::max(1, cdiv(c.L.cells(), TPB))); }
 
 }  // namespace
 
@@ -444,7 +477,7 @@ void launch_max_slope(Ctx& c) {
 void launch_cfl(Ctx& c, const double* u, double safety, double dt_cap) {
     {
         PROF(c, "k_cfl");
-        launch_k(c, k_cfl, red_grid(c), TPB, 0, c.L, u, c.sc, safety, dt_cap, c.red, c.red_count, 0, 0.0, 1.0);
+        launch_k(c, k_cfl, red_blocks(c, k_cfl, c.L.cells()), TPB, 0, c.L, u, c.sc, safety, dt_cap, c.red, c.red_count, 0, 0.0, 1.0);
         CK_LAUNCH();
     }
 }
@@ -455,22 +488,24 @@ void launch_inj_pvi(Ctx& c, const double* u, double inflow, int cn, bool add_pvi
         CK_LAUNCH();
     }
 }
-void launch_upwind(Ctx& c, const double* s_in, double* s_out, const double* u, double inflow) {
+void launch_upwind(Ctx& c, const double* s_in, double* s_out, const double* u, double inflow, bool take_next,
+                   int inj_cn) {
     {
         PROF(c, "k_upwind");
-        launch_k(c, k_upwind, cdiv(c.L.cells(), TPB), TPB, 0, c.L, s_in, s_out, u, c.sc, inflow, c.M);
+        launch_k(c, k_upwind, cdiv(c.L.cells(), TPB), TPB, 0, c.L, s_in, s_out, u, c.sc, inflow, c.M, take_next ? 1 : 0,
+                 inj_cn);
         CK_LAUNCH();
     }
 }
 void launch_cfl_inj(Ctx& c, const double* u, double safety, double dt_cap, double inflow, int cn) {
     PROF(c, "k_cfl");
-    launch_k(c, k_cfl, red_grid(c), TPB, 0, c.L, u, c.sc, safety, dt_cap, c.red, c.red_count, cn, inflow, c.M);
+    launch_k(c, k_cfl, red_blocks(c, k_cfl, c.L.cells()), TPB, 0, c.L, u, c.sc, safety, dt_cap, c.red, c.red_count, cn, inflow, c.M);
     CK_LAUNCH();
 }
 void launch_conductivity_decide(Ctx& c, const double* s, double* kappa, int eps_mode, int rebuilt, int method,
                                 double eta) {
     PROF(c, "k_kappa");
-    launch_k(c, k_kappa, red_grid(c), TPB, 0, c.L, c.K, s, kappa, c.kappa_m, c.lam_reb, c.sc, c.M, eps_mode, c.red,
+    launch_k(c, k_kappa, red_blocks(c, k_kappa, c.L.cells()), TPB, 0, c.L, c.K, s, kappa, c.kappa_m, c.lam_reb, c.sc, c.M, eps_mode, c.red,
                                            c.red_count, method, rebuilt, eta, c.T.p);
     c.trans_fresh = true;  // T = transmissibility(kappa) is current: the next rebuild / MPM step skips k_trans
     CK_LAUNCH();
@@ -478,7 +513,7 @@ void launch_conductivity_decide(Ctx& c, const double* s, double* kappa, int eps_
 void launch_conductivity(Ctx& c, const double* s, double* kappa, int eps_mode, bool want_eps) {
     {
         PROF(c, "k_kappa");
-        launch_k(c, k_kappa, red_grid(c), TPB, 0, c.L, c.K, s, kappa, c.kappa_m, c.lam_reb, c.sc, c.M,
+        launch_k(c, k_kappa, red_blocks(c, k_kappa, c.L.cells()), TPB, 0, c.L, c.K, s, kappa, c.kappa_m, c.lam_reb, c.sc, c.M,
                                                want_eps ? eps_mode : -1, c.red, c.red_count, -1, 0, 0.0, nullptr);
         CK_LAUNCH();
     }
@@ -514,7 +549,7 @@ void launch_decide(Ctx& c, int rebuilt, int method, double eta, int step) {
 void launch_epsilon_fields(Ctx& c, const double* kn, const double* km, int mode) {
     {
         PROF(c, "k_eps_fields");
-        launch_k(c, k_eps_fields, red_grid(c), TPB, 0, c.L, kn, km, c.sc, mode, c.red, c.red_count);
+        launch_k(c, k_eps_fields, red_blocks(c, k_eps_fields, c.L.cells()), TPB, 0, c.L, kn, km, c.sc, mode, c.red, c.red_count);
         CK_LAUNCH();
     }
 }
