@@ -177,6 +177,19 @@ int mpm2p_max_outlet_saturation(mpm2p_ctx* ctx, const double* s, const double* u
 /* CellField divergence(u)                          grid.hpp:79       */
 int mpm2p_divergence(mpm2p_ctx* ctx, const double* u, double* div);
 
+/* ---- fine-reference solve (simulation.cpp:143-150) ----------------------- */
+/* LocalSolution solve_cell_centered(grid, kappa, q, bc, anchor)  elliptic.hpp
+ * (elliptic.cpp:245-250) on the whole grid: p (cells) and u (faces) of the
+ * undecomposed 5-point problem, anchor cell 0 iff every physical face is
+ * Flux. Device path: two-level-Schwarz PCG to ||r|| <= 1e-13 ||b|| (fine.cu);
+ * NumericError if it does not converge. Bumps SolveCounters::fine. */
+int mpm2p_fine_solve(mpm2p_ctx* ctx, const double* kappa, double* p, double* u);
+/* Diagnostics of the last fine solve (no reference counterpart): PCG
+ * iterations, final relative residual, and conservation_residual /
+ * residual_scale of its velocity (elliptic.cpp:252-267). Any pointer may be NULL. */
+int mpm2p_fine_stats(mpm2p_ctx* ctx, int32_t* iterations, double* relres, double* div_residual,
+                     double* div_scale);
+
 /* ---- drift test (mpm.cpp:9-29) ----------------------------------------- */
 /* double epsilon(kappa_n, kappa_m, mode)           mpm.hpp:20        */
 int mpm2p_epsilon(mpm2p_ctx* ctx, const double* kappa_n, const double* kappa_m, int32_t mode,

@@ -21,6 +21,7 @@ struct oracle_ctx {
     PerturbationState state;  // installed by oracle_mrcm_solve
     std::unique_ptr<Runner> runner;
     int64_t clamp_base = 0;
+    double fine_div_res = 0.0, fine_div_scale = 1.0;  // last oracle_fine_solve
 };
 
 namespace {
@@ -398,8 +399,22 @@ int oracle_fine_solve(oracle_ctx* ctx, const double* kappa, double* p, double* u
         const Grid& g = ctx->dd->grid;
         const int anchor = ctx->bc.pure_neumann() ? 0 : -1;
         LocalSolution s = solve_cell_centered(g, Vec(kappa, kappa + g.cells()), ctx->q, ctx->bc, anchor);
+        ctx->fine_div_res = conservation_residual(g, s, ctx->q);
+        ctx->fine_div_scale = residual_scale(g, s, ctx->q);
         copy_out(p, s.p);
         copy_out(u, s.u);
+    });
+}
+
+/* Mirror of mpm2p_fine_stats: a direct solve reports 0 iterations and 0
+ * residual; conservation_residual / residual_scale of the last solve. */
+int oracle_fine_stats(oracle_ctx* ctx, int32_t* iterations, double* relres, double* div_residual,
+                      double* div_scale) {
+    return guarded(ctx, [&] {
+        if (iterations) *iterations = 0;
+        if (relres) *relres = 0.0;
+        if (div_residual) *div_residual = ctx->fine_div_res;
+        if (div_scale) *div_scale = ctx->fine_div_scale;
     });
 }
 

@@ -88,6 +88,8 @@ PROTOTYPES = {
     "injection_rate": (C.c_int, [_vp, _dp, C.c_double, _dp]),
     "max_outlet_saturation": (C.c_int, [_vp, _dp, _dp, _dp]),
     "divergence": (C.c_int, [_vp, _dp, _dp]),
+    "fine_solve": (C.c_int, [_vp, _dp, _dp, _dp]),
+    "fine_stats": (C.c_int, [_vp, C.POINTER(C.c_int32), _dp, _dp, _dp]),
     "epsilon": (C.c_int, [_vp, _dp, _dp, C.c_int32, _dp]),
     "compute_beta": (C.c_int, [_vp, _dp, _dp, _dp, _dp]),
     "mrcm_solve": (C.c_int, [_vp, _dp, _dp, _dp, _dp, _dp, _dp, C.POINTER(DownscaleInfo), C.POINTER(Counters)]),

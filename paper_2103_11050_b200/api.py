@@ -118,7 +118,7 @@ class SplittingConfig:  # simulation.hpp:18-31
     stop_on_breakthrough: bool = False
     max_steps_hard: int = 50000
     breakthrough_threshold: float = 0.05
-    track_errors: bool = False  # fine-reference tracking is outside the GPU path
+    track_errors: bool = False  # fine-reference shadow run + flux/saturation error records (simulation.cpp:133-150)
 
 
 @dataclasses.dataclass
@@ -325,6 +325,24 @@ class Simulator:
         out = np.empty(self.cells)
         self._check(self.lib.divergence(self.h, dptr(u), dptr(out)))
         return out
+
+    # ---- fine-reference solve (simulation.cpp:143-150; elliptic.cpp:245-250) ----
+    def fine_solve(self, kappa):
+        """solve_cell_centered on the whole grid: (p cells, u faces). Anchor cell 0
+        iff every physical face is Flux. Device PCG (fine.cu), NumericError if it
+        does not converge."""
+        kappa = self._f64(kappa, self.cells)
+        p = np.empty(self.cells)
+        u = np.empty(self.faces)
+        self._check(self.lib.fine_solve(self.h, dptr(kappa), dptr(p), dptr(u)))
+        return p, u
+
+    def fine_stats(self):
+        """(iterations, relative residual, conservation_residual, residual_scale) of the last fine solve."""
+        it = C.c_int32()
+        rr, dr, ds = C.c_double(), C.c_double(), C.c_double()
+        self._check(self.lib.fine_stats(self.h, C.byref(it), C.byref(rr), C.byref(dr), C.byref(ds)))
+        return it.value, rr.value, dr.value, ds.value
 
     # ---- drift (mpm.hpp:20) ----
     def epsilon(self, kappa_n, kappa_m, mode=EPS_RELATIVE):

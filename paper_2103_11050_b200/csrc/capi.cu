@@ -33,6 +33,9 @@ struct Driver {
     std::vector<mpm2p_step_record> steps;
     long long tm_total = 0;
     double min_rcond = -1.0;
+    // FineReference method (every velocity from the fine solve) / track_errors
+    // (a fine-reference shadow run beside the multiscale one); both run eagerly
+    bool fine_ref = false, track = false;
 };
 
 }  // namespace
@@ -90,6 +93,10 @@ const Scalars& sync_scalars(Ctx& c) {
         if (e & ERR_ROBIN_BETA) throw ConfigError("CellCenteredSolver: Robin face requires beta > 0");
         if (e & ERR_PIVOT) throw NumericError("CellCenteredSolver: direct solve failed");
         if (e & ERR_EPS_ZERO) throw NumericError("epsilon: zero reference norm in relative mode");
+        if (e & ERR_TRACK_ZERO) throw NumericError("relative_flux_error: zero reference norm");
+        if (e & ERR_FINE_NOCONV)
+            throw NumericError("CellCenteredSolver: fine-grid PCG did not converge (relres " +
+                               std::to_string(c.sc_host->fine_relres) + ")");
         if (e & ERR_SINGULAR)
             throw NumericError("compute_basis_set: interface matrix is numerically singular (rcond=" +
                                std::to_string(c.sc_host->rcond) + ")");
@@ -441,6 +448,135 @@ void breakthrough_check(Driver& d, const Scalars& s) {  // simulation.cpp:253-25
     }
 }
 
+// ---- fine-reference / track_errors runs (simulation.cpp:133-150,232-329) ----
+// Eager (no graphs): the sub-cycling count of track_errors depends on both
+// CFL steps (simulation.cpp:268-272), decided on the host each step. The
+// multiscale branch, the transport and every record field are the same
+// kernels as the graph path; the fine solves are fine.cu's PCG.
+void swap_sat(Ctx& c) {
+    std::swap(c.s.p, c.s2.p);
+    c.s_par ^= 1;
+}
+
+void fine_record_extras(const Driver& d, const Scalars& s, mpm2p_step_record& r) {
+    if (d.track) {
+        r.flux_err = s.flux_err;
+        r.sat_err = s.sat_err;
+    }
+    if (d.fine_ref) r.epsilon = 0.0;
+}
+
+void fine_run_begin(Ctx& c, Driver& d, mpm2p_step_record* first, std::chrono::steady_clock::time_point t0) {
+    const mpm2p_split& sp = d.sp;
+    const size_t nc = c.L.cells(), nf = c.L.faces();
+    if (d.track) {
+        c.t_sref.alloc(nc);
+        c.t_sref2.alloc(nc);
+        c.t_kref.alloc(nc);
+        c.t_uref.alloc(nf);
+        c.t_pref.alloc(nc);
+        CK(cudaMemcpyAsync(c.t_sref.p, c.s.p, nc * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
+    }
+    launch_conductivity(c, c.s, c.kappa_n, -1, false);  // k0
+    if (d.fine_ref) {
+        fine_solve(c, c.kappa_n, c.p, c.u, true);  // p_main = p_ref, u_main = u_ref (simulation.cpp:241-249)
+    } else {
+        fine_solve(c, c.kappa_n, c.t_pref, c.t_uref, true);
+        launch_rebuild(c, c.kappa_n);
+        launch_lambda(c, c.s, c.lam_reb);
+    }
+    launch_outlet(c, c.s, c.u);
+    CK(cudaMemcpyAsync(&c.sc.p->eps_pending, &sp.eta, sizeof(double), cudaMemcpyHostToDevice, c.st));
+    launch_decide(c, 0, sp.method, sp.eta, 0);
+    if (d.track) launch_track_errors(c, c.u, c.t_uref, c.s, c.t_sref);
+    const Scalars& s = sync_scalars(c);
+    note(d, s);
+    if (!d.fine_ref) note_rcond(c, d, s.rcond);
+    Scalars s_rec = s;
+    s_rec.eps = 0.0;
+    const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    mpm2p_step_record r = make_record(c, d, s_rec, 1, 0.0, wall);
+    fine_record_extras(d, s_rec, r);
+    d.steps.push_back(r);
+    d.tm_total = 1;
+    if (first) *first = r;
+    d.n = 1;
+    d.rebuild_next = s.rebuild_next;
+    breakthrough_check(d, s);
+    d.active = true;
+}
+
+bool fine_run_step(Ctx& c, Driver& d, mpm2p_step_record* out) {
+    const mpm2p_split& sp = d.sp;
+    const auto t0 = std::chrono::steady_clock::now();
+    const int rebuilt = d.fine_ref ? 1 : d.rebuild_next;
+    if (!d.fine_ref && rebuilt) ++d.ell;
+    const double* usched = d.track ? c.t_uref.p : c.u.p;  // simulation.cpp:266
+    int sub = 1;
+    if (d.track) {
+        launch_cfl(c, c.u, sp.cfl_safety, sp.dt_cap);
+        launch_save_dt_main(c);
+    }
+    launch_cfl(c, usched, sp.cfl_safety, sp.dt_cap);
+    launch_inj_pvi(c, usched, sp.inflow_sat, sp.cn, true);  // pvi += inj dt / pore, cn times
+    if (d.track) {  // simulation.cpp:268-272
+        const Scalars& sc = sync_scalars(c);
+        const double dt = sc.dt, dtm = sc.dt_main;
+        if (dt > dtm * (1.0 + 1e-12)) sub = (int)std::ceil(dt / dtm - 1e-12);
+    }
+    c.outlet_s = nullptr;
+    for (int k = 0; k < sp.cn; ++k) {
+        for (int j = 0; j < sub; ++j) {
+            launch_upwind(c, c.s, c.s2, c.u, sp.inflow_sat, false, 0, sub);
+            swap_sat(c);
+        }
+        if (d.track) {
+            launch_upwind(c, c.t_sref, c.t_sref2, c.t_uref, sp.inflow_sat);
+            std::swap(c.t_sref.p, c.t_sref2.p);
+        }
+    }
+    try {
+        if (d.fine_ref) {
+            launch_conductivity(c, c.s, c.kappa_n, -1, false);
+            fine_solve(c, c.kappa_n, c.p, c.u);
+            launch_outlet(c, c.s, c.u);
+        } else {
+            launch_conductivity_decide(c, c.s, c.kappa_n, sp.eta_mode, rebuilt, sp.method, sp.eta);
+            launch_conductivity(c, c.t_sref, c.t_kref, -1, false);
+            fine_solve(c, c.t_kref, c.t_pref, c.t_uref);  // u_ref, p_ref (simulation.cpp:281-285)
+            c.outlet_s = c.s;
+            if (rebuilt) {
+                launch_rebuild(c, c.kappa_n);
+                launch_lambda(c, c.s, c.lam_reb);
+            } else {
+                launch_mpm(c, c.kappa_n);
+            }
+            launch_track_errors(c, c.u, c.t_uref, c.s, c.t_sref);
+        }
+    } catch (...) {
+        c.outlet_s = nullptr;
+        c.trans_fresh = false;
+        throw;
+    }
+    c.outlet_s = nullptr;
+    c.trans_fresh = false;
+    const Scalars& s = sync_scalars(c);
+    note(d, s);
+    const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    mpm2p_step_record r = make_record(c, d, s, rebuilt, s.dt, wall);
+    fine_record_extras(d, s, r);
+    d.steps.push_back(r);
+    if (rebuilt) {
+        ++d.tm_total;
+        if (!d.fine_ref) note_rcond(c, d, s.rcond);
+    }
+    if (out) *out = r;
+    d.rebuild_next = d.fine_ref ? 0 : s.rebuild_next;
+    ++d.n;
+    breakthrough_check(d, s);
+    return true;
+}
+
 void run_begin(mpm2p_ctx* ctx, const mpm2p_split* sp, const double* s0, mpm2p_step_record* first) {
     Ctx& c = ctx->c;
     Driver& d = ctx->d;
@@ -448,13 +584,13 @@ void run_begin(mpm2p_ctx* ctx, const mpm2p_split* sp, const double* s0, mpm2p_st
     if (sp->te <= 0 && sp->pvi_max <= 0.0 && !sp->stop_on_breakthrough)
         throw ConfigError("run: no stop condition configured");
     if (sp->method == MPM2P_METHOD_MPM2P && sp->eta < 0.0) throw ConfigError("run: negative eta");
-    if (sp->method == MPM2P_METHOD_FINE_REFERENCE)
-        throw ConfigError("run: the fine-reference method is outside the GPU path (use the oracle)");
-    if (sp->track_errors)
-        throw ConfigError("run: fine-reference error tracking is outside the GPU path; set track_errors = 0");
     if (!s0) throw ConfigError("run: initial saturation grid mismatch");
+    const bool multiscale = sp->method != MPM2P_METHOD_FINE_REFERENCE;  // simulation.cpp:131-133
+    if (!multiscale || sp->track_errors) fine_setup(c);  // capacity / width checks before any state changes
     d = Driver{};
     d.sp = *sp;
+    d.fine_ref = !multiscale;
+    d.track = sp->track_errors != 0 && multiscale;
     d.rec.breakthrough_step = -1;
     d.rec.breakthrough_pvi = -1.0;
     d.rec.n_sub = c.L.n_sub;
@@ -465,6 +601,10 @@ void run_begin(mpm2p_ctx* ctx, const mpm2p_split* sp, const double* s0, mpm2p_st
     reset_scalars(c);
     const auto t0 = std::chrono::steady_clock::now();
     upload(c, c.s, s0, c.L.cells());
+    if (d.fine_ref || d.track) {
+        fine_run_begin(c, d, first, t0);
+        return;
+    }
     // every pressure update of the run also forms the next step's CFL dt
     c.cfl_fused = true;
     c.cfl_safety = sp->cfl_safety;
@@ -502,6 +642,7 @@ bool run_step(mpm2p_ctx* ctx, mpm2p_step_record* out) {
     if (sp.pvi_max > 0.0 && c.sc_host->pvi >= sp.pvi_max) return false;
     if (sp.stop_on_breakthrough && d.rec.breakthrough_step >= 0) return false;
     if (d.n >= sp.max_steps_hard) return false;
+    if (d.fine_ref || d.track) return fine_run_step(c, d, out);
     const auto t0 = std::chrono::steady_clock::now();
     const int rebuilt = d.rebuild_next;
     if (rebuilt) ++d.ell;
@@ -750,6 +891,31 @@ int mpm2p_max_outlet_saturation(mpm2p_ctx* ctx, const double* s, const double* u
         upload(c, b, u, c.L.faces());
         launch_outlet(c, a, b);
         *out = sync_scalars(c).outlet_max;
+    });
+}
+
+int mpm2p_fine_solve(mpm2p_ctx* ctx, const double* kappa, double* p, double* u) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        auto& a = scratch(ctx->scratch_a, c.L.cells());
+        auto& pb = scratch(ctx->scratch_b, c.L.cells());
+        auto& ub = scratch(ctx->scratch_c, c.L.faces());
+        upload(c, a, kappa, c.L.cells());
+        fine_solve(c, a, pb, ub, true);
+        download(c, p, pb, c.L.cells());
+        download(c, u, ub, c.L.faces());
+        sync_scalars(c);
+    });
+}
+
+int mpm2p_fine_stats(mpm2p_ctx* ctx, int32_t* iterations, double* relres, double* div_residual,
+                     double* div_scale) {
+    return guarded(ctx, [&] {
+        const Scalars& s = sync_scalars(ctx->c);
+        if (iterations) *iterations = s.fine_iters;
+        if (relres) *relres = s.fine_relres;
+        if (div_residual) *div_residual = s.div_residual;
+        if (div_scale) *div_scale = s.div_scale;
     });
 }
 

@@ -30,7 +30,9 @@ enum : unsigned {
     ERR_SINGULAR = 1u << 3,     // interface matrix numerically singular (mrcm.cpp:227-238)
     ERR_EPS_ZERO = 1u << 4,     // epsilon: zero reference norm (mpm.cpp:23)
     ERR_ROBIN_BETA = 1u << 5,   // Robin face requires beta > 0 (elliptic.cpp:134-135)
-    ERR_REPAIR_SINGULAR = 1u << 6
+    ERR_REPAIR_SINGULAR = 1u << 6,
+    ERR_FINE_NOCONV = 1u << 7,  // fine-reference PCG did not reach its tolerance (fine.cu)
+    ERR_TRACK_ZERO = 1u << 8    // relative_flux/sat_error: zero reference norm (simulation.cpp:37-41,53-57)
 };
 
 inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }

@@ -29,8 +29,11 @@ struct Scalars {
     int kr_iters_max, kr_solves;
     double dt_next, inj_next;  // next step's cfl_timestep / injection_rate (k_ds_u_div with CflNext)
     int any_next;
-    int pad_i;
-    double pad[3];
+    int fine_iters;            // PCG iterations of the last fine solve (fine.cu)
+    double fine_relres;        // its final ||r|| / ||b||
+    long long fine_iters_total;
+    double dt_main;            // track_errors: cfl_timestep of u_main (sub-cycling, simulation.cpp:270-272)
+    double flux_err, sat_err;  // track_errors records (simulation.cpp:30-59,210-215)
 };
 
 template <typename T>
@@ -129,7 +132,18 @@ struct Ctx {
     // (CflNext) instead of a separate k_cfl pass.
     bool cfl_fused = false;
     double cfl_safety = 0.0, cfl_dt_cap = 0.0, cfl_inflow = 0.0;
-    std::unordered_map<const void*, int> occ;  // resident blocks / SM per grid-stride kernel (TPB threads)
+    std::unordered_map<const void*, int> occ;
+    // fine-reference solve (fine.cu): global transmissibilities, blocked band
+    // rows / factors of the block-Jacobi preconditioner, CG vectors (blocked
+    // order; f_x is the warm start), coarse operator and its inverse
+    DevBuf<double> f_T, f_BD, f_BW, f_BS, f_D, f_Lc, f_Lr, f_b, f_x, f_r, f_p, f_q, f_y;
+    DevBuf<double> f_A0, f_A0i, f_c0, f_e, f_part;
+    bool f_ready = false, f_warm = false;
+    int f_anchor = -1;
+    double f_tol = 1e-13;
+    // track_errors / fine-reference runs: reference saturation (ping-pong),
+    // its conductivity and the fine solution (simulation.cpp:133-150)
+    DevBuf<double> t_sref, t_sref2, t_kref, t_uref, t_pref;  // resident blocks / SM per grid-stride kernel (TPB threads)
     bool trans_fresh = false;  // T already matches kappa_n (set by the driver's fused k_kappa)
     bool refine = true;        // one refinement step in MPM-2P interface solves (decided per rebuild from rcond)
     bool force_refine = false; // MPM2P_REFINE=1: always refine
@@ -269,7 +283,9 @@ void launch_max_slope(Ctx& c);
 void launch_cfl(Ctx& c, const double* u, double safety, double dt_cap);
 void launch_inj_pvi(Ctx& c, const double* u, double inflow, int cn, bool add_pvi);
 void launch_upwind(Ctx& c, const double* s_in, double* s_out, const double* u, double inflow, bool take_next = false,
-                   int inj_cn = 0);
+                   int inj_cn = 0, int sub = 1);
+void launch_track_errors(Ctx& c, const double* u, const double* ur, const double* s, const double* sr);
+void launch_save_dt_main(Ctx& c);  // sc->dt_main = sc->dt
 void launch_conductivity(Ctx& c, const double* s, double* kappa, int eps_mode, bool want_eps);
 void launch_cfl_inj(Ctx& c, const double* u, double safety, double dt_cap, double inflow, int cn);
 void launch_conductivity_decide(Ctx& c, const double* s, double* kappa, int eps_mode, int rebuilt, int method,
@@ -305,6 +321,10 @@ void interface_inverse_async(Ctx& c, const double* M, double* Minv, int n, doubl
                              double threshold);
 // SPD matrix (repair Laplacian): pivot-free blocked GJ; returns rcond.
 double spd_inverse(Ctx& c, const double* A, double* Ainv, int n);
+void block_gj_inplace_pub(Ctx& c, double* W, int n);  // SPD / quasi-definite, pivot-free, in place
+// ---- fine-reference solve (fine.cu) ------------------------------------------
+void fine_setup(Ctx& c);
+void fine_solve(Ctx& c, const double* kappa, double* p, double* u, bool cold = false);
 void launch_gemv(Ctx& c, const double* A, const double* x, double* y, int n);
 void launch_gemv_acc(Ctx& c, const double* A, const double* x, double* y, int n);  // y += A x
 void launch_csr_residual(Ctx& c, const int* ptr, const int* col, const double* val, const double* x,

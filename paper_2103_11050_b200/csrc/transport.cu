@@ -232,12 +232,14 @@ __global__ void k_inj_pvi(Layout L, const double* __restrict__ u, Scalars* sc, d
 // previous pressure update's k_ds_u_div (CflNext); this first sub-step reads
 // dt_next and thread 0 promotes it (dt, any_flow, inj) and advances the PVI
 // clock inj_cn times exactly as k_cfl's epilogue does.
+// sub > 1: the track_errors sub-cycling of s_main, dt / sub per sub-step
+// (simulation.cpp:270-276).
 __global__ void k_upwind(Layout L, const double* __restrict__ s, double* __restrict__ s_out,
                          const double* __restrict__ u, Scalars* sc, double inflow, double M, int take_next = 0,
-                         int inj_cn = 0) {
+                         int inj_cn = 0, int sub = 1) {
     pdl_begin();
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    const double dt = take_next ? sc->dt_next : sc->dt;
+    const double dt = take_next ? sc->dt_next : (sub > 1 ? sc->dt / sub : sc->dt);
     if (c == 0) {
         (void)frac_flow(inflow, M, &sc->clamp);  // f_in is evaluated once per call
         if (take_next) {
@@ -465,6 +467,64 @@ __global__ void k_lambda(Layout L, const double* __restrict__ s, double* __restr
 }
 
 
+
+// relative_flux_error / relative_sat_error (simulation.cpp:30-59) in
+// double-double: area-weighted L2 of u - u_ref over all faces, L1 of
+// s - s_ref over cells, each relative to the reference's norm.
+__global__ void k_track_errors(Layout L, const double* __restrict__ u, const double* __restrict__ ur,
+                               const double* __restrict__ s, const double* __restrict__ sr, Scalars* sc,
+                               double* part, unsigned* counter) {
+    pdl_begin();
+    DD fn{0.0, 0.0}, fd{0.0, 0.0}, sn{0.0, 0.0}, sd{0.0, 0.0};
+    const int nf = L.faces(), nc = L.cells();
+    for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < nf; f += gridDim.x * blockDim.x) {
+        const double w = L.area(f), d = u[f] - ur[f];
+        fn = dd_add(fn, DD{w * d * d, 0.0});
+        fd = dd_add(fd, DD{w * ur[f] * ur[f], 0.0});
+        if (f < nc) {
+            sn = dd_add(sn, DD{fabs(s[f] - sr[f]), 0.0});
+            sd = dd_add(sd, DD{fabs(sr[f]), 0.0});
+        }
+    }
+    __shared__ DD shd[64];
+    block_reduce_dd2(fn, fd, shd);
+    block_reduce_dd2(sn, sd, shd);
+    if (threadIdx.x == 0) {
+        double* pp = part + 8 * blockIdx.x;
+        pp[0] = fn.hi; pp[1] = fn.lo; pp[2] = fd.hi; pp[3] = fd.lo;
+        pp[4] = sn.hi; pp[5] = sn.lo; pp[6] = sd.hi; pp[7] = sd.lo;
+    }
+    if (!last_block_done(counter)) return;
+    DD a{0.0, 0.0}, b{0.0, 0.0}, e{0.0, 0.0}, g{0.0, 0.0};
+    for (int k = threadIdx.x; k < (int)gridDim.x; k += blockDim.x) {
+        const double* pp = part + 8 * k;
+        a = dd_add(a, DD{__ldcg(pp + 0), __ldcg(pp + 1)});
+        b = dd_add(b, DD{__ldcg(pp + 2), __ldcg(pp + 3)});
+        e = dd_add(e, DD{__ldcg(pp + 4), __ldcg(pp + 5)});
+        g = dd_add(g, DD{__ldcg(pp + 6), __ldcg(pp + 7)});
+    }
+    block_reduce_dd2(a, b, shd);
+    block_reduce_dd2(e, g, shd);
+    if (threadIdx.x == 0) {
+        const double num = a.hi + a.lo, den = b.hi + b.lo, sn2 = e.hi + e.lo, sd2 = g.hi + g.lo;
+        if (!(den > 0.0)) {
+            sc->flux_err = 0.0;
+            if (num != 0.0) atomicOr(&sc->err, ERR_TRACK_ZERO);
+        } else {
+            sc->flux_err = sqrt(num / den);
+        }
+        if (sn2 == 0.0) sc->sat_err = 0.0;  // simulation.cpp:219-221: exact agreement reports 0
+        else if (!(sd2 > 0.0)) atomicOr(&sc->err, ERR_TRACK_ZERO);
+        else sc->sat_err = sn2 / sd2;
+        *counter = 0;
+    }
+}
+
+__global__ void k_save_dt_main(Scalars* sc) {
+    pdl_begin();
+    sc->dt_main = sc->dt;
+}
+
 }  // namespace
 
 void launch_max_slope(Ctx& c) {
@@ -489,11 +549,11 @@ void launch_inj_pvi(Ctx& c, const double* u, double inflow, int cn, bool add_pvi
     }
 }
 void launch_upwind(Ctx& c, const double* s_in, double* s_out, const double* u, double inflow, bool take_next,
-                   int inj_cn) {
+                   int inj_cn, int sub) {
     {
         PROF(c, "k_upwind");
         launch_k(c, k_upwind, cdiv(c.L.cells(), TPB), TPB, 0, c.L, s_in, s_out, u, c.sc, inflow, c.M, take_next ? 1 : 0,
-                 inj_cn);
+                 inj_cn, sub);
         CK_LAUNCH();
     }
 }
@@ -554,4 +614,18 @@ void launch_epsilon_fields(Ctx& c, const double* kn, const double* km, int mode)
     }
 }
 
+}  // namespace mpm2p
+
+namespace mpm2p {
+void launch_track_errors(Ctx& c, const double* u, const double* ur, const double* s, const double* sr) {
+    PROF(c, "k_track_errors");
+    launch_k(c, k_track_errors, red_blocks(c, k_track_errors, c.L.faces()), TPB, 0, c.L, u, ur, s, sr, c.sc, c.red,
+             c.red_count);
+    CK_LAUNCH();
+}
+void launch_save_dt_main(Ctx& c) {
+    PROF(c, "k_save_dt_main");
+    launch_k(c, k_save_dt_main, 1, 1, 0, c.sc.p);
+    CK_LAUNCH();
+}
 }  // namespace mpm2p
