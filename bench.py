@@ -126,6 +126,8 @@ def kernel_work(name, cfg, sz, dim):
         "k_kappa": ("hbm", 32.0 * cells),                        # s, K, kappa_m, kappa
         "k_part_solve": ("hbm", ns * n * (16.0 * B + 24.0)),     # Lcol, Lrow, D, x r/w
         "k_ds_solve": ("fp64", ns * (n * B * B + 4.0 * n * B)),  # banded LDL^T factor + 2 sweeps
+        "k_ds_factor": ("fp64", ns * n * B * B),                # split downscale: factor (side stream)
+        "k_ds_sweep": ("hbm", ns * n * (16.0 * B + 24.0)),       # split downscale: 2 sweeps with the stored factor
         "k_factor_solve": ("fp64", ns * (n * B * B + 4.0 * n * B * (1 + sz.nhat / max(ns, 1)))),
         "k_gemv": ("hbm", 8.0 * dim * dim),
         "k_mpm_rhs": ("hbm", 56.0 * cells),

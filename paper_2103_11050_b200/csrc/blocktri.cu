@@ -128,31 +128,75 @@ __global__ void k_bt_unpermute(const double* __restrict__ xb, int n, const int* 
     x[r] = xb[voff[blk[r]] + loc[r]];
 }
 
+// The block steps of a solve are a dependent chain of small products, each
+// latency-bound (one L2/HBM round trip for the block plus the launch). The
+// matrices are constant between rebuilds, so each kernel loads its rows into
+// registers BEFORE griddepcontrol.wait and triggers its dependents at entry:
+// launched with programmatic dependent launch (bt_solve), step j+1's block
+// streams in while step j finishes, and only the vector part is serialised.
+constexpr int BT_NPL = 24;  // prefetched doubles per lane: rows of up to 768 columns
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <int NPL>
+__device__ __forceinline__ void bt_row_prefetch(double (&v)[NPL], const double* row, int cols, bool on, int lane) {
+#pragma unroll
+    for (int q = 0; q < NPL; ++q) {
+        const int c = lane + 32 * q;
+        v[q] = (on && c < cols) ? __ldg(row + c) : 0.0;
+    }
+}
+template <int NPL>
+__device__ __forceinline__ double bt_row_dot(const double (&v)[NPL], const double* row, int cols, const double* x,
+                                             double acc, int lane) {
+#pragma unroll
+    for (int q = 0; q < NPL; ++q) {
+        const int c = lane + 32 * q;
+        if (c < cols) acc = fma(v[q], __ldcg(x + c), acc);
+    }
+    for (int c = lane + 32 * NPL; c < cols; c += 32) acc = fma(row[c], __ldcg(x + c), acc);  // wider blocks
+    return acc;
+}
+
 // y_j -= G y_{j-1} (G = T_{j-1}^T, rows x cols), one warp per row
-__global__ void k_bt_fwd(const double* __restrict__ G, int rows, int cols, const double* __restrict__ yprev,
-                         double* __restrict__ y) {
-    pdl_begin();
+__global__ void k_bt_fwd(const double* __restrict__ G, int rows, int cols, const double* yprev,
+                         double* y) {
+    pdl_trigger();
     const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-    if (row >= rows) return;
-    const double* g = G + (size_t)row * cols;
-    double acc = 0.0;
-    for (int c = lane; c < cols; c += 32) acc = fma(g[c], yprev[c], acc);
+    const bool on = row < rows;
+    const double* g = G + (size_t)(on ? row : 0) * cols;
+    double gv[BT_NPL];
+    bt_row_prefetch(gv, g, cols, on, lane);
+    pdl_begin();  // y_{j-1} is complete and visible
+    if (!on) return;
+    double acc = bt_row_dot(gv, g, cols, yprev, 0.0, lane);
     acc = warp_sum(acc);
     if (lane == 0) y[row] -= acc;
 }
 
 // x_j = Sinv_j y_j - T_j x_{j+1} (T_j: rows x cols_next), one warp per row
 __global__ void k_bt_bwd(const double* __restrict__ Sinv, const double* __restrict__ T, int rows, int cols_next,
-                         const double* __restrict__ y, const double* __restrict__ xnext, double* __restrict__ x) {
-    pdl_begin();
+                         const double* y, const double* xnext, double* x) {
+    pdl_trigger();
     const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-    if (row >= rows) return;
-    const double* s = Sinv + (size_t)row * rows;
-    double acc = 0.0;
-    for (int c = lane; c < rows; c += 32) acc = fma(s[c], y[c], acc);
+    const bool on = row < rows;
+    const double* s = Sinv + (size_t)(on ? row : 0) * rows;
+    const double* t = T ? T + (size_t)(on ? row : 0) * cols_next : nullptr;
+    double sv[BT_NPL], tv[BT_NPL];
+    bt_row_prefetch(sv, s, rows, on, lane);
+    bt_row_prefetch(tv, t, T ? cols_next : 0, on && T, lane);
+    pdl_begin();  // x_{j+1} is complete and visible (y_j was finished by the forward sweep)
+    if (!on) return;
+    double acc = bt_row_dot(sv, s, rows, y, 0.0, lane);
     if (T) {
-        const double* t = T + (size_t)row * cols_next;
-        for (int c = lane; c < cols_next; c += 32) acc = fma(-t[c], xnext[c], acc);
+#pragma unroll
+        for (int q = 0; q < BT_NPL; ++q) tv[q] = -tv[q];
+        // same operation order as acc = fma(-t[c], xnext[c], acc) over c
+#pragma unroll
+        for (int q = 0; q < BT_NPL; ++q) {
+            const int c = lane + 32 * q;
+            if (c < cols_next) acc = fma(tv[q], __ldcg(xnext + c), acc);
+        }
+        for (int c = lane + 32 * BT_NPL; c < cols_next; c += 32) acc = fma(-t[c], __ldcg(xnext + c), acc);
     }
     acc = warp_sum(acc);
     if (lane == 0) x[row] = acc;
@@ -268,11 +312,25 @@ void bt_solve(Ctx& c, const double* rhs, double* x) {
         launch_k(c, k_bt_gather, cdiv(n, TPB), TPB, 0, rhs, n, c.bt_blk, c.bt_loc, c.bt_voffd, y);
         CK_LAUNCH();
     }
+    // block steps with programmatic dependent launch (see k_bt_fwd)
+    auto launch_pdl = [&](auto kern, int grid, auto... args) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(TPB);
+        cfg.dynamicSmemBytes = 0;
+        cfg.stream = c.st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = c.bt_pdl ? 1 : 0;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        CK(cudaLaunchKernelEx(&cfg, kern, args...));
+    };
     for (int j = 1; j < nb; ++j) {
         const int s = c.bt_sz[j], sp = c.bt_sz[j - 1];
         PROF(c, "k_bt_fwd");
-        launch_k(c, k_bt_fwd, cdiv((long long)s * 32, TPB), TPB, 0, c.bt_G.p + c.bt_eoff[j - 1], s, sp,
-                 y + c.bt_voff[j - 1], y + c.bt_voff[j]);
+        launch_pdl(k_bt_fwd, cdiv((long long)s * 32, TPB), (const double*)(c.bt_G.p + c.bt_eoff[j - 1]), s, sp,
+                   (const double*)(y + c.bt_voff[j - 1]), y + c.bt_voff[j]);
         CK_LAUNCH();
     }
     for (int j = nb - 1; j >= 0; --j) {
@@ -280,9 +338,9 @@ void bt_solve(Ctx& c, const double* rhs, double* x) {
         const bool last = j == nb - 1;
         const int sn = last ? 0 : c.bt_sz[j + 1];
         PROF(c, "k_bt_bwd");
-        launch_k(c, k_bt_bwd, cdiv((long long)s * 32, TPB), TPB, 0, c.bt_Sinv.p + c.bt_doff[j],
-                 last ? nullptr : c.bt_T.p + c.bt_eoff[j], s, sn, y + c.bt_voff[j], last ? nullptr : xb + c.bt_voff[j + 1],
-                 xb + c.bt_voff[j]);
+        launch_pdl(k_bt_bwd, cdiv((long long)s * 32, TPB), (const double*)(c.bt_Sinv.p + c.bt_doff[j]),
+                   (const double*)(last ? nullptr : c.bt_T.p + c.bt_eoff[j]), s, sn, (const double*)(y + c.bt_voff[j]),
+                   (const double*)(last ? nullptr : xb + c.bt_voff[j + 1]), xb + c.bt_voff[j]);
         CK_LAUNCH();
     }
     {

@@ -264,6 +264,7 @@ void create_ctx(mpm2p_ctx* ctx, const mpm2p_problem* P) {
     if (const char* e = std::getenv("MPM2P_GJ")) c.gj_legacy = std::strcmp(e, "legacy") == 0;
     if (const char* e = std::getenv("MPM2P_NO_TWIST")) c.no_twist = e[0] == '1';
     if (const char* e = std::getenv("MPM2P_PDL")) c.pdl = e[0] == '1';
+    if (const char* e = std::getenv("MPM2P_BT_PDL")) c.bt_pdl = e[0] != '0';
     if (const char* e = std::getenv("MPM2P_REFINE")) {  // 1: always refine, 0: never (experiments)
         c.force_refine = e[0] == '1';
         c.never_refine = e[0] == '0';
@@ -366,6 +367,21 @@ void create_ctx(mpm2p_ctx* ctx, const mpm2p_problem* P) {
     if (c.twist_store) {
         c.tw_midb.alloc(ns * B * B);
         c.tw_sinv.alloc(ns * B * B);
+    }
+    // B <= 20: at B = 32 (C4) the stored two-sided factor doubles the
+    // downscale's factor traffic and the side-stream factor competes with the
+    // particular solve (measured C4 362 -> 400 us per step; C2 140 -> 127, C3 202 -> 165)
+    c.ds_split = c.twist_store && L.snx <= 20;
+    if (const char* e = std::getenv("MPM2P_DS_SPLIT")) c.ds_split = c.ds_split && e[0] != '0';
+    if (c.ds_split) {
+        CK(cudaStreamCreateWithFlags(&c.st2, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming));
+        c.Lcd.alloc(ns * ncs * B);
+        c.ds_midb.alloc(ns * B * B);
+        c.ds_sinv.alloc(ns * B * B);
+        c.ds_yscr.alloc(ns * ncs);
+        c.ds_yscr.zero(c.st);
     }
     c.sc.alloc(1);
     c.red.alloc(16 * 8 * (size_t)c.num_sms + 4096);  // <= 16 values x 8 resident blocks / SM (red_blocks)
@@ -801,9 +817,12 @@ void mpm2p_destroy(mpm2p_ctx* ctx) {
     for (cudaEvent_t e : ctx->c.timers)
         if (e) cudaEventDestroy(e);
     ctx->c.drop_graphs();
-    cudaStream_t st = ctx->c.st;
+    if (ctx->c.ev_fork) cudaEventDestroy(ctx->c.ev_fork);
+    if (ctx->c.ev_join) cudaEventDestroy(ctx->c.ev_join);
+    cudaStream_t st = ctx->c.st, st2 = ctx->c.st2;
     delete ctx;
     if (st) cudaStreamDestroy(st);
+    if (st2) cudaStreamDestroy(st2);
 }
 
 const char* mpm2p_last_error(const mpm2p_ctx* ctx) { return ctx ? ctx->c.err.c_str() : g_create_err.c_str(); }

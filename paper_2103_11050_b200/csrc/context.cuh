@@ -94,7 +94,7 @@ struct Ctx {
     // interface system (CSR pattern built once; values per rebuild)
     DevBuf<int> csr_ptr, csr_col, csr_row, csr_tpos;  // tpos[z]: position of the transposed entry
     DevBuf<double> csr_val, Mdense, Minv, gj_work, gj_col, gj_row, gj_krow;
-    DevBuf<int> gj_piv;
+    DevBuf<int> gj_piv, gj_aux;
     DevBuf<double> gj_pp;     // ping-pong GJ: two padded copies + two 32 x 32 pivot inverses
     bool gj_legacy = false;   // MPM2P_GJ=legacy: the two-barrier k_block_gj
     DevBuf<double> irhs, icoef, ires, idelta;
@@ -109,6 +109,7 @@ struct Ctx {
     // K7b direct block-tridiagonal interface solve (blocktri.cu): the default
     // above the dense limit; MPM2P_IFACE=blocktri forces it, =krylov selects MINRES
     bool use_blocktri = false;
+    bool bt_pdl = true;  // programmatic dependent launch of the block steps (MPM2P_BT_PDL=0 disables)
     int bt_nblk = 0;
     std::vector<int> bt_sz, bt_voff;
     std::vector<long long> bt_doff, bt_eoff;
@@ -119,6 +120,14 @@ struct Ctx {
     DevBuf<double> X, PU, PB, PS, GZ, WU, RU, RS, skel, resid, delta, corr;
     // downscale
     DevBuf<double> BDd, BWd, BSd, Dd, Lrd, Xd;
+    // split downscale (latency regime): the kappa_n operator is factored on a
+    // side stream (st2) while the particular / interface / recon chain runs;
+    // only the two sweeps stay on the critical path
+    bool ds_split = false;
+    bool ds_pending = false;  // a forked factor awaits its join (ev_join)
+    cudaStream_t st2 = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    DevBuf<double> Lcd, ds_midb, ds_sinv, ds_yscr;
     // scalars and reduction workspace
     DevBuf<Scalars> sc;
     DevBuf<double> red;

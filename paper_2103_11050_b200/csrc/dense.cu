@@ -354,6 +354,7 @@ struct PPArgs {
     int ld;     // = npad = nb * 32
     int nb, nch, cpb;
     int* singular;
+    int* aux;  // [0] the lookahead CTA's SM id, [1] the worker CTA sharing that SM (-1: none)
     unsigned long long* trace;  // optional (MPM2P_GJ_TRACE=1): per-step %globaltimer marks
 };
 typedef double PPTile[PPB][PPB + 1];
@@ -372,6 +373,31 @@ __device__ __forceinline__ void pp_load(PPTile S, const double* g, int ld) {
         const int x = threadIdx.x + 256 * q;
         v[q] = __ldcg(g + (size_t)(x >> 5) * ld + (x & 31));
     }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int x = threadIdx.x + 256 * q;
+        S[x >> 5][x & 31] = v[q];
+    }
+}
+// D += A B on the fp64 tensor cores (mma.sync m8n8k4, DMMA): A 8 x 4 row-major,
+// lane l holds A[l / 4][l % 4]; B 4 x 8, lane l holds B[l % 4][l / 4]; C/D
+// 8 x 8, lane l holds D[l / 4][2 (l % 4) + {0, 1}].
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+// Split load: every thread's four loads of a 32 x 32 tile into registers
+// (pp_fetch), later stored to shared memory (pp_put), so several tiles'
+// loads are in flight together (one L2 round trip for all of them).
+__device__ __forceinline__ void pp_fetch(double (&v)[4], const double* g, int ld) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int x = threadIdx.x + 256 * q;
+        v[q] = __ldcg(g + (size_t)(x >> 5) * ld + (x & 31));
+    }
+}
+__device__ __forceinline__ void pp_put(PPTile S, const double (&v)[4]) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         const int x = threadIdx.x + 256 * q;
@@ -442,7 +468,8 @@ __device__ void pp_invert(PPTile S, double* xb, int* singular) {
 // Dynamic shared memory of k_gj_pp: four 32 x 33 tiles, a 32 x 128 slice of
 // the pivot block row, and the pivot row/column exchange buffers.
 constexpr int PPW = 128;  // columns per work item (4 blocks)
-constexpr size_t PP_SMEM = (4 * PPB * (PPB + 1) + PPB * PPW + 2 * PPB + 4 * 2 * 8) * sizeof(double);
+constexpr int PWS = PPW + 8;  // padded row stride of the pivot block-row slice (conflict-free DMMA B loads)
+constexpr size_t PP_SMEM = (4 * PPB * (PPB + 1) + PPB * PWS + 2 * PPB + 4 * 2 * 8) * sizeof(double);
 
 __global__ void __launch_bounds__(256, 2) k_gj_pp(PPArgs a) {
     pdl_begin();
@@ -452,14 +479,19 @@ __global__ void __launch_bounds__(256, 2) k_gj_pp(PPArgs a) {
     PPTile& Cs = *reinterpret_cast<PPTile*>(pp_sm + PPB * (PPB + 1));
     PPTile& Ts = *reinterpret_cast<PPTile*>(pp_sm + 2 * PPB * (PPB + 1));
     PPTile& Bs = *reinterpret_cast<PPTile*>(pp_sm + 3 * PPB * (PPB + 1));
-    double* Ws = pp_sm + 4 * PPB * (PPB + 1);  // 32 x 128, row-major
-    double* xrow = Ws + PPB * PPW;  // pivot-row exchange (2 x 32, 16-byte aligned)
+    double* Ws = pp_sm + 4 * PPB * (PPB + 1);  // 32 x 128, row-major, row stride PWS
+    double* xrow = Ws + PPB * PWS;  // pivot-row exchange (2 x 32, 16-byte aligned)
     const int ld = a.ld, nb = a.nb, np = nb * PPB;
     const int r = threadIdx.x >> 3, c0 = threadIdx.x & 7;
-    const int wy = threadIdx.x >> 5, wx = threadIdx.x & 31;  // 4 x 4 register tile: rows 4 wy.., cols wx + 32 m
+    // DMMA (mma.m8n8k4.f64) fragments: warp w owns rows 8 (w & 3).. of the item and
+    // columns 64 (w >> 2).. (eight 8 x 8 tiles); lane (lr, lc) = (lane / 4, lane % 4)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int lr = lane >> 2, lc = lane & 3, rg = warp & 3, ch = warp >> 2;
     const bool look = blockIdx.x == gridDim.x - 1;
-    const int nwork = gridDim.x - 1;
     const int nch = (np + PPW - 1) / PPW;
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    if (look && threadIdx.x == 0) a.aux[0] = (int)smid;
     auto blk = [&](double* W, int I, int J) { return W + (size_t)I * PPB * ld + (size_t)J * PPB; };
     auto pslot = [&](int k) { return a.P + (size_t)(k & 1) * PPB * PPB; };
     if (look) {  // P_0
@@ -469,24 +501,38 @@ __global__ void __launch_bounds__(256, 2) k_gj_pp(PPArgs a) {
         for (int x = threadIdx.x; x < PPB * PPB; x += blockDim.x) pslot(0)[x] = Cs[x >> 5][x & 31];
     }
     grid.sync();
+    // The lookahead chain (load, two 32^3 products, a 32-pivot inverse) is the
+    // critical path of every step; a worker CTA on the same SM competes for
+    // its shared-memory and FP64 issue slots (measured: prep 3.2 -> 6.0 us).
+    // That worker sits the steps out; the others take its items.
+    if (!look && gridDim.x > 2 && threadIdx.x == 0 && __ldcg(a.aux) == (int)smid) a.aux[1] = (int)blockIdx.x;
+    grid.sync();
+    const int idle = __ldcg(a.aux + 1);
+    const int nwork = gridDim.x - 1 - (idle >= 0 ? 1 : 0);
+    const int widx = (idle >= 0 && (int)blockIdx.x > idle) ? (int)blockIdx.x - 1 : (int)blockIdx.x;
+    const bool works = !look && (int)blockIdx.x != idle;
     for (int k = 0; k < nb; ++k) {
         double* src = (k & 1) ? a.W1 : a.W0;
         double* dst = (k & 1) ? a.W0 : a.W1;
         auto mark = [&](int slot) {
             if (a.trace && threadIdx.x == 0) a.trace[(size_t)k * 8 + slot] = gtimer();
         };
-        pp_load(Ps, pslot(k), PPB);
+        double pv[4];
+        pp_fetch(pv, pslot(k), PPB);  // P_k: put into Ps together with each branch's first loads
         if (look) mark(0);
         if (!look && blockIdx.x == 0) mark(5);
         if (look) {
             if (k + 1 < nb) {  // next pivot block: W_{k+1,k+1} - (W_{k+1,k} P_k) W_{k,k+1}, inverted
-                // all inputs in one round of loads (P_k was loaded above)
+                // all inputs (P_k, W_{k+1,k+1}, W_{k+1,k}, W_{k,k+1}) in one round of loads
                 const double* g = blk(src, k + 1, k + 1);
-                double gv[4];
+                double gv[4], cv[4], bv[4];
 #pragma unroll
                 for (int m = 0; m < 4; ++m) gv[m] = __ldcg(g + (size_t)r * ld + c0 + 8 * m);
-                pp_load(Cs, blk(src, k + 1, k), ld);
-                pp_load(Bs, blk(src, k, k + 1), ld);
+                pp_fetch(cv, blk(src, k + 1, k), ld);
+                pp_fetch(bv, blk(src, k, k + 1), ld);
+                pp_put(Ps, pv);
+                pp_put(Cs, cv);
+                pp_put(Bs, bv);
                 __syncthreads();
                 double t[4];
                 pp_mul(Cs, Ps, t);
@@ -506,71 +552,80 @@ __global__ void __launch_bounds__(256, 2) k_gj_pp(PPArgs a) {
                 for (int x = threadIdx.x; x < PPB * PPB; x += blockDim.x) pslot(k + 1)[x] = Cs[x >> 5][x & 31];
                 mark(3);
             }
-        } else {
-            for (int item = blockIdx.x; item < nb * nch; item += nwork) {
+        } else if (works) {
+            for (int item = widx; item < nb * nch; item += nwork) {
                 const int i = item / nch, q = item % nch;
                 const int col0 = q * PPW;
-                // this thread's 4 x 4 source values, issued first (used last)
-                double gsrc[4][4];
+                const int row = rg * 8 + lr;  // this lane's output row in the block row
+                // this lane's source values (the C fragments' positions), issued first, used last
+                double2 gsrc[8];
 #pragma unroll
-                for (int a2 = 0; a2 < 4; ++a2)
-#pragma unroll
-                    for (int m = 0; m < 4; ++m) {
-                        const int col = col0 + wx + 32 * m;
-                        gsrc[a2][m] = col < np ? __ldcg(src + (size_t)(i * PPB + 4 * wy + a2) * ld + col) : 0.0;
-                    }
-                __syncthreads();  // previous item's readers of Cs / Ts / Ws are done
-                if (i != k) pp_load(Cs, blk(src, i, k), ld);
-                {  // pivot block-row slice W_k,[col0, col0+128) (columns past np read as 0), loads batched
+                for (int cg = 0; cg < 8; ++cg) {
+                    const int col = col0 + ch * 64 + cg * 8 + lc * 2;
+                    gsrc[cg] = col < np ? __ldcg(reinterpret_cast<const double2*>(src + (size_t)(i * PPB + row) * ld + col))
+                                        : make_double2(0.0, 0.0);
+                }
+                {  // W_ik and the pivot block-row slice W_k,[col0, col0+128) (columns past np
+                   // read as 0): issued with gsrc's loads, one L2 round trip per item
+                    double cv[4];
+                    if (i != k) pp_fetch(cv, blk(src, i, k), ld);
                     double v[PPB * PPW / 256];
 #pragma unroll
-                    for (int q = 0; q < PPB * PPW / 256; ++q) {
-                        const int x = threadIdx.x + 256 * q, rr = x / PPW, cc = col0 + x % PPW;
-                        v[q] = cc < np ? __ldcg(src + (size_t)(k * PPB + rr) * ld + cc) : 0.0;
+                    for (int qq = 0; qq < PPB * PPW / 256; ++qq) {
+                        const int x = threadIdx.x + 256 * qq, rr = x / PPW, cc = col0 + x % PPW;
+                        v[qq] = cc < np ? __ldcg(src + (size_t)(k * PPB + rr) * ld + cc) : 0.0;
                     }
+                    __syncthreads();  // previous item's readers of Ps / Cs / Ts / Ws are done
+                    if (item == widx) pp_put(Ps, pv);
+                    if (i != k) pp_put(Cs, cv);
 #pragma unroll
-                    for (int q = 0; q < PPB * PPW / 256; ++q) Ws[threadIdx.x + 256 * q] = v[q];
+                    for (int qq = 0; qq < PPB * PPW / 256; ++qq) {
+                        const int x = threadIdx.x + 256 * qq;
+                        Ws[(x / PPW) * PWS + x % PPW] = v[qq];
+                    }
                 }
                 __syncthreads();
-                if (i != k) {  // T = W_ik P_k
-                    double t[4];
-                    pp_mul(Cs, Ps, t);
+                if (i != k) {  // T = W_ik P_k: warp w computes tiles (rg, 2 ch), (rg, 2 ch + 1)
+                    double t[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
-                    for (int m = 0; m < 4; ++m) Ts[r][c0 + 8 * m] = t[m];
+                    for (int kk = 0; kk < PPB / 4; ++kk) {
+                        const double av = Cs[row][4 * kk + lc];
+#pragma unroll
+                        for (int f = 0; f < 2; ++f) dmma_8x8x4(t[f][0], t[f][1], av, Ps[4 * kk + lc][(2 * ch + f) * 8 + lr]);
+                    }
+#pragma unroll
+                    for (int f = 0; f < 2; ++f) {
+                        Ts[row][(2 * ch + f) * 8 + 2 * lc] = t[f][0];
+                        Ts[row][(2 * ch + f) * 8 + 2 * lc + 1] = t[f][1];
+                    }
                     __syncthreads();
                 }
                 const PPTile& Lf = (i == k) ? Ps : Ts;
-                double acc[4][4];
+                double af[PPB / 4];
 #pragma unroll
-                for (int a2 = 0; a2 < 4; ++a2)
+                for (int kk = 0; kk < PPB / 4; ++kk) af[kk] = Lf[row][4 * kk + lc];
+                double acc[8][2];
 #pragma unroll
-                    for (int m = 0; m < 4; ++m) acc[a2][m] = 0.0;
-#pragma unroll 4
-                for (int t = 0; t < PPB; ++t) {
-                    double xl[4], yl[4];
+                for (int cg = 0; cg < 8; ++cg) acc[cg][0] = acc[cg][1] = 0.0;
 #pragma unroll
-                    for (int a2 = 0; a2 < 4; ++a2) xl[a2] = Lf[4 * wy + a2][t];
+                for (int kk = 0; kk < PPB / 4; ++kk) {
+                    const double* wrow = Ws + (4 * kk + lc) * PWS + ch * 64 + lr;
 #pragma unroll
-                    for (int m = 0; m < 4; ++m) yl[m] = Ws[t * PPW + wx + 32 * m];
-#pragma unroll
-                    for (int a2 = 0; a2 < 4; ++a2)
-#pragma unroll
-                        for (int m = 0; m < 4; ++m) acc[a2][m] = fma(xl[a2], yl[m], acc[a2][m]);
+                    for (int cg = 0; cg < 8; ++cg) dmma_8x8x4(acc[cg][0], acc[cg][1], af[kk], wrow[cg * 8]);
                 }
+                double* orow = dst + (size_t)(i * PPB + row) * ld;
 #pragma unroll
-                for (int a2 = 0; a2 < 4; ++a2) {
-                    const int row = 4 * wy + a2;
-                    double* orow = dst + (size_t)(i * PPB + row) * ld;
+                for (int cg = 0; cg < 8; ++cg) {
 #pragma unroll
-                    for (int m = 0; m < 4; ++m) {
-                        const int col = col0 + wx + 32 * m;
+                    for (int e = 0; e < 2; ++e) {
+                        const int col = col0 + ch * 64 + cg * 8 + lc * 2 + e;
                         if (col >= np) continue;
                         const int jb = col / PPB, cl = col % PPB;
                         double o;
                         if (jb == k) o = (i == k) ? Ps[row][cl] : -Ts[row][cl];
-                        else if (i == k) o = acc[a2][m];
+                        else if (i == k) o = acc[cg][e];
                         else if (i == k + 1 && jb == k + 1) continue;  // the lookahead's block
-                        else o = gsrc[a2][m] - acc[a2][m];
+                        else o = (e ? gsrc[cg].y : gsrc[cg].x) - acc[cg][e];
                         orow[col] = o;
                     }
                 }
@@ -909,8 +964,10 @@ void gj_pp_run(Ctx& c, double* W0, double* W1, int nb, int ld, int n) {
     }
     const int cap = per_sm * c.num_sms;
     if (cap < 2) throw CudaError("dense_inverse: ping-pong Gauss-Jordan does not fit");
-    const int nch = cdiv(ld, PPW), cpb = PPW / PPB;  // work item: one block row x 128 columns
-    const int blocks = std::min(nb * nch, cap - 1) + 1;
+    const int nch = cdiv(ld, PPW), cpb = PPW / PPB;  // work item: one block row x PPW columns
+    // one worker per item, plus one spare: the worker that shares the lookahead
+    // CTA's SM sits out (k_gj_pp), so nb * nch workers stay active
+    const int blocks = std::min(nb * nch + 1, cap - 1) + 1;
     static const bool trace = [] {
         const char* e = std::getenv("MPM2P_GJ_TRACE");
         return e && e[0] == '1';
@@ -920,7 +977,9 @@ void gj_pp_run(Ctx& c, double* W0, double* W1, int nb, int ld, int n) {
         tr.alloc((size_t)nb * 8);
         tr.zero(c.st);
     }
-    PPArgs pa{W0, W1, W1 + (size_t)ld * ld, ld, nb, nch, cpb, c.gj_piv.p + n, trace ? tr.p : nullptr};
+    c.gj_aux.alloc(2);
+    CK(cudaMemsetAsync(c.gj_aux.p, 0xFF, 2 * sizeof(int), c.st));  // aux[1] = -1: no idle worker yet
+    PPArgs pa{W0, W1, W1 + (size_t)ld * ld, ld, nb, nch, cpb, c.gj_piv.p + n, c.gj_aux.p, trace ? tr.p : nullptr};
     void* args[] = {&pa};
     {
         PROF(c, "k_gj_pp");

@@ -712,13 +712,27 @@ __global__ void k_ds_prep(Layout L, const double* __restrict__ kappa, const doub
                           const double* __restrict__ skel, const double* __restrict__ corr,
                           const double* __restrict__ RU, const double* __restrict__ delta, int grounded,
                           double* __restrict__ BD, double* __restrict__ BW, double* __restrict__ BS,
-                          double* __restrict__ Xd, double* __restrict__ EU, Scalars* sc) {
+                          double* __restrict__ Xd, double* __restrict__ EU, Scalars* sc, int mode = 0) {
+    // mode 0: operator and rhs; 1: operator only (split downscale, side
+    // stream); 2: rhs only (the operator was factored on the side stream)
     pdl_begin();
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= L.cells()) return;
     const int i = c % L.nx, j = c / L.nx;
     const int s = (j / L.sny) * L.nsx + i / L.snx;
     const int ii = i % L.snx, jj = j % L.sny, r = jj * L.snx + ii;
+    if (mode == 1) {
+        double diag = 0.0;
+        if (ii > 0) diag += T[L.vface(i, j)];
+        if (ii < L.snx - 1) diag += T[L.vface(i + 1, j)];
+        if (jj > 0) diag += T[L.hface(i, j)];
+        if (jj < L.sny - 1) diag += T[L.hface(i, j + 1)];
+        const size_t o = (size_t)s * L.ncs + r;
+        BD[o] = r == 0 ? 1.0 : diag;
+        BW[o] = (ii > 0 && r != 1) ? T[L.vface(i, j)] : 0.0;
+        BS[o] = (jj > 0 && r != L.snx) ? T[L.hface(i, j)] : 0.0;
+        return;
+    }
     const double kc = kappa[c];
     if (!(kc > 0.0) || !isfinite(kc)) atomicOr(&sc->err, ERR_KAPPA);
     double diag = 0.0;
@@ -750,9 +764,11 @@ __global__ void k_ds_prep(Layout L, const double* __restrict__ kappa, const doub
     if (r == 1) ow = 0.0;
     if (r == L.snx) os = 0.0;
     const size_t o = (size_t)s * L.ncs + r;
-    BD[o] = diag;
-    BW[o] = ow;
-    BS[o] = os;
+    if (mode == 0) {
+        BD[o] = diag;
+        BW[o] = ow;
+        BS[o] = os;
+    }
     Xd[o] = b;
 }
 
@@ -975,6 +991,63 @@ __global__ void __launch_bounds__(twist_threads<B>()) k_ds_solve_t(Layout L, con
 }
 #define MPM2P_TWIST_WIDTHS(X) X(4) X(8) X(10) X(12) X(16) X(20) X(24) X(32)
 
+// Split downscale, critical-path half: the two sweeps with the kappa_n factor
+// stored by k_factor1_t on the side stream, then k_ds_solve_t's mean shift
+// (mrcm.cpp:414-424) and scatter.
+template <int B>
+__global__ void __launch_bounds__(twist_threads<B>()) k_ds_sweep_t(Layout L, const double* __restrict__ D,
+                                                                   const double* __restrict__ Lc,
+                                                                   const double* __restrict__ Lr,
+                                                                   const double* __restrict__ MidB,
+                                                                   const double* __restrict__ Sinv, double* Xd,
+                                                                   const double* __restrict__ RS, double* p) {
+    pdl_begin();
+    double* tsm;
+    if constexpr (twist_warps<B>()) {
+        extern __shared__ __align__(16) double tsm_dyn[];
+        tsm = tsm_dyn;
+    } else {
+        __shared__ __align__(16) double tsm_st[twist_smem_doubles<B>()];
+        tsm = tsm_st;
+    }
+    const int lane = threadIdx.x & 31;
+    const int s = blockIdx.x;
+    if (s >= L.n_sub) return;
+    const int n = L.ncs;
+    const size_t so = (size_t)s * n;
+    double* x = Xd + so;
+    twisted_sweep<B>(n, D + so, Lc + so * B, Lr + so * B, MidB + (size_t)s * B * B, Sinv + (size_t)s * B * B, x, tsm);
+    if (threadIdx.x >= 32) return;
+    constexpr int PER = 8;
+    double v = 0.0;
+    const double rs = RS[s];
+    for (int r0 = 0; r0 < n; r0 += 32 * PER) {
+        double xv[PER];
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int r = r0 + lane + 32 * q;
+            xv[q] = r < n ? __ldcg(x + r) : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < PER; ++q) v += xv[q];
+    }
+    v = warp_sum(v);
+    const double shift = (rs - __shfl_sync(0xffffffffu, v, 0)) / n;
+    for (int r0 = 0; r0 < n; r0 += 32 * PER) {
+        double xv[PER];
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int r = r0 + lane + 32 * q;
+            xv[q] = r < n ? __ldcg(x + r) : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int r = r0 + lane + 32 * q;
+            if (r < n) p[L.gcell_of(s, r)] = xv[q] + shift;
+        }
+    }
+}
+
 // Rebuild with the two-sided scheme: the factor (twisted layout + the middle
 // block's S^-1 and bottom multipliers) and the particular solve...
 template <int B>
@@ -1077,6 +1150,7 @@ void twist_configure() {
     CK(cudaFuncSetAttribute(k_factor1_t<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     CK(cudaFuncSetAttribute(k_hom_solve_t<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     CK(cudaFuncSetAttribute(k_part_solve_t<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    CK(cudaFuncSetAttribute(k_ds_sweep_t<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     done = true;
 }
 
@@ -1451,6 +1525,48 @@ void launch_setup_static(Ctx& c) {
 
 namespace {
 
+// Split downscale, side-stream half: the downscale operator depends only on
+// T = transmissibility(kappa_n) (pure Neumann, all-Flux, anchor 0;
+// mrcm.cpp:391-411), so it is assembled and factored (two-sided layout) on
+// st2 as soon as T is formed, concurrently with the particular solve,
+// interface solve and recombination on the main stream. downscale() joins
+// before its sweeps. Works both captured into a graph (fork/join edges) and
+// eagerly.
+void ds_factor_fork(Ctx& c) {
+    if (!c.ds_split || c.ds_pending) return;
+    const Layout& L = c.L;
+    CK(cudaEventRecord(c.ev_fork, c.st));
+    CK(cudaStreamWaitEvent(c.st2, c.ev_fork, 0));
+    const cudaStream_t main_st = c.st;
+    c.st = c.st2;
+    {
+        PROF(c, "k_ds_band");
+        launch_k(c, k_ds_prep, grid_for(L.cells()), TPB, 0, L, nullptr, c.T, nullptr, nullptr, nullptr, nullptr,
+                 nullptr, nullptr, 0, c.BDd, c.BWd, c.BSd, nullptr, nullptr, c.sc.p, 1);
+        CK_LAUNCH();
+    }
+    {
+        PROF(c, "k_ds_factor");
+        switch (L.snx) {
+#define X(BW_)                                                                                                  \
+    case BW_:                                                                                                   \
+        twist_configure<BW_>();                                                                                 \
+        launch_k(c, k_factor1_t<BW_>, L.n_sub, twist_threads<BW_>(), twist_smem_bytes<BW_>(), L, 1, c.BDd, c.BWd, \
+                 c.BSd, c.Dd, c.Lcd, c.Lrd, c.ds_midb, c.ds_sinv, c.ds_yscr, c.sc);                             \
+        break;
+            MPM2P_TWIST_WIDTHS(X)
+#undef X
+            default:
+                c.st = main_st;
+                throw ConfigError("split downscale: unsupported subdomain width");
+        }
+        CK_LAUNCH();
+    }
+    CK(cudaEventRecord(c.ev_join, c.st2));
+    c.st = main_st;
+    c.ds_pending = true;
+}
+
 // Downscale shared by the rebuild and the MPM step (mrcm.cpp:306-439); needs
 // c.T = transmissibility(kappa), RU/RS = recon traces and pressure sums.
 void downscale(Ctx& c, const double* kappa) {
@@ -1472,16 +1588,37 @@ void downscale(Ctx& c, const double* kappa) {
             L, 0, c.grounded ? 1 : 0, c.delta, c.ground, c.corr, c.sc, c.red, c.red_count);
         CK_LAUNCH();
     }
+    const bool split = c.ds_split;
+    if (split) ds_factor_fork(c);  // no-op when the caller already forked it
     {
         PROF(c, "k_ds_prep");
         launch_k(c, k_ds_prep, grid_for(L.cells()), TPB, 0, L, kappa, c.T, c.q, c.bc_kind, c.skel, c.corr, c.RU, c.delta,
-                                                         c.grounded ? 1 : 0, c.BDd, c.BWd, c.BSd, c.Xd, c.GZ, c.sc);
+                                                         c.grounded ? 1 : 0, c.BDd, c.BWd, c.BSd, c.Xd, c.GZ, c.sc,
+                                                         split ? 2 : 0);
         CK_LAUNCH();
     }
     const size_t sm1 = (size_t)WPB * band_smem_doubles(L.snx, 1) * sizeof(double);
     const bool twist = c.twist_ok;
     bool done = false;
-    if (twist) {
+    if (split) {
+        CK(cudaStreamWaitEvent(c.st, c.ev_join, 0));
+        c.ds_pending = false;
+        PROF(c, "k_ds_sweep");
+        switch (L.snx) {
+#define X(BW_)                                                                                                  \
+    case BW_:                                                                                                   \
+        launch_k(c, k_ds_sweep_t<BW_>, L.n_sub, twist_threads<BW_>(), twist_smem_bytes<BW_>(), L, c.Dd, c.Lcd,  \
+                 c.Lrd, c.ds_midb, c.ds_sinv, c.Xd, c.RS, c.p);                                                 \
+        done = true;                                                                                            \
+        break;
+            MPM2P_TWIST_WIDTHS(X)
+#undef X
+            default:
+                break;
+        }
+        if (done) CK_LAUNCH();
+    }
+    if (!done && twist) {
         PROF(c, "k_ds_solve");
         switch (L.snx) {
 #define X(BW_)                                                                                                  \
@@ -1563,6 +1700,7 @@ void launch_rebuild(Ctx& c, const double* kappa, bool compute_beta) {  // comput
     const Layout& L = c.L;
     if (compute_beta) launch_beta(c, kappa);
     launch_trans(c, kappa);
+    ds_factor_fork(c);  // downscale operator of kappa, concurrent with the basis rebuild
     {
         PROF(c, "k_band_entries");
         launch_k(c, k_band_entries, grid_for(L.cells()), TPB, 0, L, kappa, c.T, 0, c.anchor_m ? 1 : 0, c.beta_m, c.beta_p,
@@ -1702,6 +1840,7 @@ void launch_mpm(Ctx& c, const double* kn) {  // mpm_pressure_update (mpm.cpp:31-
     const Layout& L = c.L;
     if (!c.has_basis) throw ConfigError("mpm_pressure_update: no basis set (rebuild first)");
     launch_trans(c, kn);
+    ds_factor_fork(c);  // downscale operator of kappa_n, concurrent with the particular / interface chain
     {
         PROF(c, "k_mpm_rhs");
         launch_k(c, k_mpm_rhs, grid_for(L.cells()), TPB, 0, L, c.max_rhs, c.anchor_m ? 1 : 0, kn, c.kappa_m, c.T, c.q,

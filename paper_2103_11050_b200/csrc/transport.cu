@@ -255,25 +255,27 @@ __global__ void k_upwind(Layout L, const double* __restrict__ s, double* __restr
     const int i = c % L.nx, j = c / L.nx;
     const double fin = frac_flow(inflow, M, nullptr);
     long long* cnt = &sc->clamp;
-    // vertical faces: owner counts clamps (face i is owned by cell i, face nx by cell nx-1)
-    auto vflux = [&](int fi, bool own) {
-        const double un = u[L.vface(fi, j)];
+    // every operand loaded up front, unconditionally (one memory round trip;
+    // the upwind choice below only selects among registers)
+    const double uW = u[L.vface(i, j)], uE = u[L.vface(i + 1, j)];
+    const double uS = u[L.hface(i, j)], uN = u[L.hface(i, j + 1)];
+    const double sC = s[c];
+    const double sW = i > 0 ? s[c - 1] : 0.0, sE = i + 1 < L.nx ? s[c + 1] : 0.0;
+    const double sS = j > 0 ? s[c - L.nx] : 0.0, sN = j + 1 < L.ny ? s[c + L.nx] : 0.0;
+    // face water flux from the upwind side; vertical faces: owner counts clamps
+    // (face i is owned by cell i, face nx by cell nx-1)
+    auto flux = [&](double un, bool lo_bnd, double s_lo, bool hi_bnd, double s_hi, bool own, double area) {
         double fs;
-        if (un >= 0.0) fs = (fi == 0) ? fin : frac_flow(s[L.cell(fi - 1, j)], M, own ? cnt : nullptr);
-        else fs = (fi == L.nx) ? fin : frac_flow(s[L.cell(fi, j)], M, own ? cnt : nullptr);
-        return fs * un * L.hy;
+        if (un >= 0.0) fs = lo_bnd ? fin : frac_flow(s_lo, M, own ? cnt : nullptr);
+        else fs = hi_bnd ? fin : frac_flow(s_hi, M, own ? cnt : nullptr);
+        return fs * un * area;
     };
-    auto hflux = [&](int fj, bool own) {
-        const double un = u[L.hface(i, fj)];
-        double fs;
-        if (un >= 0.0) fs = (fj == 0) ? fin : frac_flow(s[L.cell(i, fj - 1)], M, own ? cnt : nullptr);
-        else fs = (fj == L.ny) ? fin : frac_flow(s[L.cell(i, fj)], M, own ? cnt : nullptr);
-        return fs * un * L.hx;
-    };
-    const double wE = vflux(i + 1, i + 1 == L.nx), wW = vflux(i, true);
-    const double wN = hflux(j + 1, j + 1 == L.ny), wS = hflux(j, true);
+    const double wE = flux(uE, false, sC, i + 1 == L.nx, sE, i + 1 == L.nx, L.hy);
+    const double wW = flux(uW, i == 0, sW, false, sC, true, L.hy);
+    const double wN = flux(uN, false, sC, j + 1 == L.ny, sN, j + 1 == L.ny, L.hx);
+    const double wS = flux(uS, j == 0, sS, false, sC, true, L.hx);
     const double net = wE - wW + wN - wS;
-    const double sn = s[c] - dt / L.vol() * net;
+    const double sn = sC - dt / L.vol() * net;
     if (sn < -1e-12 || sn > 1.0 + 1e-12) atomicOr(&sc->err, ERR_CFL);
     s_out[c] = sn < 0.0 ? 0.0 : (sn > 1.0 ? 1.0 : sn);
 }
