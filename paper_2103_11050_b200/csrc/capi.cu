@@ -265,6 +265,8 @@ void create_ctx(mpm2p_ctx* ctx, const mpm2p_problem* P) {
     if (const char* e = std::getenv("MPM2P_NO_TWIST")) c.no_twist = e[0] == '1';
     if (const char* e = std::getenv("MPM2P_PDL")) c.pdl = e[0] == '1';
     if (const char* e = std::getenv("MPM2P_BT_PDL")) c.bt_pdl = e[0] != '0';
+    if (const char* e = std::getenv("MPM2P_GRAPH_TIMING")) c.graph_timing = e[0] == '1';
+    if (const char* e = std::getenv("MPM2P_UPWIND_TILE")) c.upwind_tiled = e[0] != '0';
     if (const char* e = std::getenv("MPM2P_REFINE")) {  // 1: always refine, 0: never (experiments)
         c.force_refine = e[0] == '1';
         c.never_refine = e[0] == '0';
@@ -725,7 +727,13 @@ bool run_step(mpm2p_ctx* ctx, mpm2p_step_record* out) {
             c.c_iface = before[4];
             c.launch_count = launches_before;
         }
+        if (c.graph_timing) {  // device time of the replay alone (timer slots 14 / 15)
+            for (int t = 14; t < 16; ++t)
+                if (!c.timers[t]) CK(cudaEventCreate(&c.timers[t]));
+            CK(cudaEventRecord(c.timers[14], c.st));
+        }
         CK(cudaGraphLaunch(g, c.st));
+        if (c.graph_timing) CK(cudaEventRecord(c.timers[15], c.st));
         c.c_hom += delta[0];
         c.c_part += delta[1];
         c.c_down += delta[2];

@@ -124,6 +124,7 @@ struct Ctx {
     // side stream (st2) while the particular / interface / recon chain runs;
     // only the two sweeps stay on the critical path
     bool ds_split = false;
+    bool upwind_tiled = true;  // k_upwind_tile (MPM2P_UPWIND_TILE=0: one thread per cell, k_upwind)
     bool ds_pending = false;  // a forked factor awaits its join (ev_join)
     cudaStream_t st2 = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -198,6 +199,7 @@ struct Ctx {
     std::vector<double> prof_ms;
     std::vector<long long> prof_count;
     cudaEvent_t timers[16] = {};
+    bool graph_timing = false;  // MPM2P_GRAPH_TIMING=1: timers 14 / 15 bracket each step's graph replay
     DevBuf<unsigned char> flush_buf;
 
     cudaEvent_t take_event() {

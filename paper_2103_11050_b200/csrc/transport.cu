@@ -280,6 +280,92 @@ __global__ void k_upwind(Layout L, const double* __restrict__ s, double* __restr
     s_out[c] = sn < 0.0 ? 0.0 : (sn > 1.0 ? 1.0 : sn);
 }
 
+// Tiled upwind_step: a CTA owns a 32 x 8 tile of cells. Every cell's
+// fractional flow f(s) is evaluated ONCE into shared memory (tile + one-cell
+// halo: 340 evaluations for 256 cells, against 4 per cell when each cell
+// evaluates both sides of its faces); a face then only selects the upwind
+// cell's value. f is a pure function of s, so every face flux, and hence s,
+// is bit-identical to k_upwind. Clamp counting follows k_upwind: a face's
+// owner (west / south face of each cell, plus the east / north domain
+// boundary) counts an out-of-range upwind saturation.
+constexpr int UT_X = 32, UT_Y = 8;
+__global__ void __launch_bounds__(UT_X * UT_Y) k_upwind_tile(Layout L, const double* __restrict__ s,
+                                                             double* __restrict__ s_out, const double* __restrict__ u,
+                                                             Scalars* sc, double inflow, double M, int take_next = 0,
+                                                             int inj_cn = 0, int sub = 1) {
+    pdl_begin();
+    __shared__ double F[UT_Y + 2][UT_X + 2];
+    __shared__ unsigned char OOR[UT_Y + 2][UT_X + 2];
+    const int i0 = blockIdx.x * UT_X, j0 = blockIdx.y * UT_Y;
+    const int ti = threadIdx.x % UT_X, tj = threadIdx.x / UT_X;
+    const int i = i0 + ti, j = j0 + tj;
+    const double dt = take_next ? sc->dt_next : (sub > 1 ? sc->dt / sub : sc->dt);
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+        (void)frac_flow(inflow, M, &sc->clamp);  // f_in is evaluated once per call
+        if (take_next) {
+            sc->dt = dt;
+            sc->any_flow = sc->any_next;
+            const double rt = sc->inj_next;
+            sc->inj = rt;
+            const double pore = L.lx * L.ly;
+            for (int k = 0; k < inj_cn; ++k) sc->pvi += rt * dt / pore;
+        }
+    }
+    const bool in = i < L.nx && j < L.ny;
+    // the thread's own operands first (one round trip with the halo loads)
+    double uW = 0.0, uE = 0.0, uS = 0.0, uN = 0.0, sC = 0.0;
+    if (in) {
+        uW = u[L.vface(i, j)];
+        uE = u[L.vface(i + 1, j)];
+        uS = u[L.hface(i, j)];
+        uN = u[L.hface(i, j + 1)];
+        sC = s[L.cell(i, j)];
+    }
+    constexpr int HN = (UT_X + 2) * (UT_Y + 2);
+    for (int h = threadIdx.x; h < HN; h += UT_X * UT_Y) {
+        const int hx = h % (UT_X + 2), hy = h / (UT_X + 2);
+        const int gi = i0 + hx - 1, gj = j0 + hy - 1;
+        double f = 0.0;
+        unsigned char o = 0;
+        if (gi >= 0 && gi < L.nx && gj >= 0 && gj < L.ny) {
+            const double sv = s[L.cell(gi, gj)];
+            o = (sv < 0.0 || sv > 1.0) ? 1 : 0;
+            f = frac_flow(sv, M, nullptr);
+        }
+        F[hy][hx] = f;
+        OOR[hy][hx] = o;
+    }
+    __shared__ double cst[2];  // f(inflow) and dt / vol: evaluated once per CTA (same IEEE operations)
+    if (threadIdx.x == 0) {
+        cst[0] = frac_flow(inflow, M, nullptr);
+        cst[1] = dt / L.vol();
+    }
+    __syncthreads();
+    if (!in) return;
+    const double fin = cst[0];
+    const double fC = F[tj + 1][ti + 1];
+    const bool lastx = i + 1 == L.nx, lasty = j + 1 == L.ny;
+    // face fluxes with k_upwind's operations: (f * u) * area
+    const double fE = uE >= 0.0 ? fC : (lastx ? fin : F[tj + 1][ti + 2]);
+    const double fWv = uW >= 0.0 ? (i == 0 ? fin : F[tj + 1][ti]) : fC;
+    const double fN = uN >= 0.0 ? fC : (lasty ? fin : F[tj + 2][ti + 1]);
+    const double fSv = uS >= 0.0 ? (j == 0 ? fin : F[tj][ti + 1]) : fC;
+    const double wE = fE * uE * L.hy, wW = fWv * uW * L.hy;
+    const double wN = fN * uN * L.hx, wS = fSv * uS * L.hx;
+    {  // clamp counts of the owned faces' evaluations
+        int cnt = 0;
+        cnt += uW >= 0.0 ? (i > 0 && OOR[tj + 1][ti]) : OOR[tj + 1][ti + 1];
+        cnt += uS >= 0.0 ? (j > 0 && OOR[tj][ti + 1]) : OOR[tj + 1][ti + 1];
+        if (lastx && uE >= 0.0) cnt += OOR[tj + 1][ti + 1];
+        if (lasty && uN >= 0.0) cnt += OOR[tj + 1][ti + 1];
+        if (cnt) atomicAdd((unsigned long long*)&sc->clamp, (unsigned long long)cnt);
+    }
+    const double net = wE - wW + wN - wS;
+    const double sn = sC - cst[1] * net;
+    if (sn < -1e-12 || sn > 1.0 + 1e-12) atomicOr(&sc->err, ERR_CFL);
+    s_out[L.cell(i, j)] = sn < 0.0 ? 0.0 : (sn > 1.0 ? 1.0 : sn);
+}
+
 // conductivity (transport.cpp:122-126) + the drift partial sums
 // (mpm.cpp:14-20 / simulation.cpp:169-172) in double-double.
 // eps_mode: -1 none, 0 relative, 1 absolute, 2 mobility (vs lam_reb)
@@ -554,8 +640,12 @@ void launch_upwind(Ctx& c, const double* s_in, double* s_out, const double* u, d
                    int inj_cn, int sub) {
     {
         PROF(c, "k_upwind");
-        launch_k(c, k_upwind, cdiv(c.L.cells(), TPB), TPB, 0, c.L, s_in, s_out, u, c.sc, inflow, c.M, take_next ? 1 : 0,
-                 inj_cn, sub);
+        if (c.upwind_tiled)
+            launch_k(c, k_upwind_tile, dim3(cdiv(c.L.nx, UT_X), cdiv(c.L.ny, UT_Y)), UT_X * UT_Y, 0, c.L, s_in, s_out, u,
+                     c.sc, inflow, c.M, take_next ? 1 : 0, inj_cn, sub);
+        else
+            launch_k(c, k_upwind, cdiv(c.L.cells(), TPB), TPB, 0, c.L, s_in, s_out, u, c.sc, inflow, c.M,
+                     take_next ? 1 : 0, inj_cn, sub);
         CK_LAUNCH();
     }
 }

@@ -34,3 +34,21 @@ for flush in (1, 0):
                   f"mean {statistics.mean(v):8.1f} us min {min(v):8.1f} us")
 sim.run_end()
 sim.close()
+if os.environ.get("MPM2P_GRAPH_TIMING") == "1":  # replay-only device time (timers 14/15 inside run_step)
+    sim = api.Simulator(cfg.problem, lib)
+    sim.run_begin(split, cfg.s0(), cfg.inflow_sat)
+    t = {0: [], 1: []}
+    for _ in range(nsteps):
+        lib.flush_l2(sim.h)
+        r = sim.run_step()
+        if r is None:
+            break
+        ms = ctypes.c_double()
+        lib.timer_elapsed(sim.h, 14, 15, ctypes.byref(ms))
+        t[r["rebuilt"]].append(ms.value * 1e3)
+    for b, nm in ((0, "mpm"), (1, "rebuild")):
+        v = t[b][2:] if b == 0 else t[b]
+        if v:
+            print(f"{name} replay-only {nm:8s} n={len(v):4d} median {statistics.median(v):8.1f} us")
+    sim.run_end()
+    sim.close()
