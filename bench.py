@@ -392,7 +392,8 @@ def main():
                 tr = {k.split("::")[-1]: v for k, v in json.load(f).items()}
             # keys carry template arguments (k_ds_solve_r<16>): match the launcher name as a prefix
             hit = [v for k, v in tr.items() if k == roof["kernel"] or k.startswith(roof["kernel"] + "_r<")
-                   or k.startswith(roof["kernel"] + "<")]
+                   or k.startswith(roof["kernel"] + "_t<") or k.startswith(roof["kernel"] + "<")
+                   or k.startswith(roof["kernel"] + "_tile")]
             roof["traffic"] = hit[0] if hit else None
             roof["traffic_source"] = f"profiles/ncu_traffic_r01_{cfg.name}.json (dram__bytes_read+write per launch)"
         except (OSError, ValueError):
