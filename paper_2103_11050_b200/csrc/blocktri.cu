@@ -134,72 +134,85 @@ __global__ void k_bt_unpermute(const double* __restrict__ xb, int n, const int* 
 // registers BEFORE griddepcontrol.wait and triggers its dependents at entry:
 // launched with programmatic dependent launch (bt_solve), step j+1's block
 // streams in while step j finishes, and only the vector part is serialised.
-constexpr int BT_NPL = 24;  // prefetched doubles per lane: rows of up to 768 columns
+constexpr int BT_Q = 4;     // warps per row: a row's columns are split in BT_Q quarters
+constexpr int BT_NPL = 6;   // prefetched doubles per lane: quarters of up to 32 * 6 columns
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
-template <int NPL>
-__device__ __forceinline__ void bt_row_prefetch(double (&v)[NPL], const double* row, int cols, bool on, int lane) {
+// Lane's share of a row quarter [c0, c1): columns c0 + lane + 32 q.
+__device__ __forceinline__ void bt_prefetch(double (&v)[BT_NPL], const double* row, int c0, int c1, bool on, int lane) {
 #pragma unroll
-    for (int q = 0; q < NPL; ++q) {
-        const int c = lane + 32 * q;
-        v[q] = (on && c < cols) ? __ldg(row + c) : 0.0;
+    for (int q = 0; q < BT_NPL; ++q) {
+        const int c = c0 + lane + 32 * q;
+        v[q] = (on && c < c1) ? __ldg(row + c) : 0.0;
     }
 }
-template <int NPL>
-__device__ __forceinline__ double bt_row_dot(const double (&v)[NPL], const double* row, int cols, const double* x,
-                                             double acc, int lane) {
+__device__ __forceinline__ double bt_dot(const double (&v)[BT_NPL], const double* row, int c0, int c1,
+                                         const double* x, double acc, int lane) {
 #pragma unroll
-    for (int q = 0; q < NPL; ++q) {
-        const int c = lane + 32 * q;
-        if (c < cols) acc = fma(v[q], __ldcg(x + c), acc);
+    for (int q = 0; q < BT_NPL; ++q) {
+        const int c = c0 + lane + 32 * q;
+        if (c < c1) acc = fma(v[q], __ldcg(x + c), acc);
     }
-    for (int c = lane + 32 * NPL; c < cols; c += 32) acc = fma(row[c], __ldcg(x + c), acc);  // wider blocks
+    for (int c = c0 + lane + 32 * BT_NPL; c < c1; c += 32) acc = fma(row[c], __ldcg(x + c), acc);  // wider blocks
     return acc;
 }
-
-// y_j -= G y_{j-1} (G = T_{j-1}^T, rows x cols), one warp per row
-__global__ void k_bt_fwd(const double* __restrict__ G, int rows, int cols, const double* yprev,
-                         double* y) {
-    pdl_trigger();
-    const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-    const bool on = row < rows;
-    const double* g = G + (size_t)(on ? row : 0) * cols;
-    double gv[BT_NPL];
-    bt_row_prefetch(gv, g, cols, on, lane);
-    pdl_begin();  // y_{j-1} is complete and visible
-    if (!on) return;
-    double acc = bt_row_dot(gv, g, cols, yprev, 0.0, lane);
+// Quarter partials of the block's rows, combined in quarter order (deterministic).
+__device__ __forceinline__ bool bt_combine(double& acc, int lane) {
+    __shared__ double part[256 / 32];
+    const int w = threadIdx.x >> 5;
     acc = warp_sum(acc);
-    if (lane == 0) y[row] -= acc;
+    if (lane == 0) part[w] = acc;
+    __syncthreads();
+    if ((w % BT_Q) != 0 || lane != 0) return false;
+    acc = part[w];
+#pragma unroll
+    for (int q = 1; q < BT_Q; ++q) acc += part[w + q];
+    return true;
 }
 
-// x_j = Sinv_j y_j - T_j x_{j+1} (T_j: rows x cols_next), one warp per row
-__global__ void k_bt_bwd(const double* __restrict__ Sinv, const double* __restrict__ T, int rows, int cols_next,
-                         const double* y, const double* xnext, double* x) {
+// y_j -= G y_{j-1} (G = T_{j-1}^T, rows x cols): BT_Q warps per row (two rows
+// per 256-thread block, so a step spreads over ~4x more SMs than one warp per
+// row would), the row's quarter loaded before griddepcontrol.wait.
+__global__ void __launch_bounds__(256) k_bt_fwd(const double* __restrict__ G, int rows, int cols,
+                                                const double* yprev, double* y) {
     pdl_trigger();
-    const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int row = blockIdx.x * (256 / 32 / BT_Q) + w / BT_Q, qw = w % BT_Q;
     const bool on = row < rows;
-    const double* s = Sinv + (size_t)(on ? row : 0) * rows;
-    const double* t = T ? T + (size_t)(on ? row : 0) * cols_next : nullptr;
+    const int qlen = (cols + BT_Q - 1) / BT_Q, c0 = qw * qlen, c1 = min(cols, c0 + qlen);
+    const double* g = G + (size_t)(on ? row : 0) * cols;
+    double gv[BT_NPL];
+    bt_prefetch(gv, g, c0, c1, on, lane);
+    pdl_begin();  // y_{j-1} is complete and visible
+    double acc = on ? bt_dot(gv, g, c0, c1, yprev, 0.0, lane) : 0.0;
+    if (bt_combine(acc, lane) && on) y[row] -= acc;
+}
+
+// x_j = Sinv_j y_j - T_j x_{j+1} (T_j: rows x cols_next), BT_Q warps per row
+__global__ void __launch_bounds__(256) k_bt_bwd(const double* __restrict__ Sinv, const double* __restrict__ T,
+                                                int rows, int cols_next, const double* y, const double* xnext,
+                                                double* x) {
+    pdl_trigger();
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int row = blockIdx.x * (256 / 32 / BT_Q) + w / BT_Q, qw = w % BT_Q;
+    const bool on = row < rows;
+    const int qs = (rows + BT_Q - 1) / BT_Q, s0 = qw * qs, s1 = min(rows, s0 + qs);
+    const int qt = (cols_next + BT_Q - 1) / BT_Q, t0 = qw * qt, t1 = min(cols_next, t0 + qt);
+    const double* sr = Sinv + (size_t)(on ? row : 0) * rows;
+    const double* tr = T ? T + (size_t)(on ? row : 0) * cols_next : nullptr;
     double sv[BT_NPL], tv[BT_NPL];
-    bt_row_prefetch(sv, s, rows, on, lane);
-    bt_row_prefetch(tv, t, T ? cols_next : 0, on && T, lane);
+    bt_prefetch(sv, sr, s0, s1, on, lane);
+    bt_prefetch(tv, tr, t0, T ? t1 : t0, on && T, lane);
     pdl_begin();  // x_{j+1} is complete and visible (y_j was finished by the forward sweep)
-    if (!on) return;
-    double acc = bt_row_dot(sv, s, rows, y, 0.0, lane);
-    if (T) {
-#pragma unroll
-        for (int q = 0; q < BT_NPL; ++q) tv[q] = -tv[q];
-        // same operation order as acc = fma(-t[c], xnext[c], acc) over c
-#pragma unroll
-        for (int q = 0; q < BT_NPL; ++q) {
-            const int c = lane + 32 * q;
-            if (c < cols_next) acc = fma(tv[q], __ldcg(xnext + c), acc);
+    double acc = 0.0;
+    if (on) {
+        acc = bt_dot(sv, sr, s0, s1, y, 0.0, lane);
+        if (T) {
+            double a2 = bt_dot(tv, tr, t0, t1, xnext, 0.0, lane);
+            acc -= a2;
         }
-        for (int c = lane + 32 * BT_NPL; c < cols_next; c += 32) acc = fma(-t[c], __ldcg(xnext + c), acc);
     }
-    acc = warp_sum(acc);
-    if (lane == 0) x[row] = acc;
+    if (bt_combine(acc, lane) && on) x[row] = acc;
 }
 
 }  // namespace
@@ -329,7 +342,7 @@ void bt_solve(Ctx& c, const double* rhs, double* x) {
     for (int j = 1; j < nb; ++j) {
         const int s = c.bt_sz[j], sp = c.bt_sz[j - 1];
         PROF(c, "k_bt_fwd");
-        launch_pdl(k_bt_fwd, cdiv((long long)s * 32, TPB), (const double*)(c.bt_G.p + c.bt_eoff[j - 1]), s, sp,
+        launch_pdl(k_bt_fwd, cdiv((long long)s * 32 * BT_Q, TPB), (const double*)(c.bt_G.p + c.bt_eoff[j - 1]), s, sp,
                    (const double*)(y + c.bt_voff[j - 1]), y + c.bt_voff[j]);
         CK_LAUNCH();
     }
@@ -338,7 +351,7 @@ void bt_solve(Ctx& c, const double* rhs, double* x) {
         const bool last = j == nb - 1;
         const int sn = last ? 0 : c.bt_sz[j + 1];
         PROF(c, "k_bt_bwd");
-        launch_pdl(k_bt_bwd, cdiv((long long)s * 32, TPB), (const double*)(c.bt_Sinv.p + c.bt_doff[j]),
+        launch_pdl(k_bt_bwd, cdiv((long long)s * 32 * BT_Q, TPB), (const double*)(c.bt_Sinv.p + c.bt_doff[j]),
                    (const double*)(last ? nullptr : c.bt_T.p + c.bt_eoff[j]), s, sn, (const double*)(y + c.bt_voff[j]),
                    (const double*)(last ? nullptr : xb + c.bt_voff[j + 1]), xb + c.bt_voff[j]);
         CK_LAUNCH();
