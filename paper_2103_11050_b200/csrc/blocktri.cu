@@ -134,7 +134,7 @@ __global__ void k_bt_unpermute(const double* __restrict__ xb, int n, const int* 
 // registers BEFORE griddepcontrol.wait and triggers its dependents at entry:
 // launched with programmatic dependent launch (bt_solve), step j+1's block
 // streams in while step j finishes, and only the vector part is serialised.
-constexpr int BT_Q = 4;     // warps per row: a row's columns are split in BT_Q quarters
+constexpr int BT_Q = 8;     // warps per row: a row's columns are split in BT_Q quarters
 constexpr int BT_NPL = 6;   // prefetched doubles per lane: quarters of up to 32 * 6 columns
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
