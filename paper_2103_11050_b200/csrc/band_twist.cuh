@@ -269,16 +269,18 @@ __device__ bool twist_middle_gj(double (&srow)[B], double& sr, double* pr) {
 // ---- phase 3: back substitution, both halves outwards from the middle -------
 // midL(i, o): multiplier of this half's middle row i (its virtual order) at
 // Lrow position o; xm: the middle solution (natural order, shared memory).
+// dfirst: D of this lane's first back-substitution row when the caller
+// prefetched it (negative: load it here).
 template <int B, typename MidL>
 __device__ void twist_backward(const Twist<B>& T, const double* D, const double* Lrow, double* Y, const double* xm,
-                               double* ring, MidL midL) {
+                               double* ring, MidL midL, double dfirst = -1.0) {
     constexpr int RG = twist_ring<B>();
     const int h = T.h, ll = T.ll, llc = T.llc, nch = T.Cb;
     auto xmid = [&](int i) { return xm[h ? B - 1 - i : i]; };
     double z;
     {
         const int row = (T.Ch - 1) * B + llc;
-        z = Y[T.orig(row)] * (1.0 / D[T.obase + row]);
+        z = Y[T.orig(row)] * (1.0 / (dfirst > 0.0 ? dfirst : D[T.obase + row]));
         double corr = 0.0;
         for (int i = 0; i <= llc; ++i) corr = fma(midL(i, llc - i), xmid(i), corr);
         z -= corr;
@@ -465,8 +467,25 @@ __device__ void twisted_sweep(int n, const double* D, const double* Lcol, const 
                               const double* Sinv, double* Y, double* sm) {
     const Twist<B> T(n);
     const TwistSmem<B> S(T, sm);
+    // Static operands of the middle solve and of the back substitution's first
+    // step (this half's middle multipliers, S^-1, the middle rows' RHS, which
+    // the forward phase does not touch, and the first pivot) are fetched now,
+    // asynchronously, instead of on the chain after the forward phase.
+    double* mids_s = S.stage;           // B x B, this half (stage is idle in a sweep)
+    double* sinv_s = S.mid;             // B x B (leader half)
+    double* ymid_s = S.mid + B * B;     // B
+    {
+        const double* mids_g = T.h ? MidB : Lrow + (size_t)T.m * B;
+        for (int p = T.ll; p < B * B / 2; p += T.NL) cp_async16(mids_s + 2 * p, mids_g + 2 * p);
+        if (T.leader()) {
+            for (int p = T.ll; p < B * B / 2; p += T.NL) cp_async16(sinv_s + 2 * p, Sinv + 2 * p);
+            for (int p = T.ll; p < B / 2; p += T.NL) cp_async16(ymid_s + 2 * p, Y + T.m + 2 * p);
+        }
+        cp_async_commit();
+    }
+    const double dfirst = D[T.obase + (T.Ch - 1) * B + T.llc];
     double yv;
-    twist_forward<B>(T, Lcol, Y, S.ring, yv);
+    twist_forward<B>(T, Lcol, Y, S.ring, yv);  // drains every cp.async group (ours included)
     double* rhs = S.mid + 2 * B * B;  // [2][B]
     double* xm = rhs + 2 * B;
     if (T.act) rhs[T.h * B + T.ll] = yv;
@@ -475,13 +494,12 @@ __device__ void twisted_sweep(int n, const double* D, const double* Lcol, const 
     if (T.leader() && lane < B) {
         double x = 0.0;
 #pragma unroll
-        for (int jj = 0; jj < B; ++jj) x = fma(Sinv[lane * B + jj], rhs[jj] + rhs[B + B - 1 - jj] - Y[T.m + jj], x);
+        for (int jj = 0; jj < B; ++jj) x = fma(sinv_s[lane * B + jj], rhs[jj] + rhs[B + B - 1 - jj] - ymid_s[jj], x);
         xm[lane] = x;
     }
     T.team_sync();
     if (T.leader() && lane < B) Y[T.m + lane] = xm[lane];
-    const double* mids = T.h ? MidB : Lrow + (size_t)T.m * B;
-    twist_backward<B>(T, D, Lrow, Y, xm, S.ring, [&](int i, int o) { return mids[i * B + o]; });
+    twist_backward<B>(T, D, Lrow, Y, xm, S.ring, [&](int i, int o) { return mids_s[i * B + o]; }, dfirst);
     T.team_sync();
 }
 

@@ -265,6 +265,7 @@ void create_ctx(mpm2p_ctx* ctx, const mpm2p_problem* P) {
     if (const char* e = std::getenv("MPM2P_NO_TWIST")) c.no_twist = e[0] == '1';
     if (const char* e = std::getenv("MPM2P_PDL")) c.pdl = e[0] == '1';
     if (const char* e = std::getenv("MPM2P_BT_PDL")) c.bt_pdl = e[0] != '0';
+    if (const char* e = std::getenv("MPM2P_BT_PERSIST")) c.bt_persistent = e[0] == '1';
     if (const char* e = std::getenv("MPM2P_GRAPH_TIMING")) c.graph_timing = e[0] == '1';
     if (const char* e = std::getenv("MPM2P_UPWIND_TILE")) c.upwind_tiled = e[0] != '0';
     if (const char* e = std::getenv("MPM2P_REFINE")) {  // 1: always refine, 0: never (experiments)
