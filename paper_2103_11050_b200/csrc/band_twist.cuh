@@ -190,9 +190,26 @@ __device__ bool twist_eliminate(const Twist<B>& T, const BandRows A, double* D, 
 // ---- phase 2: the middle block ----------------------------------------------
 // Writes both windows and RHS to `mid`, assembles S in lanes 0..B-1 (row i of
 // S in srow) and the middle RHS r_i = y_top[i] + y_bot[B-1-i] - b[m+i].
+// The middle rows' operator entries and RHS (untouched by the elimination),
+// fetched by the leader lanes before it, so the assembly waits on no load.
+struct MidPre {
+    double d, wi, wi1, y;  // diag[m+i], offw[m+i], offw[m+i+1], Y[m+i] of leader lane i
+};
+template <int B>
+__device__ __forceinline__ MidPre mid_prefetch(const Twist<B>& T, const BandRows A, const double* Y) {
+    MidPre p{0.0, 0.0, 0.0, 0.0};
+    const int i = threadIdx.x & 31;
+    if (T.leader() && i < B) {
+        p.d = A.diag[T.m + i];
+        p.wi = A.offw[T.m + i];
+        p.wi1 = A.offw[T.m + (i + 1 < B ? i + 1 : i)];
+        p.y = Y[T.m + i];
+    }
+    return p;
+}
 template <int B>
 __device__ void twist_middle_assemble(const Twist<B>& T, const BandRows A, const double* Y, const double (&reg)[B],
-                                      double yv, double* mid, double (&srow)[B], double& sr) {
+                                      double yv, double* mid, double (&srow)[B], double& sr, const MidPre& pre) {
     const int lane = threadIdx.x & 31, m = T.m;
     double* W = mid + T.h * B * B;
     double* rhs = mid + 2 * B * B;  // [2][B]
@@ -208,12 +225,14 @@ __device__ void twist_middle_assemble(const Twist<B>& T, const BandRows A, const
 #pragma unroll
         for (int jj = 0; jj < B; ++jj) {
             const int lo = jj <= i ? i : jj, hi2 = jj <= i ? jj : i;  // (row lo, col hi2), hi2 <= lo
-            double a0 = 0.0;
-            if (lo == hi2) a0 = A.diag[m + lo];
-            else if (lo == hi2 + 1) a0 = -A.offw[m + lo];
+            double a0 = 0.0;  // A.diag[m + lo] on the diagonal, -A.offw[m + lo] one below
+            if (lo == hi2) a0 = pre.d;
+            else if (lo == hi2 + 1) a0 = -(lo == i ? pre.wi : pre.wi1);
             srow[jj] = mid[lo * B + hi2] + mid[B * B + (B - 1 - hi2) * B + (B - 1 - lo)] - a0;
         }
-        sr = rhs[i] + rhs[B + B - 1 - i] - Y[m + i];
+        sr = rhs[i] + rhs[B + B - 1 - i] - pre.y;
+        (void)Y;
+        (void)m;
     } else {
 #pragma unroll
         for (int jj = 0; jj < B; ++jj) srow[jj] = (jj == 0 ? 1.0 : 0.0);
@@ -408,10 +427,11 @@ __device__ bool twisted_solve(int n, const BandRows A, double* D, double* Lrow, 
     static_assert(B <= 32 && B % 2 == 0, "two halves of B lanes");
     const Twist<B> T(n);
     const TwistSmem<B> S(T, sm);
+    const MidPre pre = mid_prefetch<B>(T, A, Y);
     double reg[B], yv;
     bool ok = twist_eliminate<B, false>(T, A, D, nullptr, Lrow, Y, S.stage, S.xb, reg, yv);
     double srow[B], sr;
-    twist_middle_assemble<B>(T, A, Y, reg, yv, S.mid, srow, sr);
+    twist_middle_assemble<B>(T, A, Y, reg, yv, S.mid, srow, sr, pre);
     double* xm = S.mid + 2 * B * B + 2 * B;
     const int lane = threadIdx.x & 31;
     if (T.leader()) {
@@ -435,6 +455,7 @@ __device__ bool twisted_factor(int n, const BandRows A, double* D, double* Lcol,
     static_assert(B <= 32 && B % 2 == 0, "two halves of B lanes");
     const Twist<B> T(n);
     const TwistSmem<B> S(T, sm);
+    const MidPre pre = mid_prefetch<B>(T, A, Y);
     double reg[B], yv;
     bool ok = twist_eliminate<B, true>(T, A, D, Lcol, Lrow, Y, S.stage, S.xb, reg, yv);
     {  // middle multipliers of each side: top as Lrow rows [m, m+B), bottom in MidB
@@ -442,7 +463,7 @@ __device__ bool twisted_factor(int n, const BandRows A, double* D, double* Lcol,
         for (int x = T.ll; x < B * B; x += T.NL) dst[x] = S.stage[x];
     }
     double srow[B], sr;
-    twist_middle_assemble<B>(T, A, Y, reg, yv, S.mid, srow, sr);
+    twist_middle_assemble<B>(T, A, Y, reg, yv, S.mid, srow, sr, pre);
     double* xm = S.mid + 2 * B * B + 2 * B;
     const int lane = threadIdx.x & 31;
     if (T.leader()) {
