@@ -845,37 +845,6 @@ __device__ __forceinline__ double part_trace(const Layout& L, int s, int idx, do
     return GZ[x];
 }
 
-// part_trace split in two: the operands that do not depend on the solution
-// (loaded before the sweep, off the chain), then the same expressions of pc.
-struct TracePre {
-    double a, g, area;
-    int mode;  // 0 skeleton (Robin, rhs 0), 1 pressure face, 2 flux face
-};
-__device__ __forceinline__ TracePre part_trace_pre(const Layout& L, int s, int idx, const double* km,
-                                                   const int* bc_kind, const double* bm, const double* bp,
-                                                   const double* GZ) {
-    const EdgeInfo e = L.edge(s, idx);
-    const double th = half_trans(L, e.side, km[e.global_cell]);
-    const size_t x = (size_t)s * L.nbe + idx;
-    TracePre t;
-    t.area = e.area;
-    if (e.iface >= 0) {
-        t.mode = 0;
-        t.a = eff_robin(th, edge_beta(L, e, bm, bp), e.area);
-        t.g = 0.0;
-    } else {
-        t.mode = bc_kind[e.gbc] == BC_PRESSURE ? 1 : 2;
-        t.a = th;
-        t.g = GZ[x];
-    }
-    return t;
-}
-__device__ __forceinline__ double part_trace_apply(const TracePre& t, double pc) {
-    if (t.mode == 0) return t.a * (pc - 0.0) / t.area;
-    if (t.mode == 1) return t.a * (pc - t.g) / t.area;
-    return t.g;
-}
-
 // MPM-2P particular solve with the cached factor, then (same warp, same
 // subdomain) its boundary traces PU and pressure sum PS — the work of
 // k_part_traces / k_part_psum without two more launches.
@@ -1159,24 +1128,9 @@ __global__ void __launch_bounds__(twist_threads<B>()) k_part_solve_t(Layout L, i
     const int n = L.ncs;
     const size_t so = (size_t)s * n;
     double* x = X + xoff(L, max_rhs, s, 0);
-    // trace operands of the epilogue's edges, fetched before the sweep
-    constexpr int TQ = 4;  // edges per lane (nbe <= 128; wider subdomains fall back below)
-    TracePre pre[TQ];
-    if (threadIdx.x < 32) {
-#pragma unroll
-        for (int q = 0; q < TQ; ++q) {
-            const int idx = lane + 32 * q;
-            if (idx < L.nbe) pre[q] = part_trace_pre(L, s, idx, km, bc_kind, bm, bp, GZ);
-        }
-    }
     twisted_sweep<B>(n, D + so, Lc + so * B, Lr + so * B, MidB + (size_t)s * B * B, Sinv + (size_t)s * B * B, x, tsm);
     if (threadIdx.x >= 32) return;  // epilogue on warp 0
-#pragma unroll
-    for (int q = 0; q < TQ; ++q) {
-        const int idx = lane + 32 * q;
-        if (idx < L.nbe) PU[(size_t)s * L.nbe + idx] = part_trace_apply(pre[q], x[L.edge(s, idx).local_cell]);
-    }
-    for (int idx = lane + 32 * TQ; idx < L.nbe; idx += 32) {
+    for (int idx = lane; idx < L.nbe; idx += 32) {
         const EdgeInfo e = L.edge(s, idx);
         PU[(size_t)s * L.nbe + idx] = part_trace(L, s, idx, x[e.local_cell], km, bc_kind, bm, bp, GZ);
     }
