@@ -450,7 +450,7 @@ __device__ void pp_invert(PPTile S, double* xb, int* singular) {
             }
             const double piv = cb[k];
             const double colk = cb[r];
-            const double p = 1.0 / piv;
+            const double p = fast_rcp(piv);  // Newton-refined (<= 1 ulp), off the division slow path
             if (threadIdx.x == 0 && (!(piv != 0.0) || !isfinite(piv))) *singular = 1;
             const bool on = r == k;
             const double f = on ? 0.0 : colk * p;

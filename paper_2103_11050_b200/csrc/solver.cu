@@ -801,7 +801,7 @@ __global__ void k_ds_solve(Layout L, const double* __restrict__ BD, const double
 
 // Register-window variants (band_reg.cuh) for the common subdomain widths.
 template <int B>
-__global__ void __launch_bounds__(WPB * 32) k_ds_solve_r(Layout L, const double* __restrict__ BD,
+__global__ void __launch_bounds__(WPB * 32, 4) k_ds_solve_r(Layout L, const double* __restrict__ BD,
                                                          const double* __restrict__ BW, const double* __restrict__ BS,
                                                          double* D, double* Lr,
                                                          double* Xd, const double* __restrict__ RS,

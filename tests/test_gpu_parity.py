@@ -384,3 +384,55 @@ def test_blocktri_matches_dense_c2_sample():
     assert [s["rebuilt"] for s in rb.record.steps] == [s["rebuilt"] for s in rd.record.steps]
     assert np.max(np.abs(rb.s_final - rd.s_final)) <= TOL_S
     assert rel_l2(rb.p_final, rd.p_final) <= TOL_PU and rel_l2(rb.u_final, rd.u_final) <= TOL_PU
+
+
+def _sim_env(prob, **env):
+    """A context created with MPM2P_* switches set (read once, at creation)."""
+    import os
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update({k: str(v) for k, v in env.items()})
+    try:
+        return api.Simulator(prob)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+@pytest.mark.parametrize("name", ["C2", "C3"])
+def test_split_downscale_matches_fused(oracle, name):
+    """Split downscale (kappa_n operator factored on the side stream, sweeps on
+    the critical path) vs the fused factor + solve: same decisions and
+    counters, fields within the parity bar (C3: 10x its direct-solve floor)."""
+    import dataclasses
+    c = configs.build(name, te_override=41)
+    split = dataclasses.replace(c.split, stop_on_breakthrough=False, te=41)
+    rs = _sim_env(c.problem, MPM2P_DS_SPLIT=1).run(split, c.s0(), c.inflow_sat)
+    rf = _sim_env(c.problem, MPM2P_DS_SPLIT=0).run(split, c.s0(), c.inflow_sat)
+    assert [s["rebuilt"] for s in rs.record.steps] == [s["rebuilt"] for s in rf.record.steps]
+    assert rs.record.counters == rf.record.counters
+    fl = run_floor(oracle, c.problem, split, c.s0()) if name == "C3" else {"s": 0.0, "p": 0.0, "u": 0.0}
+    assert np.max(np.abs(rs.s_final - rf.s_final)) <= max(TOL_S, 10 * fl["s"])
+    assert rel_l2(rs.p_final, rf.p_final) <= max(TOL_PU, 10 * fl["p"])
+    assert rel_l2(rs.u_final, rf.u_final) <= max(TOL_PU, 10 * fl["u"])
+
+
+def test_upwind_tile_bitwise():
+    """The tiled upwind step is bit-identical to one thread per cell."""
+    c = configs.build("C2", te_override=31)
+    a = _sim_env(c.problem, MPM2P_UPWIND_TILE=1).run(c.split, c.s0())
+    b = _sim_env(c.problem, MPM2P_UPWIND_TILE=0).run(c.split, c.s0())
+    assert np.array_equal(a.s_final, b.s_final) and np.array_equal(a.u_final, b.u_final)
+    assert [s["dt"] for s in a.record.steps] == [s["dt"] for s in b.record.steps]
+
+
+def test_blocktri_persistent_sweeps_match():
+    """The persistent (one cooperative kernel) block sweeps vs per-step launches."""
+    c = configs.build("C2", te_override=21)
+    ra = _sim_env(c.problem, MPM2P_IFACE="blocktri", MPM2P_BT_PERSIST=1).run(c.split, c.s0())
+    rb = _sim_env(c.problem, MPM2P_IFACE="blocktri", MPM2P_BT_PERSIST=0).run(c.split, c.s0())
+    assert [s["rebuilt"] for s in ra.record.steps] == [s["rebuilt"] for s in rb.record.steps]
+    assert np.max(np.abs(ra.s_final - rb.s_final)) <= TOL_S
+    assert rel_l2(ra.p_final, rb.p_final) <= 1e-10 and rel_l2(ra.u_final, rb.u_final) <= 1e-10
