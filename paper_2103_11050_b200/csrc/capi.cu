@@ -301,7 +301,8 @@ void create_ctx(mpm2p_ctx* ctx, const mpm2p_problem* P) {
     c.bc_kind.alloc(nb);
     c.qsum_sub.alloc(ns);
     c.ground.alloc(ns);
-    if (c.repair_active) c.Linv.alloc(ns * ns);
+    c.sep_repair = c.repair_active && sep_repair_setup(c);
+    if (c.repair_active && !c.sep_repair) c.Linv.alloc(ns * ns);
     c.s.alloc(cells);
     c.s2.alloc(cells);
     c.u.alloc(faces);

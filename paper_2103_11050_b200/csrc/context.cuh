@@ -125,6 +125,8 @@ struct Ctx {
     // side stream (st2) while the particular / interface / recon chain runs;
     // only the two sweeps stay on the critical path
     bool ds_split = false;
+    bool sep_repair = false;  // separable repair solve (sep_repair_setup) instead of the dense inverse
+    DevBuf<double> sep_qx, sep_qy, sep_lam, sep_z1, sep_z2;
     bool upwind_tiled = true;  // k_upwind_tile (MPM2P_UPWIND_TILE=0: one thread per cell, k_upwind)
     bool ds_pending = false;  // a forked factor awaits its join (ev_join)
     cudaStream_t st2 = nullptr;
@@ -314,6 +316,7 @@ void launch_beta(Ctx& c, const double* kappa);
 void launch_rebuild(Ctx& c, const double* kappa, bool compute_beta = true);  // basis + interface matrix + recon_m + downscale
 void launch_mpm(Ctx& c, const double* kappa_n);       // MPM-2P update + downscale
 void launch_setup_static(Ctx& c);                     // qsum, ground, repair operator inverse
+bool sep_repair_setup(Ctx& c);                        // separable repair operator (before the Linv allocation)
 void configure_kernels();
 
 // ---- launchers (dense.cu) --------------------------------------------------

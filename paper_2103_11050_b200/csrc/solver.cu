@@ -1420,6 +1420,28 @@ __global__ void k_part_psum(Layout L, int max_rhs, const double* __restrict__ X,
 }
 
 // ---------------------------------------------------------------- static --
+// Separable repair solve (uniform subdomains, ground split by subdomain
+// column + row): L = I (x) Ax + Ay (x) I, so with Ax = Qx Lx Qx^T and
+// Ay = Qy Ly Qy^T, delta = Qy [(Qy^T R Qx) ./ (ly_i + lx_j)] Qx^T, where
+// R[sy][sx] = resid[sy nsx + sx]. One small GEMM per launch, one thread per
+// output: C[m x n] = op(A) op(B), op(X) = X or X^T (row-major, square
+// factors), optionally divided by (ly_i + lx_j).
+__global__ void k_sep_gemm(int m, int n, int kk, const double* __restrict__ A, int ta, const double* __restrict__ Bm,
+                           int tb, double* __restrict__ C, const double* __restrict__ lx, const double* __restrict__ ly) {
+    pdl_begin();
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= m * n) return;
+    const int i = idx / n, j = idx % n;
+    double acc = 0.0;
+    for (int t = 0; t < kk; ++t) {
+        const double a = ta ? A[(size_t)t * m + i] : A[(size_t)i * kk + t];
+        const double b = tb ? Bm[(size_t)j * kk + t] : Bm[(size_t)t * n + j];
+        acc = fma(a, b, acc);
+    }
+    if (lx) acc /= (ly[i] + lx[j]);
+    C[idx] = acc;
+}
+
 __global__ void k_static(Layout L, const double* __restrict__ q, const int* __restrict__ bc_kind,
                          double* __restrict__ qsum, double* __restrict__ ground) {
     pdl_begin();
@@ -1503,6 +1525,117 @@ void launch_beta(Ctx& c, const double* kappa) {
     }
 }
 
+namespace {
+// Cyclic Jacobi eigen-decomposition of a small symmetric matrix (row-major):
+// A = V diag(w) V^T, V's columns the eigenvectors.
+void jacobi_eigen(std::vector<double> A, int n, std::vector<double>& V, std::vector<double>& w) {
+    V.assign((size_t)n * n, 0.0);
+    for (int i = 0; i < n; ++i) V[(size_t)i * n + i] = 1.0;
+    double scale = 0.0;
+    for (double v : A) scale += v * v;
+    for (int sweep = 0; sweep < 100; ++sweep) {
+        double off = 0.0;
+        for (int p = 0; p < n; ++p)
+            for (int q = p + 1; q < n; ++q) off += A[(size_t)p * n + q] * A[(size_t)p * n + q];
+        if (off <= 1e-32 * scale) break;
+        for (int p = 0; p < n; ++p)
+            for (int q = p + 1; q < n; ++q) {
+                const double apq = A[(size_t)p * n + q];
+                if (apq == 0.0) continue;
+                const double theta = (A[(size_t)q * n + q] - A[(size_t)p * n + p]) / (2.0 * apq);
+                const double t = (theta >= 0.0 ? 1.0 : -1.0) / (std::fabs(theta) + std::sqrt(theta * theta + 1.0));
+                const double cs = 1.0 / std::sqrt(t * t + 1.0), sn = t * cs;
+                for (int k = 0; k < n; ++k) {  // columns p, q
+                    const double akp = A[(size_t)k * n + p], akq = A[(size_t)k * n + q];
+                    A[(size_t)k * n + p] = cs * akp - sn * akq;
+                    A[(size_t)k * n + q] = sn * akp + cs * akq;
+                }
+                for (int k = 0; k < n; ++k) {  // rows p, q
+                    const double apk = A[(size_t)p * n + k], aqk = A[(size_t)q * n + k];
+                    A[(size_t)p * n + k] = cs * apk - sn * aqk;
+                    A[(size_t)q * n + k] = sn * apk + cs * aqk;
+                }
+                for (int k = 0; k < n; ++k) {
+                    const double vkp = V[(size_t)k * n + p], vkq = V[(size_t)k * n + q];
+                    V[(size_t)k * n + p] = cs * vkp - sn * vkq;
+                    V[(size_t)k * n + q] = sn * vkp + cs * vkq;
+                }
+            }
+    }
+    w.resize(n);
+    for (int i = 0; i < n; ++i) w[i] = A[(size_t)i * n + i];
+}
+}  // namespace
+
+// The repair Laplacian (mrcm.cpp:347-371) is a Kronecker sum when every
+// vertical interface has the same area, every horizontal one too, and the
+// ground splits as g[s] = gx[sx] + gy[sy] (e.g. pressure faces on whole
+// west / east sides): L = I (x) Ax + Ay (x) I. Then the static n_sub x n_sub
+// inverse (C5: 16,384^2 = 2.1 GB, inverted at creation and read every step)
+// is replaced by two small eigen-decompositions and four small GEMMs per
+// step. Used above 4,096 subdomains (below, the dense GEMV is one launch);
+// MPM2P_REPAIR=sep / dense overrides.
+bool sep_repair_setup(Ctx& c) {
+    const Layout& L = c.L;
+    const char* env = std::getenv("MPM2P_REPAIR");
+    const bool force = env && std::strcmp(env, "sep") == 0;
+    if (env && std::strcmp(env, "dense") == 0) return false;
+    if (!c.grounded || L.n_sub < 2 || (!force && L.n_sub <= 4096)) return false;
+    const int nx = L.nsx, ny = L.nsy;
+    std::vector<double> g(L.n_sub, 0.0);  // k_static's ground, mrcm.cpp:333-336
+    for (int sd = 0; sd < L.n_sub; ++sd)
+        for (int idx = 0; idx < L.nbe; ++idx) {
+            const EdgeInfo e = L.edge(sd, idx);
+            if (e.iface < 0 && c.bc_kind_h[e.gbc] == BC_PRESSURE) g[sd] += e.area;
+        }
+    std::vector<double> gx(nx), gy(ny);
+    for (int i = 0; i < nx; ++i) gx[i] = g[i];
+    for (int j = 0; j < ny; ++j) gy[j] = g[(size_t)j * nx] - g[0];
+    for (int j = 0; j < ny; ++j)
+        for (int i = 0; i < nx; ++i) {
+            const double d = g[(size_t)j * nx + i] - (gx[i] + gy[j]);
+            if (std::fabs(d) > 1e-13 * (std::fabs(g[(size_t)j * nx + i]) + 1e-300)) return false;
+        }
+    const double av = L.sny * L.hy, ah = L.snx * L.hx;  // interface areas (uniform subdomains)
+    std::vector<double> Ax((size_t)nx * nx, 0.0), Ay((size_t)ny * ny, 0.0);
+    for (int i = 0; i + 1 < nx; ++i) {
+        Ax[(size_t)i * nx + i] += av;
+        Ax[(size_t)(i + 1) * nx + i + 1] += av;
+        Ax[(size_t)i * nx + i + 1] -= av;
+        Ax[(size_t)(i + 1) * nx + i] -= av;
+    }
+    for (int j = 0; j + 1 < ny; ++j) {
+        Ay[(size_t)j * ny + j] += ah;
+        Ay[(size_t)(j + 1) * ny + j + 1] += ah;
+        Ay[(size_t)j * ny + j + 1] -= ah;
+        Ay[(size_t)(j + 1) * ny + j] -= ah;
+    }
+    for (int i = 0; i < nx; ++i) Ax[(size_t)i * nx + i] += gx[i];
+    for (int j = 0; j < ny; ++j) Ay[(size_t)j * ny + j] += gy[j];
+    std::vector<double> Qx, Qy, lx, ly;
+    jacobi_eigen(Ax, nx, Qx, lx);
+    jacobi_eigen(Ay, ny, Qy, ly);
+    double mn = INFINITY, mx = 0.0;
+    for (double a : lx)
+        for (double b : ly) {
+            mn = std::min(mn, a + b);
+            mx = std::max(mx, std::fabs(a + b));
+        }
+    if (!(mn > 1e-12 * mx)) return false;  // singular: keep the dense path and its guard
+    c.sep_qx.alloc(Qx.size());
+    c.sep_qy.alloc(Qy.size());
+    c.sep_lam.alloc(nx + ny);
+    c.sep_z1.alloc((size_t)nx * ny);
+    c.sep_z2.alloc((size_t)nx * ny);
+    std::vector<double> lam(lx);
+    lam.insert(lam.end(), ly.begin(), ly.end());
+    CK(cudaMemcpyAsync(c.sep_qx.p, Qx.data(), Qx.size() * sizeof(double), cudaMemcpyHostToDevice, c.st));
+    CK(cudaMemcpyAsync(c.sep_qy.p, Qy.data(), Qy.size() * sizeof(double), cudaMemcpyHostToDevice, c.st));
+    CK(cudaMemcpyAsync(c.sep_lam.p, lam.data(), lam.size() * sizeof(double), cudaMemcpyHostToDevice, c.st));
+    CK(cudaStreamSynchronize(c.st));
+    return true;
+}
+
 void launch_setup_static(Ctx& c) {
     const Layout& L = c.L;
     {
@@ -1510,7 +1643,7 @@ void launch_setup_static(Ctx& c) {
         launch_k(c, k_static, grid_for(L.n_sub), TPB, 0, L, c.q, c.bc_kind, c.qsum_sub, c.ground);
         CK_LAUNCH();
     }
-    if (c.repair_active) {
+    if (c.repair_active && !c.sep_repair) {
         DevBuf<double> A;
         A.alloc((size_t)L.n_sub * L.n_sub);
         {
@@ -1577,7 +1710,35 @@ void downscale(Ctx& c, const double* kappa) {
                                                              c.red_count, 1);
         CK_LAUNCH();
     }
-    if (c.repair_active) {
+    if (c.repair_active && c.sep_repair) {  // delta = Qy [(Qy^T R Qx) ./ (ly + lx)] Qx^T
+        const int nx = L.nsx, ny = L.nsy, g = cdiv((long long)nx * ny, TPB);
+        const double* lx = c.sep_lam.p;
+        const double* ly = c.sep_lam.p + nx;
+        {
+            PROF(c, "k_sep_gemm");
+            launch_k(c, k_sep_gemm, g, TPB, 0, ny, nx, nx, c.resid.p, 0, c.sep_qx.p, 0, c.sep_z1.p, nullptr, nullptr);
+            CK_LAUNCH();
+        }
+        {
+            PROF(c, "k_sep_gemm");
+            launch_k(c, k_sep_gemm, g, TPB, 0, ny, nx, ny, c.sep_qy.p, 1, c.sep_z1.p, 0, c.sep_z2.p, lx, ly);
+            CK_LAUNCH();
+        }
+        {
+            PROF(c, "k_sep_gemm");
+            launch_k(c, k_sep_gemm, g, TPB, 0, ny, nx, ny, c.sep_qy.p, 0, c.sep_z2.p, 0, c.sep_z1.p, nullptr, nullptr);
+            CK_LAUNCH();
+        }
+        {
+            PROF(c, "k_sep_gemm");
+            launch_k(c, k_sep_gemm, g, TPB, 0, ny, nx, nx, c.sep_z1.p, 0, c.sep_qx.p, 1, c.delta.p, nullptr, nullptr);
+            CK_LAUNCH();
+        }
+        PROF(c, "k_repair_corr");
+        launch_k(c, k_repair_corr, std::min(grid_for(std::max(L.n_iface, L.n_sub)), 2 * c.num_sms), TPB, 0, L, 1,
+                 1, c.delta, c.ground, c.corr, c.sc, c.red, c.red_count);
+        CK_LAUNCH();
+    } else if (c.repair_active) {
         PROF(c, "k_repair_delta");
         launch_k(c, k_repair_delta, cdiv((long long)L.n_sub * 32, TPB), TPB, 0, 
             L.n_sub, c.Linv, c.resid, c.delta, L, c.grounded ? 1 : 0, c.ground, c.corr, c.sc, c.red_count);

@@ -436,3 +436,26 @@ def test_blocktri_persistent_sweeps_match():
     assert [s["rebuilt"] for s in ra.record.steps] == [s["rebuilt"] for s in rb.record.steps]
     assert np.max(np.abs(ra.s_final - rb.s_final)) <= TOL_S
     assert rel_l2(ra.p_final, rb.p_final) <= 1e-10 and rel_l2(ra.u_final, rb.u_final) <= 1e-10
+
+
+@pytest.mark.parametrize("nx,ny,nsx,nsy", [(32, 32, 4, 4), (48, 32, 6, 2), (64, 64, 16, 8)])
+def test_separable_repair_parity(oracle, nx, ny, nsx, nsy):
+    """The separable repair solve (Kronecker-sum eigen-decomposition, used
+    above 4,096 subdomains) forced on small pressure-drop problems: vs the
+    dense-inverse path and vs the oracle's dense LDL^T (mrcm.cpp:347-383)."""
+    K = random_kappa(nx, ny, 5, 0.1, 10.0)
+    prob = problem(nx, ny, nsx, nsy, K, M=5.0)
+    gs = _sim_env(prob, MPM2P_REPAIR="sep")
+    gd = _sim_env(prob, MPM2P_REPAIR="dense")
+    o = api.Simulator(prob, oracle)
+    a, b, r = gs.mrcm_solve(K), gd.mrcm_solve(K), o.mrcm_solve(K)
+    for x, y in ((a.p, b.p), (a.u, b.u), (a.p, r.p), (a.u, r.u)):
+        assert rel_l2(x, y) <= 1e-10
+    kn = K * np.exp(0.05 * np.random.default_rng(7).standard_normal(K.size))
+    ma, mr = gs.mpm_pressure_update(kn), o.mpm_pressure_update(kn)
+    assert rel_l2(ma.p, mr.p) <= 1e-10 and rel_l2(ma.u, mr.u) <= 1e-10
+    sp = api.SplittingConfig(method=api.MPM2P, eta=0.01, eta_mode=api.EPS_RELATIVE, te=25, cfl_safety=0.5)
+    ra, rr = gs.run(sp), o.run(sp)
+    assert [s["rebuilt"] for s in ra.record.steps] == [s["rebuilt"] for s in rr.record.steps]
+    assert np.max(np.abs(ra.s_final - rr.s_final)) <= TOL_S
+    assert rel_l2(ra.u_final, rr.u_final) <= TOL_PU
