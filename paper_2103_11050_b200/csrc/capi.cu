@@ -268,6 +268,7 @@ void create_ctx(mpm2p_ctx* ctx, const mpm2p_problem* P) {
     if (const char* e = std::getenv("MPM2P_BT_PERSIST")) c.bt_persistent = e[0] == '1';
     if (const char* e = std::getenv("MPM2P_GRAPH_TIMING")) c.graph_timing = e[0] == '1';
     if (const char* e = std::getenv("MPM2P_UPWIND_TILE")) c.upwind_tiled = e[0] != '0';
+    if (const char* e = std::getenv("MPM2P_RHS_SUB")) c.rhs_sub = e[0] != '0';
     if (const char* e = std::getenv("MPM2P_REFINE")) {  // 1: always refine, 0: never (experiments)
         c.force_refine = e[0] == '1';
         c.never_refine = e[0] == '0';
@@ -365,6 +366,7 @@ void create_ctx(mpm2p_ctx* ctx, const mpm2p_problem* P) {
     // subdomains per SM); with many subdomains the one-warp kernels keep
     // higher occupancy (C5: 16,384 subdomains)
     c.twist_ok = !c.no_regband && !c.no_twist && L.sny >= 3 && L.n_sub <= 8 * c.num_sms;
+    if (const char* e = std::getenv("MPM2P_TWIST")) c.twist_ok = !c.no_regband && L.sny >= 3 && e[0] == '1';
     c.twist_store = c.twist_ok &&
                     (L.snx == 4 || L.snx == 8 || L.snx == 10 || L.snx == 12 || L.snx == 16 || L.snx == 20 ||
                      L.snx == 24 || L.snx == 32);

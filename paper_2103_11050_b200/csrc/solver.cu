@@ -1369,6 +1369,100 @@ __global__ void k_mpm_rhs(Layout L, int max_rhs, int anchor, const double* __res
 }
 
 // Particular solve with the cached rebuild factor (mrcm.cpp:248).
+// k_mpm_rhs restructured per subdomain: one 256-thread CTA per subdomain.
+// Every operand (the cells' face transmissibilities, q, neighbour pressures
+// and the boundary edges' data) is loaded in one round, the boundary-edge
+// terms are formed once per edge by dedicated threads (no divergent edge
+// loop in the cell threads), and each cell applies its edges' terms to b in
+// k_mpm_rhs's W, E, S, N order, so X, GZ and WU are bit-identical.
+constexpr int RHS_TPB = 256, RHS_CPT = 4;  // cells per thread (subdomains up to 1,024 cells)
+__global__ void __launch_bounds__(RHS_TPB) k_mpm_rhs_sub(Layout L, int max_rhs, int anchor,
+                                                         const double* __restrict__ kn, const double* __restrict__ km,
+                                                         const double* __restrict__ Tn, const double* __restrict__ q,
+                                                         const int* __restrict__ bc_kind,
+                                                         const double* __restrict__ bc_value,
+                                                         const double* __restrict__ bm, const double* __restrict__ bp,
+                                                         const double* __restrict__ pm, const double* __restrict__ bpm,
+                                                         double* __restrict__ X, double* __restrict__ GZ,
+                                                         double* __restrict__ WU) {
+    pdl_begin();
+    extern __shared__ double rsm[];
+    double* pmS = rsm;                 // ncs
+    double* wunS = rsm + L.ncs;        // nbe: outward w of each boundary edge
+    double* termS = wunS + L.nbe;      // nbe: the edge's term in b
+    const int s = blockIdx.x;
+    const int i0 = L.sub_i0(s), j0 = L.sub_j0(s);
+    // cell operands (registers), issued together with the pm / edge loads
+    double pc[RHS_CPT], tW[RHS_CPT], tE[RHS_CPT], tS[RHS_CPT], tN[RHS_CPT], qv[RHS_CPT];
+#pragma unroll
+    for (int k = 0; k < RHS_CPT; ++k) {
+        const int r = threadIdx.x + RHS_TPB * k;
+        pc[k] = tW[k] = tE[k] = tS[k] = tN[k] = qv[k] = 0.0;
+        if (r < L.ncs) {
+            const int ii = r % L.snx, jj = r / L.snx, i = i0 + ii, j = j0 + jj;
+            pc[k] = pm[L.cell(i, j)];
+            tW[k] = Tn[L.vface(i, j)];
+            tE[k] = Tn[L.vface(i + 1, j)];
+            tS[k] = Tn[L.hface(i, j)];
+            tN[k] = Tn[L.hface(i, j + 1)];
+            qv[k] = q[L.cell(i, j)];
+        }
+    }
+    // boundary edges (k_mpm_rhs's per-edge arithmetic, mpm.cpp:64-85)
+    for (int idx = threadIdx.x; idx < L.nbe; idx += RHS_TPB) {
+        const EdgeInfo e = L.edge(s, idx);
+        const size_t eo = (size_t)s * L.nbe + idx;
+        const double pce = pm[e.global_cell];
+        const double tn = half_trans(L, e.side, kn[e.global_cell]);
+        const double wun = tn * (pce - bpm[eo]) / e.area;
+        const double th = half_trans(L, e.side, km[e.global_cell]);
+        WU[eo] = wun;
+        double term;
+        if (e.iface >= 0) {
+            term = eff_robin(th, edge_beta(L, e, bm, bp), e.area) * 0.0;
+            GZ[eo] = 0.0;
+        } else if (bc_kind[e.gbc] == BC_PRESSURE) {
+            const double g = bc_value[e.gbc] - bpm[eo];
+            GZ[eo] = g;
+            term = th * g;
+        } else {
+            const double z = bc_value[e.gbc] - wun;
+            GZ[eo] = z;
+            term = -(z * e.area);
+        }
+        wunS[idx] = (e.side == SIDE_E || e.side == SIDE_N) ? wun : -wun;  // global orientation
+        termS[idx] = term;
+    }
+#pragma unroll
+    for (int k = 0; k < RHS_CPT; ++k) {
+        const int r = threadIdx.x + RHS_TPB * k;
+        if (r < L.ncs) pmS[r] = pc[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < RHS_CPT; ++k) {
+        const int r = threadIdx.x + RHS_TPB * k;
+        if (r >= L.ncs) continue;
+        const int ii = r % L.snx, jj = r / L.snx;
+        const double p0 = pc[k];
+        const int eW = jj, eE = L.sny + jj, eS = 2 * L.sny + ii, eN = 2 * L.sny + L.snx + ii;
+        const double wW = ii > 0 ? tW[k] * (pmS[r - 1] - p0) / L.hy : wunS[eW];
+        const double wE = ii < L.snx - 1 ? tE[k] * (p0 - pmS[r + 1]) / L.hy : wunS[eE];
+        const double wS = jj > 0 ? tS[k] * (pmS[r - L.snx] - p0) / L.hx : wunS[eS];
+        const double wN = jj < L.sny - 1 ? tN[k] * (p0 - pmS[r + L.snx]) / L.hx : wunS[eN];
+        const double fx = (wE - wW) * L.hy;
+        const double fy = (wN - wS) * L.hx;
+        const double divw = (fx + fy) / L.vol();
+        double b = (qv[k] - divw) * L.vol();
+        if (ii == 0) b += termS[eW];
+        if (ii == L.snx - 1) b += termS[eE];
+        if (jj == 0) b += termS[eS];
+        if (jj == L.sny - 1) b += termS[eN];
+        if (anchor && r == 0) b = 0.0;
+        X[xoff(L, max_rhs, s, 0) + r] = b;
+    }
+}
+
 __global__ void k_part_solve(Layout L, int max_rhs, const double* __restrict__ D, const double* __restrict__ Lc,
                              const double* __restrict__ Lr, double* __restrict__ X) {
     pdl_begin();
@@ -2004,9 +2098,13 @@ void launch_mpm(Ctx& c, const double* kn) {  // mpm_pressure_update (mpm.cpp:31-
     ds_factor_fork(c);  // downscale operator of kappa_n, concurrent with the particular / interface chain
     {
         PROF(c, "k_mpm_rhs");
-        launch_k(c, k_mpm_rhs, grid_for(L.cells()), TPB, 0, L, c.max_rhs, c.anchor_m ? 1 : 0, kn, c.kappa_m, c.T, c.q,
-                                                         c.bc_kind, c.bc_value, c.beta_m, c.beta_p, c.pm, c.bpm, c.X,
-                                                         c.GZ, c.WU);
+        if (c.rhs_sub && L.ncs <= RHS_TPB * RHS_CPT)
+            launch_k(c, k_mpm_rhs_sub, L.n_sub, RHS_TPB, (size_t)(L.ncs + 2 * L.nbe) * sizeof(double), L, c.max_rhs,
+                     c.anchor_m ? 1 : 0, kn, c.kappa_m, c.T, c.q, c.bc_kind, c.bc_value, c.beta_m, c.beta_p, c.pm,
+                     c.bpm, c.X, c.GZ, c.WU);
+        else
+            launch_k(c, k_mpm_rhs, grid_for(L.cells()), TPB, 0, L, c.max_rhs, c.anchor_m ? 1 : 0, kn, c.kappa_m, c.T,
+                     c.q, c.bc_kind, c.bc_value, c.beta_m, c.beta_p, c.pm, c.bpm, c.X, c.GZ, c.WU);
         CK_LAUNCH();
     }
     const size_t sm1 = (size_t)WPB * band_smem_doubles(L.snx, 1) * sizeof(double);

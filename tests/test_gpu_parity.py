@@ -459,3 +459,12 @@ def test_separable_repair_parity(oracle, nx, ny, nsx, nsy):
     assert [s["rebuilt"] for s in ra.record.steps] == [s["rebuilt"] for s in rr.record.steps]
     assert np.max(np.abs(ra.s_final - rr.s_final)) <= TOL_S
     assert rel_l2(ra.u_final, rr.u_final) <= TOL_PU
+
+
+def test_mpm_rhs_per_subdomain_bitwise():
+    """k_mpm_rhs_sub (one CTA per subdomain) is bit-identical to one thread per cell."""
+    c = configs.build("C2", te_override=31)
+    a = _sim_env(c.problem, MPM2P_RHS_SUB=1).run(c.split, c.s0())
+    b = _sim_env(c.problem, MPM2P_RHS_SUB=0).run(c.split, c.s0())
+    assert np.array_equal(a.s_final, b.s_final) and np.array_equal(a.u_final, b.u_final)
+    assert np.array_equal(a.p_final, b.p_final)
