@@ -366,10 +366,200 @@ __global__ void __launch_bounds__(UT_X * UT_Y) k_upwind_tile(Layout L, const dou
     s_out[L.cell(i, j)] = sn < 0.0 ? 0.0 : (sn > 1.0 ? 1.0 : sn);
 }
 
+// Column-marching upwind_step. A warp owns 30 columns (lanes 1..30; lanes 0
+// and 31 are the west / east halo columns and only evaluate f) and marches
+// `rows` rows northwards. The f of the rows below / at / above stays in
+// registers and the west / east neighbours' f come by shuffle, so a cell costs
+// one f evaluation (plus 1/rows for the segment's two halo rows and 2/30 for
+// the halo lanes) and no shared-memory round trip or CTA barrier. k_upwind_tile
+// spent ~370 issued instructions per cell (C2 ncu: issue-bound at C5). Each
+// chunk of RB rows issues its loads one chunk ahead of its arithmetic. Face fluxes
+// use k_upwind's operations in the same order, so s is bit-identical; clamp
+// counts follow k_upwind_tile (the owner of a face counts an out-of-range
+// upwind saturation).
+constexpr int UC_COLS = 30;
+__device__ __forceinline__ bool out_of_range(double v) { return v < 0.0 || v > 1.0; }
+template <int RB, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_upwind_col(Layout L, const double* __restrict__ s, double* __restrict__ s_out,
+                                                    const double* __restrict__ u, Scalars* sc, double inflow, double M,
+                                                    int take_next, int inj_cn, int sub, int rows) {
+    pdl_begin();
+    const int lane = threadIdx.x & 31;
+    const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int ncw = (L.nx + UC_COLS - 1) / UC_COLS;
+    const int wc = gw % ncw, wr = gw / ncw;
+    const int j0 = wr * rows;
+    const double dt = take_next ? sc->dt_next : (sub > 1 ? sc->dt / sub : sc->dt);
+    if (gw == 0 && lane == 0) {
+        (void)frac_flow(inflow, M, &sc->clamp);  // f_in is evaluated once per call
+        if (take_next) {
+            sc->dt = dt;
+            sc->any_flow = sc->any_next;
+            const double rt = sc->inj_next;
+            sc->inj = rt;
+            const double pore = L.lx * L.ly;
+            for (int k = 0; k < inj_cn; ++k) sc->pvi += rt * dt / pore;
+        }
+    }
+    if (j0 >= L.ny) return;  // warp-uniform
+    const int j1 = min(j0 + rows, L.ny);
+    const int i = wc * UC_COLS + lane - 1;
+    const bool col = i >= 0 && i < L.nx;
+    const bool own = col && lane >= 1 && lane <= UC_COLS;
+    const bool firstx = i == 0, lastx = i + 1 == L.nx;
+    const double fin = frac_flow(inflow, M, nullptr);
+    const double dtv = dt / L.vol();
+    const double hx = L.hx, hy = L.hy;
+    // the row below the segment and the segment's first row
+    double fS = 0.0, fC = 0.0, uS = 0.0;
+    bool oS = false, oC = false;
+    const double sc0 = col ? s[L.cell(i, j0)] : 0.0;
+    {
+        const double sb = (col && j0 > 0) ? s[L.cell(i, j0 - 1)] : 0.0;
+        if (own) uS = u[L.hface(i, j0)];
+        if (col && j0 > 0) {
+            oS = out_of_range(sb);
+            fS = frac_flow(sb, M, nullptr);
+        }
+        if (col) {
+            oC = out_of_range(sc0);
+            fC = frac_flow(sc0, M, nullptr);
+        }
+    }
+    double sCv = sc0;
+    unsigned long long cnt = 0;
+    bool err = false;
+    unsigned obS = __ballot_sync(0xffffffffu, oS);
+    // running row pointers (clamped column for the lanes that load nothing)
+    const int ic = col ? i : 0;
+    const double* ps = s + L.cell(ic, j0) + L.nx;   // s of row j + 1
+    const double* pv = u + L.vface(ic, j0);          // vertical faces of row j
+    const double* ph = u + L.hface(ic, j0) + L.nx;   // horizontal face north of row j
+    double* po = s_out + L.cell(ic, j0);
+    // software pipeline: chunk n + 1's loads are in flight while chunk n computes
+    double sN[RB], uW[RB], uE[RB], uN[RB];
+    auto load_chunk = [&](int jb, double* a, double* w, double* e, double* n) {
+#pragma unroll
+        for (int k = 0; k < RB; ++k) {
+            const int j = jb + k;
+            a[k] = (col && j < j1 && j + 1 < L.ny) ? ps[k * L.nx] : 0.0;
+            const bool ld = own && j < j1;
+            w[k] = ld ? pv[k * (L.nx + 1)] : 0.0;
+            e[k] = ld ? pv[k * (L.nx + 1) + 1] : 0.0;
+            n[k] = ld ? ph[k * L.nx] : 0.0;
+        }
+        ps += RB * L.nx;
+        pv += RB * (L.nx + 1);
+        ph += RB * L.nx;
+    };
+    load_chunk(j0, sN, uW, uE, uN);
+    for (int jb = j0; jb < j1; jb += RB) {
+        double sN2[RB], uW2[RB], uE2[RB], uN2[RB];
+        load_chunk(jb + RB, sN2, uW2, uE2, uN2);
+#pragma unroll
+        for (int k = 0; k < RB; ++k) {
+            // the tail rows of a segment (j >= j1) run predicated, so the
+            // shuffles below stay outside any divergent region
+            const int j = jb + k;
+            const bool row = j < j1;
+            // rows / lanes without a north cell loaded s = 0 (in range, f = 0),
+            // and their f is never selected: no branch around the division
+            const bool oN = out_of_range(sN[k]);
+            const double fN = frac_flow(sN[k], M, nullptr);
+            const double fWc = __shfl_up_sync(0xffffffffu, fC, 1);
+            const double fEc = __shfl_down_sync(0xffffffffu, fC, 1);
+            const unsigned ob = __ballot_sync(0xffffffffu, oC);
+            if (own && row) {
+                const bool lasty = j + 1 == L.ny;
+                const double fE = uE[k] >= 0.0 ? fC : (lastx ? fin : fEc);
+                const double fWv = uW[k] >= 0.0 ? (firstx ? fin : fWc) : fC;
+                const double fNv = uN[k] >= 0.0 ? fC : (lasty ? fin : fN);
+                const double fSv = uS >= 0.0 ? (j == 0 ? fin : fS) : fC;
+                const double wE = fE * uE[k] * hy, wW = fWv * uW[k] * hy;
+                const double wN = fNv * uN[k] * hx, wS = fSv * uS * hx;
+                if (ob | obS) {  // warp-uniform: some saturation of this row or the one below is out of range
+                    const bool oW = (ob >> (lane - 1)) & 1u;
+                    cnt += uW[k] >= 0.0 ? (!firstx && oW) : oC;
+                    cnt += uS >= 0.0 ? (j > 0 && oS) : oC;
+                    cnt += (lastx && uE[k] >= 0.0) ? oC : 0;
+                    cnt += (lasty && uN[k] >= 0.0) ? oC : 0;
+                }
+                const double net = wE - wW + wN - wS;
+                const double sn = sCv - dtv * net;
+                err |= sn < -1e-12 || sn > 1.0 + 1e-12;
+                po[k * L.nx] = sn < 0.0 ? 0.0 : (sn > 1.0 ? 1.0 : sn);
+            }
+            fS = fC;
+            oS = oC;
+            obS = ob;
+            fC = fN;
+            oC = oN;
+            sCv = sN[k];
+            uS = uN[k];
+        }
+        po += RB * L.nx;
+#pragma unroll
+        for (int k = 0; k < RB; ++k) {
+            sN[k] = sN2[k];
+            uW[k] = uW2[k];
+            uE[k] = uE2[k];
+            uN[k] = uN2[k];
+        }
+    }
+    if (cnt) atomicAdd((unsigned long long*)&sc->clamp, cnt);
+    if (err) atomicOr(&sc->err, ERR_CFL);
+}
+
+int upwind_col_rows(const Layout& L, int nsm) {
+    const long ncw = (L.nx + UC_COLS - 1) / UC_COLS;
+    int rows = 32;
+    while (rows > 4 && ncw * ((L.ny + rows - 1) / rows) < 48L * nsm) rows >>= 1;
+    return rows;
+}
+
 // conductivity (transport.cpp:122-126) + the drift partial sums
 // (mpm.cpp:14-20 / simulation.cpp:169-172) in double-double.
 // eps_mode: -1 none, 0 relative, 1 absolute, 2 mobility (vs lam_reb)
 __device__ __forceinline__ void decide(Scalars* sc, int rebuilt, int method, double eta, int step);
+
+// Block partials of the drift sums, then (last block) the combination in
+// block order, eps and the next-step decision.
+__device__ __forceinline__ void kappa_eps_tail(DD num, DD den, Scalars* sc, double M, int eps_mode, double* part,
+                                               unsigned* counter, int decide_method, int rebuilt, double eta) {
+    __shared__ DD shd2[64];
+    block_reduce_dd2(num, den, shd2);
+    if (threadIdx.x == 0) {
+        part[4 * blockIdx.x + 0] = num.hi;
+        part[4 * blockIdx.x + 1] = num.lo;
+        part[4 * blockIdx.x + 2] = den.hi;
+        part[4 * blockIdx.x + 3] = den.lo;
+    }
+    if (last_block_done(counter)) {
+        DD n{0.0, 0.0}, d{0.0, 0.0};
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+            n = dd_add(n, DD{__ldcg(part + 4 * b), __ldcg(part + 4 * b + 1)});
+            d = dd_add(d, DD{__ldcg(part + 4 * b + 2), __ldcg(part + 4 * b + 3)});
+        }
+        block_reduce_dd2(n, d, shd2);
+        if (threadIdx.x == 0) {
+            const double a = sqrt(n.hi);
+            double e;
+            if (eps_mode == 1) e = a;
+            else if (eps_mode == 2) e = a / M;
+            else {
+                if (!(d.hi > 0.0)) atomicOr(&sc->err, ERR_EPS_ZERO);
+                e = a / sqrt(d.hi);
+            }
+            sc->eps_pending = e;
+            sc->eps_num_hi = n.hi;
+            sc->eps_num_lo = n.lo;
+            sc->eps_den_hi = d.hi;
+            sc->eps_den_lo = d.lo;
+            *counter = 0;
+            if (decide_method >= 0) decide(sc, rebuilt, decide_method, eta, 1);
+        }
+    }
+}
 
 // With decide_method >= 0 the last block also takes the next-step decision
 // (k_decide) from the drift it just formed.
@@ -407,39 +597,74 @@ __global__ void k_kappa(Layout L, const double* __restrict__ K, const double* __
         }
     }
     if (eps_mode < 0) return;
-    __shared__ DD shd2[64];
-    block_reduce_dd2(num, den, shd2);
-    if (threadIdx.x == 0) {
-        part[4 * blockIdx.x + 0] = num.hi;
-        part[4 * blockIdx.x + 1] = num.lo;
-        part[4 * blockIdx.x + 2] = den.hi;
-        part[4 * blockIdx.x + 3] = den.lo;
-    }
-    if (last_block_done(counter)) {
-        DD n{0.0, 0.0}, d{0.0, 0.0};
-        for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
-            n = dd_add(n, DD{__ldcg(part + 4 * b), __ldcg(part + 4 * b + 1)});
-            d = dd_add(d, DD{__ldcg(part + 4 * b + 2), __ldcg(part + 4 * b + 3)});
-        }
-        block_reduce_dd2(n, d, shd2);
-        if (threadIdx.x == 0) {
-            const double a = sqrt(n.hi);
-            double e;
-            if (eps_mode == 1) e = a;
-            else if (eps_mode == 2) e = a / M;
-            else {
-                if (!(d.hi > 0.0)) atomicOr(&sc->err, ERR_EPS_ZERO);
-                e = a / sqrt(d.hi);
+    kappa_eps_tail(num, den, sc, M, eps_mode, part, counter, decide_method, rebuilt, eta);
+}
+
+// Row-marching k_kappa (same outputs): a warp owns 31 columns (lane 0 is the
+// west halo column) and `rows` rows. The west neighbour's conductivity comes
+// by shuffle and the south one stays in a register, so each cell's total
+// mobility is evaluated once (k_kappa evaluates it three times per cell with
+// T and recovers (i, j) by a division). Transmissibilities use the same
+// harm_trans_v / harm_trans_h operations on the same conductivity values, so
+// kappa and T are bit-identical; the drift sums are double-double as in
+// k_kappa (only the partition into partials differs). Warp tasks are
+// grid-strided over one resident wave, so c.red holds the block partials.
+constexpr int KC_COLS = 31;
+__global__ void __launch_bounds__(256) k_kappa_col(Layout L, const double* __restrict__ K, const double* __restrict__ s,
+                                                   double* __restrict__ kappa, const double* __restrict__ kappa_m,
+                                                   const double* __restrict__ lam_reb, Scalars* sc, double M,
+                                                   int eps_mode, double* part, unsigned* counter, int decide_method,
+                                                   int rebuilt, double eta, double* __restrict__ T, int rows) {
+    pdl_begin();
+    const double vol = L.vol();
+    const int lane = threadIdx.x & 31;
+    const int ncw = (L.nx + KC_COLS - 1) / KC_COLS, tasks = ncw * ((L.ny + rows - 1) / rows);
+    DD num{0.0, 0.0}, den{0.0, 0.0};
+    unsigned long long clampc = 0;
+    bool bad = false;
+    for (int task = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); task < tasks;
+         task += gridDim.x * (blockDim.x >> 5)) {  // warp-uniform
+        const int wc = task % ncw, j0 = (task / ncw) * rows, j1 = min(j0 + rows, L.ny);
+        const int i = wc * KC_COLS + lane - 1;
+        const bool col = i >= 0 && i < L.nx, own = col && lane >= 1;
+        const int ic = col ? i : 0;
+        double kS = 0.0;
+        if (col && j0 > 0) kS = total_mob(s[L.cell(ic, j0 - 1)], M, nullptr) * K[L.cell(ic, j0 - 1)];
+#pragma unroll 2
+        for (int j = j0; j < j1; ++j) {
+            const int c = L.cell(ic, j);
+            const double sv = col ? s[c] : 0.0, Kv = col ? K[c] : 1.0;
+            const double km = (own && (eps_mode == 0 || eps_mode == 1)) ? kappa_m[c] : 0.0;
+            const double lr = (own && eps_mode == 2) ? lam_reb[c] : 0.0;
+            const double lam = total_mob(sv, M, nullptr);
+            const double k = lam * Kv;
+            const double kW = __shfl_up_sync(0xffffffffu, k, 1);
+            if (own) {
+                clampc += (sv < 0.0 || sv > 1.0) ? 1 : 0;  // the cell's own evaluation counts (transport.cpp:13-21)
+                kappa[c] = k;
+                if (T) {  // elliptic.cpp:44-61 for this cell's faces (boundary faces carry 0)
+                    T[L.vface(i, j)] = i > 0 ? harm_trans_v(L, kW, k) : 0.0;
+                    T[L.hface(i, j)] = j > 0 ? harm_trans_h(L, kS, k) : 0.0;
+                    if (i == L.nx - 1) T[L.vface(L.nx, j)] = 0.0;
+                    if (j == L.ny - 1) T[L.hface(i, L.ny)] = 0.0;
+                }
+                bad |= !(k > 0.0) || !isfinite(k);
+                if (eps_mode == 0 || eps_mode == 1) {
+                    const double d = k - km;
+                    num = dd_add(num, DD{d * d * vol, 0.0});
+                    den = dd_add(den, DD{km * km * vol, 0.0});
+                } else if (eps_mode == 2) {
+                    const double d = lam - lr;
+                    num = dd_add(num, DD{d * d * vol, 0.0});
+                }
             }
-            sc->eps_pending = e;
-            sc->eps_num_hi = n.hi;
-            sc->eps_num_lo = n.lo;
-            sc->eps_den_hi = d.hi;
-            sc->eps_den_lo = d.lo;
-            *counter = 0;
-            if (decide_method >= 0) decide(sc, rebuilt, decide_method, eta, 1);
+            kS = k;
         }
     }
+    if (clampc) atomicAdd((unsigned long long*)&sc->clamp, clampc);
+    if (bad) atomicOr(&sc->err, ERR_KAPPA);
+    if (eps_mode < 0) return;
+    kappa_eps_tail(num, den, sc, M, eps_mode, part, counter, decide_method, rebuilt, eta);
 }
 
 // The MPM-2P vs MRCM decision for the NEXT step, on the device
@@ -640,7 +865,17 @@ void launch_upwind(Ctx& c, const double* s_in, double* s_out, const double* u, d
                    int inj_cn, int sub) {
     {
         PROF(c, "k_upwind");
-        if (c.upwind_tiled)
+        const int rows = upwind_col_rows(c.L, c.num_sms);
+        // auto (-1): column marching where each warp gets a long segment
+        // (C5: 191 vs 254 us); short segments (C2, C4) keep the tiled step
+        if (c.upwind_col > 0 || (c.upwind_col < 0 && rows >= 16)) {
+            const long ncw = (c.L.nx + UC_COLS - 1) / UC_COLS, warps = ncw * ((c.L.ny + rows - 1) / rows);
+            auto kern = k_upwind_col<1, 3>;
+            if (c.upwind_rb == 2) kern = k_upwind_col<2, 3>;
+            else if (c.upwind_rb == 4) kern = k_upwind_col<4, 2>;
+            launch_k(c, kern, (int)((warps + 7) / 8), 256, 0, c.L, s_in, s_out, u, c.sc, inflow, c.M,
+                     take_next ? 1 : 0, inj_cn, sub, rows);
+        } else if (c.upwind_tiled)
             launch_k(c, k_upwind_tile, dim3(cdiv(c.L.nx, UT_X), cdiv(c.L.ny, UT_Y)), UT_X * UT_Y, 0, c.L, s_in, s_out, u,
                      c.sc, inflow, c.M, take_next ? 1 : 0, inj_cn, sub);
         else
@@ -654,19 +889,33 @@ void launch_cfl_inj(Ctx& c, const double* u, double safety, double dt_cap, doubl
     launch_k(c, k_cfl, red_blocks(c, k_cfl, c.L.cells()), TPB, 0, c.L, u, c.sc, safety, dt_cap, c.red, c.red_count, cn, inflow, c.M);
     CK_LAUNCH();
 }
+// auto (kappa_col < 0): the row-marching kernel where warps get long row
+// segments (C5); otherwise the one-thread-per-cell k_kappa
+static void launch_kappa(Ctx& c, const double* s, double* kappa, int eps_mode, int method, int rebuilt, double eta,
+                         double* T) {
+    const long ncw = (c.L.nx + KC_COLS - 1) / KC_COLS;
+    int rows = 32;
+    while (rows > 4 && ncw * ((c.L.ny + rows - 1) / rows) < 48L * c.num_sms) rows >>= 1;
+    if (c.kappa_col > 0 || (c.kappa_col < 0 && rows >= 16)) {
+        const long tasks = ncw * ((c.L.ny + rows - 1) / rows);
+        launch_k(c, k_kappa_col, red_blocks(c, k_kappa_col, 32 * tasks), TPB, 0, c.L, c.K, s, kappa, c.kappa_m,
+                 c.lam_reb, c.sc, c.M, eps_mode, c.red, c.red_count, method, rebuilt, eta, T, rows);
+    } else {
+        launch_k(c, k_kappa, red_blocks(c, k_kappa, c.L.cells()), TPB, 0, c.L, c.K, s, kappa, c.kappa_m, c.lam_reb,
+                 c.sc, c.M, eps_mode, c.red, c.red_count, method, rebuilt, eta, T);
+    }
+}
 void launch_conductivity_decide(Ctx& c, const double* s, double* kappa, int eps_mode, int rebuilt, int method,
                                 double eta) {
     PROF(c, "k_kappa");
-    launch_k(c, k_kappa, red_blocks(c, k_kappa, c.L.cells()), TPB, 0, c.L, c.K, s, kappa, c.kappa_m, c.lam_reb, c.sc, c.M, eps_mode, c.red,
-                                           c.red_count, method, rebuilt, eta, c.T.p);
+    launch_kappa(c, s, kappa, eps_mode, method, rebuilt, eta, c.T.p);
     c.trans_fresh = true;  // T = transmissibility(kappa) is current: the next rebuild / MPM step skips k_trans
     CK_LAUNCH();
 }
 void launch_conductivity(Ctx& c, const double* s, double* kappa, int eps_mode, bool want_eps) {
     {
         PROF(c, "k_kappa");
-        launch_k(c, k_kappa, red_blocks(c, k_kappa, c.L.cells()), TPB, 0, c.L, c.K, s, kappa, c.kappa_m, c.lam_reb, c.sc, c.M,
-                                               want_eps ? eps_mode : -1, c.red, c.red_count, -1, 0, 0.0, nullptr);
+        launch_kappa(c, s, kappa, want_eps ? eps_mode : -1, -1, 0, 0.0, nullptr);
         CK_LAUNCH();
     }
 }
