@@ -129,7 +129,9 @@ def kernel_work(name, cfg, sz, dim):
     table = {
         "k_upwind": ("hbm", 32.0 * cells),                       # s r/w + 2 faces of u
         "k_cfl": ("hbm", 16.0 * cells),
-        "k_kappa": ("hbm", 32.0 * cells),                        # s, K, kappa_m, kappa
+        # the driver's per-step launch reads s, K, kappa_m and writes kappa and the
+        # fused transmissibilities T (2 faces per cell): 24 + 8 + 16 B per cell
+        "k_kappa": ("hbm", 48.0 * cells),
         "k_part_solve": ("hbm", ns * n * (16.0 * B + 24.0)),     # Lcol, Lrow, D, x r/w
         "k_ds_solve": ("fp64", ns * (n * B * B + 4.0 * n * B)),  # banded LDL^T factor + 2 sweeps
         "k_ds_factor": ("fp64", ns * n * B * B),                # split downscale: factor (side stream)

@@ -419,13 +419,71 @@ def test_split_downscale_matches_fused(oracle, name):
     assert rel_l2(rs.u_final, rf.u_final) <= max(TOL_PU, 10 * fl["u"])
 
 
-def test_upwind_tile_bitwise():
-    """The tiled upwind step is bit-identical to one thread per cell."""
-    c = configs.build("C2", te_override=31)
-    a = _sim_env(c.problem, MPM2P_UPWIND_TILE=1).run(c.split, c.s0())
-    b = _sim_env(c.problem, MPM2P_UPWIND_TILE=0).run(c.split, c.s0())
-    assert np.array_equal(a.s_final, b.s_final) and np.array_equal(a.u_final, b.u_final)
-    assert [s["dt"] for s in a.record.steps] == [s["dt"] for s in b.record.steps]
+UPWIND_VARIANTS = {
+    "col": dict(MPM2P_UPWIND_COL=1),
+    "col_rb1": dict(MPM2P_UPWIND_COL=1, MPM2P_UPWIND_RB=1),
+    "col_rb4": dict(MPM2P_UPWIND_COL=1, MPM2P_UPWIND_RB=4),
+    "tile": dict(MPM2P_UPWIND_COL=0, MPM2P_UPWIND_TILE=1),
+    "cell": dict(MPM2P_UPWIND_COL=0, MPM2P_UPWIND_TILE=0),
+}
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3"])
+def test_upwind_variants_bitwise(name):
+    """Column-marching, tiled and one-thread-per-cell upwind steps give
+    bit-identical saturation, dt sequence and clamp counts over a run."""
+    c = configs.build(name, te_override=31)
+    runs = {k: _sim_env(c.problem, **env).run(c.split, c.s0(), c.inflow_sat) for k, env in UPWIND_VARIANTS.items()}
+    a = runs["col"]
+    for k in ("col_rb1", "col_rb4", "tile", "cell"):
+        b = runs[k]
+        assert np.array_equal(a.s_final, b.s_final) and np.array_equal(a.u_final, b.u_final), k
+        assert [s["dt"] for s in a.record.steps] == [s["dt"] for s in b.record.steps], k
+        assert a.record.clamp_count == b.record.clamp_count, k
+
+
+@pytest.mark.parametrize("variant", sorted(UPWIND_VARIANTS))
+@pytest.mark.parametrize("nx,ny,sx,sy", [(31, 7, 1, 1), (62, 45, 2, 3), (93, 130, 3, 5), (300, 20, 10, 1),
+                                         (256, 256, 16, 16)])
+def test_upwind_step_ragged_bitwise(oracle, variant, nx, ny, sx, sy):
+    """upwind_step on widths that are not multiples of a warp's 30 columns or a
+    tile, heights that end mid row-chunk, and a velocity field with both signs
+    on every face family, bit-identical to the oracle (transport.cpp:73-120)."""
+    rng = np.random.default_rng(nx * 1000 + ny)
+    prob = problem(nx, ny, sx, sy, np.ones(nx * ny), M=3.0)
+    g = _sim_env(prob, **UPWIND_VARIANTS[variant])
+    o = api.Simulator(prob, oracle)
+    u = rng.standard_normal(g.faces)
+    s = rng.uniform(0.05, 0.95, nx * ny)
+    dt = 0.02 * o.cfl_timestep(u, 0.9, 1.0)  # random u is not divergence-free: keep s inside [0, 1]
+    for inflow in (1.0, 0.25):
+        assert np.array_equal(g.upwind_step(s, inflow, u, dt), o.upwind_step(s, inflow, u, dt))
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3"])
+def test_kappa_col_bitwise(name):
+    """Row-marching k_kappa_col vs one thread per cell: kappa and the fused
+    transmissibilities are bit-identical, so whole runs are (the drift sums
+    only change their partition into double-double partials)."""
+    c = configs.build(name, te_override=31)
+    a = _sim_env(c.problem, MPM2P_KAPPA_COL=1).run(c.split, c.s0(), c.inflow_sat)
+    b = _sim_env(c.problem, MPM2P_KAPPA_COL=0).run(c.split, c.s0(), c.inflow_sat)
+    assert [s["rebuilt"] for s in a.record.steps] == [s["rebuilt"] for s in b.record.steps]
+    assert a.record.counters == b.record.counters and a.record.clamp_count == b.record.clamp_count
+    for x, y in ((a.s_final, b.s_final), (a.p_final, b.p_final), (a.u_final, b.u_final)):
+        assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("nx,ny,sx,sy", [(31, 7, 1, 1), (62, 45, 2, 3), (93, 130, 3, 5)])
+def test_conductivity_col_ragged_bitwise(oracle, nx, ny, sx, sy):
+    """conductivity through k_kappa_col on ragged sizes, bit-identical to the oracle."""
+    rng = np.random.default_rng(nx + ny)
+    K = np.exp(rng.standard_normal(nx * ny))
+    prob = problem(nx, ny, sx, sy, K, M=4.0)
+    g = _sim_env(prob, MPM2P_KAPPA_COL=1)
+    o = api.Simulator(prob, oracle)
+    s = rng.uniform(0.0, 1.0, nx * ny)
+    assert np.array_equal(g.conductivity(s), o.conductivity(s))
 
 
 def test_blocktri_persistent_sweeps_match():
