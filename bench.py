@@ -257,9 +257,18 @@ def _e2e(api, lib, cfg, split, args, reps=3):
     (uploads K, q, the boundary spec; static operators) + mpm2p_run (s0 upload,
     every Algorithm-1 step with its scalar readback, final s/p/u download).
     Teardown is outside the timed region (cudaFree timing is noisy). Median of
-    `reps` runs; all samples are reported."""
+    `reps` runs after one untimed run; all samples are reported."""
     walls = []
     res = None
+    # one untimed simulation first: process-level one-time costs (module
+    # loading, allocator pools) are not per-simulation work; short runs
+    # (< 1 s) take the median of five
+    t0 = time.perf_counter()
+    sim = api.Simulator(cfg.problem, lib)
+    sim.run(split, cfg.s0(), cfg.inflow_sat)
+    sim.close()
+    if time.perf_counter() - t0 < 1.0:
+        reps = max(reps, 5)
     for _ in range(reps):
         t0 = time.perf_counter()
         sim = api.Simulator(cfg.problem, lib)
