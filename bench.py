@@ -155,9 +155,12 @@ def run_ours(args, ws, rank, local, dist, torch):
     cfg = configs.build(args.config)
     te_needed = args.warmup + args.steps + 1
     split = cfg.split
+    e2e_split = cfg.split
     if cfg.two_pass or (split.te and split.te < te_needed):
         import dataclasses
-        split = dataclasses.replace(split, te=max(te_needed, split.te or 0), stop_on_breakthrough=False)
+        e2e_split = dataclasses.replace(split, te=max(te_needed, split.te or 0), stop_on_breakthrough=False)
+        # room for the profiled window after the timed steps
+        split = dataclasses.replace(e2e_split, te=max(te_needed + args.profile_steps, split.te or 0))
     sim = api.Simulator(cfg.problem, lib)
     sz = sim.sizes
     dim = sim.dim
@@ -203,7 +206,7 @@ def run_ours(args, ws, rank, local, dist, torch):
     # end-to-end: a whole simulation through the C ABI with host buffers
     e2e = None
     if not args.skip_e2e:
-        e2e = _e2e(api, lib, cfg, split if cfg.two_pass else cfg.split, args)
+        e2e = _e2e(api, lib, cfg, e2e_split if cfg.two_pass else cfg.split, args)
     return dict(cfg=cfg, split=split, sz=sz, dim=dim, cn=cn, done=done, done_total=done_total,
                 dev_ms=dev_ms, dev_ms_max=dev_ms_max, wall=wall, rebuilds=rebuilds, clocks=clocks,
                 launches=launches, prof=prof, e2e=e2e)
