@@ -5,18 +5,24 @@ A "step" is one Algorithm-1 iteration of the reference driver
 (proj/src/simulation.cpp:262-329): CFL reduction, `cn` explicit upwind
 saturation substeps, conductivity + drift test, and one velocity update
 (MPM-2P reuse, or a full MRCM rebuild when the device-side drift test says
-so). The workload is BASELINE.json configs[1] (C2: 256x256 cells, 16x16
-subdomains of 16x16, exponential-covariance lognormal field) unless
---config says otherwise; inputs are seeded synthetic fields (no dataset).
+so). The headline workload is C5, the largest single-GPU config of
+BASELINE.json (4096^2 cells, 128x128 subdomains of 32x32, interface dim
+65,024); C2 (configs[1]) is measured in the same run as a second workload
+under "also". Inputs are seeded synthetic fields (no dataset).
 
-  value    velocity updates/s over the timed steps, inputs resident in HBM,
-           device time from CUDA events on the library's stream (L2 flushed
-           between steps: the C2 working set is smaller than L2)
-  e2e      the same metric for a whole simulation through the C ABI with host
-           buffers (context creation + mpm2p_run incl. all H2D/D2H copies)
+  value    velocity updates/s over the timed steps, inputs resident in HBM;
+           device time of each step's CUDA-graph replay from CUDA events on
+           the library's stream (timer slots 14/15 around cudaGraphLaunch, so
+           host-side driver work and first-use graph capture are excluded),
+           L2 flushed before every step; split by branch (MPM-2P / MRCM)
+  e2e      the same metric for whole simulations through the C ABI with host
+           buffers (context creation + mpm2p_run incl. all H2D/D2H copies;
+           C3: both passes, to breakthrough and to breakthrough + 50 %)
   cpu_baseline / --impl reference
            the CPU restatement of the reference (oracle/, C++ -O3, 1 thread:
            the reference has no threads) on a bounded sample of the same run
+           (C5: the banded interface LU — the reference's dense LU would need
+           34 GB); CPU model and nproc recorded
 
 Multi-GPU (torchrun): N independent replicas, one per GPU, no data-path
 collective (the sharded path is future work); value is the
@@ -147,20 +153,22 @@ def kernel_work(name, cfg, sz, dim):
     return table.get(name)
 
 
-def run_ours(args, ws, rank, local, dist, torch):
+def run_ours(args, ws, rank, local, dist, torch, config=None, steps=None):
+    import ctypes
+    import dataclasses
+    os.environ["MPM2P_GRAPH_TIMING"] = "1"  # replay-only device timing (read at context creation)
     from paper_2103_11050_b200 import api, configs
     lib = api.product_lib()
     if ws > 1:
         lib.set_device(local)
-    cfg = configs.build(args.config)
-    te_needed = args.warmup + args.steps + 1
+    cfg = configs.build(config or args.config)
+    n_steps = steps if steps is not None else args.steps
+    te_needed = args.warmup + n_steps + 1
     split = cfg.split
-    e2e_split = cfg.split
-    if cfg.two_pass or (split.te and split.te < te_needed):
-        import dataclasses
-        e2e_split = dataclasses.replace(split, te=max(te_needed, split.te or 0), stop_on_breakthrough=False)
-        # room for the profiled window after the timed steps
-        split = dataclasses.replace(e2e_split, te=max(te_needed + args.profile_steps, split.te or 0))
+    if cfg.two_pass or (split.te and split.te < te_needed + args.profile_steps):
+        # room for the timed and the profiled window (the e2e run keeps the config's own schedule)
+        split = dataclasses.replace(split, te=max(te_needed + args.profile_steps, split.te or 0),
+                                    stop_on_breakthrough=False)
     sim = api.Simulator(cfg.problem, lib)
     sz = sim.sizes
     dim = sim.dim
@@ -175,23 +183,25 @@ def run_ours(args, ws, rank, local, dist, torch):
         torch.cuda.synchronize()
     sampler.start()
     dev_ms = 0.0
+    span_ms = 0.0
     done = 0
-    rebuilds = 0
+    branch = {0: [], 1: []}
     launches0 = _launches(sim)
     t_wall0 = time.perf_counter()
-    for _ in range(args.steps):
+    ms = ctypes.c_double()
+    for _ in range(n_steps):
         lib.flush_l2(sim.h)
         lib.timer_record(sim.h, 0)
         rec = sim.run_step()
         lib.timer_record(sim.h, 1)
         if rec is None:
             break
-        import ctypes
-        ms = ctypes.c_double()
-        lib.timer_elapsed(sim.h, 0, 1, ctypes.byref(ms))
+        lib.timer_elapsed(sim.h, 14, 15, ctypes.byref(ms))  # the graph replay alone
         dev_ms += ms.value
+        branch[rec["rebuilt"]].append(ms.value)
+        lib.timer_elapsed(sim.h, 0, 1, ctypes.byref(ms))    # stream span incl. host-side driver work
+        span_ms += ms.value
         done += 1
-        rebuilds += rec["rebuilt"]
     wall = time.perf_counter() - t_wall0
     launches = _launches(sim) - launches0
     clocks = sampler.stop()
@@ -203,13 +213,19 @@ def run_ours(args, ws, rank, local, dist, torch):
     prof = _profile(sim, lib, min(args.profile_steps, max(0, split.te - 1 - args.warmup - done)))
     sim.run_end()
     sim.close()
-    # end-to-end: a whole simulation through the C ABI with host buffers
+    # end-to-end: whole simulations through the C ABI with host buffers
     e2e = None
     if not args.skip_e2e:
-        e2e = _e2e(api, lib, cfg, e2e_split if cfg.two_pass else cfg.split, args)
+        e2e = _e2e(api, lib, cfg, args)
+    split_out = {}
+    for b, nm in ((0, "mpm2p"), (1, "mrcm_rebuild")):
+        v = branch[b]
+        if v:
+            split_out[nm] = {"steps": len(v), "ms_per_step": sum(v) / len(v),
+                             "updates_per_s": len(v) / (sum(v) / 1e3)}
     return dict(cfg=cfg, split=split, sz=sz, dim=dim, cn=cn, done=done, done_total=done_total,
-                dev_ms=dev_ms, dev_ms_max=dev_ms_max, wall=wall, rebuilds=rebuilds, clocks=clocks,
-                launches=launches, prof=prof, e2e=e2e)
+                dev_ms=dev_ms, dev_ms_max=dev_ms_max, span_ms=span_ms, wall=wall, rebuilds=len(branch[1]),
+                clocks=clocks, launches=launches, prof=prof, e2e=e2e, branch_split=split_out)
 
 
 def reduce_over_ranks(dev_ms, done, dist, device):
@@ -255,76 +271,119 @@ def _profile(sim, lib, steps):
     return out
 
 
-def _e2e(api, lib, cfg, split, args, reps=3):
+def _simulate(api, lib, cfg):
+    """One whole simulation through the C ABI: create + run (+ C3's second pass)."""
+    import dataclasses
+    sim = api.Simulator(cfg.problem, lib)
+    try:
+        res = sim.run(cfg.split, cfg.s0(), cfg.inflow_sat)
+        steps, rebuilds = res.record.te - 1, res.record.tm_total
+        if cfg.two_pass:  # "until breakthrough + 50 %": second pass with te from the first
+            from paper_2103_11050_b200 import configs
+            b = res.record.breakthrough_step
+            if b < 0:
+                raise RuntimeError(f"{cfg.name}: no breakthrough in pass 1")
+            sp2 = dataclasses.replace(cfg.split, stop_on_breakthrough=False, te=configs.breakthrough_plus_50(b))
+            res2 = sim.run(sp2, cfg.s0(), cfg.inflow_sat)
+            steps += res2.record.te - 1
+            rebuilds += res2.record.tm_total
+        return steps, rebuilds
+    finally:
+        sim.close()
+
+
+def _e2e(api, lib, cfg, args, reps=3):
     """Whole simulations through the C ABI with host buffers: context creation
     (uploads K, q, the boundary spec; static operators) + mpm2p_run (s0 upload,
     every Algorithm-1 step with its scalar readback, final s/p/u download).
     Teardown is outside the timed region (cudaFree timing is noisy). Median of
     `reps` runs after one untimed run; all samples are reported."""
     walls = []
-    res = None
     # one untimed simulation first: process-level one-time costs (module
     # loading, allocator pools) are not per-simulation work; short runs
     # (< 1 s) take the median of five
     t0 = time.perf_counter()
-    sim = api.Simulator(cfg.problem, lib)
-    sim.run(split, cfg.s0(), cfg.inflow_sat)
-    sim.close()
+    _simulate(api, lib, cfg)
     if time.perf_counter() - t0 < 1.0:
         reps = max(reps, 5)
     for _ in range(reps):
         t0 = time.perf_counter()
-        sim = api.Simulator(cfg.problem, lib)
-        res = sim.run(split, cfg.s0(), cfg.inflow_sat)
+        steps, rebuilds = _simulate(api, lib, cfg)
         walls.append(time.perf_counter() - t0)
-        sim.close()
     wall = sorted(walls)[len(walls) // 2]
-    steps = res.record.te - 1
     cells = cfg.cells
     faces = (cfg.problem.nx + 1) * cfg.problem.ny + cfg.problem.nx * (cfg.problem.ny + 1)
     nb = 2 * (cfg.problem.nx + cfg.problem.ny)
-    h2d = 8 * cells * 2 + 12 * nb  # K + s0 + boundary spec
-    d2h = 8 * (2 * cells + faces) + 256 * (steps + 1)  # final s, p, u + per-step scalars
+    passes = 2 if cfg.two_pass else 1
+    h2d = passes * (8 * cells * 2 + 12 * nb)  # K + s0 + boundary spec
+    d2h = passes * 8 * (2 * cells + faces) + 256 * (steps + passes)  # final s, p, u + per-step scalars
     return {"value": steps / wall, "unit": "velocity_updates/s", "h2d_bytes_per_step": h2d / max(steps, 1),
             "d2h_bytes_per_step": d2h / max(steps, 1), "wall_s_per_simulation": wall, "steps": steps,
-            "rebuilds": res.record.tm_total, "wall_samples_s": [round(w, 4) for w in walls]}
+            "rebuilds": rebuilds, "passes": passes, "wall_samples_s": [round(w, 4) for w in walls]}
+
+
+def cpu_info():
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"model": model, "nproc": os.cpu_count()}
 
 
 def cpu_reference(cfg, split, budget_s):
     """The reference's CPU path (oracle restatement, C++ -O3, 1 thread) on a
-    bounded sample: as many steps of the same run as fit in budget_s."""
+    bounded sample: the initial MRCM solve (reported, not in the rate), then as
+    many Algorithm-1 steps of the same run as fit in budget_s."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from oracle_bind import oracle_lib
     from paper_2103_11050_b200 import api
     lib = oracle_lib()
+    lib.dll.oracle_set_threads(1)  # the reference is single-threaded
     sim = api.Simulator(cfg.problem, lib)
     t0 = time.perf_counter()
     sim.run_begin(split, cfg.s0(), cfg.inflow_sat)
     t_begin = time.perf_counter() - t0
     n = 0
+    br = {0: [], 1: []}
     t1 = time.perf_counter()
     while time.perf_counter() - t1 < budget_s:
-        if sim.run_step() is None:
+        ts = time.perf_counter()
+        r = sim.run_step()
+        if r is None:
             break
+        br[r["rebuilt"]].append(time.perf_counter() - ts)
         n += 1
     el = time.perf_counter() - t1
-    rec = sim.run_end()
+    sim.run_end()
     sim.close()
+    iface = "banded partial-pivot LU of the interface matrix (dense LU: 34 GB)" if cfg.name == "C5" else \
+        "dense partial-pivot LU of the interface matrix, as the reference"
     return {"value": n / el if el > 0 else 0.0, "unit": "velocity_updates/s", "cores": 1, "kind": "port",
-            "sample": f"{cfg.name}: initial rebuild ({t_begin:.2f} s) then the first {n} Algorithm-1 steps "
-                      f"({el:.1f} s, {rec.tm_total - 1} rebuilds) of the same run; oracle/ C++ -O3 single thread "
-                      f"(the reference is single-threaded and cannot be built here: no Eigen)",
-            "steps": n, "seconds": el}
+            "sample": f"{cfg.name}: initial MRCM solve ({t_begin:.2f} s, not in the rate) then the first {n} "
+                      f"Algorithm-1 steps ({el:.1f} s, {len(br[1])} rebuilds) of the same run; oracle/ C++ -O3 "
+                      f"single thread (the reference is single-threaded and cannot be built here: no Eigen); "
+                      f"{iface}",
+            "branch_s_per_step": {"mpm2p": (sum(br[0]) / len(br[0])) if br[0] else None,
+                                  "mrcm_rebuild": (sum(br[1]) / len(br[1])) if br[1] else None},
+            "initial_solve_s": t_begin, "cpu": cpu_info(), "steps": n, "seconds": el}
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--also", default="C2", help="further workloads measured in the same run (N=1 only)")
+    ap.add_argument("--also-steps", type=int, default=300)
+    ap.add_argument("--also-cpu-budget", type=float, default=10.0)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--profile-steps", type=int, default=50)
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
@@ -352,10 +411,27 @@ def main():
         return
 
     r = run_ours(args, ws, rank, local, dist, torch)
+    also = {}
+    if args.also and ws == 1:
+        for name in [x for x in args.also.split(",") if x and x.upper() != r["cfg"].name]:
+            ra = run_ours(args, ws, rank, local, dist, torch, config=name, steps=args.also_steps)
+            la = build_line(ra, args, ws, cpu_budget=args.also_cpu_budget)
+            also[ra["cfg"].name] = {k: la[k] for k in ("value", "unit", "ms_per_step", "steps", "cell_updates_per_s",
+                                                       "branch_split", "roofline", "e2e", "cpu_baseline",
+                                                       "gpu_launches", "config", "clocks")}
     if rank != 0:
         if dist is not None:
             dist.barrier()
         return
+    line = build_line(r, args, ws, cpu_budget=args.cpu_budget)
+    if also:
+        line["also"] = also
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+
+
+def build_line(r, args, ws, cpu_budget):
     cfg, sz, dim = r["cfg"], r["sz"], r["dim"]
     secs = r["dev_ms_max"] / 1e3
     value = r["done_total"] / secs
@@ -401,33 +477,44 @@ def main():
                     "algorithmic_per_launch": w[1], "avg_launch_us": avg_s * 1e6}
         break
     if roof is not None:  # dram bytes per launch from the committed ncu --set full capture
+        tpath = None
+        for rnd in ("r02", "r01"):  # the latest round's capture
+            cand = os.path.join(ROOT, "profiles", f"ncu_traffic_{rnd}_{cfg.name}.json")
+            if os.path.exists(cand):
+                tpath = cand
+                break
         try:
-            with open(os.path.join(ROOT, "profiles", f"ncu_traffic_r01_{cfg.name}.json")) as f:
+            with open(tpath or "") as f:
                 tr = {k.split("::")[-1]: v for k, v in json.load(f).items()}
             # keys carry template arguments (k_ds_solve_r<16>): match the launcher name as a prefix
             hit = [v for k, v in tr.items() if k == roof["kernel"] or k.startswith(roof["kernel"] + "_r<")
                    or k.startswith(roof["kernel"] + "_t<") or k.startswith(roof["kernel"] + "<")
                    or k.startswith(roof["kernel"] + "_tile")]
             roof["traffic"] = hit[0] if hit else None
-            roof["traffic_source"] = f"profiles/ncu_traffic_r01_{cfg.name}.json (dram__bytes_read+write per launch)"
+            roof["traffic_source"] = f"{os.path.relpath(tpath, ROOT)} (ncu dram__bytes_read+write per launch)"
         except (OSError, ValueError):
             pass
     cpu = None
-    if not args.skip_cpu and ws == 1:
+    if not args.skip_cpu and ws == 1 and cpu_budget > 0:
         import dataclasses
         cpu_split = dataclasses.replace(r["split"], stop_on_breakthrough=False)
-        cb = cpu_reference(cfg, cpu_split, args.cpu_budget)
-        cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
-    line = {
+        cb = cpu_reference(cfg, cpu_split, cpu_budget)
+        cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "branch_s_per_step",
+                                  "initial_solve_s", "cpu")}
+    return {
         "metric": METRIC, "value": value, "unit": "velocity_updates/s", "n_gpus": ws, "steps": r["done"],
         "warmup": args.warmup, "ms_per_step": r["dev_ms_max"] / max(r["done"], 1), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded field generator)",
         "config": {"workload": cfg.name, "description": cfg.description, "cells": cells,
                    "subdomains": sz.n_sub, "interface_dim": dim, "cn": r["cn"],
-                   "l2": "flushed between timed steps (working set < L2)",
+                   "l2": "flushed before every timed step",
+                   "timing": "CUDA events around each step's graph replay (host driver work excluded; "
+                             "stream_ms_per_step includes it)",
                    "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU"},
         "cell_updates_per_s": cell_updates,
+        "branch_split": r["branch_split"],
         "rebuilds_in_timed_steps": r["rebuilds"],
+        "stream_ms_per_step": r["span_ms"] / max(r["done"], 1),
         "host_wall_ms_per_step": 1e3 * r["wall"] / max(r["done"], 1),
         "gpu_launches": r["launches"],
         "roofline": roof,
@@ -436,9 +523,6 @@ def main():
         "e2e": r["e2e"],
         "cpu_baseline": cpu,
     }
-    print(json.dumps(line), flush=True)
-    if dist is not None:
-        dist.barrier()
 
 
 if __name__ == "__main__":

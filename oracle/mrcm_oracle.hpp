@@ -35,14 +35,22 @@ struct ConfigError : std::runtime_error { using std::runtime_error::runtime_erro
 struct NumericError : std::runtime_error { using std::runtime_error::runtime_error; };
 struct CapacityError : std::runtime_error { using std::runtime_error::runtime_error; };
 
-using Vec = std::vector<double>;
+// Scalar type of the restatement: double (the reference's), or long double
+// in the extended-precision build (liboracle_ld.so, -DORACLE_LONG_DOUBLE) used
+// only to measure how far double-precision answers sit from the exact one.
+#ifdef ORACLE_LONG_DOUBLE
+using Real = long double;
+#else
+using Real = double;
+#endif
+using Vec = std::vector<Real>;
 
 // grid.hpp:14-43
 struct Grid {
     int nx = 0, ny = 0;
-    double lx = 0, ly = 0, hx = 0, hy = 0;
+    Real lx = 0, ly = 0, hx = 0, hy = 0;
     Grid() = default;
-    Grid(int nx_, int ny_, double lx_, double ly_)
+    Grid(int nx_, int ny_, Real lx_, Real ly_)
         : nx(nx_), ny(ny_), lx(lx_), ly(ly_), hx(lx_ / nx_), hy(ly_ / ny_) {}
     int cells() const { return nx * ny; }
     int vcount() const { return (nx + 1) * ny; }
@@ -52,23 +60,23 @@ struct Grid {
     int vface(int i, int j) const { return j * (nx + 1) + i; }
     int hface(int i, int j) const { return vcount() + j * nx + i; }
     bool is_vface(int f) const { return f < vcount(); }
-    double cx(int i) const { return (i + 0.5) * hx; }
-    double cy(int j) const { return (j + 0.5) * hy; }
-    double vol() const { return hx * hy; }
-    double area(int f) const { return is_vface(f) ? hy : hx; }
+    Real cx(int i) const { return (i + 0.5) * hx; }
+    Real cy(int j) const { return (j + 0.5) * hy; }
+    Real vol() const { return hx * hy; }
+    Real area(int f) const { return is_vface(f) ? hy : hx; }
     bool same_shape(const Grid& o) const { return nx == o.nx && ny == o.ny && lx == o.lx && ly == o.ly; }
 };
-Grid build_grid(int nx, int ny, double lx, double ly);       // grid.cpp:9-15
+Grid build_grid(int nx, int ny, Real lx, Real ly);       // grid.cpp:9-15
 Vec divergence(const Grid& g, const Vec& u);                  // grid.cpp:19-31
 
 // decomposition.hpp:11-70
 enum Side { West = 0, East = 1, South = 2, North = 3 };
-inline double side_sign(int s) { return (s == East || s == North) ? 1.0 : -1.0; }
+inline Real side_sign(int s) { return (s == East || s == North) ? 1.0 : -1.0; }
 struct Rect { int i0, j0, nx, ny; };
 struct Interface { int minus = -1, plus = -1; bool vertical = true; std::vector<int> faces; };
 struct BoundaryEdge {
     int global_face = -1, local_face = -1, local_cell = -1, side = 0;
-    double sign = 0.0;
+    Real sign = 0.0;
     bool on_skeleton = false;
     int iface = -1, pos = -1;
 };
@@ -82,14 +90,14 @@ struct Decomp {
     int n_sub() const { return nsx * nsy; }
     int n_iface() const { return (int)ifaces.size(); }
     int skeleton_edges() const;
-    double coarse_h() const;
+    Real coarse_h() const;
     Vec restrict_cells(const Vec& global, int s) const;
 };
 Decomp build_decomposition(const Grid& g, int nsx, int nsy);  // decomposition.cpp:21-132
 
 // elliptic.hpp:13-64
 enum BcKind { Pressure = 0, Flux = 1, Robin = 2 };
-struct FaceBc { int kind = Flux; double value = 0, beta = 0, robin_rhs = 0; };
+struct FaceBc { int kind = Flux; Real value = 0, beta = 0, robin_rhs = 0; };
 struct BoundarySpec {
     int nx = 0, ny = 0;
     std::vector<FaceBc> faces;
@@ -133,8 +141,8 @@ private:
 };
 LocalSolution solve_cell_centered(const Grid& g, const Vec& kappa, const Vec& q,
                                   const BoundarySpec& bc, int anchor = -1);
-double conservation_residual(const Grid& g, const LocalSolution& sol, const Vec& q);
-double residual_scale(const Grid& g, const LocalSolution& sol, const Vec& q);
+Real conservation_residual(const Grid& g, const LocalSolution& sol, const Vec& q);
+Real residual_scale(const Grid& g, const LocalSolution& sol, const Vec& q);
 
 // interface_space.hpp:11-48
 struct HbarSpec { int mode = 0; int edges = 0; };  // 0 whole, 1 half, 2 per-edge, 3 segment
@@ -151,11 +159,11 @@ Space build_interface_space(const Decomp& dd, int kind, HbarSpec hbar);
 // robin.hpp:15-38
 struct AlphaSpec {
     int mode = 0;  // 0 uniform, 1 adaptive
-    double alpha = 1.0, alpha_min = 1e-2, alpha_max = 1e2, pct_lo = 10.0, pct_hi = 90.0;
+    Real alpha = 1.0, alpha_min = 1e-2, alpha_max = 1e2, pct_lo = 10.0, pct_hi = 90.0;
 };
 struct RobinParameter {
     std::vector<Vec> beta_minus, beta_plus, alpha;
-    double beta(int k, int pos, bool minus) const { return minus ? beta_minus[k][pos] : beta_plus[k][pos]; }
+    Real beta(int k, int pos, bool minus) const { return minus ? beta_minus[k][pos] : beta_plus[k][pos]; }
 };
 RobinParameter compute_beta(const Vec& kappa, const Decomp& dd, const AlphaSpec& spec);
 
@@ -167,8 +175,35 @@ struct DenseLU {
     void compute(const Vec& M, int n);
     Vec solve(const Vec& b) const;
     Vec solve_transposed(const Vec& b) const;
-    double rcond(const Vec& M) const;  // Hager/Higham 1-norm estimate
+    Real rcond(const Vec& M) const;  // Hager/Higham 1-norm estimate
 };
+
+// Banded partial-pivot LU of a row- and column-permuted sparse matrix
+// (the LAPACK dgbtrf/dgbtrs algorithm, column-major band storage). The
+// interface matrix is solved with it above kDenseInterfaceMax unknowns, where
+// the reference's dense PartialPivLU (mrcm.cpp:198,226-238) would need a
+// dim^2 matrix (C5: 34 GB, 1.8e14 flop). With the unknowns ordered by the
+// interfaces' position in the subdomain grid (vertical interfaces of subdomain
+// row j, then the horizontal ones above it) M is banded (C5: bandwidth ~510).
+// Same mathematics as the dense LU: agreement at solver roundoff.
+struct BandLU {
+    int n = 0, kl = 0, ku = 0, ld = 0;
+    std::vector<int> prow, pcol;  // A'(i, j) = M(prow[i], pcol[j])
+    Vec AB;                       // A'(i, j) at AB[j * ld + kl + ku + i - j]
+    std::vector<int> ipiv;
+    bool singular = false;
+    void init(int n, std::vector<int> prow, std::vector<int> pcol, int kl, int ku);
+    Real& at(int i, int j) { return AB[(size_t)j * ld + kl + ku + i - j]; }
+    Real get(int i, int j) const { return AB[(size_t)j * ld + kl + ku + i - j]; }
+    void factor();
+    Vec solve(const Vec& b) const;             // M x = b (original ordering)
+    Vec solve_transposed(const Vec& b) const;  // M^T x = b
+    Real rcond(Real anorm) const;          // Hager/Higham 1-norm estimate
+};
+constexpr int kDenseInterfaceMax = 16384;
+void set_interface_solver(int mode);  // 0 auto (dense up to kDenseInterfaceMax), 1 dense, 2 banded
+int interface_solver_mode();
+void set_threads(int n);              // per-subdomain loops (default 1: the reference is single-threaded)
 
 // mrcm.hpp:15-153
 struct SolveCounters { long homogeneous = 0, particular = 0, downscale = 0, fine = 0, interface_solves = 0; };
@@ -182,8 +217,11 @@ struct BasisSet {
     RobinParameter beta;
     Vec kappa_m;
     std::vector<Sub> subs;
-    Vec M;  // dense interface matrix, row-major
+    Vec M;  // dense interface matrix, row-major (dense solver only)
     DenseLU lu;
+    bool banded = false;
+    BandLU blu;  // banded solver (large interface systems)
+    Vec dense_matrix() const;  // M, re-assembled when the banded solver holds it
     std::vector<LocalSolution> particular;
     int n_flux = 0, n_pres = 0;
     int dim() const { return n_flux + n_pres; }
@@ -204,9 +242,9 @@ std::vector<LocalSolution> reconstruct(const BasisSet& b, const SkeletonCoeffs& 
 std::vector<Vec> averaged_skeleton_flux(const Decomp& dd, const std::vector<LocalSolution>& recon);
 struct DownscaleResult {
     Vec p, u;
-    double repair_max = 0, flux_scale = 0;
+    Real repair_max = 0, flux_scale = 0;
     bool repair_warning = false;
-    double div_residual = 0, div_scale = 1;
+    Real div_residual = 0, div_scale = 1;
 };
 DownscaleResult downscale(const Decomp& dd, const Vec& kappa, const Vec& q, const BoundarySpec& bc,
                           const std::vector<LocalSolution>& recon, const std::vector<Vec>& skel,
@@ -220,16 +258,16 @@ struct GlobalSolution {
 GlobalSolution mrcm_solve(const Vec& kappa, std::shared_ptr<const Decomp> dd,
                           std::shared_ptr<const Space> space, const RobinParameter& beta,
                           const Vec& q, const BoundarySpec& bc, SolveCounters& c);
-struct WeakResiduals { double flux_jump = 0, pressure_jump = 0; };
+struct WeakResiduals { Real flux_jump = 0, pressure_jump = 0; };
 WeakResiduals weak_continuity_residuals(const BasisSet& b, const std::vector<LocalSolution>& recon);
 
 // mpm.hpp:15-55
 enum EpsMode { EpsRelative = 0, EpsAbsolute = 1, EpsMobility = 2 };
-double epsilon(const Grid& g, const Vec& kn, const Vec& km, int mode);
+Real epsilon(const Grid& g, const Vec& kn, const Vec& km, int mode);
 struct PerturbationState {
     std::shared_ptr<const BasisSet> basis;
     std::vector<LocalSolution> recon_m;
-    double eta = 0.01;
+    Real eta = 0.01;
     int mode = EpsRelative;
 };
 struct MpmResult { SkeletonCoeffs delta; std::vector<LocalSolution> recon_n; DownscaleResult ds; };
@@ -239,59 +277,59 @@ MpmResult mpm_pressure_update(const PerturbationState& st, const Vec& kappa_n, c
 // transport.hpp:11-50
 int64_t clamp_count();
 void reset_clamp_count();
-double total_mobility(double s, double M);
-double fractional_flow(double s, double M);
-double max_fractional_flow_slope(double M);
-double cfl_timestep(const Grid& g, const Vec& u, double M, double safety, double dt_cap);
-Vec upwind_step(const Grid& g, const Vec& s, double inflow, const Vec& u, double dt, double M);
-Vec conductivity(const Vec& K, const Vec& s, double M);
+Real total_mobility(Real s, Real M);
+Real fractional_flow(Real s, Real M);
+Real max_fractional_flow_slope(Real M);
+Real cfl_timestep(const Grid& g, const Vec& u, Real M, Real safety, Real dt_cap);
+Vec upwind_step(const Grid& g, const Vec& s, Real inflow, const Vec& u, Real dt, Real M);
+Vec conductivity(const Vec& K, const Vec& s, Real M);
 
 // simulation.hpp:13-128
 enum Method { FineReference = 0, MrcmEveryStep = 1, Mpm2p = 2, Mpm2pNoUpdates = 3 };
 struct Split {
     int method = Mpm2p, cn = 1;
-    double eta = 0.01;
+    Real eta = 0.01;
     int eta_mode = EpsRelative;
-    double cfl_safety = 0.9, dt_cap = 1.0;
+    Real cfl_safety = 0.9, dt_cap = 1.0;
     long te = 0;
-    double pvi_max = 0.0;
+    Real pvi_max = 0.0;
     bool stop_on_breakthrough = false;
     long max_steps_hard = 50000;
-    double breakthrough_threshold = 0.05;
+    Real breakthrough_threshold = 0.05;
     bool track_errors = true;
 };
 struct StepRecord {
-    long step = 0; double pvi = 0, epsilon = 0; int rebuilt = 0;
-    double flux_err = 0, sat_err = 0; long bf_homog_cum = 0, bf_part_cum = 0;
-    double dt = 0, wall_s = 0, div_residual = 0;
+    long step = 0; Real pvi = 0, epsilon = 0; int rebuilt = 0;
+    Real flux_err = 0, sat_err = 0; long bf_homog_cum = 0, bf_part_cum = 0;
+    Real dt = 0, wall_s = 0, div_residual = 0;
 };
 struct RunRecord {
     std::vector<StepRecord> steps;
     std::vector<long> update_steps;
-    long breakthrough_step = -1; double breakthrough_pvi = -1.0;
+    long breakthrough_step = -1; Real breakthrough_pvi = -1.0;
     long te = 0, tm_updates = 0, tm_total = 0, nhat = 0; int n_sub = 0;
     SolveCounters counters;
-    double max_div_residual = 0, max_div_ratio = 0; int repair_warnings = 0;
-    double final_pvi = 0;
-    double min_eps_margin = INFINITY;
+    Real max_div_residual = 0, max_div_ratio = 0; int repair_warnings = 0;
+    Real final_pvi = 0;
+    Real min_eps_margin = INFINITY;
 };
 struct RunInputs {
     std::shared_ptr<const Decomp> dd;
     Vec K, q;
-    double M = 1.0;
+    Real M = 1.0;
     BoundarySpec bc;
     std::shared_ptr<const Space> space;
     AlphaSpec alpha;
     Split split;
     Vec s0;
-    double inflow_sat = 1.0;
+    Real inflow_sat = 1.0;
 };
 struct RunResult { RunRecord rec; Vec s_final, p_final, u_final; };
-double rcr(long nhat, long n, long te, long tm);
-double relative_flux_error(const Grid& g, const Vec& u, const Vec& u_ref);
-double relative_sat_error(const Vec& s, const Vec& s_ref);
-double max_outlet_saturation(const Grid& g, const Vec& s, const Vec& u);
-double injection_rate(const Grid& g, const Vec& u, double inflow, double M);
+Real rcr(long nhat, long n, long te, long tm);
+Real relative_flux_error(const Grid& g, const Vec& u, const Vec& u_ref);
+Real relative_sat_error(const Vec& s, const Vec& s_ref);
+Real max_outlet_saturation(const Grid& g, const Vec& s, const Vec& u);
+Real injection_rate(const Grid& g, const Vec& u, Real inflow, Real M);
 
 // The Algorithm-1 driver, split into begin/step for the step-wise ABI.
 class Runner {
@@ -309,9 +347,9 @@ private:
     void rebuild(const Vec& kappa);
     void reuse(const Vec& kappa);
     LocalSolution fine_solve(const Vec& kappa);
-    double drift(const Vec& kappa_n);
-    void note(double dres, double dscale, bool warn);
-    void record_step(int rebuilt, double eps, double dt, double wall);
+    Real drift(const Vec& kappa_n);
+    void note(Real dres, Real dscale, bool warn);
+    void record_step(int rebuilt, Real eps, Real dt, Real wall);
     void breakthrough_check();
     RunInputs in_;
     RunRecord rec_;
@@ -320,14 +358,14 @@ private:
     PerturbationState state_;
     std::unique_ptr<LocalSolver> fine_;
     int fine_anchor_ = -1;
-    double pvi_ = 0, eps_ = 0, step_div_ = 0;
+    Real pvi_ = 0, eps_ = 0, step_div_ = 0;
     long n_ = 0, ell_ = 0;
 };
 RunResult run(const RunInputs& in);
 
 // fields_io.cpp:25-116 (test-only restatement, used to pin the slab study)
-Vec gaussian_field(const Grid& g, double delta, double mean_coeff, uint64_t seed, bool range_norm,
-                   double range_target);
+Vec gaussian_field(const Grid& g, Real delta, Real mean_coeff, uint64_t seed, bool range_norm,
+                   Real range_target);
 Vec load_cell_field(const std::string& path, const Grid& g);
 void save_cell_field(const std::string& path, const Grid& g, const Vec& f);
 

@@ -52,7 +52,8 @@ int guarded(oracle_ctx* ctx, F&& fn) {
 }
 
 void copy_out(double* dst, const Vec& v) {
-    if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(double));
+    if (dst)
+        for (size_t i = 0; i < v.size(); ++i) dst[i] = (double)v[i];
 }
 
 Vec flatten(const std::vector<Vec>& vv) {
@@ -330,7 +331,7 @@ int oracle_mpm_update(oracle_ctx* ctx, const double* kappa_n, double* p, double*
 int oracle_interface_matrix(oracle_ctx* ctx, double* M) {
     return guarded(ctx, [&] {
         if (!ctx->state.basis) throw ConfigError("interface_matrix: no basis installed");
-        copy_out(M, ctx->state.basis->M);
+        copy_out(M, ctx->state.basis->dense_matrix());
     });
 }
 
@@ -442,6 +443,10 @@ int64_t oracle_clamp_count(void) { return clamp_count(); }
 /* 0: natural elimination order (default), 1: reversed — an equally exact
  * direct solve with different rounding, used to measure solver-noise floors. */
 void oracle_set_elimination_order(int32_t order) { set_elimination_order(order); }
+// 0 auto (dense LU up to 16,384 unknowns, banded LU above), 1 dense, 2 banded
+void oracle_set_interface_solver(int32_t mode) { set_interface_solver(mode); }
+// threads for the per-subdomain loops (default 1, the reference's single thread)
+void oracle_set_threads(int32_t n) { set_threads(n); }
 
 /* Decomposition tables built the reference's way (decomposition.cpp:35-132,
  * mrcm.cpp:157-189), same layout as mpm2p_layout_tables. */

@@ -26,7 +26,10 @@ __device__ __forceinline__ double clamp_s(double s, long long* cnt) {  // transp
 __device__ __forceinline__ double frac_flow(double s, double M, long long* cnt) {  // transport.cpp:39-43
     s = clamp_s(s, cnt);
     const double w = M * s * s;
-    return w / (w + (1.0 - s) * (1.0 - s));
+    // w == +0 (s == 0 ahead of the flood front, the bulk of C5's cells) gives
+    // +0 / 1 == +0 exactly; returning it directly keeps every bit and skips the
+    // IEEE division, whose zero-dividend operand takes its slow-path subroutine
+    return w == 0.0 ? 0.0 : w / (w + (1.0 - s) * (1.0 - s));
 }
 __device__ __forceinline__ double total_mob(double s, double M, long long* cnt) {  // transport.cpp:34-37
     s = clamp_s(s, cnt);
