@@ -140,6 +140,9 @@ def kernel_work(name, cfg, sz, dim):
         "k_kappa": ("hbm", 48.0 * cells),
         "k_part_solve": ("hbm", ns * n * (16.0 * B + 24.0)),     # Lcol, Lrow, D, x r/w
         "k_ds_solve": ("fp64", ns * (n * B * B + 4.0 * n * B)),  # banded LDL^T factor + 2 sweeps
+        # blocked DMMA downscale (band_blk.cuh): factor + forward sweep; backward sweep from the stored panels
+        "k_ds_blk_factor": ("fp64", ns * (n * B * B + 2.0 * n * B)),
+        "k_ds_blk_solve": ("hbm", ns * n * (8.0 * B + 8.0 + 16.0)),  # X panels + t1 read, x written, p written
         "k_ds_factor": ("fp64", ns * n * B * B),                # split downscale: factor (side stream)
         "k_ds_sweep": ("hbm", ns * n * (16.0 * B + 24.0)),       # split downscale: 2 sweeps with the stored factor
         "k_factor_solve": ("fp64", ns * (n * B * B + 4.0 * n * B * (1 + sz.nhat / max(ns, 1)))),

@@ -263,6 +263,7 @@ void create_ctx(mpm2p_ctx* ctx, const mpm2p_problem* P) {
     if (const char* e = std::getenv("MPM2P_NO_REGBAND")) c.no_regband = e[0] == '1';
     if (const char* e = std::getenv("MPM2P_GJ")) c.gj_legacy = std::strcmp(e, "legacy") == 0;
     if (const char* e = std::getenv("MPM2P_NO_TWIST")) c.no_twist = e[0] == '1';
+    if (const char* e = std::getenv("MPM2P_DS_BLK")) c.ds_blk = std::atoi(e);
     if (const char* e = std::getenv("MPM2P_PDL")) c.pdl = e[0] == '1';
     if (const char* e = std::getenv("MPM2P_BT_PDL")) c.bt_pdl = e[0] != '0';
     if (const char* e = std::getenv("MPM2P_BT_PERSIST")) c.bt_persistent = e[0] == '1';

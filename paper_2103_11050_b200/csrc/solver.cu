@@ -17,6 +17,7 @@
 
 #include "band.cuh"
 #include "band_reg.cuh"
+#include "band_blk.cuh"
 #include "band_twist.cuh"
 #include "context.cuh"
 
@@ -825,6 +826,46 @@ __global__ void __launch_bounds__(WPB * 32, 4) k_ds_solve_r(Layout L, const doub
     double v = 0.0;
     for (int r = lane; r < n; r += 32) v += x[r];
     v = warp_sum(v);
+    const double shift = (__shfl_sync(0xffffffffu, RS[s], 0) - __shfl_sync(0xffffffffu, v, 0)) / n;
+    for (int r = lane; r < n; r += 32) p[L.gcell_of(s, r)] = x[r] + shift;
+}
+
+// Downscale on the fp64 tensor cores (band_blk.cuh), two kernels: the
+// blocked LDL^T with DMMA Schur updates and the forward sweep (X panels in
+// Lr, t1 in D; register-heavy, latency-bound), then the backward sweep from
+// the stored panels with the mean shift (few registers, full occupancy,
+// bandwidth-bound on the panel stream).
+template <int B>
+__global__ void __launch_bounds__(WPB * 32, 3) k_ds_blk_factor(Layout L, const double* __restrict__ BD,
+                                                            const double* __restrict__ BW,
+                                                            const double* __restrict__ BS, double* T1, double* Xs,
+                                                            const double* Xd, Scalars* sc) {
+    pdl_begin();
+    __shared__ __align__(16) double sm[WPB][blk_smem_doubles<B>()];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int s = blockIdx.x * WPB + w;
+    if (s >= L.n_sub) return;
+    const int n = L.ncs;
+    const size_t so = (size_t)s * n;
+    const BandRows A{BD + so, BW + so, BS + so};
+    const bool ok = blk_factor_fwd<B>(n, A, Xd + so, Xs + so * B, T1 + so, sm[w]);
+    if (!ok && lane == 0) atomicOr(&sc->err, ERR_PIVOT);
+}
+
+template <int B>
+__global__ void __launch_bounds__(WPB * 32) k_ds_blk_solve(Layout L, const double* __restrict__ T1,
+                                                           const double* __restrict__ Xs, double* Xd,
+                                                           const double* __restrict__ RS, double* p) {
+    pdl_begin();
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int s = blockIdx.x * WPB + w;
+    if (s >= L.n_sub) return;
+    const int n = L.ncs;
+    const size_t so = (size_t)s * n;
+    double* x = Xd + so;
+    const double part = blk_backward<B>(n, Xs + so * B, T1 + so, x);
+    __syncwarp();
+    const double v = warp_sum(part);
     const double shift = (__shfl_sync(0xffffffffu, RS[s], 0) - __shfl_sync(0xffffffffu, v, 0)) / n;
     for (int r = lane; r < n; r += 32) p[L.gcell_of(s, r)] = x[r] + shift;
 }
@@ -1884,6 +1925,31 @@ void downscale(Ctx& c, const double* kappa) {
         done = true;                                                                                            \
         break;
             MPM2P_TWIST_WIDTHS(X)
+#undef X
+            default:
+                break;
+        }
+        if (done) CK_LAUNCH();
+    }
+    const bool blk = c.ds_blk == 1 || (c.ds_blk < 0 && (L.snx == 24 || L.snx == 32));
+    if (!done && blk && L.snx % 8 == 0 && L.snx >= 16 && L.snx <= 32) {
+        switch (L.snx) {
+#define X(BW_)                                                                                                     \
+    case BW_:                                                                                                      \
+        {                                                                                                          \
+            PROF(c, "k_ds_blk_factor");                                                                            \
+            launch_k(c, k_ds_blk_factor<BW_>, band_blocks(L), WPB * 32, 0, L, c.BDd, c.BWd, c.BSd, c.Dd, c.Lrd,  \
+                     (const double*)c.Xd, c.sc);                                                                  \
+        }                                                                                                          \
+        CK_LAUNCH();                                                                                               \
+        {                                                                                                          \
+            PROF(c, "k_ds_blk_solve");                                                                             \
+            launch_k(c, k_ds_blk_solve<BW_>, band_blocks(L), WPB * 32, 0, L, (const double*)c.Dd,                 \
+                     (const double*)c.Lrd, c.Xd, c.RS, c.p);                                                      \
+        }                                                                                                          \
+        done = true;                                                                                               \
+        break;
+            X(16) X(24) X(32)
 #undef X
             default:
                 break;

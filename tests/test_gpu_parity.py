@@ -527,3 +527,27 @@ def test_mpm_rhs_per_subdomain_bitwise():
     b = _sim_env(c.problem, MPM2P_RHS_SUB=0).run(c.split, c.s0())
     assert np.array_equal(a.s_final, b.s_final) and np.array_equal(a.u_final, b.u_final)
     assert np.array_equal(a.p_final, b.p_final)
+
+
+@pytest.mark.parametrize("nx,nsx", [(64, 4), (96, 4), (64, 2), (128, 4)])
+def test_blocked_dmma_downscale_parity(oracle, nx, nsx):
+    """The fused downscale on the fp64 tensor cores (band_blk.cuh: 8-pivot
+    panels, DMMA Schur updates; B = 16, 24, 32) vs the register-window
+    scalar LDL^T and vs the oracle's banded LDL^T (mrcm.cpp:388-427)."""
+    K = random_kappa(nx, nx, 4, 1e-2, 1e2)
+    prob = problem(nx, nx, nsx, nsx, K, M=5.0)
+    gb = _sim_env(prob, MPM2P_DS_BLK=1, MPM2P_DS_SPLIT=0, MPM2P_NO_TWIST=1)
+    gr = _sim_env(prob, MPM2P_DS_BLK=0, MPM2P_DS_SPLIT=0, MPM2P_NO_TWIST=1)
+    o = api.Simulator(prob, oracle)
+    a, b, r = gb.mrcm_solve(K), gr.mrcm_solve(K), o.mrcm_solve(K)
+    for x, y in ((a.p, b.p), (a.u, b.u), (a.p, r.p), (a.u, r.u)):
+        assert rel_l2(x, y) <= 1e-10
+    assert a.info.div_residual <= 1e-10 * a.info.div_scale
+    kn = K * np.exp(0.1 * np.random.default_rng(2).standard_normal(K.size))
+    ma, mr = gb.mpm_pressure_update(kn), o.mpm_pressure_update(kn)
+    assert rel_l2(ma.p, mr.p) <= 1e-10 and rel_l2(ma.u, mr.u) <= 1e-10
+    sp = api.SplittingConfig(method=api.MPM2P, eta=0.01, eta_mode=api.EPS_RELATIVE, te=30, cfl_safety=0.5)
+    ra, rr = gb.run(sp), o.run(sp)
+    assert [s["rebuilt"] for s in ra.record.steps] == [s["rebuilt"] for s in rr.record.steps]
+    assert np.max(np.abs(ra.s_final - rr.s_final)) <= TOL_S
+    assert rel_l2(ra.u_final, rr.u_final) <= TOL_PU and rel_l2(ra.p_final, rr.p_final) <= TOL_PU

@@ -124,11 +124,23 @@ def make(name):
             out[pre + "ld_s"] = round_mantissa(x.s_final)
             out[pre + "ld_p"] = round_mantissa(x.p_final)
             out[pre + "ld_u"] = round_mantissa(x.u_final)
+            out[pre + "ld_dt"] = np.array([s["dt"] for s in x.record.steps])
+            out[pre + "ld_pvi"] = np.array([s["pvi"] for s in x.record.steps])
         el = t1 + t2
         msg = (f"pass1 te {r1.record.te} (breakthrough {b}), pass2 te {r2.record.te} rebuilds {r2.record.tm_total}; "
                f"long double {t3 + t4:.0f} s")
     elif name == "C5":
         sp = c5_split(cfg)
+        if os.environ.get("EXTENDED") == "1":
+            # the whole run in extended precision (long double), the exact-answer
+            # yardstick for double-precision roundoff at C5 (written beside run_C5.npz)
+            x, el = run_oracle(cfg, sp, extended=True)
+            out.update(record_arrays(x))
+            out.update(field_arrays(x, full=False))
+            path = os.path.join(GOLDEN, "run_C5_ld.npz")
+            np.savez_compressed(path, **out)
+            print(f"C5 long double: rebuilds {x.record.update_steps}; {el:.0f} s -> {path}", flush=True)
+            return
         r, el = run_oracle(cfg, sp)
         out.update(record_arrays(r))
         out.update(field_arrays(r, full=False))
