@@ -14,11 +14,9 @@
 // two GEMMs per block; per solve: 2 nblk - 1 dependent block products, each
 // HBM-bound. At C5: 128 blocks of 510 unknowns, S^-1 / T / T^T / D / E about
 // 0.27 GB each.
-#include <cooperative_groups.h>
 
 #include "context.cuh"
 
-namespace cg = cooperative_groups;
 
 namespace mpm2p {
 
@@ -219,146 +217,6 @@ __global__ void __launch_bounds__(256) k_bt_bwd(const double* __restrict__ Sinv,
     if (bt_combine(acc, lane) && on) x[row] = acc;
 }
 
-// ---- persistent sweeps ------------------------------------------------------
-// Both block sweeps of a solve in ONE cooperative kernel, one grid barrier
-// per block step instead of one launch. CTA c owns rows [c s_j / G, (c+1) s_j / G)
-// of every block j (at most RPC rows; WPR = 8 / RPC warps per row, NPL
-// doubles per lane). A step's matrix rows are loaded into registers one step
-// ahead (issued before the previous step's barrier), so after each barrier
-// only the vector part is on the chain:
-//   forward  y_j -= G_j y_{j-1}, and sy_{j-1} = Sinv_{j-1} y_{j-1}   (j = 1 .. nb-1)
-//   then     sy_{nb-1} = Sinv_{nb-1} y_{nb-1},  x_{nb-1} = sy_{nb-1}
-//   backward x_j = sy_j - T_j x_{j+1}                               (j = nb-2 .. 0)
-struct BtSweepArgs {
-    const double *G, *Sinv, *T;
-    const long long *doff, *eoff;
-    const int *sz, *voff;
-    int nb, n;
-    double *y, *x, *sy;
-};
-template <int RPC, int NPL>
-__global__ void __launch_bounds__(256) k_bt_sweeps(BtSweepArgs a) {
-    pdl_begin();
-    cg::grid_group grid = cg::this_grid();
-    constexpr int WPR = 8 / RPC;
-    __shared__ double part[2][8];
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int lr = w / WPR, pw = w % WPR;
-    const int G = gridDim.x, cta = blockIdx.x;
-    struct Slice {
-        int row, c0, c1, cols;
-    };
-    // this warp's (row, column range) of a block-j matrix with `cols` columns; row -1: idle
-    auto slice = [&](int j, int cols) {
-        Slice t;
-        const int s = a.sz[j];
-        const int r0 = (int)((long long)cta * s / G), r1 = (int)((long long)(cta + 1) * s / G);
-        t.row = r0 + lr < r1 ? r0 + lr : -1;
-        const int ql = (cols + WPR - 1) / WPR;
-        t.c0 = pw * ql;
-        t.c1 = min(cols, t.c0 + ql);
-        t.cols = cols;
-        return t;
-    };
-    auto fetch = [&](double (&v)[NPL], const double* base, const Slice& t) {
-#pragma unroll
-        for (int q = 0; q < NPL; ++q) {
-            const int c = t.c0 + lane + 32 * q;
-            v[q] = (t.row >= 0 && c < t.c1) ? __ldg(base + (size_t)t.row * t.cols + c) : 0.0;
-        }
-    };
-    auto dot = [&](const double (&v)[NPL], const Slice& t, const double* xv) {
-        double acc = 0.0;
-        if (t.row >= 0) {
-#pragma unroll
-            for (int q = 0; q < NPL; ++q) {
-                const int c = t.c0 + lane + 32 * q;
-                if (c < t.c1) acc = fma(v[q], __ldcg(xv + c), acc);
-            }
-        }
-        return warp_sum(acc);
-    };
-    // two row sums at once (partials combined in part order); valid in lane 0 of pw == 0
-    auto combine2 = [&](double& u, double& v) {
-        if (lane == 0) {
-            part[0][w] = u;
-            part[1][w] = v;
-        }
-        __syncthreads();
-        if (pw == 0 && lane == 0) {
-            u = part[0][w];
-            v = part[1][w];
-            for (int q = 1; q < WPR; ++q) {
-                u += part[0][w + q];
-                v += part[1][w + q];
-            }
-        }
-        __syncthreads();
-    };
-    double gc[NPL], gn[NPL], sc_[NPL], sn[NPL];
-    Slice tg{}, ts{};
-    // ---- forward sweep, with sy_{j-1} alongside
-    if (a.nb > 1) {
-        tg = slice(1, a.sz[0]);
-        fetch(gn, a.G + a.eoff[0], tg);
-    }
-    ts = slice(0, a.sz[0]);
-    fetch(sn, a.Sinv + a.doff[0], ts);
-    for (int j = 1; j < a.nb; ++j) {
-        const Slice cg_ = tg, cs_ = ts;
-#pragma unroll
-        for (int q = 0; q < NPL; ++q) {
-            gc[q] = gn[q];
-            sc_[q] = sn[q];
-        }
-        if (j + 1 < a.nb) {
-            tg = slice(j + 1, a.sz[j]);
-            fetch(gn, a.G + a.eoff[j], tg);
-        }
-        ts = slice(j, a.sz[j]);
-        fetch(sn, a.Sinv + a.doff[j], ts);
-        const double* yp = a.y + a.voff[j - 1];
-        double u = dot(gc, cg_, yp), v = dot(sc_, cs_, yp);
-        combine2(u, v);
-        if (pw == 0 && lane == 0) {
-            if (cg_.row >= 0) a.y[a.voff[j] + cg_.row] -= u;
-            if (cs_.row >= 0) a.sy[a.voff[j - 1] + cs_.row] = v;
-        }
-        grid.sync();
-    }
-    {  // last block: sy and x (same CTA rows, no barrier between)
-        const int jl = a.nb - 1;
-        const Slice cs_ = ts;
-#pragma unroll
-        for (int q = 0; q < NPL; ++q) sc_[q] = sn[q];
-        if (jl >= 1) {
-            tg = slice(jl - 1, a.sz[jl]);
-            fetch(gn, a.T + a.eoff[jl - 1], tg);
-        }
-        double u = 0.0, v = dot(sc_, cs_, a.y + a.voff[jl]);
-        combine2(u, v);
-        if (pw == 0 && lane == 0 && cs_.row >= 0) {
-            a.sy[a.voff[jl] + cs_.row] = v;
-            a.x[a.voff[jl] + cs_.row] = v;
-        }
-        if (jl >= 1) grid.sync();
-    }
-    // ---- backward sweep
-    for (int j = a.nb - 2; j >= 0; --j) {
-        const Slice ct = tg;
-#pragma unroll
-        for (int q = 0; q < NPL; ++q) gc[q] = gn[q];
-        if (j >= 1) {
-            tg = slice(j - 1, a.sz[j]);
-            fetch(gn, a.T + a.eoff[j - 1], tg);
-        }
-        double u = dot(gc, ct, a.x + a.voff[j + 1]), v = 0.0;
-        combine2(u, v);
-        if (pw == 0 && lane == 0 && ct.row >= 0) a.x[a.voff[j] + ct.row] = __ldcg(a.sy + a.voff[j] + ct.row) - u;
-        if (j > 0) grid.sync();
-    }
-}
-
 }  // namespace
 
 // In-place inverse of an n x n row-major matrix (dense.cu).
@@ -460,21 +318,6 @@ void bt_factor(Ctx& c) {
     }
 }
 
-// Persistent-sweep configuration (bt_setup): rows per CTA and doubles per lane.
-namespace {
-template <int RPC, int NPL>
-bool bt_sweeps_launch(Ctx& c, BtSweepArgs& args) {
-    static int per_sm = -1;
-    if (per_sm < 0) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bt_sweeps<RPC, NPL>, 256, 0));
-    if (per_sm < 1) return false;
-    void* p[] = {&args};
-    PROF(c, "k_bt_sweeps");
-    CK(cudaLaunchCooperativeKernel((void*)k_bt_sweeps<RPC, NPL>, c.num_sms, 256, p, 0, c.st));
-    CK_LAUNCH();
-    return true;
-}
-}  // namespace
-
 // x = M^-1 rhs through K x = J rhs.
 void bt_solve(Ctx& c, const double* rhs, double* x) {
     const int n = c.dim, nb = c.bt_nblk;
@@ -484,26 +327,6 @@ void bt_solve(Ctx& c, const double* rhs, double* x) {
         PROF(c, "k_bt_gather");
         launch_k(c, k_bt_gather, cdiv(n, TPB), TPB, 0, rhs, n, c.bt_blk, c.bt_loc, c.bt_voffd, y);
         CK_LAUNCH();
-    }
-    if (c.bt_persistent) {  // one cooperative kernel for both sweeps (one grid barrier per block step)
-        int smax = 0;
-        for (int v : c.bt_sz) smax = std::max(smax, v);
-        const int rpc = cdiv(smax, c.num_sms);
-        BtSweepArgs args{c.bt_G.p, c.bt_Sinv.p, c.bt_T.p, c.bt_doffd.p, c.bt_eoffd.p, c.bt_bsz.p, c.bt_voffd.p,
-                         nb, n, y, xb, c.bt_sy.p};
-        bool done = false;
-        // doubles per lane: a row's column range over 8 / RPC warps
-        auto npl = [&](int r) { return cdiv(smax, (8 / r) * 32); };
-        if (rpc <= 2 && npl(2) <= 8) done = bt_sweeps_launch<2, 8>(c, args);
-        else if (rpc <= 4 && npl(4) <= 8) done = bt_sweeps_launch<4, 8>(c, args);
-        else if (rpc <= 4 && npl(4) <= 16) done = bt_sweeps_launch<4, 16>(c, args);
-        else if (rpc <= 8 && npl(8) <= 16) done = bt_sweeps_launch<8, 16>(c, args);
-        if (done) {
-            PROF(c, "k_bt_unpermute");
-            launch_k(c, k_bt_unpermute, cdiv(n, TPB), TPB, 0, xb, n, c.bt_blk, c.bt_loc, c.bt_voffd, x);
-            CK_LAUNCH();
-            return;
-        }
     }
     // block steps with programmatic dependent launch (see k_bt_fwd)
     auto launch_pdl = [&](auto kern, int grid, auto... args) {

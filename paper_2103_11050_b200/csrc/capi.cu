@@ -261,17 +261,14 @@ void create_ctx(mpm2p_ctx* ctx, const mpm2p_problem* P) {
     c.repair_active = L.n_sub > 1 || c.grounded;
     if (const char* e = std::getenv("MPM2P_NO_GRAPHS")) c.use_graphs = e[0] != 0 && e[0] == '0';
     if (const char* e = std::getenv("MPM2P_NO_REGBAND")) c.no_regband = e[0] == '1';
-    if (const char* e = std::getenv("MPM2P_GJ")) c.gj_legacy = std::strcmp(e, "legacy") == 0;
     if (const char* e = std::getenv("MPM2P_NO_TWIST")) c.no_twist = e[0] == '1';
     if (const char* e = std::getenv("MPM2P_DS_BLK")) c.ds_blk = std::atoi(e);
     if (const char* e = std::getenv("MPM2P_PDL")) c.pdl = e[0] == '1';
     if (const char* e = std::getenv("MPM2P_BT_PDL")) c.bt_pdl = e[0] != '0';
-    if (const char* e = std::getenv("MPM2P_BT_PERSIST")) c.bt_persistent = e[0] == '1';
     if (const char* e = std::getenv("MPM2P_GRAPH_TIMING")) c.graph_timing = e[0] == '1';
     if (const char* e = std::getenv("MPM2P_UPWIND_TILE")) c.upwind_tiled = e[0] != '0';
     if (const char* e = std::getenv("MPM2P_UPWIND_COL")) c.upwind_col = std::atoi(e);
     if (const char* e = std::getenv("MPM2P_UPWIND_RB")) c.upwind_rb = std::atoi(e);
-    if (const char* e = std::getenv("MPM2P_UPWIND_PAIR")) c.upwind_pair = e[0] != '0';
     if (const char* e = std::getenv("MPM2P_KAPPA_COL")) c.kappa_col = std::atoi(e);
     if (const char* e = std::getenv("MPM2P_RHS_SUB")) c.rhs_sub = e[0] != '0';
     if (const char* e = std::getenv("MPM2P_REFINE")) {  // 1: always refine, 0: never (experiments)

@@ -96,7 +96,6 @@ struct Ctx {
     DevBuf<double> csr_val, Mdense, Minv, gj_work, gj_col, gj_row, gj_krow;
     DevBuf<int> gj_piv, gj_aux;
     DevBuf<double> gj_pp;     // ping-pong GJ: two padded copies + two 32 x 32 pivot inverses
-    bool gj_legacy = false;   // MPM2P_GJ=legacy: the two-barrier k_block_gj
     DevBuf<double> irhs, icoef, ires, idelta;
     int nnz = 0;
     // K7 Krylov interface solve (dimension above the dense limit, or forced by
@@ -116,7 +115,6 @@ struct Ctx {
     DevBuf<int> bt_blk, bt_loc, bt_bsz, bt_voffd;
     DevBuf<long long> bt_doffd, bt_eoffd;
     DevBuf<double> bt_D, bt_E, bt_Sinv, bt_T, bt_G, bt_y, bt_x, bt_sy;
-    bool bt_persistent = false;  // MPM2P_BT_PERSIST=1: both sweeps in one cooperative kernel (measured slower at C5: 10.30 vs 9.90 ms)
     // per-solve scratch
     DevBuf<double> X, PU, PB, PS, GZ, WU, RU, RS, skel, resid, delta, corr;
     // downscale
@@ -128,7 +126,6 @@ struct Ctx {
     bool sep_repair = false;  // separable repair solve (sep_repair_setup) instead of the dense inverse
     DevBuf<double> sep_qx, sep_qy, sep_lam, sep_z1, sep_z2;
     bool rhs_sub = true;  // k_mpm_rhs_sub, one CTA per subdomain (MPM2P_RHS_SUB=0: one thread per cell)
-    bool upwind_pair = false;  // k_upwind_pair: two columns per lane (MPM2P_UPWIND_PAIR=1)
     int upwind_rb = 1;         // rows per k_upwind_col chunk (MPM2P_UPWIND_RB = 1 | 2 | 4)
     int kappa_col = -1;        // k_kappa_col: -1 auto (long row segments), 1 always, 0 never (MPM2P_KAPPA_COL)
     int upwind_col = -1;       // k_upwind_col: -1 auto (long row segments), 1 always, 0 never (MPM2P_UPWIND_COL)

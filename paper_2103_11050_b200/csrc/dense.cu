@@ -206,140 +206,11 @@ __global__ void __launch_bounds__(GJ_THREADS) k_gauss_jordan(GJArgs a) {
     }
 }
 
-// ---- pivot-free blocked Gauss-Jordan (symmetric quasi-definite / SPD) -----
-// In-place inversion of W (n x n). For each diagonal block p (pb <= 32):
-//   A: every CTA inverts W_pp redundantly in shared memory (P = W_pp^-1),
-//      then a slice of Rbuf = P W_p,: (new block row) and Cbuf = W_:,p (old
-//      block column);
-//   B: W_ij -= Cbuf_i Rbuf_j off the block; W_pj = Rbuf_j; W_ip = -Cbuf_i P;
-//      W_pp = P.
-// Two grid barriers per block, every CTA busy in both phases. Stable without
-// pivoting for quasi-definite K = J M (checked per context) and
-// for the SPD repair Laplacian.
-struct BGJArgs {
-    double* W;
-    int n;
-    double* Rbuf;  // 32 x n
-    double* Cbuf;  // n x 32
-    int* singular;
-};
-
-constexpr int GJB = 32;  // diagonal block width
-
-__global__ void __launch_bounds__(256) k_block_gj(BGJArgs a) {
-    pdl_begin();
-    cg::grid_group grid = cg::this_grid();
-    extern __shared__ double dsm[];
-    double (*P)[GJB + 1] = reinterpret_cast<double (*)[GJB + 1]>(dsm);  // 32 x 33
-    double* sg = dsm + GJB * (GJB + 1);                                // 64 x 32 tile of Cbuf
-    double* sr = sg + 64 * GJB;                                        // 32 x 128 tile of Rbuf
-    const int n = a.n, tid = threadIdx.x, nt = blockDim.x;
-    const long long gtid = (long long)blockIdx.x * nt + tid, gnt = (long long)gridDim.x * nt;
-    for (int p0 = 0; p0 < n; p0 += GJB) {
-        const int pb = n - p0 < GJB ? n - p0 : GJB;
-        // ---- phase A: every CTA inverts the diagonal block ------------------
-        for (int x = tid; x < GJB * GJB; x += nt) {
-            const int r = x / GJB, cc = x % GJB;
-            P[r][cc] = (r < pb && cc < pb) ? a.W[(size_t)(p0 + r) * n + p0 + cc] : (r == cc ? 1.0 : 0.0);
-        }
-        __syncthreads();
-        for (int k = 0; k < pb; ++k) {
-            const double piv = P[k][k];
-            const double pinv = 1.0 / piv;
-            double f[4], rk[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int x = tid + q * 256, r = x / GJB, cc = x % GJB;
-                f[q] = P[r][k];
-                rk[q] = P[k][cc];
-            }
-            __syncthreads();
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int x = tid + q * 256, r = x / GJB, cc = x % GJB;
-                if (r == k) P[r][cc] = (cc == k) ? pinv : rk[q] * pinv;
-                else P[r][cc] = (cc == k) ? -f[q] * pinv : P[r][cc] - f[q] * pinv * rk[q];
-            }
-            if (blockIdx.x == 0 && tid == 0 && (!(piv != 0.0) || !isfinite(piv))) *a.singular = 1;
-            __syncthreads();
-        }
-        // new block row Rbuf = P W[p, :] (one thread per (r, j)), old block column Cbuf
-        for (long long x = gtid; x < (long long)GJB * n; x += gnt) {
-            const int r = (int)(x / n), j = (int)(x % n);
-            if (r >= pb || (j >= p0 && j < p0 + pb)) continue;
-            double acc = 0.0;
-            for (int c = 0; c < pb; ++c) acc += P[r][c] * a.W[(size_t)(p0 + c) * n + j];
-            a.Rbuf[(size_t)r * n + j] = acc;
-        }
-        for (long long x = gtid; x < (long long)n * GJB; x += gnt) {
-            const int i = (int)(x / GJB), c = (int)(x % GJB);
-            a.Cbuf[x] = (c < pb && (i < p0 || i >= p0 + pb)) ? a.W[(size_t)i * n + p0 + c] : 0.0;
-        }
-        grid.sync();
-        // ---- phase B: rank-pb update and block row/column writes -------------
-        const int tr = (n + 63) / 64, tc = (n + 127) / 128;
-        const int ty = tid >> 4, tx = tid & 15;  // 16 x 16 threads: 4 rows x 8 cols each
-        for (int tile = blockIdx.x; tile < tr * tc; tile += gridDim.x) {
-            const int i0 = (tile / tc) * 64, j0 = (tile % tc) * 128;
-            __syncthreads();
-            for (int x = tid; x < 64 * GJB; x += nt) {
-                const int i = i0 + x / GJB;
-                sg[x] = i < n ? a.Cbuf[(size_t)i * GJB + x % GJB] : 0.0;
-            }
-            for (int x = tid; x < GJB * 128; x += nt) {
-                const int c = x / 128, j = j0 + x % 128;
-                sr[x] = (c < pb && j < n && (j < p0 || j >= p0 + pb)) ? a.Rbuf[(size_t)c * n + j] : 0.0;
-            }
-            __syncthreads();
-            double acc[4][8];
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-#pragma unroll
-                for (int t = 0; t < 8; ++t) acc[q][t] = 0.0;
-#pragma unroll 8
-            for (int c = 0; c < GJB; ++c) {
-                double gv[4], rv[8];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) gv[q] = sg[(ty + 16 * q) * GJB + c];
-#pragma unroll
-                for (int t = 0; t < 8; ++t) rv[t] = sr[c * 128 + tx + 16 * t];
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-#pragma unroll
-                    for (int t = 0; t < 8; ++t) acc[q][t] += gv[q] * rv[t];
-            }
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int i = i0 + ty + 16 * q;
-                if (i >= n) continue;
-                const bool ip = i >= p0 && i < p0 + pb;
-#pragma unroll
-                for (int t = 0; t < 8; ++t) {
-                    const int j = j0 + tx + 16 * t;
-                    if (j >= n) continue;
-                    const bool jp = j >= p0 && j < p0 + pb;
-                    double* w = a.W + (size_t)i * n + j;
-                    if (!ip && !jp) *w -= acc[q][t];
-                    else if (ip && !jp) *w = sr[(i - p0) * 128 + (j - j0)];
-                    else if (!ip && jp) {
-                        double v = 0.0;
-                        for (int c = 0; c < pb; ++c) v -= sg[(i - i0) * GJB + c] * P[c][j - p0];
-                        *w = v;
-                    } else {
-                        *w = P[i - p0][j - p0];
-                    }
-                }
-            }
-        }
-        grid.sync();
-    }
-}
-
-constexpr size_t GJB_SMEM = (GJB * (GJB + 1) + 64 * GJB + GJB * 128) * sizeof(double);
 
 // ---- ping-pong blocked Gauss-Jordan with lookahead -------------------------
-// Same mathematics as k_block_gj (pivot-free GJ over 32 x 32 blocks of a
-// padded npad x npad matrix), restructured so each block step costs ONE grid
+// Pivot-free Gauss-Jordan over 32 x 32 blocks of a padded npad x npad matrix
+// (stable without pivoting for the quasi-definite K = J M, SURVEY.md H1, and
+// the SPD repair Laplacian), structured so each block step costs ONE grid
 // barrier: step k reads W_src and writes W_dst (no read/write conflicts inside
 // a step), and a dedicated lookahead CTA updates the next diagonal block and
 // inverts it during step k, so P_{k+1} = W_{k+1,k+1}^-1 is ready when step k+1
@@ -925,15 +796,10 @@ __global__ void k_axpy(double* __restrict__ y, const double* __restrict__ x, int
 
 namespace {
 
-void block_gj_legacy(Ctx& c, double* W, int n);
 void gj_pp_run(Ctx& c, double* W0, double* W1, int nb, int ld, int n);
 
 // In-place inverse of W (n x n) by the ping-pong blocked GJ (k_gj_pp).
 void block_gj_inplace(Ctx& c, double* W, int n) {
-    if (c.gj_legacy) {
-        block_gj_legacy(c, W, n);
-        return;
-    }
     const int nb = cdiv(n, PPB), ld = nb * PPB;
     c.gj_pp.alloc(std::max(c.gj_pp.n, 2 * (size_t)ld * ld + 2 * PPB * PPB));
     c.gj_piv.alloc(std::max(c.gj_piv.n, (size_t)n + 1));
@@ -1001,27 +867,6 @@ void gj_pp_run(Ctx& c, double* W0, double* W1, int nb, int ld, int n) {
     }
 }
 
-void block_gj_legacy(Ctx& c, double* W, int n) {
-    c.gj_col.alloc(std::max(c.gj_col.n, (size_t)n * GJB));
-    c.gj_row.alloc(std::max(c.gj_row.n, (size_t)n * GJB));
-    static bool attr_set = false;  // set once, outside any graph capture
-    if (!attr_set) {
-        CK(cudaFuncSetAttribute(k_block_gj, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GJB_SMEM));
-        attr_set = true;
-    }
-    c.gj_piv.alloc(std::max(c.gj_piv.n, (size_t)n + 1));
-    CK(cudaMemsetAsync(c.gj_piv.p + n, 0, sizeof(int), c.st));
-    int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_block_gj, 256, GJB_SMEM));
-    if (per_sm < 1) throw CudaError("dense_inverse: block Gauss-Jordan does not fit on an SM");
-    const int tiles = cdiv(n, 64) * cdiv(n, 128);
-    const int blocks = std::min(per_sm * c.num_sms, std::max(c.num_sms, tiles));
-    BGJArgs ga{W, n, c.gj_row.p, c.gj_col.p, c.gj_piv.p + n};
-    void* args[] = {&ga};
-    PROF(c, "k_block_gj");
-    CK(cudaLaunchCooperativeKernel((void*)k_block_gj, blocks, 256, args, GJB_SMEM, c.st));
-    CK_LAUNCH();
-}
 
 void launch_rcond(Ctx& c, const double* A, const double* Ainv, int n, double* rcond_dev, unsigned err_bit,
                   double threshold) {

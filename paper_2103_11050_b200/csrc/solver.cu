@@ -2119,8 +2119,8 @@ void launch_rebuild(Ctx& c, const double* kappa, bool compute_beta) {  // comput
             // block LDL^T; a zero / non-finite pivot in any block raises ERR_SINGULAR
             krylov_prepare(c);
             bt_factor(c);
-        } else if (c.gj_legacy || !interface_inverse_csr(c, &c.sc.p->rcond, ERR_SINGULAR, 1e-14)) {
-            // legacy / non-symmetric fallback through a dense copy of M
+        } else if (!interface_inverse_csr(c, &c.sc.p->rcond, ERR_SINGULAR, 1e-14)) {
+            // non-symmetric fallback through a dense copy of M
             c.Mdense.alloc((size_t)c.dim * c.dim);
             {
                 PROF(c, "k_csr_to_dense");

@@ -513,133 +513,6 @@ __global__ void __launch_bounds__(256, MINB) k_upwind_col(Layout L, const double
     if (err) atomicOr(&sc->err, ERR_CFL);
 }
 
-// Two columns per lane: lane l (1..30) owns columns c0 = 60 w + 2 (l - 1) and
-// c0 + 1; lanes 0 and 31 hold the halo pairs. The pair shares its middle
-// vertical face, the inner neighbours' f are the lane's own registers and
-// only the outer ones come by shuffle, so the per-lane pointer, predicate,
-// shuffle and loop work is spread over two cells. Same face-flux operations
-// as k_upwind_col (bit-identical).
-constexpr int UP_COLS = 60;
-struct UpCell {  // one cell's row state
-    double f, s;
-    bool o;
-};
-template <int MINB>
-__global__ void __launch_bounds__(256, MINB) k_upwind_pair(Layout L, const double* __restrict__ s,
-                                                           double* __restrict__ s_out, const double* __restrict__ u,
-                                                           Scalars* sc, double inflow, double M, int take_next,
-                                                           int inj_cn, int sub, int rows) {
-    pdl_begin();
-    const int lane = threadIdx.x & 31;
-    const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int ncw = (L.nx + UP_COLS - 1) / UP_COLS;
-    const int wc = gw % ncw, wr = gw / ncw;
-    const int j0 = wr * rows;
-    const double dt = take_next ? sc->dt_next : (sub > 1 ? sc->dt / sub : sc->dt);
-    if (gw == 0 && lane == 0) {
-        (void)frac_flow(inflow, M, &sc->clamp);  // f_in is evaluated once per call
-        if (take_next) {
-            sc->dt = dt;
-            sc->any_flow = sc->any_next;
-            const double rt = sc->inj_next;
-            sc->inj = rt;
-            const double pore = L.lx * L.ly;
-            for (int k = 0; k < inj_cn; ++k) sc->pvi += rt * dt / pore;
-        }
-    }
-    if (j0 >= L.ny) return;  // warp-uniform
-    const int j1 = min(j0 + rows, L.ny);
-    const int c0 = wc * UP_COLS + 2 * (lane - 1), c1 = c0 + 1;
-    const bool in0 = c0 >= 0 && c0 < L.nx, in1 = c1 >= 0 && c1 < L.nx;
-    const bool own = lane >= 1 && lane <= UP_COLS / 2;
-    const bool own0 = own && in0, own1 = own && in1;
-    const double fin = frac_flow(inflow, M, nullptr);
-    const double dtv = dt / L.vol();
-    const double hx = L.hx, hy = L.hy;
-    const int ic0 = in0 ? c0 : 0, ic1 = in1 ? c1 : 0;
-    auto ld_s = [&](int ic, bool in, int j) { return (in && j >= 0 && j < L.ny) ? s[L.cell(ic, j)] : 0.0; };
-    UpCell S0, S1, C0, C1;
-    {
-        const double a = ld_s(ic0, in0, j0 - 1), b = ld_s(ic1, in1, j0 - 1);
-        const double p = ld_s(ic0, in0, j0), q = ld_s(ic1, in1, j0);
-        S0 = {frac_flow(a, M, nullptr), a, out_of_range(a)};
-        S1 = {frac_flow(b, M, nullptr), b, out_of_range(b)};
-        C0 = {frac_flow(p, M, nullptr), p, out_of_range(p)};
-        C1 = {frac_flow(q, M, nullptr), q, out_of_range(q)};
-    }
-    double uS0 = own0 ? u[L.hface(ic0, j0)] : 0.0, uS1 = own1 ? u[L.hface(ic1, j0)] : 0.0;
-    unsigned long long cnt = 0;
-    bool err = false;
-    unsigned obS0 = __ballot_sync(0xffffffffu, S0.o), obS1 = __ballot_sync(0xffffffffu, S1.o);
-    // next row's operands (one row ahead) through running row pointers based
-    // at column c0 (only in-range lanes dereference them)
-    double nS0, nS1, uW, uM, uE, uN0, uN1;
-    const double* ps = s + (long)(j0 + 1) * L.nx + c0;
-    const double* pv = u + (long)j0 * (L.nx + 1) + c0;
-    const double* ph = u + L.vcount() + (long)(j0 + 1) * L.nx + c0;
-    double* po = s_out + (long)j0 * L.nx + c0;
-    auto load_row = [&](int j) {
-        const bool r = j < j1, rn = r && j + 1 < L.ny;
-        nS0 = (rn && in0) ? ps[0] : 0.0;
-        nS1 = (rn && in1) ? ps[1] : 0.0;
-        uW = (r && own0) ? pv[0] : 0.0;
-        uM = (r && own0) ? pv[1] : 0.0;
-        uE = (r && own1) ? pv[2] : 0.0;
-        uN0 = (r && own0) ? ph[0] : 0.0;
-        uN1 = (r && own1) ? ph[1] : 0.0;
-        ps += L.nx;
-        pv += L.nx + 1;
-        ph += L.nx;
-    };
-    load_row(j0);
-    for (int j = j0; j < j1; ++j) {
-        const double cS0 = nS0, cS1 = nS1, cW = uW, cM = uM, cE = uE, cN0 = uN0, cN1 = uN1;
-        load_row(j + 1);
-        const UpCell N0{frac_flow(cS0, M, nullptr), cS0, out_of_range(cS0)};
-        const UpCell N1{frac_flow(cS1, M, nullptr), cS1, out_of_range(cS1)};
-        const double fWo = __shfl_up_sync(0xffffffffu, C1.f, 1);    // west of c0: lane - 1's c1
-        const double fEo = __shfl_down_sync(0xffffffffu, C0.f, 1);  // east of c1: lane + 1's c0
-        const unsigned ob0 = __ballot_sync(0xffffffffu, C0.o), ob1 = __ballot_sync(0xffffffffu, C1.o);
-        const bool lasty = j + 1 == L.ny;
-        const bool anyo = (ob0 | ob1 | obS0 | obS1) != 0u;  // warp-uniform
-        // one cell: k_upwind_col's operations
-        auto update = [&](int i, int k, const UpCell& C, const UpCell& S, const UpCell& N, double fW, double fE,
-                          bool oW, double uw, double ue, double un, double us, bool ownc) {
-            const bool firstx = i == 0, lastx = i + 1 == L.nx;
-            const double fEv = ue >= 0.0 ? C.f : (lastx ? fin : fE);
-            const double fWv = uw >= 0.0 ? (firstx ? fin : fW) : C.f;
-            const double fNv = un >= 0.0 ? C.f : (lasty ? fin : N.f);
-            const double fSv = us >= 0.0 ? (j == 0 ? fin : S.f) : C.f;
-            const double wE = fEv * ue * hy, wW = fWv * uw * hy;
-            const double wN = fNv * un * hx, wS = fSv * us * hx;
-            if (anyo) {
-                cnt += ownc && (uw >= 0.0 ? (!firstx && oW) : C.o);
-                cnt += ownc && (us >= 0.0 ? (j > 0 && S.o) : C.o);
-                cnt += (ownc && lastx && ue >= 0.0) ? C.o : 0;
-                cnt += (ownc && lasty && un >= 0.0) ? C.o : 0;
-            }
-            const double net = wE - wW + wN - wS;
-            const double sn = C.s - dtv * net;
-            if (ownc) {
-                err |= sn < -1e-12 || sn > 1.0 + 1e-12;
-                po[k] = sn < 0.0 ? 0.0 : (sn > 1.0 ? 1.0 : sn);
-            }
-        };
-        update(c0, 0, C0, S0, N0, fWo, C1.f, (ob1 >> (lane - 1)) & 1u, cW, cM, cN0, uS0, own0);
-        update(c1, 1, C1, S1, N1, C0.f, fEo, C0.o, cM, cE, cN1, uS1, own1);
-        S0 = C0;
-        S1 = C1;
-        C0 = N0;
-        C1 = N1;
-        obS0 = ob0;
-        obS1 = ob1;
-        uS0 = cN0;
-        uS1 = cN1;
-        po += L.nx;
-    }
-    if (cnt) atomicAdd((unsigned long long*)&sc->clamp, cnt);
-    if (err) atomicOr(&sc->err, ERR_CFL);
-}
 
 int upwind_col_rows(const Layout& L, int nsm) {
     const long ncw = (L.nx + UC_COLS - 1) / UC_COLS;
@@ -1001,17 +874,11 @@ void launch_upwind(Ctx& c, const double* s_in, double* s_out, const double* u, d
         // (C5: 191 vs 254 us); short segments (C2, C4) keep the tiled step
         if (c.upwind_col > 0 || (c.upwind_col < 0 && rows >= 16)) {
             const long ncw = (c.L.nx + UC_COLS - 1) / UC_COLS, warps = ncw * ((c.L.ny + rows - 1) / rows);
-            if (c.upwind_pair) {
-                const long npw = (c.L.nx + UP_COLS - 1) / UP_COLS, pw = npw * ((c.L.ny + rows - 1) / rows);
-                launch_k(c, k_upwind_pair<2>, (int)((pw + 7) / 8), 256, 0, c.L, s_in, s_out, u, c.sc, inflow, c.M,
-                         take_next ? 1 : 0, inj_cn, sub, rows);
-            } else {
             auto kern = k_upwind_col<1, 3>;
             if (c.upwind_rb == 2) kern = k_upwind_col<2, 3>;
             else if (c.upwind_rb == 4) kern = k_upwind_col<4, 2>;
             launch_k(c, kern, (int)((warps + 7) / 8), 256, 0, c.L, s_in, s_out, u, c.sc, inflow, c.M,
                      take_next ? 1 : 0, inj_cn, sub, rows);
-            }
         } else if (c.upwind_tiled)
             launch_k(c, k_upwind_tile, dim3(cdiv(c.L.nx, UT_X), cdiv(c.L.ny, UT_Y)), UT_X * UT_Y, 0, c.L, s_in, s_out, u,
                      c.sc, inflow, c.M, take_next ? 1 : 0, inj_cn, sub);

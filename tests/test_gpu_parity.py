@@ -423,7 +423,6 @@ UPWIND_VARIANTS = {
     "col": dict(MPM2P_UPWIND_COL=1),
     "col_rb1": dict(MPM2P_UPWIND_COL=1, MPM2P_UPWIND_RB=1),
     "col_rb4": dict(MPM2P_UPWIND_COL=1, MPM2P_UPWIND_RB=4),
-    "pair": dict(MPM2P_UPWIND_COL=1, MPM2P_UPWIND_PAIR=1),
     "tile": dict(MPM2P_UPWIND_COL=0, MPM2P_UPWIND_TILE=1),
     "cell": dict(MPM2P_UPWIND_COL=0, MPM2P_UPWIND_TILE=0),
 }
@@ -436,7 +435,7 @@ def test_upwind_variants_bitwise(name):
     c = configs.build(name, te_override=31)
     runs = {k: _sim_env(c.problem, **env).run(c.split, c.s0(), c.inflow_sat) for k, env in UPWIND_VARIANTS.items()}
     a = runs["col"]
-    for k in ("col_rb1", "col_rb4", "pair", "tile", "cell"):
+    for k in ("col_rb1", "col_rb4", "tile", "cell"):
         b = runs[k]
         assert np.array_equal(a.s_final, b.s_final) and np.array_equal(a.u_final, b.u_final), k
         assert [s["dt"] for s in a.record.steps] == [s["dt"] for s in b.record.steps], k
@@ -485,16 +484,6 @@ def test_conductivity_col_ragged_bitwise(oracle, nx, ny, sx, sy):
     o = api.Simulator(prob, oracle)
     s = rng.uniform(0.0, 1.0, nx * ny)
     assert np.array_equal(g.conductivity(s), o.conductivity(s))
-
-
-def test_blocktri_persistent_sweeps_match():
-    """The persistent (one cooperative kernel) block sweeps vs per-step launches."""
-    c = configs.build("C2", te_override=21)
-    ra = _sim_env(c.problem, MPM2P_IFACE="blocktri", MPM2P_BT_PERSIST=1).run(c.split, c.s0())
-    rb = _sim_env(c.problem, MPM2P_IFACE="blocktri", MPM2P_BT_PERSIST=0).run(c.split, c.s0())
-    assert [s["rebuilt"] for s in ra.record.steps] == [s["rebuilt"] for s in rb.record.steps]
-    assert np.max(np.abs(ra.s_final - rb.s_final)) <= TOL_S
-    assert rel_l2(ra.p_final, rb.p_final) <= 1e-10 and rel_l2(ra.u_final, rb.u_final) <= 1e-10
 
 
 @pytest.mark.parametrize("nx,ny,nsx,nsy", [(32, 32, 4, 4), (48, 32, 6, 2), (64, 64, 16, 8)])
