@@ -19,7 +19,8 @@
 //    diag(s) G, S22[NT][J] -= diag(s) X_J^T, S22[NT][NT] -= diag(s) G diag(s).
 //    DMMA count per panel: 2(NT-1) for X plus NT(NT-1) for the update
 //    (C5: 18 DMMA per 8 pivots).
-//  * Solve: forward y2 -= X y1 and t1 = G y1 fused into the factorisation;
+//  * Solve: forward y2 -= X y1 and t1 = G y1 fused into the factorisation
+//    (DMMA with y1 as column 0 of the B operand);
 //    backward x1 = t1 - X^T x2. Only X (B x 8 per panel, the accumulator
 //    fragments as they are) and t1 are stored: n*B + n doubles per subdomain,
 //    the same footprint as the scalar factor's L.
@@ -84,7 +85,7 @@ __device__ bool blk_factor_fwd(int n, const BandRows A, const double* y, double*
     double* sX = sS + NT * 64;    // X tiles 1..NT-1 (index I-1)
     double* sy = sX + NT * 64;    // y1
     BlkTile w[NT + 1][NT + 1];    // lower triangle used (J <= I)
-    double yw[NT + 1];            // y of window rows 8I + r (replicated over the quad)
+    double yw[NT + 1];            // y of window rows 8I + r (column 0 of a DMMA accumulator: lanes q == 0)
 #pragma unroll
     for (int I = 0; I <= NT; ++I)
 #pragma unroll
@@ -190,25 +191,28 @@ __device__ bool blk_factor_fwd(int n, const BandRows A, const double* y, double*
 #pragma unroll
         for (int I = 1; I <= NT; ++I)
             *reinterpret_cast<double2*>(xs + (I - 1) * 64 + 2 * lane) = make_double2(x[I].v[0], x[I].v[1]);
-        // ---- forward substitution: t1 = G y1, y2 -= X y1
-        const double y0v = sy[c0], y1v = sy[c1];
-        auto quad_sum = [](double v) {
-            v += __shfl_xor_sync(0xffffffffu, v, 1);
-            v += __shfl_xor_sync(0xffffffffu, v, 2);
-            return v;
-        };
-        const double t1 = quad_sum(fma(g0, y0v, g1 * y1v));
-        st_global_if(Ts + k0 + r, t1, q == 0);
-#pragma unroll
-        for (int I = 1; I <= NT; ++I) yw[I] -= quad_sum(fma(x[I].v[0], y0v, x[I].v[1] * y1v));
         // ---- trailing update S22 -= X S21^T
 #pragma unroll
         for (int I = 1; I < NT; ++I)
             *reinterpret_cast<double2*>(sX + (I - 1) * 64 + r * 8 + c0) = make_double2(x[I].v[0], x[I].v[1]);
         __syncwarp();
+        // forward substitution on the tensor cores too: y1 is the B operand
+        // column 0 (lane (0, q) holds y1[q], y1[q+4]), so X_I Y1 and t1 = G y1
+        // land in column 0 of the accumulators, lanes q == 0 (no shuffles)
+        const double yb0 = r == 0 ? sy[q] : 0.0, yb1 = r == 0 ? sy[q + 4] : 0.0;
+        {
+            double t1 = 0.0, z1 = 0.0;
+            blk_dmma(t1, z1, sg[r * 8 + q], yb0);
+            blk_dmma(t1, z1, sg[r * 8 + q + 4], yb1);
+            st_global_if(Ts + k0 + r, t1, q == 0);
+            yw[NT] -= s_r * t1;  // X_NT y1 = diag(s) G y1
+        }
 #pragma unroll
         for (int I = 1; I < NT; ++I) {
             const double xa0 = -sX[(I - 1) * 64 + r * 8 + q], xa1 = -sX[(I - 1) * 64 + r * 8 + q + 4];
+            double z1 = 0.0;
+            blk_dmma(yw[I], z1, xa0, yb0);
+            blk_dmma(yw[I], z1, xa1, yb1);
 #pragma unroll
             for (int J = 1; J <= I; ++J) {
                 blk_dmma(w[I][J].v[0], w[I][J].v[1], xa0, sa[J - 1][0]);

@@ -91,7 +91,33 @@ __global__ void probe(double seed, long long* out, double* sink) {
     }
     t1 = clock64();
     out[8] = t1 - t0;
-    double s = x + f;
+    // 10. DMMA (mma.sync m8n8k4 f64) dependent chain through the accumulator
+    double d0 = x, d1 = x;
+    t0 = clock64();
+#pragma unroll 16
+    for (int i = 0; i < N; ++i)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                     : "+d"(d0), "+d"(d1)
+                     : "d"(0.5), "d"(0.25));
+    t1 = clock64();
+    out[9] = t1 - t0;
+    // 11. DMMA throughput: 8 independent accumulators
+    double acc[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc[j] = x;
+    t0 = clock64();
+    for (int i = 0; i < N / 8; ++i) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                         : "+d"(acc[2 * j]), "+d"(acc[2 * j + 1])
+                         : "d"(0.5), "d"(0.25));
+    }
+    t1 = clock64();
+    out[10] = t1 - t0;
+    double s = x + f + d0 + d1;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) s += acc[j];
 #pragma unroll
     for (int j = 0; j < 16; ++j) s += y[j];
     sink[lane] = s;
@@ -106,9 +132,10 @@ int main() {
     long long h[16];
     cudaMemcpy(h, d_out, sizeof(h), cudaMemcpyDeviceToHost);
     const char* names[] = {"DFMA dep", "SHFL64 dep", "RCP64+2Newton+DADD dep", "IEEE div dep", "STS+LDS bcast dep",
-                           "SHFL32 dep", "DMUL dep", "DFMA thrpt (per warp-instr)", "SHFL64 thrpt (per shfl64)"};
-    const double per[] = {N, N, N, N, N, N, N, 16.0 * N, N};
-    for (int i = 0; i < 9; ++i) printf("%-32s %8.2f cycles\n", names[i], h[i] / per[i]);
+                           "SHFL32 dep", "DMUL dep", "DFMA thrpt (per warp-instr)", "SHFL64 thrpt (per shfl64)",
+                           "DMMA.884 dep", "DMMA.884 thrpt (1 warp)"};
+    const double per[] = {N, N, N, N, N, N, N, 16.0 * N, N, N, N};
+    for (int i = 0; i < 11; ++i) printf("%-32s %8.2f cycles\n", names[i], h[i] / per[i]);
     printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
 }
