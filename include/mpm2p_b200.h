@@ -22,7 +22,8 @@
  *
  * Error convention (errors.hpp:9-24, mrcmflow_main.cpp:119-129): every call
  * returns 0 on success, MPM2P_ECONFIG (ConfigError), MPM2P_ENUMERIC
- * (NumericError), MPM2P_ECAPACITY (CapacityError) or MPM2P_ECUDA; the message
+ * (NumericError), MPM2P_ECAPACITY (CapacityError, also a failed host
+ * allocation), MPM2P_ECUDA or MPM2P_EINTERNAL; the message
  * is available from mpm2p_last_error(ctx).
  *
  * The CPU oracle (oracle/, test infrastructure only) exports the same
@@ -42,7 +43,8 @@ enum {
     MPM2P_ECONFIG = 2,   /* ConfigError   (errors.hpp:9-12)  */
     MPM2P_ENUMERIC = 3,  /* NumericError  (errors.hpp:14-17) */
     MPM2P_ECAPACITY = 4, /* CapacityError (errors.hpp:19-22) */
-    MPM2P_ECUDA = 5
+    MPM2P_ECUDA = 5,     /* CUDA runtime failure (no reference counterpart) */
+    MPM2P_EINTERNAL = 6  /* unexpected exception inside the library (a bug, never a config problem) */
 };
 
 /* BcKind (elliptic.hpp:13) */
@@ -79,6 +81,12 @@ typedef struct mpm2p_problem {
     const double* q;         /* sources nx*ny, or NULL for zero     */
     const int32_t* bc_kind;  /* 2(nx+ny) BcKind                     */
     const double* bc_value;  /* 2(nx+ny) Pressure g / Flux z (outward) */
+    /* FaceBc::beta / FaceBc::robin_rhs of physical Robin faces
+     * (-beta u.n_out + p_face = robin_rhs, elliptic.hpp:16-28), 2(nx+ny)
+     * each; read only where bc_kind == MPM2P_BC_ROBIN. NULL when the spec has
+     * no Robin face. */
+    const double* bc_beta;
+    const double* bc_robin_rhs;
 } mpm2p_problem;
 
 /* SplittingConfig (simulation.hpp:18-31) + RunInputs::inflow_sat. */
@@ -93,7 +101,7 @@ typedef struct mpm2p_split {
     int32_t stop_on_breakthrough;
     int64_t max_steps_hard;
     double breakthrough_threshold;
-    int32_t track_errors;   /* fine-reference tracking: oracle only (out of the GPU scope) */
+    int32_t track_errors;   /* RunInputs::track_errors: a fine-reference shadow run (fine.cu) */
     double inflow_sat;
 } mpm2p_split;
 

@@ -1,6 +1,7 @@
 // CPU ORACLE — TEST INFRASTRUCTURE ONLY. C ABI over the restatement, with the
 // same signatures as include/mpm2p_b200.h (prefix oracle_ instead of mpm2p_),
 // so parity tests call both implementations identically.
+#include <new>
 #include <algorithm>
 #include <cstring>
 #include <string>
@@ -44,10 +45,14 @@ int guarded(oracle_ctx* ctx, F&& fn) {
         if (ctx) ctx->err = e.what();
         else g_create_err = e.what();
         return MPM2P_ECAPACITY;
+    } catch (const std::bad_alloc& e) {
+        if (ctx) ctx->err = e.what();
+        else g_create_err = e.what();
+        return MPM2P_ECAPACITY;
     } catch (const std::exception& e) {
         if (ctx) ctx->err = e.what();
         else g_create_err = e.what();
-        return MPM2P_ECONFIG;
+        return MPM2P_EINTERNAL;
     }
 }
 
@@ -179,8 +184,14 @@ int oracle_create(const mpm2p_problem* p, oracle_ctx** out) {
         for (int i = 0; i < ctx->bc.count(); ++i) {
             ctx->bc.faces[i].kind = p->bc_kind[i];
             ctx->bc.faces[i].value = p->bc_value[i];
-            if (p->bc_kind[i] != Pressure && p->bc_kind[i] != Flux)
-                throw ConfigError("problem: physical boundary faces must be Pressure or Flux");
+            if (p->bc_kind[i] != Pressure && p->bc_kind[i] != Flux && p->bc_kind[i] != Robin)
+                throw ConfigError("problem: unknown boundary kind");
+            if (p->bc_kind[i] == Robin) {  // FaceBc::robin(beta, rhs) (elliptic.hpp:27)
+                if (!p->bc_beta || !p->bc_robin_rhs) throw ConfigError("problem: Robin faces need bc_beta and bc_robin_rhs");
+                ctx->bc.faces[i].value = 0.0;
+                ctx->bc.faces[i].beta = p->bc_beta[i];
+                ctx->bc.faces[i].robin_rhs = p->bc_robin_rhs[i];
+            }
         }
         ctx->alpha.mode = p->alpha_mode;
         ctx->alpha.alpha = p->alpha;

@@ -22,6 +22,7 @@ class Problem(C.Structure):
         ("alpha_max", C.c_double), ("percentile_lo", C.c_double), ("percentile_hi", C.c_double),
         ("viscosity_ratio", C.c_double),
         ("K", _dp), ("q", _dp), ("bc_kind", _ip), ("bc_value", _dp),
+        ("bc_beta", _dp), ("bc_robin_rhs", _dp),
     ]
 
 
@@ -115,7 +116,7 @@ INSTR_PROTOTYPES = {
 }
 
 # Status codes (errors.hpp:9-24 mapped by the header).
-OK, ECONFIG, ENUMERIC, ECAPACITY, ECUDA = 0, 2, 3, 4, 5
+OK, ECONFIG, ENUMERIC, ECAPACITY, ECUDA, EINTERNAL = 0, 2, 3, 4, 5, 6
 
 
 class Lib:

@@ -50,8 +50,12 @@ class CudaError(RuntimeError):
     pass
 
 
+class InternalError(RuntimeError):
+    pass
+
+
 _ERRORS = {_abi.ECONFIG: ConfigError, _abi.ENUMERIC: NumericError, _abi.ECAPACITY: CapacityError,
-           _abi.ECUDA: CudaError}
+           _abi.ECUDA: CudaError, _abi.EINTERNAL: InternalError}
 
 _LIB = None
 
@@ -69,18 +73,29 @@ def product_lib() -> _abi.Lib:
 @dataclasses.dataclass
 class BoundarySpec:
     """Per-face physical conditions in W(ny) E(ny) S(nx) N(nx) order (elliptic.hpp:33-55)."""
-    kind: np.ndarray   # int32, PRESSURE or FLUX
+    kind: np.ndarray   # int32, PRESSURE, FLUX or ROBIN
     value: np.ndarray  # float64: pressure g, or outward normal velocity z
+    beta: Optional[np.ndarray] = None       # Robin faces: -beta u.n_out + p_face = robin_rhs
+    robin_rhs: Optional[np.ndarray] = None
 
     @staticmethod
     def uniform(nx: int, ny: int, w, e, s, n) -> "BoundarySpec":
         """BoundarySpec::uniform (elliptic.cpp:28-40); each side is (kind, value)."""
         kind = np.empty(2 * (nx + ny), np.int32)
         val = np.empty(2 * (nx + ny), np.float64)
-        for (k, v), sl in ((w, slice(0, ny)), (e, slice(ny, 2 * ny)), (s, slice(2 * ny, 2 * ny + nx)),
-                           (n, slice(2 * ny + nx, 2 * (nx + ny)))):
-            kind[sl] = k
-            val[sl] = v
+        beta = np.zeros(2 * (nx + ny))
+        rhs = np.zeros(2 * (nx + ny))
+        for side, sl in ((w, slice(0, ny)), (e, slice(ny, 2 * ny)), (s, slice(2 * ny, 2 * ny + nx)),
+                         (n, slice(2 * ny + nx, 2 * (nx + ny)))):
+            kind[sl] = side[0]
+            if side[0] == ROBIN:  # (ROBIN, beta, robin_rhs): FaceBc::robin (elliptic.hpp:27)
+                val[sl] = 0.0
+                beta[sl] = side[1]
+                rhs[sl] = side[2]
+            else:
+                val[sl] = side[1]
+        if np.any(kind == ROBIN):
+            return BoundarySpec(kind, val, beta, rhs)
         return BoundarySpec(kind, val)
 
     def pure_neumann(self) -> bool:
@@ -144,11 +159,14 @@ class Problem:
         q = None if self.q is None else np.ascontiguousarray(self.q, np.float64).ravel()
         kind = np.ascontiguousarray(self.bc.kind, np.int32)
         val = np.ascontiguousarray(self.bc.value, np.float64)
-        keep = (K, q, kind, val)
+        rb = None if self.bc.beta is None else np.ascontiguousarray(self.bc.beta, np.float64)
+        rr = None if self.bc.robin_rhs is None else np.ascontiguousarray(self.bc.robin_rhs, np.float64)
+        keep = (K, q, kind, val, rb, rr)
         a = self.alpha
         p = _abi.Problem(self.nx, self.ny, self.lx, self.ly, self.nsx, self.nsy, self.space_kind, self.hbar_mode,
                          self.hbar_edges, a.mode, a.alpha, a.alpha_min, a.alpha_max, a.percentile_lo,
-                         a.percentile_hi, self.viscosity_ratio, dptr(K), dptr(q), iptr(kind), dptr(val))
+                         a.percentile_hi, self.viscosity_ratio, dptr(K), dptr(q), iptr(kind), dptr(val),
+                         dptr(rb), dptr(rr))
         return p, keep
 
 

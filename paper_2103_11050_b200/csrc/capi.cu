@@ -3,6 +3,7 @@
 // over the device kernels, and the extern "C" boundary of
 // include/mpm2p_b200.h. Exceptions map to the reference's error classes
 // (errors.hpp:9-24) as status codes.
+#include <new>
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -66,9 +67,12 @@ int guarded(mpm2p_ctx* ctx, F&& fn) {
     } catch (const CudaError& e) {
         *err = e.what();
         return MPM2P_ECUDA;
-    } catch (const std::exception& e) {
-        *err = e.what();
-        return MPM2P_ECONFIG;
+    } catch (const std::bad_alloc& e) {  // host allocation: out of capacity, not a bad config
+        *err = std::string("host allocation failed: ") + e.what();
+        return MPM2P_ECAPACITY;
+    } catch (const std::exception& e) {  // anything else is an implementation fault, not the caller's config
+        *err = std::string("internal error: ") + e.what();
+        return MPM2P_EINTERNAL;
     }
 }
 
@@ -249,13 +253,17 @@ void create_ctx(mpm2p_ctx* ctx, const mpm2p_problem* P) {
     const int nb = L.bfaces();
     c.bc_kind_h.assign(P->bc_kind, P->bc_kind + nb);
     bool pure_neumann = true;
+    bool any_robin = false;
     for (int i = 0; i < nb; ++i) {
-        if (c.bc_kind_h[i] != BC_PRESSURE && c.bc_kind_h[i] != BC_FLUX)
-            throw ConfigError("problem: physical boundary faces must be Pressure or Flux");
-        if (c.bc_kind_h[i] == BC_PRESSURE) {
-            c.grounded = true;
-            pure_neumann = false;
+        const int k = c.bc_kind_h[i];
+        if (k != BC_PRESSURE && k != BC_FLUX && k != BC_ROBIN) throw ConfigError("problem: unknown boundary kind");
+        if (k == BC_ROBIN) {  // FaceBc::robin(beta, rhs) (elliptic.hpp:27)
+            if (!P->bc_beta || !P->bc_robin_rhs)
+                throw ConfigError("problem: Robin faces need bc_beta and bc_robin_rhs");
+            any_robin = true;
         }
+        if (k != BC_FLUX) pure_neumann = false;  // BoundarySpec::pure_neumann (elliptic.hpp:46-50)
+        if (k == BC_PRESSURE) c.grounded = true;  // only Pressure faces absorb repair residual (mrcm.cpp:333-336)
     }
     c.anchor_m = (L.n_iface == 0) && pure_neumann;
     c.repair_active = L.n_sub > 1 || c.grounded;
@@ -403,6 +411,24 @@ void create_ctx(mpm2p_ctx* ctx, const mpm2p_problem* P) {
     else c.q.zero(c.st);
     upload(c, c.bc_value, P->bc_value, nb);
     CK(cudaMemcpyAsync(c.bc_kind.p, P->bc_kind, nb * sizeof(int), cudaMemcpyHostToDevice, c.st));
+    c.rb_beta.alloc(nb);
+    c.rb_rhs.alloc(nb);
+    if (any_robin) {
+        std::vector<double> rb(nb, 0.0), rr(nb, 0.0);
+        for (int i = 0; i < nb; ++i)
+            if (c.bc_kind_h[i] == BC_ROBIN) {
+                rb[i] = P->bc_beta[i];
+                rr[i] = P->bc_robin_rhs[i];
+            }
+        upload(c, c.rb_beta, rb.data(), nb);
+        upload(c, c.rb_rhs, rr.data(), nb);
+        CK(cudaStreamSynchronize(c.st));
+    } else {
+        c.rb_beta.zero(c.st);
+        c.rb_rhs.zero(c.st);
+    }
+    c.L.rb_beta = c.rb_beta.p;
+    c.L.rb_rhs = c.rb_rhs.p;
     if (L.max_hom > 0) {  // static (interface, basis, flux?, column) table of the homogeneous functions
         std::vector<int4> tab((size_t)L.n_sub * L.max_hom, make_int4(0, 0, 0, 0));
         for (int sd = 0; sd < L.n_sub; ++sd)

@@ -79,7 +79,7 @@ struct Ctx {
     int dim = 0;            // interface system dimension (2 * dim_flux)
 
     // static data
-    DevBuf<double> K, q, bc_value, qsum_sub, ground, Linv;
+    DevBuf<double> K, q, bc_value, rb_beta, rb_rhs, qsum_sub, ground, Linv;
     DevBuf<int4> homtab;  // Layout::hom(s, h) for every (subdomain, homogeneous function)
     DevBuf<int> bc_kind;
     // transport / driver state

@@ -92,6 +92,11 @@ __global__ void k_fine_assemble(Layout L, int anchor, const double* __restrict__
                 rhs += th * bc_value[gbc];
             } else if (kind == BC_FLUX) {
                 rhs -= bc_value[gbc] * area;
+            } else {  // Robin (elliptic.cpp:133-136,176-177)
+                if (!(L.rb_beta[gbc] > 0.0)) atomicOr(&sc->err, ERR_ROBIN_BETA);
+                const double er = eff_robin(th, L.rb_beta[gbc], area);
+                diag += er;
+                rhs += er * L.rb_rhs[gbc];
             }
         };
         if (i == 0) bnd(gbc_w(L, j), tw, L.hy);
@@ -415,7 +420,10 @@ __global__ void k_fine_velocity(Layout L, const double* __restrict__ T, const in
         const double xc = x[bidx(L, i, j)];
         p[c] = xc;
         auto bnd = [&](int gbc, int f, double area, double sgn) {
-            const double un = bc_kind[gbc] == BC_PRESSURE ? T[f] * (xc - bc_value[gbc]) / area : bc_value[gbc];
+            const int kind = bc_kind[gbc];
+            const double un = kind == BC_PRESSURE ? T[f] * (xc - bc_value[gbc]) / area
+                              : kind == BC_ROBIN  ? eff_robin(T[f], L.rb_beta[gbc], area) * (xc - L.rb_rhs[gbc]) / area
+                                                  : bc_value[gbc];
             return sgn * un;
         };
         const int fw = L.vface(i, j), fe = L.vface(i + 1, j), fs = L.hface(i, j), fn = L.hface(i, j + 1);

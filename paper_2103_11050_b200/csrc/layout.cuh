@@ -54,6 +54,11 @@ struct Layout {
     int dim_flux;    // == dim_pressure
     int max_hom;     // max homogeneous solves per subdomain
     const int4* homtab = nullptr;  // device table of hom(s, h) (set once the context exists)
+    // physical Robin faces (FaceBc::beta / robin_rhs by global BoundarySpec
+    // index; elliptic.hpp:16-28), device pointers, read only where
+    // bc_kind == BC_ROBIN
+    const double* rb_beta = nullptr;
+    const double* rb_rhs = nullptr;
 
     HD int cells() const { return nx * ny; }
     HD int vcount() const { return (nx + 1) * ny; }

@@ -173,6 +173,10 @@ __global__ void k_band_entries(Layout L, const double* __restrict__ kappa, const
                 diag += eff_robin(th, beta, e.area);
             } else if (bc_kind[e.gbc] == BC_PRESSURE) {
                 diag += th;
+            } else if (bc_kind[e.gbc] == BC_ROBIN) {  // elliptic.cpp:133-136
+                const double beta = L.rb_beta[e.gbc];
+                if (!(beta > 0.0)) atomicOr(&sc->err, ERR_ROBIN_BETA);
+                diag += eff_robin(th, beta, e.area);
             }
         }
     }
@@ -208,8 +212,9 @@ __global__ void k_rebuild_rhs(Layout L, int max_rhs, const double* __restrict__ 
     for (int t = 0; t < ne; ++t) {
         e[t] = L.edge(s, idx[t]);
         th[t] = half_trans(L, e[t].side, kappa[c]);
-        beta[t] = e[t].iface >= 0 ? edge_beta(L, e[t], bm, bp) : 0.0;
-        er[t] = e[t].iface >= 0 ? eff_robin(th[t], beta[t], e[t].area) : 0.0;
+        const bool prob = e[t].iface < 0 && bc_kind[e[t].gbc] == BC_ROBIN;  // physical Robin face
+        beta[t] = e[t].iface >= 0 ? edge_beta(L, e[t], bm, bp) : prob ? L.rb_beta[e[t].gbc] : 0.0;
+        er[t] = (e[t].iface >= 0 || prob) ? eff_robin(th[t], beta[t], e[t].area) : 0.0;
     }
     // m = 0 (particular): interface edges contribute er * 0
     {
@@ -219,7 +224,9 @@ __global__ void k_rebuild_rhs(Layout L, int max_rhs, const double* __restrict__ 
                 b += er[t] * 0.0;
             } else {
                 const double val = bc_value[e[t].gbc];
-                if (bc_kind[e[t].gbc] == BC_PRESSURE) b += th[t] * val;
+                const int kind = bc_kind[e[t].gbc];
+                if (kind == BC_PRESSURE) b += th[t] * val;
+                else if (kind == BC_ROBIN) b += er[t] * L.rb_rhs[e[t].gbc];  // elliptic.cpp:176-177
                 else b -= val * e[t].area;
             }
         }
@@ -239,6 +246,10 @@ __global__ void k_rebuild_rhs(Layout L, int max_rhs, const double* __restrict__ 
                 const double v = L.basis_val(hk, ht, e[t].pos);
                 const double rr = hflux ? -beta[t] * v * e[t].sign : v;
                 b += er[t] * rr;
+            } else if (e[t].iface < 0 && bc_kind[e[t].gbc] == BC_ROBIN) {
+                // the homogeneous problems keep a physical Robin face's data
+                // (only non-Robin values are zeroed, mrcm.cpp:166-167)
+                b += er[t] * L.rb_rhs[e[t].gbc];
             }
         }
         if (anchor && r == 0) b = 0.0;
@@ -309,6 +320,10 @@ __global__ void k_rebuild_traces(Layout L, int max_rhs, const double* __restrict
             }
             un = te * (pc - rr) / e.area;
             pf = rr + beta * un;
+        } else if (bc_kind[e.gbc] == BC_ROBIN) {  // elliptic.cpp:231-235, every m (mrcm.cpp:166-167)
+            const double rb = L.rb_beta[e.gbc], rr = L.rb_rhs[e.gbc];
+            un = eff_robin(th, rb, e.area) * (pc - rr) / e.area;
+            pf = rr + rb * un;
         } else {
             const double val = m == 0 ? bc_value[e.gbc] : 0.0;
             if (bc_kind[e.gbc] == BC_PRESSURE) {
@@ -645,7 +660,9 @@ __global__ void k_repair_delta(int n, const double* __restrict__ Linv, const dou
     if (gw < n) {
         const double* row = Linv + (size_t)gw * n;
         double v = 0.0;
-        for (int t = lane; t < n; t += 32) v += row[t] * resid[t];
+        // pure-flux physical data: the pinned row's right-hand side is 0
+        // (rhs[0] = 0.0, mrcm.cpp:364-367), so resid[0] does not enter
+        for (int t = lane; t < n; t += 32) v += row[t] * ((grounded || t != 0) ? resid[t] : 0.0);
         v = warp_sum(v);
         if (lane == 0) delta[gw] = v;
     }
@@ -883,6 +900,7 @@ __device__ __forceinline__ double part_trace(const Layout& L, int s, int idx, do
         return te * (pc - 0.0) / e.area;
     }
     if (bc_kind[e.gbc] == BC_PRESSURE) return th * (pc - GZ[x]) / e.area;
+    if (bc_kind[e.gbc] == BC_ROBIN) return eff_robin(th, L.rb_beta[e.gbc], e.area) * (pc - GZ[x]) / e.area;
     return GZ[x];
 }
 
@@ -1399,6 +1417,10 @@ __global__ void k_mpm_rhs(Layout L, int max_rhs, int anchor, const double* __res
             const double g = bc_value[e.gbc] - bpm[eo];
             GZ[eo] = g;
             b += th * g;
+        } else if (bc_kind[e.gbc] == BC_ROBIN) {  // kept as restricted (mpm.cpp:80-81)
+            const double rr = L.rb_rhs[e.gbc];
+            GZ[eo] = rr;
+            b += eff_robin(th, L.rb_beta[e.gbc], e.area) * rr;
         } else {
             const double z = bc_value[e.gbc] - wun[t];
             GZ[eo] = z;
@@ -1466,6 +1488,10 @@ __global__ void __launch_bounds__(RHS_TPB) k_mpm_rhs_sub(Layout L, int max_rhs, 
             const double g = bc_value[e.gbc] - bpm[eo];
             GZ[eo] = g;
             term = th * g;
+        } else if (bc_kind[e.gbc] == BC_ROBIN) {  // kept as restricted (mpm.cpp:80-81)
+            const double rr = L.rb_rhs[e.gbc];
+            GZ[eo] = rr;
+            term = eff_robin(th, L.rb_beta[e.gbc], e.area) * rr;
         } else {
             const double z = bc_value[e.gbc] - wun;
             GZ[eo] = z;
@@ -1537,6 +1563,8 @@ __global__ void k_part_traces(Layout L, int max_rhs, const double* __restrict__ 
         un = te * (pc - 0.0) / e.area;
     } else if (bc_kind[e.gbc] == BC_PRESSURE) {
         un = th * (pc - GZ[x]) / e.area;
+    } else if (bc_kind[e.gbc] == BC_ROBIN) {
+        un = eff_robin(th, L.rb_beta[e.gbc], e.area) * (pc - GZ[x]) / e.area;
     } else {
         un = GZ[x];
     }
