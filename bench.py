@@ -147,7 +147,10 @@ def kernel_work(name, cfg, sz, dim):
         "k_ds_sweep": ("hbm", ns * n * (16.0 * B + 24.0)),       # split downscale: 2 sweeps with the stored factor
         "k_factor_solve": ("fp64", ns * (n * B * B + 4.0 * n * B * (1 + sz.nhat / max(ns, 1)))),
         "k_gemv": ("hbm", 8.0 * dim * dim),
-        "k_mpm_rhs": ("hbm", 56.0 * cells),
+        # MPM-2P right-hand side: p^m, two faces of T(kappa_n), q read; X written (edge terms O(1/w))
+        "k_mpm_rhs": ("hbm", 40.0 * cells),
+        # velocity scatter: X (downscaled potential), two faces of T, q read; two faces of u written
+        "k_ds_u_div": ("hbm", 48.0 * cells),
         "k_ds_prep": ("hbm", 72.0 * cells),
         "k_ds_u": ("hbm", 32.0 * faces),
         "k_divres": ("hbm", 24.0 * cells + 8.0 * faces),

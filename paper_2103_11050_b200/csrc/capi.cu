@@ -302,6 +302,11 @@ void create_ctx(mpm2p_ctx* ctx, const mpm2p_problem* P) {
     int dev = 0;
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&c.num_sms, cudaDevAttrMultiProcessorCount, dev));
+    // per-edge + per-cell right-hand side where the subdomains outnumber the
+    // resident warps (C5: 457 -> 334 us); with few subdomains (C2) one CTA per
+    // subdomain saves a launch (105 vs 109 us per MPM-2P step)
+    c.rhs_w = L.n_sub > 8 * c.num_sms;
+    if (const char* e = std::getenv("MPM2P_RHS_W")) c.rhs_w = e[0] != '0';
     CK(cudaStreamCreateWithFlags(&c.st, cudaStreamNonBlocking));
     configure_kernels();
     const size_t cells = L.cells(), faces = L.faces(), ns = L.n_sub, nbe = L.nbe, ncs = L.ncs;
@@ -359,6 +364,7 @@ void create_ctx(mpm2p_ctx* ctx, const mpm2p_problem* P) {
     c.PS.alloc(ns);
     c.GZ.alloc(ns * nbe);
     c.WU.alloc(ns * nbe);
+    c.ET.alloc(ns * nbe);
     c.RU.alloc(ns * nbe);
     c.RS.alloc(ns);
     c.skel.alloc(skel);

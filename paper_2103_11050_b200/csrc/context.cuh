@@ -108,6 +108,7 @@ struct Ctx {
     // K7b direct block-tridiagonal interface solve (blocktri.cu): the default
     // above the dense limit; MPM2P_IFACE=blocktri forces it, =krylov selects MINRES
     bool use_blocktri = false;
+    bool rhs_w = true;  // per-edge + per-cell MPM-2P right-hand side (k_mpm_edges, k_mpm_rhs_w); MPM2P_RHS_W=0: k_mpm_rhs_sub
     bool bt_pdl = true;  // programmatic dependent launch of the block steps (MPM2P_BT_PDL=0 disables)
     int bt_nblk = 0;
     std::vector<int> bt_sz, bt_voff;
@@ -116,7 +117,7 @@ struct Ctx {
     DevBuf<long long> bt_doffd, bt_eoffd;
     DevBuf<double> bt_D, bt_E, bt_Sinv, bt_T, bt_G, bt_y, bt_x, bt_sy;
     // per-solve scratch
-    DevBuf<double> X, PU, PB, PS, GZ, WU, RU, RS, skel, resid, delta, corr;
+    DevBuf<double> X, PU, PB, PS, GZ, WU, ET, RU, RS, skel, resid, delta, corr;
     // downscale
     DevBuf<double> BDd, BWd, BSd, Dd, Lrd, Xd;
     // split downscale (latency regime): the kappa_n operator is factored on a

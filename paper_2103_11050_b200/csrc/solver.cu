@@ -1235,106 +1235,177 @@ struct CflNext {
     int on = 0;
     double safety = 0.0, dt_cap = 0.0, inflow = 0.0, M = 1.0;
 };
-__global__ void k_ds_u_div(Layout L, const double* __restrict__ T, const double* __restrict__ Xd,
-                           const double* __restrict__ EU, double* __restrict__ u, const double* __restrict__ q,
-                           Scalars* sc, double* part, unsigned* counter, const double* __restrict__ s_out,
-                           CflNext cfl) {
+// Velocity scatter of the downscaled solution (mrcm.cpp:409-431) with the
+// divergence residual and scale (mrcm.cpp:429-437) and the next step's CFL
+// reduction (cfl_timestep, transport.cpp:51-71) in the same pass. One thread
+// per cell, warps over 32 consecutive cells of a row, every load of a cell
+// issued before its arithmetic (one memory round trip per iteration). Each
+// face velocity is one division: the east face of a cell is the west face
+// of the next lane's cell (shuffle; computed directly only by lane 31 and on
+// the east boundary). The divisions of the maxima are pulled out of them
+// (correctly rounded multiplication and division are monotone):
+// max_f fl(fl(|u_f| h) / vol) = fl(fl(max_f |u_f| h) / vol) per face
+// orientation, and cfl_timestep's min_c fl(vol / d_c) = fl(vol / max_c d_c)
+// for d_c = fl(outflux_c slope) > 0 — bit-identical to the per-face form.
+// The boundary-face work (injection rate, outlet probe) is k_bnd_probe's.
+// Slots: res, vmax, hmax, qmax, dmax, any.
+__global__ void __launch_bounds__(256, 4) k_ds_u_div(Layout L, const double* __restrict__ T,
+                                                  const double* __restrict__ Xd, const double* __restrict__ EU,
+                                                  double* __restrict__ u, const double* __restrict__ q, Scalars* sc,
+                                                  double* part, unsigned* counter, CflNext cfl) {
     pdl_begin();
-    // res, scale, 4 x side net, 4 x side max, -min cfl dt, any outflow, injection rate
-    constexpr int NP = 13;
-    double res = 0.0, scale = 0.0, net[4] = {0.0, 0.0, 0.0, 0.0}, smax[4] = {0.0, 0.0, 0.0, 0.0};
-    double best = INFINITY, anyf = 0.0, rate = 0.0;
-    const double vol = L.vol();
+    constexpr int NP = 6;
+    const int lane = threadIdx.x & 31;
+    double res = 0.0, vmax = 0.0, hmax = 0.0, qmax = 0.0, dmax = 0.0, anyf = 0.0;
+    const double vol = L.vol(), hx = L.hx, hy = L.hy;
     const double slope = cfl.on ? sc->slope : 1.0;
+    const int ncell = L.cells();
+    const int stride = gridDim.x * blockDim.x;
+    // warp-uniform trip count (the east faces come by shuffle)
+    for (int c0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31); c0 < ncell; c0 += stride) {
+        const int c = c0 + lane;
+        const bool valid = c < ncell;
+        const int cc = valid ? c : ncell - 1;
+        const int i = cc % L.nx, j = cc / L.nx;
+        const int sx = i / L.snx, ii = i % L.snx, sy = j / L.sny, jj = j % L.sny;
+        const int s = sy * L.nsx + sx;
+        const size_t xo = (size_t)s * L.ncs;
+        const int r = jj * L.snx + ii;
+        const size_t eo = (size_t)s * L.nbe;
+        const bool de = lane == 31 || i + 1 == L.nx || c + 1 >= ncell;  // east face not held by lane + 1
+        const bool hw = ii > 0, he = ii + 1 < L.snx, hs = jj > 0, hn = jj + 1 < L.sny;
+        const double xc = Xd[xo + r];
+        const double xw = hw ? Xd[xo + r - 1] : 0.0;
+        const double tw = hw ? T[L.vface(i, j)] : 0.0;
+        const double ew = hw ? 0.0 : EU[eo + jj];
+        const double xe = (de && he) ? Xd[xo + r + 1] : 0.0;
+        const double te = (de && he) ? T[L.vface(i + 1, j)] : 0.0;
+        // east face on a subdomain edge: the west edge of the subdomain to the east, or the domain boundary
+        const double ee = (de && !he) ? (i + 1 < L.nx ? -EU[eo + L.nbe + jj] : EU[eo + L.sny + jj]) : 0.0;
+        const double xs = hs ? Xd[xo + r - L.snx] : 0.0;
+        const double ts = hs ? T[L.hface(i, j)] : 0.0;
+        const double es = hs ? 0.0 : EU[eo + 2 * L.sny + ii];
+        const double xn = hn ? Xd[xo + r + L.snx] : 0.0;
+        const double tn = hn ? T[L.hface(i, j + 1)] : 0.0;
+        // north face on a subdomain edge: the south edge of the one above, or the domain boundary
+        const double en = hn ? 0.0 : (j + 1 < L.ny ? -EU[(size_t)(s + L.nsx) * L.nbe + 2 * L.sny + ii]
+                                                   : EU[eo + 2 * L.sny + L.snx + ii]);
+        const double qc = q[cc];
+        const double uW = hw ? tw * (xw - xc) / hy : -ew;
+        double uE = __shfl_down_sync(0xffffffffu, uW, 1);
+        if (de) uE = he ? te * (xc - xe) / hy : ee;
+        if (!valid) continue;
+        const double uS = hs ? ts * (xs - xc) / hx : -es;
+        const double uN = hn ? tn * (xc - xn) / hx : en;
+        u[L.vface(i, j)] = uW;
+        u[L.hface(i, j)] = uS;
+        vmax = fmax(vmax, fabs(uW));
+        hmax = fmax(hmax, fabs(uS));
+        if (i == L.nx - 1) {
+            u[L.vface(i + 1, j)] = uE;
+            vmax = fmax(vmax, fabs(uE));
+        }
+        if (j == L.ny - 1) {
+            u[L.hface(i, j + 1)] = uN;
+            hmax = fmax(hmax, fabs(uN));
+        }
+        // divergence(u) - q (grid.cpp:19-31), unfused as in the reference build
+        const double fx = __dmul_rn(__dsub_rn(uE, uW), hy);
+        const double fy = __dmul_rn(__dsub_rn(uN, uS), hx);
+        res = fmax(res, fabs(__dsub_rn(__ddiv_rn(__dadd_rn(fx, fy), vol), qc)));
+        qmax = fmax(qmax, fabs(qc));
+        if (cfl.on) {  // cfl_timestep's per-cell outflux (transport.cpp:59-67), same order and rounding
+            double o = __dmul_rn(0.0 < uE ? uE : 0.0, hy);
+            o = __dadd_rn(o, __dmul_rn(0.0 < -uW ? -uW : 0.0, hy));
+            o = __dadd_rn(o, __dmul_rn(0.0 < uN ? uN : 0.0, hx));
+            o = __dadd_rn(o, __dmul_rn(0.0 < -uS ? -uS : 0.0, hx));
+            if (o > 0.0) {
+                anyf = 1.0;
+                dmax = fmax(dmax, __dmul_rn(o, slope));
+            }
+        }
+    }
+    __shared__ double shm[32 * NP];
+    __shared__ double red[NP];
+    double v[NP] = {res, vmax, hmax, qmax, dmax, anyf};
+    block_reduce_multi<NP>(v, 0u, shm, red);
+    if (threadIdx.x < NP) part[NP * blockIdx.x + threadIdx.x] = red[threadIdx.x];
+    if (last_block_done(counter)) {
+        double a[NP];
+#pragma unroll
+        for (int k = 0; k < NP; ++k) a[k] = 0.0;
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+#pragma unroll
+            for (int k = 0; k < NP; ++k) a[k] = fmax(a[k], __ldcg(part + (size_t)NP * b + k));
+        }
+        block_reduce_multi<NP>(a, 0u, shm, red);
+        if (threadIdx.x == 0) {
+            sc->div_residual = red[0];
+            // max(|q|, |u_f| area_f / vol) (mrcm.cpp:432-437)
+            const double scale = fmax(fmax(red[3], __ddiv_rn(__dmul_rn(red[1], hy), vol)),
+                                      __ddiv_rn(__dmul_rn(red[2], hx), vol));
+            sc->div_scale = scale > 0.0 ? scale : 1.0;
+            if (cfl.on) {  // cfl_timestep's epilogue (transport.cpp:55-70), for the next step
+                const bool af = red[5] > 0.0;
+                const double dt = af ? fmin(cfl.dt_cap / cfl.safety, __ddiv_rn(vol, red[4])) : 0.0;
+                sc->any_next = af;
+                sc->dt_next = af ? fmin(cfl.safety * dt, cfl.dt_cap) : cfl.dt_cap;
+            }
+            *counter = 0;
+        }
+    }
+}
+
+// The boundary-face half of the downscale epilogue, over the 2(nx + ny)
+// exterior faces in BoundarySpec order: the next step's injection rate
+// (injection_rate, simulation.cpp:85-101; inflow faces, outward velocity < 0)
+// and the outlet probe (max_outlet_saturation, simulation.cpp:61-83: the
+// largest saturation behind an outflow face of a side whose net outflow is
+// positive). Slots: net W/E/S/N (sums), smax W/E/S/N, rate (sum).
+__global__ void __launch_bounds__(256) k_bnd_probe(Layout L, const double* __restrict__ u,
+                                                   const double* __restrict__ s_out, Scalars* sc, double* part,
+                                                   unsigned* counter, CflNext cfl) {
+    pdl_begin();
+    constexpr int NP = 9;
+    double net[4] = {0.0, 0.0, 0.0, 0.0}, smax[4] = {0.0, 0.0, 0.0, 0.0}, rate = 0.0;
+    const double hx = L.hx, hy = L.hy;
     double fin = 0.0;  // frac_flow(inflow) (transport.cpp:39-43), clamped, unrounded-FMA-free
     if (cfl.on) {
         const double si = cfl.inflow < 0.0 ? 0.0 : (cfl.inflow > 1.0 ? 1.0 : cfl.inflow);
         const double w = __dmul_rn(__dmul_rn(cfl.M, si), si), t = 1.0 - si;
         fin = __ddiv_rn(w, __dadd_rn(w, __dmul_rn(t, t)));
     }
-    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < L.cells(); c += gridDim.x * blockDim.x) {
-        const int i = c % L.nx, j = c / L.nx;
-        const int sx = i / L.snx, ii = i % L.snx, sy = j / L.sny, jj = j % L.sny;
-        const int s = sy * L.nsx + sx;
-        const size_t xo = (size_t)s * L.ncs;
-        const int r = jj * L.snx + ii;
-        const size_t eo = (size_t)s * L.nbe;
-        const int fW = L.vface(i, j), fE = L.vface(i + 1, j), fS = L.hface(i, j), fN = L.hface(i, j + 1);
-        const double uW = ii > 0 ? T[fW] * (Xd[xo + r - 1] - Xd[xo + r]) / L.hy : -EU[eo + jj];
-        double uE;
-        if (ii + 1 < L.snx) uE = T[fE] * (Xd[xo + r] - Xd[xo + r + 1]) / L.hy;
-        else if (i + 1 < L.nx) uE = -EU[eo + L.nbe + jj];  // west edge of the subdomain to the east
-        else uE = EU[eo + L.sny + jj];                    // east domain boundary
-        const double uS = jj > 0 ? T[fS] * (Xd[xo + r - L.snx] - Xd[xo + r]) / L.hx : -EU[eo + 2 * L.sny + ii];
-        double uN;
-        if (jj + 1 < L.sny) uN = T[fN] * (Xd[xo + r] - Xd[xo + r + L.snx]) / L.hx;
-        else if (j + 1 < L.ny) uN = -EU[(size_t)(s + L.nsx) * L.nbe + 2 * L.sny + ii];  // south edge of the one above
-        else uN = EU[eo + 2 * L.sny + L.snx + ii];                                         // north domain boundary
-        u[fW] = uW;
-        u[fS] = uS;
-        scale = fmax(scale, fabs(uW) * L.hy / vol);
-        scale = fmax(scale, fabs(uS) * L.hx / vol);
-        if (i == L.nx - 1) {
-            u[fE] = uE;
-            scale = fmax(scale, fabs(uE) * L.hy / vol);
+    const int nb = L.bfaces();
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
+        int side, c;
+        double ug, area;  // face velocity in global orientation
+        if (b < L.ny) {
+            side = 0, c = L.cell(0, b), ug = u[L.vface(0, b)], area = hy;
+        } else if (b < 2 * L.ny) {
+            side = 1, c = L.cell(L.nx - 1, b - L.ny), ug = u[L.vface(L.nx, b - L.ny)], area = hy;
+        } else if (b < 2 * L.ny + L.nx) {
+            side = 2, c = L.cell(b - 2 * L.ny, 0), ug = u[L.hface(b - 2 * L.ny, 0)], area = hx;
+        } else {
+            side = 3, c = L.cell(b - 2 * L.ny - L.nx, L.ny - 1), ug = u[L.hface(b - 2 * L.ny - L.nx, L.ny)], area = hx;
         }
-        if (j == L.ny - 1) {
-            u[fN] = uN;
-            scale = fmax(scale, fabs(uN) * L.hx / vol);
-        }
-        const double fx = (uE - uW) * L.hy;
-        const double fy = (uN - uS) * L.hx;
-        res = fmax(res, fabs((fx + fy) / vol - q[c]));
-        scale = fmax(scale, fabs(q[c]));
-        if (cfl.on) {  // k_cfl's per-cell outflux, same term order and rounding
-            double o = __dmul_rn(0.0 < uE ? uE : 0.0, L.hy);
-            o = __dadd_rn(o, __dmul_rn(0.0 < -uW ? -uW : 0.0, L.hy));
-            o = __dadd_rn(o, __dmul_rn(0.0 < uN ? uN : 0.0, L.hx));
-            o = __dadd_rn(o, __dmul_rn(0.0 < -uS ? -uS : 0.0, L.hx));
-            if (o > 0.0) {
-                anyf = 1.0;
-                best = fmin(best, __ddiv_rn(vol, __dmul_rn(o, slope)));
-            }
-            // injection_rate terms of the boundary faces (inflow: outward normal velocity < 0)
-            if (i == 0 && -uW < 0.0) rate = __dadd_rn(rate, __dmul_rn(__dmul_rn(uW, L.hy), fin));
-            if (i == L.nx - 1 && uE < 0.0) rate = __dadd_rn(rate, __dmul_rn(__dmul_rn(-uE, L.hy), fin));
-            if (j == 0 && -uS < 0.0) rate = __dadd_rn(rate, __dmul_rn(__dmul_rn(uS, L.hx), fin));
-            if (j == L.ny - 1 && uN < 0.0) rate = __dadd_rn(rate, __dmul_rn(__dmul_rn(-uN, L.hx), fin));
-        }
-        if (s_out) {  // outlet probe: outward flux of boundary faces, sides W, E, S, N
-            const double so = s_out[c];
-            if (i == 0) {
-                const double fo = -uW;
-                net[0] += fo * L.hy;
-                if (fo > 1e-14) smax[0] = fmax(smax[0], so);
-            }
-            if (i == L.nx - 1) {
-                const double fo = uE;
-                net[1] += fo * L.hy;
-                if (fo > 1e-14) smax[1] = fmax(smax[1], so);
-            }
-            if (j == 0) {
-                const double fo = -uS;
-                net[2] += fo * L.hx;
-                if (fo > 1e-14) smax[2] = fmax(smax[2], so);
-            }
-            if (j == L.ny - 1) {
-                const double fo = uN;
-                net[3] += fo * L.hx;
-                if (fo > 1e-14) smax[3] = fmax(smax[3], so);
-            }
+        const bool lo = side == 0 || side == 2;  // W / S: outward normal is -x / -y
+        const double fo = lo ? -ug : ug;         // outward normal velocity
+        if (cfl.on && fo < 0.0) rate = __dadd_rn(rate, __dmul_rn(__dmul_rn(lo ? ug : -ug, area), fin));
+        if (s_out) {
+            net[side] += fo * area;
+            if (fo > 1e-14) smax[side] = fmax(smax[side], s_out[c]);
         }
     }
     __shared__ double shm[32 * NP];
     __shared__ double red[NP];
-    constexpr unsigned SUMS = 0x103Cu;  // slots 2..5 (side nets) and 12 (rate) are sums, the rest maxima
-    double v[NP] = {res, scale, net[0], net[1], net[2], net[3], smax[0], smax[1], smax[2], smax[3], -best, anyf, rate};
+    constexpr unsigned SUMS = 0x10Fu;  // slots 0..3 (side nets) and 8 (rate) are sums, 4..7 maxima
+    double v[NP] = {net[0], net[1], net[2], net[3], smax[0], smax[1], smax[2], smax[3], rate};
     block_reduce_multi<NP>(v, SUMS, shm, red);
     if (threadIdx.x < NP) part[NP * blockIdx.x + threadIdx.x] = red[threadIdx.x];
     if (last_block_done(counter)) {
         double a[NP];
 #pragma unroll
-        for (int k = 0; k < NP; ++k) a[k] = k == 10 ? -INFINITY : 0.0;
+        for (int k = 0; k < NP; ++k) a[k] = 0.0;
         for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
 #pragma unroll
             for (int k = 0; k < NP; ++k) {
@@ -1344,19 +1415,13 @@ __global__ void k_ds_u_div(Layout L, const double* __restrict__ T, const double*
         }
         block_reduce_multi<NP>(a, SUMS, shm, red);
         if (threadIdx.x == 0) {
-            double om = 0.0;
-            for (int sd = 0; sd < 4; ++sd)
-                if (red[2 + sd] > 1e-14) om = fmax(om, red[6 + sd]);
-            sc->div_residual = red[0];
-            sc->div_scale = red[1] > 0.0 ? red[1] : 1.0;
-            if (s_out) sc->outlet_max = om;
-            if (cfl.on) {  // k_cfl's epilogue, for the next step
-                const double dt = fmin(cfl.dt_cap / cfl.safety, -red[10]);
-                const bool af = red[11] > 0.0;
-                sc->any_next = af;
-                sc->dt_next = af ? fmin(cfl.safety * dt, cfl.dt_cap) : cfl.dt_cap;
-                sc->inj_next = red[12];
+            if (s_out) {
+                double om = 0.0;
+                for (int sd = 0; sd < 4; ++sd)
+                    if (red[sd] > 1e-14) om = fmax(om, red[4 + sd]);
+                sc->outlet_max = om;
             }
+            if (cfl.on) sc->inj_next = red[8];
             *counter = 0;
         }
     }
@@ -1429,6 +1494,107 @@ __global__ void k_mpm_rhs(Layout L, int max_rhs, int anchor, const double* __res
     }
     if (anchor && r == 0) b = 0.0;
     X[xoff(L, max_rhs, s, 0) + r] = b;
+}
+
+// k_mpm_rhs split in two for many subdomains. k_mpm_edges: one thread per
+// subdomain boundary edge — the edge's w (outward, this subdomain's own:
+// tn (p^m - p^m_face) / area, mpm.cpp:73-75), its modified data g' / z' and
+// its term in the particular right-hand side (mpm.cpp:76-85,
+// elliptic.cpp:161-181) into WU, GZ and ET.
+__global__ void __launch_bounds__(256) k_mpm_edges(Layout L, const double* __restrict__ kn,
+                                                   const double* __restrict__ km, const int* __restrict__ bc_kind,
+                                                   const double* __restrict__ bc_value, const double* __restrict__ bm,
+                                                   const double* __restrict__ bp, const double* __restrict__ pm,
+                                                   const double* __restrict__ bpm, double* __restrict__ GZ,
+                                                   double* __restrict__ WU, double* __restrict__ ET) {
+    pdl_begin();
+    const int ne = L.n_sub * L.nbe;
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < ne; x += gridDim.x * blockDim.x) {
+        const int s = x / L.nbe, idx = x % L.nbe;
+        const EdgeInfo e = L.edge(s, idx);
+        const double kc = kn[e.global_cell], kmc = km[e.global_cell], pc = pm[e.global_cell], bpv = bpm[x];
+        const double wun = half_trans(L, e.side, kc) * (pc - bpv) / e.area;
+        const double th = half_trans(L, e.side, kmc);
+        WU[x] = wun;
+        double term;
+        if (e.iface >= 0) {
+            term = __dmul_rn(eff_robin(th, edge_beta(L, e, bm, bp), e.area), 0.0);
+            GZ[x] = 0.0;
+        } else if (bc_kind[e.gbc] == BC_PRESSURE) {
+            const double g = __dsub_rn(bc_value[e.gbc], bpv);
+            GZ[x] = g;
+            term = __dmul_rn(th, g);
+        } else if (bc_kind[e.gbc] == BC_ROBIN) {  // kept as restricted (mpm.cpp:80-81)
+            const double rr = L.rb_rhs[e.gbc];
+            GZ[x] = rr;
+            term = __dmul_rn(eff_robin(th, L.rb_beta[e.gbc], e.area), rr);
+        } else {
+            const double z = __dsub_rn(bc_value[e.gbc], wun);
+            GZ[x] = z;
+            term = -__dmul_rn(z, e.area);
+        }
+        ET[x] = term;
+    }
+}
+
+// ... and k_mpm_rhs_w: one thread per cell, warps over 32 consecutive cells
+// of a row, every load of the cell issued before its arithmetic. An interior
+// east face's w is the next lane's west face (shuffle); a subdomain-edge face
+// takes the edge's own w from k_mpm_edges (w is per subdomain). The
+// divergence and the right-hand side are unfused, as in the reference build;
+// the edge terms are added in W, E, S, N order (k_mpm_rhs's).
+__global__ void __launch_bounds__(256) k_mpm_rhs_w(Layout L, int max_rhs, int anchor,
+                                                   const double* __restrict__ Tn, const double* __restrict__ q,
+                                                   const double* __restrict__ pm, const double* __restrict__ WU,
+                                                   const double* __restrict__ ET, double* __restrict__ X) {
+    pdl_begin();
+    const int lane = threadIdx.x & 31;
+    const int ncell = L.cells();
+    const double vol = L.vol(), hx = L.hx, hy = L.hy;
+    for (int c0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31); c0 < ncell; c0 += gridDim.x * blockDim.x) {
+        const int c = c0 + lane;
+        const bool valid = c < ncell;
+        const int cc = valid ? c : ncell - 1;
+        const int i = cc % L.nx, j = cc / L.nx;
+        const int sx = i / L.snx, ii = i % L.snx, sy = j / L.sny, jj = j % L.sny;
+        const int s = sy * L.nsx + sx;
+        const int r = jj * L.snx + ii;
+        const size_t eo = (size_t)s * L.nbe;
+        const bool de = lane == 31 || i + 1 == L.nx || c + 1 >= ncell;
+        const bool hw = ii > 0, he = ii + 1 < L.snx, hs = jj > 0, hn = jj + 1 < L.sny;
+        const int eW = jj, eE = L.sny + jj, eS = 2 * L.sny + ii, eN = 2 * L.sny + L.snx + ii;
+        const double pc = pm[cc];
+        const double pw = hw ? pm[cc - 1] : 0.0;
+        const double tw = hw ? Tn[L.vface(i, j)] : 0.0;
+        const double pe = (de && he) ? pm[cc + 1] : 0.0;
+        const double te = (de && he) ? Tn[L.vface(i + 1, j)] : 0.0;
+        const double ps = hs ? pm[cc - L.nx] : 0.0;
+        const double ts = hs ? Tn[L.hface(i, j)] : 0.0;
+        const double pn = hn ? pm[cc + L.nx] : 0.0;
+        const double tn = hn ? Tn[L.hface(i, j + 1)] : 0.0;
+        const double qc = q[cc];
+        const double uw = hw ? 0.0 : WU[eo + eW], ue = he ? 0.0 : WU[eo + eE];
+        const double us = hs ? 0.0 : WU[eo + eS], un = hn ? 0.0 : WU[eo + eN];
+        const double xw = hw ? 0.0 : ET[eo + eW], xe = he ? 0.0 : ET[eo + eE];
+        const double xs = hs ? 0.0 : ET[eo + eS], xn = hn ? 0.0 : ET[eo + eN];
+        const double wW = hw ? tw * (pw - pc) / hy : -uw;
+        double wE = __shfl_down_sync(0xffffffffu, wW, 1);
+        if (!he) wE = ue;
+        else if (de) wE = te * (pc - pe) / hy;
+        if (!valid) continue;
+        const double wS = hs ? ts * (ps - pc) / hx : -us;
+        const double wN = hn ? tn * (pc - pn) / hx : un;
+        const double fx = __dmul_rn(__dsub_rn(wE, wW), hy);
+        const double fy = __dmul_rn(__dsub_rn(wN, wS), hx);
+        const double divw = __ddiv_rn(__dadd_rn(fx, fy), vol);
+        double b = __dmul_rn(__dsub_rn(qc, divw), vol);
+        if (!hw) b = __dadd_rn(b, xw);
+        if (!he) b = __dadd_rn(b, xe);
+        if (!hs) b = __dadd_rn(b, xs);
+        if (!hn) b = __dadd_rn(b, xn);
+        if (anchor && r == 0) b = 0.0;
+        X[xoff(L, max_rhs, s, 0) + r] = b;
+    }
 }
 
 // Particular solve with the cached rebuild factor (mrcm.cpp:248).
@@ -2005,7 +2171,15 @@ void downscale(Ctx& c, const double* kappa) {
         CflNext cfl;
         if (c.cfl_fused) cfl = CflNext{1, c.cfl_safety, c.cfl_dt_cap, c.cfl_inflow, c.M};
         launch_k(c, k_ds_u_div, red_blocks(c, k_ds_u_div, L.cells()), TPB, 0, L, c.T, c.Xd, c.GZ, c.u, c.q,
-                 c.sc.p, c.red.p, c.red_count.p, c.outlet_s, cfl);
+                 c.sc.p, c.red.p, c.red_count.p, cfl);
+        CK_LAUNCH();
+    }
+    if (c.cfl_fused || c.outlet_s) {
+        PROF(c, "k_bnd_probe");
+        CflNext cfl;
+        if (c.cfl_fused) cfl = CflNext{1, c.cfl_safety, c.cfl_dt_cap, c.cfl_inflow, c.M};
+        launch_k(c, k_bnd_probe, std::min(cdiv(L.bfaces(), TPB), 4 * c.num_sms), TPB, 0, L, c.u, c.outlet_s,
+                 c.sc.p, c.red.p, c.red_count.p, cfl);
         CK_LAUNCH();
     }
     c.c_down += L.n_sub;
@@ -2192,7 +2366,14 @@ void launch_mpm(Ctx& c, const double* kn) {  // mpm_pressure_update (mpm.cpp:31-
     ds_factor_fork(c);  // downscale operator of kappa_n, concurrent with the particular / interface chain
     {
         PROF(c, "k_mpm_rhs");
-        if (c.rhs_sub && L.ncs <= RHS_TPB * RHS_CPT)
+        if (c.rhs_w) {
+            launch_k(c, k_mpm_edges, std::min(grid_for((long long)L.n_sub * L.nbe), 8 * c.num_sms), TPB, 0, L, kn,
+                     c.kappa_m, c.bc_kind, c.bc_value, c.beta_m, c.beta_p, c.pm, c.bpm, c.GZ, c.WU, c.ET);
+            CK_LAUNCH();
+            launch_k(c, k_mpm_rhs_w, std::min(grid_for(L.cells()), 8 * c.num_sms), TPB, 0, L, c.max_rhs,
+                     c.anchor_m ? 1 : 0, c.T, c.q, c.pm, c.WU, c.ET, c.X);
+        }
+        else if (c.rhs_sub && L.ncs <= RHS_TPB * RHS_CPT)
             launch_k(c, k_mpm_rhs_sub, L.n_sub, RHS_TPB, (size_t)(L.ncs + 2 * L.nbe) * sizeof(double), L, c.max_rhs,
                      c.anchor_m ? 1 : 0, kn, c.kappa_m, c.T, c.q, c.bc_kind, c.bc_value, c.beta_m, c.beta_p, c.pm,
                      c.bpm, c.X, c.GZ, c.WU);

@@ -512,10 +512,27 @@ def test_separable_repair_parity(oracle, nx, ny, nsx, nsy):
 def test_mpm_rhs_per_subdomain_bitwise():
     """k_mpm_rhs_sub (one CTA per subdomain) is bit-identical to one thread per cell."""
     c = configs.build("C2", te_override=31)
-    a = _sim_env(c.problem, MPM2P_RHS_SUB=1).run(c.split, c.s0())
-    b = _sim_env(c.problem, MPM2P_RHS_SUB=0).run(c.split, c.s0())
+    a = _sim_env(c.problem, MPM2P_RHS_W=0, MPM2P_RHS_SUB=1).run(c.split, c.s0())
+    b = _sim_env(c.problem, MPM2P_RHS_W=0, MPM2P_RHS_SUB=0).run(c.split, c.s0())
     assert np.array_equal(a.s_final, b.s_final) and np.array_equal(a.u_final, b.u_final)
     assert np.array_equal(a.p_final, b.p_final)
+
+
+@pytest.mark.parametrize("nx,ny,sx,sy", [(62, 45, 2, 3), (93, 130, 3, 5), (300, 20, 10, 1), (40, 96, 2, 4)])
+def test_mpm_rhs_cell_ragged(oracle, nx, ny, sx, sy):
+    """k_mpm_rhs_w (one thread per cell, east faces by shuffle inside a
+    subdomain, each subdomain's own w on its edges) on ragged grids: the
+    MPM-2P update matches the oracle and the per-subdomain kernel."""
+    K = random_kappa(nx, ny, 13, 0.1, 10.0)
+    for bc in (api.pressure_drop(nx, ny), api.unit_inflow(nx, ny)):
+        prob = problem(nx, ny, sx, sy, K, bc=bc)
+        a, b, o = _sim_env(prob, MPM2P_RHS_W=1), _sim_env(prob, MPM2P_RHS_W=0), api.Simulator(prob, oracle)
+        for sim in (a, b, o):
+            sim.mrcm_solve(K)
+        kn = K * np.exp(0.1 * np.random.default_rng(2).standard_normal(K.size))
+        ma, mb, mo = a.mpm_pressure_update(kn), b.mpm_pressure_update(kn), o.mpm_pressure_update(kn)
+        assert rel_l2(ma.u, mo.u) < TOL_PU and rel_l2(ma.p, mo.p) < TOL_PU
+        assert rel_l2(ma.u, mb.u) < 1e-12
 
 
 @pytest.mark.parametrize("nx,nsx", [(64, 4), (96, 4), (64, 2), (128, 4)])
@@ -540,3 +557,30 @@ def test_blocked_dmma_downscale_parity(oracle, nx, nsx):
     assert [s["rebuilt"] for s in ra.record.steps] == [s["rebuilt"] for s in rr.record.steps]
     assert np.max(np.abs(ra.s_final - rr.s_final)) <= TOL_S
     assert rel_l2(ra.u_final, rr.u_final) <= TOL_PU and rel_l2(ra.p_final, rr.p_final) <= TOL_PU
+
+
+
+@pytest.mark.parametrize("nx,ny,sx,sy", [(62, 45, 2, 3), (93, 130, 3, 5), (300, 20, 10, 1), (40, 96, 2, 4),
+                                         (64, 64, 2, 2)])
+def test_velocity_scatter_ragged(oracle, nx, ny, sx, sy):
+    """k_ds_u_div on ragged grids (rows that end inside a warp, subdomain
+    widths that do not divide 32): east faces by shuffle, the maxima's and
+    the CFL's divisions hoisted out of the reductions. MRCM and MPM-2P
+    velocities match the oracle to the parity bar, the downscale diagnostics
+    to roundoff, and the fused next-step CFL dt of a run equals
+    cfl_timestep (transport kernel) of the run's velocity bitwise."""
+    K = random_kappa(nx, ny, 3, 0.1, 10.0)
+    prob = problem(nx, ny, sx, sy, K)
+    g, o = api.Simulator(prob), api.Simulator(prob, oracle)
+    sg, so = g.mrcm_solve(K), o.mrcm_solve(K)
+    assert rel_l2(sg.u, so.u) < TOL_PU
+    assert abs(sg.info.div_scale - so.info.div_scale) <= 1e-12 * so.info.div_scale
+    assert sg.info.div_residual <= 1e-10 * sg.info.div_scale
+    mg, mo = g.mpm_pressure_update(K * 1.05), o.mpm_pressure_update(K * 1.05)
+    assert rel_l2(mg.u, mo.u) < TOL_PU
+    sp = api.SplittingConfig(method=api.MPM2P, eta=0.01, te=2, cfl_safety=0.7)
+    r = g.run(sp)
+    g2 = api.Simulator(prob)
+    g2.run_begin(sp)
+    s_, p_, u_ = g2.run_read()
+    assert r.record.steps[1]["dt"] == g2.cfl_timestep(u_, 0.7, 1.0)
