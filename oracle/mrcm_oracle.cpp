@@ -1406,6 +1406,10 @@ void Runner::note(Real dres, Real dscale, bool warn) {  // simulation.cpp:176-18
 
 void Runner::rebuild(const Vec& kappa) {  // simulation.cpp:183-193
     const RobinParameter beta = compute_beta(kappa, *in_.dd, in_.alpha);
+    // the old basis is not needed by the new one: release it first, so the
+    // peak footprint is one basis (C5 in long double: ~35 GB) instead of two
+    state_.basis.reset();
+    state_.recon_m.clear();
     GlobalSolution sol = mrcm_solve(kappa, in_.dd, in_.space, beta, q_, in_.bc, rec_.counters);
     state_.basis = sol.basis;
     state_.recon_m = std::move(sol.recon);

@@ -112,22 +112,162 @@ __global__ void k_flag_err(const int* flag, Scalars* sc, unsigned bit) {
 }
 
 // y (block order) <- J rhs gathered: y[off[blk[r]] + loc[r]] = (J rhs)_r
+// (transposed = 0) y = J rhs, (1) y = rhs, in block order
 __global__ void k_bt_gather(const double* __restrict__ rhs, int n, const int* __restrict__ blk,
-                            const int* __restrict__ loc, const int* __restrict__ voff, double* __restrict__ y) {
+                            const int* __restrict__ loc, const int* __restrict__ voff, double* __restrict__ y,
+                            int transposed) {
     pdl_begin();
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n) return;
     const int h = n / 2;
-    const double v = r < h ? rhs[h + r] : -rhs[r - h];
+    const double v = transposed ? rhs[r] : (r < h ? rhs[h + r] : -rhs[r - h]);
     y[voff[blk[r]] + loc[r]] = v;
 }
 
+// (transposed = 0) x = xb, (1) x = J^T xb, from block order
 __global__ void k_bt_unpermute(const double* __restrict__ xb, int n, const int* __restrict__ blk,
-                               const int* __restrict__ loc, const int* __restrict__ voff, double* __restrict__ x) {
+                               const int* __restrict__ loc, const int* __restrict__ voff, double* __restrict__ x,
+                               int transposed) {
     pdl_begin();
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n) return;
-    x[r] = xb[voff[blk[r]] + loc[r]];
+    const int h = n / 2;
+    if (!transposed) {
+        x[r] = xb[voff[blk[r]] + loc[r]];
+    } else {  // (J^T w)_i = -w_{i+h} (i < h), w_{i-h} (i >= h)
+        const int q = r < h ? r + h : r - h;
+        const double w = xb[voff[blk[q]] + loc[q]];
+        x[r] = r < h ? -w : w;
+    }
+}
+
+// ---- 1-norm condition estimate of the interface matrix M (the reference's
+// rcond() guard, mrcm.cpp:227-238; Hager 1984 / Higham 1988 as the oracle's
+// hager_rcond): at most five rounds of y = M^-1 x, xi = sign(y),
+// z = M^-T xi, x = e_argmax|z|. Every round's kernels are always launched
+// (graph-capturable); a device flag freezes the state once the estimate has
+// converged. M^-T v = J^T K^-1 v (K = J M symmetric).
+struct HagerState {
+    double est, anorm;
+    int done;
+};
+
+// ||M||_1 = max column sum of |M|: column j's entries are row j's transposed
+// positions (the CSR pattern is structurally symmetric)
+__global__ void __launch_bounds__(1024) k_hager_init(const int* __restrict__ ptr, const int* __restrict__ tpos,
+                                                     const double* __restrict__ val, int n, double* __restrict__ x,
+                                                     HagerState* st) {
+    __shared__ double sh[32];
+    double m = 0.0;
+    for (int jc = threadIdx.x; jc < n; jc += blockDim.x) {
+        double s = 0.0;
+        for (int z = ptr[jc]; z < ptr[jc + 1]; ++z) s += fabs(val[tpos[z]]);
+        m = fmax(m, s);
+        x[jc] = 1.0 / n;
+    }
+    m = warp_max(m);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        m = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
+        m = warp_max(m);
+        if (threadIdx.x == 0) {
+            st->anorm = m;
+            st->est = 0.0;
+            st->done = 0;
+        }
+    }
+}
+
+// round `it`, after y = M^-1 x: ny = ||y||_1; stop if it does not grow; else xi = sign(y)
+__global__ void __launch_bounds__(1024) k_hager_a(const double* __restrict__ y, int n, int it,
+                                                  double* __restrict__ xi, HagerState* st) {
+    __shared__ double sh[32];
+    __shared__ int stop;
+    if (st->done) return;
+    double a = 0.0;
+    for (int r = threadIdx.x; r < n; r += blockDim.x) a += fabs(y[r]);
+    a = warp_sum(a);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = a;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double ny = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) ny += sh[w];
+        int sp = 0;
+        if (!isfinite(ny)) {
+            st->est = 0.0;
+            sp = 1;
+        } else if (it > 0 && ny <= st->est) {
+            sp = 1;
+        } else {
+            st->est = ny;
+        }
+        st->done = sp;
+        stop = sp;
+    }
+    __syncthreads();
+    if (stop) return;
+    for (int r = threadIdx.x; r < n; r += blockDim.x) xi[r] = y[r] >= 0.0 ? 1.0 : -1.0;
+}
+
+// after z = M^-T xi: j = first argmax |z|; stop if |z_j| <= z.x; else x = e_j
+__global__ void __launch_bounds__(1024) k_hager_b(const double* __restrict__ z, int n, double* __restrict__ x,
+                                                  HagerState* st) {
+    __shared__ double shv[32], shz[32];
+    __shared__ int shi[32];
+    __shared__ int stop, jbest;
+    if (st->done) return;
+    double zm = -1.0, ztx = 0.0;
+    int jm = 0x7fffffff;
+    for (int r = threadIdx.x; r < n; r += blockDim.x) {
+        const double a = fabs(z[r]);
+        ztx += z[r] * x[r];
+        if (a > zm) {
+            zm = a;
+            jm = r;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const double v2 = __shfl_down_sync(0xffffffffu, zm, o);
+        const int j2 = __shfl_down_sync(0xffffffffu, jm, o);
+        if (v2 > zm || (v2 == zm && j2 < jm)) {
+            zm = v2;
+            jm = j2;
+        }
+        ztx += __shfl_down_sync(0xffffffffu, ztx, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        shv[threadIdx.x >> 5] = zm;
+        shi[threadIdx.x >> 5] = jm;
+        shz[threadIdx.x >> 5] = ztx;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double bv = -1.0, t = 0.0;
+        int bj = 0x7fffffff;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            if (shv[w] > bv || (shv[w] == bv && shi[w] < bj)) {
+                bv = shv[w];
+                bj = shi[w];
+            }
+            t += shz[w];
+        }
+        const int sp = bv <= t;
+        st->done = sp;
+        stop = sp;
+        jbest = bj;
+    }
+    __syncthreads();
+    if (stop) return;
+    for (int r = threadIdx.x; r < n; r += blockDim.x) x[r] = r == jbest ? 1.0 : 0.0;
+}
+
+// rcond = 1 / (||M||_1 est); the reference's guard rcond > 1e-14
+__global__ void k_hager_fin(HagerState* st, Scalars* sc, double threshold, unsigned bit) {
+    const double est = st->est, an = st->anorm;
+    const double rc = (est > 0.0 && an > 0.0) ? 1.0 / an / est : 0.0;
+    sc->rcond = rc;
+    if (!(rc > threshold)) atomicOr(&sc->err, bit);
 }
 
 // The block steps of a solve are a dependent chain of small products, each
@@ -267,6 +407,11 @@ void bt_setup(Ctx& c) {
     c.bt_y.alloc(n);
     c.bt_x.alloc(n);
     c.bt_sy.alloc(n);
+    c.hg_x.alloc(n);
+    c.hg_y.alloc(n);
+    c.hg_z.alloc(n);
+    c.hg_xi.alloc(n);
+    c.hg_state.alloc(sizeof(HagerState) / sizeof(double) + 1);
     CK(cudaStreamSynchronize(c.st));
 }
 
@@ -318,14 +463,14 @@ void bt_factor(Ctx& c) {
     }
 }
 
-// x = M^-1 rhs through K x = J rhs.
-void bt_solve(Ctx& c, const double* rhs, double* x) {
+// x = M^-1 rhs through K x = J rhs (transposed: x = M^-T rhs = J^T K^-1 rhs).
+void bt_solve_t(Ctx& c, const double* rhs, double* x, int transposed) {
     const int n = c.dim, nb = c.bt_nblk;
     double* y = c.bt_y.p;
     double* xb = c.bt_x.p;
     {
         PROF(c, "k_bt_gather");
-        launch_k(c, k_bt_gather, cdiv(n, TPB), TPB, 0, rhs, n, c.bt_blk, c.bt_loc, c.bt_voffd, y);
+        launch_k(c, k_bt_gather, cdiv(n, TPB), TPB, 0, rhs, n, c.bt_blk, c.bt_loc, c.bt_voffd, y, transposed);
         CK_LAUNCH();
     }
     // block steps with programmatic dependent launch (see k_bt_fwd)
@@ -361,7 +506,41 @@ void bt_solve(Ctx& c, const double* rhs, double* x) {
     }
     {
         PROF(c, "k_bt_unpermute");
-        launch_k(c, k_bt_unpermute, cdiv(n, TPB), TPB, 0, xb, n, c.bt_blk, c.bt_loc, c.bt_voffd, x);
+        launch_k(c, k_bt_unpermute, cdiv(n, TPB), TPB, 0, xb, n, c.bt_blk, c.bt_loc, c.bt_voffd, x, transposed);
+        CK_LAUNCH();
+    }
+}
+
+void bt_solve(Ctx& c, const double* rhs, double* x) { bt_solve_t(c, rhs, x, 0); }
+
+// The rcond guard of the block-tridiagonal path (each rebuild, after bt_factor):
+// the oracle's Hager/Higham estimate with device solves; sets sc->rcond and
+// ERR_SINGULAR when !(rcond > threshold).
+void bt_rcond(Ctx& c, double threshold, unsigned err_bit) {
+    const int n = c.dim;
+    HagerState* st = reinterpret_cast<HagerState*>(c.hg_state.p);
+    {
+        PROF(c, "k_hager");
+        launch_k(c, k_hager_init, 1, 1024, 0, c.csr_ptr.p, c.csr_tpos.p, c.csr_val.p, n, c.hg_x.p, st);
+        CK_LAUNCH();
+    }
+    for (int it = 0; it < 5; ++it) {
+        bt_solve_t(c, c.hg_x, c.hg_y, 0);
+        {
+            PROF(c, "k_hager");
+            launch_k(c, k_hager_a, 1, 1024, 0, (const double*)c.hg_y.p, n, it, c.hg_xi.p, st);
+            CK_LAUNCH();
+        }
+        bt_solve_t(c, c.hg_xi, c.hg_z, 1);
+        {
+            PROF(c, "k_hager");
+            launch_k(c, k_hager_b, 1, 1024, 0, (const double*)c.hg_z.p, n, c.hg_x.p, st);
+            CK_LAUNCH();
+        }
+    }
+    {
+        PROF(c, "k_hager");
+        launch_k(c, k_hager_fin, 1, 1, 0, st, c.sc.p, threshold, err_bit);
         CK_LAUNCH();
     }
 }

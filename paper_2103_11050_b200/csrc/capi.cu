@@ -491,8 +491,9 @@ mpm2p_step_record make_record(const Ctx& c, const Driver& d, const Scalars& s, i
 // field (rcond 4e-10). C1/C2/C4 (rcond >= 2e-7) pass the 1e-8 parity bar with
 // no refinement at all (MPM2P_REFINE=0).
 void note_rcond(Ctx& c, Driver& d, double rcond) {
-    if (c.use_krylov || c.use_blocktri || c.dim == 0) return;
+    if (c.use_krylov || c.dim == 0) return;
     if (d.min_rcond < 0.0 || rcond < d.min_rcond) d.min_rcond = rcond;
+    if (c.use_blocktri) return;  // direct block solves: no refinement step
     c.refine = !c.never_refine && (c.force_refine || !(rcond > c.refine_rcond));
 }
 

@@ -116,6 +116,7 @@ struct Ctx {
     DevBuf<int> bt_blk, bt_loc, bt_bsz, bt_voffd;
     DevBuf<long long> bt_doffd, bt_eoffd;
     DevBuf<double> bt_D, bt_E, bt_Sinv, bt_T, bt_G, bt_y, bt_x, bt_sy;
+    DevBuf<double> hg_x, hg_y, hg_z, hg_xi, hg_state;  // rcond estimate (bt_rcond)
     // per-solve scratch
     DevBuf<double> X, PU, PB, PS, GZ, WU, ET, RU, RS, skel, resid, delta, corr;
     // downscale
@@ -360,5 +361,6 @@ void krylov_solve(Ctx& c, const double* rhs, double* x);      // x = M^-1 rhs
 void bt_setup(Ctx& c);                                    // block layout and buffers (once)
 void bt_factor(Ctx& c);                                   // block LDL^T with explicit S_j^-1 (each rebuild)
 void bt_solve(Ctx& c, const double* rhs, double* x);      // x = M^-1 rhs
+void bt_rcond(Ctx& c, double threshold, unsigned err_bit);  // Hager/Higham rcond guard (each rebuild)
 
 }  // namespace mpm2p

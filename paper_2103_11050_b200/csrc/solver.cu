@@ -2318,9 +2318,12 @@ void launch_rebuild(Ctx& c, const double* kappa, bool compute_beta) {  // comput
             // non-convergence (ERR_SINGULAR raised by k_minres)
             krylov_prepare(c);
         } else if (c.use_blocktri) {
-            // block LDL^T; a zero / non-finite pivot in any block raises ERR_SINGULAR
+            // block LDL^T; a zero / non-finite pivot in any block raises
+            // ERR_SINGULAR, and so does the reference's rcond guard
+            // (mrcm.cpp:227-238), estimated with the block solves
             krylov_prepare(c);
             bt_factor(c);
+            bt_rcond(c, 1e-14, ERR_SINGULAR);
         } else if (!interface_inverse_csr(c, &c.sc.p->rcond, ERR_SINGULAR, 1e-14)) {
             // non-symmetric fallback through a dense copy of M
             c.Mdense.alloc((size_t)c.dim * c.dim);

@@ -5,6 +5,8 @@ relative L2 <= 1e-8; saturation max-abs <= 1e-8 after the full run.
 Transport and beta are checked bitwise (the kernels keep the reference's
 operation order under --fmad=false).
 """
+import dataclasses
+
 import numpy as np
 import pytest
 
@@ -373,6 +375,33 @@ def test_blocktri_interface_parity(oracle, nsx, nsy, space, hbar, contrast):
     kn = K * np.exp(0.05 * np.random.default_rng(3).standard_normal(K.size))
     mg, mo = g.mpm_pressure_update(kn), o.mpm_pressure_update(kn)
     assert rel_l2(mg.p, mo.p) <= 1e-10 and rel_l2(mg.u, mo.u) <= 1e-10
+
+
+@pytest.mark.parametrize("name", ["C1", "C3"])
+def test_blocktri_rcond_estimate(name):
+    """The block-tridiagonal path's rcond guard (Hager/Higham with the block
+    solves, as the oracle's banded path) against the dense path's exact
+    1 / (||M||_1 ||M^-1||_1): the estimate of ||M^-1||_1 is a lower bound that
+    is rarely off by more than a small factor."""
+    c = configs.build(name, te_override=3)
+    sp = dataclasses.replace(c.split, stop_on_breakthrough=False)
+    rb = _sim_iface(c.problem, "blocktri").run(sp, c.s0(), c.inflow_sat)
+    rd = _sim_iface(c.problem, "dense").run(sp, c.s0(), c.inflow_sat)
+    exact, est = rd.record.min_rcond, rb.record.min_rcond
+    assert rb.record.interface_krylov == 2 and exact > 0
+    assert exact * (1 - 1e-9) <= est <= 10 * exact, (est, exact)
+
+
+def test_blocktri_rcond_guard_raises():
+    """Pure-flux data on several subdomains: the interface matrix is singular
+    (constant null space). The block path now raises the reference's
+    NumericError (mrcm.cpp:227-238) instead of returning garbage."""
+    nx = ny = 32
+    K = random_kappa(nx, ny, 5, 0.1, 10.0)
+    bc = api.BoundarySpec.uniform(nx, ny, (api.FLUX, -1.0), (api.FLUX, 1.0), (api.FLUX, 0.0), (api.FLUX, 0.0))
+    g = _sim_iface(problem(nx, ny, 4, 4, K, bc=bc), "blocktri")
+    with pytest.raises(api.NumericError):
+        g.mrcm_solve(K)
 
 
 def test_blocktri_matches_dense_c2_sample():
