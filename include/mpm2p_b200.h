@@ -154,6 +154,7 @@ typedef struct mpm2p_sizes {
     int32_t dim_flux, dim_pressure;
     int64_t nhat;             /* homogeneous solves per rebuild (BasisSet::nhat) */
     int32_t sub_nx, sub_ny;
+    int32_t sub_faces;        /* local faces per subdomain: (sub_nx+1) sub_ny + sub_nx (sub_ny+1) */
 } mpm2p_sizes;
 
 typedef struct mpm2p_ctx mpm2p_ctx;
@@ -222,6 +223,51 @@ int mpm2p_mpm_update(mpm2p_ctx* ctx, const double* kappa_n, double* p, double* u
                      double* delta_coeffs, mpm2p_downscale_info* info, mpm2p_counters* counters);
 /* BasisSet::iface_matrix (mrcm.hpp:68), dense dim x dim row-major. */
 int mpm2p_interface_matrix(mpm2p_ctx* ctx, double* M);
+
+/* ---- MRCM sub-steps (mrcm.hpp:77-136, 157-161) ---------------------------
+ * Per-subdomain layouts (subdomain-major, s = sy*nsx + sx):
+ *   cells     [n_sub][sub_nx*sub_ny]  local row-major r = jj*sub_nx + ii
+ *   faces     [n_sub][sub_faces]      local faces: vertical (sub_nx+1)*sub_ny,
+ *                                     then horizontal; global orientation
+ *   edges     [n_sub][2(sub_nx+sub_ny)] boundary edges W, E, S, N (the local
+ *                                     BoundarySpec order, elliptic.hpp:30-44)
+ * LocalData = (q cells, edge kind / value / beta / robin_rhs);
+ * LocalSolution = (p cells, u faces, boundary_p edges). */
+
+/* std::shared_ptr<BasisSet> compute_basis_set(kappa, dd, space, beta, q, bc, counters)
+ *                                                       mrcm.hpp:77-81
+ * Factors every subdomain operator, solves the homogeneous and particular
+ * problems, assembles and factors the interface matrix (rcond guard), and
+ * installs the result as the context's basis. beta_minus/beta_plus NULL =>
+ * compute_beta(kappa) with the problem's AlphaSpec. */
+int mpm2p_compute_basis_set(mpm2p_ctx* ctx, const double* kappa, const double* beta_minus,
+                            const double* beta_plus, mpm2p_counters* counters);
+/* std::vector<LocalData> restrict_physical_data(dd, beta, q, bc)   mrcm.hpp:85-87
+ * With the installed basis's beta. */
+int mpm2p_restrict_physical_data(mpm2p_ctx* ctx, double* q_local, int32_t* kind_local, double* value_local,
+                                 double* beta_local, double* robin_rhs_local);
+/* ParticularSolution solve_particular(basis, data, counters)        mrcm.hpp:91-92
+ * NumericError if the edges' kinds / betas differ from the factorization's. */
+int mpm2p_solve_particular(mpm2p_ctx* ctx, const double* q_local, const int32_t* kind_local,
+                           const double* value_local, const double* beta_local, const double* robin_rhs_local,
+                           double* p_local, double* u_local, double* bp_local, mpm2p_counters* counters);
+/* SkeletonCoeffs solve_interface(basis, particular, counters)       mrcm.hpp:95-96
+ * u_local: the particular solution's face velocities. coeffs: U_H then P_H. */
+int mpm2p_solve_interface(mpm2p_ctx* ctx, const double* u_local, double* coeffs, mpm2p_counters* counters);
+/* MrcmReconstruction reconstruct(basis, coeffs, particular)         mrcm.hpp:100-101 */
+int mpm2p_reconstruct(mpm2p_ctx* ctx, const double* coeffs, const double* p_local, const double* u_local,
+                      const double* bp_local, double* p_out, double* u_out, double* bp_out);
+/* std::vector<std::vector<double>> averaged_skeleton_flux(dd, recon) mrcm.hpp:105-106
+ * flux per skeleton edge, interface-major (vertical interfaces first). */
+int mpm2p_averaged_skeleton_flux(mpm2p_ctx* ctx, const double* u_local, double* flux);
+/* DownscaleResult downscale(dd, kappa_current, q, bc, recon, skeleton_flux, counters)
+ *                                                       mrcm.hpp:122-126 */
+int mpm2p_downscale(mpm2p_ctx* ctx, const double* kappa, const double* p_local, const double* u_local,
+                    const double* flux, double* p, double* u, mpm2p_downscale_info* info,
+                    mpm2p_counters* counters);
+/* WeakResiduals weak_continuity_residuals(basis, recon)             mrcm.hpp:157-161 */
+int mpm2p_weak_continuity_residuals(mpm2p_ctx* ctx, const double* u_local, const double* bp_local, double* flux_jump,
+                         double* pressure_jump);
 
 /* ---- the driver (simulation.cpp:118-340) ------------------------------- */
 /* RunResult run(in, snapshot_steps, snap)          simulation.hpp:127-128

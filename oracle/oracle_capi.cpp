@@ -233,6 +233,8 @@ int oracle_get_sizes(const oracle_ctx* ctx, mpm2p_sizes* o) {
     o->nhat = nhat;
     o->sub_nx = dd.subs[0].nx;
     o->sub_ny = dd.subs[0].ny;
+    const Grid& lg0 = dd.subgrids[0];
+    o->sub_faces = lg0.faces();
     return MPM2P_OK;
 }
 
@@ -436,6 +438,156 @@ int oracle_gaussian_field(int32_t nx, int32_t ny, double lx, double ly, double d
     return guarded(nullptr, [&] {
         const Grid g = build_grid(nx, ny, lx, ly);
         copy_out(out, gaussian_field(g, delta, mean_coeff, seed, range_norm != 0, range_target));
+    });
+}
+
+// ---- MRCM sub-steps (mrcm.hpp:77-136) over the per-subdomain C-ABI layouts
+namespace {
+std::vector<LocalSolution> locals_in(const oracle_ctx* ctx, const double* p, const double* u, const double* bp) {
+    const Decomp& dd = *ctx->dd;
+    std::vector<LocalSolution> out(dd.n_sub());
+    size_t oc = 0, of = 0, oe = 0;
+    for (int s = 0; s < dd.n_sub(); ++s) {
+        const Grid& lg = dd.subgrids[s];
+        const size_t ne = dd.sub_boundary[s].size();
+        out[s].p = p ? Vec(p + oc, p + oc + lg.cells()) : Vec(lg.cells(), 0.0);
+        out[s].u = u ? Vec(u + of, u + of + lg.faces()) : Vec(lg.faces(), 0.0);
+        out[s].boundary_p = bp ? Vec(bp + oe, bp + oe + ne) : Vec(ne, 0.0);
+        oc += lg.cells(), of += lg.faces(), oe += ne;
+    }
+    return out;
+}
+void locals_out(const std::vector<LocalSolution>& v, double* p, double* u, double* bp) {
+    size_t oc = 0, of = 0, oe = 0;
+    for (const auto& l : v) {
+        if (p) copy_out(p + oc, l.p);
+        if (u) copy_out(u + of, l.u);
+        if (bp) copy_out(bp + oe, l.boundary_p);
+        oc += l.p.size(), of += l.u.size(), oe += l.boundary_p.size();
+    }
+}
+}  // namespace
+
+int oracle_compute_basis_set(oracle_ctx* ctx, const double* kappa, const double* bm, const double* bp,
+                             mpm2p_counters* counters) {
+    return guarded(ctx, [&] {
+        const int n = ctx->dd->grid.cells();
+        const Vec k(kappa, kappa + n);
+        const RobinParameter rp = beta_from(ctx, k, bm, bp);
+        SolveCounters c;
+        ctx->state.basis.reset();
+        ctx->state.recon_m.clear();
+        ctx->state.basis = compute_basis_set(k, ctx->dd, ctx->space, rp, ctx->q, ctx->bc, c);
+        fill_counters(counters, c);
+    });
+}
+
+int oracle_restrict_physical_data(oracle_ctx* ctx, double* q_local, int32_t* kind, double* val, double* beta,
+                                  double* rhs) {
+    return guarded(ctx, [&] {
+        if (!ctx->state.basis) throw ConfigError("restrict_physical_data: no basis installed");
+        const auto data = restrict_physical_data(*ctx->dd, ctx->state.basis->beta, ctx->q, ctx->bc);
+        size_t oc = 0, oe = 0;
+        for (const auto& d : data) {
+            if (q_local) copy_out(q_local + oc, d.q);
+            for (const auto& f : d.bc.faces) {
+                if (kind) kind[oe] = f.kind;
+                if (val) val[oe] = (double)f.value;
+                if (beta) beta[oe] = (double)f.beta;
+                if (rhs) rhs[oe] = (double)f.robin_rhs;
+                ++oe;
+            }
+            oc += d.q.size();
+        }
+    });
+}
+
+int oracle_solve_particular(oracle_ctx* ctx, const double* q_local, const int32_t* kind, const double* val,
+                            const double* beta, const double* rhs, double* p, double* u, double* bp,
+                            mpm2p_counters* counters) {
+    return guarded(ctx, [&] {
+        if (!ctx->state.basis) throw ConfigError("solve_particular: no basis installed");
+        const Decomp& dd = *ctx->dd;
+        std::vector<LocalData> data(dd.n_sub());
+        size_t oc = 0, oe = 0;
+        for (int s = 0; s < dd.n_sub(); ++s) {
+            const Grid& lg = dd.subgrids[s];
+            data[s].q = Vec(q_local + oc, q_local + oc + lg.cells());
+            data[s].bc = BoundarySpec(lg.nx, lg.ny);
+            for (auto& f : data[s].bc.faces) {
+                f.kind = kind[oe];
+                f.value = val[oe];
+                f.beta = beta[oe];
+                f.robin_rhs = rhs[oe];
+                ++oe;
+            }
+            oc += lg.cells();
+        }
+        SolveCounters c;
+        locals_out(solve_particular(*ctx->state.basis, data, c), p, u, bp);
+        fill_counters(counters, c);
+    });
+}
+
+int oracle_solve_interface(oracle_ctx* ctx, const double* u_local, double* coeffs, mpm2p_counters* counters) {
+    return guarded(ctx, [&] {
+        if (!ctx->state.basis) throw ConfigError("solve_interface: no basis installed");
+        SolveCounters c;
+        const SkeletonCoeffs co = solve_interface(*ctx->state.basis, locals_in(ctx, nullptr, u_local, nullptr), c);
+        if (coeffs) {
+            copy_out(coeffs, co.flux);
+            copy_out(coeffs + co.flux.size(), co.pres);
+        }
+        fill_counters(counters, c);
+    });
+}
+
+int oracle_reconstruct(oracle_ctx* ctx, const double* coeffs, const double* p, const double* u, const double* bp,
+                       double* po, double* uo, double* bpo) {
+    return guarded(ctx, [&] {
+        if (!ctx->state.basis) throw ConfigError("reconstruct: no basis installed");
+        const BasisSet& b = *ctx->state.basis;
+        SkeletonCoeffs co;
+        co.flux = Vec(coeffs, coeffs + b.n_flux);
+        co.pres = Vec(coeffs + b.n_flux, coeffs + b.n_flux + b.n_pres);
+        locals_out(reconstruct(b, co, locals_in(ctx, p, u, bp)), po, uo, bpo);
+    });
+}
+
+int oracle_averaged_skeleton_flux(oracle_ctx* ctx, const double* u_local, double* flux) {
+    return guarded(ctx, [&] {
+        copy_out(flux, flatten(averaged_skeleton_flux(*ctx->dd, locals_in(ctx, nullptr, u_local, nullptr))));
+    });
+}
+
+int oracle_downscale(oracle_ctx* ctx, const double* kappa, const double* p_local, const double* u_local,
+                     const double* flux, double* p, double* u, mpm2p_downscale_info* info, mpm2p_counters* counters) {
+    return guarded(ctx, [&] {
+        const Decomp& dd = *ctx->dd;
+        std::vector<Vec> skel(dd.n_iface());
+        size_t off = 0;
+        for (int k = 0; k < dd.n_iface(); ++k) {
+            const size_t ne = dd.ifaces[k].faces.size();
+            skel[k] = Vec(flux + off, flux + off + ne);
+            off += ne;
+        }
+        SolveCounters c;
+        const int n = dd.grid.cells();
+        const DownscaleResult ds =
+            downscale(dd, Vec(kappa, kappa + n), ctx->q, ctx->bc, locals_in(ctx, p_local, u_local, nullptr), skel, c);
+        copy_out(p, ds.p);
+        copy_out(u, ds.u);
+        fill_info(info, ds);
+        fill_counters(counters, c);
+    });
+}
+
+int oracle_weak_continuity_residuals(oracle_ctx* ctx, const double* u_local, const double* bp_local, double* fj, double* pj) {
+    return guarded(ctx, [&] {
+        if (!ctx->state.basis) throw ConfigError("weak_continuity_residuals: no basis installed");
+        const WeakResiduals w = weak_continuity_residuals(*ctx->state.basis, locals_in(ctx, nullptr, u_local, bp_local));
+        if (fj) *fj = w.flux_jump;
+        if (pj) *pj = w.pressure_jump;
     });
 }
 

@@ -72,6 +72,7 @@ class Sizes(C.Structure):
         ("cells", C.c_int32), ("faces", C.c_int32), ("bfaces", C.c_int32), ("n_sub", C.c_int32),
         ("n_interfaces", C.c_int32), ("skeleton_edges", C.c_int32), ("dim_flux", C.c_int32),
         ("dim_pressure", C.c_int32), ("nhat", C.c_int64), ("sub_nx", C.c_int32), ("sub_ny", C.c_int32),
+        ("sub_faces", C.c_int32),
     ]
 
 
@@ -96,6 +97,15 @@ PROTOTYPES = {
     "mrcm_solve": (C.c_int, [_vp, _dp, _dp, _dp, _dp, _dp, _dp, C.POINTER(DownscaleInfo), C.POINTER(Counters)]),
     "mpm_update": (C.c_int, [_vp, _dp, _dp, _dp, _dp, C.POINTER(DownscaleInfo), C.POINTER(Counters)]),
     "interface_matrix": (C.c_int, [_vp, _dp]),
+    # MRCM sub-steps (mrcm.hpp:77-136, 157-161)
+    "compute_basis_set": (C.c_int, [_vp, _dp, _dp, _dp, C.POINTER(Counters)]),
+    "restrict_physical_data": (C.c_int, [_vp, _dp, _ip, _dp, _dp, _dp]),
+    "solve_particular": (C.c_int, [_vp, _dp, _ip, _dp, _dp, _dp, _dp, _dp, _dp, C.POINTER(Counters)]),
+    "solve_interface": (C.c_int, [_vp, _dp, _dp, C.POINTER(Counters)]),
+    "reconstruct": (C.c_int, [_vp, _dp, _dp, _dp, _dp, _dp, _dp, _dp]),
+    "averaged_skeleton_flux": (C.c_int, [_vp, _dp, _dp]),
+    "downscale": (C.c_int, [_vp, _dp, _dp, _dp, _dp, _dp, _dp, C.POINTER(DownscaleInfo), C.POINTER(Counters)]),
+    "weak_continuity_residuals": (C.c_int, [_vp, _dp, _dp, _dp, _dp]),
     "run": (C.c_int, [_vp, C.POINTER(Split), _dp, _dp, _dp, _dp, C.POINTER(StepRecord), C.c_int64,
                       C.POINTER(RunRecord)]),
     "run_begin": (C.c_int, [_vp, C.POINTER(Split), _dp, C.POINTER(StepRecord)]),

@@ -401,6 +401,88 @@ class Simulator:
         return GlobalSolution(p, u, co[:self.dim], DownscaleInfo(info.repair_max, info.flux_scale,
                               bool(info.repair_warning), info.div_residual, info.div_scale), _counters(cnt))
 
+    # ---- MRCM sub-steps (mrcm.hpp:77-136, 157-161) ----
+    # LocalData / LocalSolution are dicts of per-subdomain arrays (subdomain-major):
+    #   q, p: [n_sub, sub_nx*sub_ny]; u: [n_sub, sub_faces]; kind, value, beta,
+    #   robin_rhs, boundary_p: [n_sub, 2(sub_nx+sub_ny)] (W, E, S, N)
+    def _shapes(self):
+        sz = self.sizes
+        return sz.n_sub, sz.sub_nx * sz.sub_ny, sz.sub_faces, 2 * (sz.sub_nx + sz.sub_ny)
+
+    def compute_basis_set(self, kappa, beta=None) -> SolveCounters:
+        k = self._f64(kappa, self.cells)
+        bm = bp = None
+        if beta is not None:
+            bm = self._f64(beta[0], self.sizes.skeleton_edges)
+            bp = self._f64(beta[1], self.sizes.skeleton_edges)
+        cnt = _abi.Counters()
+        self._check(self.lib.compute_basis_set(self.h, dptr(k), dptr(bm), dptr(bp), C.byref(cnt)))
+        return _counters(cnt)
+
+    def restrict_physical_data(self) -> dict:
+        ns, nc, nf, ne = self._shapes()
+        d = {"q": np.empty((ns, nc)), "kind": np.empty((ns, ne), np.int32), "value": np.empty((ns, ne)),
+             "beta": np.empty((ns, ne)), "robin_rhs": np.empty((ns, ne))}
+        self._check(self.lib.restrict_physical_data(self.h, dptr(d["q"]), iptr(d["kind"]), dptr(d["value"]),
+                                                    dptr(d["beta"]), dptr(d["robin_rhs"])))
+        return d
+
+    def solve_particular(self, data: dict):
+        ns, nc, nf, ne = self._shapes()
+        q = self._f64(data["q"], ns * nc)
+        kind = np.ascontiguousarray(data["kind"], np.int32).ravel()
+        val, beta, rr = (self._f64(data[k], ns * ne) for k in ("value", "beta", "robin_rhs"))
+        out = {"p": np.empty((ns, nc)), "u": np.empty((ns, nf)), "boundary_p": np.empty((ns, ne))}
+        cnt = _abi.Counters()
+        self._check(self.lib.solve_particular(self.h, dptr(q), iptr(kind), dptr(val), dptr(beta), dptr(rr),
+                                              dptr(out["p"]), dptr(out["u"]), dptr(out["boundary_p"]),
+                                              C.byref(cnt)))
+        return out, _counters(cnt)
+
+    def solve_interface(self, particular: dict):
+        ns, nc, nf, ne = self._shapes()
+        u = self._f64(particular["u"], ns * nf)
+        co = np.empty(max(self.dim, 1))
+        cnt = _abi.Counters()
+        self._check(self.lib.solve_interface(self.h, dptr(u), dptr(co), C.byref(cnt)))
+        return co[:self.dim], _counters(cnt)
+
+    def reconstruct(self, coeffs, particular: dict) -> dict:
+        ns, nc, nf, ne = self._shapes()
+        co = self._f64(coeffs, self.dim) if self.dim else np.zeros(1)
+        p, u, bp = (self._f64(particular[k], n) for k, n in (("p", ns * nc), ("u", ns * nf),
+                                                              ("boundary_p", ns * ne)))
+        out = {"p": np.empty((ns, nc)), "u": np.empty((ns, nf)), "boundary_p": np.empty((ns, ne))}
+        self._check(self.lib.reconstruct(self.h, dptr(co), dptr(p), dptr(u), dptr(bp), dptr(out["p"]),
+                                         dptr(out["u"]), dptr(out["boundary_p"])))
+        return out
+
+    def averaged_skeleton_flux(self, recon: dict):
+        ns, nc, nf, ne = self._shapes()
+        u = self._f64(recon["u"], ns * nf)
+        out = np.empty(max(self.sizes.skeleton_edges, 1))
+        self._check(self.lib.averaged_skeleton_flux(self.h, dptr(u), dptr(out)))
+        return out[:self.sizes.skeleton_edges]
+
+    def downscale(self, kappa, recon: dict, skeleton_flux):
+        ns, nc, nf, ne = self._shapes()
+        k = self._f64(kappa, self.cells)
+        p, u = self._f64(recon["p"], ns * nc), self._f64(recon["u"], ns * nf)
+        fl = self._f64(skeleton_flux, self.sizes.skeleton_edges) if self.sizes.skeleton_edges else np.zeros(1)
+        po, uo = np.empty(self.cells), np.empty(self.faces)
+        info, cnt = _abi.DownscaleInfo(), _abi.Counters()
+        self._check(self.lib.downscale(self.h, dptr(k), dptr(p), dptr(u), dptr(fl), dptr(po), dptr(uo),
+                                       C.byref(info), C.byref(cnt)))
+        return po, uo, DownscaleInfo(info.repair_max, info.flux_scale, bool(info.repair_warning),
+                                     info.div_residual, info.div_scale), _counters(cnt)
+
+    def weak_continuity_residuals(self, recon: dict):
+        ns, nc, nf, ne = self._shapes()
+        u, bp = self._f64(recon["u"], ns * nf), self._f64(recon["boundary_p"], ns * ne)
+        fj, pj = C.c_double(), C.c_double()
+        self._check(self.lib.weak_continuity_residuals(self.h, dptr(u), dptr(bp), C.byref(fj), C.byref(pj)))
+        return fj.value, pj.value
+
     def interface_matrix(self):
         M = np.empty((self.dim, self.dim))
         self._check(self.lib.interface_matrix(self.h, dptr(M)))

@@ -96,6 +96,7 @@ const Scalars& sync_scalars(Ctx& c) {
         if (e & ERR_KAPPA) throw NumericError("CellCenteredSolver: conductivity must be positive and finite");
         if (e & ERR_ROBIN_BETA) throw ConfigError("CellCenteredSolver: Robin face requires beta > 0");
         if (e & ERR_PIVOT) throw NumericError("CellCenteredSolver: direct solve failed");
+        if (e & ERR_STRUCT) throw NumericError("CellCenteredSolver: boundary structure changed since factorization");
         if (e & ERR_EPS_ZERO) throw NumericError("epsilon: zero reference norm in relative mode");
         if (e & ERR_TRACK_ZERO) throw NumericError("relative_flux_error: zero reference norm");
         if (e & ERR_FINE_NOCONV)
@@ -888,6 +889,7 @@ int mpm2p_get_sizes(const mpm2p_ctx* ctx, mpm2p_sizes* o) {
     o->nhat = ctx->c.nhat;
     o->sub_nx = L.snx;
     o->sub_ny = L.sny;
+    o->sub_faces = sub_local_faces(L);
     return MPM2P_OK;
 }
 
@@ -1087,6 +1089,188 @@ int mpm2p_interface_matrix(mpm2p_ctx* ctx, double* M) {
                 for (int z = ptr[r]; z < ptr[r + 1]; ++z) M[(size_t)r * c.dim + col[z]] = val[z];
         }
         CK(cudaStreamSynchronize(c.st));
+    });
+}
+
+// ---- MRCM sub-steps (substeps.cu) ------------------------------------------
+namespace {
+struct LocalBufs {  // device copies of the per-subdomain C-ABI arrays
+    DevBuf<double> q, val, beta, rhs, p, u, bp, p2, u2, bp2, flux;
+    DevBuf<int> kind;
+};
+void need_basis(const Ctx& c, const char* fn) {
+    if (!c.has_basis) throw ConfigError(std::string(fn) + ": no basis installed (compute_basis_set or mrcm_solve first)");
+}
+void up_cells(Ctx& c, DevBuf<double>& d, const double* h, size_t n, const char* what) {
+    if (!h) throw ConfigError(std::string("missing ") + what);
+    d.alloc(std::max<size_t>(n, 1));
+    upload(c, d, h, n);
+}
+}  // namespace
+
+int mpm2p_compute_basis_set(mpm2p_ctx* ctx, const double* kappa, const double* bm, const double* bp,
+                            mpm2p_counters* counters) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        const Layout& L = c.L;
+        c.c_hom = c.c_part = c.c_down = c.c_fine = c.c_iface = 0;
+        upload(c, c.kappa_n, kappa, L.cells());
+        const bool given = bm && bp;
+        if (given && L.skeleton_edges() > 0) {
+            upload(c, c.beta_m, bm, L.skeleton_edges());
+            upload(c, c.beta_p, bp, L.skeleton_edges());
+        }
+        if (!given) launch_beta(c, c.kappa_n);
+        c.trans_fresh = false;
+        launch_trans(c, c.kappa_n);
+        launch_basis_core(c, c.kappa_n);
+        sync_scalars(c);
+        c.has_basis = true;
+        if (counters) fill_counters(c, counters);
+    });
+}
+
+int mpm2p_restrict_physical_data(mpm2p_ctx* ctx, double* q_local, int32_t* kind_local, double* value_local,
+                                 double* beta_local, double* rhs_local) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        const Layout& L = c.L;
+        need_basis(c, "restrict_physical_data");
+        const size_t nc = (size_t)L.n_sub * L.ncs, ne = (size_t)L.n_sub * L.nbe;
+        LocalBufs b;
+        b.q.alloc(nc), b.kind.alloc(ne), b.val.alloc(ne), b.beta.alloc(ne), b.rhs.alloc(ne);
+        sub_restrict(c, b.q, b.kind, b.val, b.beta, b.rhs);
+        download(c, q_local, b.q, nc);
+        if (kind_local) CK(cudaMemcpyAsync(kind_local, b.kind.p, ne * sizeof(int), cudaMemcpyDeviceToHost, c.st));
+        download(c, value_local, b.val, ne);
+        download(c, beta_local, b.beta, ne);
+        download(c, rhs_local, b.rhs, ne);
+        sync_scalars(c);
+    });
+}
+
+int mpm2p_solve_particular(mpm2p_ctx* ctx, const double* q_local, const int32_t* kind_local, const double* value_local,
+                           const double* beta_local, const double* rhs_local, double* p_local, double* u_local,
+                           double* bp_local, mpm2p_counters* counters) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        const Layout& L = c.L;
+        need_basis(c, "solve_particular");
+        c.c_hom = c.c_part = c.c_down = c.c_fine = c.c_iface = 0;
+        const size_t nc = (size_t)L.n_sub * L.ncs, ne = (size_t)L.n_sub * L.nbe;
+        const size_t nf = (size_t)L.n_sub * sub_local_faces(L);
+        LocalBufs b;
+        up_cells(c, b.q, q_local, nc, "q_local");
+        if (!kind_local) throw ConfigError("missing kind_local");
+        b.kind.alloc(ne);
+        CK(cudaMemcpyAsync(b.kind.p, kind_local, ne * sizeof(int), cudaMemcpyHostToDevice, c.st));
+        up_cells(c, b.val, value_local, ne, "value_local");
+        up_cells(c, b.beta, beta_local, ne, "beta_local");
+        up_cells(c, b.rhs, rhs_local, ne, "robin_rhs_local");
+        b.p.alloc(nc), b.u.alloc(nf), b.bp.alloc(ne);
+        sub_solve_particular(c, b.q, b.kind, b.val, b.beta, b.rhs, b.p, b.u, b.bp);
+        sync_scalars(c);
+        download(c, p_local, b.p, nc);
+        download(c, u_local, b.u, nf);
+        download(c, bp_local, b.bp, ne);
+        CK(cudaStreamSynchronize(c.st));
+        if (counters) fill_counters(c, counters);
+    });
+}
+
+int mpm2p_solve_interface(mpm2p_ctx* ctx, const double* u_local, double* coeffs, mpm2p_counters* counters) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        const Layout& L = c.L;
+        need_basis(c, "solve_interface");
+        c.c_hom = c.c_part = c.c_down = c.c_fine = c.c_iface = 0;
+        LocalBufs b;
+        up_cells(c, b.u, u_local, (size_t)L.n_sub * sub_local_faces(L), "u_local");
+        sub_solve_interface(c, b.u);
+        sync_scalars(c);
+        if (coeffs && c.dim > 0) download(c, coeffs, c.icoef, c.dim);
+        CK(cudaStreamSynchronize(c.st));
+        if (counters) fill_counters(c, counters);
+    });
+}
+
+int mpm2p_reconstruct(mpm2p_ctx* ctx, const double* coeffs, const double* p_local, const double* u_local,
+                      const double* bp_local, double* p_out, double* u_out, double* bp_out) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        const Layout& L = c.L;
+        need_basis(c, "reconstruct");
+        const size_t nc = (size_t)L.n_sub * L.ncs, ne = (size_t)L.n_sub * L.nbe;
+        const size_t nf = (size_t)L.n_sub * sub_local_faces(L);
+        LocalBufs b;
+        up_cells(c, b.p, p_local, nc, "p_local");
+        up_cells(c, b.u, u_local, nf, "u_local");
+        up_cells(c, b.bp, bp_local, ne, "bp_local");
+        DevBuf<double> co;
+        co.alloc(std::max(1, c.dim));
+        if (c.dim > 0) up_cells(c, co, coeffs, c.dim, "coeffs");
+        b.p2.alloc(nc), b.u2.alloc(nf), b.bp2.alloc(ne);
+        sub_reconstruct(c, co, b.p, b.u, b.bp, b.p2, b.u2, b.bp2);
+        sync_scalars(c);
+        download(c, p_out, b.p2, nc);
+        download(c, u_out, b.u2, nf);
+        download(c, bp_out, b.bp2, ne);
+        CK(cudaStreamSynchronize(c.st));
+    });
+}
+
+int mpm2p_averaged_skeleton_flux(mpm2p_ctx* ctx, const double* u_local, double* flux) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        const Layout& L = c.L;
+        LocalBufs b;
+        up_cells(c, b.u, u_local, (size_t)L.n_sub * sub_local_faces(L), "u_local");
+        b.flux.alloc(std::max(1, L.skeleton_edges()));
+        sub_skeleton_flux(c, b.u, b.flux);
+        download(c, flux, b.flux, L.skeleton_edges());
+        sync_scalars(c);
+    });
+}
+
+int mpm2p_downscale(mpm2p_ctx* ctx, const double* kappa, const double* p_local, const double* u_local,
+                    const double* flux, double* p, double* u, mpm2p_downscale_info* info, mpm2p_counters* counters) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        const Layout& L = c.L;
+        c.c_hom = c.c_part = c.c_down = c.c_fine = c.c_iface = 0;
+        LocalBufs b;
+        up_cells(c, b.p, p_local, (size_t)L.n_sub * L.ncs, "p_local");
+        up_cells(c, b.u, u_local, (size_t)L.n_sub * sub_local_faces(L), "u_local");
+        b.flux.alloc(std::max(1, L.skeleton_edges()));
+        if (L.skeleton_edges() > 0) up_cells(c, b.flux, flux, L.skeleton_edges(), "skeleton flux");
+        upload(c, c.kappa_n, kappa, L.cells());
+        sub_downscale(c, c.kappa_n, b.p, b.u, b.flux);
+        const Scalars& s = sync_scalars(c);
+        download(c, p, c.p, L.cells());
+        download(c, u, c.u, L.faces());
+        CK(cudaStreamSynchronize(c.st));
+        fill_info(s, info);
+        if (counters) fill_counters(c, counters);
+    });
+}
+
+int mpm2p_weak_continuity_residuals(mpm2p_ctx* ctx, const double* u_local, const double* bp_local, double* flux_jump,
+                         double* pressure_jump) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        const Layout& L = c.L;
+        need_basis(c, "weak_continuity_residuals");
+        LocalBufs b;
+        up_cells(c, b.u, u_local, (size_t)L.n_sub * sub_local_faces(L), "u_local");
+        up_cells(c, b.bp, bp_local, (size_t)L.n_sub * L.nbe, "bp_local");
+        DevBuf<double> out;
+        out.alloc(2);
+        sub_weak_residuals(c, b.u, b.bp, out);
+        double h[2];
+        CK(cudaMemcpyAsync(h, out.p, sizeof(h), cudaMemcpyDeviceToHost, c.st));
+        sync_scalars(c);
+        if (flux_jump) *flux_jump = h[0];
+        if (pressure_jump) *pressure_jump = h[1];
     });
 }
 

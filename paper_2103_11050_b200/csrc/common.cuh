@@ -32,7 +32,8 @@ enum : unsigned {
     ERR_ROBIN_BETA = 1u << 5,   // Robin face requires beta > 0 (elliptic.cpp:134-135)
     ERR_REPAIR_SINGULAR = 1u << 6,
     ERR_FINE_NOCONV = 1u << 7,  // fine-reference PCG did not reach its tolerance (fine.cu)
-    ERR_TRACK_ZERO = 1u << 8    // relative_flux/sat_error: zero reference norm (simulation.cpp:37-41,53-57)
+    ERR_TRACK_ZERO = 1u << 8,   // relative_flux/sat_error: zero reference norm (simulation.cpp:37-41,53-57)
+    ERR_STRUCT = 1u << 9        // solve with a boundary structure other than the factorization's (elliptic.cpp:155-160)
 };
 
 inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }

@@ -320,6 +320,22 @@ void launch_trans(Ctx& c, const double* kappa);
 void launch_beta(Ctx& c, const double* kappa);
 void launch_rebuild(Ctx& c, const double* kappa, bool compute_beta = true);  // basis + interface matrix + recon_m + downscale
 void launch_mpm(Ctx& c, const double* kappa_n);       // MPM-2P update + downscale
+void launch_basis_core(Ctx& c, const double* kappa);  // compute_basis_set with beta and T in place (X, traces, interface factor)
+bool particular_solve_x(Ctx& c);                      // particular solve in place on X[s][0] with the cached factor
+void interface_solve(Ctx& c, bool refine);            // c.PU -> c.irhs -> c.icoef (mrcm.cpp:254-268)
+void downscale(Ctx& c, const double* kappa, bool skel_given = false);  // c.RU, c.RS (+ c.skel) -> p, u (mrcm.cpp:306-439)
+void ds_factor_fork(Ctx& c);                          // split downscale: factor on the side stream
+// ---- MRCM sub-steps (substeps.cu; mrcm.hpp:77-136,157-161), device arrays in the C-ABI layouts
+int sub_local_faces(const Layout& L);
+void sub_restrict(Ctx& c, double* qL, int* kindL, double* valL, double* betaL, double* rhsL);
+void sub_solve_particular(Ctx& c, const double* qL, const int* kindL, const double* valL, const double* betaL,
+                          const double* rhsL, double* pL, double* uL, double* bpL);
+void sub_solve_interface(Ctx& c, const double* uL);  // -> c.icoef
+void sub_reconstruct(Ctx& c, const double* coef, const double* pL, const double* uL, const double* bpL, double* pO,
+                     double* uO, double* bpO);
+void sub_skeleton_flux(Ctx& c, const double* uL, double* flux);
+void sub_downscale(Ctx& c, const double* kappa, const double* pL, const double* uL, const double* flux);
+void sub_weak_residuals(Ctx& c, const double* uL, const double* bpL, double* out2);
 void launch_setup_static(Ctx& c);                     // qsum, ground, repair operator inverse
 bool sep_repair_setup(Ctx& c);                        // separable repair operator (before the Linv allocation)
 void configure_kernels();

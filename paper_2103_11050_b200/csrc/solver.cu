@@ -1985,7 +1985,7 @@ void launch_setup_static(Ctx& c) {
     }
 }
 
-namespace {
+// split downscale, downscale, interface solve (declared in context.cuh)
 
 // Split downscale, side-stream half: the downscale operator depends only on
 // T = transmissibility(kappa_n) (pure Neumann, all-Flux, anchor 0;
@@ -2031,12 +2031,12 @@ void ds_factor_fork(Ctx& c) {
 
 // Downscale shared by the rebuild and the MPM step (mrcm.cpp:306-439); needs
 // c.T = transmissibility(kappa), RU/RS = recon traces and pressure sums.
-void downscale(Ctx& c, const double* kappa) {
+void downscale(Ctx& c, const double* kappa, bool skel_given) {
     const Layout& L = c.L;
-    {  // skeleton fluxes (k_skel) are formed inside k_resid
+    {  // skeleton fluxes (k_skel) are formed inside k_resid unless given
         PROF(c, "k_resid");
         launch_k(c, k_resid, grid_for(32LL * L.n_sub), TPB, 0, L, c.skel, c.RU, c.qsum_sub, c.resid, c.sc, c.red,
-                                                             c.red_count, 1);
+                                                             c.red_count, skel_given ? 0 : 1);
         CK_LAUNCH();
     }
     if (c.repair_active && c.sep_repair) {  // delta = Qy [(Qy^T R Qx) ./ (ly + lx)] Qx^T
@@ -2211,7 +2211,7 @@ void interface_solve(Ctx& c, bool refine) {
     }
 }
 
-}  // namespace
+
 
 void configure_kernels() {
     CK(cudaFuncSetAttribute(k_factor_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -2224,6 +2224,39 @@ void launch_rebuild(Ctx& c, const double* kappa, bool compute_beta) {  // comput
     if (compute_beta) launch_beta(c, kappa);
     launch_trans(c, kappa);
     ds_factor_fork(c);  // downscale operator of kappa, concurrent with the basis rebuild
+    launch_basis_core(c, kappa);
+    interface_solve(c, true);  // the new inverse's rcond is not known yet
+    // recon_m (kept for MPM steps) and its traces
+    if (c.dim == 0) CK(cudaMemsetAsync(c.icoef, 0, sizeof(double), c.st));
+    {
+        PROF(c, "k_recon_traces");
+        launch_k(c, k_recon_traces, grid_for((long long)L.n_sub * L.nbe), TPB, 0, L, c.icoef, c.PU, c.PB, c.HU, c.HB, nullptr,
+                                                                               c.RU, c.bpm);
+        CK_LAUNCH();
+    }
+    {
+        PROF(c, "k_recon_p");
+        launch_k(c, k_recon_p, grid_for(L.cells()), TPB, 0, L, c.max_rhs, c.icoef, c.X, c.pm);
+        CK_LAUNCH();
+    }
+    {
+        PROF(c, "k_sub_sum");
+        launch_k(c, k_sub_sum, cdiv((long long)L.n_sub * 32, TPB), TPB, 0, L, c.pm, c.pmsum);
+        CK_LAUNCH();
+    }
+    CK(cudaMemcpyAsync(c.RS, c.pmsum, L.n_sub * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
+    downscale(c, kappa);
+    c.has_basis = true;
+}
+
+// compute_basis_set (mrcm.cpp:132-240): with beta_m / beta_p and T =
+// transmissibility(kappa) in place, factor every subdomain operator, solve
+// the particular (q, bc) and homogeneous problems, their traces and pressure
+// sums, assemble the interface matrix and factor it (with the rcond guard).
+// Leaves the particular solution in X[s][0] and the homogeneous ones in
+// X[s][1..]; kappa_m = kappa.
+void launch_basis_core(Ctx& c, const double* kappa) {
+    const Layout& L = c.L;
     {
         PROF(c, "k_band_entries");
         launch_k(c, k_band_entries, grid_for(L.cells()), TPB, 0, L, kappa, c.T, 0, c.anchor_m ? 1 : 0, c.beta_m, c.beta_p,
@@ -2337,54 +2370,15 @@ void launch_rebuild(Ctx& c, const double* kappa, bool compute_beta) {  // comput
             interface_inverse_async(c, c.Mdense, c.Minv, c.dim, &c.sc.p->rcond, ERR_SINGULAR, 1e-14);
         }
     }
-    interface_solve(c, true);  // the new inverse's rcond is not known yet
-    // recon_m (kept for MPM steps) and its traces
-    if (c.dim == 0) CK(cudaMemsetAsync(c.icoef, 0, sizeof(double), c.st));
-    {
-        PROF(c, "k_recon_traces");
-        launch_k(c, k_recon_traces, grid_for((long long)L.n_sub * L.nbe), TPB, 0, L, c.icoef, c.PU, c.PB, c.HU, c.HB, nullptr,
-                                                                               c.RU, c.bpm);
-        CK_LAUNCH();
-    }
-    {
-        PROF(c, "k_recon_p");
-        launch_k(c, k_recon_p, grid_for(L.cells()), TPB, 0, L, c.max_rhs, c.icoef, c.X, c.pm);
-        CK_LAUNCH();
-    }
-    {
-        PROF(c, "k_sub_sum");
-        launch_k(c, k_sub_sum, cdiv((long long)L.n_sub * 32, TPB), TPB, 0, L, c.pm, c.pmsum);
-        CK_LAUNCH();
-    }
-    CK(cudaMemcpyAsync(c.RS, c.pmsum, L.n_sub * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
-    CK(cudaMemcpyAsync(c.kappa_m, kappa, L.cells() * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
-    downscale(c, kappa);
-    c.has_basis = true;
+    if (kappa != c.kappa_m.p)
+        CK(cudaMemcpyAsync(c.kappa_m, kappa, L.cells() * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
 }
 
-void launch_mpm(Ctx& c, const double* kn) {  // mpm_pressure_update (mpm.cpp:31-114)
+// The particular solve with the cached basis factor, in place on X[s][0]
+// (mrcm.cpp:242-252). The register-window kernels also write the traces PU
+// and pressure sums PS of the MPM-2P data (GZ); returns whether they did.
+bool particular_solve_x(Ctx& c) {
     const Layout& L = c.L;
-    if (!c.has_basis) throw ConfigError("mpm_pressure_update: no basis set (rebuild first)");
-    launch_trans(c, kn);
-    ds_factor_fork(c);  // downscale operator of kappa_n, concurrent with the particular / interface chain
-    {
-        PROF(c, "k_mpm_rhs");
-        if (c.rhs_w) {
-            launch_k(c, k_mpm_edges, std::min(grid_for((long long)L.n_sub * L.nbe), 8 * c.num_sms), TPB, 0, L, kn,
-                     c.kappa_m, c.bc_kind, c.bc_value, c.beta_m, c.beta_p, c.pm, c.bpm, c.GZ, c.WU, c.ET);
-            CK_LAUNCH();
-            launch_k(c, k_mpm_rhs_w, std::min(grid_for(L.cells()), 8 * c.num_sms), TPB, 0, L, c.max_rhs,
-                     c.anchor_m ? 1 : 0, c.T, c.q, c.pm, c.WU, c.ET, c.X);
-        }
-        else if (c.rhs_sub && L.ncs <= RHS_TPB * RHS_CPT)
-            launch_k(c, k_mpm_rhs_sub, L.n_sub, RHS_TPB, (size_t)(L.ncs + 2 * L.nbe) * sizeof(double), L, c.max_rhs,
-                     c.anchor_m ? 1 : 0, kn, c.kappa_m, c.T, c.q, c.bc_kind, c.bc_value, c.beta_m, c.beta_p, c.pm,
-                     c.bpm, c.X, c.GZ, c.WU);
-        else
-            launch_k(c, k_mpm_rhs, grid_for(L.cells()), TPB, 0, L, c.max_rhs, c.anchor_m ? 1 : 0, kn, c.kappa_m, c.T,
-                     c.q, c.bc_kind, c.bc_value, c.beta_m, c.beta_p, c.pm, c.bpm, c.X, c.GZ, c.WU);
-        CK_LAUNCH();
-    }
     const size_t sm1 = (size_t)WPB * band_smem_doubles(L.snx, 1) * sizeof(double);
     bool fused_traces = false;  // the register-window kernel also writes PU / PS
     if (c.twist_store) {
@@ -2420,6 +2414,33 @@ void launch_mpm(Ctx& c, const double* kn) {  // mpm_pressure_update (mpm.cpp:31-
         }
         CK_LAUNCH();
     }
+    return fused_traces;
+}
+
+void launch_mpm(Ctx& c, const double* kn) {  // mpm_pressure_update (mpm.cpp:31-114)
+    const Layout& L = c.L;
+    if (!c.has_basis) throw ConfigError("mpm_pressure_update: no basis set (rebuild first)");
+    launch_trans(c, kn);
+    ds_factor_fork(c);  // downscale operator of kappa_n, concurrent with the particular / interface chain
+    {
+        PROF(c, "k_mpm_rhs");
+        if (c.rhs_w) {
+            launch_k(c, k_mpm_edges, std::min(grid_for((long long)L.n_sub * L.nbe), 8 * c.num_sms), TPB, 0, L, kn,
+                     c.kappa_m, c.bc_kind, c.bc_value, c.beta_m, c.beta_p, c.pm, c.bpm, c.GZ, c.WU, c.ET);
+            CK_LAUNCH();
+            launch_k(c, k_mpm_rhs_w, std::min(grid_for(L.cells()), 8 * c.num_sms), TPB, 0, L, c.max_rhs,
+                     c.anchor_m ? 1 : 0, c.T, c.q, c.pm, c.WU, c.ET, c.X);
+        }
+        else if (c.rhs_sub && L.ncs <= RHS_TPB * RHS_CPT)
+            launch_k(c, k_mpm_rhs_sub, L.n_sub, RHS_TPB, (size_t)(L.ncs + 2 * L.nbe) * sizeof(double), L, c.max_rhs,
+                     c.anchor_m ? 1 : 0, kn, c.kappa_m, c.T, c.q, c.bc_kind, c.bc_value, c.beta_m, c.beta_p, c.pm,
+                     c.bpm, c.X, c.GZ, c.WU);
+        else
+            launch_k(c, k_mpm_rhs, grid_for(L.cells()), TPB, 0, L, c.max_rhs, c.anchor_m ? 1 : 0, kn, c.kappa_m, c.T,
+                     c.q, c.bc_kind, c.bc_value, c.beta_m, c.beta_p, c.pm, c.bpm, c.X, c.GZ, c.WU);
+        CK_LAUNCH();
+    }
+    const bool fused_traces = particular_solve_x(c);
     if (!fused_traces) {
         {
             PROF(c, "k_part_traces");
