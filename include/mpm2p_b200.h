@@ -275,6 +275,15 @@ int mpm2p_weak_continuity_residuals(mpm2p_ctx* ctx, const double* u_local, const
 int mpm2p_run(mpm2p_ctx* ctx, const mpm2p_split* split, const double* s0, double* s_final,
               double* p_final, double* u_final, mpm2p_step_record* steps, int64_t max_steps,
               mpm2p_run_record* rec);
+/* RunResult run(in, snapshot_steps, snap) with snapshots   simulation.hpp:119-128
+ * SnapshotCallback: called on the calling thread after each step record whose
+ * step is listed (the initial solve is step 0; simulation.cpp:207-227), with
+ * host copies of s, p, u that are valid only during the call. */
+typedef void (*mpm2p_snapshot_fn)(void* user, int64_t step, const double* s, const double* p, const double* u);
+int mpm2p_run_snapshots(mpm2p_ctx* ctx, const mpm2p_split* split, const double* s0, double* s_final,
+                        double* p_final, double* u_final, mpm2p_step_record* steps, int64_t max_steps,
+                        mpm2p_run_record* rec, const int64_t* snapshot_steps, int64_t n_snapshots,
+                        mpm2p_snapshot_fn snap, void* user);
 /* The same loop, one Algorithm-1 iteration per call (inputs stay resident in
  * HBM). run_begin performs the initial solve and writes its record. */
 int mpm2p_run_begin(mpm2p_ctx* ctx, const mpm2p_split* split, const double* s0,

@@ -362,6 +362,35 @@ int oracle_run(oracle_ctx* ctx, const mpm2p_split* sp, const double* s0, double*
     });
 }
 
+int oracle_run_snapshots(oracle_ctx* ctx, const mpm2p_split* sp, const double* s0, double* s_final, double* p_final,
+                         double* u_final, mpm2p_step_record* steps, int64_t max_steps, mpm2p_run_record* rec,
+                         const int64_t* snapshot_steps, int64_t n_snapshots, mpm2p_snapshot_fn snap, void* user) {
+    return guarded(ctx, [&] {
+        const int64_t c0 = clamp_count();
+        Runner r(make_inputs(ctx, sp, s0));
+        std::vector<double> hs, hp, hu;
+        auto maybe_snap = [&]() {  // simulation.cpp:224-226
+            if (!snap || !snapshot_steps) return;
+            const int64_t n = r.record().steps.back().step;
+            if (std::find(snapshot_steps, snapshot_steps + n_snapshots, n) == snapshot_steps + n_snapshots) return;
+            hs.assign(r.s().begin(), r.s().end());
+            hp.assign(r.p().begin(), r.p().end());
+            hu.assign(r.u().begin(), r.u().end());
+            snap(user, n, hs.data(), hp.data(), hu.data());
+        };
+        r.begin();
+        maybe_snap();
+        while (r.step()) maybe_snap();
+        copy_out(s_final, r.s());
+        copy_out(p_final, r.p());
+        copy_out(u_final, r.u());
+        RunResult res = r.finish();
+        if (steps)
+            for (int64_t i = 0; i < (int64_t)res.rec.steps.size() && i < max_steps; ++i) fill_step(&steps[i], res.rec.steps[i]);
+        if (rec) fill_run(rec, res.rec, clamp_count() - c0);
+    });
+}
+
 int oracle_run_begin(oracle_ctx* ctx, const mpm2p_split* sp, const double* s0, mpm2p_step_record* first) {
     return guarded(ctx, [&] {
         ctx->clamp_base = clamp_count();

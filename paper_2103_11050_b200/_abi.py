@@ -77,6 +77,7 @@ class Sizes(C.Structure):
 
 
 _vp = C.c_void_p
+SNAPSHOT_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_int64, _dp, _dp, _dp)  # mpm2p_snapshot_fn
 PROTOTYPES = {
     "create": (C.c_int, [C.POINTER(Problem), C.POINTER(_vp)]),
     "destroy": (None, [_vp]),
@@ -108,6 +109,8 @@ PROTOTYPES = {
     "weak_continuity_residuals": (C.c_int, [_vp, _dp, _dp, _dp, _dp]),
     "run": (C.c_int, [_vp, C.POINTER(Split), _dp, _dp, _dp, _dp, C.POINTER(StepRecord), C.c_int64,
                       C.POINTER(RunRecord)]),
+    "run_snapshots": (C.c_int, [_vp, C.POINTER(Split), _dp, _dp, _dp, _dp, C.POINTER(StepRecord), C.c_int64,
+                                C.POINTER(RunRecord), C.POINTER(C.c_int64), C.c_int64, SNAPSHOT_FN, _vp]),
     "run_begin": (C.c_int, [_vp, C.POINTER(Split), _dp, C.POINTER(StepRecord)]),
     "run_step": (C.c_int, [_vp, C.POINTER(StepRecord), C.POINTER(C.c_int32)]),
     "run_read": (C.c_int, [_vp, _dp, _dp, _dp]),

@@ -489,15 +489,30 @@ class Simulator:
         return M
 
     # ---- driver (simulation.hpp:127-128) ----
-    def run(self, split: SplittingConfig, s0=None, inflow_sat=1.0, max_records=None) -> RunResult:
+    def run(self, split: SplittingConfig, s0=None, inflow_sat=1.0, max_records=None, snapshot_steps=(),
+            snap=None) -> RunResult:
+        """run(in, snapshot_steps, snap) (simulation.hpp:119-128): snap(step, s, p, u)
+        is called with copies of the fields after each listed step's record."""
         s0 = np.zeros(self.cells) if s0 is None else self._f64(s0, self.cells)
         cs = split_to_c(split, inflow_sat)
         n_rec = max_records or (split.te if split.te > 0 else split.max_steps_hard) + 1
         recs = (_abi.StepRecord * n_rec)()
         rr = _abi.RunRecord()
         s, p, u = np.empty(self.cells), np.empty(self.cells), np.empty(self.faces)
-        self._check(self.lib.run(self.h, C.byref(cs), dptr(s0), dptr(s), dptr(p), dptr(u), recs, n_rec,
-                                 C.byref(rr)))
+        if snap is not None and len(snapshot_steps):
+            cells, faces = self.cells, self.faces
+
+            def _cb(_user, step, sp_, pp_, up_):
+                snap(int(step), np.ctypeslib.as_array(sp_, (cells,)).copy(),
+                     np.ctypeslib.as_array(pp_, (cells,)).copy(), np.ctypeslib.as_array(up_, (faces,)).copy())
+            cb = _abi.SNAPSHOT_FN(_cb)
+            want = np.ascontiguousarray(snapshot_steps, np.int64)
+            self._check(self.lib.run_snapshots(self.h, C.byref(cs), dptr(s0), dptr(s), dptr(p), dptr(u), recs, n_rec,
+                                               C.byref(rr), want.ctypes.data_as(C.POINTER(C.c_int64)), want.size,
+                                               cb, None))
+        else:
+            self._check(self.lib.run(self.h, C.byref(cs), dptr(s0), dptr(s), dptr(p), dptr(u), recs, n_rec,
+                                     C.byref(rr)))
         steps = [_step_dict(recs[i]) for i in range(min(rr.te, n_rec))]
         return RunResult(_record(steps, rr), s, p, u)
 

@@ -1299,6 +1299,37 @@ int mpm2p_run_step(mpm2p_ctx* ctx, mpm2p_step_record* out, int32_t* done) {
     return guarded(ctx, [&] { *done = run_step(ctx, out) ? 0 : 1; });
 }
 
+int mpm2p_run_snapshots(mpm2p_ctx* ctx, const mpm2p_split* sp, const double* s0, double* s_final, double* p_final,
+                        double* u_final, mpm2p_step_record* steps, int64_t max_steps, mpm2p_run_record* rec,
+                        const int64_t* snapshot_steps, int64_t n_snapshots, mpm2p_snapshot_fn snap, void* user) {
+    return guarded(ctx, [&] {
+        Ctx& c = ctx->c;
+        const std::set<int64_t> want(snapshot_steps, snapshot_steps + (snapshot_steps ? n_snapshots : 0));
+        std::vector<double> hs, hp, hu;
+        auto maybe_snap = [&]() {  // simulation.cpp:224-226, after the step's record
+            if (!snap || want.empty()) return;
+            const int64_t n = ctx->d.steps.back().step;
+            if (!want.count(n)) return;
+            hs.resize(c.L.cells()), hp.resize(c.L.cells()), hu.resize(c.L.faces());
+            download(c, hs.data(), c.s, c.L.cells());
+            download(c, hp.data(), c.p, c.L.cells());
+            download(c, hu.data(), c.u, c.L.faces());
+            CK(cudaStreamSynchronize(c.st));
+            snap(user, n, hs.data(), hp.data(), hu.data());
+        };
+        run_begin(ctx, sp, s0, nullptr);
+        maybe_snap();
+        while (run_step(ctx, nullptr)) maybe_snap();
+        download(c, s_final, c.s, c.L.cells());
+        download(c, p_final, c.p, c.L.cells());
+        download(c, u_final, c.u, c.L.faces());
+        CK(cudaStreamSynchronize(c.st));
+        if (steps)
+            for (int64_t i = 0; i < (int64_t)ctx->d.steps.size() && i < max_steps; ++i) steps[i] = ctx->d.steps[i];
+        run_end(ctx, rec);
+    });
+}
+
 int mpm2p_run_read(mpm2p_ctx* ctx, double* s, double* p, double* u) {
     return guarded(ctx, [&] {
         Ctx& c = ctx->c;

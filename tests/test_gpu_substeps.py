@@ -10,7 +10,6 @@ import pytest
 from cases import problem, random_kappa, rel_l2
 from paper_2103_11050_b200 import api
 
-pytestmark = pytest.mark.gpu
 
 CASES = {
     "c1like": dict(nx=64, ny=64, nsx=4, nsy=4, bc="pd", space=api.SPACE_CONSTANT, hbar=api.HBAR_WHOLE),
@@ -37,6 +36,7 @@ def _pair(oracle, case):
     return api.Simulator(prob), api.Simulator(prob, oracle), K
 
 
+@pytest.mark.gpu
 @pytest.mark.parametrize("case", sorted(CASES))
 def test_substeps_match_oracle(oracle, case):
     g, o, K = _pair(oracle, case)
@@ -81,6 +81,7 @@ def test_substeps_match_oracle(oracle, case):
         assert abs(a - b) <= 1e-9 * scale
 
 
+@pytest.mark.gpu
 @pytest.mark.parametrize("case", sorted(CASES))
 def test_substeps_compose_to_mrcm_solve(oracle, case):
     """compute_basis_set -> restrict -> solve_particular -> solve_interface ->
@@ -105,6 +106,7 @@ def test_substeps_compose_to_mrcm_solve(oracle, case):
     assert rel_l2(u, mo.u) < 1e-8
 
 
+@pytest.mark.gpu
 def test_solve_particular_structure_check(oracle):
     """elliptic.cpp:155-160: a solve whose boundary kinds or Robin betas differ
     from the factorization's raises NumericError."""
@@ -124,8 +126,45 @@ def test_solve_particular_structure_check(oracle):
             sim.solve_particular(bad)
 
 
+@pytest.mark.gpu
 def test_substeps_need_a_basis(oracle):
     g, o, K = _pair(oracle, "c1like")
     for sim in (g, o):
         with pytest.raises(api.ConfigError):
             sim.restrict_physical_data()
+
+
+def _snap_run(sim, split, steps):
+    got = {}
+    res = sim.run(split, snapshot_steps=steps, snap=lambda n, s, p, u: got.__setitem__(n, (s, p, u)))
+    return res, got
+
+
+@pytest.mark.parametrize("gpu", [pytest.param(True, marks=pytest.mark.gpu),
+                                 False])
+def test_run_snapshots(oracle, gpu):
+    """run(in, snapshot_steps, snap) (simulation.hpp:119-128, simulation.cpp:
+    224-226): the callback fires once per listed step (0 = the initial solve)
+    with the fields the step-by-step driver holds after that step."""
+    nx = ny = 32
+    K = random_kappa(nx, ny, 4, 0.1, 10.0)
+    prob = problem(nx, ny, 4, 4, K)
+    sp = api.SplittingConfig(method=api.MPM2P, eta=0.01, te=12, cfl_safety=0.5)
+    make = (lambda: api.Simulator(prob)) if gpu else (lambda: api.Simulator(prob, oracle))
+    want = [0, 3, 7, 11, 50]
+    res, got = _snap_run(make(), sp, want)
+    assert sorted(got) == [0, 3, 7, 11]
+    ref = make()
+    ref.run_begin(sp)
+    for n in range(0, 12):
+        if n > 0:
+            assert ref.run_step() is not None
+        if n in got:
+            s, p, u = ref.run_read()
+            assert np.array_equal(got[n][0], s) and np.array_equal(got[n][1], p) and np.array_equal(got[n][2], u)
+    plain = make().run(sp)
+    assert np.array_equal(plain.s_final, res.s_final) and np.array_equal(plain.u_final, res.u_final)
+    if gpu:
+        _, go = _snap_run(api.Simulator(prob, oracle), sp, want)
+        for n in got:
+            assert np.max(np.abs(got[n][0] - go[n][0])) <= 1e-8 and rel_l2(got[n][2], go[n][2]) <= 1e-8
