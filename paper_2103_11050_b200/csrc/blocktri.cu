@@ -5,15 +5,27 @@
 // Ordered by subdomain row (the vertical interfaces of row j and the
 // horizontal interfaces between rows j and j+1 form block j), K = J M is
 // block tridiagonal: an interface only couples to interfaces that share a
-// subdomain with it. K is symmetric quasi-definite, so block
-// LDL^T needs no pivoting:
-//   S_0 = D_0,  T_{j-1} = S_{j-1}^-1 E_{j-1},  S_j = D_j - E_{j-1}^T T_{j-1};
-//   solve: y_j = b_j - T_{j-1}^T y_{j-1} (forward),
-//          x_j = S_j^-1 y_j - T_j x_{j+1} (backward).
-// Per rebuild: nblk dense inversions (ping-pong Gauss-Jordan, dense.cu) and
-// two GEMMs per block; per solve: 2 nblk - 1 dependent block products, each
-// HBM-bound. At C5: 128 blocks of 510 unknowns, S^-1 / T / T^T / D / E about
-// 0.27 GB each.
+// subdomain with it. K is symmetric quasi-definite: every
+// principal submatrix and Schur complement is factorable without pivoting.
+//
+// Block cyclic reduction (odd-even), all blocks padded to one size S (a
+// multiple of 64; the pad is an identity block):
+//   level l works on the blocks j = 0 (mod 2^l); at every level the odd
+//   members o are eliminated and the even members e keep a block-tridiagonal
+//   system of half the size:
+//     Dinv_o = D_o^-1, P_o = Dinv_o Lo_o, Q_o = Dinv_o Up_o
+//     D_e <- D_e - Lo_e Q_{o-} - Up_e P_{o+}
+//     Lo_e <- -Lo_e P_{o-},  Up_e <- -Up_e Q_{o+}
+//   until one block is left (Dinv_0). A solve is then
+//     forward,  per level: c_o = Dinv_o y_o;  y_e -= Lo_e c_{o-} + Up_e c_{o+}
+//     top:      x_0 = Dinv_0 y_0
+//     backward, per level: x_o = c_o - P_o x_{o-} - Q_o x_{o+}
+// i.e. 2 log2(nb) + 1 dependent batched GEMV launches (C5: 15) instead of the
+// 2 nb - 1 block steps of a sequential block LDL^T (255), each launch
+// streaming a whole level's matrices. The factorization is per level one
+// batched Gauss-Jordan inversion (one launch pair per 32-column panel for all
+// of the level's blocks) and batched GEMMs on the fp64 tensor cores
+// (mma.sync.m8n8k4, DMMA).
 
 #include "context.cuh"
 
@@ -24,119 +36,296 @@ namespace {
 
 constexpr int TPB = 256;
 
-// C[m x n] = op(A)[m x k] * B[k x n] (+ beta C0), row-major. TA: A is stored
-// k x m (use A^T). 64 x 64 tiles, k-slabs of 16, 4 x 4 outputs per thread.
-template <bool TA>
-__global__ void __launch_bounds__(256) k_dgemm(int m, int n, int kk, const double* __restrict__ A, int lda,
-                                               const double* __restrict__ Bm, int ldb, double* __restrict__ C,
-                                               int ldc, double alpha, const double* __restrict__ C0, int ldc0) {
-    pdl_begin();
-    __shared__ double As[16][64 + 1], Bs[16][64 + 1];
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    const int i0 = blockIdx.y * 64, j0 = blockIdx.x * 64;
-    double acc[4][4] = {};
-    for (int k0 = 0; k0 < kk; k0 += 16) {
-        for (int x = threadIdx.x; x < 16 * 64; x += 256) {
-            const int kq = x / 64, ii = x % 64;  // As[kq][ii] = op(A)[i0+ii][k0+kq]
-            const int gi = i0 + ii, gk = k0 + kq;
-            double v = 0.0;
-            if (gi < m && gk < kk) v = TA ? A[(size_t)gk * lda + gi] : A[(size_t)gi * lda + gk];
-            As[kq][ii] = v;
-            const int gj = j0 + ii;  // Bs[kq][jj] = B[k0+kq][j0+jj]
-            Bs[kq][ii] = (gj < n && gk < kk) ? Bm[(size_t)gk * ldb + gj] : 0.0;
-        }
-        __syncthreads();
+__device__ __forceinline__ void cr_dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+// One batched GEMM job: C = C0 + a1 A1 B1 (+ a2 A2 B2), all S x S row-major
+// (C may alias C0).
+struct GemmJob {
+    double* C;
+    const double* C0;
+    const double* A1;
+    const double* B1;
+    const double* A2;
+    const double* B2;
+    double a1, a2;
+};
+
+// 64 x 64 output tile per CTA (4 warps, 32 x 32 each = 4 x 4 DMMA tiles),
+// k-slabs of 16 staged in shared memory (padded rows: conflict-free fragment
+// loads), the next slab loaded into registers while the current one is used.
+constexpr int GT = 64, GK = 16, LDA = GK + 4, LDB = GT + 4;
+__global__ void __launch_bounds__(128) k_cr_gemm(const GemmJob* __restrict__ jobs, int S) {
+    __shared__ double As[GT * LDA], Bs[GK * LDB];
+    const GemmJob jb = jobs[blockIdx.z];
+    const int tiles = S / GT;
+    const int i0 = (blockIdx.x / tiles) * GT, j0 = (blockIdx.x % tiles) * GT;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wr = (w >> 1) * 32, wc = (w & 1) * 32;
+    double acc[4][4][2];
 #pragma unroll
-        for (int kq = 0; kq < 16; ++kq) {
-            double a[4], b[4];
+    for (int a = 0; a < 4; ++a)
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                a[q] = As[kq][ty + 16 * q];
-                b[q] = Bs[kq][tx + 16 * q];
+        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int term = 0; term < 2; ++term) {
+        const double* A = term ? jb.A2 : jb.A1;
+        const double* B = term ? jb.B2 : jb.B1;
+        if (!A) continue;
+        const double alpha = term ? jb.a2 : jb.a1;
+        double ra[8], rb[8];
+        auto fetch = [&](int k0) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int x = threadIdx.x + 128 * q;           // 0..1023
+                ra[q] = A[(size_t)(i0 + (x >> 4)) * S + k0 + (x & 15)];  // 64 x 16
+                rb[q] = B[(size_t)(k0 + (x >> 6)) * S + j0 + (x & 63)];  // 16 x 64
             }
+        };
+        fetch(0);
+        for (int k0 = 0; k0 < S; k0 += GK) {
+            __syncthreads();
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
+            for (int q = 0; q < 8; ++q) {
+                const int x = threadIdx.x + 128 * q;
+                As[(x >> 4) * LDA + (x & 15)] = alpha * ra[q];
+                Bs[(x >> 6) * LDB + (x & 63)] = rb[q];
+            }
+            __syncthreads();
+            if (k0 + GK < S) fetch(k0 + GK);
 #pragma unroll
-                for (int r = 0; r < 4; ++r) acc[q][r] = fma(a[q], b[r], acc[q][r]);
+            for (int kk = 0; kk < GK; kk += 4) {
+                double af[4], bf[4];
+#pragma unroll
+                for (int a = 0; a < 4; ++a) af[a] = As[(wr + a * 8 + (lane >> 2)) * LDA + kk + (lane & 3)];
+#pragma unroll
+                for (int b = 0; b < 4; ++b) bf[b] = Bs[(kk + (lane & 3)) * LDB + wc + b * 8 + (lane >> 2)];
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) cr_dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+            }
         }
-        __syncthreads();
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+    for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            const int gi = i0 + ty + 16 * q, gj = j0 + tx + 16 * r;
-            if (gi < m && gj < n) {
-                double v = alpha * acc[q][r];
-                if (C0) v += C0[(size_t)gi * ldc0 + gj];
-                C[(size_t)gi * ldc + gj] = v;
+        for (int b = 0; b < 4; ++b) {
+            const int r = i0 + wr + a * 8 + (lane >> 2), col = j0 + wc + b * 8 + 2 * (lane & 3);
+            const size_t o = (size_t)r * S + col;
+            double v0 = acc[a][b][0], v1 = acc[a][b][1];
+            if (jb.C0) {
+                v0 += jb.C0[o];
+                v1 += jb.C0[o + 1];
             }
+            jb.C[o] = v0;
+            jb.C[o + 1] = v1;
         }
 }
 
-// D_j and E_j (= K[block j, block j+1]) from the CSR of K.
-__global__ void k_bt_scatter(const int* __restrict__ kptr, const int* __restrict__ kcol, const double* __restrict__ kval,
-                             int n, const int* __restrict__ blk, const int* __restrict__ loc,
-                             const long long* __restrict__ doff, const long long* __restrict__ eoff,
-                             const int* __restrict__ bsz, double* __restrict__ D, double* __restrict__ E) {
+// ---- batched Gauss-Jordan inversion without pivoting (in place), one
+// launch pair per 32-column panel k for all matrices of the batch:
+//   k_gj_pivot: per matrix, save the panel column W[:, k] (S x 32), invert
+//               the pivot block (one warp per row, pivot by pivot) and form
+//               R = P W[k, :] (the new row panel)
+//   k_gj_update: W[i, j] -= C_i R_j (i outside the panel), W[k, :] = R,
+//               W[i, k] = -C_i P
+constexpr int GP = 32;
+// grid (S / 32 column tiles, batch): every CTA inverts the 32 x 32 pivot block
+// in shared memory (redundantly, it is small), forms its 32 x 32 tile of R and
+// saves its 32 rows of the panel column
+__global__ void __launch_bounds__(256) k_gj_pivot(double* const* __restrict__ mats, int S, int k0,
+                                                  double* __restrict__ colbuf, double* __restrict__ rowbuf,
+                                                  int* __restrict__ flag) {
+    pdl_begin();
+    __shared__ double Pv[GP][GP + 1];
+    __shared__ double Wk[GP][GP + 1];
+    double* W = mats[blockIdx.y];
+    double* Cb = colbuf + (size_t)blockIdx.y * S * GP;
+    double* Rb = rowbuf + (size_t)blockIdx.y * S * GP;
+    const int j0 = blockIdx.x * GP;
+    for (int x = threadIdx.x; x < GP * GP; x += blockDim.x) {
+        const int r = x / GP, q = x % GP;
+        Pv[r][q] = W[(size_t)(k0 + r) * S + k0 + q];
+        Wk[r][q] = W[(size_t)(k0 + r) * S + j0 + q];  // this CTA's tile of the pivot rows
+        Cb[(size_t)(j0 + r) * GP + q] = W[(size_t)(j0 + r) * S + k0 + q];  // rows j0.. of the panel column
+    }
+    __syncthreads();
+    // Gauss-Jordan of the pivot block in place (no pivoting): thread (r, q-group)
+    const int r = threadIdx.x >> 3, qg = (threadIdx.x & 7) * 4;
+    for (int p = 0; p < GP; ++p) {
+        const double d = Pv[p][p];
+        const double inv = 1.0 / d;
+        const double f = Pv[r][p];
+        double rp[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) rp[t] = Pv[p][qg + t];
+        __syncthreads();
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int q = qg + t;
+            if (r == p) Pv[r][q] = q == p ? inv : rp[t] * inv;
+            else Pv[r][q] = q == p ? -f * inv : Pv[r][q] - f * rp[t] * inv;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && blockIdx.x == 0 && (!(d != 0.0) || !isfinite(d))) atomicOr(flag, 1);
+    }
+    // R tile = P W[k, j0..j0+31]; the panel's own tile is P itself
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        const int q = qg + t;
+        double v;
+        if (j0 == k0) {
+            v = Pv[r][q];
+        } else {
+            v = 0.0;
+#pragma unroll 8
+            for (int u = 0; u < GP; ++u) v = fma(Pv[r][u], Wk[u][q], v);
+        }
+        Rb[(size_t)r * S + j0 + q] = v;
+    }
+}
+
+// tiles of 32 rows x 64 columns; C_i = saved panel rows, R = new row panel
+__global__ void __launch_bounds__(256) k_gj_update(double* const* __restrict__ mats, int S, int k0,
+                                                   const double* __restrict__ colbuf, const double* __restrict__ rowbuf) {
+    __shared__ double Cs[GP][GP + 1];
+    __shared__ double Rs[GP][64 + 1];
+    double* W = mats[blockIdx.z];
+    const double* Cb = colbuf + (size_t)blockIdx.z * S * GP;
+    const double* Rb = rowbuf + (size_t)blockIdx.z * S * GP;
+    const int i0 = blockIdx.y * GP, j0 = blockIdx.x * 64;
+    for (int x = threadIdx.x; x < GP * GP; x += blockDim.x) Cs[x / GP][x % GP] = Cb[(size_t)(i0 + x / GP) * GP + x % GP];
+    for (int x = threadIdx.x; x < GP * 64; x += blockDim.x) Rs[x / 64][x % 64] = Rb[(size_t)(x / 64) * S + j0 + x % 64];
+    __syncthreads();
+    const bool pivot_rows = i0 == k0;
+    for (int x = threadIdx.x; x < GP * 64; x += blockDim.x) {
+        const int r = x / 64, cc = x % 64, col = j0 + cc;
+        const size_t o = (size_t)(i0 + r) * S + col;
+        if (pivot_rows) {
+            W[o] = Rs[r][cc];
+        } else if (col >= k0 && col < k0 + GP) {
+            // -C_i P: R's panel columns hold P
+            double v = 0.0;
+            for (int q = 0; q < GP; ++q) v += Cs[r][q] * Rs[q][cc];
+            W[o] = -v;
+        } else {
+            double v = W[o];
+            for (int q = 0; q < GP; ++q) v -= Cs[r][q] * Rs[q][cc];
+            W[o] = v;
+        }
+    }
+}
+
+// ---- batched GEMV jobs: out = base + s1 M1 v1 (+ s2 M2 v2), S x S matrices
+struct GemvJob {
+    double* out;
+    const double* base;
+    const double* M1;
+    const double* v1;
+    const double* M2;
+    const double* v2;
+    double s1, s2;
+};
+constexpr int GV_ROWS = 32;  // rows per CTA (8 warps x 4 rows, the 4 rows' loads interleaved)
+__global__ void __launch_bounds__(256) k_cr_gemv(const GemvJob* __restrict__ jobs, int S) {
+    pdl_begin();
+    extern __shared__ double vs[];  // 2 S
+    const GemvJob jb = jobs[blockIdx.y];
+    for (int x = threadIdx.x; x < S; x += blockDim.x) {
+        vs[x] = jb.v1 ? jb.v1[x] : 0.0;
+        vs[S + x] = jb.v2 ? jb.v2[x] : 0.0;
+    }
+    __syncthreads();
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int r0 = blockIdx.x * GV_ROWS + w * 4;
+    double a[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int term = 0; term < 2; ++term) {
+        const double* M = term ? jb.M2 : jb.M1;
+        if (!M) continue;
+        const double s = term ? jb.s2 : jb.s1;
+        const double* v = vs + term * S;
+        double t[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int c = lane; c < S; c += 64) {
+            double m[4][2];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                m[q][0] = __ldg(M + (size_t)(r0 + q) * S + c);
+                m[q][1] = c + 32 < S ? __ldg(M + (size_t)(r0 + q) * S + c + 32) : 0.0;
+            }
+            const double v0 = v[c], v1 = c + 32 < S ? v[c + 32] : 0.0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) t[q] = fma(m[q][1], v1, fma(m[q][0], v0, t[q]));
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) a[q] += s * warp_sum(t[q]);
+    }
+    if (lane == 0)  // warp_sum leaves the total in lane 0
+#pragma unroll
+        for (int q = 0; q < 4; ++q) jb.out[r0 + q] = (jb.base ? jb.base[r0 + q] : 0.0) + a[q];
+}
+
+// D_j (padded, identity on the pad) and Up_j = K[block j, block j+1] from the CSR of K
+__global__ void k_cr_scatter(const int* __restrict__ kptr, const int* __restrict__ kcol, const double* __restrict__ kval,
+                             int n, const int* __restrict__ blk, const int* __restrict__ loc, int S,
+                             double* __restrict__ D, double* __restrict__ Up) {
     pdl_begin();
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n) return;
     const int j = blk[r], lr = loc[r];
     for (int z = kptr[r]; z < kptr[r + 1]; ++z) {
         const int c = kcol[z], jc = blk[c], lc = loc[c];
-        if (jc == j) D[doff[j] + (long long)lr * bsz[j] + lc] = kval[z];
-        else if (jc == j + 1) E[eoff[j] + (long long)lr * bsz[j + 1] + lc] = kval[z];
+        if (jc == j) D[((size_t)j * S + lr) * S + lc] = kval[z];
+        else if (jc == j + 1) Up[((size_t)j * S + lr) * S + lc] = kval[z];
     }
 }
-
-// out[cols x rows] = in[rows x cols]^T
-__global__ void k_transpose(const double* __restrict__ in, int rows, int cols, double* __restrict__ out) {
-    pdl_begin();
+__global__ void k_cr_pad(const int* __restrict__ bsz, int nb, int S, double* __restrict__ D) {
+    const long long n = (long long)nb * S;
+    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < n; x += (long long)gridDim.x * blockDim.x) {
+        const int j = (int)(x / S), r = (int)(x % S);
+        if (r >= bsz[j]) D[((size_t)j * S + r) * S + r] = 1.0;
+    }
+}
+// Lo_{j+1} = Up_j^T (batched 32 x 32 tile transposes)
+__global__ void k_cr_transpose(double* const* __restrict__ dst, const double* const* __restrict__ src, int S) {
     __shared__ double t[32][33];
+    const double* in = src[blockIdx.z];
+    double* out = dst[blockIdx.z];
     const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
-    for (int y = threadIdx.y; y < 32; y += blockDim.y) {
-        const int r = by + y, cc = bx + threadIdx.x;
-        t[y][threadIdx.x] = (r < rows && cc < cols) ? in[(size_t)r * cols + cc] : 0.0;
-    }
+    for (int y = threadIdx.y; y < 32; y += blockDim.y) t[y][threadIdx.x] = in[(size_t)(by + y) * S + bx + threadIdx.x];
     __syncthreads();
-    for (int y = threadIdx.y; y < 32; y += blockDim.y) {
-        const int cc = bx + y, r = by + threadIdx.x;
-        if (cc < cols && r < rows) out[(size_t)cc * rows + r] = t[threadIdx.x][y];
-    }
+    for (int y = threadIdx.y; y < 32; y += blockDim.y) out[(size_t)(bx + y) * S + by + threadIdx.x] = t[threadIdx.x][y];
 }
 
 __global__ void k_flag_err(const int* flag, Scalars* sc, unsigned bit) {
-    pdl_begin();
     if (*flag) atomicOr(&sc->err, bit);
 }
 
-// y (block order) <- J rhs gathered: y[off[blk[r]] + loc[r]] = (J rhs)_r
-// (transposed = 0) y = J rhs, (1) y = rhs, in block order
+// y (padded block order) <- J rhs (transposed = 0) or rhs (1)
 __global__ void k_bt_gather(const double* __restrict__ rhs, int n, const int* __restrict__ blk,
-                            const int* __restrict__ loc, const int* __restrict__ voff, double* __restrict__ y,
-                            int transposed) {
+                            const int* __restrict__ loc, int S, double* __restrict__ y, int transposed) {
     pdl_begin();
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n) return;
     const int h = n / 2;
     const double v = transposed ? rhs[r] : (r < h ? rhs[h + r] : -rhs[r - h]);
-    y[voff[blk[r]] + loc[r]] = v;
+    y[(size_t)blk[r] * S + loc[r]] = v;
 }
 
-// (transposed = 0) x = xb, (1) x = J^T xb, from block order
+// (transposed = 0) x = xb, (1) x = J^T xb, from padded block order
 __global__ void k_bt_unpermute(const double* __restrict__ xb, int n, const int* __restrict__ blk,
-                               const int* __restrict__ loc, const int* __restrict__ voff, double* __restrict__ x,
-                               int transposed) {
+                               const int* __restrict__ loc, int S, double* __restrict__ x, int transposed) {
     pdl_begin();
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n) return;
     const int h = n / 2;
     if (!transposed) {
-        x[r] = xb[voff[blk[r]] + loc[r]];
+        x[r] = xb[(size_t)blk[r] * S + loc[r]];
     } else {  // (J^T w)_i = -w_{i+h} (i < h), w_{i-h} (i >= h)
         const int q = r < h ? r + h : r - h;
-        const double w = xb[voff[blk[q]] + loc[q]];
+        const double w = xb[(size_t)blk[q] * S + loc[q]];
         x[r] = r < h ? -w : w;
     }
 }
@@ -270,97 +459,45 @@ __global__ void k_hager_fin(HagerState* st, Scalars* sc, double threshold, unsig
     if (!(rc > threshold)) atomicOr(&sc->err, bit);
 }
 
-// The block steps of a solve are a dependent chain of small products, each
-// latency-bound (one L2/HBM round trip for the block plus the launch). The
-// matrices are constant between rebuilds, so each kernel loads its rows into
-// registers BEFORE griddepcontrol.wait and triggers its dependents at entry:
-// launched with programmatic dependent launch (bt_solve), step j+1's block
-// streams in while step j finishes, and only the vector part is serialised.
-constexpr int BT_Q = 8;     // warps per row: a row's columns are split in BT_Q quarters
-constexpr int BT_NPL = 6;   // prefetched doubles per lane: quarters of up to 32 * 6 columns
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// The factorization / solve plan, built once from the block layout: device
+// job arrays and the host launch sequence.
+struct CrLaunch {
+    int kind;  // 0 gemm, 1 gj (pivot+update pair over all panels), 2 gemv
+    int first, count;  // job range (gemm / gemv jobs) or matrix-pointer range (gj)
+};
+struct CrPlan {
+    int S = 0, nb = 0, max_batch = 1;
+    DevBuf<GemmJob> gemm;
+    DevBuf<GemvJob> gemv;
+    DevBuf<double*> gjmats;
+    DevBuf<double*> tr_dst;
+    DevBuf<const double*> tr_src;
+    std::vector<CrLaunch> factor, solve;
+    DevBuf<double> D, LU, P, Q, cvec, colbuf, rowbuf;
+    DevBuf<int> flag;
+    std::vector<long long> lu_first;  // first LU slot of each level: Lo slots p, then Up slots m_l + p
+};
 
-// Lane's share of a row quarter [c0, c1): columns c0 + lane + 32 q.
-__device__ __forceinline__ void bt_prefetch(double (&v)[BT_NPL], const double* row, int c0, int c1, bool on, int lane) {
-#pragma unroll
-    for (int q = 0; q < BT_NPL; ++q) {
-        const int c = c0 + lane + 32 * q;
-        v[q] = (on && c < c1) ? __ldg(row + c) : 0.0;
-    }
-}
-__device__ __forceinline__ double bt_dot(const double (&v)[BT_NPL], const double* row, int c0, int c1,
-                                         const double* x, double acc, int lane) {
-#pragma unroll
-    for (int q = 0; q < BT_NPL; ++q) {
-        const int c = c0 + lane + 32 * q;
-        if (c < c1) acc = fma(v[q], __ldcg(x + c), acc);
-    }
-    for (int c = c0 + lane + 32 * BT_NPL; c < c1; c += 32) acc = fma(row[c], __ldcg(x + c), acc);  // wider blocks
-    return acc;
-}
-// Quarter partials of the block's rows, combined in quarter order (deterministic).
-__device__ __forceinline__ bool bt_combine(double& acc, int lane) {
-    __shared__ double part[256 / 32];
-    const int w = threadIdx.x >> 5;
-    acc = warp_sum(acc);
-    if (lane == 0) part[w] = acc;
-    __syncthreads();
-    if ((w % BT_Q) != 0 || lane != 0) return false;
-    acc = part[w];
-#pragma unroll
-    for (int q = 1; q < BT_Q; ++q) acc += part[w + q];
-    return true;
-}
+CrPlan& plan_of(Ctx& c) { return *static_cast<CrPlan*>(c.cr_plan.get()); }
 
-// y_j -= G y_{j-1} (G = T_{j-1}^T, rows x cols): BT_Q warps per row (two rows
-// per 256-thread block, so a step spreads over ~4x more SMs than one warp per
-// row would), the row's quarter loaded before griddepcontrol.wait.
-__global__ void __launch_bounds__(256) k_bt_fwd(const double* __restrict__ G, int rows, int cols,
-                                                const double* yprev, double* y) {
-    pdl_trigger();
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int row = blockIdx.x * (256 / 32 / BT_Q) + w / BT_Q, qw = w % BT_Q;
-    const bool on = row < rows;
-    const int qlen = (cols + BT_Q - 1) / BT_Q, c0 = qw * qlen, c1 = min(cols, c0 + qlen);
-    const double* g = G + (size_t)(on ? row : 0) * cols;
-    double gv[BT_NPL];
-    bt_prefetch(gv, g, c0, c1, on, lane);
-    pdl_begin();  // y_{j-1} is complete and visible
-    double acc = on ? bt_dot(gv, g, c0, c1, yprev, 0.0, lane) : 0.0;
-    if (bt_combine(acc, lane) && on) y[row] -= acc;
-}
-
-// x_j = Sinv_j y_j - T_j x_{j+1} (T_j: rows x cols_next), BT_Q warps per row
-__global__ void __launch_bounds__(256) k_bt_bwd(const double* __restrict__ Sinv, const double* __restrict__ T,
-                                                int rows, int cols_next, const double* y, const double* xnext,
-                                                double* x) {
-    pdl_trigger();
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int row = blockIdx.x * (256 / 32 / BT_Q) + w / BT_Q, qw = w % BT_Q;
-    const bool on = row < rows;
-    const int qs = (rows + BT_Q - 1) / BT_Q, s0 = qw * qs, s1 = min(rows, s0 + qs);
-    const int qt = (cols_next + BT_Q - 1) / BT_Q, t0 = qw * qt, t1 = min(cols_next, t0 + qt);
-    const double* sr = Sinv + (size_t)(on ? row : 0) * rows;
-    const double* tr = T ? T + (size_t)(on ? row : 0) * cols_next : nullptr;
-    double sv[BT_NPL], tv[BT_NPL];
-    bt_prefetch(sv, sr, s0, s1, on, lane);
-    bt_prefetch(tv, tr, t0, T ? t1 : t0, on && T, lane);
-    pdl_begin();  // x_{j+1} is complete and visible (y_j was finished by the forward sweep)
-    double acc = 0.0;
-    if (on) {
-        acc = bt_dot(sv, sr, s0, s1, y, 0.0, lane);
-        if (T) {
-            double a2 = bt_dot(tv, tr, t0, t1, xnext, 0.0, lane);
-            acc -= a2;
+void run_gj(Ctx& c, CrPlan& pl, int first, int count) {
+    for (int k0 = 0; k0 < pl.S; k0 += GP) {
+        {
+            PROF(c, "k_gj_pivot");
+            launch_k(c, k_gj_pivot, dim3(pl.S / GP, count), 256, 0, (double* const*)(pl.gjmats.p + first), pl.S, k0,
+                     pl.colbuf.p, pl.rowbuf.p, pl.flag.p);
+            CK_LAUNCH();
+        }
+        {
+            PROF(c, "k_gj_update");
+            launch_k(c, k_gj_update, dim3(pl.S / 64, pl.S / GP, count), 256, 0, (double* const*)(pl.gjmats.p + first),
+                     pl.S, k0, (const double*)pl.colbuf.p, (const double*)pl.rowbuf.p);
+            CK_LAUNCH();
         }
     }
-    if (bt_combine(acc, lane) && on) x[row] = acc;
 }
 
 }  // namespace
-
-// In-place inverse of an n x n row-major matrix (dense.cu).
-void block_gj_inplace_pub(Ctx& c, double* W, int n);
 
 void bt_setup(Ctx& c) {
     const Layout& L = c.L;
@@ -374,19 +511,14 @@ void bt_setup(Ctx& c) {
     }
     std::vector<int> sz(nblk, 0);
     for (int r = 0; r < n; ++r) loc[r] = sz[blk[r]]++;
-    std::vector<long long> doff(nblk + 1, 0), eoff(nblk + 1, 0);
-    std::vector<int> voff(nblk + 1, 0);
+    int smax = 0;
     for (int j = 0; j < nblk; ++j) {
         if (sz[j] == 0) throw ConfigError("block-tridiagonal interface solve: empty block");
-        doff[j + 1] = doff[j] + (long long)sz[j] * sz[j];
-        eoff[j + 1] = eoff[j] + (j + 1 < nblk ? (long long)sz[j] * sz[j + 1] : 0);
-        voff[j + 1] = voff[j] + sz[j];
+        smax = std::max(smax, sz[j]);
     }
+    const int S = (smax + 63) / 64 * 64;
     c.bt_nblk = nblk;
     c.bt_sz = sz;
-    c.bt_doff = doff;
-    c.bt_eoff = eoff;
-    c.bt_voff = voff;
     auto up_i = [&](DevBuf<int>& d, const std::vector<int>& h) {
         d.alloc(std::max<size_t>(h.size(), 1));
         CK(cudaMemcpyAsync(d.p, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice, c.st));
@@ -394,119 +526,209 @@ void bt_setup(Ctx& c) {
     up_i(c.bt_blk, blk);
     up_i(c.bt_loc, loc);
     up_i(c.bt_bsz, sz);
-    up_i(c.bt_voffd, voff);
-    c.bt_doffd.alloc(doff.size());
-    c.bt_eoffd.alloc(eoff.size());
-    CK(cudaMemcpyAsync(c.bt_doffd.p, doff.data(), doff.size() * sizeof(long long), cudaMemcpyHostToDevice, c.st));
-    CK(cudaMemcpyAsync(c.bt_eoffd.p, eoff.data(), eoff.size() * sizeof(long long), cudaMemcpyHostToDevice, c.st));
-    c.bt_D.alloc(doff[nblk]);
-    c.bt_Sinv.alloc(doff[nblk]);
-    c.bt_E.alloc(std::max<long long>(eoff[nblk], 1));
-    c.bt_T.alloc(std::max<long long>(eoff[nblk], 1));
-    c.bt_G.alloc(std::max<long long>(eoff[nblk], 1));
-    c.bt_y.alloc(n);
-    c.bt_x.alloc(n);
-    c.bt_sy.alloc(n);
+    auto plp = std::make_shared<CrPlan>();
+    CrPlan& pl = *plp;
+    pl.S = S;
+    pl.nb = nblk;
+    const size_t SS = (size_t)S * S;
+    // active block lists per level
+    std::vector<std::vector<int>> act(1);
+    for (int j = 0; j < nblk; ++j) act[0].push_back(j);
+    while (act.back().size() > 1) {
+        std::vector<int> nx;
+        for (size_t p = 0; p < act.back().size(); p += 2) nx.push_back(act.back()[p]);
+        act.push_back(nx);
+    }
+    const int levels = (int)act.size() - 1;  // levels with an elimination
+    long long slots = 0;
+    for (int l = 0; l <= levels; ++l) {
+        pl.lu_first.push_back(slots);
+        slots += 2 * (long long)act[l].size();
+    }
+    pl.D.alloc(nblk * SS);
+    pl.LU.alloc(std::max<long long>(slots, 1) * SS);
+    pl.P.alloc(nblk * SS);
+    pl.Q.alloc(nblk * SS);
+    pl.cvec.alloc((size_t)nblk * S);
+    c.bt_y.alloc((size_t)nblk * S);
+    c.bt_x.alloc((size_t)nblk * S);
+    auto Dp = [&](int j) { return pl.D.p + j * SS; };
+    auto Lo = [&](int l, int p) { return pl.LU.p + (pl.lu_first[l] + p) * SS; };
+    auto Up = [&](int l, int p) { return pl.LU.p + (pl.lu_first[l] + (long long)act[l].size() + p) * SS; };
+    auto Pp = [&](int j) { return pl.P.p + j * SS; };
+    auto Qp = [&](int j) { return pl.Q.p + j * SS; };
+    auto yv = [&](int j) { return c.bt_y.p + (size_t)j * S; };
+    auto xv = [&](int j) { return c.bt_x.p + (size_t)j * S; };
+    auto cv = [&](int j) { return pl.cvec.p + (size_t)j * S; };
+    std::vector<GemmJob> gemm;
+    std::vector<GemvJob> gemv;
+    std::vector<double*> gjm;
+    auto gj = [&](const std::vector<double*>& mats) {
+        pl.factor.push_back({1, (int)gjm.size(), (int)mats.size()});
+        gjm.insert(gjm.end(), mats.begin(), mats.end());
+        pl.max_batch = std::max(pl.max_batch, (int)mats.size());
+    };
+    auto gemm_launch = [&](const std::vector<GemmJob>& jobs) {
+        if (jobs.empty()) return;
+        pl.factor.push_back({0, (int)gemm.size(), (int)jobs.size()});
+        gemm.insert(gemm.end(), jobs.begin(), jobs.end());
+    };
+    auto gemv_launch = [&](const std::vector<GemvJob>& jobs) {
+        if (jobs.empty()) return;
+        pl.solve.push_back({2, (int)gemv.size(), (int)jobs.size()});
+        gemv.insert(gemv.end(), jobs.begin(), jobs.end());
+    };
+    // factorization (levels), then the solve's launches in order
+    for (int l = 0; l < levels; ++l) {
+        const std::vector<int>& A = act[l];
+        const int m = (int)A.size();
+        std::vector<double*> odd;
+        for (int p = 1; p < m; p += 2) odd.push_back(Dp(A[p]));
+        gj(odd);  // Dinv_o in place of D_o
+        std::vector<GemmJob> pq, ev;
+        for (int p = 1; p < m; p += 2) {
+            const int o = A[p];
+            pq.push_back({Pp(o), nullptr, Dp(o), Lo(l, p), nullptr, nullptr, 1.0, 0.0});
+            if (p + 1 < m) pq.push_back({Qp(o), nullptr, Dp(o), Up(l, p), nullptr, nullptr, 1.0, 0.0});
+        }
+        gemm_launch(pq);
+        for (int p = 0; p < m; p += 2) {
+            const int e = A[p];
+            const bool lo = p >= 1, hi = p + 1 < m;
+            GemmJob d{Dp(e), Dp(e), nullptr, nullptr, nullptr, nullptr, -1.0, -1.0};
+            if (lo) d.A1 = Lo(l, p), d.B1 = Qp(A[p - 1]);
+            if (hi) {
+                if (!d.A1) d.A1 = Up(l, p), d.B1 = Pp(A[p + 1]);
+                else d.A2 = Up(l, p), d.B2 = Pp(A[p + 1]);
+            }
+            if (d.A1) ev.push_back(d);
+            if (p >= 2) ev.push_back({Lo(l + 1, p / 2), nullptr, Lo(l, p), Pp(A[p - 1]), nullptr, nullptr, -1.0, 0.0});
+            if (p + 2 < m) ev.push_back({Up(l + 1, p / 2), nullptr, Up(l, p), Qp(A[p + 1]), nullptr, nullptr, -1.0, 0.0});
+        }
+        gemm_launch(ev);
+        // solve, forward half of level l: c_o = Dinv_o y_o, then the evens
+        std::vector<GemvJob> fo, fe;
+        for (int p = 1; p < m; p += 2) fo.push_back({cv(A[p]), nullptr, Dp(A[p]), yv(A[p]), nullptr, nullptr, 1.0, 0.0});
+        for (int p = 0; p < m; p += 2) {
+            GemvJob j{yv(A[p]), yv(A[p]), nullptr, nullptr, nullptr, nullptr, -1.0, -1.0};
+            if (p >= 1) j.M1 = Lo(l, p), j.v1 = cv(A[p - 1]);
+            if (p + 1 < m) {
+                if (!j.M1) j.M1 = Up(l, p), j.v1 = cv(A[p + 1]);
+                else j.M2 = Up(l, p), j.v2 = cv(A[p + 1]);
+            }
+            fe.push_back(j);
+        }
+        gemv_launch(fo);
+        gemv_launch(fe);
+    }
+    gj({Dp(act[levels][0])});
+    gemv_launch({{xv(act[levels][0]), nullptr, Dp(act[levels][0]), yv(act[levels][0]), nullptr, nullptr, 1.0, 0.0}});
+    for (int l = levels - 1; l >= 0; --l) {  // backward: x_o = c_o - P_o x_{o-} - Q_o x_{o+}
+        const std::vector<int>& A = act[l];
+        const int m = (int)A.size();
+        std::vector<GemvJob> bo;
+        for (int p = 1; p < m; p += 2) {
+            GemvJob j{xv(A[p]), cv(A[p]), Pp(A[p]), xv(A[p - 1]), nullptr, nullptr, -1.0, -1.0};
+            if (p + 1 < m) j.M2 = Qp(A[p]), j.v2 = xv(A[p + 1]);
+            bo.push_back(j);
+        }
+        gemv_launch(bo);
+    }
+    pl.gemm.alloc(std::max<size_t>(gemm.size(), 1));
+    pl.gemv.alloc(std::max<size_t>(gemv.size(), 1));
+    pl.gjmats.alloc(std::max<size_t>(gjm.size(), 1));
+    if (!gemm.empty()) CK(cudaMemcpyAsync(pl.gemm.p, gemm.data(), gemm.size() * sizeof(GemmJob), cudaMemcpyHostToDevice, c.st));
+    if (!gemv.empty()) CK(cudaMemcpyAsync(pl.gemv.p, gemv.data(), gemv.size() * sizeof(GemvJob), cudaMemcpyHostToDevice, c.st));
+    CK(cudaMemcpyAsync(pl.gjmats.p, gjm.data(), gjm.size() * sizeof(double*), cudaMemcpyHostToDevice, c.st));
+    // level-0 Lo_j = Up_{j-1}^T
+    std::vector<double*> td;
+    std::vector<const double*> ts;
+    for (int p = 1; p < nblk; ++p) {
+        td.push_back(Lo(0, p));
+        ts.push_back(Up(0, p - 1));
+    }
+    pl.tr_dst.alloc(std::max<size_t>(td.size(), 1));
+    pl.tr_src.alloc(std::max<size_t>(ts.size(), 1));
+    if (!td.empty()) {
+        CK(cudaMemcpyAsync(pl.tr_dst.p, td.data(), td.size() * sizeof(double*), cudaMemcpyHostToDevice, c.st));
+        CK(cudaMemcpyAsync(pl.tr_src.p, ts.data(), ts.size() * sizeof(const double*), cudaMemcpyHostToDevice, c.st));
+    }
+    pl.colbuf.alloc((size_t)pl.max_batch * S * GP);
+    pl.rowbuf.alloc((size_t)pl.max_batch * S * GP);
+    pl.flag.alloc(1);
     c.hg_x.alloc(n);
     c.hg_y.alloc(n);
     c.hg_z.alloc(n);
     c.hg_xi.alloc(n);
     c.hg_state.alloc(sizeof(HagerState) / sizeof(double) + 1);
+    c.cr_plan = plp;
     CK(cudaStreamSynchronize(c.st));
 }
 
 // Factorisation at every rebuild (after the CSR of K holds the new values).
 void bt_factor(Ctx& c) {
-    const int n = c.dim, nb = c.bt_nblk;
-    c.bt_D.zero(c.st);
-    c.bt_E.zero(c.st);
+    CrPlan& pl = plan_of(c);
+    const int n = c.dim, S = pl.S, nb = pl.nb;
+    const size_t SS = (size_t)S * S;
+    CK(cudaMemsetAsync(pl.D.p, 0, nb * SS * sizeof(double), c.st));
+    CK(cudaMemsetAsync(pl.LU.p, 0, 2 * (size_t)nb * SS * sizeof(double), c.st));  // level-0 Lo and Up slots
+    CK(cudaMemsetAsync(pl.flag.p, 0, sizeof(int), c.st));
     {
         PROF(c, "k_bt_scatter");
-        launch_k(c, k_bt_scatter, cdiv(n, TPB), TPB, 0, c.k_ptr, c.k_col, c.k_val, n, c.bt_blk, c.bt_loc, c.bt_doffd,
-                 c.bt_eoffd, c.bt_bsz, c.bt_D, c.bt_E);
+        launch_k(c, k_cr_scatter, cdiv(n, TPB), TPB, 0, (const int*)c.k_ptr.p, (const int*)c.k_col.p,
+                 (const double*)c.k_val.p, n, (const int*)c.bt_blk.p, (const int*)c.bt_loc.p, S, pl.D.p,
+                 pl.LU.p + (size_t)nb * SS);
         CK_LAUNCH();
     }
-    auto gemm = [&](bool ta, int m, int nn, int kk, const double* A, int lda, const double* Bm, int ldb, double* C,
-                    int ldc, double alpha, const double* C0, int ldc0) {
-        PROF(c, "k_dgemm");
-        const dim3 g(cdiv(nn, 64), cdiv(m, 64));
-        if (ta) launch_k(c, k_dgemm<true>, g, 256, 0, m, nn, kk, A, lda, Bm, ldb, C, ldc, alpha, C0, ldc0);
-        else launch_k(c, k_dgemm<false>, g, 256, 0, m, nn, kk, A, lda, Bm, ldb, C, ldc, alpha, C0, ldc0);
+    {
+        PROF(c, "k_bt_scatter");
+        launch_k(c, k_cr_pad, cdiv((long long)nb * S, TPB), TPB, 0, (const int*)c.bt_bsz.p, nb, S, pl.D.p);
         CK_LAUNCH();
-    };
-    for (int j = 0; j < nb; ++j) {
-        const int s = c.bt_sz[j];
-        double* Sj = c.bt_Sinv.p + c.bt_doff[j];
-        const double* Dj = c.bt_D.p + c.bt_doff[j];
-        if (j == 0) {
-            CK(cudaMemcpyAsync(Sj, Dj, (size_t)s * s * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
+    }
+    if (nb > 1) {
+        PROF(c, "k_transpose");
+        launch_k(c, k_cr_transpose, dim3(S / 32, S / 32, nb - 1), dim3(32, 8), 0, (double* const*)pl.tr_dst.p,
+                 (const double* const*)pl.tr_src.p, S);
+        CK_LAUNCH();
+    }
+    for (const CrLaunch& st : pl.factor) {
+        if (st.kind == 1) {
+            run_gj(c, pl, st.first, st.count);
         } else {
-            const int sp = c.bt_sz[j - 1];
-            const double* Sp = c.bt_Sinv.p + c.bt_doff[j - 1];
-            const double* Ep = c.bt_E.p + c.bt_eoff[j - 1];  // sp x s
-            double* Tp = c.bt_T.p + c.bt_eoff[j - 1];         // sp x s
-            gemm(false, sp, s, sp, Sp, sp, Ep, s, Tp, s, 1.0, nullptr, 0);  // T = Sinv_{j-1} E_{j-1}
-            gemm(true, s, s, sp, Ep, s, Tp, s, Sj, s, -1.0, Dj, s);         // S_j = D_j - E^T T
-            {
-                PROF(c, "k_transpose");
-                launch_k(c, k_transpose, dim3(cdiv(s, 32), cdiv(sp, 32)), dim3(32, 8), 0, Tp, sp, s,
-                         c.bt_G.p + c.bt_eoff[j - 1]);  // G = T^T (s x sp)
-                CK_LAUNCH();
-            }
-        }
-        block_gj_inplace_pub(c, Sj, s);
-        {
-            PROF(c, "k_flag_err");
-            launch_k(c, k_flag_err, 1, 1, 0, c.gj_piv.p + s, c.sc.p, ERR_SINGULAR);
+            PROF(c, "k_cr_gemm");
+            launch_k(c, k_cr_gemm, dim3((S / GT) * (S / GT), 1, st.count), 128, 0,
+                     (const GemmJob*)(pl.gemm.p + st.first), S);
             CK_LAUNCH();
         }
+    }
+    {
+        PROF(c, "k_flag_err");
+        launch_k(c, k_flag_err, 1, 1, 0, (const int*)pl.flag.p, c.sc.p, ERR_SINGULAR);
+        CK_LAUNCH();
     }
 }
 
 // x = M^-1 rhs through K x = J rhs (transposed: x = M^-T rhs = J^T K^-1 rhs).
 void bt_solve_t(Ctx& c, const double* rhs, double* x, int transposed) {
-    const int n = c.dim, nb = c.bt_nblk;
-    double* y = c.bt_y.p;
-    double* xb = c.bt_x.p;
+    CrPlan& pl = plan_of(c);
+    const int n = c.dim, S = pl.S;
+    CK(cudaMemsetAsync(c.bt_y.p, 0, (size_t)pl.nb * S * sizeof(double), c.st));
     {
         PROF(c, "k_bt_gather");
-        launch_k(c, k_bt_gather, cdiv(n, TPB), TPB, 0, rhs, n, c.bt_blk, c.bt_loc, c.bt_voffd, y, transposed);
+        launch_k(c, k_bt_gather, cdiv(n, TPB), TPB, 0, rhs, n, (const int*)c.bt_blk.p, (const int*)c.bt_loc.p, S,
+                 c.bt_y.p, transposed);
         CK_LAUNCH();
     }
-    // block steps with programmatic dependent launch (see k_bt_fwd)
-    auto launch_pdl = [&](auto kern, int grid, auto... args) {
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(grid);
-        cfg.blockDim = dim3(TPB);
-        cfg.dynamicSmemBytes = 0;
-        cfg.stream = c.st;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[0].val.programmaticStreamSerializationAllowed = c.bt_pdl ? 1 : 0;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        CK(cudaLaunchKernelEx(&cfg, kern, args...));
-    };
-    for (int j = 1; j < nb; ++j) {
-        const int s = c.bt_sz[j], sp = c.bt_sz[j - 1];
-        PROF(c, "k_bt_fwd");
-        launch_pdl(k_bt_fwd, cdiv((long long)s * 32 * BT_Q, TPB), (const double*)(c.bt_G.p + c.bt_eoff[j - 1]), s, sp,
-                   (const double*)(y + c.bt_voff[j - 1]), y + c.bt_voff[j]);
-        CK_LAUNCH();
-    }
-    for (int j = nb - 1; j >= 0; --j) {
-        const int s = c.bt_sz[j];
-        const bool last = j == nb - 1;
-        const int sn = last ? 0 : c.bt_sz[j + 1];
-        PROF(c, "k_bt_bwd");
-        launch_pdl(k_bt_bwd, cdiv((long long)s * 32 * BT_Q, TPB), (const double*)(c.bt_Sinv.p + c.bt_doff[j]),
-                   (const double*)(last ? nullptr : c.bt_T.p + c.bt_eoff[j]), s, sn, (const double*)(y + c.bt_voff[j]),
-                   (const double*)(last ? nullptr : xb + c.bt_voff[j + 1]), xb + c.bt_voff[j]);
+    for (const CrLaunch& st : pl.solve) {
+        PROF(c, "k_cr_gemv");
+        launch_k(c, k_cr_gemv, dim3(S / GV_ROWS, st.count), 256, 2 * S * sizeof(double),
+                 (const GemvJob*)(pl.gemv.p + st.first), S);
         CK_LAUNCH();
     }
     {
         PROF(c, "k_bt_unpermute");
-        launch_k(c, k_bt_unpermute, cdiv(n, TPB), TPB, 0, xb, n, c.bt_blk, c.bt_loc, c.bt_voffd, x, transposed);
+        launch_k(c, k_bt_unpermute, cdiv(n, TPB), TPB, 0, (const double*)c.bt_x.p, n, (const int*)c.bt_blk.p,
+                 (const int*)c.bt_loc.p, S, x, transposed);
         CK_LAUNCH();
     }
 }

@@ -273,7 +273,6 @@ void create_ctx(mpm2p_ctx* ctx, const mpm2p_problem* P) {
     if (const char* e = std::getenv("MPM2P_NO_TWIST")) c.no_twist = e[0] == '1';
     if (const char* e = std::getenv("MPM2P_DS_BLK")) c.ds_blk = std::atoi(e);
     if (const char* e = std::getenv("MPM2P_PDL")) c.pdl = e[0] == '1';
-    if (const char* e = std::getenv("MPM2P_BT_PDL")) c.bt_pdl = e[0] != '0';
     if (const char* e = std::getenv("MPM2P_GRAPH_TIMING")) c.graph_timing = e[0] == '1';
     if (const char* e = std::getenv("MPM2P_UPWIND_TILE")) c.upwind_tiled = e[0] != '0';
     if (const char* e = std::getenv("MPM2P_UPWIND_COL")) c.upwind_col = std::atoi(e);

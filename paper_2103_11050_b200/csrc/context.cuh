@@ -5,6 +5,7 @@
 
 #include <cuda_runtime.h>
 
+#include <memory>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -109,13 +110,13 @@ struct Ctx {
     // above the dense limit; MPM2P_IFACE=blocktri forces it, =krylov selects MINRES
     bool use_blocktri = false;
     bool rhs_w = true;  // per-edge + per-cell MPM-2P right-hand side (k_mpm_edges, k_mpm_rhs_w); MPM2P_RHS_W=0: k_mpm_rhs_sub
-    bool bt_pdl = true;  // programmatic dependent launch of the block steps (MPM2P_BT_PDL=0 disables)
+    // block-tridiagonal interface solve (blocktri.cu): block of each unknown,
+    // its position in the block, block sizes; the cyclic-reduction plan
     int bt_nblk = 0;
-    std::vector<int> bt_sz, bt_voff;
-    std::vector<long long> bt_doff, bt_eoff;
-    DevBuf<int> bt_blk, bt_loc, bt_bsz, bt_voffd;
-    DevBuf<long long> bt_doffd, bt_eoffd;
-    DevBuf<double> bt_D, bt_E, bt_Sinv, bt_T, bt_G, bt_y, bt_x, bt_sy;
+    std::vector<int> bt_sz;
+    DevBuf<int> bt_blk, bt_loc, bt_bsz;
+    DevBuf<double> bt_y, bt_x;  // padded block-order work vectors
+    std::shared_ptr<void> cr_plan;
     DevBuf<double> hg_x, hg_y, hg_z, hg_xi, hg_state;  // rcond estimate (bt_rcond)
     // per-solve scratch
     DevBuf<double> X, PU, PB, PS, GZ, WU, ET, RU, RS, skel, resid, delta, corr;
