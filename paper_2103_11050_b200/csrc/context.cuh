@@ -5,6 +5,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <memory>
 #include <string>
 #include <unordered_map>
@@ -264,6 +265,21 @@ inline void launch_k(const Ctx& c, void (*kern)(KArgs...), dim3 grid, dim3 block
 // Grid for a grid-stride reduction kernel of 256-thread blocks over `work`
 // items: one wave of resident blocks (at most 8 per SM, which the reduction
 // partial buffer c.red is sized for), never more blocks than items need.
+// Per-device cache of a launch attribute / occupancy figure: function
+// attributes and occupancy are properties of the device, so a process with
+// contexts on several devices keeps one value per device ordinal.
+struct DeviceCache {
+    std::atomic<int> v[64];
+    DeviceCache() {
+        for (auto& x : v) x.store(-1);
+    }
+    std::atomic<int>& at() {
+        int d = 0;
+        cudaGetDevice(&d);
+        return v[d & 63];
+    }
+};
+
 template <typename... KArgs>
 inline int red_blocks(Ctx& c, void (*kern)(KArgs...), long long work) {
     int& n = c.occ[(const void*)kern];

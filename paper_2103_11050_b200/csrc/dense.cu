@@ -823,10 +823,12 @@ void block_gj_inplace(Ctx& c, double* W, int n) {
 // k_gj_pp on the padded pair (W0 holds the matrix; the inverse ends in
 // W[nb % 2]).
 void gj_pp_run(Ctx& c, double* W0, double* W1, int nb, int ld, int n) {
-    static int per_sm = -1;
-    if (per_sm < 0) {  // set once, outside any graph capture
+    static DeviceCache occ;
+    int per_sm = occ.at().load();
+    if (per_sm < 0) {  // once per device, outside any graph capture
         CK(cudaFuncSetAttribute(k_gj_pp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PP_SMEM));
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gj_pp, 256, PP_SMEM));
+        occ.at().store(per_sm);
     }
     const int cap = per_sm * c.num_sms;
     if (cap < 2) throw CudaError("dense_inverse: ping-pong Gauss-Jordan does not fit");
@@ -1079,13 +1081,13 @@ template <bool ACC>
 void gemv_dispatch(Ctx& c, const double* A, const double* x, double* y, int n) {
     PROF(c, "k_gemv");
     if ((n & 1) == 0 && n <= GEMV_TMA_MAX) {
-        static bool attr = false;  // once, outside any graph capture (first use is eager)
-        if (!attr) {
+        static DeviceCache attr;  // once per device, outside any graph capture (first use is eager)
+        if (attr.at().load() < 0) {
             CK(cudaFuncSetAttribute(k_gemv_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     9 * GEMV_TMA_MAX * (int)sizeof(double)));
             CK(cudaFuncSetAttribute(k_gemv_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     9 * GEMV_TMA_MAX * (int)sizeof(double)));
-            attr = true;
+            attr.at().store(1);
         }
         launch_k(c, k_gemv_tma<ACC>, cdiv(n, 8), 256, (size_t)9 * n * sizeof(double), A, x, y, n);
     } else {

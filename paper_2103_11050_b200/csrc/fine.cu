@@ -494,9 +494,12 @@ void fine_launch(Ctx& c, const FineArgs& fa) {
     CK(cudaMemcpyAsync(c.f_A0i.p, c.f_A0.p, (size_t)L.n_sub * L.n_sub * sizeof(double), cudaMemcpyDeviceToDevice,
                        c.st));
     block_gj_inplace_pub(c, c.f_A0i.p, L.n_sub);  // SPD: pivot-free blocked Gauss-Jordan
-    static int per_sm[64] = {0};
-    int& occ = per_sm[B];
-    if (occ == 0) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fine_pcg<B>, FWPB * 32, 0));
+    static DeviceCache per_sm;  // one per instantiation B, per device
+    int occ = per_sm.at().load();
+    if (occ < 0) {
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fine_pcg<B>, FWPB * 32, 0));
+        per_sm.at().store(occ);
+    }
     if (occ < 1) throw CudaError("fine solve: the PCG kernel does not fit on an SM");
     const int blocks = std::max(1, std::min(occ * c.num_sms, cdiv(L.n_sub, FWPB)));
     FineArgs a = fa;
@@ -523,7 +526,7 @@ void fine_setup(Ctx& c) {
         MPM2P_FINE_WIDTHS(X)
 #undef X
         default:
-            throw ConfigError("fine solve: unsupported subdomain width " + std::to_string(L.snx));
+            throw CapacityError("fine solve: subdomain width " + std::to_string(L.snx) + " has no PCG kernel instantiation (supported: 4, 8, 10, 12, 16, 20, 24, 32)");
     }
     const size_t nc = L.cells(), nb = (size_t)L.n_sub * L.ncs, ns = L.n_sub;
     c.f_T.alloc(L.faces());
@@ -579,7 +582,7 @@ void fine_solve(Ctx& c, const double* kappa, double* p, double* u, bool cold) {
         MPM2P_FINE_WIDTHS(X)
 #undef X
         default:
-            throw ConfigError("fine solve: unsupported subdomain width");
+            throw CapacityError("fine solve: subdomain width has no PCG kernel instantiation");
     }
     {
         PROF(c, "k_fine_velocity");

@@ -232,8 +232,12 @@ void krylov_prepare(Ctx& c) {
 // x = M^-1 rhs by MINRES on K x = J rhs.
 void krylov_solve(Ctx& c, const double* rhs, double* x) {
     const int n = c.dim;
-    static int per_sm = -1;
-    if (per_sm < 0) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_minres, KTPB, 0));
+    static DeviceCache occ;
+    int per_sm = occ.at().load();
+    if (per_sm < 0) {
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_minres, KTPB, 0));
+        occ.at().store(per_sm);
+    }
     if (per_sm < 1) throw CudaError("krylov_solve: cooperative kernel does not fit on an SM");
     const int blocks = std::max(1, std::min(per_sm * c.num_sms, cdiv(n, KTPB)));
     double* wk = c.kr_work.p;

@@ -1202,15 +1202,15 @@ __global__ void __launch_bounds__(twist_threads<B>()) k_part_solve_t(Layout L, i
 // Dynamic shared memory opt-in for each instantiation (once, outside capture).
 template <int B>
 void twist_configure() {
-    static bool done = false;
-    if (done || !twist_warps<B>()) return;
+    static DeviceCache done;  // per device
+    if (done.at().load() > 0 || !twist_warps<B>()) return;
     const int bytes = (int)twist_smem_bytes<B>();
     CK(cudaFuncSetAttribute(k_ds_solve_t<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     CK(cudaFuncSetAttribute(k_factor1_t<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     CK(cudaFuncSetAttribute(k_hom_solve_t<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     CK(cudaFuncSetAttribute(k_part_solve_t<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     CK(cudaFuncSetAttribute(k_ds_sweep_t<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    done = true;
+    done.at().store(1);
 }
 
 // Subdomain widths with a register-window instantiation; others use band.cuh.

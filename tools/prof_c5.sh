@@ -1,7 +1,12 @@
-# ncu --set full capture of selected C5 kernels (run on the GPU box after a plain run exits 0)
-# usage: bash tools/prof_c5.sh TAG "regex" COUNT
-TAG=${1:-c5}; RX=${2:-"k_ds_u_div|k_mpm_rhs|k_ds_prep|k_upwind_col|k_kappa_col"}; CNT=${3:-5}
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-python bench.py --config C5 --steps 2 --warmup 3 --skip-e2e --skip-cpu --profile-steps 0 --also "" > gpurun_out/${TAG}_plain.log 2>&1 || { echo plain run failed; tail gpurun_out/${TAG}_plain.log; exit 1; }
-ncu --set full --import-source on --clock-control none -k "regex:${RX}" -c ${CNT} -o gpurun_out/${TAG} python bench.py --config C5 --steps 2 --warmup 3 --skip-e2e --skip-cpu --profile-steps 0 --also "" > gpurun_out/${TAG}_ncu.log 2>&1
+# ncu --set full captures of the C5 step's kernels (run on the GPU box from the
+# repo root, after a plain run exits 0). The MPM-2P kernels in one pass; the
+# interface GEMV separately, skipping the initial solve's rcond-estimate launches.
+TAG=${1:-full_c5}
+set -x
+python bench.py --config C5 --steps 2 --warmup 3 --skip-e2e --skip-cpu --profile-steps 0 --also "" > gpurun_out/${TAG}_plain.log 2>&1 || exit 1
+ncu --set full --import-source on --clock-control none \
+    -k "regex:k_ds_blk_factor|k_ds_blk_solve|k_part_solve|k_mpm_rhs_w|k_mpm_edges|k_ds_u_div|k_ds_prep|k_upwind_col|k_kappa_col|k_recon_mpm" \
+    -c 11 -o gpurun_out/${TAG}_a python bench.py --config C5 --steps 2 --warmup 3 --skip-e2e --skip-cpu --profile-steps 0 --also "" > gpurun_out/${TAG}_a.log 2>&1
+ncu --set full --import-source on --clock-control none -k "regex:k_cr_gemv" --launch-skip 300 -c 15 \
+    -o gpurun_out/${TAG}_b python bench.py --config C5 --steps 2 --warmup 3 --skip-e2e --skip-cpu --profile-steps 0 --also "" > gpurun_out/${TAG}_b.log 2>&1
 echo rc=$?
