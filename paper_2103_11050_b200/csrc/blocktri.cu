@@ -229,7 +229,11 @@ struct GemvJob {
     const double* v2;
     double s1, s2;
 };
-constexpr int GV_ROWS = 32;  // rows per CTA (8 warps x 4 rows, the 4 rows' loads interleaved)
+// RPW rows per warp, 8 warps per CTA (the rows' loads interleaved); the
+// launcher picks RPW = 4 for wide levels and RPW = 1 for the last levels of
+// the reduction, where few blocks remain and more warps per row set hide
+// the load latency
+template <int RPW>
 __global__ void __launch_bounds__(256) k_cr_gemv(const GemvJob* __restrict__ jobs, int S) {
     pdl_begin();
     extern __shared__ double vs[];  // 2 S
@@ -240,31 +244,35 @@ __global__ void __launch_bounds__(256) k_cr_gemv(const GemvJob* __restrict__ job
     }
     __syncthreads();
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int r0 = blockIdx.x * GV_ROWS + w * 4;
-    double a[4] = {0.0, 0.0, 0.0, 0.0};
+    const int r0 = (blockIdx.x * 8 + w) * RPW;
+    double a[RPW];
+#pragma unroll
+    for (int q = 0; q < RPW; ++q) a[q] = 0.0;
     for (int term = 0; term < 2; ++term) {
         const double* M = term ? jb.M2 : jb.M1;
         if (!M) continue;
         const double s = term ? jb.s2 : jb.s1;
         const double* v = vs + term * S;
-        double t[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int c = lane; c < S; c += 64) {
-            double m[4][2];
+        double t[RPW];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < RPW; ++q) t[q] = 0.0;
+        for (int c = lane; c < S; c += 64) {  // S is a multiple of 64
+            double m[RPW][2];
+#pragma unroll
+            for (int q = 0; q < RPW; ++q) {
                 m[q][0] = __ldg(M + (size_t)(r0 + q) * S + c);
-                m[q][1] = c + 32 < S ? __ldg(M + (size_t)(r0 + q) * S + c + 32) : 0.0;
+                m[q][1] = __ldg(M + (size_t)(r0 + q) * S + c + 32);
             }
-            const double v0 = v[c], v1 = c + 32 < S ? v[c + 32] : 0.0;
+            const double v0 = v[c], v1 = v[c + 32];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) t[q] = fma(m[q][1], v1, fma(m[q][0], v0, t[q]));
+            for (int q = 0; q < RPW; ++q) t[q] = fma(m[q][1], v1, fma(m[q][0], v0, t[q]));
         }
 #pragma unroll
-        for (int q = 0; q < 4; ++q) a[q] += s * warp_sum(t[q]);
+        for (int q = 0; q < RPW; ++q) a[q] += s * warp_sum(t[q]);
     }
     if (lane == 0)  // warp_sum leaves the total in lane 0
 #pragma unroll
-        for (int q = 0; q < 4; ++q) jb.out[r0 + q] = (jb.base ? jb.base[r0 + q] : 0.0) + a[q];
+        for (int q = 0; q < RPW; ++q) jb.out[r0 + q] = (jb.base ? jb.base[r0 + q] : 0.0) + a[q];
 }
 
 // D_j (padded, identity on the pad) and Up_j = K[block j, block j+1] from the CSR of K
@@ -721,8 +729,12 @@ void bt_solve_t(Ctx& c, const double* rhs, double* x, int transposed) {
     }
     for (const CrLaunch& st : pl.solve) {
         PROF(c, "k_cr_gemv");
-        launch_k(c, k_cr_gemv, dim3(S / GV_ROWS, st.count), 256, 2 * S * sizeof(double),
-                 (const GemvJob*)(pl.gemv.p + st.first), S);
+        if ((long long)st.count * (S / 32) >= 4LL * c.num_sms)
+            launch_k(c, k_cr_gemv<4>, dim3(S / 32, st.count), 256, 2 * S * sizeof(double),
+                     (const GemvJob*)(pl.gemv.p + st.first), S);
+        else
+            launch_k(c, k_cr_gemv<1>, dim3(S / 8, st.count), 256, 2 * S * sizeof(double),
+                     (const GemvJob*)(pl.gemv.p + st.first), S);
         CK_LAUNCH();
     }
     {
