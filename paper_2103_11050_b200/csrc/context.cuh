@@ -130,7 +130,6 @@ struct Ctx {
     bool sep_repair = false;  // separable repair solve (sep_repair_setup) instead of the dense inverse
     DevBuf<double> sep_qx, sep_qy, sep_lam, sep_z1, sep_z2;
     bool rhs_sub = true;  // k_mpm_rhs_sub, one CTA per subdomain (MPM2P_RHS_SUB=0: one thread per cell)
-    int upwind_rb = 1;         // rows per k_upwind_col chunk (MPM2P_UPWIND_RB = 1 | 2 | 4)
     int kappa_col = -1;        // k_kappa_col: -1 auto (long row segments), 1 always, 0 never (MPM2P_KAPPA_COL)
     int upwind_col = -1;       // k_upwind_col: -1 auto (long row segments), 1 always, 0 never (MPM2P_UPWIND_COL)
     bool upwind_tiled = true;  // k_upwind_tile (MPM2P_UPWIND_TILE=0: one thread per cell, k_upwind)

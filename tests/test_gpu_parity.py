@@ -450,8 +450,6 @@ def test_split_downscale_matches_fused(oracle, name):
 
 UPWIND_VARIANTS = {
     "col": dict(MPM2P_UPWIND_COL=1),
-    "col_rb1": dict(MPM2P_UPWIND_COL=1, MPM2P_UPWIND_RB=1),
-    "col_rb4": dict(MPM2P_UPWIND_COL=1, MPM2P_UPWIND_RB=4),
     "tile": dict(MPM2P_UPWIND_COL=0, MPM2P_UPWIND_TILE=1),
     "cell": dict(MPM2P_UPWIND_COL=0, MPM2P_UPWIND_TILE=0),
 }
@@ -464,7 +462,7 @@ def test_upwind_variants_bitwise(name):
     c = configs.build(name, te_override=31)
     runs = {k: _sim_env(c.problem, **env).run(c.split, c.s0(), c.inflow_sat) for k, env in UPWIND_VARIANTS.items()}
     a = runs["col"]
-    for k in ("col_rb1", "col_rb4", "tile", "cell"):
+    for k in ("tile", "cell"):
         b = runs[k]
         assert np.array_equal(a.s_final, b.s_final) and np.array_equal(a.u_final, b.u_final), k
         assert [s["dt"] for s in a.record.steps] == [s["dt"] for s in b.record.steps], k
