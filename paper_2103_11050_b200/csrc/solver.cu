@@ -1755,20 +1755,39 @@ __global__ void k_part_psum(Layout L, int max_rhs, const double* __restrict__ X,
 // R[sy][sx] = resid[sy nsx + sx]. One small GEMM per launch, one thread per
 // output: C[m x n] = op(A) op(B), op(X) = X or X^T (row-major, square
 // factors), optionally divided by (ly_i + lx_j).
-__global__ void k_sep_gemm(int m, int n, int kk, const double* __restrict__ A, int ta, const double* __restrict__ Bm,
-                           int tb, double* __restrict__ C, const double* __restrict__ lx, const double* __restrict__ ly) {
+// 32 x 32 output tile per 256-thread block, k in slabs of 32 staged in
+// shared memory (all of a slab's loads issued together), 4 outputs per thread
+__global__ void __launch_bounds__(256) k_sep_gemm(int m, int n, int kk, const double* __restrict__ A, int ta,
+                                                  const double* __restrict__ Bm, int tb, double* __restrict__ C,
+                                                  const double* __restrict__ lx, const double* __restrict__ ly) {
     pdl_begin();
-    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= m * n) return;
-    const int i = idx / n, j = idx % n;
-    double acc = 0.0;
-    for (int t = 0; t < kk; ++t) {
-        const double a = ta ? A[(size_t)t * m + i] : A[(size_t)i * kk + t];
-        const double b = tb ? Bm[(size_t)j * kk + t] : Bm[(size_t)t * n + j];
-        acc = fma(a, b, acc);
+    __shared__ double As[32][33], Bs[32][33];
+    const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // output column tx, rows ty + 8 q
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int k0 = 0; k0 < kk; k0 += 32) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int r = ty + 8 * q;  // As[r][c] = op(A)[i0 + r][k0 + c]; Bs[r][c] = op(B)[k0 + r][j0 + c]
+            const int ia = i0 + r, ka = k0 + tx;
+            As[r][tx] = (ia < m && ka < kk) ? (ta ? A[(size_t)ka * m + ia] : A[(size_t)ia * kk + ka]) : 0.0;
+            const int kb = k0 + r, jb = j0 + tx;
+            Bs[r][tx] = (kb < kk && jb < n) ? (tb ? Bm[(size_t)jb * kk + kb] : Bm[(size_t)kb * n + jb]) : 0.0;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int t = 0; t < 32; ++t) {
+            const double b = Bs[t][tx];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[q] = fma(As[ty + 8 * q][t], b, acc[q]);
+        }
+        __syncthreads();
     }
-    if (lx) acc /= (ly[i] + lx[j]);
-    C[idx] = acc;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int i = i0 + ty + 8 * q, j = j0 + tx;
+        if (i < m && j < n) C[(size_t)i * n + j] = lx ? acc[q] / (ly[i] + lx[j]) : acc[q];
+    }
 }
 
 __global__ void k_static(Layout L, const double* __restrict__ q, const int* __restrict__ bc_kind,
@@ -2040,7 +2059,8 @@ void downscale(Ctx& c, const double* kappa, bool skel_given) {
         CK_LAUNCH();
     }
     if (c.repair_active && c.sep_repair) {  // delta = Qy [(Qy^T R Qx) ./ (ly + lx)] Qx^T
-        const int nx = L.nsx, ny = L.nsy, g = cdiv((long long)nx * ny, TPB);
+        const int nx = L.nsx, ny = L.nsy;
+        const dim3 g(cdiv(nx, 32), cdiv(ny, 32));
         const double* lx = c.sep_lam.p;
         const double* ly = c.sep_lam.p + nx;
         {
