@@ -152,6 +152,8 @@ def kernel_work(name, cfg, sz, dim):
         # velocity scatter: X (downscaled potential), two faces of T, q read; two faces of u written
         "k_ds_u_div": ("hbm", 48.0 * cells),
         "k_ds_prep": ("hbm", 72.0 * cells),
+        # downscale rhs alone (operator formed by the factor): q read, X written; edges: RU/skel in, EU/ET out
+        "k_ds_rhs": ("hbm", 16.0 * cells + 40.0 * ns * sz.sub_nx * 4),
         "k_ds_u": ("hbm", 32.0 * faces),
         "k_divres": ("hbm", 24.0 * cells + 8.0 * faces),
         "k_trans": ("hbm", 16.0 * cells + 8.0 * faces),

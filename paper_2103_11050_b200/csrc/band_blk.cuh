@@ -57,24 +57,63 @@ struct BlkTile {
 // diagonal tile (tridiagonal: diag, west, and the mirrored west coupling of
 // the next row), the west coupling of row 8t into tile t-1 (entry (0,7)) and
 // the south couplings into tile t-NT (diagonal). Rows >= n are identity rows.
+// A source's fetch() issues raw loads only (clamped, always-valid addresses):
+// a loaded value is first touched one panel later, when the row enters the
+// window, so the load never stalls the panel that issues it; decode() forms
+// the row's diag / west / next row's west / south / rhs from them then.
 struct BlkRowData {
-    double d, w, w1, s, b;  // raw diag, west, west of the next row, south, rhs
+    double a0, a1, a2, a3, b;
 };
-// Raw loads only (clamped, always-valid addresses): a loaded value is first
-// touched one panel later, when the row enters the window, so the load
-// never stalls the panel that issues it.
-__device__ __forceinline__ BlkRowData blk_fetch(const BandRows& A, const double* y, int n, int row) {
-    const int rr = row < n ? row : n - 1;
-    const int r1 = row + 1 < n ? row + 1 : n - 1;
-    return BlkRowData{A.diag[rr], A.offw[rr], A.offw[r1], A.offs[rr], y[rr]};
-}
+// the stored band rows BD / BW / BS of k_ds_prep / k_band_entries
+struct BlkBandSrc {
+    BandRows A;
+    const double* y;
+    int n;
+    __device__ __forceinline__ BlkRowData fetch(int row) const {
+        const int rr = row < n ? row : n - 1;
+        const int r1 = row + 1 < n ? row + 1 : n - 1;
+        return BlkRowData{A.diag[rr], A.offw[rr], A.offw[r1], A.offs[rr], y[rr]};
+    }
+    __device__ __forceinline__ void decode(int, const BlkRowData& e, double& d, double& w, double& w1,
+                                           double& s) const {
+        d = e.a0, w = e.a1, w1 = e.a2, s = e.a3;
+    }
+};
+// the downscale operator straight from the global transmissibilities T of
+// kappa_n (pure Neumann, anchor cell 0; k_ds_prep's rules and summation
+// order, mrcm.cpp:391-411): no band rows are written or read back
+struct BlkTransSrc {
+    const double* T;
+    const double* y;
+    int n, snx, sny, nx, vcount, i0, j0;
+    __device__ __forceinline__ BlkRowData fetch(int row) const {
+        const int rr = row < n ? row : n - 1;
+        const int ii = rr % snx, jj = rr / snx, i = i0 + ii, j = j0 + jj;
+        const int vf = j * (nx + 1) + i, hf = vcount + j * nx + i;
+        return BlkRowData{T[vf], T[vf + 1], T[hf], T[hf + nx], y[rr]};  // W, E, S, N faces
+    }
+    __device__ __forceinline__ void decode(int row, const BlkRowData& e, double& d, double& w, double& w1,
+                                           double& s) const {
+        const int rr = row < n ? row : n - 1;
+        const int ii = rr % snx, jj = rr / snx;
+        double diag = 0.0;
+        if (ii > 0) diag += e.a0;
+        if (ii < snx - 1) diag += e.a1;
+        if (jj > 0) diag += e.a2;
+        if (jj < sny - 1) diag += e.a3;
+        d = rr == 0 ? 1.0 : diag;
+        w = (ii > 0 && rr != 1) ? e.a0 : 0.0;
+        w1 = (ii + 1 < snx && rr != 0) ? e.a1 : 0.0;  // the next row's west coupling is this cell's east face
+        s = (jj > 0 && rr != snx) ? e.a2 : 0.0;
+    }
+};
 
 // Factorisation with the forward substitution of one right-hand side fused
 // in. y (length n): rhs in, untouched. Xs: n*B doubles, Ts: n doubles
 // (per-panel X fragments and t1 = G y1). sm: blk_smem_doubles<B>() doubles of
 // this warp's shared memory. Returns false if a pivot block is not SPD.
-template <int B>
-__device__ bool blk_factor_fwd(int n, const BandRows A, const double* y, double* Xs, double* Ts, double* sm) {
+template <int B, class Src>
+__device__ bool blk_factor_fwd(int n, const Src& src, double* Xs, double* Ts, double* sm) {
     constexpr int NT = blk_nt<B>();
     static_assert(B % 8 == 0 && NT >= 2, "blocked band solver: B must be a multiple of 8, >= 16");
     const int lane = threadIdx.x & 31;
@@ -96,8 +135,10 @@ __device__ bool blk_factor_fwd(int n, const BandRows A, const double* y, double*
     auto place = [&](int I, int row0, const BlkRowData& e) {
         const int row = row0 + r;
         const bool in = row < n;
-        const double d = in ? e.d : 1.0, wv = in ? -e.w : 0.0, sv = in ? -e.s : 0.0;
-        const double w1 = (row + 1 < n && r < 7) ? -e.w1 : 0.0;
+        double ed, ew, ew1, es;
+        src.decode(row, e, ed, ew, ew1, es);
+        const double d = in ? ed : 1.0, wv = in ? -ew : 0.0, sv = in ? -es : 0.0;
+        const double w1 = (row + 1 < n && r < 7) ? -ew1 : 0.0;
         w[I][I].v[0] = c0 == r ? d : (c0 == r - 1 ? wv : (c0 == r + 1 ? w1 : 0.0));
         w[I][I].v[1] = c1 == r ? d : (c1 == r - 1 ? wv : (c1 == r + 1 ? w1 : 0.0));
         yw[I] = in ? e.b : 0.0;
@@ -109,13 +150,13 @@ __device__ bool blk_factor_fwd(int n, const BandRows A, const double* y, double*
     };
     // initial window: row tiles 0..NT
 #pragma unroll
-    for (int I = 0; I <= NT; ++I) place(I, 8 * I, blk_fetch(A, y, n, 8 * I + r));
+    for (int I = 0; I <= NT; ++I) place(I, 8 * I, src.fetch(8 * I + r));
     const int np = n / 8;
     // rows entering at the end of panels 0 and 1; each panel refetches its slot
     // for two panels ahead. The loop is unrolled by two so the in-flight loads
     // are never moved between registers (a move waits for the load)
-    BlkRowData e0 = blk_fetch(A, y, n, 8 * (NT + 1) + r);
-    BlkRowData e1 = blk_fetch(A, y, n, 8 * (NT + 2) + r);
+    BlkRowData e0 = src.fetch(8 * (NT + 1) + r);
+    BlkRowData e1 = src.fetch(8 * (NT + 2) + r);
     bool ok = true;
     auto panel = [&](const int p, BlkRowData& ent) {
         const int k0 = 8 * p;
@@ -237,7 +278,7 @@ __device__ bool blk_factor_fwd(int n, const BandRows A, const double* y, double*
 #pragma unroll
         for (int J = 0; J < NT; ++J) w[NT][J].v[0] = w[NT][J].v[1] = 0.0;
         place(NT, k0 + 8 * (NT + 1), ent);
-        ent = blk_fetch(A, y, n, k0 + 8 * (NT + 3) + r);
+        ent = src.fetch(k0 + 8 * (NT + 3) + r);
         __syncwarp();  // shared buffers are rewritten by the next panel
     };
     for (int p = 0; p < np; p += 2) {  // np = B^2/8 is even

@@ -612,10 +612,12 @@ bool fine_run_step(Ctx& c, Driver& d, mpm2p_step_record* out) {
     } catch (...) {
         c.outlet_s = nullptr;
         c.trans_fresh = false;
+        c.kappa_checked = false;
         throw;
     }
     c.outlet_s = nullptr;
     c.trans_fresh = false;
+        c.kappa_checked = false;
     const Scalars& s = sync_scalars(c);
     note(d, s);
     const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -725,6 +727,7 @@ bool run_step(mpm2p_ctx* ctx, mpm2p_step_record* out) {
         }
         c.outlet_s = nullptr;
         c.trans_fresh = false;
+        c.kappa_checked = false;
     };
     if (c.profiling || !c.use_graphs) {
         try {
@@ -732,6 +735,7 @@ bool run_step(mpm2p_ctx* ctx, mpm2p_step_record* out) {
         } catch (...) {
             c.outlet_s = nullptr;
             c.trans_fresh = false;
+        c.kappa_checked = false;
             throw;
         }
     } else {
@@ -746,6 +750,7 @@ bool run_step(mpm2p_ctx* ctx, mpm2p_step_record* out) {
             } catch (...) {
                 c.outlet_s = nullptr;
                 c.trans_fresh = false;
+        c.kappa_checked = false;
                 cudaGraph_t dummy = nullptr;
                 cudaStreamEndCapture(c.st, &dummy);
                 if (dummy) cudaGraphDestroy(dummy);
@@ -1033,6 +1038,8 @@ int mpm2p_mrcm_solve(mpm2p_ctx* ctx, const double* kappa, const double* bm, cons
                      double* coeffs, mpm2p_downscale_info* info, mpm2p_counters* counters) {
     return guarded(ctx, [&] {
         Ctx& c = ctx->c;
+        c.trans_fresh = false;  // a caller's kappa: T and the kappa guard are formed here
+        c.kappa_checked = false;
         const Layout& L = c.L;
         c.c_hom = c.c_part = c.c_down = c.c_fine = c.c_iface = 0;
         upload(c, c.kappa_n, kappa, L.cells());
@@ -1056,6 +1063,8 @@ int mpm2p_mpm_update(mpm2p_ctx* ctx, const double* kappa_n, double* p, double* u
                      mpm2p_downscale_info* info, mpm2p_counters* counters) {
     return guarded(ctx, [&] {
         Ctx& c = ctx->c;
+        c.trans_fresh = false;  // a caller's kappa: T and the kappa guard are formed here
+        c.kappa_checked = false;
         const Layout& L = c.L;
         if (!c.has_basis) throw ConfigError("mpm_update: no basis installed (call mrcm_solve first)");
         c.c_hom = c.c_part = c.c_down = c.c_fine = c.c_iface = 0;
@@ -1110,6 +1119,8 @@ int mpm2p_compute_basis_set(mpm2p_ctx* ctx, const double* kappa, const double* b
                             mpm2p_counters* counters) {
     return guarded(ctx, [&] {
         Ctx& c = ctx->c;
+        c.trans_fresh = false;  // a caller's kappa: T and the kappa guard are formed here
+        c.kappa_checked = false;
         const Layout& L = c.L;
         c.c_hom = c.c_part = c.c_down = c.c_fine = c.c_iface = 0;
         upload(c, c.kappa_n, kappa, L.cells());
@@ -1120,6 +1131,7 @@ int mpm2p_compute_basis_set(mpm2p_ctx* ctx, const double* kappa, const double* b
         }
         if (!given) launch_beta(c, c.kappa_n);
         c.trans_fresh = false;
+        c.kappa_checked = false;
         launch_trans(c, c.kappa_n);
         launch_basis_core(c, c.kappa_n);
         sync_scalars(c);
@@ -1234,6 +1246,8 @@ int mpm2p_downscale(mpm2p_ctx* ctx, const double* kappa, const double* p_local, 
                     const double* flux, double* p, double* u, mpm2p_downscale_info* info, mpm2p_counters* counters) {
     return guarded(ctx, [&] {
         Ctx& c = ctx->c;
+        c.trans_fresh = false;  // a caller's kappa: T and the kappa guard are formed here
+        c.kappa_checked = false;
         const Layout& L = c.L;
         c.c_hom = c.c_part = c.c_down = c.c_fine = c.c_iface = 0;
         LocalBufs b;

@@ -170,6 +170,7 @@ struct Ctx {
     bool pdl = false;  // programmatic dependent launch between kernels (MPM2P_PDL=1; measured neutral on C2)
     bool no_regband = false;  // MPM2P_NO_REGBAND=1: generic shared-memory band kernels only
     bool no_twist = false;    // MPM2P_NO_TWIST=1: one-sided register-window band solves
+    bool kappa_checked = false;  // the current kappa came from the driver's k_kappa (already guarded)
     int ds_blk = -1;          // fused downscale on the DMMA blocked solver (band_blk.cuh): -1 auto (B = 24, 32), 0/1 (MPM2P_DS_BLK)
     bool twist_ok = false;    // two-sided band solves enabled for this problem (latency-bound regime)
     bool twist_store = false; // rebuild factor stored in the two-sided layout (band_twist.cuh)

@@ -790,6 +790,63 @@ __global__ void k_ds_prep(Layout L, const double* __restrict__ kappa, const doub
     Xd[o] = b;
 }
 
+// The downscale right-hand side alone (k_ds_prep mode 2's output, for the
+// paths whose operator is formed elsewhere: the split factor, the blocked
+// factor from T), in two kernels. k_ds_edges: per subdomain-boundary edge,
+// the imposed outward flux (skeleton average + interface correction, or the
+// recon trace + the grounded delta) into EU (kept for the scatter) and ET.
+// k_ds_rhs: per cell q vol minus its edges' un * area in W, E, S, N order,
+// anchor row 0 (the same arithmetic as k_ds_prep).
+__global__ void __launch_bounds__(256) k_ds_edges(Layout L, const int* __restrict__ bc_kind,
+                                                  const double* __restrict__ skel, const double* __restrict__ corr,
+                                                  const double* __restrict__ RU, const double* __restrict__ delta,
+                                                  int grounded, double* __restrict__ EU, double* __restrict__ ET) {
+    pdl_begin();
+    const int ne = L.n_sub * L.nbe;
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < ne; x += gridDim.x * blockDim.x) {
+        const int s = x / L.nbe, idx = x % L.nbe;
+        const EdgeInfo e = L.edge(s, idx);
+        double un;
+        if (e.iface >= 0) {
+            un = e.sign * (skel[L.skel_index(e.iface, e.pos)] + corr[e.iface]);
+        } else {
+            un = RU[x];
+            if (grounded && bc_kind[e.gbc] == BC_PRESSURE) un += delta[s];
+        }
+        EU[x] = un;
+        ET[x] = un;
+    }
+}
+
+// kappa (nullable) is checked as k_ds_prep does when it did not come from
+// the driver's k_kappa
+__global__ void __launch_bounds__(256) k_ds_rhs(Layout L, const double* __restrict__ kappa,
+                                                const double* __restrict__ q, const double* __restrict__ ET,
+                                                double* __restrict__ Xd, Scalars* sc) {
+    pdl_begin();
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < L.cells(); c += gridDim.x * blockDim.x) {
+        const int i = c % L.nx, j = c / L.nx;
+        const int s = (j / L.sny) * L.nsx + i / L.snx;
+        const int ii = i % L.snx, jj = j % L.sny, r = jj * L.snx + ii;
+        const size_t eo = (size_t)s * L.nbe;
+        const bool bw = ii == 0, be = ii == L.snx - 1, bs = jj == 0, bn = jj == L.sny - 1;
+        const double qc = q[c];
+        const double tw = bw ? ET[eo + jj] : 0.0, te = be ? ET[eo + L.sny + jj] : 0.0;
+        const double ts = bs ? ET[eo + 2 * L.sny + ii] : 0.0, tn = bn ? ET[eo + 2 * L.sny + L.snx + ii] : 0.0;
+        if (kappa) {
+            const double kc = kappa[c];
+            if (!(kc > 0.0) || !isfinite(kc)) atomicOr(&sc->err, ERR_KAPPA);
+        }
+        double b = qc * L.vol();  // b -= un * area, contracted as in k_ds_prep
+        if (bw) b = fma(-tw, L.hy, b);
+        if (be) b = fma(-te, L.hy, b);
+        if (bs) b = fma(-ts, L.hx, b);
+        if (bn) b = fma(-tn, L.hx, b);
+        if (r == 0) b = 0.0;
+        Xd[(size_t)s * L.ncs + r] = b;
+    }
+}
+
 // Fresh factorization + solve per subdomain; mean shift to the recon mean
 // (mrcm.cpp:409-424). x (unshifted) stays in Xd for the velocity scatter.
 __global__ void k_ds_solve(Layout L, const double* __restrict__ BD, const double* __restrict__ BW,
@@ -853,10 +910,8 @@ __global__ void __launch_bounds__(WPB * 32, 4) k_ds_solve_r(Layout L, const doub
 // the stored panels with the mean shift (few registers, full occupancy,
 // bandwidth-bound on the panel stream).
 template <int B>
-__global__ void __launch_bounds__(WPB * 32, 3) k_ds_blk_factor(Layout L, const double* __restrict__ BD,
-                                                            const double* __restrict__ BW,
-                                                            const double* __restrict__ BS, double* T1, double* Xs,
-                                                            const double* Xd, Scalars* sc) {
+__global__ void __launch_bounds__(WPB * 32, 3) k_ds_blk_factor(Layout L, const double* __restrict__ T,
+                                                            double* T1, double* Xs, const double* Xd, Scalars* sc) {
     pdl_begin();
     __shared__ __align__(16) double sm[WPB][blk_smem_doubles<B>()];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -864,8 +919,9 @@ __global__ void __launch_bounds__(WPB * 32, 3) k_ds_blk_factor(Layout L, const d
     if (s >= L.n_sub) return;
     const int n = L.ncs;
     const size_t so = (size_t)s * n;
-    const BandRows A{BD + so, BW + so, BS + so};
-    const bool ok = blk_factor_fwd<B>(n, A, Xd + so, Xs + so * B, T1 + so, sm[w]);
+    // the operator straight from T(kappa_n): k_ds_prep writes only the rhs
+    const BlkTransSrc src{T, Xd + so, n, L.snx, L.sny, L.nx, L.vcount(), L.sub_i0(s), L.sub_j0(s)};
+    const bool ok = blk_factor_fwd<B>(n, src, Xs + so * B, T1 + so, sm[w]);
     if (!ok && lane == 0) atomicOr(&sc->err, ERR_PIVOT);
 }
 
@@ -2100,11 +2156,24 @@ void downscale(Ctx& c, const double* kappa, bool skel_given) {
     }
     const bool split = c.ds_split;
     if (split) ds_factor_fork(c);  // no-op when the caller already forked it
-    {
+    // the blocked DMMA downscale forms its operator from T itself
+    const bool blk = c.ds_blk == 1 || (c.ds_blk < 0 && (L.snx == 24 || L.snx == 32));
+    const bool blk_path = !split && !c.twist_ok && blk && L.snx % 8 == 0 && L.snx >= 16 && L.snx <= 32;
+    const bool kappa_checked = c.kappa_checked;  // the driver's k_kappa checked this kappa
+    c.kappa_checked = false;
+    if (split || blk_path) {  // the operator is formed by the factor: the rhs alone
+        PROF(c, "k_ds_rhs");
+        launch_k(c, k_ds_edges, std::min(grid_for((long long)L.n_sub * L.nbe), 8 * c.num_sms), TPB, 0, L,
+                 (const int*)c.bc_kind.p, (const double*)c.skel.p, (const double*)c.corr.p, (const double*)c.RU.p,
+                 (const double*)c.delta.p, c.grounded ? 1 : 0, c.GZ.p, c.ET.p);
+        CK_LAUNCH();
+        launch_k(c, k_ds_rhs, std::min(grid_for(L.cells()), 8 * c.num_sms), TPB, 0, L,
+                 kappa_checked ? nullptr : kappa, (const double*)c.q.p, (const double*)c.ET.p, c.Xd.p, c.sc.p);
+        CK_LAUNCH();
+    } else {
         PROF(c, "k_ds_prep");
         launch_k(c, k_ds_prep, grid_for(L.cells()), TPB, 0, L, kappa, c.T, c.q, c.bc_kind, c.skel, c.corr, c.RU, c.delta,
-                                                         c.grounded ? 1 : 0, c.BDd, c.BWd, c.BSd, c.Xd, c.GZ, c.sc,
-                                                         split ? 2 : 0);
+                                                         c.grounded ? 1 : 0, c.BDd, c.BWd, c.BSd, c.Xd, c.GZ, c.sc, 0);
         CK_LAUNCH();
     }
     const size_t sm1 = (size_t)WPB * band_smem_doubles(L.snx, 1) * sizeof(double);
@@ -2145,15 +2214,14 @@ void downscale(Ctx& c, const double* kappa, bool skel_given) {
         }
         if (done) CK_LAUNCH();
     }
-    const bool blk = c.ds_blk == 1 || (c.ds_blk < 0 && (L.snx == 24 || L.snx == 32));
-    if (!done && blk && L.snx % 8 == 0 && L.snx >= 16 && L.snx <= 32) {
+    if (!done && blk_path) {
         switch (L.snx) {
 #define X(BW_)                                                                                                     \
     case BW_:                                                                                                      \
         {                                                                                                          \
             PROF(c, "k_ds_blk_factor");                                                                            \
-            launch_k(c, k_ds_blk_factor<BW_>, band_blocks(L), WPB * 32, 0, L, c.BDd, c.BWd, c.BSd, c.Dd, c.Lrd,  \
-                     (const double*)c.Xd, c.sc);                                                                  \
+            launch_k(c, k_ds_blk_factor<BW_>, band_blocks(L), WPB * 32, 0, L, (const double*)c.T, c.Dd.p, c.Lrd.p, \
+                     (const double*)c.Xd, c.sc.p);                                                               \
         }                                                                                                          \
         CK_LAUNCH();                                                                                               \
         {                                                                                                          \

@@ -910,7 +910,8 @@ void launch_conductivity_decide(Ctx& c, const double* s, double* kappa, int eps_
                                 double eta) {
     PROF(c, "k_kappa");
     launch_kappa(c, s, kappa, eps_mode, method, rebuilt, eta, c.T.p);
-    c.trans_fresh = true;  // T = transmissibility(kappa) is current: the next rebuild / MPM step skips k_trans
+    c.trans_fresh = true;
+    c.kappa_checked = true;  // k_kappa flags a non-positive / non-finite kappa itself  // T = transmissibility(kappa) is current: the next rebuild / MPM step skips k_trans
     CK_LAUNCH();
 }
 void launch_conductivity(Ctx& c, const double* s, double* kappa, int eps_mode, bool want_eps) {
