@@ -32,7 +32,7 @@ __device__ __forceinline__ bool last_block_done(unsigned* counter) {
     __shared__ bool last;
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x * gridDim.y * gridDim.z - 1;
     __syncthreads();
     return last;
 }
@@ -824,10 +824,13 @@ __global__ void __launch_bounds__(256) k_ds_rhs(Layout L, const double* __restri
                                                 const double* __restrict__ q, const double* __restrict__ ET,
                                                 double* __restrict__ Xd, Scalars* sc) {
     pdl_begin();
-    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < L.cells(); c += gridDim.x * blockDim.x) {
-        const int i = c % L.nx, j = c / L.nx;
-        const int s = (j / L.sny) * L.nsx + i / L.snx;
-        const int ii = i % L.snx, jj = j % L.sny, r = jj * L.snx + ii;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;  // 2-D grid as k_ds_u_div
+    if (i >= L.nx) return;
+    const int sx = i / L.snx, ii = i - sx * L.snx;
+    for (int j = blockIdx.y; j < L.ny; j += gridDim.y) {
+        const int sy = j / L.sny, jj = j - sy * L.sny;
+        const int c = j * L.nx + i;
+        const int s = sy * L.nsx + sx, r = jj * L.snx + ii;
         const size_t eo = (size_t)s * L.nbe;
         const bool bw = ii == 0, be = ii == L.snx - 1, bs = jj == 0, bn = jj == L.sny - 1;
         const double qc = q[c];
@@ -1315,34 +1318,35 @@ __global__ void __launch_bounds__(256, 4) k_ds_u_div(Layout L, const double* __r
     double res = 0.0, vmax = 0.0, hmax = 0.0, qmax = 0.0, dmax = 0.0, anyf = 0.0;
     const double vol = L.vol(), hx = L.hx, hy = L.hy;
     const double slope = cfl.on ? sc->slope : 1.0;
-    const int ncell = L.cells();
-    const int stride = gridDim.x * blockDim.x;
-    // warp-uniform trip count (the east faces come by shuffle)
-    for (int c0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31); c0 < ncell; c0 += stride) {
-        const int c = c0 + lane;
-        const bool valid = c < ncell;
-        const int cc = valid ? c : ncell - 1;
-        const int i = cc % L.nx, j = cc / L.nx;
-        const int sx = i / L.snx, ii = i % L.snx, sy = j / L.sny, jj = j % L.sny;
+    // 2-D grid: blockIdx.x over 256-column strips (warps = 32 consecutive
+    // cells of a row), rows strided by blockIdx.y: the column's subdomain
+    // index math once per thread, the row's once per row (block-uniform)
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool valid = i < L.nx;
+    const int ic = valid ? i : L.nx - 1;
+    const int sx = ic / L.snx, ii = ic - sx * L.snx;
+    for (int j = blockIdx.y; j < L.ny; j += gridDim.y) {
+        const int sy = j / L.sny, jj = j - sy * L.sny;
+        const int cc = j * L.nx + ic;
         const int s = sy * L.nsx + sx;
         const size_t xo = (size_t)s * L.ncs;
         const int r = jj * L.snx + ii;
         const size_t eo = (size_t)s * L.nbe;
-        const bool de = lane == 31 || i + 1 == L.nx || c + 1 >= ncell;  // east face not held by lane + 1
+        const bool de = lane == 31 || i + 1 >= L.nx;  // east face not held by lane + 1
         const bool hw = ii > 0, he = ii + 1 < L.snx, hs = jj > 0, hn = jj + 1 < L.sny;
         const double xc = Xd[xo + r];
         const double xw = hw ? Xd[xo + r - 1] : 0.0;
-        const double tw = hw ? T[L.vface(i, j)] : 0.0;
+        const double tw = hw ? T[L.vface(ic, j)] : 0.0;
         const double ew = hw ? 0.0 : EU[eo + jj];
         const double xe = (de && he) ? Xd[xo + r + 1] : 0.0;
-        const double te = (de && he) ? T[L.vface(i + 1, j)] : 0.0;
+        const double te = (de && he) ? T[L.vface(ic + 1, j)] : 0.0;
         // east face on a subdomain edge: the west edge of the subdomain to the east, or the domain boundary
-        const double ee = (de && !he) ? (i + 1 < L.nx ? -EU[eo + L.nbe + jj] : EU[eo + L.sny + jj]) : 0.0;
+        const double ee = (de && !he) ? (ic + 1 < L.nx ? -EU[eo + L.nbe + jj] : EU[eo + L.sny + jj]) : 0.0;
         const double xs = hs ? Xd[xo + r - L.snx] : 0.0;
-        const double ts = hs ? T[L.hface(i, j)] : 0.0;
+        const double ts = hs ? T[L.hface(ic, j)] : 0.0;
         const double es = hs ? 0.0 : EU[eo + 2 * L.sny + ii];
         const double xn = hn ? Xd[xo + r + L.snx] : 0.0;
-        const double tn = hn ? T[L.hface(i, j + 1)] : 0.0;
+        const double tn = hn ? T[L.hface(ic, j + 1)] : 0.0;
         // north face on a subdomain edge: the south edge of the one above, or the domain boundary
         const double en = hn ? 0.0 : (j + 1 < L.ny ? -EU[(size_t)(s + L.nsx) * L.nbe + 2 * L.sny + ii]
                                                    : EU[eo + 2 * L.sny + L.snx + ii]);
@@ -1385,12 +1389,12 @@ __global__ void __launch_bounds__(256, 4) k_ds_u_div(Layout L, const double* __r
     __shared__ double red[NP];
     double v[NP] = {res, vmax, hmax, qmax, dmax, anyf};
     block_reduce_multi<NP>(v, 0u, shm, red);
-    if (threadIdx.x < NP) part[NP * blockIdx.x + threadIdx.x] = red[threadIdx.x];
+    if (threadIdx.x < NP) part[NP * (blockIdx.y * gridDim.x + blockIdx.x) + threadIdx.x] = red[threadIdx.x];
     if (last_block_done(counter)) {
         double a[NP];
 #pragma unroll
         for (int k = 0; k < NP; ++k) a[k] = 0.0;
-        for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+        for (int b = threadIdx.x; b < (int)(gridDim.x * gridDim.y); b += blockDim.x) {
 #pragma unroll
             for (int k = 0; k < NP; ++k) a[k] = fmax(a[k], __ldcg(part + (size_t)NP * b + k));
         }
@@ -1605,29 +1609,30 @@ __global__ void __launch_bounds__(256) k_mpm_rhs_w(Layout L, int max_rhs, int an
                                                    const double* __restrict__ ET, double* __restrict__ X) {
     pdl_begin();
     const int lane = threadIdx.x & 31;
-    const int ncell = L.cells();
     const double vol = L.vol(), hx = L.hx, hy = L.hy;
-    for (int c0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31); c0 < ncell; c0 += gridDim.x * blockDim.x) {
-        const int c = c0 + lane;
-        const bool valid = c < ncell;
-        const int cc = valid ? c : ncell - 1;
-        const int i = cc % L.nx, j = cc / L.nx;
-        const int sx = i / L.snx, ii = i % L.snx, sy = j / L.sny, jj = j % L.sny;
+    // 2-D grid as k_ds_u_div: column strips x rows
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool valid = i < L.nx;
+    const int ic = valid ? i : L.nx - 1;
+    const int sx = ic / L.snx, ii = ic - sx * L.snx;
+    for (int j = blockIdx.y; j < L.ny; j += gridDim.y) {
+        const int sy = j / L.sny, jj = j - sy * L.sny;
+        const int cc = j * L.nx + ic;
         const int s = sy * L.nsx + sx;
         const int r = jj * L.snx + ii;
         const size_t eo = (size_t)s * L.nbe;
-        const bool de = lane == 31 || i + 1 == L.nx || c + 1 >= ncell;
+        const bool de = lane == 31 || i + 1 >= L.nx;
         const bool hw = ii > 0, he = ii + 1 < L.snx, hs = jj > 0, hn = jj + 1 < L.sny;
         const int eW = jj, eE = L.sny + jj, eS = 2 * L.sny + ii, eN = 2 * L.sny + L.snx + ii;
         const double pc = pm[cc];
         const double pw = hw ? pm[cc - 1] : 0.0;
-        const double tw = hw ? Tn[L.vface(i, j)] : 0.0;
+        const double tw = hw ? Tn[L.vface(ic, j)] : 0.0;
         const double pe = (de && he) ? pm[cc + 1] : 0.0;
-        const double te = (de && he) ? Tn[L.vface(i + 1, j)] : 0.0;
+        const double te = (de && he) ? Tn[L.vface(ic + 1, j)] : 0.0;
         const double ps = hs ? pm[cc - L.nx] : 0.0;
-        const double ts = hs ? Tn[L.hface(i, j)] : 0.0;
+        const double ts = hs ? Tn[L.hface(ic, j)] : 0.0;
         const double pn = hn ? pm[cc + L.nx] : 0.0;
-        const double tn = hn ? Tn[L.hface(i, j + 1)] : 0.0;
+        const double tn = hn ? Tn[L.hface(ic, j + 1)] : 0.0;
         const double qc = q[cc];
         const double uw = hw ? 0.0 : WU[eo + eW], ue = he ? 0.0 : WU[eo + eE];
         const double us = hs ? 0.0 : WU[eo + eS], un = hn ? 0.0 : WU[eo + eN];
@@ -1892,6 +1897,13 @@ __global__ void k_repair_matrix(Layout L, int grounded, const double* __restrict
 }
 
 int grid_for(long long n) { return std::max(1, cdiv(n, TPB)); }
+// 2-D grid of the row kernels: 256-column strips x rows, about `cap` blocks
+dim3 grid2d(const Ctx& c, const Layout& L, int cap = 0) {
+    if (cap <= 0) cap = 8 * c.num_sms;
+    const int gx = cdiv(L.nx, TPB);
+    const int gy = std::max(1, std::min(L.ny, cap / gx));
+    return dim3(gx, gy);
+}
 int band_blocks(const Layout& L) { return cdiv(L.n_sub, WPB); }
 
 }  // namespace
@@ -2167,7 +2179,7 @@ void downscale(Ctx& c, const double* kappa, bool skel_given) {
                  (const int*)c.bc_kind.p, (const double*)c.skel.p, (const double*)c.corr.p, (const double*)c.RU.p,
                  (const double*)c.delta.p, c.grounded ? 1 : 0, c.GZ.p, c.ET.p);
         CK_LAUNCH();
-        launch_k(c, k_ds_rhs, std::min(grid_for(L.cells()), 8 * c.num_sms), TPB, 0, L,
+        launch_k(c, k_ds_rhs, grid2d(c, L), TPB, 0, L,
                  kappa_checked ? nullptr : kappa, (const double*)c.q.p, (const double*)c.ET.p, c.Xd.p, c.sc.p);
         CK_LAUNCH();
     } else {
@@ -2258,7 +2270,7 @@ void downscale(Ctx& c, const double* kappa, bool skel_given) {
         PROF(c, "k_ds_u_div");
         CflNext cfl;
         if (c.cfl_fused) cfl = CflNext{1, c.cfl_safety, c.cfl_dt_cap, c.cfl_inflow, c.M};
-        launch_k(c, k_ds_u_div, red_blocks(c, k_ds_u_div, L.cells()), TPB, 0, L, c.T, c.Xd, c.GZ, c.u, c.q,
+        launch_k(c, k_ds_u_div, grid2d(c, L, red_blocks(c, k_ds_u_div, L.cells())), TPB, 0, L, c.T, c.Xd, c.GZ, c.u, c.q,
                  c.sc.p, c.red.p, c.red_count.p, cfl);
         CK_LAUNCH();
     }
@@ -2516,7 +2528,7 @@ void launch_mpm(Ctx& c, const double* kn) {  // mpm_pressure_update (mpm.cpp:31-
             launch_k(c, k_mpm_edges, std::min(grid_for((long long)L.n_sub * L.nbe), 8 * c.num_sms), TPB, 0, L, kn,
                      c.kappa_m, c.bc_kind, c.bc_value, c.beta_m, c.beta_p, c.pm, c.bpm, c.GZ, c.WU, c.ET);
             CK_LAUNCH();
-            launch_k(c, k_mpm_rhs_w, std::min(grid_for(L.cells()), 8 * c.num_sms), TPB, 0, L, c.max_rhs,
+            launch_k(c, k_mpm_rhs_w, grid2d(c, L), TPB, 0, L, c.max_rhs,
                      c.anchor_m ? 1 : 0, c.T, c.q, c.pm, c.WU, c.ET, c.X);
         }
         else if (c.rhs_sub && L.ncs <= RHS_TPB * RHS_CPT)
