@@ -28,6 +28,7 @@
 // (mma.sync.m8n8k4, DMMA).
 
 #include "context.cuh"
+#include "cr.cuh"
 
 
 namespace mpm2p {
@@ -220,15 +221,6 @@ __global__ void __launch_bounds__(256) k_gj_update(double* const* __restrict__ m
 }
 
 // ---- batched GEMV jobs: out = base + s1 M1 v1 (+ s2 M2 v2), S x S matrices
-struct GemvJob {
-    double* out;
-    const double* base;
-    const double* M1;
-    const double* v1;
-    const double* M2;
-    const double* v2;
-    double s1, s2;
-};
 // RPW rows per warp, 8 warps per CTA (the rows' loads interleaved); the
 // launcher picks RPW = 4 for wide levels and RPW = 1 for the last levels of
 // the reduction, where few blocks remain and more warps per row set hide
@@ -477,6 +469,7 @@ struct CrPlan {
     int S = 0, nb = 0, max_batch = 1;
     DevBuf<GemmJob> gemm;
     DevBuf<GemvJob> gemv;
+    DevBuf<int2> phases;  // the solve's launches as (first job, count), for in-kernel solves
     DevBuf<double*> gjmats;
     DevBuf<double*> tr_dst;
     DevBuf<const double*> tr_src;
@@ -507,33 +500,10 @@ void run_gj(Ctx& c, CrPlan& pl, int first, int count) {
 
 }  // namespace
 
-void bt_setup(Ctx& c) {
-    const Layout& L = c.L;
-    const int n = c.dim, np = L.dim_flux;
-    auto block_of_iface = [&](int k) { return k < L.NV ? k / (L.nsx - 1) : (k - L.NV) / L.nsx; };
-    std::vector<int> blk(n), loc(n);
-    int nblk = 0;
-    for (int r = 0; r < n; ++r) {
-        blk[r] = block_of_iface(L.basis_iface(r % np));
-        nblk = std::max(nblk, blk[r] + 1);
-    }
-    std::vector<int> sz(nblk, 0);
-    for (int r = 0; r < n; ++r) loc[r] = sz[blk[r]]++;
-    int smax = 0;
-    for (int j = 0; j < nblk; ++j) {
-        if (sz[j] == 0) throw ConfigError("block-tridiagonal interface solve: empty block");
-        smax = std::max(smax, sz[j]);
-    }
-    const int S = (smax + 63) / 64 * 64;
-    c.bt_nblk = nblk;
-    c.bt_sz = sz;
-    auto up_i = [&](DevBuf<int>& d, const std::vector<int>& h) {
-        d.alloc(std::max<size_t>(h.size(), 1));
-        CK(cudaMemcpyAsync(d.p, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice, c.st));
-    };
-    up_i(c.bt_blk, blk);
-    up_i(c.bt_loc, loc);
-    up_i(c.bt_bsz, sz);
+// A cyclic-reduction system of nb blocks of S x S (S a multiple of 64): its
+// level buffers, the factor's launch plan and the solve's job lists, which
+// read y and write x (nb * S each, caller-owned; y is overwritten).
+std::shared_ptr<void> cr_create(Ctx& c, int nblk, int S, double* yvec, double* xvec) {
     auto plp = std::make_shared<CrPlan>();
     CrPlan& pl = *plp;
     pl.S = S;
@@ -558,15 +528,13 @@ void bt_setup(Ctx& c) {
     pl.P.alloc(nblk * SS);
     pl.Q.alloc(nblk * SS);
     pl.cvec.alloc((size_t)nblk * S);
-    c.bt_y.alloc((size_t)nblk * S);
-    c.bt_x.alloc((size_t)nblk * S);
     auto Dp = [&](int j) { return pl.D.p + j * SS; };
     auto Lo = [&](int l, int p) { return pl.LU.p + (pl.lu_first[l] + p) * SS; };
     auto Up = [&](int l, int p) { return pl.LU.p + (pl.lu_first[l] + (long long)act[l].size() + p) * SS; };
     auto Pp = [&](int j) { return pl.P.p + j * SS; };
     auto Qp = [&](int j) { return pl.Q.p + j * SS; };
-    auto yv = [&](int j) { return c.bt_y.p + (size_t)j * S; };
-    auto xv = [&](int j) { return c.bt_x.p + (size_t)j * S; };
+    auto yv = [&](int j) { return yvec + (size_t)j * S; };
+    auto xv = [&](int j) { return xvec + (size_t)j * S; };
     auto cv = [&](int j) { return pl.cvec.p + (size_t)j * S; };
     std::vector<GemmJob> gemm;
     std::vector<GemvJob> gemv;
@@ -664,35 +632,35 @@ void bt_setup(Ctx& c) {
     pl.colbuf.alloc((size_t)pl.max_batch * S * GP);
     pl.rowbuf.alloc((size_t)pl.max_batch * S * GP);
     pl.flag.alloc(1);
-    c.hg_x.alloc(n);
-    c.hg_y.alloc(n);
-    c.hg_z.alloc(n);
-    c.hg_xi.alloc(n);
-    c.hg_state.alloc(sizeof(HagerState) / sizeof(double) + 1);
-    c.cr_plan = plp;
+    std::vector<int2> ph;
+    for (const CrLaunch& st : pl.solve) ph.push_back(make_int2(st.first, st.count));
+    pl.phases.alloc(std::max<size_t>(ph.size(), 1));
+    if (!ph.empty()) CK(cudaMemcpyAsync(pl.phases.p, ph.data(), ph.size() * sizeof(int2), cudaMemcpyHostToDevice, c.st));
     CK(cudaStreamSynchronize(c.st));
+    return plp;
 }
 
-// Factorisation at every rebuild (after the CSR of K holds the new values).
-void bt_factor(Ctx& c) {
-    CrPlan& pl = plan_of(c);
-    const int n = c.dim, S = pl.S, nb = pl.nb;
-    const size_t SS = (size_t)S * S;
-    CK(cudaMemsetAsync(pl.D.p, 0, nb * SS * sizeof(double), c.st));
-    CK(cudaMemsetAsync(pl.LU.p, 0, 2 * (size_t)nb * SS * sizeof(double), c.st));  // level-0 Lo and Up slots
+
+CrView cr_view(const std::shared_ptr<void>& plan) {
+    CrPlan& pl = *static_cast<CrPlan*>(plan.get());
+    const size_t SS = (size_t)pl.S * pl.S;
+    return CrView{pl.D.p, pl.LU.p + (size_t)pl.nb * SS, pl.nb, pl.S, pl.gemv.p, pl.phases.p, (int)pl.solve.size()};
+}
+
+// zero D and the level-0 Lo / Up slots before the caller fills them
+void cr_zero(Ctx& c, const std::shared_ptr<void>& plan) {
+    CrPlan& pl = *static_cast<CrPlan*>(plan.get());
+    const size_t SS = (size_t)pl.S * pl.S;
+    CK(cudaMemsetAsync(pl.D.p, 0, pl.nb * SS * sizeof(double), c.st));
+    CK(cudaMemsetAsync(pl.LU.p, 0, 2 * (size_t)pl.nb * SS * sizeof(double), c.st));
     CK(cudaMemsetAsync(pl.flag.p, 0, sizeof(int), c.st));
-    {
-        PROF(c, "k_bt_scatter");
-        launch_k(c, k_cr_scatter, cdiv(n, TPB), TPB, 0, (const int*)c.k_ptr.p, (const int*)c.k_col.p,
-                 (const double*)c.k_val.p, n, (const int*)c.bt_blk.p, (const int*)c.bt_loc.p, S, pl.D.p,
-                 pl.LU.p + (size_t)nb * SS);
-        CK_LAUNCH();
-    }
-    {
-        PROF(c, "k_bt_scatter");
-        launch_k(c, k_cr_pad, cdiv((long long)nb * S, TPB), TPB, 0, (const int*)c.bt_bsz.p, nb, S, pl.D.p);
-        CK_LAUNCH();
-    }
+}
+
+// factor after D and Up_0 hold the system: Lo_0 = Up^T, the level plan,
+// ERR_SINGULAR on a zero / non-finite pivot
+void cr_factor(Ctx& c, const std::shared_ptr<void>& plan, unsigned err_bit) {
+    CrPlan& pl = *static_cast<CrPlan*>(plan.get());
+    const int S = pl.S, nb = pl.nb;
     if (nb > 1) {
         PROF(c, "k_transpose");
         launch_k(c, k_cr_transpose, dim3(S / 32, S / 32, nb - 1), dim3(32, 8), 0, (double* const*)pl.tr_dst.p,
@@ -711,9 +679,87 @@ void bt_factor(Ctx& c) {
     }
     {
         PROF(c, "k_flag_err");
-        launch_k(c, k_flag_err, 1, 1, 0, (const int*)pl.flag.p, c.sc.p, ERR_SINGULAR);
+        launch_k(c, k_flag_err, 1, 1, 0, (const int*)pl.flag.p, c.sc.p, err_bit);
         CK_LAUNCH();
     }
+}
+
+namespace {
+
+// the solve's batched GEMV launches (y -> x)
+void cr_solve_launches(Ctx& c, CrPlan& pl) {
+    const int S = pl.S;
+    for (const CrLaunch& st : pl.solve) {
+        PROF(c, "k_cr_gemv");
+        if ((long long)st.count * (S / 32) >= 4LL * c.num_sms)
+            launch_k(c, k_cr_gemv<4>, dim3(S / 32, st.count), 256, 2 * S * sizeof(double),
+                     (const GemvJob*)(pl.gemv.p + st.first), S);
+        else
+            launch_k(c, k_cr_gemv<1>, dim3(S / 8, st.count), 256, 2 * S * sizeof(double),
+                     (const GemvJob*)(pl.gemv.p + st.first), S);
+        CK_LAUNCH();
+    }
+}
+
+}  // namespace
+
+void bt_setup(Ctx& c) {
+    const Layout& L = c.L;
+    const int n = c.dim, np = L.dim_flux;
+    auto block_of_iface = [&](int k) { return k < L.NV ? k / (L.nsx - 1) : (k - L.NV) / L.nsx; };
+    std::vector<int> blk(n), loc(n);
+    int nblk = 0;
+    for (int r = 0; r < n; ++r) {
+        blk[r] = block_of_iface(L.basis_iface(r % np));
+        nblk = std::max(nblk, blk[r] + 1);
+    }
+    std::vector<int> sz(nblk, 0);
+    for (int r = 0; r < n; ++r) loc[r] = sz[blk[r]]++;
+    int smax = 0;
+    for (int j = 0; j < nblk; ++j) {
+        if (sz[j] == 0) throw ConfigError("block-tridiagonal interface solve: empty block");
+        smax = std::max(smax, sz[j]);
+    }
+    const int S = (smax + 63) / 64 * 64;
+    c.bt_nblk = nblk;
+    c.bt_sz = sz;
+    auto up_i = [&](DevBuf<int>& d, const std::vector<int>& h) {
+        d.alloc(std::max<size_t>(h.size(), 1));
+        CK(cudaMemcpyAsync(d.p, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice, c.st));
+    };
+    up_i(c.bt_blk, blk);
+    up_i(c.bt_loc, loc);
+    up_i(c.bt_bsz, sz);
+    c.bt_y.alloc((size_t)nblk * S);
+    c.bt_x.alloc((size_t)nblk * S);
+    c.cr_plan = cr_create(c, nblk, S, c.bt_y.p, c.bt_x.p);
+    c.hg_x.alloc(n);
+    c.hg_y.alloc(n);
+    c.hg_z.alloc(n);
+    c.hg_xi.alloc(n);
+    c.hg_state.alloc(sizeof(HagerState) / sizeof(double) + 1);
+    CK(cudaStreamSynchronize(c.st));
+}
+
+// Factorisation at every rebuild (after the CSR of K holds the new values).
+void bt_factor(Ctx& c) {
+    CrPlan& pl = plan_of(c);
+    const int n = c.dim, S = pl.S, nb = pl.nb;
+    const size_t SS = (size_t)S * S;
+    cr_zero(c, c.cr_plan);
+    {
+        PROF(c, "k_bt_scatter");
+        launch_k(c, k_cr_scatter, cdiv(n, TPB), TPB, 0, (const int*)c.k_ptr.p, (const int*)c.k_col.p,
+                 (const double*)c.k_val.p, n, (const int*)c.bt_blk.p, (const int*)c.bt_loc.p, S, pl.D.p,
+                 pl.LU.p + (size_t)nb * SS);
+        CK_LAUNCH();
+    }
+    {
+        PROF(c, "k_bt_scatter");
+        launch_k(c, k_cr_pad, cdiv((long long)nb * S, TPB), TPB, 0, (const int*)c.bt_bsz.p, nb, S, pl.D.p);
+        CK_LAUNCH();
+    }
+    cr_factor(c, c.cr_plan, ERR_SINGULAR);
 }
 
 // x = M^-1 rhs through K x = J rhs (transposed: x = M^-T rhs = J^T K^-1 rhs).
@@ -727,16 +773,7 @@ void bt_solve_t(Ctx& c, const double* rhs, double* x, int transposed) {
                  c.bt_y.p, transposed);
         CK_LAUNCH();
     }
-    for (const CrLaunch& st : pl.solve) {
-        PROF(c, "k_cr_gemv");
-        if ((long long)st.count * (S / 32) >= 4LL * c.num_sms)
-            launch_k(c, k_cr_gemv<4>, dim3(S / 32, st.count), 256, 2 * S * sizeof(double),
-                     (const GemvJob*)(pl.gemv.p + st.first), S);
-        else
-            launch_k(c, k_cr_gemv<1>, dim3(S / 8, st.count), 256, 2 * S * sizeof(double),
-                     (const GemvJob*)(pl.gemv.p + st.first), S);
-        CK_LAUNCH();
-    }
+    cr_solve_launches(c, pl);
     {
         PROF(c, "k_bt_unpermute");
         launch_k(c, k_bt_unpermute, cdiv(n, TPB), TPB, 0, (const double*)c.bt_x.p, n, (const int*)c.bt_blk.p,

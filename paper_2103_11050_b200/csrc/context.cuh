@@ -156,6 +156,11 @@ struct Ctx {
     // order; f_x is the warm start), coarse operator and its inverse
     DevBuf<double> f_T, f_BD, f_BW, f_BS, f_D, f_Lc, f_Lr, f_b, f_x, f_r, f_p, f_q, f_y;
     DevBuf<double> f_A0, f_A0i, f_c0, f_e, f_part;
+    // coarse space above 4,096 subdomains (or MPM2P_FINE_COARSE=cr): block-
+    // tridiagonal by subdomain rows, solved by cyclic reduction inside the PCG
+    bool f_cr = false;
+    std::shared_ptr<void> f_cr_plan;
+    DevBuf<double> f_cy, f_cx;
     bool f_ready = false, f_warm = false;
     int f_anchor = -1;
     double f_tol = 1e-13;
@@ -395,5 +400,18 @@ void bt_setup(Ctx& c);                                    // block layout and bu
 void bt_factor(Ctx& c);                                   // block LDL^T with explicit S_j^-1 (each rebuild)
 void bt_solve(Ctx& c, const double* rhs, double* x);      // x = M^-1 rhs
 void bt_rcond(Ctx& c, double threshold, unsigned err_bit);  // Hager/Higham rcond guard (each rebuild)
+// generic cyclic-reduction systems (blocktri.cu): nb blocks of S x S (S % 64 == 0)
+struct CrView {
+    double* D;    // nb diagonal blocks, to fill (after cr_zero)
+    double* Up0;  // nb upper coupling blocks K[j][j+1], to fill (the lower ones are their transposes)
+    int nb, S;
+    const void* jobs;    // GemvJob array of the solve
+    const int2* phases;  // (first, count) per solve phase
+    int nphase;
+};
+std::shared_ptr<void> cr_create(Ctx& c, int nb, int S, double* y, double* x);  // solve: y (overwritten) -> x
+CrView cr_view(const std::shared_ptr<void>& plan);
+void cr_zero(Ctx& c, const std::shared_ptr<void>& plan);
+void cr_factor(Ctx& c, const std::shared_ptr<void>& plan, unsigned err_bit);
 
 }  // namespace mpm2p

@@ -28,9 +28,11 @@
 
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 
 #include "band_reg.cuh"
 #include "context.cuh"
+#include "cr.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -208,6 +210,60 @@ __global__ void k_fine_coarse(Layout L, int anchor, const double* __restrict__ T
     }
 }
 
+// The same coarse operator into block-tridiagonal form for the cyclic
+// reduction: block sy = the subdomains of row sy (S >= nsx, identity pad),
+// D[sy][sx][sx'] and the upper coupling Up[sy][sx][sx] to row sy + 1. Same
+// per-edge sums and order as k_fine_coarse.
+__global__ void k_fine_coarse_cr(Layout L, int anchor, const double* __restrict__ T, const double* __restrict__ BD,
+                                 const double* __restrict__ BW, const double* __restrict__ BS, int S,
+                                 double* __restrict__ D, double* __restrict__ Up) {
+    pdl_begin();
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const int nblk_rows = L.nsy * S;
+    if (w >= nblk_rows) return;
+    const int sy = w / S, sx = w % S;
+    double* drow = D + ((size_t)sy * S + sx) * S;
+    if (sx >= L.nsx) {  // pad row: identity
+        if (lane == 0) drow[sx] = 1.0;
+        return;
+    }
+    const int s = sy * L.nsx + sx;
+    const int n = L.ncs;
+    const size_t so = (size_t)s * n;
+    double d = 0.0;
+    for (int r = lane; r < n; r += 32) d += BD[so + r] - 2.0 * (BW[so + r] + BS[so + r]);
+    d = warp_sum(d);
+    const int i0 = L.sub_i0(s), j0 = L.sub_j0(s);
+    auto edge = [&](int cnt, bool vert, int fi, int fj) {
+        double t = 0.0;
+        for (int m = lane; m < cnt; m += 32) {
+            const int ii = vert ? fi : fi + m, jj = vert ? fj + m : fj;
+            int ca, cb;
+            double tf;
+            if (vert) {
+                ca = L.cell(ii - 1, jj);
+                cb = L.cell(ii, jj);
+                tf = T[L.vface(ii, jj)];
+            } else {
+                ca = L.cell(ii, jj - 1);
+                cb = L.cell(ii, jj);
+                tf = T[L.hface(ii, jj)];
+            }
+            if (ca != anchor && cb != anchor) t -= tf;
+        }
+        return warp_sum(t);
+    };
+    const double ew = sx > 0 ? edge(L.sny, true, i0, j0) : 0.0;
+    const double ee = sx < L.nsx - 1 ? edge(L.sny, true, i0 + L.snx, j0) : 0.0;
+    const double en = sy < L.nsy - 1 ? edge(L.snx, false, i0, j0 + L.sny) : 0.0;
+    if (lane == 0) {
+        drow[sx] = d;
+        if (sx > 0) drow[sx - 1] = ew;
+        if (sx < L.nsx - 1) drow[sx + 1] = ee;
+        if (sy < L.nsy - 1) Up[((size_t)sy * S + sx) * S + sx] = en;
+    }
+}
+
 struct FineArgs {
     Layout L;
     int anchor;
@@ -224,6 +280,11 @@ struct FineArgs {
     double tol;
     int maxit;
     Scalars* sc;
+    // cyclic-reduction coarse solve (cr_nphase > 0): jobs read cy, write cx
+    const GemvJob* cr_jobs;
+    const int2* cr_phases;
+    int cr_nphase, cr_S;
+    double *cy, *cx;
 };
 
 // Sum of n per-subdomain partials; every block forms it in the same order.
@@ -240,9 +301,19 @@ __device__ __forceinline__ double fine_all_sum(const double* part, int n, double
     return s;
 }
 
-// e = A0^-1 c0: one warp per coarse row.
-__device__ __forceinline__ void fine_coarse_solve(const FineArgs& a, int gw, int nw, int lane) {
+// e = A0^-1 c0: one warp per coarse row of the dense inverse, or the
+// cyclic-reduction phases (c0 into the padded block vector, the solve, e out)
+__device__ __forceinline__ void fine_coarse_solve(const FineArgs& a, int gw, int nw, int lane,
+                                                  cg::grid_group& grid) {
     const int ns = a.L.n_sub;
+    if (a.cr_nphase > 0) {
+        const int nsx = a.L.nsx;
+        for (int s = gw * 32 + lane; s < ns; s += nw * 32) a.cy[(size_t)(s / nsx) * a.cr_S + s % nsx] = __ldcg(a.c0 + s);
+        grid.sync();
+        cr_solve_in_kernel(a.cr_jobs, a.cr_phases, a.cr_nphase, a.cr_S, grid);
+        for (int s = gw * 32 + lane; s < ns; s += nw * 32) a.e[s] = __ldcg(a.cx + (size_t)(s / nsx) * a.cr_S + s % nsx);
+        return;
+    }
     for (int row = gw; row < ns; row += nw) {
         const double* ar = a.A0i + (size_t)row * ns;
         double t = 0.0;
@@ -291,7 +362,7 @@ __global__ void __launch_bounds__(FWPB * 32) k_fine_pcg(FineArgs a) {
         }
     }
     grid.sync();
-    fine_coarse_solve(a, gw, nw, lane);
+    fine_coarse_solve(a, gw, nw, lane, grid);
     grid.sync();
     // deflated start: x += R^T e, r -= A R^T e
     for (int s = gw; s < ns; s += nw) {
@@ -342,7 +413,7 @@ __global__ void __launch_bounds__(FWPB * 32) k_fine_pcg(FineArgs a) {
             if (lane == 0) a.c0[s] = sr;
         }
         grid.sync();
-        fine_coarse_solve(a, gw, nw, lane);
+        fine_coarse_solve(a, gw, nw, lane, grid);
         grid.sync();
         // z = y + R^T e (in place on y); rho = r . z
         for (int s = gw; s < ns; s += nw) {
@@ -484,16 +555,28 @@ void fine_launch(Ctx& c, const FineArgs& fa) {
                  c.f_Lc.p, c.f_Lr.p, c.f_y.p, c.sc.p);
         CK_LAUNCH();
     }
-    {
-        PROF(c, "k_fine_coarse");
-        CK(cudaMemsetAsync(c.f_A0.p, 0, (size_t)L.n_sub * L.n_sub * sizeof(double), c.st));
-        launch_k(c, k_fine_coarse, cdiv((long long)L.n_sub * 32, TPB), TPB, 0, L, c.f_anchor, c.f_T.p, c.f_BD.p,
-                 c.f_BW.p, c.f_BS.p, c.f_A0.p);
-        CK_LAUNCH();
+    if (c.f_cr) {  // block-tridiagonal coarse operator, cyclic reduction
+        const CrView v = cr_view(c.f_cr_plan);
+        cr_zero(c, c.f_cr_plan);
+        {
+            PROF(c, "k_fine_coarse");
+            launch_k(c, k_fine_coarse_cr, cdiv((long long)L.nsy * v.S * 32, TPB), TPB, 0, L, c.f_anchor, c.f_T.p,
+                     c.f_BD.p, c.f_BW.p, c.f_BS.p, v.S, v.D, v.Up0);
+            CK_LAUNCH();
+        }
+        cr_factor(c, c.f_cr_plan, ERR_FINE_NOCONV);  // a zero coarse pivot: the solve cannot proceed
+    } else {
+        {
+            PROF(c, "k_fine_coarse");
+            CK(cudaMemsetAsync(c.f_A0.p, 0, (size_t)L.n_sub * L.n_sub * sizeof(double), c.st));
+            launch_k(c, k_fine_coarse, cdiv((long long)L.n_sub * 32, TPB), TPB, 0, L, c.f_anchor, c.f_T.p, c.f_BD.p,
+                     c.f_BW.p, c.f_BS.p, c.f_A0.p);
+            CK_LAUNCH();
+        }
+        CK(cudaMemcpyAsync(c.f_A0i.p, c.f_A0.p, (size_t)L.n_sub * L.n_sub * sizeof(double), cudaMemcpyDeviceToDevice,
+                           c.st));
+        block_gj_inplace_pub(c, c.f_A0i.p, L.n_sub);  // SPD: pivot-free blocked Gauss-Jordan
     }
-    CK(cudaMemcpyAsync(c.f_A0i.p, c.f_A0.p, (size_t)L.n_sub * L.n_sub * sizeof(double), cudaMemcpyDeviceToDevice,
-                       c.st));
-    block_gj_inplace_pub(c, c.f_A0i.p, L.n_sub);  // SPD: pivot-free blocked Gauss-Jordan
     static DeviceCache per_sm;  // one per instantiation B, per device
     int occ = per_sm.at().load();
     if (occ < 0) {
@@ -516,9 +599,12 @@ void fine_launch(Ctx& c, const FineArgs& fa) {
 void fine_setup(Ctx& c) {
     const Layout& L = c.L;
     if (c.f_ready) return;
-    if (L.n_sub > 4096)
-        throw CapacityError("fine solve: the coarse space of " + std::to_string(L.n_sub) +
-                            " subdomains exceeds the dense coarse solve (4096)");
+    // the dense coarse inverse up to 4,096 subdomains, cyclic reduction above
+    c.f_cr = L.n_sub > 4096;
+    if (const char* e = std::getenv("MPM2P_FINE_COARSE")) {
+        if (std::strcmp(e, "cr") == 0) c.f_cr = true;
+        else if (std::strcmp(e, "dense") == 0) c.f_cr = false;
+    }
     switch (L.snx) {
 #define X(BW_) \
     case BW_:  \
@@ -542,8 +628,17 @@ void fine_setup(Ctx& c) {
     c.f_p.alloc(nb);
     c.f_q.alloc(nb);
     c.f_y.alloc(nb);
-    c.f_A0.alloc(ns * ns);
-    c.f_A0i.alloc(ns * ns);
+    if (c.f_cr) {
+        const int S = (L.nsx + 63) / 64 * 64;
+        c.f_cy.alloc((size_t)L.nsy * S);
+        c.f_cx.alloc((size_t)L.nsy * S);
+        c.f_cy.zero(c.st);
+        c.f_cx.zero(c.st);
+        c.f_cr_plan = cr_create(c, L.nsy, S, c.f_cy.p, c.f_cx.p);
+    } else {
+        c.f_A0.alloc(ns * ns);
+        c.f_A0i.alloc(ns * ns);
+    }
     c.f_c0.alloc(ns);
     c.f_e.alloc(ns);
     c.f_part.alloc(4 * ns);
@@ -573,7 +668,16 @@ void fine_solve(Ctx& c, const double* kappa, double* p, double* u, bool cold) {
     }
     FineArgs fa{L, c.f_anchor, c.f_T.p, c.f_BD.p, c.f_D.p, c.f_Lc.p, c.f_Lr.p, c.f_A0i.p, c.f_b.p, c.f_x.p,
                 c.f_r.p, c.f_p.p, c.f_q.p, c.f_y.p, c.f_c0.p, c.f_e.p, c.f_part.p, c.f_tol,
-                std::max(1000, 4 * L.n_sub), c.sc.p};
+                std::max(1000, std::min(4 * L.n_sub, 20000)), c.sc.p, nullptr, nullptr, 0, 0, nullptr, nullptr};
+    if (c.f_cr) {
+        const CrView v = cr_view(c.f_cr_plan);
+        fa.cr_jobs = static_cast<const GemvJob*>(v.jobs);
+        fa.cr_phases = v.phases;
+        fa.cr_nphase = v.nphase;
+        fa.cr_S = v.S;
+        fa.cy = c.f_cy.p;
+        fa.cx = c.f_cx.p;
+    }
     switch (L.snx) {
 #define X(BW_)                  \
     case BW_:                   \
