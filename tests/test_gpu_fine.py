@@ -297,3 +297,16 @@ def test_fine_solve_c5():
     assert rel_l2(m.u, u) < 0.5  # multiscale vs fine: the method's own error (0.32 on the recorded slab study)
     print(f"C5 fine solve: {it} PCG iterations, relres {rr:.2e}, div residual {dres / dscale:.2e} of scale, "
           f"MRCM vs fine u {rel_l2(m.u, u):.3e}")
+
+
+def test_track_errors_c5_short():
+    """track_errors at C5 (a fine-reference shadow run in lockstep,
+    simulation.cpp:133-150,266-298): three steps run, every step solves the
+    fine system once and records finite flux / saturation errors."""
+    import dataclasses
+    cfg = configs.build("C5")
+    sp = dataclasses.replace(cfg.split, te=4, track_errors=True)
+    r = api.Simulator(cfg.problem).run(sp, cfg.s0(), cfg.inflow_sat)
+    assert r.record.te == 4 and r.record.counters.fine >= 4
+    fe = [s["flux_err"] for s in r.record.steps]
+    assert all(np.isfinite(fe)) and 0.0 < fe[-1] < 1.0
