@@ -874,7 +874,7 @@ void launch_upwind(Ctx& c, const double* s_in, double* s_out, const double* u, d
         // (C5: 191 vs 254 us); short segments (C2, C4) keep the tiled step
         if (c.upwind_col > 0 || (c.upwind_col < 0 && rows >= 16)) {
             const long ncw = (c.L.nx + UC_COLS - 1) / UC_COLS, warps = ncw * ((c.L.ny + rows - 1) / rows);
-            launch_k(c, k_upwind_col<1, 3>, (int)((warps + 7) / 8), 256, 0, c.L, s_in, s_out, u, c.sc, inflow, c.M,
+            launch_k(c, k_upwind_col<1, 4>, (int)((warps + 7) / 8), 256, 0, c.L, s_in, s_out, u, c.sc, inflow, c.M,
                      take_next ? 1 : 0, inj_cn, sub, rows);
         } else if (c.upwind_tiled)
             launch_k(c, k_upwind_tile, dim3(cdiv(c.L.nx, UT_X), cdiv(c.L.ny, UT_Y)), UT_X * UT_Y, 0, c.L, s_in, s_out, u,
