@@ -42,11 +42,18 @@ template <int B>
 __host__ __device__ constexpr int blk_nt() {
     return B / 8;
 }
-// per-warp shared memory (doubles): two Gauss-Jordan buffers, NT tiles of
-// S21, NT tiles of X, 8 right-hand-side values
+// per-warp shared memory (doubles): two Gauss-Jordan buffers, NT-1 tiles of
+// S21, NT-1 tiles of X^T, 8 right-hand-side values, 8 south couplings
 template <int B>
 __host__ __device__ constexpr int blk_smem_doubles() {
-    return 2 * 64 + 2 * blk_nt<B>() * 64 + 8;
+    return 2 * 64 + 2 * (blk_nt<B>() - 1) * 64 + 16;
+}
+// an 8x8 tile in shared memory, row-major, columns XORed with 6 on rows 2, 3,
+// 6, 7: the DMMA operand loads (A: row r, columns q and q+4; B: row q,
+// column pi(r)) then touch every bank pair once per half-warp, and the
+// accumulator pairs (r, 2q..2q+1) stay contiguous
+__device__ __forceinline__ int blk_sw(int row, int col) {
+    return row * 8 + (col ^ (((row >> 1) & 1) * 6));
 }
 
 struct BlkTile {
@@ -110,21 +117,35 @@ struct BlkTransSrc {
 
 // Factorisation with the forward substitution of one right-hand side fused
 // in. y (length n): rhs in, untouched. Xs: n*B doubles, Ts: n doubles
-// (per-panel X fragments and t1 = G y1). sm: blk_smem_doubles<B>() doubles of
+// (per-panel X tiles and t1 = G y1). sm: blk_smem_doubles<B>() doubles of
 // this warp's shared memory. Returns false if a pivot block is not SPD.
+//
+// DMMA and the scalar fp64 instructions share one pipe (a DMMA.884 holds it
+// for 16 cycles, a DFMA for 2), so only the Schur products run on DMMA:
+//  * X is formed directly in the A-operand layout: with B = G Pi, Pi the
+//    column permutation pi(2q) = q, pi(2q+1) = q + 4, the accumulator of lane
+//    (r, q) holds X[r][q], X[r][q+4], which is what the update's A operand and
+//    the stored panel need (X never goes through shared memory for the update);
+//  * the right-hand-side products (t1 = G y1, X_I y1) are quad dot products
+//    (two FMAs and a two-step butterfly);
+//  * row tile NT (S21_NT = diag(s)) is updated by row scalings of X^T, read
+//    back transposed from shared memory, and diag(s) G diag(s).
 template <int B, class Src>
 __device__ bool blk_factor_fwd(int n, const Src& src, double* Xs, double* Ts, double* sm) {
     constexpr int NT = blk_nt<B>();
     static_assert(B % 8 == 0 && NT >= 2, "blocked band solver: B must be a multiple of 8, >= 16");
     const int lane = threadIdx.x & 31;
     const int r = lane >> 2, q = lane & 3, c0 = 2 * q, c1 = c0 + 1;
-    double* sg0 = sm;             // Gauss-Jordan ping-pong buffers (8 x 8, row-major)
+    const int pr = (r >> 1) + 4 * (r & 1);  // pi(r)
+    double* sg0 = sm;                        // Gauss-Jordan ping-pong buffers (swizzled 8 x 8)
     double* sg1 = sm + 64;
-    double* sS = sm + 128;        // S21 tiles 1..NT (index I-1)
-    double* sX = sS + NT * 64;    // X tiles 1..NT-1 (index I-1)
-    double* sy = sX + NT * 64;    // y1
-    BlkTile w[NT + 1][NT + 1];    // lower triangle used (J <= I)
-    double yw[NT + 1];            // y of window rows 8I + r (column 0 of a DMMA accumulator: lanes q == 0)
+    double* sS = sm + 128;                   // S21 tiles 1..NT-1 (index I-1)
+    double* sT = sS + (NT - 1) * 64;         // X^T tiles 1..NT-1
+    double* sy = sT + (NT - 1) * 64;         // y1
+    double* ss = sy + 8;                     // s of row tile NT
+    BlkTile w[NT + 1][NT + 1];               // lower triangle used (J <= I), w[NT][0] unused
+    double yw[NT + 1];   // y of window rows 8I + r (every lane of the row)
+    double s_row = 0.0;  // south coupling of row tile NT's row r into pivot row r
 #pragma unroll
     for (int I = 0; I <= NT; ++I)
 #pragma unroll
@@ -137,16 +158,17 @@ __device__ bool blk_factor_fwd(int n, const Src& src, double* Xs, double* Ts, do
         const bool in = row < n;
         double ed, ew, ew1, es;
         src.decode(row, e, ed, ew, ew1, es);
-        const double d = in ? ed : 1.0, wv = in ? -ew : 0.0, sv = in ? -es : 0.0;
+        const double d = in ? ed : 1.0, wv = in ? -ew : 0.0;
         const double w1 = (row + 1 < n && r < 7) ? -ew1 : 0.0;
         w[I][I].v[0] = c0 == r ? d : (c0 == r - 1 ? wv : (c0 == r + 1 ? w1 : 0.0));
         w[I][I].v[1] = c1 == r ? d : (c1 == r - 1 ? wv : (c1 == r + 1 ? w1 : 0.0));
         yw[I] = in ? e.b : 0.0;
         if (I >= 1) w[I][I - 1].v[1] = (r == 0 && q == 3) ? wv : 0.0;
-        if (I == NT) {
-            w[I][0].v[0] = c0 == r ? sv : 0.0;
-            w[I][0].v[1] = c1 == r ? sv : 0.0;
-        }
+        if (I == NT) s_row = in ? -es : 0.0;
+    };
+    // positive and finite, on the bits (keeps the check off the fp64 pipe)
+    auto spd = [](double v) {
+        return (unsigned long long)(__double_as_longlong(v) - 1) < 0x7fefffffffffffffull;
     };
     // initial window: row tiles 0..NT
 #pragma unroll
@@ -161,63 +183,64 @@ __device__ bool blk_factor_fwd(int n, const Src& src, double* Xs, double* Ts, do
     auto panel = [&](const int p, BlkRowData& ent) {
         const int k0 = 8 * p;
         // ---- G = S11^-1 by Gauss-Jordan (SPD: no pivoting); each lane owns
-        // entries (r, c0), (r, c1) and publishes them every step
+        // entries (r, c0), (r, c0+1) and publishes them every step
         double g0 = w[0][0].v[0], g1 = w[0][0].v[1];
-        *reinterpret_cast<double2*>(sg0 + r * 8 + c0) = make_double2(g0, g1);
+        *reinterpret_cast<double2*>(sg0 + blk_sw(r, c0)) = make_double2(g0, g1);
         // the S21 tiles go to shared memory at the same time (read back in
         // the DMMA operand layout below)
 #pragma unroll
-        for (int I = 1; I <= NT; ++I)
-            *reinterpret_cast<double2*>(sS + (I - 1) * 64 + r * 8 + c0) = make_double2(w[I][0].v[0], w[I][0].v[1]);
-        if (q == 0) sy[r] = yw[0];
+        for (int I = 1; I < NT; ++I)
+            *reinterpret_cast<double2*>(sS + (I - 1) * 64 + blk_sw(r, c0)) = make_double2(w[I][0].v[0], w[I][0].v[1]);
+        if (q == 0) {
+            sy[r] = yw[0];
+            ss[r] = s_row;
+        }
         __syncwarp();
         // four steps with 2 x 2 pivot blocks K = {2m, 2m+1} (half the
-        // dependent chain of scalar pivots); a lane's column pair is a block
+        // dependent chain of scalar pivots); a lane's column pair is a block.
+        // Branch-free: pivot rows take P^-1 A[K][c], pivot columns the
+        // multipliers, the rest A[r][c] - A[r][K] P^-1 A[K][c]
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
             const double* src = (m & 1) ? sg1 : sg0;
             double* dst = (m & 1) ? sg0 : sg1;
-            const double2 k0r = *reinterpret_cast<const double2*>(src + (2 * m) * 8 + 2 * m);      // a, b
-            const double2 k1r = *reinterpret_cast<const double2*>(src + (2 * m + 1) * 8 + 2 * m);  // b', d
-            const double2 arK = *reinterpret_cast<const double2*>(src + r * 8 + 2 * m);            // A[r][K]
-            const double2 aK0 = *reinterpret_cast<const double2*>(src + (2 * m) * 8 + c0);         // A[2m][c]
-            const double2 aK1 = *reinterpret_cast<const double2*>(src + (2 * m + 1) * 8 + c0);     // A[2m+1][c]
+            const double2 k0r = *reinterpret_cast<const double2*>(src + blk_sw(2 * m, 2 * m));      // a, b
+            const double2 k1r = *reinterpret_cast<const double2*>(src + blk_sw(2 * m + 1, 2 * m));  // b', d
+            const double2 arK = *reinterpret_cast<const double2*>(src + blk_sw(r, 2 * m));          // A[r][K]
+            const double2 aK0 = *reinterpret_cast<const double2*>(src + blk_sw(2 * m, c0));         // A[2m][c]
+            const double2 aK1 = *reinterpret_cast<const double2*>(src + blk_sw(2 * m + 1, c0));     // A[2m+1][c]
             const double det = fma(k0r.x, k1r.y, -(k0r.y * k1r.x));
-            ok = ok && (k0r.x > 0.0) && (det > 0.0);
+            ok = ok & spd(k0r.x) & spd(det);
             const double id = fast_rcp(det);
             const double p00 = k1r.y * id, p01 = -k0r.y * id, p10 = -k1r.x * id, p11 = k0r.x * id;  // P^-1
             const double u0 = fma(arK.x, p00, arK.y * p10), u1 = fma(arK.x, p01, arK.y * p11);  // A[r][K] P^-1
-            double n0 = fma(-u0, aK0.x, fma(-u1, aK1.x, g0));
-            double n1 = fma(-u0, aK0.y, fma(-u1, aK1.y, g1));
-            if ((r >> 1) == m) {  // pivot rows: P^-1 A[K][c]
-                const double pr0 = (r & 1) ? p10 : p00, pr1 = (r & 1) ? p11 : p01;
-                n0 = fma(pr0, aK0.x, pr1 * aK1.x);
-                n1 = fma(pr0, aK0.y, pr1 * aK1.y);
-                if (q == m) {
-                    n0 = pr0;
-                    n1 = pr1;
-                }
-            } else if (q == m) {  // pivot columns: -A[r][K] P^-1
-                n0 = -u0;
-                n1 = -u1;
+            const bool prow = (r >> 1) == m;
+            const double al0 = prow ? ((r & 1) ? p10 : p00) : -u0;
+            const double al1 = prow ? ((r & 1) ? p11 : p01) : -u1;
+            const double h0 = prow ? 0.0 : g0, h1 = prow ? 0.0 : g1;
+            g0 = fma(al0, aK0.x, fma(al1, aK1.x, h0));
+            g1 = fma(al0, aK0.y, fma(al1, aK1.y, h1));
+            if (q == m) {
+                g0 = al0;
+                g1 = al1;
             }
-            g0 = n0;
-            g1 = n1;
-            *reinterpret_cast<double2*>(dst + r * 8 + c0) = make_double2(g0, g1);
+            *reinterpret_cast<double2*>(dst + blk_sw(r, c0)) = make_double2(g0, g1);
             __syncwarp();
         }
         const double* sg = sg0;  // 4 steps: the inverse is in buffer 0
-        // ---- operands in DMMA layout
-        const double gb0 = sg[q * 8 + r], gb1 = sg[(q + 4) * 8 + r];  // B = G: lane holds G[q][r], G[q+4][r]
-        double sa[NT][2];                                                // A layout of S21 tiles 1..NT-1
+        // ---- operands in DMMA layout: G as A (G[r][q], G[r][q+4]), G Pi as B
+        // (G[q][pi(r)], G[q+4][pi(r)]), S21 tiles 1..NT-1 as A
+        const double ga0 = sg[blk_sw(r, q)], ga1 = sg[blk_sw(r, q + 4)];
+        const double gb0 = sg[blk_sw(q, pr)], gb1 = sg[blk_sw(q + 4, pr)];
+        double sa[NT - 1][2];
 #pragma unroll
         for (int I = 1; I < NT; ++I) {
-            sa[I - 1][0] = sS[(I - 1) * 64 + r * 8 + q];
-            sa[I - 1][1] = sS[(I - 1) * 64 + r * 8 + q + 4];
+            sa[I - 1][0] = sS[(I - 1) * 64 + blk_sw(r, q)];
+            sa[I - 1][1] = sS[(I - 1) * 64 + blk_sw(r, q + 4)];
         }
-        const double* sN = sS + (NT - 1) * 64;  // S21 tile NT (diagonal: south couplings)
-        const double s_r = sN[r * 8 + r], s_c0 = sN[c0 * 8 + c0], s_c1 = sN[c1 * 8 + c1];
-        // ---- X = S21 G
+        const double yq0 = sy[q], yq1 = sy[q + 4];
+        const double2 sc = *reinterpret_cast<const double2*>(ss + c0);  // s of rows c0, c0+1
+        // ---- X = S21 G, in A layout (lane: X[r][q], X[r][q+4])
         BlkTile x[NT + 1];
 #pragma unroll
         for (int I = 1; I < NT; ++I) {
@@ -225,49 +248,55 @@ __device__ bool blk_factor_fwd(int n, const Src& src, double* Xs, double* Ts, do
             blk_dmma(x[I].v[0], x[I].v[1], sa[I - 1][0], gb0);
             blk_dmma(x[I].v[0], x[I].v[1], sa[I - 1][1], gb1);
         }
-        x[NT].v[0] = s_r * g0;
-        x[NT].v[1] = s_r * g1;
+        x[NT].v[0] = s_row * ga0;
+        x[NT].v[1] = s_row * ga1;
         // stored for the backward sweep: tiles 1..NT, fragment order (coalesced)
         double* xs = Xs + (size_t)p * NT * 64;
 #pragma unroll
         for (int I = 1; I <= NT; ++I)
             *reinterpret_cast<double2*>(xs + (I - 1) * 64 + 2 * lane) = make_double2(x[I].v[0], x[I].v[1]);
-        // ---- trailing update S22 -= X S21^T
+        // X^T for row tile NT's update
 #pragma unroll
-        for (int I = 1; I < NT; ++I)
-            *reinterpret_cast<double2*>(sX + (I - 1) * 64 + r * 8 + c0) = make_double2(x[I].v[0], x[I].v[1]);
-        __syncwarp();
-        // forward substitution on the tensor cores too: y1 is the B operand
-        // column 0 (lane (0, q) holds y1[q], y1[q+4]), so X_I Y1 and t1 = G y1
-        // land in column 0 of the accumulators, lanes q == 0 (no shuffles)
-        const double yb0 = r == 0 ? sy[q] : 0.0, yb1 = r == 0 ? sy[q + 4] : 0.0;
-        {
-            double t1 = 0.0, z1 = 0.0;
-            blk_dmma(t1, z1, sg[r * 8 + q], yb0);
-            blk_dmma(t1, z1, sg[r * 8 + q + 4], yb1);
-            st_global_if(Ts + k0 + r, t1, q == 0);
-            yw[NT] -= s_r * t1;  // X_NT y1 = diag(s) G y1
+        for (int J = 1; J < NT; ++J) {
+            sT[(J - 1) * 64 + blk_sw(q, r)] = x[J].v[0];
+            sT[(J - 1) * 64 + blk_sw(q + 4, r)] = x[J].v[1];
         }
+        // ---- forward substitution: t1 = G y1 and y_I -= X_I y1 as quad dot
+        // products (lane: columns q and q+4)
+        double t1 = fma(ga0, yq0, ga1 * yq1);
+        double py[NT];
+#pragma unroll
+        for (int I = 1; I < NT; ++I) py[I] = fma(x[I].v[0], yq0, x[I].v[1] * yq1);
+#pragma unroll
+        for (int o = 1; o < 4; o <<= 1) {
+            t1 += __shfl_xor_sync(0xffffffffu, t1, o);
+#pragma unroll
+            for (int I = 1; I < NT; ++I) py[I] += __shfl_xor_sync(0xffffffffu, py[I], o);
+        }
+        st_global_if(Ts + k0 + r, t1, q == 0);
+        yw[NT] -= s_row * t1;  // X_NT y1 = diag(s) G y1
+#pragma unroll
+        for (int I = 1; I < NT; ++I) yw[I] -= py[I];
+        // ---- trailing update S22 -= X S21^T on DMMA (row tiles 1..NT-1)
 #pragma unroll
         for (int I = 1; I < NT; ++I) {
-            const double xa0 = -sX[(I - 1) * 64 + r * 8 + q], xa1 = -sX[(I - 1) * 64 + r * 8 + q + 4];
-            double z1 = 0.0;
-            blk_dmma(yw[I], z1, xa0, yb0);
-            blk_dmma(yw[I], z1, xa1, yb1);
+            const double xa0 = -x[I].v[0], xa1 = -x[I].v[1];
 #pragma unroll
             for (int J = 1; J <= I; ++J) {
                 blk_dmma(w[I][J].v[0], w[I][J].v[1], xa0, sa[J - 1][0]);
                 blk_dmma(w[I][J].v[0], w[I][J].v[1], xa1, sa[J - 1][1]);
             }
         }
-        // row tile NT: S21_NT = diag(s), so X_NT = diag(s) G
+        __syncwarp();  // X^T visible
+        // row tile NT: -= diag(s) X_J^T (J < NT), -= diag(s) G diag(s)
 #pragma unroll
-        for (int J = 1; J < NT; ++J) {  // -= diag(s) X_J^T
-            w[NT][J].v[0] -= s_r * sX[(J - 1) * 64 + c0 * 8 + r];
-            w[NT][J].v[1] -= s_r * sX[(J - 1) * 64 + c1 * 8 + r];
+        for (int J = 1; J < NT; ++J) {
+            const double2 xt = *reinterpret_cast<const double2*>(sT + (J - 1) * 64 + blk_sw(r, c0));
+            w[NT][J].v[0] = fma(-s_row, xt.x, w[NT][J].v[0]);
+            w[NT][J].v[1] = fma(-s_row, xt.y, w[NT][J].v[1]);
         }
-        w[NT][NT].v[0] -= s_r * g0 * s_c0;
-        w[NT][NT].v[1] -= s_r * g1 * s_c1;
+        w[NT][NT].v[0] = fma(-(s_row * g0), sc.x, w[NT][NT].v[0]);
+        w[NT][NT].v[1] = fma(-(s_row * g1), sc.y, w[NT][NT].v[1]);
         // ---- shift the window by one row tile; row tile NT enters
 #pragma unroll
         for (int I = 0; I < NT; ++I)
@@ -289,12 +318,14 @@ __device__ bool blk_factor_fwd(int n, const Src& src, double* Xs, double* Ts, do
 }
 
 // Backward sweep x1 = t1 - X^T x2 from the stored panels; x (length n) out.
-// Returns this lane's partial sum of x (lanes 0..3 hold all of it).
+// Lane (r, q) holds X[r][q], X[r][q+4] of each stored tile, so the column
+// sums over r give x1[q] and x1[q+4]. Returns this lane's partial sum of x
+// (lanes 0..3 hold all of it).
 template <int B>
 __device__ double blk_backward(int n, const double* Xs, const double* Ts, double* x) {
     constexpr int NT = blk_nt<B>();
     const int lane = threadIdx.x & 31;
-    const int r = lane >> 2, q = lane & 3, c0 = 2 * q;
+    const int r = lane >> 2, q = lane & 3;
     const int np = n / 8;
     double xw[NT];  // x of rows k0+8+8i+r (i = 0..NT-1): the rows after the panel
 #pragma unroll
@@ -305,7 +336,7 @@ __device__ double blk_backward(int n, const double* Xs, const double* Ts, double
         const double* xs = Xs + (size_t)pp * NT * 64;
 #pragma unroll
         for (int I = 0; I < NT; ++I) xt[I] = *reinterpret_cast<const double2*>(xs + I * 64 + 2 * lane);
-        tt = *reinterpret_cast<const double2*>(Ts + 8 * pp + c0);
+        tt = make_double2(Ts[8 * pp + q], Ts[8 * pp + q + 4]);
     };
     // four-panel-deep register ring of the stored panels (an HBM round trip
     // is several panels long); unrolled by four so slots are never moved
@@ -325,15 +356,16 @@ __device__ double blk_backward(int n, const double* Xs, const double* Ts, double
             a0 += __shfl_xor_sync(0xffffffffu, a0, o);
             a1 += __shfl_xor_sync(0xffffffffu, a1, o);
         }
-        const double x0 = tt.x - a0, x1 = tt.y - a1;
+        const double x0 = tt.x - a0, x1 = tt.y - a1;  // x1[q], x1[q+4]
         if (r == 0) {
-            *reinterpret_cast<double2*>(x + 8 * p + c0) = make_double2(x0, x1);
+            x[8 * p + q] = x0;
+            x[8 * p + q + 4] = x1;
             sum += x0 + x1;
         }
-        const double v0 = __shfl_sync(0xffffffffu, x0, r >> 1), v1 = __shfl_sync(0xffffffffu, x1, r >> 1);
+        const double v0 = __shfl_sync(0xffffffffu, x0, r & 3), v1 = __shfl_sync(0xffffffffu, x1, r & 3);
 #pragma unroll
         for (int i = NT - 1; i > 0; --i) xw[i] = xw[i - 1];
-        xw[0] = (r & 1) ? v1 : v0;
+        xw[0] = (r & 4) ? v1 : v0;
         fetch(p - DEPTH, xt, tt);
     };
     for (int p = np - 1; p >= 0; p -= DEPTH) {  // np = B^2/8 is a multiple of 8
