@@ -190,6 +190,16 @@ Layout make_layout(const mpm2p_problem* P) {
     L.ly = P->ly;
     L.hx = P->lx / P->nx;
     L.hy = P->ly / P->ny;
+    {
+        int e;
+        const bool px = std::frexp(L.hx, &e) == 0.5, py = std::frexp(L.hy, &e) == 0.5;
+        const double v = L.hx * L.hy;
+        L.pow2 = px && py && std::isnormal(v) && std::isnormal(1.0 / v) && std::isnormal(1.0 / L.hx) &&
+                 std::isnormal(1.0 / L.hy);
+        L.inv_hx = 1.0 / L.hx;
+        L.inv_hy = 1.0 / L.hy;
+        L.inv_vol = 1.0 / v;
+    }
     L.nsx = P->nsx;
     L.nsy = P->nsy;
     L.snx = P->nx / P->nsx;

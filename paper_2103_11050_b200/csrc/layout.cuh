@@ -59,6 +59,11 @@ struct Layout {
     // bc_kind == BC_ROBIN
     const double* rb_beta = nullptr;
     const double* rb_rhs = nullptr;
+    // hx, hy (hence vol) exact powers of two: a division by them is then the
+    // multiplication by the exact reciprocal, bit for bit (both round the same
+    // real number), and the hot kernels take that path
+    bool pow2 = false;
+    double inv_hx = 0.0, inv_hy = 0.0, inv_vol = 0.0;
 
     HD int cells() const { return nx * ny; }
     HD int vcount() const { return (nx + 1) * ny; }
@@ -69,6 +74,16 @@ struct Layout {
     HD int hface(int i, int j) const { return vcount() + j * nx + i; }
     HD double vol() const { return hx * hy; }
     HD double area(int f) const { return f < vcount() ? hy : hx; }
+    // x / hx, x / hy, x / vol with the reference's rounding
+#ifdef __CUDA_ARCH__
+    __device__ double div_hx(double x) const { return pow2 ? __dmul_rn(x, inv_hx) : __ddiv_rn(x, hx); }
+    __device__ double div_hy(double x) const { return pow2 ? __dmul_rn(x, inv_hy) : __ddiv_rn(x, hy); }
+    __device__ double div_vol(double x) const { return pow2 ? __dmul_rn(x, inv_vol) : __ddiv_rn(x, hx * hy); }
+#else
+    double div_hx(double x) const { return x / hx; }
+    double div_hy(double x) const { return x / hy; }
+    double div_vol(double x) const { return x / vol(); }
+#endif
 
     // subdomain-local grid (snx x sny, same spacing)
     HD int lvcount() const { return (snx + 1) * sny; }
@@ -248,7 +263,7 @@ HD double eff_robin(double t_half, double beta, double area) {
     return 1.0 / (1.0 / t_half + beta / area);
 }
 // harmonic-mean interior transmissibility (elliptic.cpp:46,50,56)
-HD double harm_trans_v(const Layout& L, double a, double b) { return 2.0 * a * b / (a + b) * L.hy / L.hx; }
-HD double harm_trans_h(const Layout& L, double a, double b) { return 2.0 * a * b / (a + b) * L.hx / L.hy; }
+HD double harm_trans_v(const Layout& L, double a, double b) { return L.div_hx(2.0 * a * b / (a + b) * L.hy); }
+HD double harm_trans_h(const Layout& L, double a, double b) { return L.div_hy(2.0 * a * b / (a + b) * L.hx); }
 
 }  // namespace mpm2p

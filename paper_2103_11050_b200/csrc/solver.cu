@@ -1351,12 +1351,12 @@ __global__ void __launch_bounds__(256, 4) k_ds_u_div(Layout L, const double* __r
         const double en = hn ? 0.0 : (j + 1 < L.ny ? -EU[(size_t)(s + L.nsx) * L.nbe + 2 * L.sny + ii]
                                                    : EU[eo + 2 * L.sny + L.snx + ii]);
         const double qc = q[cc];
-        const double uW = hw ? tw * (xw - xc) / hy : -ew;
+        const double uW = hw ? L.div_hy(tw * (xw - xc)) : -ew;
         double uE = __shfl_down_sync(0xffffffffu, uW, 1);
-        if (de) uE = he ? te * (xc - xe) / hy : ee;
+        if (de) uE = he ? L.div_hy(te * (xc - xe)) : ee;
         if (!valid) continue;
-        const double uS = hs ? ts * (xs - xc) / hx : -es;
-        const double uN = hn ? tn * (xc - xn) / hx : en;
+        const double uS = hs ? L.div_hx(ts * (xs - xc)) : -es;
+        const double uN = hn ? L.div_hx(tn * (xc - xn)) : en;
         u[L.vface(i, j)] = uW;
         u[L.hface(i, j)] = uS;
         vmax = fmax(vmax, fabs(uW));
@@ -1372,7 +1372,7 @@ __global__ void __launch_bounds__(256, 4) k_ds_u_div(Layout L, const double* __r
         // divergence(u) - q (grid.cpp:19-31), unfused as in the reference build
         const double fx = __dmul_rn(__dsub_rn(uE, uW), hy);
         const double fy = __dmul_rn(__dsub_rn(uN, uS), hx);
-        res = fmax(res, fabs(__dsub_rn(__ddiv_rn(__dadd_rn(fx, fy), vol), qc)));
+        res = fmax(res, fabs(__dsub_rn(L.div_vol(__dadd_rn(fx, fy)), qc)));
         qmax = fmax(qmax, fabs(qc));
         if (cfl.on) {  // cfl_timestep's per-cell outflux (transport.cpp:59-67), same order and rounding
             double o = __dmul_rn(0.0 < uE ? uE : 0.0, hy);
@@ -1638,16 +1638,16 @@ __global__ void __launch_bounds__(256) k_mpm_rhs_w(Layout L, int max_rhs, int an
         const double us = hs ? 0.0 : WU[eo + eS], un = hn ? 0.0 : WU[eo + eN];
         const double xw = hw ? 0.0 : ET[eo + eW], xe = he ? 0.0 : ET[eo + eE];
         const double xs = hs ? 0.0 : ET[eo + eS], xn = hn ? 0.0 : ET[eo + eN];
-        const double wW = hw ? tw * (pw - pc) / hy : -uw;
+        const double wW = hw ? L.div_hy(tw * (pw - pc)) : -uw;
         double wE = __shfl_down_sync(0xffffffffu, wW, 1);
         if (!he) wE = ue;
-        else if (de) wE = te * (pc - pe) / hy;
+        else if (de) wE = L.div_hy(te * (pc - pe));
         if (!valid) continue;
-        const double wS = hs ? ts * (ps - pc) / hx : -us;
-        const double wN = hn ? tn * (pc - pn) / hx : un;
+        const double wS = hs ? L.div_hx(ts * (ps - pc)) : -us;
+        const double wN = hn ? L.div_hx(tn * (pc - pn)) : un;
         const double fx = __dmul_rn(__dsub_rn(wE, wW), hy);
         const double fy = __dmul_rn(__dsub_rn(wN, wS), hx);
-        const double divw = __ddiv_rn(__dadd_rn(fx, fy), vol);
+        const double divw = L.div_vol(__dadd_rn(fx, fy));
         double b = __dmul_rn(__dsub_rn(qc, divw), vol);
         if (!hw) b = __dadd_rn(b, xw);
         if (!he) b = __dadd_rn(b, xe);
