@@ -280,8 +280,11 @@ def _profile(sim, lib, steps):
 
 
 def _simulate(api, lib, cfg):
-    """One whole simulation through the C ABI: create + run (+ C3's second pass)."""
+    """One whole simulation through the C ABI: create + run (+ C3's second pass).
+    Returns (steps, rebuilds, seconds); the context teardown after the run is
+    not in the timed region."""
     import dataclasses
+    t0 = time.perf_counter()
     sim = api.Simulator(cfg.problem, lib)
     try:
         res = sim.run(cfg.split, cfg.s0(), cfg.inflow_sat)
@@ -295,7 +298,7 @@ def _simulate(api, lib, cfg):
             res2 = sim.run(sp2, cfg.s0(), cfg.inflow_sat)
             steps += res2.record.te - 1
             rebuilds += res2.record.tm_total
-        return steps, rebuilds
+        return steps, rebuilds, time.perf_counter() - t0
     finally:
         sim.close()
 
@@ -310,14 +313,11 @@ def _e2e(api, lib, cfg, args, reps=3):
     # one untimed simulation first: process-level one-time costs (module
     # loading, allocator pools) are not per-simulation work; short runs
     # (< 1 s) take the median of five
-    t0 = time.perf_counter()
-    _simulate(api, lib, cfg)
-    if time.perf_counter() - t0 < 1.0:
+    if _simulate(api, lib, cfg)[2] < 1.0:
         reps = max(reps, 5)
     for _ in range(reps):
-        t0 = time.perf_counter()
-        steps, rebuilds = _simulate(api, lib, cfg)
-        walls.append(time.perf_counter() - t0)
+        steps, rebuilds, w = _simulate(api, lib, cfg)
+        walls.append(w)
     wall = sorted(walls)[len(walls) // 2]
     cells = cfg.cells
     faces = (cfg.problem.nx + 1) * cfg.problem.ny + cfg.problem.nx * (cfg.problem.ny + 1)

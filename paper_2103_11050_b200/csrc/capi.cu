@@ -5,6 +5,7 @@
 // (errors.hpp:9-24) as status codes.
 #include <new>
 #include <algorithm>
+#include <mutex>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -76,11 +77,99 @@ int guarded(mpm2p_ctx* ctx, F&& fn) {
     }
 }
 
+// Large transfers from / to pageable host memory go through pinned staging:
+// a pageable cudaMemcpy runs through the driver's bounce buffer with one host
+// thread (C5's final s, p, u: 0.54 GB in ~112 ms). Two pinned 16 MB buffers
+// per device, shared by the process's contexts; the device copies are
+// pipelined against a multi-threaded host memcpy.
+struct HostStage {
+    std::mutex mu;
+    char* buf[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2];
+    bool ready = false;
+};
+constexpr size_t STAGE_BYTES = size_t(16) << 20;
+constexpr size_t STAGE_MIN = size_t(8) << 20;  // smaller transfers: the plain copy
+constexpr int STAGE_DEVICES = 64;
+
+HostStage* host_stage() {  // the calling thread's current device, nullptr if unusable
+    static HostStage stages[STAGE_DEVICES];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= STAGE_DEVICES) return nullptr;
+    HostStage& h = stages[dev];
+    std::lock_guard<std::mutex> g(h.mu);
+    if (!h.ready) {
+        for (int k = 0; k < 2; ++k) {
+            CK(cudaMallocHost(&h.buf[k], STAGE_BYTES));
+            CK(cudaEventCreateWithFlags(&h.ev[k], cudaEventDisableTiming));
+        }
+        h.ready = true;
+    }
+    return &h;
+}
+
+bool host_pinned(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+void par_memcpy(void* dst, const void* src, size_t bytes) {
+    const int nt = (int)std::max<size_t>(1, std::min<size_t>(8, bytes >> 20));
+#pragma omp parallel for num_threads(nt) schedule(static)
+    for (int t = 0; t < nt; ++t) {
+        const size_t b0 = bytes * t / nt, b1 = bytes * (t + 1) / nt;
+        std::memcpy(static_cast<char*>(dst) + b0, static_cast<const char*>(src) + b0, b1 - b0);
+    }
+}
+
 void upload(Ctx& c, double* dst, const double* src, size_t n) {
-    CK(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyHostToDevice, c.st));
+    const size_t bytes = n * sizeof(double);
+    HostStage* h = bytes >= STAGE_MIN && !host_pinned(src) ? host_stage() : nullptr;
+    if (!h) {
+        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c.st));
+        return;
+    }
+    std::lock_guard<std::mutex> g(h->mu);
+    const size_t nch = (bytes + STAGE_BYTES - 1) / STAGE_BYTES;
+    for (size_t k = 0; k < nch; ++k) {
+        const int b = (int)(k & 1);
+        const size_t off = k * STAGE_BYTES, len = std::min(STAGE_BYTES, bytes - off);
+        if (k >= 2) CK(cudaEventSynchronize(h->ev[b]));  // chunk k-2 has left this buffer
+        par_memcpy(h->buf[b], reinterpret_cast<const char*>(src) + off, len);
+        CK(cudaMemcpyAsync(reinterpret_cast<char*>(dst) + off, h->buf[b], len, cudaMemcpyHostToDevice, c.st));
+        CK(cudaEventRecord(h->ev[b], c.st));
+    }
+    CK(cudaStreamSynchronize(c.st));  // the staging buffers are reused by the next transfer
 }
 void download(Ctx& c, double* dst, const double* src, size_t n) {
-    if (dst) CK(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDeviceToHost, c.st));
+    if (!dst) return;
+    const size_t bytes = n * sizeof(double);
+    HostStage* h = bytes >= STAGE_MIN && !host_pinned(dst) ? host_stage() : nullptr;
+    if (!h) {
+        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c.st));
+        return;
+    }
+    std::lock_guard<std::mutex> g(h->mu);
+    const size_t nch = (bytes + STAGE_BYTES - 1) / STAGE_BYTES;
+    auto issue = [&](size_t k) {
+        const int b = (int)(k & 1);
+        const size_t off = k * STAGE_BYTES, len = std::min(STAGE_BYTES, bytes - off);
+        CK(cudaMemcpyAsync(h->buf[b], reinterpret_cast<const char*>(src) + off, len, cudaMemcpyDeviceToHost, c.st));
+        CK(cudaEventRecord(h->ev[b], c.st));
+    };
+    issue(0);
+    if (nch > 1) issue(1);
+    for (size_t k = 0; k < nch; ++k) {
+        const int b = (int)(k & 1);
+        const size_t off = k * STAGE_BYTES, len = std::min(STAGE_BYTES, bytes - off);
+        CK(cudaEventSynchronize(h->ev[b]));
+        par_memcpy(reinterpret_cast<char*>(dst) + off, h->buf[b], len);
+        if (k + 2 < nch) issue(k + 2);
+    }
 }
 
 // Reads the per-step scalars back and raises the reference's exceptions for
@@ -127,19 +216,24 @@ void build_csr(Ctx& c) {
     const Layout& L = c.L;
     const int np = L.dim_flux;
     std::vector<int> ptr(1, 0), col;
+    ptr.reserve(2 * (size_t)np + 1);
+    col.reserve(2 * (size_t)np * 16);
     for (int R = 0; R < 2 * np; ++R) {
         const int rb = R < np ? R : R - np;
         const int k = L.basis_iface(rb);
-        std::set<int> nb;
+        int nb[8], nn = 0;  // interfaces incident to either side's subdomain, ascending, distinct
         for (int s : {L.iface_minus(k), L.iface_plus(k)}) {
             int inc[4];
             const int ni = L.incident(s, inc);
-            for (int a = 0; a < ni; ++a) nb.insert(inc[a]);
+            for (int a = 0; a < ni; ++a) nb[nn++] = inc[a];
         }
-        for (int kk : nb)
-            for (int t = 0; t < L.iface_nb(kk); ++t) col.push_back(L.iface_first_basis(kk) + t);
-        for (int kk : nb)
-            for (int t = 0; t < L.iface_nb(kk); ++t) col.push_back(np + L.iface_first_basis(kk) + t);
+        for (int a = 1; a < nn; ++a)  // insertion sort of <= 8 entries
+            for (int b = a; b > 0 && nb[b - 1] > nb[b]; --b) std::swap(nb[b - 1], nb[b]);
+        nn = (int)(std::unique(nb, nb + nn) - nb);
+        for (int a = 0; a < nn; ++a)
+            for (int t = 0; t < L.iface_nb(nb[a]); ++t) col.push_back(L.iface_first_basis(nb[a]) + t);
+        for (int a = 0; a < nn; ++a)
+            for (int t = 0; t < L.iface_nb(nb[a]); ++t) col.push_back(np + L.iface_first_basis(nb[a]) + t);
         ptr.push_back((int)col.size());
     }
     c.nnz = (int)col.size();
