@@ -381,6 +381,7 @@ void create_ctx(mpm2p_ctx* ctx, const mpm2p_problem* P) {
     if (const char* e = std::getenv("MPM2P_UPWIND_TILE")) c.upwind_tiled = e[0] != '0';
     if (const char* e = std::getenv("MPM2P_UPWIND_COL")) c.upwind_col = std::atoi(e);
     if (const char* e = std::getenv("MPM2P_KAPPA_COL")) c.kappa_col = std::atoi(e);
+    if (const char* e = std::getenv("MPM2P_HOM_GROUP")) c.hom_group = std::atoi(e);
     if (const char* e = std::getenv("MPM2P_RHS_SUB")) c.rhs_sub = e[0] != '0';
     if (const char* e = std::getenv("MPM2P_REFINE")) {  // 1: always refine, 0: never (experiments)
         c.force_refine = e[0] == '1';

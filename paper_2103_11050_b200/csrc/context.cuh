@@ -131,6 +131,7 @@ struct Ctx {
     DevBuf<double> sep_qx, sep_qy, sep_lam, sep_z1, sep_z2;
     bool rhs_sub = true;  // k_mpm_rhs_sub, one CTA per subdomain (MPM2P_RHS_SUB=0: one thread per cell)
     int kappa_col = -1;        // k_kappa_col: -1 auto (long row segments), 1 always, 0 never (MPM2P_KAPPA_COL)
+    int hom_group = 8;         // homogeneous solves per warp in the rebuild (k_hom_solve_rm); 1: k_hom_solve_r (MPM2P_HOM_GROUP)
     int upwind_col = -1;       // k_upwind_col: -1 auto (long row segments), 1 always, 0 never (MPM2P_UPWIND_COL)
     bool upwind_tiled = true;  // k_upwind_tile (MPM2P_UPWIND_TILE=0: one thread per cell, k_upwind)
     bool ds_pending = false;  // a forked factor awaits its join (ev_join)

@@ -27,6 +27,7 @@ namespace {
 
 constexpr int TPB = 256;
 constexpr int WPB = 4;  // warps (subdomains) per block in banded kernels
+constexpr int HOM_GROUP = 8;  // homogeneous right-hand sides per warp in k_hom_solve_rm
 
 __device__ __forceinline__ bool last_block_done(unsigned* counter) {
     __shared__ bool last;
@@ -1040,6 +1041,34 @@ __global__ void __launch_bounds__(WPB * 32) k_hom_solve_r(Layout L, int max_rhs,
     forward_reg<B, 1>(n, Lc + so * B, x, 1, n, nullptr, ring[w]);
     __syncwarp();
     backward_reg<B, 1>(n, D + so, Lr + so * B, x, 1, n, nullptr, ring[w]);
+}
+
+// Homogeneous solves, HR right-hand sides per warp: one warp per (subdomain,
+// group of HR functions) streams the subdomain's stored factor once for the
+// whole group (the single-RHS kernel above streams it once per function).
+// Per function the arithmetic and its order are those of k_hom_solve_r, so
+// the solutions are bit-identical.
+template <int B, int HR>
+__global__ void __launch_bounds__(WPB * 32) k_hom_solve_rm(Layout L, int max_rhs, int groups,
+                                                           const double* __restrict__ D,
+                                                           const double* __restrict__ Lc,
+                                                           const double* __restrict__ Lr, double* X) {
+    pdl_begin();
+    __shared__ __align__(16) double ring[WPB][sweep_ring<B>() * B * B + 2];
+    __shared__ __align__(16) double xb[WPB][2 * xchg_ys<HR>()];
+    const int w = threadIdx.x >> 5;
+    const int gw = blockIdx.x * WPB + w;
+    const int s = gw / groups, h0 = (gw % groups) * HR;
+    if (s >= L.n_sub) return;
+    const int nh = L.n_hom(s) - h0;
+    if (nh <= 0) return;
+    const int nr = nh < HR ? nh : HR;
+    const int n = L.ncs;
+    const size_t so = (size_t)s * n;
+    double* x = X + xoff(L, max_rhs, s, 1 + h0);
+    forward_reg<B, HR>(n, Lc + so * B, x, nr, n, xb[w], ring[w]);
+    __syncwarp();
+    backward_reg<B, HR>(n, D + so, Lr + so * B, x, nr, n, xb[w], ring[w]);
 }
 
 // Two-sided band kernels (band_twist.cuh): one team per block — one warp
@@ -2442,8 +2471,14 @@ void launch_basis_core(Ctx& c, const double* kappa) {
         if (L.max_hom > 0) {                                                                                        \
             CK_LAUNCH();                                                                                            \
             PROF(c, "k_hom_solve");                                                                                 \
-            launch_k(c, k_hom_solve_r<BW_>, cdiv((long long)L.n_sub * L.max_hom, WPB), WPB * 32, 0,                   \
-                L, c.max_rhs, c.Dm, c.Lcm, c.Lrm, c.X);                                                             \
+            if (c.hom_group > 1) {                                                                                  \
+                const int groups = cdiv(L.max_hom, HOM_GROUP);                                                      \
+                launch_k(c, k_hom_solve_rm<BW_, HOM_GROUP>, cdiv((long long)L.n_sub * groups, WPB), WPB * 32, 0,    \
+                    L, c.max_rhs, groups, c.Dm, c.Lcm, c.Lrm, c.X);                                                 \
+            } else {                                                                                                \
+                launch_k(c, k_hom_solve_r<BW_>, cdiv((long long)L.n_sub * L.max_hom, WPB), WPB * 32, 0,             \
+                    L, c.max_rhs, c.Dm, c.Lcm, c.Lrm, c.X);                                                         \
+            }                                                                                                       \
         }                                                                                                           \
         break;
             MPM2P_BAND_WIDTHS(X)
