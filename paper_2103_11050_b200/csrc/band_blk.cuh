@@ -20,10 +20,15 @@
 //    DMMA count per panel: 2(NT-1) for X plus NT(NT-1) for the update
 //    (C5: 18 DMMA per 8 pivots).
 //  * Solve: forward y2 -= X y1 and t1 = G y1 fused into the factorisation
-//    (DMMA with y1 as column 0 of the B operand);
-//    backward x1 = t1 - X^T x2. Only X (B x 8 per panel, the accumulator
-//    fragments as they are) and t1 are stored: n*B + n doubles per subdomain,
-//    the same footprint as the scalar factor's L.
+//    (quad dot products); backward x1 = t1 - X^T x2. Only X (B x 8 per panel,
+//    the accumulator fragments as they are) and t1 are stored: n*B + n doubles
+//    per subdomain, the same footprint as the scalar factor's L.
+//  * No operand ever changes layout: the k index of an m8n8k4 product is a
+//    dummy, so labelling slab s of lane (r, q) as k = 2q + s makes an
+//    accumulator fragment (lane: [r][2q], [r][2q+1]) usable as it is both as
+//    the A operand (rows r) and, for a product with the tile's transpose, as
+//    the B operand (B[k][n = r] = tile[r][k]). X = S21 G takes S21's fragment
+//    as A and G's as B (G is symmetric), S22 -= X S21^T takes X's and S21's.
 #pragma once
 
 #include "band.cuh"
@@ -42,16 +47,14 @@ template <int B>
 __host__ __device__ constexpr int blk_nt() {
     return B / 8;
 }
-// per-warp shared memory (doubles): two Gauss-Jordan buffers, NT-1 tiles of
-// S21, NT-1 tiles of X^T, 8 right-hand-side values, 8 south couplings
+// per-warp shared memory (doubles): two Gauss-Jordan buffers, 8 right-hand-
+// side values, 8 south couplings, NT-1 tiles of X^T
 template <int B>
 __host__ __device__ constexpr int blk_smem_doubles() {
-    return 2 * 64 + 2 * (blk_nt<B>() - 1) * 64 + 16;
+    return 2 * 64 + 16 + (blk_nt<B>() - 1) * 64;
 }
 // an 8x8 tile in shared memory, row-major, columns XORed with 6 on rows 2, 3,
-// 6, 7: the DMMA operand loads (A: row r, columns q and q+4; B: row q,
-// column pi(r)) then touch every bank pair once per half-warp, and the
-// accumulator pairs (r, 2q..2q+1) stay contiguous
+// 6, 7 (the accumulator pairs (r, 2q..2q+1) stay contiguous)
 __device__ __forceinline__ int blk_sw(int row, int col) {
     return row * 8 + (col ^ (((row >> 1) & 1) * 6));
 }
@@ -120,29 +123,29 @@ struct BlkTransSrc {
 // (per-panel X tiles and t1 = G y1). sm: blk_smem_doubles<B>() doubles of
 // this warp's shared memory. Returns false if a pivot block is not SPD.
 //
-// DMMA and the scalar fp64 instructions share one pipe (a DMMA.884 holds it
-// for 16 cycles, a DFMA for 2), so only the Schur products run on DMMA:
-//  * X is formed directly in the A-operand layout: with B = G Pi, Pi the
-//    column permutation pi(2q) = q, pi(2q+1) = q + 4, the accumulator of lane
-//    (r, q) holds X[r][q], X[r][q+4], which is what the update's A operand and
-//    the stored panel need (X never goes through shared memory for the update);
+// The kernel is bound by the shared-memory data pipe and by issue slots, not
+// by the DMMA pipe (profiles/blk_factor_r02_analysis.txt), so everything but
+// the pivot block's Gauss-Jordan stays in registers:
+//  * X_I = S21_I G and S22[I][J] -= X_I S21_J^T take their operands straight
+//    from the accumulator fragments (see the header);
+//  * row tile NT (S21_NT = diag(s), so X_NT = diag(s) G is a row scaling of
+//    G's fragment) is updated by row scalings of X^T, read back transposed
+//    from shared memory (NTD = false), or by the same DMMA products with X_NT
+//    as A (NTD = true: 2(NT-1) more DMMA per panel, no shared memory; measured
+//    2 % slower at B = 32, 1810 against 1774 us for 16,384 subdomains);
 //  * the right-hand-side products (t1 = G y1, X_I y1) are quad dot products
-//    (two FMAs and a two-step butterfly);
-//  * row tile NT (S21_NT = diag(s)) is updated by row scalings of X^T, read
-//    back transposed from shared memory, and diag(s) G diag(s).
-template <int B, class Src>
+//    (two FMAs and a two-step butterfly).
+template <int B, class Src, bool NTD = false>
 __device__ bool blk_factor_fwd(int n, const Src& src, double* Xs, double* Ts, double* sm) {
     constexpr int NT = blk_nt<B>();
     static_assert(B % 8 == 0 && NT >= 2, "blocked band solver: B must be a multiple of 8, >= 16");
     const int lane = threadIdx.x & 31;
     const int r = lane >> 2, q = lane & 3, c0 = 2 * q, c1 = c0 + 1;
-    const int pr = (r >> 1) + 4 * (r & 1);  // pi(r)
-    double* sg0 = sm;                        // Gauss-Jordan ping-pong buffers (swizzled 8 x 8)
+    double* sg0 = sm;        // Gauss-Jordan ping-pong buffers (swizzled 8 x 8)
     double* sg1 = sm + 64;
-    double* sS = sm + 128;                   // S21 tiles 1..NT-1 (index I-1)
-    double* sT = sS + (NT - 1) * 64;         // X^T tiles 1..NT-1
-    double* sy = sT + (NT - 1) * 64;         // y1
-    double* ss = sy + 8;                     // s of row tile NT
+    double* sy = sm + 128;   // y1
+    double* ss = sy + 8;     // s of row tile NT
+    double* sT = ss + 8;     // (NTD = false) X^T tiles 1..NT-1
     BlkTile w[NT + 1][NT + 1];               // lower triangle used (J <= I), w[NT][0] unused
     double yw[NT + 1];   // y of window rows 8I + r (every lane of the row)
     double s_row = 0.0;  // south coupling of row tile NT's row r into pivot row r
@@ -183,14 +186,9 @@ __device__ bool blk_factor_fwd(int n, const Src& src, double* Xs, double* Ts, do
     auto panel = [&](const int p, BlkRowData& ent) {
         const int k0 = 8 * p;
         // ---- G = S11^-1 by Gauss-Jordan (SPD: no pivoting); each lane owns
-        // entries (r, c0), (r, c0+1) and publishes them every step
+        // entries (r, c0), (r, c0+1) and publishes them every step but the last
         double g0 = w[0][0].v[0], g1 = w[0][0].v[1];
         *reinterpret_cast<double2*>(sg0 + blk_sw(r, c0)) = make_double2(g0, g1);
-        // the S21 tiles go to shared memory at the same time (read back in
-        // the DMMA operand layout below)
-#pragma unroll
-        for (int I = 1; I < NT; ++I)
-            *reinterpret_cast<double2*>(sS + (I - 1) * 64 + blk_sw(r, c0)) = make_double2(w[I][0].v[0], w[I][0].v[1]);
         if (q == 0) {
             sy[r] = yw[0];
             ss[r] = s_row;
@@ -224,49 +222,35 @@ __device__ bool blk_factor_fwd(int n, const Src& src, double* Xs, double* Ts, do
                 g0 = al0;
                 g1 = al1;
             }
-            *reinterpret_cast<double2*>(dst + blk_sw(r, c0)) = make_double2(g0, g1);
-            __syncwarp();
+            if (m < 3) {
+                *reinterpret_cast<double2*>(dst + blk_sw(r, c0)) = make_double2(g0, g1);
+                __syncwarp();
+            }
         }
-        const double* sg = sg0;  // 4 steps: the inverse is in buffer 0
-        // ---- operands in DMMA layout: G as A (G[r][q], G[r][q+4]), G Pi as B
-        // (G[q][pi(r)], G[q+4][pi(r)]), S21 tiles 1..NT-1 as A
-        const double ga0 = sg[blk_sw(r, q)], ga1 = sg[blk_sw(r, q + 4)];
-        const double gb0 = sg[blk_sw(q, pr)], gb1 = sg[blk_sw(q + 4, pr)];
-        double sa[NT - 1][2];
-#pragma unroll
-        for (int I = 1; I < NT; ++I) {
-            sa[I - 1][0] = sS[(I - 1) * 64 + blk_sw(r, q)];
-            sa[I - 1][1] = sS[(I - 1) * 64 + blk_sw(r, q + 4)];
-        }
-        const double yq0 = sy[q], yq1 = sy[q + 4];
+        // G[r][c0], G[r][c1] are in g0, g1: G's accumulator fragment
+        const double2 yq = *reinterpret_cast<const double2*>(sy + c0);  // y1 of rows c0, c0+1
         const double2 sc = *reinterpret_cast<const double2*>(ss + c0);  // s of rows c0, c0+1
-        // ---- X = S21 G, in A layout (lane: X[r][q], X[r][q+4])
+        // ---- X = S21 G (lane: X[r][c0], X[r][c1]); X_NT = diag(s) G
         BlkTile x[NT + 1];
 #pragma unroll
         for (int I = 1; I < NT; ++I) {
             x[I].v[0] = x[I].v[1] = 0.0;
-            blk_dmma(x[I].v[0], x[I].v[1], sa[I - 1][0], gb0);
-            blk_dmma(x[I].v[0], x[I].v[1], sa[I - 1][1], gb1);
+            blk_dmma(x[I].v[0], x[I].v[1], w[I][0].v[0], g0);
+            blk_dmma(x[I].v[0], x[I].v[1], w[I][0].v[1], g1);
         }
-        x[NT].v[0] = s_row * ga0;
-        x[NT].v[1] = s_row * ga1;
-        // stored for the backward sweep: tiles 1..NT, fragment order (coalesced)
+        x[NT].v[0] = s_row * g0;
+        x[NT].v[1] = s_row * g1;
+        // stored for the backward sweep: tiles 1..NT, row-major (coalesced)
         double* xs = Xs + (size_t)p * NT * 64;
 #pragma unroll
         for (int I = 1; I <= NT; ++I)
             *reinterpret_cast<double2*>(xs + (I - 1) * 64 + 2 * lane) = make_double2(x[I].v[0], x[I].v[1]);
-        // X^T for row tile NT's update
-#pragma unroll
-        for (int J = 1; J < NT; ++J) {
-            sT[(J - 1) * 64 + blk_sw(q, r)] = x[J].v[0];
-            sT[(J - 1) * 64 + blk_sw(q + 4, r)] = x[J].v[1];
-        }
         // ---- forward substitution: t1 = G y1 and y_I -= X_I y1 as quad dot
-        // products (lane: columns q and q+4)
-        double t1 = fma(ga0, yq0, ga1 * yq1);
+        // products (lane: columns c0 and c1)
+        double t1 = fma(g0, yq.x, g1 * yq.y);
         double py[NT];
 #pragma unroll
-        for (int I = 1; I < NT; ++I) py[I] = fma(x[I].v[0], yq0, x[I].v[1] * yq1);
+        for (int I = 1; I < NT; ++I) py[I] = fma(x[I].v[0], yq.x, x[I].v[1] * yq.y);
 #pragma unroll
         for (int o = 1; o < 4; o <<= 1) {
             t1 += __shfl_xor_sync(0xffffffffu, t1, o);
@@ -277,26 +261,35 @@ __device__ bool blk_factor_fwd(int n, const Src& src, double* Xs, double* Ts, do
         yw[NT] -= s_row * t1;  // X_NT y1 = diag(s) G y1
 #pragma unroll
         for (int I = 1; I < NT; ++I) yw[I] -= py[I];
-        // ---- trailing update S22 -= X S21^T on DMMA (row tiles 1..NT-1)
+        // ---- trailing update S22[I][J] -= X_I S21_J^T on DMMA (row tiles
+        // 1..NT, column tiles 1..min(I, NT-1): S21_NT only meets itself)
 #pragma unroll
-        for (int I = 1; I < NT; ++I) {
+        for (int I = 1; I <= NT; ++I) {
             const double xa0 = -x[I].v[0], xa1 = -x[I].v[1];
 #pragma unroll
-            for (int J = 1; J <= I; ++J) {
-                blk_dmma(w[I][J].v[0], w[I][J].v[1], xa0, sa[J - 1][0]);
-                blk_dmma(w[I][J].v[0], w[I][J].v[1], xa1, sa[J - 1][1]);
+            for (int J = 1; J <= I && J < NT; ++J) {
+                if (!NTD && I == NT) continue;
+                blk_dmma(w[I][J].v[0], w[I][J].v[1], xa0, w[J][0].v[0]);
+                blk_dmma(w[I][J].v[0], w[I][J].v[1], xa1, w[J][0].v[1]);
             }
         }
-        __syncwarp();  // X^T visible
-        // row tile NT: -= diag(s) X_J^T (J < NT), -= diag(s) G diag(s)
+        if (!NTD) {
 #pragma unroll
-        for (int J = 1; J < NT; ++J) {
-            const double2 xt = *reinterpret_cast<const double2*>(sT + (J - 1) * 64 + blk_sw(r, c0));
-            w[NT][J].v[0] = fma(-s_row, xt.x, w[NT][J].v[0]);
-            w[NT][J].v[1] = fma(-s_row, xt.y, w[NT][J].v[1]);
+            for (int J = 1; J < NT; ++J) {
+                sT[(J - 1) * 64 + blk_sw(c0, r)] = x[J].v[0];
+                sT[(J - 1) * 64 + blk_sw(c1, r)] = x[J].v[1];
+            }
+            __syncwarp();
+#pragma unroll
+            for (int J = 1; J < NT; ++J) {
+                const double2 xt = *reinterpret_cast<const double2*>(sT + (J - 1) * 64 + blk_sw(r, c0));
+                w[NT][J].v[0] = fma(-s_row, xt.x, w[NT][J].v[0]);
+                w[NT][J].v[1] = fma(-s_row, xt.y, w[NT][J].v[1]);
+            }
         }
-        w[NT][NT].v[0] = fma(-(s_row * g0), sc.x, w[NT][NT].v[0]);
-        w[NT][NT].v[1] = fma(-(s_row * g1), sc.y, w[NT][NT].v[1]);
+        // S22[NT][NT] -= diag(s) G diag(s)
+        w[NT][NT].v[0] = fma(-x[NT].v[0], sc.x, w[NT][NT].v[0]);
+        w[NT][NT].v[1] = fma(-x[NT].v[1], sc.y, w[NT][NT].v[1]);
         // ---- shift the window by one row tile; row tile NT enters
 #pragma unroll
         for (int I = 0; I < NT; ++I)
@@ -318,8 +311,8 @@ __device__ bool blk_factor_fwd(int n, const Src& src, double* Xs, double* Ts, do
 }
 
 // Backward sweep x1 = t1 - X^T x2 from the stored panels; x (length n) out.
-// Lane (r, q) holds X[r][q], X[r][q+4] of each stored tile, so the column
-// sums over r give x1[q] and x1[q+4]. Returns this lane's partial sum of x
+// Lane (r, q) holds X[r][2q], X[r][2q+1] of each stored tile, so the column
+// sums over r give x1[2q] and x1[2q+1]. Returns this lane's partial sum of x
 // (lanes 0..3 hold all of it).
 template <int B>
 __device__ double blk_backward(int n, const double* Xs, const double* Ts, double* x) {
@@ -336,7 +329,7 @@ __device__ double blk_backward(int n, const double* Xs, const double* Ts, double
         const double* xs = Xs + (size_t)pp * NT * 64;
 #pragma unroll
         for (int I = 0; I < NT; ++I) xt[I] = *reinterpret_cast<const double2*>(xs + I * 64 + 2 * lane);
-        tt = make_double2(Ts[8 * pp + q], Ts[8 * pp + q + 4]);
+        tt = *reinterpret_cast<const double2*>(Ts + 8 * pp + 2 * q);
     };
     // four-panel-deep register ring of the stored panels (an HBM round trip
     // is several panels long); unrolled by four so slots are never moved
@@ -356,16 +349,16 @@ __device__ double blk_backward(int n, const double* Xs, const double* Ts, double
             a0 += __shfl_xor_sync(0xffffffffu, a0, o);
             a1 += __shfl_xor_sync(0xffffffffu, a1, o);
         }
-        const double x0 = tt.x - a0, x1 = tt.y - a1;  // x1[q], x1[q+4]
+        const double x0 = tt.x - a0, x1 = tt.y - a1;  // x1[2q], x1[2q+1]
         if (r == 0) {
-            x[8 * p + q] = x0;
-            x[8 * p + q + 4] = x1;
+            *reinterpret_cast<double2*>(x + 8 * p + 2 * q) = make_double2(x0, x1);
             sum += x0 + x1;
         }
-        const double v0 = __shfl_sync(0xffffffffu, x0, r & 3), v1 = __shfl_sync(0xffffffffu, x1, r & 3);
+        // row r of the pivot block is column r: lanes with q = r/2 hold it
+        const double v0 = __shfl_sync(0xffffffffu, x0, r >> 1), v1 = __shfl_sync(0xffffffffu, x1, r >> 1);
 #pragma unroll
         for (int i = NT - 1; i > 0; --i) xw[i] = xw[i - 1];
-        xw[0] = (r & 4) ? v1 : v0;
+        xw[0] = (r & 1) ? v1 : v0;
         fetch(p - DEPTH, xt, tt);
     };
     for (int p = np - 1; p >= 0; p -= DEPTH) {  // np = B^2/8 is a multiple of 8

@@ -1,8 +1,8 @@
 // Blocked banded LDL^T micro-benchmark (developer tool): band_blk.cuh's
-// blk_factor_fwd against the lookahead variant of band_blk_la.cuh on random
+// blk_factor_fwd (3 and 4 blocks per SM) and blk_backward on random
 // 5-point SPD systems, one warp per system, the product kernel's launch shape
 // (4 warps per block). Checks the solution's residual on the host, that the
-// two variants' panels are bit-identical, and times the factor kernels.
+// two builds' panels are bit-identical, and times the factor kernels.
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo -o tools/blk_bench tools/blk_bench.cu
 #include <cmath>
 #include <cstdio>
@@ -10,7 +10,7 @@
 #include <random>
 #include <vector>
 
-#include "band_blk_la.cuh"
+#include "../paper_2103_11050_b200/csrc/band_blk.cuh"
 
 using namespace mpm2p;
 constexpr int WPBK = 4;
@@ -26,10 +26,7 @@ __global__ void __launch_bounds__(WPBK * 32, MINB) k_factor(int nsub, int n, con
     const size_t so = (size_t)s * n;
     const BlkBandSrc src{BandRows{BD + so, BW + so, BS + so}, Y + so, n};
     bool ok;
-    if (V == 0)
-        ok = blk_factor_fwd<B>(n, src, Xs + so * B, Ts + so, sm[w]);
-    else
-        ok = blk_factor_fwd_la<B>(n, src, Xs + so * B, Ts + so, sm[w]);
+    ok = blk_factor_fwd<B, BlkBandSrc, V == 0>(n, src, Xs + so * B, Ts + so, sm[w]);
     if (!ok && lane == 0) atomicAdd(bad, 1);
 }
 
@@ -119,11 +116,8 @@ int run(int nsub) {
     timeit([&] { k_factor<B, 0, 3><<<blocks, WPBK * 32>>>(nsub, n, dBD, dBW, dBS, dY, dXs[0], dTs[0], dbad); },
            "blk_factor_fwd (3 blk/SM)");
     timeit([&] { k_factor<B, 1, 3><<<blocks, WPBK * 32>>>(nsub, n, dBD, dBW, dBS, dY, dXs[1], dTs[1], dbad); },
-           "blk_factor_fwd_la (3 blk/SM)");
-    timeit([&] { k_factor<B, 1, 4><<<blocks, WPBK * 32>>>(nsub, n, dBD, dBW, dBS, dY, dXs[1], dTs[1], dbad); },
-           "blk_factor_fwd_la (4 blk/SM)");
-    // final state of dXs[1] / dTs[1]: the 4 blk/SM build; re-run the 3 blk/SM one for the comparison
-    k_factor<B, 1, 3><<<blocks, WPBK * 32>>>(nsub, n, dBD, dBW, dBS, dY, dXs[1], dTs[1], dbad);
+           "blk_factor_fwd !NTD (3 blk/SM)");
+    timeit([&] { k_back<B><<<blocks, WPBK * 32>>>(nsub, n, dXs[1], dTs[1], dX); }, "blk_backward");
     CK(cudaDeviceSynchronize());
     int bad;
     CK(cudaMemcpy(&bad, dbad, 4, cudaMemcpyDeviceToHost));

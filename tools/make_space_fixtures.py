@@ -38,7 +38,7 @@ def make(name):
     from oracle_bind import oracle_lib
     prob, split, s0, full, banded = build_case(name)
     if os.environ.get("EXTENDED") == "1":
-        return make_extended(name, prob, split, s0, banded)
+        return make_extended(name, prob, split, s0, full, banded)
     lib = oracle_lib()
     lib.dll.oracle_set_threads(int(os.environ.get("ORACLE_THREADS", os.cpu_count() or 1)))
     lib.dll.oracle_set_interface_solver(2 if banded else 0)
@@ -57,13 +57,13 @@ def make(name):
           f"oracle {el:.1f} s -> {path} ({os.path.getsize(path) / 1e6:.2f} MB)", flush=True)
 
 
-def make_extended(name, prob, split, s0, banded):
+def make_extended(name, prob, split, s0, full, banded):
     """The same run in extended precision (liboracle_ld.so, long double), added
-    to space_<name>.npz as ld_s / ld_p / ld_u: the exact-answer yardstick where
+    to space_<name>.npz as ld_s / ld_p / ld_u (C5 cases: the ld_-prefixed sketch,
+    subsample and non-zero saturations): the exact-answer yardstick where
     the double-precision oracle's own roundoff exceeds the 1e-8 bar (the C3 /
     C5 rule of tests/test_gpu_full_runs.py::check_fields_vs_truth)."""
     from oracle_bind import oracle_lib
-    from make_fixtures import round_mantissa
     path = os.path.join(GOLDEN, f"space_{name}.npz")
     out = dict(np.load(path))
     lib = oracle_lib(True)
@@ -75,9 +75,7 @@ def make_extended(name, prob, split, s0, banded):
     el = time.perf_counter() - t0
     sim.close()
     assert np.array_equal(np.array([s["rebuilt"] for s in x.record.steps], np.int8), out["rebuilt"])
-    out["ld_s"] = round_mantissa(x.s_final)
-    out["ld_p"] = round_mantissa(x.p_final)
-    out["ld_u"] = round_mantissa(x.u_final)
+    out.update(field_arrays(x, prefix="ld_", full=full))
     out["ld_seconds"] = np.array([el])
     np.savez_compressed(path, **out)
     print(f"{name} long double: {el:.0f} s -> {path}", flush=True)
