@@ -505,43 +505,67 @@ __global__ void k_recon_traces(Layout L, const double* __restrict__ coef, const 
 
 // MPM-2P recombination, one warp per subdomain: boundary traces
 // RU = PU + sum_h c_h HU_h + WU (k_recon_traces) and the pressure sum
-// RS = PS + sum_h c_h HP_h + pmsum (k_recon_psum), same operation order. The
-// coefficients c_h of the subdomain's homogeneous functions are warp-uniform.
-__global__ void k_recon_mpm(Layout L, const double* __restrict__ coef, const double* __restrict__ PU,
-                            const double* __restrict__ HU, const double* __restrict__ WU, double* __restrict__ RU,
-                            const double* __restrict__ PS, const double* __restrict__ HP,
-                            const double* __restrict__ pmsum, double* __restrict__ RS) {
+// RS = PS + sum_h c_h HP_h + pmsum (k_recon_psum), same operation order. Lane
+// h looks up the coefficient of homogeneous function h (one round trip for
+// all of them) and the warp shares them by shuffle; each lane then issues
+// every HU load of its edges before the sums (terms with c_h = 0 are skipped,
+// as in k_recon_traces).
+__global__ void __launch_bounds__(128) k_recon_mpm(Layout L, const double* __restrict__ coef,
+                                                   const double* __restrict__ PU, const double* __restrict__ HU,
+                                                   const double* __restrict__ WU, double* __restrict__ RU,
+                                                   const double* __restrict__ PS, const double* __restrict__ HP,
+                                                   const double* __restrict__ pmsum, double* __restrict__ RS) {
     pdl_begin();
     constexpr int MAXH = 16;
     const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (s >= L.n_sub) return;
     const int nh = L.n_hom(s);
+    double cl = 0.0, hp = 0.0;
+    if (lane < nh) {
+        int k, t, col;
+        bool fl;
+        L.hom(s, lane, k, t, fl, col);
+        cl = coef[col];
+        hp = HP[(size_t)s * L.max_hom + lane];
+    }
     double ch[MAXH];
 #pragma unroll
-    for (int h = 0; h < MAXH; ++h) {
-        double cv = 0.0;
-        if (h < nh) {
-            int k, t, col;
-            bool fl;
-            L.hom(s, h, k, t, fl, col);
-            cv = coef[col];
-        }
-        ch[h] = cv;
-    }
-    for (int idx = lane; idx < L.nbe; idx += 32) {
-        const size_t x = (size_t)s * L.nbe + idx;
-        double u = PU[x];
+    for (int h = 0; h < MAXH; ++h) ch[h] = __shfl_sync(0xffffffffu, cl, h);
+    const double* hu = HU + (size_t)s * L.max_hom * L.nbe;
+    for (int i0 = 0; i0 < L.nbe; i0 += 64) {  // two edges per lane and pass
+        const int ia = i0 + lane, ib = i0 + 32 + lane;
+        const bool va = ia < L.nbe, vb = ib < L.nbe;
+        const int ja = va ? ia : 0, jb = vb ? ib : 0;
+        const size_t xa = (size_t)s * L.nbe + ja, xb = (size_t)s * L.nbe + jb;
+        double ha[MAXH], hb[MAXH];
 #pragma unroll
-        for (int h = 0; h < MAXH; ++h)
-            if (h < nh && ch[h] != 0.0) u += ch[h] * HU[((size_t)s * L.max_hom + h) * L.nbe + idx];
-        if (WU) u += WU[x];
-        RU[x] = u;
+        for (int h = 0; h < MAXH; ++h) {
+            ha[h] = h < nh ? hu[(size_t)h * L.nbe + ja] : 0.0;  // nh is warp-uniform
+            hb[h] = h < nh ? hu[(size_t)h * L.nbe + jb] : 0.0;
+        }
+        double ua = PU[xa], ub = PU[xb];
+        const double wa = WU ? WU[xa] : 0.0, wb = WU ? WU[xb] : 0.0;
+#pragma unroll
+        for (int h = 0; h < MAXH; ++h) {
+            const bool on = h < nh && ch[h] != 0.0;
+            ua = on ? ua + ch[h] * ha[h] : ua;
+            ub = on ? ub + ch[h] * hb[h] : ub;
+        }
+        if (WU) {
+            ua += wa;
+            ub += wb;
+        }
+        if (va) RU[xa] = ua;
+        if (vb) RU[xb] = ub;
+    }
+    // pressure sum: lane 0 adds the terms in order
+    double v = PS[s];
+#pragma unroll
+    for (int h = 0; h < MAXH; ++h) {
+        const double hv = __shfl_sync(0xffffffffu, hp, h);
+        if (h < nh && ch[h] != 0.0) v += ch[h] * hv;
     }
     if (lane == 0) {
-        double v = PS[s];
-#pragma unroll
-        for (int h = 0; h < MAXH; ++h)
-            if (h < nh && ch[h] != 0.0) v += ch[h] * HP[(size_t)s * L.max_hom + h];
         if (pmsum) v += pmsum[s];
         RS[s] = v;
     }
@@ -1632,7 +1656,7 @@ __global__ void __launch_bounds__(256) k_mpm_edges(Layout L, const double* __res
 // takes the edge's own w from k_mpm_edges (w is per subdomain). The
 // divergence and the right-hand side are unfused, as in the reference build;
 // the edge terms are added in W, E, S, N order (k_mpm_rhs's).
-__global__ void __launch_bounds__(256) k_mpm_rhs_w(Layout L, int max_rhs, int anchor,
+__global__ void __launch_bounds__(256, 4) k_mpm_rhs_w(Layout L, int max_rhs, int anchor,
                                                    const double* __restrict__ Tn, const double* __restrict__ q,
                                                    const double* __restrict__ pm, const double* __restrict__ WU,
                                                    const double* __restrict__ ET, double* __restrict__ X) {
@@ -2237,7 +2261,7 @@ void downscale(Ctx& c, const double* kappa, bool skel_given) {
                  (const int*)c.bc_kind.p, (const double*)c.skel.p, (const double*)c.corr.p, (const double*)c.RU.p,
                  (const double*)c.delta.p, c.grounded ? 1 : 0, c.GZ.p, c.ET.p);
         CK_LAUNCH();
-        launch_k(c, k_ds_rhs, grid2d(c, L), TPB, 0, L,
+        launch_k(c, k_ds_rhs, grid2d(c, L, red_blocks(c, k_ds_rhs, L.cells())), TPB, 0, L,
                  kappa_checked ? nullptr : kappa, (const double*)c.q.p, (const double*)c.ET.p, c.Xd.p, c.sc.p);
         CK_LAUNCH();
     } else {
@@ -2592,7 +2616,7 @@ void launch_mpm(Ctx& c, const double* kn) {  // mpm_pressure_update (mpm.cpp:31-
             launch_k(c, k_mpm_edges, std::min(grid_for((long long)L.n_sub * L.nbe), 8 * c.num_sms), TPB, 0, L, kn,
                      c.kappa_m, c.bc_kind, c.bc_value, c.beta_m, c.beta_p, c.pm, c.bpm, c.GZ, c.WU, c.ET);
             CK_LAUNCH();
-            launch_k(c, k_mpm_rhs_w, grid2d(c, L), TPB, 0, L, c.max_rhs,
+            launch_k(c, k_mpm_rhs_w, grid2d(c, L, red_blocks(c, k_mpm_rhs_w, L.cells())), TPB, 0, L, c.max_rhs,
                      c.anchor_m ? 1 : 0, c.T, c.q, c.pm, c.WU, c.ET, c.X);
         }
         else if (c.rhs_sub && L.ncs <= RHS_TPB * RHS_CPT)
@@ -2623,7 +2647,7 @@ void launch_mpm(Ctx& c, const double* kn) {  // mpm_pressure_update (mpm.cpp:31-
     if (c.dim == 0) CK(cudaMemsetAsync(c.icoef, 0, sizeof(double), c.st));
     if (L.max_hom <= 16) {
         PROF(c, "k_recon_mpm");
-        launch_k(c, k_recon_mpm, cdiv((long long)L.n_sub * 32, TPB), TPB, 0, L, c.icoef, c.PU, c.HU, c.WU, c.RU, c.PS,
+        launch_k(c, k_recon_mpm, cdiv((long long)L.n_sub * 32, 128), 128, 0, L, c.icoef, c.PU, c.HU, c.WU, c.RU, c.PS,
                                                                           c.HP, c.pmsum, c.RS);
         CK_LAUNCH();
     } else {  // per-edge interface spaces: more homogeneous functions than k_recon_mpm keeps in registers
