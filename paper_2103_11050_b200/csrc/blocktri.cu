@@ -248,7 +248,10 @@ __global__ void __launch_bounds__(256) k_cr_gemv(const GemvJob* __restrict__ job
         double t[RPW];
 #pragma unroll
         for (int q = 0; q < RPW; ++q) t[q] = 0.0;
-        for (int c = lane; c < S; c += 64) {  // S is a multiple of 64
+        // S is a multiple of 64; several column slabs in flight per round
+        // trip (the narrow levels are a handful of dependent round trips)
+#pragma unroll(RPW == 1 ? 8 : 2)
+        for (int c = lane; c < S; c += 64) {
             double m[RPW][2];
 #pragma unroll
             for (int q = 0; q < RPW; ++q) {

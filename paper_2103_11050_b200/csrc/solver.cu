@@ -13,6 +13,7 @@
 // One warp owns one subdomain in the banded kernels (band.cuh); everything
 // else is one thread per cell / face / edge / matrix entry. No floating-point
 // atomics: every sum has a fixed order, so runs are bitwise reproducible.
+#include <cooperative_groups.h>
 #include <cub/device/device_radix_sort.cuh>
 
 #include "band.cuh"
@@ -1871,12 +1872,9 @@ __global__ void k_part_psum(Layout L, int max_rhs, const double* __restrict__ X,
 // factors), optionally divided by (ly_i + lx_j).
 // 32 x 32 output tile per 256-thread block, k in slabs of 32 staged in
 // shared memory (all of a slab's loads issued together), 4 outputs per thread
-__global__ void __launch_bounds__(256) k_sep_gemm(int m, int n, int kk, const double* __restrict__ A, int ta,
-                                                  const double* __restrict__ Bm, int tb, double* __restrict__ C,
-                                                  const double* __restrict__ lx, const double* __restrict__ ly) {
-    pdl_begin();
-    __shared__ double As[32][33], Bs[32][33];
-    const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+__device__ __forceinline__ void sep_gemm_tile(int m, int n, int kk, const double* A, int ta, const double* Bm, int tb,
+                                              double* C, const double* lx, const double* ly, int i0, int j0,
+                                              double (*As)[33], double (*Bs)[33]) {
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // output column tx, rows ty + 8 q
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     for (int k0 = 0; k0 < kk; k0 += 32) {
@@ -1902,6 +1900,32 @@ __global__ void __launch_bounds__(256) k_sep_gemm(int m, int n, int kk, const do
         const int i = i0 + ty + 8 * q, j = j0 + tx;
         if (i < m && j < n) C[(size_t)i * n + j] = lx ? acc[q] / (ly[i] + lx[j]) : acc[q];
     }
+}
+__global__ void __launch_bounds__(256) k_sep_gemm(int m, int n, int kk, const double* __restrict__ A, int ta,
+                                                  const double* __restrict__ Bm, int tb, double* __restrict__ C,
+                                                  const double* __restrict__ lx, const double* __restrict__ ly) {
+    pdl_begin();
+    __shared__ double As[32][33], Bs[32][33];
+    sep_gemm_tile(m, n, kk, A, ta, Bm, tb, C, lx, ly, blockIdx.y * 32, blockIdx.x * 32, As, Bs);
+}
+// The four products of the separable solve in one cooperative launch (every
+// product has the ny x nx output, so a block keeps its tile; grid barriers
+// between the products): delta = Qy [(Qy^T (R Qx)) ./ (ly + lx)] Qx^T. The
+// intermediates are read with plain loads (written by other blocks of this
+// launch), the arithmetic and its order are k_sep_gemm's.
+__global__ void __launch_bounds__(256) k_sep_solve(int nx, int ny, const double* R, const double* Qx, const double* Qy,
+                                                   const double* lx, const double* ly, double* z1, double* z2,
+                                                   double* delta) {
+    __shared__ double As[32][33], Bs[32][33];
+    cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+    const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+    sep_gemm_tile(ny, nx, nx, R, 0, Qx, 0, z1, nullptr, nullptr, i0, j0, As, Bs);
+    grid.sync();
+    sep_gemm_tile(ny, nx, ny, Qy, 1, z1, 0, z2, lx, ly, i0, j0, As, Bs);
+    grid.sync();
+    sep_gemm_tile(ny, nx, ny, Qy, 0, z2, 0, z1, nullptr, nullptr, i0, j0, As, Bs);
+    grid.sync();
+    sep_gemm_tile(ny, nx, nx, z1, 0, Qx, 1, delta, nullptr, nullptr, i0, j0, As, Bs);
 }
 
 __global__ void k_static(Layout L, const double* __restrict__ q, const int* __restrict__ bc_kind,
@@ -2213,25 +2237,34 @@ void downscale(Ctx& c, const double* kappa, bool skel_given) {
         const dim3 g(cdiv(nx, 32), cdiv(ny, 32));
         const double* lx = c.sep_lam.p;
         const double* ly = c.sep_lam.p + nx;
-        {
-            PROF(c, "k_sep_gemm");
-            launch_k(c, k_sep_gemm, g, TPB, 0, ny, nx, nx, c.resid.p, 0, c.sep_qx.p, 0, c.sep_z1.p, nullptr, nullptr);
-            CK_LAUNCH();
-        }
-        {
-            PROF(c, "k_sep_gemm");
-            launch_k(c, k_sep_gemm, g, TPB, 0, ny, nx, ny, c.sep_qy.p, 1, c.sep_z1.p, 0, c.sep_z2.p, lx, ly);
-            CK_LAUNCH();
-        }
-        {
-            PROF(c, "k_sep_gemm");
-            launch_k(c, k_sep_gemm, g, TPB, 0, ny, nx, ny, c.sep_qy.p, 0, c.sep_z2.p, 0, c.sep_z1.p, nullptr, nullptr);
-            CK_LAUNCH();
-        }
-        {
-            PROF(c, "k_sep_gemm");
-            launch_k(c, k_sep_gemm, g, TPB, 0, ny, nx, nx, c.sep_z1.p, 0, c.sep_qx.p, 1, c.delta.p, nullptr, nullptr);
-            CK_LAUNCH();
+        if ((int)(g.x * g.y) <= red_blocks(c, k_sep_solve, 1LL << 30)) {  // co-resident: one cooperative launch
+            PROF(c, "k_sep_solve");
+            int nxa = nx, nya = ny;
+            const double *R = c.resid.p, *qx = c.sep_qx.p, *qy = c.sep_qy.p;
+            double *z1 = c.sep_z1.p, *z2 = c.sep_z2.p, *dl = c.delta.p;
+            void* args[] = {&nxa, &nya, &R, &qx, &qy, &lx, &ly, &z1, &z2, &dl};
+            CK(cudaLaunchCooperativeKernel((void*)k_sep_solve, g, dim3(TPB), args, 0, c.st));
+        } else {
+            {
+                PROF(c, "k_sep_gemm");
+                launch_k(c, k_sep_gemm, g, TPB, 0, ny, nx, nx, c.resid.p, 0, c.sep_qx.p, 0, c.sep_z1.p, nullptr, nullptr);
+                CK_LAUNCH();
+            }
+            {
+                PROF(c, "k_sep_gemm");
+                launch_k(c, k_sep_gemm, g, TPB, 0, ny, nx, ny, c.sep_qy.p, 1, c.sep_z1.p, 0, c.sep_z2.p, lx, ly);
+                CK_LAUNCH();
+            }
+            {
+                PROF(c, "k_sep_gemm");
+                launch_k(c, k_sep_gemm, g, TPB, 0, ny, nx, ny, c.sep_qy.p, 0, c.sep_z2.p, 0, c.sep_z1.p, nullptr, nullptr);
+                CK_LAUNCH();
+            }
+            {
+                PROF(c, "k_sep_gemm");
+                launch_k(c, k_sep_gemm, g, TPB, 0, ny, nx, nx, c.sep_z1.p, 0, c.sep_qx.p, 1, c.delta.p, nullptr, nullptr);
+                CK_LAUNCH();
+            }
         }
         PROF(c, "k_repair_corr");
         launch_k(c, k_repair_corr, std::min(grid_for(std::max(L.n_iface, L.n_sub)), 2 * c.num_sms), TPB, 0, L, 1,
