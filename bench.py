@@ -147,8 +147,11 @@ def kernel_work(name, cfg, sz, dim):
         "k_ds_sweep": ("hbm", ns * n * (16.0 * B + 24.0)),       # split downscale: 2 sweeps with the stored factor
         "k_factor_solve": ("fp64", ns * (n * B * B + 4.0 * n * B * (1 + sz.nhat / max(ns, 1)))),
         "k_gemv": ("hbm", 8.0 * dim * dim),
-        # MPM-2P right-hand side: p^m, two faces of T(kappa_n), q read; X written (edge terms O(1/w))
-        "k_mpm_rhs": ("hbm", 40.0 * cells),
+        # MPM-2P right-hand side: p^m, two faces of T(kappa_n), q read; X written; per subdomain edge
+        # kappa_n, kappa_m, the face pressure read, WU / GZ / ET written, WU / ET read back: 64 B
+        "k_mpm_rhs": ("hbm", 40.0 * cells + 64.0 * ns * sz.sub_nx * 4),
+        # MPM-2P recombination: per subdomain edge PU, WU and the max_hom homogeneous traces read, RU written
+        "k_recon_mpm": ("hbm", 8.0 * ns * sz.sub_nx * 4 * (3.0 + sz.nhat / max(ns, 1))),
         # velocity scatter: X (downscaled potential), two faces of T, q read; two faces of u written
         "k_ds_u_div": ("hbm", 48.0 * cells),
         "k_ds_prep": ("hbm", 72.0 * cells),
@@ -158,6 +161,19 @@ def kernel_work(name, cfg, sz, dim):
         "k_divres": ("hbm", 24.0 * cells + 8.0 * faces),
         "k_trans": ("hbm", 16.0 * cells + 8.0 * faces),
     }
+    if name == "k_cr_gemv" and dim > 16384:
+        # interface solve by block cyclic reduction (blocktri.cu): nb block rows (one per subdomain
+        # row) padded to S; forward levels read D_o^-1, Lo_e, Up_e (3 blocks per eliminated block),
+        # the top solve one block, backward levels P_o, Q_o (2 per eliminated block); one solve is
+        # 15 launches at nb = 128, so the per-launch figure is the solve's bytes over its launches
+        nb = max(1, round(ns ** 0.5))  # subdomain rows (the configs' decompositions above dim 16,384 are square)
+        S = -(-(dim // nb) // 64) * 64
+        elim, lv, launches = 0, nb, 1
+        while lv > 1:
+            elim += lv // 2
+            lv -= lv // 2
+            launches += 2
+        return ("hbm", 8.0 * S * S * (5.0 * elim + 1.0) / launches)
     return table.get(name)
 
 

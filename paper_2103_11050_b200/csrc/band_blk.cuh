@@ -91,30 +91,33 @@ struct BlkBandSrc {
 };
 // the downscale operator straight from the global transmissibilities T of
 // kappa_n (pure Neumann, anchor cell 0; k_ds_prep's rules and summation
-// order, mrcm.cpp:391-411): no band rows are written or read back
+// order, mrcm.cpp:391-411): no band rows are written or read back. SNX (the
+// subdomain width, = the bandwidth) is a compile-time constant: the row's
+// local cell coordinates cost a shift or a multiply, not a division.
+template <int SNX>
 struct BlkTransSrc {
     const double* T;
     const double* y;
-    int n, snx, sny, nx, vcount, i0, j0;
+    int n, sny, nx, vcount, i0, j0;
     __device__ __forceinline__ BlkRowData fetch(int row) const {
         const int rr = row < n ? row : n - 1;
-        const int ii = rr % snx, jj = rr / snx, i = i0 + ii, j = j0 + jj;
+        const int jj = rr / SNX, ii = rr - jj * SNX, i = i0 + ii, j = j0 + jj;
         const int vf = j * (nx + 1) + i, hf = vcount + j * nx + i;
         return BlkRowData{T[vf], T[vf + 1], T[hf], T[hf + nx], y[rr]};  // W, E, S, N faces
     }
     __device__ __forceinline__ void decode(int row, const BlkRowData& e, double& d, double& w, double& w1,
                                            double& s) const {
         const int rr = row < n ? row : n - 1;
-        const int ii = rr % snx, jj = rr / snx;
+        const int jj = rr / SNX, ii = rr - jj * SNX;
         double diag = 0.0;
         if (ii > 0) diag += e.a0;
-        if (ii < snx - 1) diag += e.a1;
+        if (ii < SNX - 1) diag += e.a1;
         if (jj > 0) diag += e.a2;
         if (jj < sny - 1) diag += e.a3;
         d = rr == 0 ? 1.0 : diag;
         w = (ii > 0 && rr != 1) ? e.a0 : 0.0;
-        w1 = (ii + 1 < snx && rr != 0) ? e.a1 : 0.0;  // the next row's west coupling is this cell's east face
-        s = (jj > 0 && rr != snx) ? e.a2 : 0.0;
+        w1 = (ii + 1 < SNX && rr != 0) ? e.a1 : 0.0;  // the next row's west coupling is this cell's east face
+        s = (jj > 0 && rr != SNX) ? e.a2 : 0.0;
     }
 };
 
@@ -169,10 +172,10 @@ __device__ bool blk_factor_fwd(int n, const Src& src, double* Xs, double* Ts, do
         if (I >= 1) w[I][I - 1].v[1] = (r == 0 && q == 3) ? wv : 0.0;
         if (I == NT) s_row = in ? -es : 0.0;
     };
-    // positive and finite, on the bits (keeps the check off the fp64 pipe)
-    auto spd = [](double v) {
-        return (unsigned long long)(__double_as_longlong(v) - 1) < 0x7fefffffffffffffull;
-    };
+    // positive and finite, on the high word's bits (keeps the check off the
+    // fp64 pipe; a value whose high word is 0 — zero or a denormal below
+    // 2^-1042 — counts as not positive)
+    auto spd = [](double v) { return (unsigned)(__double2hiint(v) - 1) < 0x7fefffffu; };
     // initial window: row tiles 0..NT
 #pragma unroll
     for (int I = 0; I <= NT; ++I) place(I, 8 * I, src.fetch(8 * I + r));

@@ -949,7 +949,7 @@ __global__ void __launch_bounds__(WPB * 32, 3) k_ds_blk_factor(Layout L, const d
     const int n = L.ncs;
     const size_t so = (size_t)s * n;
     // the operator straight from T(kappa_n): k_ds_prep writes only the rhs
-    const BlkTransSrc src{T, Xd + so, n, L.snx, L.sny, L.nx, L.vcount(), L.sub_i0(s), L.sub_j0(s)};
+    const BlkTransSrc<B> src{T, Xd + so, n, L.sny, L.nx, L.vcount(), L.sub_i0(s), L.sub_j0(s)};
     const bool ok = blk_factor_fwd<B>(n, src, Xs + so * B, T1 + so, sm[w]);
     if (!ok && lane == 0) atomicOr(&sc->err, ERR_PIVOT);
 }
