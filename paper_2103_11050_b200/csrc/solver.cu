@@ -1348,6 +1348,44 @@ struct CflNext {
     int on = 0;
     double safety = 0.0, dt_cap = 0.0, inflow = 0.0, M = 1.0;
 };
+// Block and grid reduction of k_ds_u_div's six maxima and the scalars formed
+// from them (div_residual, div_scale, the next step's dt).
+__device__ __forceinline__ void udiv_finish(const Layout& L, double res, double vmax, double hmax, double qmax,
+                                            double dmax, double anyf, Scalars* sc, double* part, unsigned* counter,
+                                            const CflNext& cfl) {
+    constexpr int NP = 6;
+    const double vol = L.vol(), hx = L.hx, hy = L.hy;
+    __shared__ double shm[32 * NP];
+    __shared__ double red[NP];
+    double v[NP] = {res, vmax, hmax, qmax, dmax, anyf};
+    block_reduce_multi<NP>(v, 0u, shm, red);
+    if (threadIdx.x < NP) part[NP * (blockIdx.y * gridDim.x + blockIdx.x) + threadIdx.x] = red[threadIdx.x];
+    if (last_block_done(counter)) {
+        double a[NP];
+#pragma unroll
+        for (int k = 0; k < NP; ++k) a[k] = 0.0;
+        for (int b = threadIdx.x; b < (int)(gridDim.x * gridDim.y); b += blockDim.x) {
+#pragma unroll
+            for (int k = 0; k < NP; ++k) a[k] = fmax(a[k], __ldcg(part + (size_t)NP * b + k));
+        }
+        block_reduce_multi<NP>(a, 0u, shm, red);
+        if (threadIdx.x == 0) {
+            sc->div_residual = red[0];
+            // max(|q|, |u_f| area_f / vol) (mrcm.cpp:432-437)
+            const double scale = fmax(fmax(red[3], __ddiv_rn(__dmul_rn(red[1], hy), vol)),
+                                      __ddiv_rn(__dmul_rn(red[2], hx), vol));
+            sc->div_scale = scale > 0.0 ? scale : 1.0;
+            if (cfl.on) {  // cfl_timestep's epilogue (transport.cpp:55-70), for the next step
+                const bool af = red[5] > 0.0;
+                const double dt = af ? fmin(cfl.dt_cap / cfl.safety, __ddiv_rn(vol, red[4])) : 0.0;
+                sc->any_next = af;
+                sc->dt_next = af ? fmin(cfl.safety * dt, cfl.dt_cap) : cfl.dt_cap;
+            }
+            *counter = 0;
+        }
+    }
+}
+
 // Velocity scatter of the downscaled solution (mrcm.cpp:409-431) with the
 // divergence residual and scale (mrcm.cpp:429-437) and the next step's CFL
 // reduction (cfl_timestep, transport.cpp:51-71) in the same pass. One thread
@@ -1367,7 +1405,6 @@ __global__ void __launch_bounds__(256, 4) k_ds_u_div(Layout L, const double* __r
                                                   double* __restrict__ u, const double* __restrict__ q, Scalars* sc,
                                                   double* part, unsigned* counter, CflNext cfl) {
     pdl_begin();
-    constexpr int NP = 6;
     const int lane = threadIdx.x & 31;
     double res = 0.0, vmax = 0.0, hmax = 0.0, qmax = 0.0, dmax = 0.0, anyf = 0.0;
     const double vol = L.vol(), hx = L.hx, hy = L.hy;
@@ -1439,35 +1476,7 @@ __global__ void __launch_bounds__(256, 4) k_ds_u_div(Layout L, const double* __r
             }
         }
     }
-    __shared__ double shm[32 * NP];
-    __shared__ double red[NP];
-    double v[NP] = {res, vmax, hmax, qmax, dmax, anyf};
-    block_reduce_multi<NP>(v, 0u, shm, red);
-    if (threadIdx.x < NP) part[NP * (blockIdx.y * gridDim.x + blockIdx.x) + threadIdx.x] = red[threadIdx.x];
-    if (last_block_done(counter)) {
-        double a[NP];
-#pragma unroll
-        for (int k = 0; k < NP; ++k) a[k] = 0.0;
-        for (int b = threadIdx.x; b < (int)(gridDim.x * gridDim.y); b += blockDim.x) {
-#pragma unroll
-            for (int k = 0; k < NP; ++k) a[k] = fmax(a[k], __ldcg(part + (size_t)NP * b + k));
-        }
-        block_reduce_multi<NP>(a, 0u, shm, red);
-        if (threadIdx.x == 0) {
-            sc->div_residual = red[0];
-            // max(|q|, |u_f| area_f / vol) (mrcm.cpp:432-437)
-            const double scale = fmax(fmax(red[3], __ddiv_rn(__dmul_rn(red[1], hy), vol)),
-                                      __ddiv_rn(__dmul_rn(red[2], hx), vol));
-            sc->div_scale = scale > 0.0 ? scale : 1.0;
-            if (cfl.on) {  // cfl_timestep's epilogue (transport.cpp:55-70), for the next step
-                const bool af = red[5] > 0.0;
-                const double dt = af ? fmin(cfl.dt_cap / cfl.safety, __ddiv_rn(vol, red[4])) : 0.0;
-                sc->any_next = af;
-                sc->dt_next = af ? fmin(cfl.safety * dt, cfl.dt_cap) : cfl.dt_cap;
-            }
-            *counter = 0;
-        }
-    }
+    udiv_finish(L, res, vmax, hmax, qmax, dmax, anyf, sc, part, counter, cfl);
 }
 
 // The boundary-face half of the downscale epilogue, over the 2(nx + ny)
