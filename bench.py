@@ -148,8 +148,8 @@ def kernel_work(name, cfg, sz, dim):
         "k_factor_solve": ("fp64", ns * (n * B * B + 4.0 * n * B * (1 + sz.nhat / max(ns, 1)))),
         "k_gemv": ("hbm", 8.0 * dim * dim),
         # MPM-2P right-hand side: p^m, two faces of T(kappa_n), q read; X written; per subdomain edge
-        # kappa_n, kappa_m, the face pressure read, WU / GZ / ET written, WU / ET read back: 64 B
-        "k_mpm_rhs": ("hbm", 40.0 * cells + 64.0 * ns * sz.sub_nx * 4),
+        # kappa_n and the static pressure drop read, WU written, WU / ET read back: 40 B
+        "k_mpm_rhs": ("hbm", 40.0 * cells + 40.0 * ns * sz.sub_nx * 4),
         # MPM-2P recombination: per subdomain edge PU, WU and the max_hom homogeneous traces read, RU written
         "k_recon_mpm": ("hbm", 8.0 * ns * sz.sub_nx * 4 * (3.0 + sz.nhat / max(ns, 1))),
         # velocity scatter: X (downscaled potential), two faces of T, q read; two faces of u written

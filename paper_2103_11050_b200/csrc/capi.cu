@@ -469,6 +469,9 @@ void create_ctx(mpm2p_ctx* ctx, const mpm2p_problem* P) {
     c.GZ.alloc(ns * nbe);
     c.WU.alloc(ns * nbe);
     c.ET.alloc(ns * nbe);
+    c.MGZ.alloc(ns * nbe);
+    c.MET.alloc(ns * nbe);
+    c.PD.alloc(ns * nbe);
     c.RU.alloc(ns * nbe);
     c.RS.alloc(ns);
     c.skel.alloc(skel);
@@ -1241,6 +1244,7 @@ int mpm2p_compute_basis_set(mpm2p_ctx* ctx, const double* kappa, const double* b
         launch_basis_core(c, c.kappa_n);
         sync_scalars(c);
         c.has_basis = true;
+        c.mpm_static_ok = false;  // p^m of this basis is not known here: the MPM-2P edge data are formed per call
         if (counters) fill_counters(c, counters);
     });
 }

@@ -121,6 +121,10 @@ struct Ctx {
     DevBuf<double> hg_x, hg_y, hg_z, hg_xi, hg_state;  // rcond estimate (bt_rcond)
     // per-solve scratch
     DevBuf<double> X, PU, PB, PS, GZ, WU, ET, RU, RS, skel, resid, delta, corr;
+    // MPM-2P edge data owned by the MPM path (GZ / ET are the downscale's scratch): g' / z', the edge's rhs term,
+    // and the static pressure drop p^m - p^m_face of the last rebuild
+    DevBuf<double> MGZ, MET, PD;
+    bool mpm_static_ok = false;  // MGZ / MET / PD hold the last rebuild's static entries (launch_rebuild)
     // downscale
     DevBuf<double> BDd, BWd, BSd, Dd, Lrd, Xd;
     // split downscale (latency regime): the kappa_n operator is factored on a

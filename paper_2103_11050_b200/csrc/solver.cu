@@ -1629,14 +1629,17 @@ __global__ void __launch_bounds__(256) k_mpm_edges(Layout L, const double* __res
                                                    const double* __restrict__ bc_value, const double* __restrict__ bm,
                                                    const double* __restrict__ bp, const double* __restrict__ pm,
                                                    const double* __restrict__ bpm, double* __restrict__ GZ,
-                                                   double* __restrict__ WU, double* __restrict__ ET) {
+                                                   double* __restrict__ WU, double* __restrict__ ET,
+                                                   double* __restrict__ PD) {
     pdl_begin();
     const int ne = L.n_sub * L.nbe;
     for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < ne; x += gridDim.x * blockDim.x) {
         const int s = x / L.nbe, idx = x % L.nbe;
         const EdgeInfo e = L.edge(s, idx);
         const double kc = kn[e.global_cell], kmc = km[e.global_cell], pc = pm[e.global_cell], bpv = bpm[x];
-        const double wun = half_trans(L, e.side, kc) * (pc - bpv) / e.area;
+        const double pd = __dsub_rn(pc, bpv);
+        if (PD) PD[x] = pd;
+        const double wun = half_trans(L, e.side, kc) * pd / e.area;
         const double th = half_trans(L, e.side, kmc);
         WU[x] = wun;
         double term;
@@ -1657,6 +1660,35 @@ __global__ void __launch_bounds__(256) k_mpm_edges(Layout L, const double* __res
             term = -__dmul_rn(z, e.area);
         }
         ET[x] = term;
+    }
+}
+
+// Between rebuilds only kappa_n changes: p^m, the face pressures and the
+// cached operator are those of the last rebuild, so an edge's pressure drop
+// PD = p^m - p^m_face and the g' / right-hand-side terms of interface,
+// pressure and Robin edges are static (written by k_mpm_edges at the rebuild
+// into arrays the MPM-2P path owns). Per step: w from kappa_n and PD (the
+// same product and quotient as k_mpm_edges), and the z' / term of flux faces.
+__global__ void __launch_bounds__(256) k_mpm_edges_kn(Layout L, const double* __restrict__ kn,
+                                                      const int* __restrict__ bc_kind,
+                                                      const double* __restrict__ bc_value,
+                                                      const double* __restrict__ PD, double* __restrict__ GZ,
+                                                      double* __restrict__ WU, double* __restrict__ ET) {
+    pdl_begin();
+    const int ne = L.n_sub * L.nbe;
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < ne; x += gridDim.x * blockDim.x) {
+        const int s = x / L.nbe, idx = x % L.nbe;
+        const EdgeInfo e = L.edge(s, idx);
+        const double wun = half_trans(L, e.side, kn[e.global_cell]) * PD[x] / e.area;
+        WU[x] = wun;
+        if (e.iface < 0) {
+            const int kind = bc_kind[e.gbc];
+            if (kind != BC_PRESSURE && kind != BC_ROBIN) {
+                const double z = __dsub_rn(bc_value[e.gbc], wun);
+                GZ[x] = z;
+                ET[x] = -__dmul_rn(z, e.area);
+            }
+        }
     }
 }
 
@@ -2469,6 +2501,13 @@ void launch_rebuild(Ctx& c, const double* kappa, bool compute_beta) {  // comput
         CK_LAUNCH();
     }
     CK(cudaMemcpyAsync(c.RS, c.pmsum, L.n_sub * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
+    if (c.rhs_w) {  // the MPM-2P edge data that stay fixed until the next rebuild (k_mpm_edges_kn)
+        PROF(c, "k_mpm_rhs");
+        launch_k(c, k_mpm_edges, std::min(grid_for((long long)L.n_sub * L.nbe), 8 * c.num_sms), TPB, 0, L, kappa,
+                 c.kappa_m, c.bc_kind, c.bc_value, c.beta_m, c.beta_p, c.pm, c.bpm, c.MGZ, c.WU, c.MET, c.PD.p);
+        CK_LAUNCH();
+        c.mpm_static_ok = true;
+    }
     downscale(c, kappa);
     c.has_basis = true;
 }
@@ -2481,6 +2520,7 @@ void launch_rebuild(Ctx& c, const double* kappa, bool compute_beta) {  // comput
 // X[s][1..]; kappa_m = kappa.
 void launch_basis_core(Ctx& c, const double* kappa) {
     const Layout& L = c.L;
+    c.mpm_static_ok = false;  // kappa_m changes: launch_rebuild re-forms the static MPM-2P edge data
     {
         PROF(c, "k_band_entries");
         launch_k(c, k_band_entries, grid_for(L.cells()), TPB, 0, L, kappa, c.T, 0, c.anchor_m ? 1 : 0, c.beta_m, c.beta_p,
@@ -2618,7 +2658,7 @@ bool particular_solve_x(Ctx& c) {
     case BW_:                                                                                                   \
         launch_k(c, k_part_solve_t<BW_>, L.n_sub, twist_threads<BW_>(), twist_smem_bytes<BW_>(),                  \
             L, c.max_rhs, c.Dm, c.Lcm, c.Lrm, c.tw_midb, c.tw_sinv, c.X, c.kappa_m, c.bc_kind, c.beta_m,        \
-            c.beta_p, c.GZ, c.PU, c.PS);                                                                        \
+            c.beta_p, c.MGZ, c.PU, c.PS);                                                                        \
         break;
             MPM2P_TWIST_WIDTHS(X)
 #undef X
@@ -2634,7 +2674,7 @@ bool particular_solve_x(Ctx& c) {
     case BW_:                                                                                                   \
         launch_k(c, k_part_solve_r<BW_>, band_blocks(L), WPB * 32, 0, L, c.max_rhs, c.Dm, c.Lcm, c.Lrm, c.X,     \
                                                                    c.kappa_m, c.bc_kind, c.beta_m, c.beta_p,   \
-                                                                   c.GZ, c.PU, c.PS);                          \
+                                                                   c.MGZ, c.PU, c.PS);                          \
         fused_traces = true;                                                                                    \
         break;
             MPM2P_BAND_WIDTHS(X)
@@ -2655,19 +2695,24 @@ void launch_mpm(Ctx& c, const double* kn) {  // mpm_pressure_update (mpm.cpp:31-
     {
         PROF(c, "k_mpm_rhs");
         if (c.rhs_w) {
-            launch_k(c, k_mpm_edges, std::min(grid_for((long long)L.n_sub * L.nbe), 8 * c.num_sms), TPB, 0, L, kn,
-                     c.kappa_m, c.bc_kind, c.bc_value, c.beta_m, c.beta_p, c.pm, c.bpm, c.GZ, c.WU, c.ET);
+            if (c.mpm_static_ok)  // the rebuild left PD and the static g' / terms in MGZ / MET
+                launch_k(c, k_mpm_edges_kn, std::min(grid_for((long long)L.n_sub * L.nbe), 8 * c.num_sms), TPB, 0, L, kn,
+                         c.bc_kind, c.bc_value, c.PD, c.MGZ, c.WU, c.MET);
+            else
+                launch_k(c, k_mpm_edges, std::min(grid_for((long long)L.n_sub * L.nbe), 8 * c.num_sms), TPB, 0, L, kn,
+                         c.kappa_m, c.bc_kind, c.bc_value, c.beta_m, c.beta_p, c.pm, c.bpm, c.MGZ, c.WU, c.MET,
+                         (double*)nullptr);
             CK_LAUNCH();
             launch_k(c, k_mpm_rhs_w, grid2d(c, L, red_blocks(c, k_mpm_rhs_w, L.cells())), TPB, 0, L, c.max_rhs,
-                     c.anchor_m ? 1 : 0, c.T, c.q, c.pm, c.WU, c.ET, c.X);
+                     c.anchor_m ? 1 : 0, c.T, c.q, c.pm, c.WU, c.MET, c.X);
         }
         else if (c.rhs_sub && L.ncs <= RHS_TPB * RHS_CPT)
             launch_k(c, k_mpm_rhs_sub, L.n_sub, RHS_TPB, (size_t)(L.ncs + 2 * L.nbe) * sizeof(double), L, c.max_rhs,
                      c.anchor_m ? 1 : 0, kn, c.kappa_m, c.T, c.q, c.bc_kind, c.bc_value, c.beta_m, c.beta_p, c.pm,
-                     c.bpm, c.X, c.GZ, c.WU);
+                     c.bpm, c.X, c.MGZ, c.WU);
         else
             launch_k(c, k_mpm_rhs, grid_for(L.cells()), TPB, 0, L, c.max_rhs, c.anchor_m ? 1 : 0, kn, c.kappa_m, c.T,
-                     c.q, c.bc_kind, c.bc_value, c.beta_m, c.beta_p, c.pm, c.bpm, c.X, c.GZ, c.WU);
+                     c.q, c.bc_kind, c.bc_value, c.beta_m, c.beta_p, c.pm, c.bpm, c.X, c.MGZ, c.WU);
         CK_LAUNCH();
     }
     const bool fused_traces = particular_solve_x(c);
@@ -2675,7 +2720,7 @@ void launch_mpm(Ctx& c, const double* kn) {  // mpm_pressure_update (mpm.cpp:31-
         {
             PROF(c, "k_part_traces");
             launch_k(c, k_part_traces, grid_for((long long)L.n_sub * L.nbe), TPB, 0, 
-                L, c.max_rhs, c.kappa_m, c.bc_kind, c.beta_m, c.beta_p, c.GZ, c.X, c.PU);
+                L, c.max_rhs, c.kappa_m, c.bc_kind, c.beta_m, c.beta_p, c.MGZ, c.X, c.PU);
             CK_LAUNCH();
         }
         {
