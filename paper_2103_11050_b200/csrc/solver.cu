@@ -937,9 +937,11 @@ __global__ void __launch_bounds__(WPB * 32, 4) k_ds_solve_r(Layout L, const doub
 // blocked LDL^T with DMMA Schur updates and the forward sweep (X panels in
 // Lr, t1 in D; register-heavy, latency-bound), then the backward sweep from
 // the stored panels with the mean shift (few registers, full occupancy,
-// bandwidth-bound on the panel stream).
+// bandwidth-bound on the panel stream). Four blocks per SM below B = 32
+// (tools/blk_bench at 16,384 subdomains: B = 16 298 against 337 us, B = 24 759
+// against 818 us; B = 32 1,873 against 1,799 us, so three there).
 template <int B>
-__global__ void __launch_bounds__(WPB * 32, 3) k_ds_blk_factor(Layout L, const double* __restrict__ T,
+__global__ void __launch_bounds__(WPB * 32, B < 32 ? 4 : 3) k_ds_blk_factor(Layout L, const double* __restrict__ T,
                                                             double* T1, double* Xs, const double* Xd, Scalars* sc) {
     pdl_begin();
     __shared__ __align__(16) double sm[WPB][blk_smem_doubles<B>()];

@@ -562,6 +562,38 @@ def test_mpm_rhs_cell_ragged(oracle, nx, ny, sx, sy):
         assert rel_l2(ma.u, mb.u) < 1e-12
 
 
+def test_mpm_edge_cache_across_updates_and_rebuilds(oracle):
+    """k_mpm_edges_kn reads the pressure drop and the static g' / rhs terms
+    that the rebuild cached (launch_rebuild): several MPM-2P updates with
+    different kappa_n after one rebuild, then a second rebuild with another
+    kappa_m, with flux faces (z' changes every update), pressure faces and a
+    physical Robin side; then a run that alternates MPM-2P updates and
+    rebuilds. Everything against the oracle (mpm.cpp:48-86)."""
+    from test_robin_faces import robin_slab
+    nx, ny = 96, 64
+    K = random_kappa(nx, ny, 21, 0.1, 10.0)
+    rng = np.random.default_rng(5)
+    for bc in (api.unit_inflow(nx, ny), api.pressure_drop(nx, ny), robin_slab(nx, ny, 0.5, 1.0)):
+        prob = problem(nx, ny, 3, 2, K, bc=bc)
+        g, o = _sim_env(prob, MPM2P_RHS_W=1), api.Simulator(prob, oracle)
+        km = K
+        for _ in range(2):  # two rebuilds, three updates after each
+            g.mrcm_solve(km)
+            o.mrcm_solve(km)
+            for _ in range(3):
+                kn = km * np.exp(0.1 * rng.standard_normal(K.size))
+                a, b = g.mpm_pressure_update(kn), o.mpm_pressure_update(kn)
+                assert rel_l2(a.u, b.u) <= 1e-10 and rel_l2(a.p, b.p) <= 1e-10
+            km = K * np.exp(0.3 * rng.standard_normal(K.size))
+    prob = problem(nx, ny, 3, 2, K, M=5.0, bc=api.unit_inflow(nx, ny))
+    sp = api.SplittingConfig(method=api.MPM2P, eta=0.02, eta_mode=api.EPS_RELATIVE, te=60, cfl_safety=0.5)
+    ra, rr = _sim_env(prob, MPM2P_RHS_W=1).run(sp), api.Simulator(prob, oracle).run(sp)
+    seq = [s["rebuilt"] for s in rr.record.steps]
+    assert [s["rebuilt"] for s in ra.record.steps] == seq and 1 < sum(seq) < len(seq)
+    assert np.max(np.abs(ra.s_final - rr.s_final)) <= TOL_S
+    assert rel_l2(ra.u_final, rr.u_final) <= TOL_PU and rel_l2(ra.p_final, rr.p_final) <= TOL_PU
+
+
 @pytest.mark.parametrize("nx,nsx", [(64, 4), (96, 4), (64, 2), (128, 4)])
 def test_blocked_dmma_downscale_parity(oracle, nx, nsx):
     """The fused downscale on the fp64 tensor cores (band_blk.cuh: 8-pivot

@@ -1,5 +1,6 @@
 // Blocked banded LDL^T micro-benchmark (developer tool): band_blk.cuh's
-// blk_factor_fwd (3 and 4 blocks per SM) and blk_backward on random
+// blk_factor_fwd (3 and 4 blocks per SM; the product's variant and the one with
+// the entering row tile on DMMA) and blk_backward on random
 // 5-point SPD systems, one warp per system, the product kernel's launch shape
 // (4 warps per block). Checks the solution's residual on the host, that the
 // two builds' panels are bit-identical, and times the factor kernels.
@@ -113,10 +114,15 @@ int run(int nsub) {
         printf("B=%d nsub=%d %-28s %9.1f us\n", B, nsub, name, 1e3 * ms / reps);
         return 0;
     };
-    timeit([&] { k_factor<B, 0, 3><<<blocks, WPBK * 32>>>(nsub, n, dBD, dBW, dBS, dY, dXs[0], dTs[0], dbad); },
+    timeit([&] { k_factor<B, 1, 3><<<blocks, WPBK * 32>>>(nsub, n, dBD, dBW, dBS, dY, dXs[0], dTs[0], dbad); },
            "blk_factor_fwd (3 blk/SM)");
-    timeit([&] { k_factor<B, 1, 3><<<blocks, WPBK * 32>>>(nsub, n, dBD, dBW, dBS, dY, dXs[1], dTs[1], dbad); },
-           "blk_factor_fwd !NTD (3 blk/SM)");
+    timeit([&] { k_factor<B, 1, 4><<<blocks, WPBK * 32>>>(nsub, n, dBD, dBW, dBS, dY, dXs[1], dTs[1], dbad); },
+           "blk_factor_fwd (4 blk/SM)");
+    timeit([&] { k_factor<B, 0, 3><<<blocks, WPBK * 32>>>(nsub, n, dBD, dBW, dBS, dY, dXs[1], dTs[1], dbad); },
+           "NTD variant (3 blk/SM)");
+    timeit([&] { k_factor<B, 0, 4><<<blocks, WPBK * 32>>>(nsub, n, dBD, dBW, dBS, dY, dXs[1], dTs[1], dbad); },
+           "NTD variant (4 blk/SM)");
+    k_factor<B, 1, 4><<<blocks, WPBK * 32>>>(nsub, n, dBD, dBW, dBS, dY, dXs[1], dTs[1], dbad);
     timeit([&] { k_back<B><<<blocks, WPBK * 32>>>(nsub, n, dXs[1], dTs[1], dX); }, "blk_backward");
     CK(cudaDeviceSynchronize());
     int bad;
