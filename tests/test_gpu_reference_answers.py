@@ -8,8 +8,6 @@ tolerances. No oracle is involved: each expected value is analytic, or the
 device's own fine solve (solve_cell_centered) where the reference compares
 with it. Conductivity fields are seeded random fields (the reference's
 sampler is out of scope; the properties hold for any positive field)."""
-import dataclasses
-
 import numpy as np
 import pytest
 
@@ -272,3 +270,74 @@ def test_maximum_principle_and_mass_balance_over_random_steps():
             assert s2.min() >= lo - 1e-12 and s2.max() <= hi + 1e-12
             s = s2
         g.close()
+
+
+# ---- driver accounting (proj/tests/test_simulation.cpp) ----
+
+def _small(method, eta=0.01, te=3):
+    """small_inputs (test_simulation.cpp:14-24): the gaussian-slab-small preset's
+    shape (config.cpp:433-442: 8 x 8 cells, 2 x 2 subdomains, M = 40, pressure
+    drop) on a seeded random field, with the reference's default track_errors =
+    true (simulation.hpp:31): a fine reference advances in lockstep and sets
+    the transport-step schedule."""
+    K = random_kappa(8, 8, 2, 0.2, 5.0)
+    prob = problem(8, 8, 2, 2, K, M=40.0)
+    return prob, api.SplittingConfig(method=method, eta=eta, te=te, stop_on_breakthrough=False, track_errors=True)
+
+
+def test_mrcm_every_step_baseline_accounting():
+    """test_simulation.cpp:66-79."""
+    prob, sp = _small(api.MRCM_EVERY_STEP)
+    r = api.Simulator(prob).run(sp).record
+    assert r.te == 3 and r.tm_total == 3 and len(r.steps) == 3 and all(s["rebuilt"] == 1 for s in r.steps)
+    assert r.nhat == 16
+    assert (r.counters.homogeneous, r.counters.particular, r.counters.downscale) == (48, 12, 12)
+
+
+def test_static_flow_one_rebuild_all_later_steps_reuse():
+    """test_simulation.cpp:81-95: no injection, so kappa never changes and epsilon stays zero."""
+    prob, sp = _small(api.MPM2P, 0.01, 4)
+    r = api.Simulator(prob).run(sp, np.zeros(64), 0.0).record
+    assert r.te == 4 and r.tm_total == 1 and r.tm_updates == 0
+    assert all(s["epsilon"] == 0.0 for s in r.steps)
+    assert (r.counters.homogeneous, r.counters.particular, r.counters.downscale) == (16, 16, 16)
+
+
+def test_no_updates_never_rebuilds_and_runs_share_the_schedule():
+    """test_simulation.cpp:131-148: mpm2p-no-updates rebuilds at step 0 only;
+    the three methods share dt and PVI bit for bit."""
+    runs = []
+    for m in (api.MPM2P, api.MRCM_EVERY_STEP, api.MPM2P_NO_UPDATES):
+        prob, sp = _small(m, 0.01, 5)
+        runs.append(api.Simulator(prob).run(sp).record)
+    a, b, c = runs
+    assert c.tm_total == 1 and c.update_steps == [0]
+    assert [s["dt"] for s in a.steps] == [s["dt"] for s in b.steps] == [s["dt"] for s in c.steps]
+    assert [s["pvi"] for s in a.steps] == [s["pvi"] for s in b.steps]
+
+
+def test_solve_counters_reconcile_with_the_cost_formulas():
+    """test_simulation.cpp:150-157."""
+    prob, sp = _small(api.MPM2P, 0.01, 6)
+    r = api.Simulator(prob).run(sp).record
+    assert r.counters.homogeneous == r.nhat * r.tm_total
+    assert r.counters.particular == r.n_sub * r.te and r.counters.downscale == r.n_sub * r.te
+    assert r.counters.interface_solves == r.te
+
+
+def test_velocities_delivered_to_transport_are_conservative():
+    """test_simulation.cpp:159-168."""
+    prob, sp = _small(api.MPM2P, 0.01, 5)
+    g = api.Simulator(prob)
+    res = g.run(sp)
+    assert res.record.max_div_residual <= 1e-8
+    scale = np.max(np.abs(res.u_final)) * (1.0 / 8) / (1.0 / 64)
+    assert np.max(np.abs(g.divergence(res.u_final))) <= 1e-10 * scale
+
+
+def test_fine_reference_runs_record_zero_errors():
+    """test_simulation.cpp:123-129."""
+    prob, sp = _small(api.FINE_REFERENCE, 0.01, 3)
+    r = api.Simulator(prob).run(sp).record
+    assert all(s["flux_err"] == 0.0 and s["sat_err"] == 0.0 for s in r.steps)
+    assert r.counters.homogeneous == 0
