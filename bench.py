@@ -163,17 +163,18 @@ def kernel_work(name, cfg, sz, dim):
     }
     if name == "k_cr_gemv" and dim > 16384:
         # interface solve by block cyclic reduction (blocktri.cu): nb block rows (one per subdomain
-        # row) padded to S; forward levels read D_o^-1, Lo_e, Up_e (3 blocks per eliminated block),
-        # the top solve one block, backward levels P_o, Q_o (2 per eliminated block); one solve is
-        # 15 launches at nb = 128, so the per-launch figure is the solve's bytes over its launches
+        # row) padded to S. Per level with e eliminated blocks three launches: c_o = D_o^-1 y_o (e
+        # blocks read), y_e -= Lo_e c + Up_e c (2e), backward x_o = c_o - P_o x - Q_o x (2e); the
+        # top solve reads one block. The per-launch figure is the solve's bytes over its launches
+        # (22 at nb = 128)
         nb = max(1, round(ns ** 0.5))  # subdomain rows (the configs' decompositions above dim 16,384 are square)
         S = -(-(dim // nb) // 64) * 64
-        elim, lv, launches = 0, nb, 1
+        blocks, launches, lv = 1, 1, nb
         while lv > 1:
-            elim += lv // 2
+            blocks += 5 * (lv // 2)
+            launches += 3
             lv -= lv // 2
-            launches += 2
-        return ("hbm", 8.0 * S * S * (5.0 * elim + 1.0) / launches)
+        return ("hbm", 8.0 * S * S * blocks / launches)
     return table.get(name)
 
 
