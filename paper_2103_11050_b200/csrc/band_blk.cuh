@@ -103,7 +103,7 @@ struct BlkTransSrc {
         const int rr = row < n ? row : n - 1;
         const int jj = rr / SNX, ii = rr - jj * SNX, i = i0 + ii, j = j0 + jj;
         const int vf = j * (nx + 1) + i, hf = vcount + j * nx + i;
-        return BlkRowData{T[vf], T[vf + 1], T[hf], T[hf + nx], y[rr]};  // W, E, S, N faces
+        return BlkRowData{T[vf], T[vf + 1], T[hf], T[hf + nx], y ? y[rr] : 0.0};  // W, E, S, N faces
     }
     __device__ __forceinline__ void decode(int row, const BlkRowData& e, double& d, double& w, double& w1,
                                            double& s) const {
@@ -138,8 +138,13 @@ struct BlkTransSrc {
 //    2 % slower at B = 32, 1810 against 1774 us for 16,384 subdomains);
 //  * the right-hand-side products (t1 = G y1, X_I y1) are quad dot products
 //    (two FMAs and a two-step butterfly).
-template <int B, class Src, bool NTD = false>
-__device__ bool blk_factor_fwd(int n, const Src& src, double* Xs, double* Ts, double* sm) {
+//
+// RHS = false factors alone (no right-hand side: src's y may be null) and
+// also stores every panel's G (64 doubles, fragment order) in Gs, for a
+// forward sweep run later by blk_forward — the factor can then run
+// concurrently with the chain that produces the right-hand side.
+template <int B, class Src, bool NTD = false, bool RHS = true>
+__device__ bool blk_factor_fwd(int n, const Src& src, double* Xs, double* Ts, double* sm, double* Gs = nullptr) {
     constexpr int NT = blk_nt<B>();
     static_assert(B % 8 == 0 && NT >= 2, "blocked band solver: B must be a multiple of 8, >= 16");
     const int lane = threadIdx.x & 31;
@@ -193,7 +198,7 @@ __device__ bool blk_factor_fwd(int n, const Src& src, double* Xs, double* Ts, do
         double g0 = w[0][0].v[0], g1 = w[0][0].v[1];
         *reinterpret_cast<double2*>(sg0 + blk_sw(r, c0)) = make_double2(g0, g1);
         if (q == 0) {
-            sy[r] = yw[0];
+            if (RHS) sy[r] = yw[0];
             ss[r] = s_row;
         }
         __syncwarp();
@@ -231,7 +236,8 @@ __device__ bool blk_factor_fwd(int n, const Src& src, double* Xs, double* Ts, do
             }
         }
         // G[r][c0], G[r][c1] are in g0, g1: G's accumulator fragment
-        const double2 yq = *reinterpret_cast<const double2*>(sy + c0);  // y1 of rows c0, c0+1
+        const double2 yq = RHS ? *reinterpret_cast<const double2*>(sy + c0) : make_double2(0.0, 0.0);  // y1 of rows c0, c0+1
+        if (!RHS) *reinterpret_cast<double2*>(Gs + (size_t)p * 64 + 2 * lane) = make_double2(g0, g1);
         const double2 sc = *reinterpret_cast<const double2*>(ss + c0);  // s of rows c0, c0+1
         // ---- X = S21 G (lane: X[r][c0], X[r][c1]); X_NT = diag(s) G
         BlkTile x[NT + 1];
@@ -250,20 +256,22 @@ __device__ bool blk_factor_fwd(int n, const Src& src, double* Xs, double* Ts, do
             *reinterpret_cast<double2*>(xs + (I - 1) * 64 + 2 * lane) = make_double2(x[I].v[0], x[I].v[1]);
         // ---- forward substitution: t1 = G y1 and y_I -= X_I y1 as quad dot
         // products (lane: columns c0 and c1)
-        double t1 = fma(g0, yq.x, g1 * yq.y);
-        double py[NT];
+        if (RHS) {
+            double t1 = fma(g0, yq.x, g1 * yq.y);
+            double py[NT];
 #pragma unroll
-        for (int I = 1; I < NT; ++I) py[I] = fma(x[I].v[0], yq.x, x[I].v[1] * yq.y);
+            for (int I = 1; I < NT; ++I) py[I] = fma(x[I].v[0], yq.x, x[I].v[1] * yq.y);
 #pragma unroll
-        for (int o = 1; o < 4; o <<= 1) {
-            t1 += __shfl_xor_sync(0xffffffffu, t1, o);
+            for (int o = 1; o < 4; o <<= 1) {
+                t1 += __shfl_xor_sync(0xffffffffu, t1, o);
 #pragma unroll
-            for (int I = 1; I < NT; ++I) py[I] += __shfl_xor_sync(0xffffffffu, py[I], o);
+                for (int I = 1; I < NT; ++I) py[I] += __shfl_xor_sync(0xffffffffu, py[I], o);
+            }
+            st_global_if(Ts + k0 + r, t1, q == 0);
+            yw[NT] -= s_row * t1;  // X_NT y1 = diag(s) G y1
+#pragma unroll
+            for (int I = 1; I < NT; ++I) yw[I] -= py[I];
         }
-        st_global_if(Ts + k0 + r, t1, q == 0);
-        yw[NT] -= s_row * t1;  // X_NT y1 = diag(s) G y1
-#pragma unroll
-        for (int I = 1; I < NT; ++I) yw[I] -= py[I];
         // ---- trailing update S22[I][J] -= X_I S21_J^T on DMMA (row tiles
         // 1..NT, column tiles 1..min(I, NT-1): S21_NT only meets itself)
 #pragma unroll
@@ -311,6 +319,58 @@ __device__ bool blk_factor_fwd(int n, const Src& src, double* Xs, double* Ts, do
         panel(p + 1, e1);
     }
     return __all_sync(0xffffffffu, ok);
+}
+
+// Forward sweep from the stored panels and pivot inverses (blk_factor_fwd with
+// RHS = false): t1 = G y1 into Ts, y_I -= X_I y1 on the window of the next B
+// rows, the products as in the fused sweep (quad dot products; row tile NT
+// uses its stored X_NT = diag(s) G). y (length n): rhs in, untouched.
+template <int B>
+__device__ void blk_forward(int n, const double* Xs, const double* Gs, const double* y, double* Ts) {
+    constexpr int NT = blk_nt<B>();
+    const int lane = threadIdx.x & 31;
+    const int r = lane >> 2, q = lane & 3, c0 = 2 * q;
+    const int np = n / 8;
+    double yw[NT + 1];  // y of window rows 8I + r (every lane of the row)
+#pragma unroll
+    for (int I = 0; I <= NT; ++I) yw[I] = 8 * I + r < n ? y[8 * I + r] : 0.0;
+    auto fetch = [&](int p, double2* xt, double2& g, double& yn) {
+        const int pp = p < np ? p : np - 1;
+        const double* xs = Xs + (size_t)pp * NT * 64;
+#pragma unroll
+        for (int I = 0; I < NT; ++I) xt[I] = *reinterpret_cast<const double2*>(xs + I * 64 + 2 * lane);
+        g = *reinterpret_cast<const double2*>(Gs + (size_t)pp * 64 + 2 * lane);
+        const int row = 8 * (pp + NT + 1) + r;  // the row entering the window after panel pp
+        yn = row < n ? y[row] : 0.0;
+    };
+    constexpr int DEPTH = 4;  // panels in flight (an HBM round trip is several panels long)
+    double2 ring[DEPTH][NT], gr[DEPTH];
+    double yr[DEPTH];
+#pragma unroll
+    for (int d = 0; d < DEPTH; ++d) fetch(d, ring[d], gr[d], yr[d]);
+    auto step = [&](const int p, double2* xt, double2& g, double& yn) {
+        // y1 of rows c0, c0+1: row j of the pivot block is held by the lanes with r = j
+        const double y0 = __shfl_sync(0xffffffffu, yw[0], 4 * c0), y1 = __shfl_sync(0xffffffffu, yw[0], 4 * c0 + 4);
+        double t1 = fma(g.x, y0, g.y * y1);
+        double py[NT];
+#pragma unroll
+        for (int I = 0; I < NT; ++I) py[I] = fma(xt[I].x, y0, xt[I].y * y1);
+#pragma unroll
+        for (int o = 1; o < 4; o <<= 1) {
+            t1 += __shfl_xor_sync(0xffffffffu, t1, o);
+#pragma unroll
+            for (int I = 0; I < NT; ++I) py[I] += __shfl_xor_sync(0xffffffffu, py[I], o);
+        }
+        st_global_if(Ts + 8 * p + r, t1, q == 0);
+#pragma unroll
+        for (int I = 0; I < NT; ++I) yw[I] = yw[I + 1] - py[I];  // stored tile I is row tile I + 1; then the window shifts
+        yw[NT] = yn;
+        fetch(p + DEPTH, xt, g, yn);
+    };
+    for (int p = 0; p < np; p += DEPTH) {  // np = B^2/8 is a multiple of 8
+#pragma unroll
+        for (int d = 0; d < DEPTH; ++d) step(p + d, ring[d], gr[d], yr[d]);
+    }
 }
 
 // Backward sweep x1 = t1 - X^T x2 from the stored panels; x (length n) out.

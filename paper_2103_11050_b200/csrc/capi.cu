@@ -502,10 +502,15 @@ void create_ctx(mpm2p_ctx* ctx, const mpm2p_problem* P) {
     // particular solve (measured C4 362 -> 400 us per step; C2 140 -> 127, C3 202 -> 165)
     c.ds_split = c.twist_store && L.snx <= 20;
     if (const char* e = std::getenv("MPM2P_DS_SPLIT")) c.ds_split = c.ds_split && e[0] != '0';
-    if (c.ds_split) {
+    c.blk_split = !c.ds_split && c.twist_ok && L.snx == 32 && c.ds_blk != 0;
+    if (const char* e = std::getenv("MPM2P_BLK_SPLIT")) c.blk_split = c.blk_split && e[0] != '0';
+    if (c.blk_split) c.Gd.alloc((size_t)L.n_sub * L.ncs * 8);
+    if (c.ds_split || c.blk_split) {
         CK(cudaStreamCreateWithFlags(&c.st2, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming));
+    }
+    if (c.ds_split) {
         c.Lcd.alloc(ns * ncs * B);
         c.ds_midb.alloc(ns * B * B);
         c.ds_sinv.alloc(ns * B * B);

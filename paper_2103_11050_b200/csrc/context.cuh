@@ -184,6 +184,8 @@ struct Ctx {
     int ds_blk = -1;          // fused downscale on the DMMA blocked solver (band_blk.cuh): -1 auto (B = 24, 32), 0/1 (MPM2P_DS_BLK)
     bool twist_ok = false;    // two-sided band solves enabled for this problem (latency-bound regime)
     bool twist_store = false; // rebuild factor stored in the two-sided layout (band_twist.cuh)
+    bool blk_split = false;   // B = 32 with few subdomains per SM: the blocked downscale factor on the side stream, sweeps after the join (MPM2P_BLK_SPLIT)
+    DevBuf<double> Gd;        // its pivot-block inverses (8 doubles per cell)
     DevBuf<double> tw_midb, tw_sinv;  // per subdomain: bottom middle multipliers, middle S^-1 (B x B)
     // one graph per (branch, saturation-buffer parity): the upwind ping-pong
     // swaps s/s2 instead of copying, so the captured pointers alternate

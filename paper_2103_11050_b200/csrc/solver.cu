@@ -956,6 +956,47 @@ __global__ void __launch_bounds__(WPB * 32, B < 32 ? 4 : 3) k_ds_blk_factor(Layo
     if (!ok && lane == 0) atomicOr(&sc->err, ERR_PIVOT);
 }
 
+// The blocked factor alone (no right-hand side), with the pivot inverses
+// stored: with few subdomains per SM it runs on the side stream concurrently
+// with the particular / interface chain (ds_factor_fork), and the sweeps
+// follow the join (k_ds_blk_sweeps).
+template <int B>
+__global__ void __launch_bounds__(WPB * 32, B < 32 ? 4 : 3) k_ds_blk_factor_only(Layout L, const double* __restrict__ T,
+                                                                              double* Xs, double* Gs, Scalars* sc) {
+    pdl_begin();
+    __shared__ __align__(16) double sm[WPB][blk_smem_doubles<B>()];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int s = blockIdx.x * WPB + w;
+    if (s >= L.n_sub) return;
+    const int n = L.ncs;
+    const size_t so = (size_t)s * n;
+    const BlkTransSrc<B> src{T, nullptr, n, L.sny, L.nx, L.vcount(), L.sub_i0(s), L.sub_j0(s)};
+    const bool ok = blk_factor_fwd<B, BlkTransSrc<B>, false, false>(n, src, Xs + so * B, nullptr, sm[w], Gs + so * 8);
+    if (!ok && lane == 0) atomicOr(&sc->err, ERR_PIVOT);
+}
+
+// Forward and backward sweeps from the stored panels and pivot inverses, then
+// the mean shift (k_ds_blk_solve's epilogue).
+template <int B>
+__global__ void __launch_bounds__(WPB * 32) k_ds_blk_sweeps(Layout L, double* T1, const double* __restrict__ Xs,
+                                                            const double* __restrict__ Gs, double* Xd,
+                                                            const double* __restrict__ RS, double* p) {
+    pdl_begin();
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int s = blockIdx.x * WPB + w;
+    if (s >= L.n_sub) return;
+    const int n = L.ncs;
+    const size_t so = (size_t)s * n;
+    double* x = Xd + so;
+    blk_forward<B>(n, Xs + so * B, Gs + so * 8, x, T1 + so);
+    __syncwarp();  // t1 written by the row lanes, read by the column lanes
+    const double part = blk_backward<B>(n, Xs + so * B, T1 + so, x);
+    __syncwarp();
+    const double v = warp_sum(part);
+    const double shift = (__shfl_sync(0xffffffffu, RS[s], 0) - __shfl_sync(0xffffffffu, v, 0)) / n;
+    for (int r = lane; r < n; r += 32) p[L.gcell_of(s, r)] = x[r] + shift;
+}
+
 template <int B>
 __global__ void __launch_bounds__(WPB * 32) k_ds_blk_solve(Layout L, const double* __restrict__ T1,
                                                            const double* __restrict__ Xs, double* Xd,
@@ -2231,12 +2272,22 @@ void launch_setup_static(Ctx& c) {
 // before its sweeps. Works both captured into a graph (fork/join edges) and
 // eagerly.
 void ds_factor_fork(Ctx& c) {
-    if (!c.ds_split || c.ds_pending) return;
+    if ((!c.ds_split && !c.blk_split) || c.ds_pending) return;
     const Layout& L = c.L;
     CK(cudaEventRecord(c.ev_fork, c.st));
     CK(cudaStreamWaitEvent(c.st2, c.ev_fork, 0));
     const cudaStream_t main_st = c.st;
     c.st = c.st2;
+    if (c.blk_split) {  // the blocked DMMA factor of T(kappa_n), pivot inverses stored
+        PROF(c, "k_ds_factor");
+        launch_k(c, k_ds_blk_factor_only<32>, band_blocks(L), WPB * 32, 0, L, (const double*)c.T, c.Lrd.p, c.Gd.p,
+                 c.sc.p);
+        CK_LAUNCH();
+        CK(cudaEventRecord(c.ev_join, c.st2));
+        c.st = main_st;
+        c.ds_pending = true;
+        return;
+    }
     {
         PROF(c, "k_ds_band");
         launch_k(c, k_ds_prep, grid_for(L.cells()), TPB, 0, L, nullptr, c.T, nullptr, nullptr, nullptr, nullptr,
@@ -2328,7 +2379,10 @@ void downscale(Ctx& c, const double* kappa, bool skel_given) {
     if (split) ds_factor_fork(c);  // no-op when the caller already forked it
     // the blocked DMMA downscale forms its operator from T itself
     const bool blk = c.ds_blk == 1 || (c.ds_blk < 0 && (L.snx == 24 || L.snx == 32));
-    const bool blk_path = !split && !c.twist_ok && blk && L.snx % 8 == 0 && L.snx >= 16 && L.snx <= 32;
+    // With few subdomains per SM (twist_ok) the two-sided scalar solve wins up to B = 24; at B = 32 the
+    // blocked DMMA factor is faster even one-sided (C4, 256 subdomains: 163 against 191 us)
+    const bool blk_path = !split && (!c.twist_ok || L.snx == 32) && blk && L.snx % 8 == 0 && L.snx >= 16 && L.snx <= 32;
+    if (c.blk_split && blk_path) ds_factor_fork(c);  // no-op when the caller already forked it
     const bool kappa_checked = c.kappa_checked;  // the driver's k_kappa checked this kappa
     c.kappa_checked = false;
     if (split || blk_path) {  // the operator is formed by the factor: the rhs alone
@@ -2347,7 +2401,7 @@ void downscale(Ctx& c, const double* kappa, bool skel_given) {
         CK_LAUNCH();
     }
     const size_t sm1 = (size_t)WPB * band_smem_doubles(L.snx, 1) * sizeof(double);
-    const bool twist = c.twist_ok;
+    const bool twist = c.twist_ok && !blk_path;
     bool done = false;
     if (split) {
         CK(cudaStreamWaitEvent(c.st, c.ev_join, 0));
@@ -2383,6 +2437,15 @@ void downscale(Ctx& c, const double* kappa, bool skel_given) {
                 break;
         }
         if (done) CK_LAUNCH();
+    }
+    if (!done && blk_path && c.blk_split) {  // the factor ran on the side stream: join, then both sweeps
+        CK(cudaStreamWaitEvent(c.st, c.ev_join, 0));
+        c.ds_pending = false;
+        PROF(c, "k_ds_blk_solve");
+        launch_k(c, k_ds_blk_sweeps<32>, band_blocks(L), WPB * 32, 0, L, c.Dd.p, (const double*)c.Lrd, (const double*)c.Gd,
+                 c.Xd.p, (const double*)c.RS, c.p.p);
+        CK_LAUNCH();
+        done = true;
     }
     if (!done && blk_path) {
         switch (L.snx) {
