@@ -503,7 +503,14 @@ void create_ctx(mpm2p_ctx* ctx, const mpm2p_problem* P) {
     c.ds_split = c.twist_store && L.snx <= 20;
     if (const char* e = std::getenv("MPM2P_DS_SPLIT")) c.ds_split = c.ds_split && e[0] != '0';
     c.blk_split = !c.ds_split && c.twist_ok && L.snx == 32 && c.ds_blk != 0;
-    if (const char* e = std::getenv("MPM2P_BLK_SPLIT")) c.blk_split = c.blk_split && e[0] != '0';
+    if (const char* e = std::getenv("MPM2P_BLK_SPLIT")) {
+        if (e[0] == '1' && c.twist_ok && L.snx % 8 == 0 && L.snx >= 16 && L.snx <= 32 && c.ds_blk != 0) {
+            c.blk_split = true;  // forced: instead of the two-sided split below B = 32
+            c.ds_split = false;
+        } else {
+            c.blk_split = c.blk_split && e[0] != '0';
+        }
+    }
     if (c.blk_split) c.Gd.alloc((size_t)L.n_sub * L.ncs * 8);
     if (c.ds_split || c.blk_split) {
         CK(cudaStreamCreateWithFlags(&c.st2, cudaStreamNonBlocking));

@@ -2280,8 +2280,18 @@ void ds_factor_fork(Ctx& c) {
     c.st = c.st2;
     if (c.blk_split) {  // the blocked DMMA factor of T(kappa_n), pivot inverses stored
         PROF(c, "k_ds_factor");
-        launch_k(c, k_ds_blk_factor_only<32>, band_blocks(L), WPB * 32, 0, L, (const double*)c.T, c.Lrd.p, c.Gd.p,
-                 c.sc.p);
+        switch (L.snx) {
+#define X(BW_)                                                                                                  \
+    case BW_:                                                                                                   \
+        launch_k(c, k_ds_blk_factor_only<BW_>, band_blocks(L), WPB * 32, 0, L, (const double*)c.T, c.Lrd.p,      \
+                 c.Gd.p, c.sc.p);                                                                               \
+        break;
+            X(16) X(24) X(32)
+#undef X
+            default:
+                c.st = main_st;
+                throw ConfigError("blocked split downscale: unsupported subdomain width");
+        }
         CK_LAUNCH();
         CK(cudaEventRecord(c.ev_join, c.st2));
         c.st = main_st;
@@ -2378,10 +2388,10 @@ void downscale(Ctx& c, const double* kappa, bool skel_given) {
     const bool split = c.ds_split;
     if (split) ds_factor_fork(c);  // no-op when the caller already forked it
     // the blocked DMMA downscale forms its operator from T itself
-    const bool blk = c.ds_blk == 1 || (c.ds_blk < 0 && (L.snx == 24 || L.snx == 32));
+    const bool blk = c.ds_blk == 1 || c.blk_split || (c.ds_blk < 0 && (L.snx == 24 || L.snx == 32));
     // With few subdomains per SM (twist_ok) the two-sided scalar solve wins up to B = 24; at B = 32 the
     // blocked DMMA factor is faster even one-sided (C4, 256 subdomains: 163 against 191 us)
-    const bool blk_path = !split && (!c.twist_ok || L.snx == 32) && blk && L.snx % 8 == 0 && L.snx >= 16 && L.snx <= 32;
+    const bool blk_path = !split && (!c.twist_ok || L.snx == 32 || c.blk_split) && blk && L.snx % 8 == 0 && L.snx >= 16 && L.snx <= 32;
     if (c.blk_split && blk_path) ds_factor_fork(c);  // no-op when the caller already forked it
     const bool kappa_checked = c.kappa_checked;  // the driver's k_kappa checked this kappa
     c.kappa_checked = false;
@@ -2442,8 +2452,17 @@ void downscale(Ctx& c, const double* kappa, bool skel_given) {
         CK(cudaStreamWaitEvent(c.st, c.ev_join, 0));
         c.ds_pending = false;
         PROF(c, "k_ds_blk_solve");
-        launch_k(c, k_ds_blk_sweeps<32>, band_blocks(L), WPB * 32, 0, L, c.Dd.p, (const double*)c.Lrd, (const double*)c.Gd,
-                 c.Xd.p, (const double*)c.RS, c.p.p);
+        switch (L.snx) {
+#define X(BW_)                                                                                                  \
+    case BW_:                                                                                                   \
+        launch_k(c, k_ds_blk_sweeps<BW_>, band_blocks(L), WPB * 32, 0, L, c.Dd.p, (const double*)c.Lrd,          \
+                 (const double*)c.Gd, c.Xd.p, (const double*)c.RS, c.p.p);                                      \
+        break;
+            X(16) X(24) X(32)
+#undef X
+            default:
+                throw ConfigError("blocked split downscale: unsupported subdomain width");
+        }
         CK_LAUNCH();
         done = true;
     }
