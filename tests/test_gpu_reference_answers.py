@@ -341,3 +341,41 @@ def test_fine_reference_runs_record_zero_errors():
     r = api.Simulator(prob).run(sp).record
     assert all(s["flux_err"] == 0.0 and s["sat_err"] == 0.0 for s in r.steps)
     assert r.counters.homogeneous == 0
+
+
+# ---- the fine solve, solve_cell_centered (proj/tests/test_elliptic.cpp) ----
+
+def test_fine_conservation_on_rough_fields():
+    """test_elliptic.cpp:89-97: a source / sink pair on a 1e-3 .. 1e3 field,
+    conservation_residual <= 1e-10 residual_scale."""
+    K = random_kappa(20, 20, 3, 1e-3, 1e3)
+    q = np.zeros(400)
+    q[4 * 20 + 3], q[12 * 20 + 15] = 400.0, -400.0
+    g = api.Simulator(problem(20, 20, 1, 1, K, q=q))
+    g.fine_solve(K)
+    _, _, res, scale = g.fine_stats()
+    assert res <= 1e-10 * scale
+
+
+def test_fine_mirror_symmetry():
+    """test_elliptic.cpp:99-118: with kappa symmetric about x = lx/2, swapping
+    the left and right pressures mirrors p and reverses the flux."""
+    nx, ny = 10, 6
+    K = random_kappa(nx, ny, 11).reshape(ny, nx)
+    K[:, nx // 2:] = K[:, : nx // 2][:, ::-1]
+    K = K.ravel()
+    a = api.Simulator(problem(nx, ny, 1, 1, K, bc=api.pressure_drop(nx, ny, 1.0, 0.0)))
+    b = api.Simulator(problem(nx, ny, 1, 1, K, bc=api.pressure_drop(nx, ny, 0.0, 1.0)))
+    (pa, ua), (pb, ub) = a.fine_solve(K), b.fine_solve(K)
+    assert np.max(np.abs(pb.reshape(ny, nx) - pa.reshape(ny, nx)[:, ::-1])) <= 1e-11
+    assert np.max(np.abs(_vfaces(nx, ny, ub) + _vfaces(nx, ny, ua)[:, ::-1])) <= 1e-10 * np.max(np.abs(ua))
+
+
+def test_fine_scaling_kappa_scales_u_and_leaves_p():
+    """test_elliptic.cpp:120-132 (10 x 8 cells instead of 9 x 7: the device
+    fine solve's block preconditioner has kernels for widths 4, 8, 10, 12, 16,
+    20, 24, 32)."""
+    K = random_kappa(10, 8, 5)
+    g = api.Simulator(problem(10, 8, 1, 1, K))
+    (pa, ua), (pb, ub) = g.fine_solve(K), g.fine_solve(3.0 * K)
+    assert np.max(np.abs(pb - pa)) <= 1e-11 and np.max(np.abs(ub - 3.0 * ua)) <= 1e-11
